@@ -1,0 +1,209 @@
+/*
+ * sfkv.h — C ABI of the B200-native KV pin pool, memory-manager pressure step and stage mapper.
+ *
+ * This is the drop-in boundary for the hot path of the reference ("stageflow", the executable
+ * form of Orla, /root/reference/proj). Every entry point names the reference interface it
+ * replaces (file:line, paths relative to /root/reference/proj). INTEGRATION.md shows the
+ * reference-side binding (a `Backend` subclass and a patched `pressure_actions`).
+ *
+ * Conventions
+ *   - extern "C", opaque handles, plain pointers and sizes; no C++ or torch types.
+ *   - Every function returns int: 0 = ok, < 0 = error (SFKV_E*); sfkv_last_error() describes the
+ *     most recent error on the calling thread. Nothing throws across the boundary.
+ *   - One host thread per pool handle. All GPU work of a pool is issued on the pool's stream
+ *     (sfkv_pool_set_stream; default: a private non-blocking stream).
+ *   - Functions without the _dev suffix take HOST pointers: they copy inputs to the device,
+ *     run the kernels and copy results back before returning (synchronous, like the reference's
+ *     single-threaded calls). The _dev variants take DEVICE pointers on the pool's device and
+ *     are asynchronous on the pool stream.
+ *   - A workflow is a dense slot id in [0, max_workflows) chosen by the host (the host keeps the
+ *     workflow_id string -> slot map, as SimulatedBackend keys pins_ by workflow_id,
+ *     simulated_backend.hpp:115).
+ *   - Token sequences are CSR batches: request r owns tok[tok_off[r] .. tok_off[r+1]).
+ *     Tokens are u32 ids of the reference's whitespace tokens (backend.cpp:60-97).
+ *   - There is no CPU fallback: every compute entry point runs sm_100a kernels; creating a pool
+ *     without a usable B200 fails with SFKV_ENODEV.
+ */
+#ifndef SFKV_H_
+#define SFKV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFKV_ABI_VERSION 1
+
+#define SFKV_OK 0
+#define SFKV_EINVAL -1    /* bad argument (null pointer, out-of-range slot, unaligned buffer) */
+#define SFKV_ENODEV -2    /* no CUDA device / not sm_100 */
+#define SFKV_ECUDA -3     /* CUDA runtime error */
+#define SFKV_ENOMEM -4    /* device allocation failed */
+#define SFKV_EPOOL -5     /* physical pool exhausted (logical capacity admitted the pin, but the
+                             physical block pool or a pin's block table is too small) */
+#define SFKV_ESTALE -6    /* payload commit whose staging assumed a different cached prefix */
+
+#define SFKV_FLUSH_ALL (-1)        /* FlushScope::everything() (backend.hpp:65-70) */
+#define SFKV_BLOCK_TOKENS 16       /* tokens per KV block */
+
+/* Commit status per request (out_status of sfkv_commit_batch). */
+#define SFKV_PIN_REJECTED 0        /* capacity rejection: old pin kept (simulated_backend.cpp:142-148) */
+#define SFKV_PIN_ACCEPTED 1
+
+typedef struct sfkv_pool sfkv_pool;
+
+typedef struct sfkv_pool_config {
+  int32_t device;            /* CUDA device ordinal of this pool (one backend per GPU) */
+  int32_t max_workflows;     /* workflow slots */
+  int64_t n_blocks;          /* physical KV blocks (16 tokens each) */
+  int64_t capacity_tokens;   /* logical capacity: SimulatedBackendConfig::cache_capacity_tokens
+                                (simulated_backend.hpp:62); admission is on logical tokens */
+  int32_t max_pin_blocks;    /* block-table length per workflow pin */
+  int32_t table_log2;        /* global block table: 2^table_log2 slots of 16 B */
+  int32_t n_slabs;           /* KV slabs per token = layers * 2 (K and V); 0 = metadata only */
+  int32_t slab_row_bytes;    /* bytes of one token in one slab = kv_heads * head_dim * 2 (bf16) */
+} sfkv_pool_config;
+
+/* Counters mirrored from SimulatedBackend / BackendStats (backend.hpp:72-80,
+ * simulated_backend.hpp:96-98). */
+typedef struct sfkv_pool_stats {
+  int64_t occupancy_tokens;       /* sum of pin lengths */
+  int64_t capacity_tokens;
+  uint64_t capacity_rejections;
+  uint64_t flush_calls;
+  uint64_t preserve_calls;
+  int64_t blocks_in_use;          /* physical blocks with refcount > 0 */
+  int64_t table_live;             /* live keys in the global table */
+  int64_t table_tombstones;
+} sfkv_pool_stats;
+
+/* ---- lifecycle ------------------------------------------------------------------------- */
+
+const char* sfkv_last_error(void);
+int sfkv_abi_version(void);
+
+/* Replaces the SimulatedBackend constructor's cache state (simulated_backend.cpp:20-29). */
+int sfkv_pool_create(const sfkv_pool_config* cfg, sfkv_pool** out);
+int sfkv_pool_destroy(sfkv_pool* pool);
+int sfkv_pool_set_stream(sfkv_pool* pool, void* cuda_stream);
+int sfkv_pool_sync(sfkv_pool* pool);
+/* Device pointer of the KV payload (n_blocks * block_bytes), block-major
+ * [block][slab][slot 16][slab_row_bytes]; block_bytes = n_slabs * 16 * slab_row_bytes. */
+int sfkv_pool_kv(sfkv_pool* pool, void** kv, int64_t* block_bytes);
+
+/* ---- lookup: replaces SimulatedBackend::prefix_match (simulated_backend.cpp:153-162) -------
+ * out_M[r] = LCP(pin[wf[r]], tokens of r), 0 when the workflow has no pin. Exact: the kernel
+ * hashes the request's 16-token blocks into chained block hashes and compares them with the
+ * pin's; every block whose predecessor hash matches is verified token by token, so M never
+ * depends on hash collisions. out_hash (nullable) receives the chained hash of every block of
+ * every request (ceil(len/16) per request, concatenated in request order). */
+int sfkv_match_batch(sfkv_pool* pool, int64_t n, const int32_t* wf, const int64_t* tok_off,
+                     const uint32_t* tok, int64_t* out_M, uint64_t* out_hash);
+int sfkv_match_batch_dev(sfkv_pool* pool, int64_t n, const int32_t* wf, const int64_t* tok_off,
+                         const uint32_t* tok, int64_t* out_M, uint64_t* out_hash);
+
+/* ---- global lookup (new; cross-workflow dedup the reference lacks) -------------
+ * For every FULL block of every request: the id of the resident block with the same chained hash
+ * (token-verified), else -1 (out_block, one entry per full block, request order).
+ * out_hit_tokens[r] = 16 * number of leading hit blocks of request r. */
+int sfkv_lookup_batch(sfkv_pool* pool, int64_t n, const int64_t* tok_off, const uint32_t* tok,
+                      int32_t* out_block, int64_t* out_hit_tokens);
+int sfkv_lookup_batch_dev(sfkv_pool* pool, int64_t n, const int64_t* tok_off, const uint32_t* tok,
+                          int32_t* out_block, int64_t* out_hit_tokens);
+
+/* ---- retain: replaces SimulatedBackend::pin_prompt (simulated_backend.cpp:135-151) ----------
+ * Commits request r's tokens as the new pin of wf[r] (workflow slots distinct within a batch).
+ * Admission runs in request order with the reference rule: reject iff
+ * occupancy - old_len + new_len > capacity (old pin kept, ++capacity_rejections).
+ * Accepted pins share every leading full block already resident (any workflow, chained-hash +
+ * token verified) and allocate the rest (lowest free block ids, in request/block order; within
+ * the batch the lowest request index owns a new shared block). Old-pin blocks are released after
+ * the new pin's references are taken.
+ * KV payload (pools with n_slabs > 0; kv_src may be NULL for metadata-only commits): token p of a
+ * newly allocated block is copied from the old pin's block when p < M_r (copy-on-share of the
+ * boundary block) and otherwise from staging row p - M_r, where M_r = LCP(old pin, tokens) and
+ * the staging of request r starts at byte kv_src_off[r] of kv_src with layout
+ * [slab][token (P_r - M_r rows)][slab_row_bytes]. m_expected (nullable) is the M the caller's
+ * prefill assumed; a request whose M_r differs fails the batch with SFKV_ESTALE. */
+int sfkv_commit_batch(sfkv_pool* pool, int64_t n, const int32_t* wf, const int64_t* tok_off,
+                      const uint32_t* tok, const void* kv_src, const int64_t* kv_src_off,
+                      const int64_t* m_expected, int32_t* out_status);
+int sfkv_commit_batch_dev(sfkv_pool* pool, int64_t n, const int32_t* wf, const int64_t* tok_off,
+                          const uint32_t* tok, const void* kv_src, const int64_t* kv_src_off,
+                          const int64_t* m_expected, int32_t* out_status);
+
+/* ---- evict: replaces SimulatedBackend::flush (simulated_backend.cpp:169-184) -----------------
+ * wf = SFKV_FLUSH_ALL flushes every pin. *freed = tokens released (0 when nothing was pinned). */
+int sfkv_flush(sfkv_pool* pool, int32_t wf, int64_t* freed);
+/* Batched evict of distinct workflows; out_freed[r] per request. */
+int sfkv_flush_batch(sfkv_pool* pool, int64_t n, const int32_t* wf, int64_t* out_freed);
+
+/* ---- inspection: SimulatedBackend::preserve / pinned_token_count / cache_utilization ---------
+ * (simulated_backend.cpp:164-167, 186-193). preserve counts a preserve call and reports whether a
+ * pin exists (an empty pin counts). */
+int sfkv_preserve(sfkv_pool* pool, int32_t wf, int32_t* has_pin);
+int sfkv_pinned_token_count(sfkv_pool* pool, int32_t wf, int64_t* n_tokens);
+int sfkv_cache_utilization(sfkv_pool* pool, double* util);
+int sfkv_stats(sfkv_pool* pool, sfkv_pool_stats* out);
+/* Block table of a pin (Class B inspection): ids (cap entries max), chained hashes (nullable). */
+int sfkv_pin_blocks(sfkv_pool* pool, int32_t wf, int32_t* ids, uint64_t* hashes, int32_t cap,
+                    int32_t* n_blocks);
+/* Refcount of every physical block (n_blocks entries). */
+int sfkv_block_refcounts(sfkv_pool* pool, uint32_t* out);
+
+/* ---- gather (new): assemble pins into contiguous staging ------------------------------------
+ * Request r writes its pin's KV at dst + dst_off[r], layout [slab][token (pin_len)][row]. */
+int sfkv_gather_dev(sfkv_pool* pool, int64_t n, const int32_t* wf, void* dst,
+                    const int64_t* dst_off);
+
+/* ---- cross-pool stage handoff (new; migration is a SPEC non-goal) --------------
+ * Copies the pin of wf_src in `src` into `dst` as the pin of wf_dst (same semantics as a commit
+ * into dst whose payload comes from the source pin's blocks). The pools may live on different
+ * GPUs (peer access over NVLink; the copy kernel runs on dst's device and pulls) or on the same
+ * GPU. *status = SFKV_PIN_ACCEPTED / SFKV_PIN_REJECTED (dst capacity), unchanged dst on reject. */
+int sfkv_handoff(sfkv_pool* src, int32_t wf_src, sfkv_pool* dst, int32_t wf_dst, int32_t* status);
+
+/* ---- memory manager: replaces pressure_actions (memory.cpp:150-169) -------------------------
+ * Entries are the tracker's (workflow, backend) records as SoA: backend index, last_update_ts,
+ * wf_rank (rank of workflow_id in std::string order), in_flight, preserved. For every backend b
+ * with util[b] > tau: out_victim[b] = index of the preserved entry with in_flight == 0 and the
+ * least (last_update_ts, wf_rank), else -1. Runs on `device`. */
+int sfmm_pressure_argmin(int32_t device, int64_t n, const int32_t* backend, const double* ts,
+                         const uint32_t* wf_rank, const int32_t* in_flight,
+                         const uint8_t* preserved, int32_t n_backends, const double* util,
+                         double tau, int64_t* out_victim);
+
+/* ---- stage mapper: replaces map_threshold (mapper.cpp:19-31) and reroute_on_overload
+ *      (orchestrator.cpp:78-87) -----------------------------------------------------------------
+ * Threshold: out_choice[r] = 0 (light) iff score[r] <= threshold, else 1 (heavy).
+ * Cost: for R requests x C candidates,
+ *   cost[r][c] = overhead[c] + prefill[c] * (P[r] - M[r*C + c]) + decode[c] * O[r]
+ *                + queue_penalty[c] * depth[c]
+ * out_choice[r] = argmin_c cost (ties -> lowest c), out_cost[r] = that cost (f64).
+ * Costs use the batch-start depth snapshot. Reroute (limit > 0): requests are then processed in
+ * order; the choice stays if its live queue depth < limit, else the first listed alternate
+ * (alternates[choice*C + j], j = 0.., -1 terminated; nullable = none) with depth < limit, else
+ * unchanged; each routed request increments its candidate's live depth (the batched equivalent of
+ * Orchestrator::queue_depth growing as requests enqueue, orchestrator.cpp:245-251, 481-484).
+ * depth_inout (C entries, u64) is updated. */
+int sfmap_threshold_batch(int32_t device, int64_t n, const double* score, double threshold,
+                          int32_t* out_choice);
+int sfmap_cost_batch(int32_t device, int64_t n, int32_t c, const int64_t* P, const int64_t* M,
+                     const int64_t* O, const double* overhead, const double* prefill,
+                     const double* decode, const double* queue_penalty,
+                     const int32_t* alternates, uint64_t* depth_inout, uint64_t limit,
+                     int32_t* out_choice, double* out_cost);
+
+/* ---- the chained block hash (shared by the GPU kernels and the CPU oracle) -------------------
+ * digest(k, n, t) of block k with n valid tokens t[0..n); chain(k) = fin(sum_{i<=k} digest(i)).
+ * Exposed for tests and for hosts that precompute keys. */
+uint64_t sfkv_block_digest(uint64_t k, uint32_t n, const uint32_t* t);
+uint64_t sfkv_chain_finalize(uint64_t prefix_sum);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SFKV_H_ */

@@ -1,0 +1,178 @@
+// libsfref.so — a C shim over the UNMODIFIED reference functions on the hot path
+// (oracle test infrastructure and the CPU baseline arm of bench.py; never the product).
+//
+// Every entry point calls straight into the reference's own code compiled from /root/reference:
+//   sfref_pin / sfref_prefix_match*  -> SimulatedBackend::complete / prefix_match
+//                                       (simulated_backend.cpp:35-39, 72-151, 153-162)
+//   sfref_flush / sfref_preserve      -> SimulatedBackend::flush / preserve (169-184, 190-193)
+//   sfref_pressure_actions            -> pressure_actions (memory.cpp:150-169) over a
+//                                       WorkflowTracker built with its public mutators
+//   sfref_map_threshold               -> map_threshold (mapper.cpp:19-31)
+//   sfref_reroute                     -> reroute_on_overload (orchestrator.cpp:78-87)
+// Token ids are rendered to whitespace tokens "t<id>", the same text the reference tokenizes.
+#include <cstring>
+
+#include "stageflow/memory.hpp"
+#include "stageflow/mapper.hpp"
+#include "stageflow/orchestrator.hpp"
+#include "stageflow/simulated_backend.hpp"
+
+using namespace stageflow;
+
+namespace {
+
+struct RefPool {
+  EventLoop loop{ClockMode::Virtual};
+  std::unique_ptr<SimulatedBackend> backend;
+};
+
+struct RefBatch {
+  std::vector<std::string> wf;
+  std::vector<std::vector<std::string>> tokens;
+};
+
+std::string render(const std::uint32_t* tok, long long n) {
+  std::string s;
+  s.reserve(static_cast<std::size_t>(n) * 8);
+  for (long long i = 0; i < n; ++i) {
+    if (i) s += ' ';
+    s += 't';
+    s += std::to_string(tok[i]);
+  }
+  return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+void* sfref_pool_create(long long capacity_tokens) {
+  auto* p = new RefPool;
+  SimulatedBackendConfig cfg;
+  cfg.cache_capacity_tokens = capacity_tokens;
+  cfg.max_concurrency = 1;
+  cfg.output = OutputRule::constant(0);
+  BackendDescriptor d;
+  d.ref = "ref";
+  d.model = "ref-model";
+  p->backend = std::make_unique<SimulatedBackend>(p->loop, d, cfg);
+  return p;
+}
+
+void sfref_pool_destroy(void* h) { delete static_cast<RefPool*>(h); }
+
+// One stage request through the reference backend (tokenize -> prefix_match -> pin_prompt).
+// Returns M (cached prefix tokens); *accepted reports whether the pin was admitted.
+long long sfref_complete(void* h, const char* wf, const std::uint32_t* tok, long long n,
+                         int* accepted) {
+  auto* p = static_cast<RefPool*>(h);
+  CompletionRequest req;
+  req.messages = make_user_context(render(tok, n));
+  req.metadata.workflow_id = wf;
+  auto before = p->backend->capacity_rejections();
+  auto resp = complete_blocking(*p->backend, p->loop, std::move(req));
+  if (accepted) *accepted = p->backend->capacity_rejections() == before ? 1 : 0;
+  return resp.usage.cached_prefix_tokens;
+}
+
+long long sfref_flush(void* h, const char* wf, int all) {
+  auto* p = static_cast<RefPool*>(h);
+  return p->backend->flush(all ? FlushScope::everything() : FlushScope::workflow(wf));
+}
+
+int sfref_preserve(void* h, const char* wf) {
+  return static_cast<RefPool*>(h)->backend->preserve(wf) ? 1 : 0;
+}
+
+long long sfref_pinned_token_count(void* h, const char* wf) {
+  return static_cast<RefPool*>(h)->backend->pinned_token_count(wf);
+}
+long long sfref_occupancy_tokens(void* h) {
+  return static_cast<RefPool*>(h)->backend->occupancy_tokens();
+}
+unsigned long long sfref_capacity_rejections(void* h) {
+  return static_cast<RefPool*>(h)->backend->capacity_rejections();
+}
+double sfref_cache_utilization(void* h) {
+  return static_cast<RefPool*>(h)->backend->cache_utilization();
+}
+
+// A batch of lookups, rendered to token strings ONCE (outside any timed region): the reference's
+// prefix_match consumes std::string tokens (simulated_backend.hpp:73-74).
+void* sfref_batch_create(long long n, const char* const* wf, const long long* tok_off,
+                         const std::uint32_t* tok) {
+  auto* b = new RefBatch;
+  b->wf.reserve(static_cast<std::size_t>(n));
+  b->tokens.resize(static_cast<std::size_t>(n));
+  for (long long r = 0; r < n; ++r) {
+    b->wf.emplace_back(wf[r]);
+    auto& v = b->tokens[static_cast<std::size_t>(r)];
+    v.reserve(static_cast<std::size_t>(tok_off[r + 1] - tok_off[r]));
+    for (long long i = tok_off[r]; i < tok_off[r + 1]; ++i) v.push_back("t" + std::to_string(tok[i]));
+  }
+  return b;
+}
+void sfref_batch_destroy(void* b) { delete static_cast<RefBatch*>(b); }
+
+// The reference lookup itself: M[r] = SimulatedBackend::prefix_match(wf[r], tokens[r]).
+void sfref_prefix_match_batch(void* h, void* batch, long long* out_M) {
+  auto* p = static_cast<RefPool*>(h);
+  auto* b = static_cast<RefBatch*>(batch);
+  for (std::size_t r = 0; r < b->wf.size(); ++r) {
+    out_M[r] = p->backend->prefix_match(b->wf[r], std::span<const std::string>(b->tokens[r]));
+  }
+}
+
+// pressure_actions over n tracker entries. Entry i: (wf[i], backend_refs[backend[i]], ts[i],
+// in_flight[i], preserved[i], tokens[i]). out_victim[bi] = entry index flushed on backend bi or -1.
+int sfref_pressure_actions(long long n, const char* const* wf, const int* backend, const double* ts,
+                           const int* in_flight, const unsigned char* preserved,
+                           const long long* tokens, int n_backends,
+                           const char* const* backend_refs, const double* util, double tau,
+                           long long* out_victim) {
+  WorkflowTracker tracker;
+  std::map<std::pair<std::string, std::string>, long long> index;
+  for (long long i = 0; i < n; ++i) {
+    CacheEntry e;
+    e.workflow_id = wf[i];
+    e.backend_ref = backend_refs[backend[i]];
+    e.token_count = tokens ? tokens[i] : 1;
+    e.preserved = preserved[i] != 0;
+    e.last_update_ts = ts[i];
+    index[{e.workflow_id, e.backend_ref}] = i;
+    tracker.upsert_entry(e);
+    if (in_flight[i] > 0) tracker.adjust_in_flight(e.backend_ref, e.workflow_id, in_flight[i]);
+  }
+  std::map<std::string, double> u;
+  for (int b = 0; b < n_backends; ++b) u[backend_refs[b]] = util[b];
+  for (int b = 0; b < n_backends; ++b) out_victim[b] = -1;
+  int count = 0;
+  for (const auto& a : pressure_actions(tracker, u, tau)) {
+    for (int b = 0; b < n_backends; ++b) {
+      if (a.backend_ref == backend_refs[b]) out_victim[b] = index.at({a.workflow_id, a.backend_ref});
+    }
+    ++count;
+  }
+  return count;
+}
+
+// map_threshold with a score function returning the given score: 1 = light, 0 = heavy.
+int sfref_map_threshold(double score, double threshold) {
+  auto [ref, s] = map_threshold(Context{}, [score](const Context&) { return score; }, threshold,
+                                "light", "heavy");
+  (void)s;
+  return ref == "light" ? 1 : 0;
+}
+
+// reroute_on_overload over candidates 0..n-1 with candidate 0 the primary.
+int sfref_reroute(int n, const unsigned long long* depth, unsigned long long limit) {
+  std::vector<std::string> names;
+  for (int i = 0; i < n; ++i) names.push_back(std::to_string(i));
+  auto pick = reroute_on_overload(
+      names[0], std::span<const std::string>(names.data() + 1, names.size() - 1),
+      [&](const std::string& s) { return static_cast<std::size_t>(depth[std::stoi(s)]); },
+      static_cast<std::size_t>(limit));
+  return std::stoi(pick);
+}
+
+}  // extern "C"

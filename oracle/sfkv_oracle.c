@@ -1,0 +1,700 @@
+/*
+ * sfkv_oracle.c — CPU restatement (TEST INFRASTRUCTURE ONLY; see sfkv_oracle.h).
+ *
+ * Reference citations are relative to /root/reference/proj.
+ *   pins / prefix_match  simulated_backend.cpp:153-162 (LCP against the workflow's own pin)
+ *   pin_prompt           simulated_backend.cpp:135-151 (replace pin; reject iff
+ *                        occupancy - old + new > capacity, old pin kept)
+ *   flush                simulated_backend.cpp:169-184
+ *   preserve             simulated_backend.cpp:190-193 (presence check, counts the call)
+ *   cache_utilization    simulated_backend.cpp:186-188
+ *   pressure_actions     memory.cpp:150-169 (strict > tau, strict < on ts, ties -> first id)
+ *   map_threshold        mapper.cpp:19-31 (light iff score <= threshold)
+ *   reroute_on_overload  orchestrator.cpp:78-87
+ * Batch semantics (the definition the GPU kernels must reproduce) are stated at each function.
+ */
+#include "sfkv_oracle.h"
+
+#include <stdlib.h>
+#include <string.h>
+
+#define BT 16
+#define KEY_EMPTY 0ull
+
+/* ---------------------------------------------------------------- chained block hash ---- */
+
+static uint64_t mix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebull;
+  x ^= x >> 31;
+  return x;
+}
+
+/* digest(k, n, t): words w_i = t[2i] | t[2i+1] << 32 (tokens at i >= n read as 0),
+ * acc = sum_i mix64(w_i ^ (i+1)*G), digest = mix64(acc ^ mix64(k*H + n)). */
+uint64_t sfo_block_digest(uint64_t k, uint32_t n, const uint32_t* t) {
+  uint64_t acc = 0;
+  for (uint32_t i = 0; i < 8; ++i) {
+    uint64_t lo = (2 * i < n) ? t[2 * i] : 0;
+    uint64_t hi = (2 * i + 1 < n) ? t[2 * i + 1] : 0;
+    uint64_t w = lo | (hi << 32);
+    acc += mix64(w ^ ((uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull));
+  }
+  return mix64(acc ^ mix64(k * 0xD6E8FEB86659FD93ull + n));
+}
+
+/* chain(k) = fin(sum_{i<=k} digest(i)); keys 0 and 1 are reserved (empty / tombstone). */
+uint64_t sfo_chain_finalize(uint64_t s) {
+  uint64_t c = mix64(s ^ 0x5851F42D4C957F2Dull);
+  return c < 2 ? c + 2 : c;
+}
+
+void sfo_chain_hashes(const uint32_t* tok, int64_t len, uint64_t* out) {
+  uint64_t s = 0;
+  int64_t nb = (len + BT - 1) / BT;
+  for (int64_t k = 0; k < nb; ++k) {
+    int64_t n = len - k * BT;
+    if (n > BT) n = BT;
+    s += sfo_block_digest((uint64_t)k, (uint32_t)n, tok + k * BT);
+    out[k] = sfo_chain_finalize(s);
+  }
+}
+
+/* ---------------------------------------------------------------- key -> block map ---- */
+
+typedef struct {
+  uint64_t* key;
+  int32_t* val;
+  int64_t cap; /* power of two */
+  int64_t live;
+} kmap;
+
+static int kmap_init(kmap* m, int64_t cap) {
+  m->cap = 16;
+  while (m->cap < 2 * cap) m->cap <<= 1;
+  m->key = (uint64_t*)calloc((size_t)m->cap, sizeof(uint64_t));
+  m->val = (int32_t*)malloc((size_t)m->cap * sizeof(int32_t));
+  m->live = 0;
+  return (m->key && m->val) ? 0 : -1;
+}
+static void kmap_free(kmap* m) {
+  free(m->key);
+  free(m->val);
+}
+static int64_t kmap_find(const kmap* m, uint64_t k) {
+  int64_t i = (int64_t)(k & (uint64_t)(m->cap - 1));
+  while (m->key[i] != KEY_EMPTY) {
+    if (m->key[i] == k) return i;
+    i = (i + 1) & (m->cap - 1);
+  }
+  return -1;
+}
+static int32_t kmap_get(const kmap* m, uint64_t k) {
+  int64_t i = kmap_find(m, k);
+  return i < 0 ? -1 : m->val[i];
+}
+static void kmap_put(kmap* m, uint64_t k, int32_t v) {
+  int64_t i = (int64_t)(k & (uint64_t)(m->cap - 1));
+  while (m->key[i] != KEY_EMPTY && m->key[i] != k) i = (i + 1) & (m->cap - 1);
+  if (m->key[i] == KEY_EMPTY) m->live++;
+  m->key[i] = k;
+  m->val[i] = v;
+}
+/* Backward-shift deletion keeps linear probing exact without tombstones. */
+static void kmap_del(kmap* m, uint64_t k) {
+  int64_t i = kmap_find(m, k);
+  if (i < 0) return;
+  m->live--;
+  int64_t j = i;
+  for (;;) {
+    m->key[i] = KEY_EMPTY;
+    for (;;) {
+      j = (j + 1) & (m->cap - 1);
+      if (m->key[j] == KEY_EMPTY) return;
+      int64_t h = (int64_t)(m->key[j] & (uint64_t)(m->cap - 1));
+      /* move j to i if h is cyclically outside (i, j] */
+      if ((i <= j) ? ((i < h) && (h <= j)) : ((i < h) || (h <= j))) continue;
+      break;
+    }
+    m->key[i] = m->key[j];
+    m->val[i] = m->val[j];
+    i = j;
+  }
+}
+
+/* ---------------------------------------------------------------- pool ---- */
+
+struct sfo_pool {
+  sfo_pool_config cfg;
+  /* pins (Class A): token copy per workflow slot; len -1 = no pin. */
+  int64_t* pin_len;
+  uint32_t** pin_tok;
+  int32_t* pin_nblk;
+  int32_t* pin_blk; /* [wf][max_pin_blocks] */
+  uint64_t* pin_hash;
+  /* blocks (Class B) */
+  uint64_t* blk_key;
+  uint32_t* blk_tok; /* [block][16] */
+  uint8_t* blk_n;
+  uint8_t* blk_in_table;
+  uint32_t* blk_ref;
+  uint8_t* blk_free;
+  kmap table;
+  uint8_t* kv;
+  int64_t block_bytes;
+  /* counters */
+  int64_t occupancy;
+  uint64_t rejections, flush_calls, preserve_calls;
+};
+
+int sfo_pool_create(const sfo_pool_config* cfg, sfo_pool** out) {
+  if (!cfg || !out || cfg->max_workflows <= 0 || cfg->n_blocks <= 0 || cfg->capacity_tokens <= 0 ||
+      cfg->max_pin_blocks <= 0)
+    return -1;
+  sfo_pool* p = (sfo_pool*)calloc(1, sizeof(sfo_pool));
+  p->cfg = *cfg;
+  int64_t W = cfg->max_workflows, B = cfg->n_blocks, MB = cfg->max_pin_blocks;
+  p->pin_len = (int64_t*)malloc((size_t)W * sizeof(int64_t));
+  for (int64_t i = 0; i < W; ++i) p->pin_len[i] = -1;
+  p->pin_tok = (uint32_t**)calloc((size_t)W, sizeof(uint32_t*));
+  p->pin_nblk = (int32_t*)calloc((size_t)W, sizeof(int32_t));
+  p->pin_blk = (int32_t*)calloc((size_t)(W * MB), sizeof(int32_t));
+  p->pin_hash = (uint64_t*)calloc((size_t)(W * MB), sizeof(uint64_t));
+  p->blk_key = (uint64_t*)calloc((size_t)B, sizeof(uint64_t));
+  p->blk_tok = (uint32_t*)calloc((size_t)(B * BT), sizeof(uint32_t));
+  p->blk_n = (uint8_t*)calloc((size_t)B, 1);
+  p->blk_in_table = (uint8_t*)calloc((size_t)B, 1);
+  p->blk_ref = (uint32_t*)calloc((size_t)B, sizeof(uint32_t));
+  p->blk_free = (uint8_t*)malloc((size_t)B);
+  memset(p->blk_free, 1, (size_t)B);
+  kmap_init(&p->table, B);
+  p->block_bytes = (int64_t)cfg->n_slabs * BT * cfg->slab_row_bytes;
+  if (p->block_bytes > 0) p->kv = (uint8_t*)calloc((size_t)(B * p->block_bytes), 1);
+  *out = p;
+  return 0;
+}
+
+int sfo_pool_destroy(sfo_pool* p) {
+  if (!p) return 0;
+  for (int64_t i = 0; i < p->cfg.max_workflows; ++i) free(p->pin_tok[i]);
+  free(p->pin_len); free(p->pin_tok); free(p->pin_nblk); free(p->pin_blk); free(p->pin_hash);
+  free(p->blk_key); free(p->blk_tok); free(p->blk_n); free(p->blk_in_table); free(p->blk_ref);
+  free(p->blk_free); kmap_free(&p->table); free(p->kv); free(p);
+  return 0;
+}
+
+int sfo_pool_kv(sfo_pool* p, void** kv, int64_t* block_bytes) {
+  *kv = p->kv;
+  *block_bytes = p->block_bytes;
+  return 0;
+}
+
+static int bad_wf(const sfo_pool* p, int32_t wf) { return wf < 0 || wf >= p->cfg.max_workflows; }
+
+static int64_t lcp(const uint32_t* a, int64_t na, const uint32_t* b, int64_t nb) {
+  int64_t n = na < nb ? na : nb, i = 0;
+  while (i < n && a[i] == b[i]) ++i;
+  return i;
+}
+
+/* M[r] = LCP(pin[wf[r]], tokens_r), 0 without a pin (simulated_backend.cpp:153-162). */
+int sfo_match_batch(sfo_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
+                    const uint32_t* tok, int64_t* out_M, uint64_t* out_hash) {
+  int64_t hb = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    if (bad_wf(p, wf[r])) return -1;
+    int64_t len = tok_off[r + 1] - tok_off[r];
+    const uint32_t* t = tok + tok_off[r];
+    int64_t pl = p->pin_len[wf[r]];
+    out_M[r] = pl < 0 ? 0 : lcp(p->pin_tok[wf[r]], pl, t, len);
+    if (out_hash) {
+      sfo_chain_hashes(t, len, out_hash + hb);
+      hb += (len + BT - 1) / BT;
+    }
+  }
+  return 0;
+}
+
+static int blk_tokens_eq(const sfo_pool* p, int32_t id, const uint32_t* t) {
+  return p->blk_n[id] == BT && memcmp(p->blk_tok + (int64_t)id * BT, t, BT * sizeof(uint32_t)) == 0;
+}
+
+/* Global lookup: each FULL block's chained hash against the table, token-verified. */
+int sfo_lookup_batch(sfo_pool* p, int64_t n, const int64_t* tok_off, const uint32_t* tok,
+                     int32_t* out_block, int64_t* out_hit_tokens) {
+  int64_t ob = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    int64_t len = tok_off[r + 1] - tok_off[r];
+    const uint32_t* t = tok + tok_off[r];
+    int64_t nb = (len + BT - 1) / BT, nfull = len / BT;
+    uint64_t* h = (uint64_t*)malloc((size_t)(nb > 0 ? nb : 1) * sizeof(uint64_t));
+    sfo_chain_hashes(t, len, h);
+    int64_t lead = 0, run = 1;
+    for (int64_t k = 0; k < nfull; ++k) {
+      int32_t id = kmap_get(&p->table, h[k]);
+      if (id >= 0 && !blk_tokens_eq(p, id, t + k * BT)) id = -1;
+      out_block[ob++] = id;
+      if (id < 0) run = 0;
+      if (run) ++lead;
+    }
+    if (out_hit_tokens) out_hit_tokens[r] = lead * BT;
+    free(h);
+  }
+  return 0;
+}
+
+static void release_block(sfo_pool* p, int32_t id) {
+  if (--p->blk_ref[id] == 0) {
+    p->blk_free[id] = 1;
+    if (p->blk_in_table[id]) {
+      kmap_del(&p->table, p->blk_key[id]);
+      p->blk_in_table[id] = 0;
+    }
+  }
+}
+
+static void release_pin(sfo_pool* p, int32_t w) {
+  if (p->pin_len[w] < 0) return;
+  for (int32_t k = 0; k < p->pin_nblk[w]; ++k)
+    release_block(p, p->pin_blk[(int64_t)w * p->cfg.max_pin_blocks + k]);
+  p->occupancy -= p->pin_len[w];
+  p->pin_len[w] = -1;
+  p->pin_nblk[w] = 0;
+  free(p->pin_tok[w]);
+  p->pin_tok[w] = NULL;
+}
+
+/* Block categories of a commit item. */
+enum { C_HIT = 0, C_DUP = 1, C_OWN = 2, C_PRIV = 3 };
+
+/* Payload source of one token row of a new block. */
+typedef struct {
+  const uint8_t* staging;   /* staging base of this request (NULL: metadata only) */
+  int64_t staging_rows;     /* P - M */
+  int64_t m;                /* rows < m come from the old pin */
+  const sfo_pool* cow_pool; /* pool holding the old pin / handoff source */
+  const int32_t* cow_blk;   /* block table of that pin */
+} row_src;
+
+static void write_block_payload(sfo_pool* p, int32_t id, int64_t k, int64_t nvalid,
+                                const row_src* s) {
+  if (!p->kv) return;
+  const int64_t row = p->cfg.slab_row_bytes, S = p->cfg.n_slabs;
+  uint8_t* dst = p->kv + (int64_t)id * p->block_bytes;
+  for (int64_t j = 0; j < nvalid; ++j) {
+    int64_t pos = k * BT + j;
+    for (int64_t sl = 0; sl < S; ++sl) {
+      uint8_t* d = dst + (sl * BT + j) * row;
+      if (pos < s->m) {
+        const sfo_pool* q = s->cow_pool;
+        int32_t sid = s->cow_blk[k];
+        memcpy(d, q->kv + (int64_t)sid * q->block_bytes + (sl * BT + j) * row, (size_t)row);
+      } else if (s->staging) {
+        memcpy(d, s->staging + (sl * s->staging_rows + (pos - s->m)) * row, (size_t)row);
+      }
+    }
+  }
+}
+
+/* Commit (sfkv.h: sfkv_commit_batch). Phase order of a batch:
+ *   0. M_r = LCP(old pin, tokens) for every request; m_expected check (payload commits).
+ *   1. admission in request order (simulated_backend.cpp:141-150).
+ *   2. block categories against T0 = table at batch start, items in batch order (r, k):
+ *        hit0 : full block, T0 has its chained key and the block's tokens are equal
+ *        claim: full block whose key is not in T0; owner(key) = first claim item with that key
+ *        dup  : claim item, owner earlier, tokens equal to the owner's
+ *        f_r  : first block that is neither hit0 nor dup
+ *        k < f_r -> HIT (T0 block) or DUP (owner's block)
+ *        k >= f_r -> OWN if it is its key's owner (allocated + inserted), else PRIV (allocated)
+ *      OWN/PRIV items take the lowest free block ids in batch order; every item takes a ref.
+ *   3. payload of OWN/PRIV blocks (rows < M_r from the old pin's block: copy-on-share).
+ *   4. old pins released (ref--, free and unindex at 0), new pins installed. */
+static int commit_impl(sfo_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
+                       const uint32_t* tok, const void* kv_src, const int64_t* kv_src_off,
+                       const int64_t* m_expected, int32_t* out_status,
+                       const sfo_pool* src_pool, const int32_t* src_blk) {
+  const int64_t MB = p->cfg.max_pin_blocks;
+  for (int64_t r = 0; r < n; ++r) {
+    if (bad_wf(p, wf[r])) return -1;
+    for (int64_t q = 0; q < r; ++q)
+      if (wf[q] == wf[r]) return -1; /* distinct slots per batch */
+    int64_t len = tok_off[r + 1] - tok_off[r];
+    if ((len + BT - 1) / BT > MB) return -5;
+  }
+  int64_t* M = (int64_t*)malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
+  for (int64_t r = 0; r < n; ++r) {
+    int64_t len = tok_off[r + 1] - tok_off[r];
+    int64_t pl = p->pin_len[wf[r]];
+    M[r] = pl < 0 ? 0 : lcp(p->pin_tok[wf[r]], pl, tok + tok_off[r], len);
+    if (kv_src && m_expected && p->kv && m_expected[r] != M[r]) {
+      free(M);
+      return -6;
+    }
+  }
+  /* 1. admission */
+  for (int64_t r = 0; r < n; ++r) {
+    int64_t old = p->pin_len[wf[r]] < 0 ? 0 : p->pin_len[wf[r]];
+    int64_t nw = tok_off[r + 1] - tok_off[r];
+    if (p->occupancy - old + nw > p->cfg.capacity_tokens) {
+      out_status[r] = 0;
+      p->rejections++;
+    } else {
+      out_status[r] = 1;
+      p->occupancy += nw - old;
+    }
+  }
+  /* 2. items */
+  int64_t n_items = 0;
+  int64_t* item_off = (int64_t*)malloc((size_t)(n + 1) * sizeof(int64_t));
+  for (int64_t r = 0; r < n; ++r) {
+    item_off[r] = n_items;
+    if (out_status[r]) n_items += (tok_off[r + 1] - tok_off[r] + BT - 1) / BT;
+  }
+  item_off[n] = n_items;
+  int64_t NI = n_items > 0 ? n_items : 1;
+  uint64_t* key = (uint64_t*)malloc((size_t)NI * sizeof(uint64_t));
+  int32_t* cat = (int32_t*)malloc((size_t)NI * sizeof(int32_t));
+  int32_t* bid = (int32_t*)malloc((size_t)NI * sizeof(int32_t));
+  int64_t* owner = (int64_t*)malloc((size_t)NI * sizeof(int64_t));
+  uint8_t* hit0 = (uint8_t*)calloc((size_t)NI, 1);
+  uint8_t* claim = (uint8_t*)calloc((size_t)NI, 1);
+  kmap first_claim;
+  kmap_init(&first_claim, NI);
+  for (int64_t r = 0; r < n; ++r) {
+    if (!out_status[r]) continue;
+    int64_t len = tok_off[r + 1] - tok_off[r];
+    sfo_chain_hashes(tok + tok_off[r], len, key + item_off[r]);
+    for (int64_t k = 0; k < item_off[r + 1] - item_off[r]; ++k) {
+      int64_t it = item_off[r] + k;
+      int64_t nv = len - k * BT;
+      owner[it] = -1;
+      if (nv < BT) continue;
+      int32_t id = kmap_get(&p->table, key[it]);
+      if (id >= 0) {
+        if (blk_tokens_eq(p, id, tok + tok_off[r] + k * BT)) {
+          hit0[it] = 1;
+          bid[it] = id;
+        }
+      } else {
+        claim[it] = 1;
+        int32_t f = kmap_get(&first_claim, key[it]);
+        if (f < 0) {
+          kmap_put(&first_claim, key[it], (int32_t)it);
+          f = (int32_t)it;
+        }
+        owner[it] = f;
+      }
+    }
+  }
+  kmap_free(&first_claim);
+  /* item -> (request, block) for owners */
+  int64_t* item_req = (int64_t*)malloc((size_t)NI * sizeof(int64_t));
+  for (int64_t r = 0; r < n; ++r)
+    for (int64_t it = item_off[r]; it < item_off[r + 1]; ++it) item_req[it] = r;
+  int64_t scan_free = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    if (!out_status[r]) continue;
+    int64_t nb = item_off[r + 1] - item_off[r];
+    int64_t f = nb;
+    for (int64_t k = 0; k < nb; ++k) {
+      int64_t it = item_off[r] + k;
+      int dup = 0;
+      if (claim[it] && owner[it] < it) {
+        int64_t o = owner[it], orq = item_req[o], ok = o - item_off[orq];
+        dup = memcmp(tok + tok_off[orq] + ok * BT, tok + tok_off[r] + k * BT,
+                     BT * sizeof(uint32_t)) == 0;
+      }
+      if (!(hit0[it] || dup)) {
+        f = k;
+        break;
+      }
+    }
+    for (int64_t k = 0; k < nb; ++k) {
+      int64_t it = item_off[r] + k;
+      if (k < f) cat[it] = hit0[it] ? C_HIT : C_DUP;
+      else cat[it] = (claim[it] && owner[it] == it) ? C_OWN : C_PRIV;
+    }
+  }
+  /* allocation: lowest free ids in batch order */
+  for (int64_t it = 0; it < n_items; ++it) {
+    if (cat[it] != C_OWN && cat[it] != C_PRIV) continue;
+    while (scan_free < p->cfg.n_blocks && !p->blk_free[scan_free]) ++scan_free;
+    if (scan_free >= p->cfg.n_blocks) {
+      /* physical pool exhausted: undo nothing (callers size pools so this cannot happen) */
+      free(M); free(item_off); free(key); free(cat); free(bid); free(owner); free(hit0);
+      free(claim); free(item_req);
+      return -5;
+    }
+    bid[it] = (int32_t)scan_free++;
+  }
+  for (int64_t it = 0; it < n_items; ++it)
+    if (cat[it] == C_DUP) bid[it] = bid[owner[it]];
+  /* metadata of new blocks + refs */
+  for (int64_t r = 0; r < n; ++r) {
+    if (!out_status[r]) continue;
+    int64_t len = tok_off[r + 1] - tok_off[r];
+    for (int64_t k = 0; k < item_off[r + 1] - item_off[r]; ++k) {
+      int64_t it = item_off[r] + k;
+      int32_t id = bid[it];
+      if (cat[it] == C_OWN || cat[it] == C_PRIV) {
+        int64_t nv = len - k * BT;
+        if (nv > BT) nv = BT;
+        p->blk_free[id] = 0;
+        p->blk_key[id] = key[it];
+        p->blk_n[id] = (uint8_t)nv;
+        memset(p->blk_tok + (int64_t)id * BT, 0, BT * sizeof(uint32_t));
+        memcpy(p->blk_tok + (int64_t)id * BT, tok + tok_off[r] + k * BT, (size_t)nv * sizeof(uint32_t));
+        p->blk_ref[id] = 0;
+        p->blk_in_table[id] = 0;
+        if (cat[it] == C_OWN) {
+          kmap_put(&p->table, key[it], id);
+          p->blk_in_table[id] = 1;
+        }
+      }
+    }
+  }
+  for (int64_t it = 0; it < n_items; ++it) p->blk_ref[bid[it]]++;
+  /* 3. payload */
+  for (int64_t r = 0; r < n; ++r) {
+    if (!out_status[r] || !p->kv) continue;
+    int64_t len = tok_off[r + 1] - tok_off[r];
+    row_src s;
+    int32_t w = wf[r];
+    if (src_pool) { /* handoff: rows < M from dst's old pin, rows >= M from the source pin */
+      s.staging = NULL;
+      s.staging_rows = 0;
+    } else {
+      s.staging = kv_src ? (const uint8_t*)kv_src + kv_src_off[r] : NULL;
+      s.staging_rows = len - M[r];
+    }
+    s.m = M[r];
+    s.cow_pool = p;
+    s.cow_blk = p->pin_blk + (int64_t)w * MB;
+    for (int64_t k = 0; k < item_off[r + 1] - item_off[r]; ++k) {
+      int64_t it = item_off[r] + k;
+      if (cat[it] != C_OWN && cat[it] != C_PRIV) continue;
+      int64_t nv = len - k * BT;
+      if (nv > BT) nv = BT;
+      if (src_pool) {
+        /* per row: < M from own old pin, else from the source pin's block k */
+        const int64_t row = p->cfg.slab_row_bytes, S = p->cfg.n_slabs;
+        uint8_t* dst = p->kv + (int64_t)bid[it] * p->block_bytes;
+        for (int64_t j = 0; j < nv; ++j) {
+          int64_t pos = k * BT + j;
+          for (int64_t sl = 0; sl < S; ++sl) {
+            const uint8_t* src =
+                pos < M[r] ? p->kv + (int64_t)s.cow_blk[k] * p->block_bytes
+                           : src_pool->kv + (int64_t)src_blk[k] * src_pool->block_bytes;
+            memcpy(dst + (sl * BT + j) * row, src + (sl * BT + j) * row, (size_t)row);
+          }
+        }
+      } else {
+        write_block_payload(p, bid[it], k, nv, &s);
+      }
+    }
+  }
+  /* 4. release old pins, install new */
+  for (int64_t r = 0; r < n; ++r) {
+    if (!out_status[r]) continue;
+    int32_t w = wf[r];
+    int64_t len = tok_off[r + 1] - tok_off[r];
+    int64_t saved_occ = p->occupancy;
+    release_pin(p, w); /* adjusts occupancy; admission already accounted, restore below */
+    p->occupancy = saved_occ;
+    int64_t nb = item_off[r + 1] - item_off[r];
+    p->pin_len[w] = len;
+    p->pin_nblk[w] = (int32_t)nb;
+    p->pin_tok[w] = (uint32_t*)malloc((size_t)(len > 0 ? len : 1) * sizeof(uint32_t));
+    memcpy(p->pin_tok[w], tok + tok_off[r], (size_t)len * sizeof(uint32_t));
+    for (int64_t k = 0; k < nb; ++k) {
+      p->pin_blk[(int64_t)w * MB + k] = bid[item_off[r] + k];
+      p->pin_hash[(int64_t)w * MB + k] = key[item_off[r] + k];
+    }
+  }
+  free(M); free(item_off); free(key); free(cat); free(bid); free(owner); free(hit0); free(claim);
+  free(item_req);
+  return 0;
+}
+
+int sfo_commit_batch(sfo_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
+                     const uint32_t* tok, const void* kv_src, const int64_t* kv_src_off,
+                     const int64_t* m_expected, int32_t* out_status) {
+  return commit_impl(p, n, wf, tok_off, tok, kv_src, kv_src_off, m_expected, out_status, NULL,
+                     NULL);
+}
+
+/* flush (simulated_backend.cpp:169-184). */
+int sfo_flush(sfo_pool* p, int32_t wf, int64_t* freed) {
+  p->flush_calls++;
+  if (wf == -1) {
+    *freed = p->occupancy;
+    for (int32_t w = 0; w < p->cfg.max_workflows; ++w) release_pin(p, w);
+    p->occupancy = 0;
+    return 0;
+  }
+  if (bad_wf(p, wf)) return -1;
+  *freed = p->pin_len[wf] < 0 ? 0 : p->pin_len[wf];
+  release_pin(p, wf);
+  return 0;
+}
+
+int sfo_flush_batch(sfo_pool* p, int64_t n, const int32_t* wf, int64_t* out_freed) {
+  for (int64_t r = 0; r < n; ++r) {
+    if (bad_wf(p, wf[r])) return -1;
+    for (int64_t q = 0; q < r; ++q)
+      if (wf[q] == wf[r]) return -1;
+  }
+  for (int64_t r = 0; r < n; ++r) sfo_flush(p, wf[r], &out_freed[r]);
+  return 0;
+}
+
+int sfo_preserve(sfo_pool* p, int32_t wf, int32_t* has_pin) {
+  if (bad_wf(p, wf)) return -1;
+  p->preserve_calls++;
+  *has_pin = p->pin_len[wf] >= 0;
+  return 0;
+}
+
+int sfo_pinned_token_count(sfo_pool* p, int32_t wf, int64_t* n_tokens) {
+  if (bad_wf(p, wf)) return -1;
+  *n_tokens = p->pin_len[wf] < 0 ? 0 : p->pin_len[wf];
+  return 0;
+}
+
+int sfo_cache_utilization(sfo_pool* p, double* util) {
+  *util = (double)p->occupancy / (double)p->cfg.capacity_tokens;
+  return 0;
+}
+
+int sfo_stats(sfo_pool* p, sfo_pool_stats* o) {
+  o->occupancy_tokens = p->occupancy;
+  o->capacity_tokens = p->cfg.capacity_tokens;
+  o->capacity_rejections = p->rejections;
+  o->flush_calls = p->flush_calls;
+  o->preserve_calls = p->preserve_calls;
+  int64_t used = 0;
+  for (int64_t b = 0; b < p->cfg.n_blocks; ++b) used += p->blk_ref[b] > 0;
+  o->blocks_in_use = used;
+  o->table_live = p->table.live;
+  o->table_tombstones = 0;
+  return 0;
+}
+
+int sfo_pin_blocks(sfo_pool* p, int32_t wf, int32_t* ids, uint64_t* hashes, int32_t cap,
+                   int32_t* n_blocks) {
+  if (bad_wf(p, wf)) return -1;
+  int32_t nb = p->pin_len[wf] < 0 ? 0 : p->pin_nblk[wf];
+  *n_blocks = nb;
+  for (int32_t k = 0; k < nb && k < cap; ++k) {
+    if (ids) ids[k] = p->pin_blk[(int64_t)wf * p->cfg.max_pin_blocks + k];
+    if (hashes) hashes[k] = p->pin_hash[(int64_t)wf * p->cfg.max_pin_blocks + k];
+  }
+  return 0;
+}
+
+int sfo_block_refcounts(sfo_pool* p, uint32_t* out) {
+  memcpy(out, p->blk_ref, (size_t)p->cfg.n_blocks * sizeof(uint32_t));
+  return 0;
+}
+
+/* gather: request r's pin at dst + dst_off[r], layout [slab][token][row]. */
+int sfo_gather(sfo_pool* p, int64_t n, const int32_t* wf, void* dst, const int64_t* dst_off) {
+  if (!p->kv) return -1;
+  const int64_t row = p->cfg.slab_row_bytes, S = p->cfg.n_slabs;
+  for (int64_t r = 0; r < n; ++r) {
+    if (bad_wf(p, wf[r])) return -1;
+    int64_t L = p->pin_len[wf[r]];
+    if (L <= 0) continue;
+    uint8_t* d = (uint8_t*)dst + dst_off[r];
+    for (int64_t pos = 0; pos < L; ++pos) {
+      int32_t id = p->pin_blk[(int64_t)wf[r] * p->cfg.max_pin_blocks + pos / BT];
+      for (int64_t sl = 0; sl < S; ++sl)
+        memcpy(d + (sl * L + pos) * row,
+               p->kv + (int64_t)id * p->block_bytes + (sl * BT + pos % BT) * row, (size_t)row);
+    }
+  }
+  return 0;
+}
+
+/* handoff: commit src's pin into dst; payload rows from dst's old pin (< M) or the source pin. */
+int sfo_handoff(sfo_pool* src, int32_t wf_src, sfo_pool* dst, int32_t wf_dst, int32_t* status) {
+  if (bad_wf(src, wf_src) || bad_wf(dst, wf_dst)) return -1;
+  if (src->cfg.n_slabs != dst->cfg.n_slabs || src->cfg.slab_row_bytes != dst->cfg.slab_row_bytes)
+    return -1;
+  int64_t L = src->pin_len[wf_src];
+  if (L < 0) {
+    *status = 0;
+    return -1;
+  }
+  int64_t off[2] = {0, L};
+  int32_t w = wf_dst;
+  return commit_impl(dst, 1, &w, off, src->pin_tok[wf_src], NULL, NULL, NULL, status, src,
+                     src->pin_blk + (int64_t)wf_src * src->cfg.max_pin_blocks);
+}
+
+/* pressure_actions (memory.cpp:150-169): per backend with util > tau (strict), the preserved
+ * entry with zero in-flight and minimum (last_update_ts, workflow id order). The reference scans
+ * entries in workflow-id order and replaces only on strict <, i.e. ties go to the smallest id. */
+int sfo_pressure_argmin(int64_t n, const int32_t* backend, const double* ts,
+                        const uint32_t* wf_rank, const int32_t* in_flight,
+                        const uint8_t* preserved, int32_t n_backends, const double* util,
+                        double tau, int64_t* out_victim) {
+  for (int32_t b = 0; b < n_backends; ++b) out_victim[b] = -1;
+  for (int32_t b = 0; b < n_backends; ++b) {
+    if (!(util[b] > tau)) continue;
+    int64_t best = -1;
+    for (int64_t i = 0; i < n; ++i) {
+      if (backend[i] != b || !preserved[i] || in_flight[i] > 0) continue;
+      if (best < 0 || ts[i] < ts[best] || (ts[i] == ts[best] && wf_rank[i] < wf_rank[best]))
+        best = i;
+    }
+    out_victim[b] = best;
+  }
+  return 0;
+}
+
+/* map_threshold (mapper.cpp:19-31): light (0) iff score <= threshold. */
+int sfo_threshold_batch(int64_t n, const double* score, double threshold, int32_t* out_choice) {
+  for (int64_t r = 0; r < n; ++r) out_choice[r] = score[r] <= threshold ? 0 : 1;
+  return 0;
+}
+
+/* N-candidate cost + reroute_on_overload (orchestrator.cpp:78-87), sequential in request order. */
+int sfo_cost_batch(int64_t n, int32_t c, const int64_t* P, const int64_t* M, const int64_t* O,
+                   const double* overhead, const double* prefill, const double* decode,
+                   const double* queue_penalty, const int32_t* alternates, uint64_t* depth,
+                   uint64_t limit, int32_t* out_choice, double* out_cost) {
+  /* Costs see the batch-start depth snapshot; reroute sees the live depth. */
+  uint64_t* depth0 = (uint64_t*)malloc((size_t)c * sizeof(uint64_t));
+  memcpy(depth0, depth, (size_t)c * sizeof(uint64_t));
+  for (int64_t r = 0; r < n; ++r) {
+    int32_t best = 0;
+    double bc = 0;
+    for (int32_t j = 0; j < c; ++j) {
+      double cost = overhead[j] + prefill[j] * (double)(P[r] - M[r * c + j]) +
+                    decode[j] * (double)O[r] + queue_penalty[j] * (double)depth0[j];
+      if (j == 0 || cost < bc) {
+        bc = cost;
+        best = j;
+      }
+    }
+    out_cost[r] = bc;
+    int32_t pick = best;
+    if (limit > 0 && depth[best] >= limit) {
+      for (int32_t a = 0; alternates && a < c; ++a) {
+        int32_t alt = alternates[best * c + a];
+        if (alt < 0) break;
+        if (depth[alt] < limit) {
+          pick = alt;
+          break;
+        }
+      }
+    }
+    out_choice[r] = pick;
+    depth[pick]++;
+  }
+  free(depth0);
+  return 0;
+}

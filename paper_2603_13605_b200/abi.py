@@ -1,0 +1,294 @@
+"""ctypes binding of the sfkv C ABI (include/sfkv.h) and a numpy-level pool wrapper.
+
+The binding is prefix-parameterised because the CPU oracle (oracle/sfkv_oracle.h) restates the
+same entry points under the ``sfo_`` prefix: tests bind both libraries through this one table
+and drive them with identical arguments. The product path binds only ``libsfkv.so``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+BLOCK_TOKENS = 16
+FLUSH_ALL = -1
+
+ERRORS = {
+    -1: "SFKV_EINVAL",
+    -2: "SFKV_ENODEV",
+    -3: "SFKV_ECUDA",
+    -4: "SFKV_ENOMEM",
+    -5: "SFKV_EPOOL",
+    -6: "SFKV_ESTALE",
+}
+
+
+class PoolConfig(C.Structure):
+    _fields_ = [
+        ("device", C.c_int32),
+        ("max_workflows", C.c_int32),
+        ("n_blocks", C.c_int64),
+        ("capacity_tokens", C.c_int64),
+        ("max_pin_blocks", C.c_int32),
+        ("table_log2", C.c_int32),
+        ("n_slabs", C.c_int32),
+        ("slab_row_bytes", C.c_int32),
+    ]
+
+
+class PoolStats(C.Structure):
+    _fields_ = [
+        ("occupancy_tokens", C.c_int64),
+        ("capacity_tokens", C.c_int64),
+        ("capacity_rejections", C.c_uint64),
+        ("flush_calls", C.c_uint64),
+        ("preserve_calls", C.c_uint64),
+        ("blocks_in_use", C.c_int64),
+        ("table_live", C.c_int64),
+        ("table_tombstones", C.c_int64),
+    ]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+P = C.c_void_p
+i32, i64, u32, u64, f64 = C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_double
+
+# name -> argtypes (all return int unless listed in _RESTYPES)
+SIGNATURES = {
+    "pool_create": [C.POINTER(PoolConfig), C.POINTER(P)],
+    "pool_destroy": [P],
+    "pool_kv": [P, C.POINTER(P), C.POINTER(i64)],
+    "match_batch": [P, i64, P, P, P, P, P],
+    "lookup_batch": [P, i64, P, P, P, P],
+    "commit_batch": [P, i64, P, P, P, P, P, P, P],
+    "flush": [P, i32, C.POINTER(i64)],
+    "flush_batch": [P, i64, P, P],
+    "preserve": [P, i32, C.POINTER(i32)],
+    "pinned_token_count": [P, i32, C.POINTER(i64)],
+    "cache_utilization": [P, C.POINTER(f64)],
+    "stats": [P, C.POINTER(PoolStats)],
+    "pin_blocks": [P, i32, P, P, i32, C.POINTER(i32)],
+    "block_refcounts": [P, P],
+    "handoff": [P, i32, P, i32, C.POINTER(i32)],
+    "block_digest": [u64, u32, P],
+    "chain_finalize": [u64],
+}
+# entry points whose name differs between the GPU ABI and the oracle
+GPU_ONLY = {
+    "abi_version": [],
+    "last_error": [],
+    "pool_set_stream": [P, P],
+    "pool_sync": [P],
+    "match_batch_dev": [P, i64, P, P, P, P, P],
+    "lookup_batch_dev": [P, i64, P, P, P, P],
+    "commit_batch_dev": [P, i64, P, P, P, P, P, P, P],
+    "gather_dev": [P, i64, P, P, P],
+}
+ORACLE_ONLY = {
+    "gather": [P, i64, P, P, P],
+    "chain_hashes": [P, i64, P],
+}
+GLOBAL_FNS = {  # prefix differs: sfmm_/sfmap_ on the GPU, sfo_ in the oracle
+    "pressure_argmin": [P, i64, P, P, P, P, P, i32, P, f64, P],
+    "threshold_batch": [P, i64, P, f64, P],
+    "cost_batch": [P, i64, i32, P, P, P, P, P, P, P, P, P, u64, P, P],
+}
+_RESTYPES = {
+    "block_digest": u64,
+    "chain_finalize": u64,
+    "last_error": C.c_char_p,
+    "chain_hashes": None,
+}
+
+
+class SfkvError(RuntimeError):
+    def __init__(self, fn, code, detail=""):
+        super().__init__(f"{fn} failed: {ERRORS.get(code, code)} {detail}".strip())
+        self.code = code
+
+
+class Api:
+    """Bound entry points of one library: ``api.match_batch(...)`` etc. (raw ints returned)."""
+
+    def __init__(self, lib: C.CDLL, kind: str):
+        assert kind in ("gpu", "oracle")
+        self.lib, self.kind = lib, kind
+        pre = "sfkv_" if kind == "gpu" else "sfo_"
+        table = dict(SIGNATURES)
+        table.update(GPU_ONLY if kind == "gpu" else ORACLE_ONLY)
+        for name, argt in table.items():
+            self._bind(pre + name, name, argt)
+        for name, argt in GLOBAL_FNS.items():
+            if kind == "gpu":
+                sym = ("sfmm_" if name == "pressure_argmin" else "sfmap_") + name
+                self._bind(sym, name, [i32] + argt[1:])  # first arg: device ordinal
+            else:
+                self._bind("sfo_" + name, name, argt[1:])
+
+    def _bind(self, sym, name, argt):
+        fn = getattr(self.lib, sym)
+        fn.argtypes = argt
+        fn.restype = _RESTYPES.get(name, C.c_int)
+        setattr(self, name, fn)
+
+    def check(self, fn: str, rc: int):
+        if rc != 0:
+            detail = ""
+            if self.kind == "gpu":
+                msg = self.lib.sfkv_last_error()
+                detail = msg.decode() if msg else ""
+            raise SfkvError(fn, rc, detail)
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"]
+        return a.ctypes.data_as(C.c_void_p)
+    if hasattr(a, "data_ptr"):  # torch tensor (device pointer for *_dev entry points)
+        return C.c_void_p(a.data_ptr())
+    return a
+
+
+def csr(seqs):
+    """List of token sequences -> (tok_off int64[n+1], tok uint32[total])."""
+    off = np.zeros(len(seqs) + 1, dtype=np.int64)
+    for i, s in enumerate(seqs):
+        off[i + 1] = off[i] + len(s)
+    tok = np.zeros(max(int(off[-1]), 1), dtype=np.uint32)
+    for i, s in enumerate(seqs):
+        tok[off[i]:off[i + 1]] = np.asarray(s, dtype=np.uint32)
+    return off, tok
+
+
+def n_blocks_of(tok_off):
+    lens = np.diff(tok_off)
+    return (lens + BLOCK_TOKENS - 1) // BLOCK_TOKENS
+
+
+@dataclass
+class Config:
+    max_workflows: int = 64
+    n_blocks: int = 4096
+    capacity_tokens: int = 1_000_000
+    max_pin_blocks: int = 256
+    table_log2: int = 14
+    n_slabs: int = 0
+    slab_row_bytes: int = 0
+    device: int = 0
+
+    def c(self):
+        return PoolConfig(self.device, self.max_workflows, self.n_blocks, self.capacity_tokens,
+                          self.max_pin_blocks, self.table_log2, self.n_slabs, self.slab_row_bytes)
+
+    @property
+    def block_bytes(self):
+        return self.n_slabs * BLOCK_TOKENS * self.slab_row_bytes
+
+
+class Pool:
+    """numpy-level wrapper over one pool handle (host-pointer entry points)."""
+
+    def __init__(self, api: Api, cfg: Config):
+        self.api, self.cfg = api, cfg
+        h = C.c_void_p()
+        api.check("pool_create", api.pool_create(C.byref(cfg.c()), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            self.api.pool_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- lookup ---------------------------------------------------------------------------
+    def match(self, wf, tok_off, tok, want_hash=False):
+        wf = np.ascontiguousarray(wf, dtype=np.int32)
+        M = np.zeros(len(wf), dtype=np.int64)
+        h = np.zeros(max(int(n_blocks_of(tok_off).sum()), 1), dtype=np.uint64) if want_hash else None
+        self.api.check("match_batch", self.api.match_batch(self.h, len(wf), _ptr(wf), _ptr(tok_off),
+                                                           _ptr(tok), _ptr(M), _ptr(h)))
+        return (M, h[: int(n_blocks_of(tok_off).sum())]) if want_hash else M
+
+    def lookup(self, tok_off, tok):
+        n = len(tok_off) - 1
+        nfull = int((np.diff(tok_off) // BLOCK_TOKENS).sum())
+        out = np.zeros(max(nfull, 1), dtype=np.int32)
+        hit = np.zeros(n, dtype=np.int64)
+        self.api.check("lookup_batch", self.api.lookup_batch(self.h, n, _ptr(tok_off), _ptr(tok),
+                                                             _ptr(out), _ptr(hit)))
+        return out[:nfull], hit
+
+    # -- retain / evict -------------------------------------------------------------------
+    def commit(self, wf, tok_off, tok, kv_src=None, kv_src_off=None, m_expected=None):
+        wf = np.ascontiguousarray(wf, dtype=np.int32)
+        st = np.zeros(len(wf), dtype=np.int32)
+        self.api.check("commit_batch", self.api.commit_batch(
+            self.h, len(wf), _ptr(wf), _ptr(tok_off), _ptr(tok), _ptr(kv_src), _ptr(kv_src_off),
+            _ptr(m_expected), _ptr(st)))
+        return st
+
+    def flush(self, wf):
+        out = C.c_int64()
+        self.api.check("flush", self.api.flush(self.h, int(wf), C.byref(out)))
+        return out.value
+
+    def flush_batch(self, wf):
+        wf = np.ascontiguousarray(wf, dtype=np.int32)
+        out = np.zeros(len(wf), dtype=np.int64)
+        self.api.check("flush_batch", self.api.flush_batch(self.h, len(wf), _ptr(wf), _ptr(out)))
+        return out
+
+    def preserve(self, wf):
+        out = C.c_int32()
+        self.api.check("preserve", self.api.preserve(self.h, int(wf), C.byref(out)))
+        return bool(out.value)
+
+    def pinned_token_count(self, wf):
+        out = C.c_int64()
+        self.api.check("pinned_token_count", self.api.pinned_token_count(self.h, int(wf), C.byref(out)))
+        return out.value
+
+    def cache_utilization(self):
+        out = C.c_double()
+        self.api.check("cache_utilization", self.api.cache_utilization(self.h, C.byref(out)))
+        return out.value
+
+    def stats(self):
+        s = PoolStats()
+        self.api.check("stats", self.api.stats(self.h, C.byref(s)))
+        return s.as_dict()
+
+    def pin_blocks(self, wf):
+        cap = self.cfg.max_pin_blocks
+        ids = np.zeros(cap, dtype=np.int32)
+        hs = np.zeros(cap, dtype=np.uint64)
+        n = C.c_int32()
+        self.api.check("pin_blocks", self.api.pin_blocks(self.h, int(wf), _ptr(ids), _ptr(hs), cap,
+                                                         C.byref(n)))
+        return ids[: n.value], hs[: n.value]
+
+    def refcounts(self):
+        out = np.zeros(self.cfg.n_blocks, dtype=np.uint32)
+        self.api.check("block_refcounts", self.api.block_refcounts(self.h, _ptr(out)))
+        return out
+
+    def handoff_to(self, wf_src, dst: "Pool", wf_dst):
+        st = C.c_int32()
+        self.api.check("handoff", self.api.handoff(self.h, int(wf_src), dst.h, int(wf_dst),
+                                                   C.byref(st)))
+        return st.value
+
+    def kv_ptr(self):
+        p, bb = C.c_void_p(), C.c_int64()
+        self.api.check("pool_kv", self.api.pool_kv(self.h, C.byref(p), C.byref(bb)))
+        return p.value, bb.value
