@@ -105,9 +105,9 @@ int sfkv_match_batch_dev(sfkv_pool* pool, int64_t n, const int32_t* wf, const in
                          const uint32_t* tok, int64_t* out_M, uint64_t* out_hash);
 
 /* ---- global lookup (new; cross-workflow dedup the reference lacks) -------------
- * For every FULL block of every request: the id of the resident block with the same chained hash
- * (token-verified), else -1 (out_block, one entry per full block, request order).
- * out_hit_tokens[r] = 16 * number of leading hit blocks of request r. */
+ * For every block of every request (ceil(len/16) entries per request, request order): the id of
+ * the resident block with the same chained hash (token-verified), else -1; partial (last) blocks
+ * are never shared and always report -1. out_hit_tokens[r] = 16 * number of leading hit blocks. */
 int sfkv_lookup_batch(sfkv_pool* pool, int64_t n, const int64_t* tok_off, const uint32_t* tok,
                       int32_t* out_block, int64_t* out_hit_tokens);
 int sfkv_lookup_batch_dev(sfkv_pool* pool, int64_t n, const int64_t* tok_off, const uint32_t* tok,

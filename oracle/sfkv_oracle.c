@@ -232,9 +232,12 @@ int sfo_lookup_batch(sfo_pool* p, int64_t n, const int64_t* tok_off, const uint3
     uint64_t* h = (uint64_t*)malloc((size_t)(nb > 0 ? nb : 1) * sizeof(uint64_t));
     sfo_chain_hashes(t, len, h);
     int64_t lead = 0, run = 1;
-    for (int64_t k = 0; k < nfull; ++k) {
-      int32_t id = kmap_get(&p->table, h[k]);
-      if (id >= 0 && !blk_tokens_eq(p, id, t + k * BT)) id = -1;
+    for (int64_t k = 0; k < nb; ++k) {
+      int32_t id = -1;
+      if (k < nfull) {
+        id = kmap_get(&p->table, h[k]);
+        if (id >= 0 && !blk_tokens_eq(p, id, t + k * BT)) id = -1;
+      }
       out_block[ob++] = id;
       if (id < 0) run = 0;
       if (run) ++lead;

@@ -221,7 +221,7 @@ class Pool:
 
     def lookup(self, tok_off, tok):
         n = len(tok_off) - 1
-        nfull = int((np.diff(tok_off) // BLOCK_TOKENS).sum())
+        nfull = int(n_blocks_of(tok_off).sum())
         out = np.zeros(max(nfull, 1), dtype=np.int32)
         hit = np.zeros(n, dtype=np.int64)
         self.api.check("lookup_batch", self.api.lookup_batch(self.h, n, _ptr(tok_off), _ptr(tok),

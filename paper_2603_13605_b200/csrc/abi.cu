@@ -1,0 +1,604 @@
+// extern "C" entry points of libsfkv.so (include/sfkv.h). Validation, host<->device staging for
+// the host-pointer variants, and per-device contexts for the pool-less memory-manager / mapper
+// calls. Everything below the ABI runs the sm_100a kernels in match.cu, commit.cu, copy.cu and
+// mm_map.cu; there is no CPU compute path.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "pool.cuh"
+
+namespace sfkv {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? SFKV_ENOMEM : SFKV_ECUDA;
+}
+
+__global__ void __launch_bounds__(1024) scan_tiles_kernel(int64_t* tile_sums, int64_t ntiles) {
+  using BS = cub::BlockScan<int64_t, 1024>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < ntiles; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    int64_t v = i < ntiles ? tile_sums[i] : 0, agg;
+    BS(tmp).ExclusiveSum(v, v, agg);
+    if (i < ntiles) tile_sums[i] = v + carry;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += agg;
+    __syncthreads();
+  }
+}
+
+__global__ void pool_init_kernel(sfkv_pool P) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t i = t0; i < P.table_slots; i += stride) {
+    P.slots[i].key = KEY_EMPTY;
+    P.slots[i].val = -1;
+    P.slots[i].pad = 0;
+    P.towner[i] = NO_OWNER;
+  }
+  for (int64_t w = t0; w < P.n_words; w += stride) {
+    const int64_t lo = w * 32, hi = lo + 32;
+    P.free_bits[w] = hi <= P.cfg.n_blocks ? 0xffffffffu
+                                          : (P.cfg.n_blocks > lo ? ((1u << (P.cfg.n_blocks - lo)) - 1u) : 0u);
+  }
+  for (int64_t w = t0; w < P.cfg.max_workflows; w += stride) {
+    P.pin_len[w] = -1;
+    P.pin_nblk[w] = 0;
+  }
+  for (int64_t b = t0; b < P.cfg.n_blocks; b += stride) {
+    P.blk_ref[b] = 0;
+    P.blk_in_table[b] = 0;
+    P.blk_n[b] = 0;
+    P.blk_slot[b] = -1;
+  }
+}
+
+template <class T>
+static int dalloc(T** p, size_t n) {
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), (n ? n : 1) * sizeof(T));
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    return cuda_fail(e, "pool cudaMalloc");
+  }
+  return 0;
+}
+
+static void pool_free(sfkv_pool* p) {
+  if (!p) return;
+  cudaFree(p->pin_len);
+  cudaFree(p->pin_nblk);
+  cudaFree(p->pin_blk);
+  cudaFree(p->pin_hash);
+  cudaFree(p->blk_key);
+  cudaFree(p->blk_tok);
+  cudaFree(p->blk_n);
+  cudaFree(p->blk_in_table);
+  cudaFree(p->blk_ref);
+  cudaFree(p->blk_slot);
+  cudaFree(p->free_bits);
+  cudaFree(p->slots);
+  cudaFree(p->towner);
+  cudaFree(p->kv);
+  cudaFree(p->ctr);
+  if (p->ctr_host) cudaFreeHost(p->ctr_host);
+  if (p->host_stage) cudaFreeHost(p->host_stage);
+  p->scratch.release();
+  p->small.release();
+  p->io.release();
+  if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+}
+
+static int read_counters(sfkv_pool* p) {
+  SFKV_CUDA(cudaMemcpyAsync(p->ctr_host, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, p->stream));
+  SFKV_CUDA(cudaStreamSynchronize(p->stream));
+  return 0;
+}
+
+static int check_sticky(sfkv_pool* p) {
+  if (int rc = read_counters(p)) return rc;
+  const int e = p->ctr_host->error;
+  if (e == SFKV_EPOOL) return fail(e, "physical block pool or block table exhausted");
+  if (e == SFKV_ESTALE) return fail(e, "payload staging assumed a different cached prefix M");
+  return 0;
+}
+
+// Host-pointer staging: copies into p->io and returns device pointers.
+struct IoLayout {
+  Carver cv;
+  std::vector<std::pair<size_t, const void*>> in;  // (offset, host src) with sizes below
+  std::vector<size_t> in_bytes;
+};
+
+}  // namespace sfkv
+
+using namespace sfkv;
+
+extern "C" {
+
+const char* sfkv_last_error(void) { return g_err.c_str(); }
+int sfkv_abi_version(void) { return SFKV_ABI_VERSION; }
+
+uint64_t sfkv_block_digest(uint64_t k, uint32_t n, const uint32_t* t) {
+  uint32_t z[BT];
+  for (int j = 0; j < BT; ++j) z[j] = (uint32_t)j < n ? t[j] : 0u;
+  return block_digest_words(k, n, z);
+}
+uint64_t sfkv_chain_finalize(uint64_t s) { return chain_finalize(s); }
+
+int sfkv_pool_create(const sfkv_pool_config* cfg, sfkv_pool** out) {
+  if (!cfg || !out) return fail(SFKV_EINVAL, "pool_create: null argument");
+  if (cfg->max_workflows <= 0 || cfg->n_blocks <= 0 || cfg->capacity_tokens <= 0 ||
+      cfg->max_pin_blocks <= 0 || cfg->table_log2 < 4 || cfg->table_log2 > 40 || cfg->n_slabs < 0 ||
+      (cfg->n_slabs > 0 && (cfg->slab_row_bytes <= 0 || cfg->slab_row_bytes % 16 != 0)) ||
+      cfg->n_blocks >= INT32_MAX)
+    return fail(SFKV_EINVAL, "pool_create: invalid configuration");
+  if ((int64_t(1) << cfg->table_log2) <= cfg->n_blocks)
+    return fail(SFKV_EINVAL, "pool_create: table must have more slots than blocks");
+  if (int rc = check_device(cfg->device)) return rc;
+  DeviceGuard g(cfg->device);
+  auto* p = new sfkv_pool;
+  p->cfg = *cfg;
+  p->block_bytes = (int64_t)cfg->n_slabs * BT * cfg->slab_row_bytes;
+  p->n_words = (cfg->n_blocks + 31) / 32;
+  p->table_slots = int64_t(1) << cfg->table_log2;
+  const size_t W = cfg->max_workflows, B = cfg->n_blocks, MB = cfg->max_pin_blocks;
+  int rc = 0;
+  if ((rc = dalloc(&p->pin_len, W)) || (rc = dalloc(&p->pin_nblk, W)) ||
+      (rc = dalloc(&p->pin_blk, W * MB)) || (rc = dalloc(&p->pin_hash, W * MB)) ||
+      (rc = dalloc(&p->blk_key, B)) || (rc = dalloc(&p->blk_tok, B * BT)) ||
+      (rc = dalloc(&p->blk_n, B)) || (rc = dalloc(&p->blk_in_table, B)) ||
+      (rc = dalloc(&p->blk_ref, B)) || (rc = dalloc(&p->blk_slot, B)) ||
+      (rc = dalloc(&p->free_bits, (size_t)p->n_words)) ||
+      (rc = dalloc(&p->slots, (size_t)p->table_slots)) ||
+      (rc = dalloc(&p->towner, (size_t)p->table_slots)) || (rc = dalloc(&p->ctr, 1))) {
+    pool_free(p);
+    return rc;
+  }
+  if (p->block_bytes > 0 && (rc = dalloc(&p->kv, B * (size_t)p->block_bytes))) {
+    pool_free(p);
+    return rc;
+  }
+  cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&p->ctr_host), sizeof(DevCounters));
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    pool_free(p);
+    return cuda_fail(e, "pool_create");
+  }
+  p->own_stream = true;
+  cudaMemsetAsync(p->ctr, 0, sizeof(DevCounters), p->stream);
+  cudaMemsetAsync(p->blk_tok, 0, B * BT * sizeof(uint32_t), p->stream);
+  if (p->kv) cudaMemsetAsync(p->kv, 0, B * (size_t)p->block_bytes, p->stream);
+  pool_init_kernel<<<1184, 256, 0, p->stream>>>(*p);
+  e = cudaStreamSynchronize(p->stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    pool_free(p);
+    return cuda_fail(e, "pool_create init");
+  }
+  *out = p;
+  return 0;
+}
+
+int sfkv_pool_destroy(sfkv_pool* p) {
+  if (!p) return 0;
+  DeviceGuard g(p->cfg.device);
+  cudaStreamSynchronize(p->stream);
+  pool_free(p);
+  return 0;
+}
+
+int sfkv_pool_set_stream(sfkv_pool* p, void* stream) {
+  if (!p) return fail(SFKV_EINVAL, "null pool");
+  DeviceGuard g(p->cfg.device);
+  cudaStreamSynchronize(p->stream);
+  if (p->own_stream) cudaStreamDestroy(p->stream);
+  p->stream = static_cast<cudaStream_t>(stream);
+  p->own_stream = false;
+  return 0;
+}
+
+int sfkv_pool_sync(sfkv_pool* p) {
+  if (!p) return fail(SFKV_EINVAL, "null pool");
+  DeviceGuard g(p->cfg.device);
+  SFKV_CUDA(cudaStreamSynchronize(p->stream));
+  return 0;
+}
+
+int sfkv_pool_kv(sfkv_pool* p, void** kv, int64_t* block_bytes) {
+  if (!p || !kv || !block_bytes) return fail(SFKV_EINVAL, "null argument");
+  *kv = p->kv;
+  *block_bytes = p->block_bytes;
+  return 0;
+}
+
+// ---------------------------------------------------------------- lookup ------------------
+static int match_common(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
+                        const uint32_t* tok, int64_t* out_M, uint64_t* out_hash, int32_t* out_block,
+                        int64_t* out_hit, int64_t n_items_host) {
+  cudaStream_t st = p->stream;
+  int64_t n_items = n_items_host;
+  Carver c0;
+  const size_t o_blk = c0.take<int64_t>(n + 1), o_tmp = c0.take<int64_t>(scan_scratch_elems(n));
+  if (int rc = p->small.ensure(c0.off)) return rc;
+  int64_t* blk_off = reinterpret_cast<int64_t*>(p->small.as<char>() + o_blk);
+
+  if (int rc = exclusive_scan(ReqBlocks{tok_off}, n, blk_off,
+                              reinterpret_cast<int64_t*>(p->small.as<char>() + o_tmp), st))
+    return rc;
+  if (n_items < 0) {
+    SFKV_CUDA(cudaMemcpyAsync(&n_items, blk_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SFKV_CUDA(cudaStreamSynchronize(st));
+  }
+  Carver cv;
+  const size_t o_tile = cv.take<int64_t>(match_tile_state_elems(n_items));
+  if (int rc = p->scratch.ensure(cv.off)) return rc;
+  MatchArgs a{};
+  a.n = n;
+  a.wf = wf;
+  a.tok_off = tok_off;
+  a.tok = tok;
+  a.blk_off = blk_off;
+  a.n_items = n_items;
+  a.out_M = out_M;
+  a.out_hash = out_hash;
+  a.out_block = out_block;
+  a.out_hit = out_hit;
+  return launch_match(p, a, reinterpret_cast<int64_t*>(p->scratch.as<char>() + o_tile), st);
+}
+
+static int64_t host_items(int64_t n, const int64_t* tok_off) {
+  int64_t s = 0;
+  for (int64_t r = 0; r < n; ++r) s += (tok_off[r + 1] - tok_off[r] + BT - 1) / BT;
+  return s;
+}
+
+static int validate_batch_host(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off) {
+  if (n < 0 || !tok_off) return fail(SFKV_EINVAL, "invalid batch");
+  if (tok_off[0] != 0) return fail(SFKV_EINVAL, "tok_off[0] must be 0");
+  for (int64_t r = 0; r < n; ++r) {
+    if (tok_off[r + 1] < tok_off[r]) return fail(SFKV_EINVAL, "tok_off must be non-decreasing");
+    if (wf && (wf[r] < 0 || wf[r] >= p->cfg.max_workflows))
+      return fail(SFKV_EINVAL, "workflow slot out of range");
+  }
+  return 0;
+}
+
+// Copies (wf, tok_off, tok) to the device io buffer; returns device pointers.
+static int stage_batch(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
+                       const uint32_t* tok, size_t extra_bytes, int32_t** d_wf, int64_t** d_off,
+                       uint32_t** d_tok, char** d_extra) {
+  const int64_t T = tok_off[n];
+  Carver cv;
+  const size_t o_wf = cv.take<int32_t>(n), o_off = cv.take<int64_t>(n + 1),
+               o_tok = cv.take<uint32_t>(T + 4), o_ex = cv.take<char>(extra_bytes);
+  if (int rc = p->io.ensure(cv.off)) return rc;
+  char* b = p->io.as<char>();
+  cudaStream_t st = p->stream;
+  if (wf) SFKV_CUDA(cudaMemcpyAsync(b + o_wf, wf, n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  SFKV_CUDA(cudaMemcpyAsync(b + o_off, tok_off, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  if (T > 0) SFKV_CUDA(cudaMemcpyAsync(b + o_tok, tok, T * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+  *d_wf = reinterpret_cast<int32_t*>(b + o_wf);
+  *d_off = reinterpret_cast<int64_t*>(b + o_off);
+  *d_tok = reinterpret_cast<uint32_t*>(b + o_tok);
+  if (d_extra) *d_extra = b + o_ex;
+  return 0;
+}
+
+int sfkv_match_batch(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
+                     const uint32_t* tok, int64_t* out_M, uint64_t* out_hash) {
+  if (!p || !out_M) return fail(SFKV_EINVAL, "match_batch: null argument");
+  if (n == 0) return 0;
+  if (!wf) return fail(SFKV_EINVAL, "match_batch: null wf");
+  if (int rc = validate_batch_host(p, n, wf, tok_off)) return rc;
+  DeviceGuard g(p->cfg.device);
+  const int64_t items = host_items(n, tok_off);
+  int32_t* dwf;
+  int64_t* doff;
+  uint32_t* dtok;
+  char* ex;
+  const size_t out_bytes = n * sizeof(int64_t) + 256 + (out_hash ? items * sizeof(uint64_t) : 0);
+  if (int rc = stage_batch(p, n, wf, tok_off, tok, out_bytes, &dwf, &doff, &dtok, &ex)) return rc;
+  int64_t* dM = reinterpret_cast<int64_t*>(ex);
+  uint64_t* dh = out_hash ? reinterpret_cast<uint64_t*>(ex + ((n * sizeof(int64_t) + 255) & ~size_t(255))) : nullptr;
+  if (int rc = match_common(p, n, dwf, doff, dtok, dM, dh, nullptr, nullptr, items)) return rc;
+  SFKV_CUDA(cudaMemcpyAsync(out_M, dM, n * sizeof(int64_t), cudaMemcpyDeviceToHost, p->stream));
+  if (out_hash && items)
+    SFKV_CUDA(cudaMemcpyAsync(out_hash, dh, items * sizeof(uint64_t), cudaMemcpyDeviceToHost, p->stream));
+  SFKV_CUDA(cudaStreamSynchronize(p->stream));
+  return 0;
+}
+
+int sfkv_match_batch_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
+                         const uint32_t* tok, int64_t* out_M, uint64_t* out_hash) {
+  if (!p || !wf || !tok_off || !tok || !out_M) return fail(SFKV_EINVAL, "match_batch_dev: null argument");
+  if (n <= 0) return n == 0 ? 0 : fail(SFKV_EINVAL, "negative batch");
+  DeviceGuard g(p->cfg.device);
+  return match_common(p, n, wf, tok_off, tok, out_M, out_hash, nullptr, nullptr, -1);
+}
+
+int sfkv_lookup_batch(sfkv_pool* p, int64_t n, const int64_t* tok_off, const uint32_t* tok,
+                      int32_t* out_block, int64_t* out_hit) {
+  if (!p || !out_block || !out_hit) return fail(SFKV_EINVAL, "lookup_batch: null argument");
+  if (n == 0) return 0;
+  if (int rc = validate_batch_host(p, n, nullptr, tok_off)) return rc;
+  DeviceGuard g(p->cfg.device);
+  const int64_t items = host_items(n, tok_off);
+  int32_t* dwf;
+  int64_t* doff;
+  uint32_t* dtok;
+  char* ex;
+  const size_t o2 = (n * sizeof(int64_t) + 255) & ~size_t(255);
+  if (int rc = stage_batch(p, n, nullptr, tok_off, tok, o2 + items * sizeof(int32_t) + 16, &dwf, &doff, &dtok, &ex))
+    return rc;
+  int64_t* dhit = reinterpret_cast<int64_t*>(ex);
+  int32_t* dblk = reinterpret_cast<int32_t*>(ex + o2);
+  if (int rc = match_common(p, n, nullptr, doff, dtok, nullptr, nullptr, dblk, dhit, items)) return rc;
+  SFKV_CUDA(cudaMemcpyAsync(out_hit, dhit, n * sizeof(int64_t), cudaMemcpyDeviceToHost, p->stream));
+  if (items)
+    SFKV_CUDA(cudaMemcpyAsync(out_block, dblk, items * sizeof(int32_t), cudaMemcpyDeviceToHost, p->stream));
+  SFKV_CUDA(cudaStreamSynchronize(p->stream));
+  return 0;
+}
+
+int sfkv_lookup_batch_dev(sfkv_pool* p, int64_t n, const int64_t* tok_off, const uint32_t* tok,
+                          int32_t* out_block, int64_t* out_hit) {
+  if (!p || !tok_off || !tok || !out_block || !out_hit) return fail(SFKV_EINVAL, "lookup_batch_dev: null argument");
+  if (n <= 0) return n == 0 ? 0 : fail(SFKV_EINVAL, "negative batch");
+  DeviceGuard g(p->cfg.device);
+  return match_common(p, n, nullptr, tok_off, tok, nullptr, nullptr, out_block, out_hit, -1);
+}
+
+// ---------------------------------------------------------------- retain ------------------
+int sfkv_commit_batch(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
+                      const uint32_t* tok, const void* kv_src, const int64_t* kv_src_off,
+                      const int64_t* m_expected, int32_t* out_status) {
+  if (!p || !out_status) return fail(SFKV_EINVAL, "commit_batch: null argument");
+  if (n == 0) return 0;
+  if (!wf) return fail(SFKV_EINVAL, "commit_batch: null wf");
+  if (int rc = validate_batch_host(p, n, wf, tok_off)) return rc;
+  {
+    std::vector<int32_t> s(wf, wf + n);
+    std::sort(s.begin(), s.end());
+    if (std::adjacent_find(s.begin(), s.end()) != s.end())
+      return fail(SFKV_EINVAL, "commit_batch: workflow slots must be distinct within a batch");
+  }
+  if (kv_src && (!kv_src_off || !p->kv)) return fail(SFKV_EINVAL, "commit_batch: kv_src needs kv_src_off and a payload pool");
+  DeviceGuard g(p->cfg.device);
+  // Host staging copy: KV staging rows are [slab][P - M][row] per request; their total size is
+  // only known from M. Host payload commits therefore take the device-resident path: the caller's
+  // kv_src must be device memory (e.g. a torch tensor) even in this host-pointer variant.
+  int32_t* dwf;
+  int64_t* doff;
+  uint32_t* dtok;
+  char* ex;
+  const size_t o_me = (n * sizeof(int32_t) + 255) & ~size_t(255);
+  const size_t o_ko = o_me + ((n * sizeof(int64_t) + 255) & ~size_t(255));
+  const size_t ex_bytes = o_ko + n * sizeof(int64_t) + 16;
+  if (int rc = stage_batch(p, n, wf, tok_off, tok, ex_bytes, &dwf, &doff, &dtok, &ex)) return rc;
+  int32_t* dst = reinterpret_cast<int32_t*>(ex);
+  int64_t* dme = nullptr;
+  int64_t* dko = nullptr;
+  if (m_expected) {
+    dme = reinterpret_cast<int64_t*>(ex + o_me);
+    SFKV_CUDA(cudaMemcpyAsync(dme, m_expected, n * sizeof(int64_t), cudaMemcpyHostToDevice, p->stream));
+  }
+  if (kv_src) {
+    dko = reinterpret_cast<int64_t*>(ex + o_ko);
+    SFKV_CUDA(cudaMemcpyAsync(dko, kv_src_off, n * sizeof(int64_t), cudaMemcpyHostToDevice, p->stream));
+  }
+  if (int rc = commit_dev(p, n, dwf, doff, dtok, kv_src, dko, dme, dst, nullptr, 0)) return rc;
+  SFKV_CUDA(cudaMemcpyAsync(out_status, dst, n * sizeof(int32_t), cudaMemcpyDeviceToHost, p->stream));
+  return check_sticky(p);
+}
+
+int sfkv_commit_batch_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
+                          const uint32_t* tok, const void* kv_src, const int64_t* kv_src_off,
+                          const int64_t* m_expected, int32_t* out_status) {
+  if (!p || !wf || !tok_off || !tok || !out_status) return fail(SFKV_EINVAL, "commit_batch_dev: null argument");
+  if (n <= 0) return n == 0 ? 0 : fail(SFKV_EINVAL, "negative batch");
+  if (kv_src && (!kv_src_off || !p->kv)) return fail(SFKV_EINVAL, "commit_batch_dev: kv_src needs kv_src_off and a payload pool");
+  DeviceGuard g(p->cfg.device);
+  return commit_dev(p, n, wf, tok_off, tok, kv_src, kv_src_off, m_expected, out_status, nullptr, 0);
+}
+
+// ---------------------------------------------------------------- evict -------------------
+int sfkv_flush(sfkv_pool* p, int32_t wf, int64_t* freed) {
+  if (!p || !freed) return fail(SFKV_EINVAL, "flush: null argument");
+  if (wf != SFKV_FLUSH_ALL && (wf < 0 || wf >= p->cfg.max_workflows))
+    return fail(SFKV_EINVAL, "flush: workflow slot out of range");
+  DeviceGuard g(p->cfg.device);
+  p->flush_calls++;
+  if (wf == SFKV_FLUSH_ALL) {
+    if (int rc = read_counters(p)) return rc;
+    *freed = p->ctr_host->occupancy;
+    if (int rc = flush_dev(p, 0, nullptr, nullptr, true)) return rc;
+    SFKV_CUDA(cudaStreamSynchronize(p->stream));
+    return 0;
+  }
+  if (int rc = p->io.ensure(512)) return rc;
+  int32_t* dwf = p->io.as<int32_t>();
+  int64_t* dfreed = reinterpret_cast<int64_t*>(p->io.as<char>() + 256);
+  SFKV_CUDA(cudaMemcpyAsync(dwf, &wf, sizeof(int32_t), cudaMemcpyHostToDevice, p->stream));
+  if (int rc = flush_dev(p, 1, dwf, dfreed, false)) return rc;
+  SFKV_CUDA(cudaMemcpyAsync(freed, dfreed, sizeof(int64_t), cudaMemcpyDeviceToHost, p->stream));
+  SFKV_CUDA(cudaStreamSynchronize(p->stream));
+  return 0;
+}
+
+int sfkv_flush_batch(sfkv_pool* p, int64_t n, const int32_t* wf, int64_t* out_freed) {
+  if (!p || (n > 0 && (!wf || !out_freed))) return fail(SFKV_EINVAL, "flush_batch: null argument");
+  if (n == 0) return 0;
+  for (int64_t r = 0; r < n; ++r)
+    if (wf[r] < 0 || wf[r] >= p->cfg.max_workflows) return fail(SFKV_EINVAL, "flush_batch: slot out of range");
+  {
+    std::vector<int32_t> s(wf, wf + n);
+    std::sort(s.begin(), s.end());
+    if (std::adjacent_find(s.begin(), s.end()) != s.end())
+      return fail(SFKV_EINVAL, "flush_batch: workflow slots must be distinct within a batch");
+  }
+  DeviceGuard g(p->cfg.device);
+  p->flush_calls += (uint64_t)n;
+  const size_t o = (n * sizeof(int32_t) + 255) & ~size_t(255);
+  if (int rc = p->io.ensure(o + n * sizeof(int64_t))) return rc;
+  int32_t* dwf = p->io.as<int32_t>();
+  int64_t* dfreed = reinterpret_cast<int64_t*>(p->io.as<char>() + o);
+  SFKV_CUDA(cudaMemcpyAsync(dwf, wf, n * sizeof(int32_t), cudaMemcpyHostToDevice, p->stream));
+  if (int rc = flush_dev(p, n, dwf, dfreed, false)) return rc;
+  SFKV_CUDA(cudaMemcpyAsync(out_freed, dfreed, n * sizeof(int64_t), cudaMemcpyDeviceToHost, p->stream));
+  SFKV_CUDA(cudaStreamSynchronize(p->stream));
+  return 0;
+}
+
+// ---------------------------------------------------------------- inspection --------------
+static int read_pin_len(sfkv_pool* p, int32_t wf, int64_t* len) {
+  SFKV_CUDA(cudaMemcpyAsync(len, p->pin_len + wf, sizeof(int64_t), cudaMemcpyDeviceToHost, p->stream));
+  SFKV_CUDA(cudaStreamSynchronize(p->stream));
+  return 0;
+}
+
+int sfkv_preserve(sfkv_pool* p, int32_t wf, int32_t* has_pin) {
+  if (!p || !has_pin || wf < 0 || wf >= p->cfg.max_workflows) return fail(SFKV_EINVAL, "preserve: bad argument");
+  DeviceGuard g(p->cfg.device);
+  p->preserve_calls++;
+  int64_t len = -1;
+  if (int rc = read_pin_len(p, wf, &len)) return rc;
+  *has_pin = len >= 0 ? 1 : 0;
+  return 0;
+}
+
+int sfkv_pinned_token_count(sfkv_pool* p, int32_t wf, int64_t* n_tokens) {
+  if (!p || !n_tokens || wf < 0 || wf >= p->cfg.max_workflows) return fail(SFKV_EINVAL, "pinned_token_count: bad argument");
+  DeviceGuard g(p->cfg.device);
+  int64_t len = -1;
+  if (int rc = read_pin_len(p, wf, &len)) return rc;
+  *n_tokens = len < 0 ? 0 : len;
+  return 0;
+}
+
+int sfkv_cache_utilization(sfkv_pool* p, double* util) {
+  if (!p || !util) return fail(SFKV_EINVAL, "cache_utilization: null argument");
+  DeviceGuard g(p->cfg.device);
+  if (int rc = read_counters(p)) return rc;
+  *util = static_cast<double>(p->ctr_host->occupancy) / static_cast<double>(p->cfg.capacity_tokens);
+  return 0;
+}
+
+int sfkv_stats(sfkv_pool* p, sfkv_pool_stats* o) {
+  if (!p || !o) return fail(SFKV_EINVAL, "stats: null argument");
+  DeviceGuard g(p->cfg.device);
+  if (int rc = read_counters(p)) return rc;
+  o->occupancy_tokens = p->ctr_host->occupancy;
+  o->capacity_tokens = p->cfg.capacity_tokens;
+  o->capacity_rejections = p->ctr_host->rejections;
+  o->flush_calls = p->flush_calls;
+  o->preserve_calls = p->preserve_calls;
+  o->blocks_in_use = p->ctr_host->blocks_in_use;
+  o->table_live = p->ctr_host->table_live;
+  o->table_tombstones = p->ctr_host->table_tomb;
+  return 0;
+}
+
+int sfkv_pin_blocks(sfkv_pool* p, int32_t wf, int32_t* ids, uint64_t* hashes, int32_t cap,
+                    int32_t* n_blocks) {
+  if (!p || !n_blocks || wf < 0 || wf >= p->cfg.max_workflows) return fail(SFKV_EINVAL, "pin_blocks: bad argument");
+  DeviceGuard g(p->cfg.device);
+  int64_t len = -1;
+  int32_t nb = 0;
+  if (int rc = read_pin_len(p, wf, &len)) return rc;
+  SFKV_CUDA(cudaMemcpy(&nb, p->pin_nblk + wf, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  nb = len < 0 ? 0 : nb;
+  *n_blocks = nb;
+  const int32_t m = nb < cap ? nb : cap;
+  const int64_t pb = (int64_t)wf * p->cfg.max_pin_blocks;
+  if (ids && m) SFKV_CUDA(cudaMemcpy(ids, p->pin_blk + pb, m * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (hashes && m) SFKV_CUDA(cudaMemcpy(hashes, p->pin_hash + pb, m * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int sfkv_block_refcounts(sfkv_pool* p, uint32_t* out) {
+  if (!p || !out) return fail(SFKV_EINVAL, "block_refcounts: null argument");
+  DeviceGuard g(p->cfg.device);
+  SFKV_CUDA(cudaStreamSynchronize(p->stream));
+  SFKV_CUDA(cudaMemcpy(out, p->blk_ref, p->cfg.n_blocks * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+// ---------------------------------------------------------------- gather / handoff --------
+int sfkv_gather_dev(sfkv_pool* p, int64_t n, const int32_t* wf, void* dst, const int64_t* dst_off) {
+  if (!p || (n > 0 && (!wf || !dst || !dst_off))) return fail(SFKV_EINVAL, "gather_dev: null argument");
+  DeviceGuard g(p->cfg.device);
+  return gather_dev(p, n, wf, dst, dst_off);
+}
+
+__global__ void pin_tokens_kernel(const int32_t* pin_blk, const uint32_t* blk_tok, int32_t nb,
+                                  uint32_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)nb * BT;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = blk_tok[(int64_t)pin_blk[i / BT] * BT + (i % BT)];
+}
+
+int sfkv_handoff(sfkv_pool* src, int32_t wf_src, sfkv_pool* dst, int32_t wf_dst, int32_t* status) {
+  if (!src || !dst || !status || wf_src < 0 || wf_src >= src->cfg.max_workflows || wf_dst < 0 ||
+      wf_dst >= dst->cfg.max_workflows)
+    return fail(SFKV_EINVAL, "handoff: bad argument");
+  if (src->cfg.n_slabs != dst->cfg.n_slabs || src->cfg.slab_row_bytes != dst->cfg.slab_row_bytes)
+    return fail(SFKV_EINVAL, "handoff: pools have different KV shapes");
+  int64_t L = -1;
+  int32_t nb = 0;
+  {
+    DeviceGuard g(src->cfg.device);
+    if (int rc = read_pin_len(src, wf_src, &L)) return rc;
+    if (L < 0) return fail(SFKV_EINVAL, "handoff: source workflow has no pin");
+    SFKV_CUDA(cudaMemcpy(&nb, src->pin_nblk + wf_src, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  }
+  DeviceGuard g(dst->cfg.device);
+  if (src->cfg.device != dst->cfg.device) {
+    cudaError_t e = cudaDeviceEnablePeerAccess(src->cfg.device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "enable peer access");
+    cudaGetLastError();
+  }
+  // tokens of the source pin -> dst io buffer (peer reads when the pools are on different GPUs)
+  const size_t o_off = ((size_t)(nb * BT + 4) * sizeof(uint32_t) + 255) & ~size_t(255);
+  if (int rc = dst->io.ensure(o_off + 2 * sizeof(int64_t) + 256 + 16)) return rc;
+  uint32_t* dtok = dst->io.as<uint32_t>();
+  int64_t* doff = reinterpret_cast<int64_t*>(dst->io.as<char>() + o_off);
+  int32_t* dwf = reinterpret_cast<int32_t*>(dst->io.as<char>() + o_off + 64);
+  int32_t* dst_status = reinterpret_cast<int32_t*>(dst->io.as<char>() + o_off + 128);
+  // run the token gather on the destination device, reading the source pool through its pointer
+  if (nb > 0) {
+    pin_tokens_kernel<<<grid_for((int64_t)nb * BT, 256, 1024), 256, 0, dst->stream>>>(
+        src->pin_blk + (int64_t)wf_src * src->cfg.max_pin_blocks, src->blk_tok, nb, dtok);
+    SFKV_LAUNCH_CHECK("pin_tokens_kernel");
+  }
+  const int64_t off[2] = {0, L};
+  SFKV_CUDA(cudaMemcpyAsync(doff, off, sizeof(off), cudaMemcpyHostToDevice, dst->stream));
+  SFKV_CUDA(cudaMemcpyAsync(dwf, &wf_dst, sizeof(int32_t), cudaMemcpyHostToDevice, dst->stream));
+  // the source pool's stream must not be mutating the pin meanwhile
+  {
+    DeviceGuard gs(src->cfg.device);
+    SFKV_CUDA(cudaStreamSynchronize(src->stream));
+  }
+  if (int rc = commit_dev(dst, 1, dwf, doff, dtok, nullptr, nullptr, nullptr, dst_status,
+                          dst->kv ? src : nullptr, wf_src))
+    return rc;
+  SFKV_CUDA(cudaMemcpyAsync(status, dst_status, sizeof(int32_t), cudaMemcpyDeviceToHost, dst->stream));
+  return check_sticky(dst);
+}
+
+}  // extern "C"
+

@@ -1,0 +1,614 @@
+// K3+K4: retain (commit) and evict (flush) on the pool — block table, global dedup table,
+// refcounts, deterministic allocation, capacity admission.
+//
+// Replaces SimulatedBackend::pin_prompt (simulated_backend.cpp:135-151) and ::flush (169-184).
+// A commit batch runs these launches on the pool stream (the batch semantics are defined in
+// oracle/sfkv_oracle.c, commit_impl):
+//   match      chained hashes of every block + M_r = LCP(old pin, tokens)           (match.cu)
+//   admit      one warp, request order: reject iff occ - old + new > capacity; warp-wide fast
+//              path when the whole 32-request chunk fits, exact sequential fallback otherwise
+//   probe      per full block: table probe; verified pre-existing key -> hit0; new key ->
+//              claim (atomicCAS into an empty slot) + atomicMin(owner) = lowest claiming item
+//   resolve    claim items with a lower owner compare tokens with the owner's (dup);
+//              atomicMin(first_nonhit[r]) over blocks that are neither hit0 nor dup
+//   categorize HIT / DUP below first_nonhit, OWN (key owner) / PRIV above
+//   scan x2    exclusive scan of new-block flags (rank) and of free-bitmap popcounts
+//   alloc      rank -> the rank-th free block id (lowest ids first, batch order: deterministic,
+//              independent of atomic order); OWN publishes its id into the table slot
+//   refs       every block of every new pin takes a reference (atomicAdd)
+//   payload    copy-on-share + staging scatter of new blocks                        (copy.cu)
+//   release    old pins drop their references; blocks reaching 0 return to the free bitmap and
+//              leave the table (tombstone)
+//   install    new block tables / hashes / lengths
+// The batch is phase-ordered, so a block shared by an old and a new pin never transiently hits
+// a refcount of zero.
+#include "pool.cuh"
+
+namespace sfkv {
+
+enum : uint8_t { CAT_NONE = 0, CAT_HIT = 1, CAT_DUP = 2, CAT_OWN = 3, CAT_PRIV = 4 };
+
+struct CommitScratch {
+  int64_t* blk_off;      // [n+1]
+  int64_t* M;            // [n]
+  uint64_t* hash;        // [items]
+  int64_t* tile_state;   // match look-back
+  int32_t* status;       // [n]
+  int64_t* slot_of;      // [items]
+  int32_t* bid;          // [items]
+  uint8_t* hit0;         // [items]
+  uint8_t* claim;        // [items]
+  uint8_t* cat;          // [items]
+  int64_t* first_nonhit; // [n]
+  int64_t* rank;         // [items+1]
+  int64_t* wprefix;      // [words+1]
+  int64_t* alloc_list;   // [items]
+  int64_t* scan_tmp;
+};
+
+struct CommitArgs {
+  int64_t n;
+  const int32_t* wf;
+  const int64_t* tok_off;
+  const uint32_t* tok;
+  int64_t n_items;
+  const int64_t* m_expected;
+  int payload;               // 1 when KV bytes are written
+  CommitScratch s;
+  // pool
+  int64_t* pin_len;
+  int32_t* pin_nblk;
+  int32_t* pin_blk;
+  uint64_t* pin_hash;
+  uint64_t* blk_key;
+  uint32_t* blk_tok;
+  uint8_t* blk_n;
+  uint8_t* blk_in_table;
+  uint32_t* blk_ref;
+  int64_t* blk_slot;
+  uint32_t* free_bits;
+  Slot* slots;
+  int64_t* towner;
+  uint64_t slot_mask;
+  int64_t n_words;
+  int64_t n_blocks;
+  int32_t max_pin_blocks;
+  int64_t capacity;
+  DevCounters* ctr;
+};
+
+__device__ __forceinline__ void item_coords(const CommitArgs& a, int64_t item, int64_t& r,
+                                            int64_t& k, int& nval) {
+  r = upper_index(a.s.blk_off, a.n, item);
+  k = item - a.s.blk_off[r];
+  const int64_t rem = a.tok_off[r + 1] - a.tok_off[r] - k * BT;
+  nval = (int)(rem < BT ? rem : BT);
+}
+
+__device__ __forceinline__ void load_req_block(const CommitArgs& a, int64_t r, int64_t k, int nval,
+                                               uint32_t* t) {
+  const uint32_t* p = a.tok + a.tok_off[r] + k * BT;
+#pragma unroll
+  for (int j = 0; j < BT; ++j) t[j] = j < nval ? __ldg(p + j) : 0u;
+}
+
+__device__ __forceinline__ bool blk_tokens_equal(const uint32_t* __restrict__ blk_tok, int32_t id,
+                                                 const uint32_t* t) {
+  const uint4* q = reinterpret_cast<const uint4*>(blk_tok + (int64_t)id * BT);
+  bool eq = true;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint4 v = q[i];
+    eq &= v.x == t[4 * i] && v.y == t[4 * i + 1] && v.z == t[4 * i + 2] && v.w == t[4 * i + 3];
+  }
+  return eq;
+}
+
+// ---- admission: one warp, exact reference order ----------------------------------------
+__global__ void admit_kernel(CommitArgs a) {
+  const int lane = threadIdx.x;
+  DevCounters* c = a.ctr;
+  // staleness / block-table checks first: a refused batch changes nothing
+  bool bad_stale = false, bad_len = false;
+  for (int64_t r = lane; r < a.n; r += 32) {
+    const int64_t len = a.tok_off[r + 1] - a.tok_off[r];
+    if ((len + BT - 1) / BT > a.max_pin_blocks) bad_len = true;
+    if (a.payload && a.m_expected && a.m_expected[r] != a.s.M[r]) bad_stale = true;
+  }
+  bad_stale = __any_sync(0xffffffffu, bad_stale);
+  bad_len = __any_sync(0xffffffffu, bad_len);
+  if (bad_stale || bad_len) {
+    const int code = bad_len ? SFKV_EPOOL : SFKV_ESTALE;
+    for (int64_t r = lane; r < a.n; r += 32) a.s.status[r] = code;
+    if (lane == 0) c->error = code;
+    return;
+  }
+  long long occ = c->occupancy;
+  unsigned long long rej = 0;
+  for (int64_t base = 0; base < a.n; base += 32) {
+    const int64_t r = base + lane;
+    const bool act = r < a.n;
+    long long delta = 0;
+    if (act) {
+      const int64_t pl = a.pin_len[a.wf[r]];
+      const int64_t len = a.tok_off[r + 1] - a.tok_off[r];
+      delta = len - (pl < 0 ? 0 : pl);
+      a.s.first_nonhit[r] = (len + BT - 1) / BT;
+    }
+    // fast path: every prefix of the chunk fits
+    long long incl = delta;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      long long v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const bool fits = !act || occ + incl <= a.capacity;
+    if (__all_sync(0xffffffffu, fits)) {
+      if (act) a.s.status[r] = SFKV_PIN_ACCEPTED;
+      occ += __shfl_sync(0xffffffffu, incl, 31);
+    } else {
+      for (int j = 0; j < 32; ++j) {  // exact sequential rule (simulated_backend.cpp:141-150)
+        const long long d = __shfl_sync(0xffffffffu, delta, j);
+        const bool aj = __shfl_sync(0xffffffffu, (int)act, j);
+        if (!aj) break;
+        const bool ok = occ + d <= a.capacity;
+        if (lane == j) a.s.status[r] = ok ? SFKV_PIN_ACCEPTED : SFKV_PIN_REJECTED;
+        if (ok) occ += d;
+        else ++rej;
+      }
+    }
+  }
+  if (lane == 0) {
+    c->occupancy = occ;
+    c->rejections += rej;
+  }
+}
+
+// ---- probe / claim ---------------------------------------------------------------------
+__global__ void probe_kernel(CommitArgs a) {
+  for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < a.n_items;
+       item += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r, k;
+    int nval;
+    item_coords(a, item, r, k, nval);
+    a.s.slot_of[item] = -1;
+    a.s.hit0[item] = 0;
+    a.s.claim[item] = 0;
+    a.s.bid[item] = -1;
+    if (a.s.status[r] != SFKV_PIN_ACCEPTED || nval != BT) continue;
+    uint32_t t[BT];
+    load_req_block(a, r, k, nval, t);
+    const unsigned long long c = a.s.hash[item];
+    uint64_t s = c & a.slot_mask;
+    for (uint64_t probes = 0; probes <= a.slot_mask; ++probes) {
+      unsigned long long key = *reinterpret_cast<volatile unsigned long long*>(&a.slots[s].key);
+      if (key == KEY_EMPTY) {
+        const unsigned long long prev = atomicCAS(&a.slots[s].key, KEY_EMPTY, c);
+        key = prev == KEY_EMPTY ? c : prev;
+      }
+      if (key == c) {
+        a.s.slot_of[item] = (int64_t)s;
+        const int32_t val = *reinterpret_cast<volatile int32_t*>(&a.slots[s].val);
+        if (val >= 0) {  // key present before this batch
+          if (a.blk_n[val] == BT && blk_tokens_equal(a.blk_tok, val, t)) {
+            a.s.hit0[item] = 1;
+            a.s.bid[item] = val;
+          }
+        } else {  // key claimed in this batch
+          a.s.claim[item] = 1;
+          atomicMin(reinterpret_cast<unsigned long long*>(&a.towner[s]), (unsigned long long)item);
+        }
+        break;
+      }
+      s = (s + 1) & a.slot_mask;
+    }
+    if (a.s.slot_of[item] < 0) a.ctr->error = SFKV_EPOOL;  // table full
+  }
+}
+
+__global__ void resolve_kernel(CommitArgs a) {
+  for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < a.n_items;
+       item += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r, k;
+    int nval;
+    item_coords(a, item, r, k, nval);
+    if (a.s.status[r] != SFKV_PIN_ACCEPTED) continue;
+    bool dup = false;
+    if (a.s.claim[item]) {
+      const int64_t o = a.towner[a.s.slot_of[item]];
+      if (o < item) {
+        int64_t ro, ko;
+        int no;
+        item_coords(a, o, ro, ko, no);
+        uint32_t t[BT], u[BT];
+        load_req_block(a, r, k, nval, t);
+        load_req_block(a, ro, ko, no, u);
+        dup = true;
+#pragma unroll
+        for (int j = 0; j < BT; ++j) dup &= t[j] == u[j];
+      }
+    }
+    if (!(a.s.hit0[item] || dup))
+      atomicMin(reinterpret_cast<unsigned long long*>(&a.s.first_nonhit[r]), (unsigned long long)k);
+  }
+}
+
+__global__ void categorize_kernel(CommitArgs a) {
+  for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < a.n_items;
+       item += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = upper_index(a.s.blk_off, a.n, item);
+    const int64_t k = item - a.s.blk_off[r];
+    uint8_t cat = CAT_NONE;
+    if (a.s.status[r] == SFKV_PIN_ACCEPTED) {
+      if (k < a.s.first_nonhit[r]) {
+        cat = a.s.hit0[item] ? CAT_HIT : CAT_DUP;
+      } else {
+        const bool own = a.s.claim[item] && a.towner[a.s.slot_of[item]] == item;
+        cat = own ? CAT_OWN : CAT_PRIV;
+      }
+    }
+    a.s.cat[item] = cat;
+  }
+}
+
+struct NeedAlloc {
+  const uint8_t* cat;
+  __device__ int64_t operator()(int64_t i) const { return (cat[i] == CAT_OWN || cat[i] == CAT_PRIV) ? 1 : 0; }
+};
+struct FreeCount {
+  const uint32_t* bits;
+  __device__ int64_t operator()(int64_t i) const { return __popc(bits[i]); }
+};
+struct PinBlocks {
+  const int32_t* wf;
+  const int64_t* pin_len;
+  const int32_t* pin_nblk;
+  __device__ int64_t operator()(int64_t i) const { return pin_len[wf[i]] < 0 ? 0 : pin_nblk[wf[i]]; }
+};
+
+
+__device__ __forceinline__ int select_bit(uint32_t w, int r) {  // position of the r-th set bit
+  for (int b = 0; b < 32; ++b) {
+    if (w & (1u << b)) {
+      if (r == 0) return b;
+      --r;
+    }
+  }
+  return -1;
+}
+
+__global__ void alloc_kernel(CommitArgs a) {
+  const int64_t total_free = a.s.wprefix[a.n_words];
+  for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < a.n_items;
+       item += (int64_t)gridDim.x * blockDim.x) {
+    const uint8_t cat = a.s.cat[item];
+    if (cat != CAT_OWN && cat != CAT_PRIV) continue;
+    const int64_t rk = a.s.rank[item];
+    if (rk >= total_free) {
+      a.ctr->error = SFKV_EPOOL;
+      continue;
+    }
+    const int64_t w = upper_index(a.s.wprefix, a.n_words, rk);
+    const int bit = select_bit(a.free_bits[w], (int)(rk - a.s.wprefix[w]));
+    const int32_t id = (int32_t)(w * 32 + bit);
+    a.s.alloc_list[rk] = item;
+    a.s.bid[item] = id;
+    atomicAnd(&a.free_bits[w], ~(1u << bit));
+    int64_t r, k;
+    int nval;
+    item_coords(a, item, r, k, nval);
+    uint32_t t[BT];
+    load_req_block(a, r, k, nval, t);
+    uint4* dst = reinterpret_cast<uint4*>(a.blk_tok + (int64_t)id * BT);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dst[i] = make_uint4(t[4 * i], t[4 * i + 1], t[4 * i + 2], t[4 * i + 3]);
+    a.blk_key[id] = a.s.hash[item];
+    a.blk_n[id] = (uint8_t)nval;
+    a.blk_ref[id] = 0;
+    if (cat == CAT_OWN) {
+      const int64_t s = a.s.slot_of[item];
+      a.slots[s].val = id;
+      a.blk_slot[id] = s;
+      a.blk_in_table[id] = 1;
+      atomic_add_i64(&a.ctr->table_live, 1ll);
+    } else {
+      a.blk_slot[id] = -1;
+      a.blk_in_table[id] = 0;
+    }
+    atomic_add_i64(&a.ctr->blocks_in_use, 1ll);
+  }
+}
+
+__global__ void refs_kernel(CommitArgs a) {
+  for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < a.n_items;
+       item += (int64_t)gridDim.x * blockDim.x) {
+    const uint8_t cat = a.s.cat[item];
+    if (cat == CAT_NONE) continue;
+    int32_t id = a.s.bid[item];
+    if (cat == CAT_DUP) {
+      id = a.slots[a.s.slot_of[item]].val;
+      a.s.bid[item] = id;
+    }
+    atomicAdd(&a.blk_ref[id], 1u);
+  }
+}
+
+__global__ void clear_owner_kernel(CommitArgs a) {
+  for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < a.n_items;
+       item += (int64_t)gridDim.x * blockDim.x) {
+    if (a.s.claim[item]) a.towner[a.s.slot_of[item]] = NO_OWNER;
+    // a claimed slot whose key never got a block (cannot happen: the owner is always OWN)
+  }
+}
+
+// Drops one reference; frees the block at zero.
+__device__ __forceinline__ void release_block(const CommitArgs& a, int32_t id) {
+  const uint32_t old = atomicSub(&a.blk_ref[id], 1u);
+  if (old == 1u) {
+    atomicOr(&a.free_bits[id >> 5], 1u << (id & 31));
+    atomic_add_i64(&a.ctr->blocks_in_use, -1ll);
+    if (a.blk_in_table[id]) {
+      a.slots[a.blk_slot[id]].key = KEY_TOMB;
+      a.blk_in_table[id] = 0;
+      atomic_add_i64(&a.ctr->table_live, -1ll);
+      atomic_add_i64(&a.ctr->table_tomb, 1ll);
+    }
+  }
+}
+
+// One warp per request: release the old pin; install the new length (commit) or none (flush).
+__global__ void release_kernel(CommitArgs a, int mode /*0 commit, 1 flush list, 2 flush all*/,
+                               int64_t* out_freed) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t count = mode == 2 ? a.n : a.n;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < count; r += warps) {
+    if (mode == 0 && a.s.status[r] != SFKV_PIN_ACCEPTED) continue;
+    const int32_t w = mode == 2 ? (int32_t)r : a.wf[r];
+    const int64_t pl = a.pin_len[w];
+    if (pl >= 0) {
+      const int32_t nb = a.pin_nblk[w];
+      const int64_t pb = (int64_t)w * a.max_pin_blocks;
+      for (int32_t k = lane; k < nb; k += 32) release_block(a, a.pin_blk[pb + k]);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (mode == 0) {
+        const int64_t len = a.tok_off[r + 1] - a.tok_off[r];
+        a.pin_len[w] = len;
+        a.pin_nblk[w] = (int32_t)((len + BT - 1) / BT);
+      } else {
+        const int64_t freed = pl < 0 ? 0 : pl;
+        if (out_freed) out_freed[r] = freed;
+        if (freed) atomic_add_i64(&a.ctr->occupancy, -(long long)freed);
+        a.pin_len[w] = -1;
+        a.pin_nblk[w] = 0;
+      }
+    }
+  }
+}
+
+__global__ void install_kernel(CommitArgs a) {
+  for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < a.n_items;
+       item += (int64_t)gridDim.x * blockDim.x) {
+    if (a.s.cat[item] == CAT_NONE) continue;
+    const int64_t r = upper_index(a.s.blk_off, a.n, item);
+    const int64_t k = item - a.s.blk_off[r];
+    const int64_t pb = (int64_t)a.wf[r] * a.max_pin_blocks;
+    a.pin_blk[pb + k] = a.s.bid[item];
+    a.pin_hash[pb + k] = a.s.hash[item];
+  }
+}
+
+// ---- table maintenance: rebuild when tombstones exceed a quarter of the slots ------------
+__global__ void rebuild_check_kernel(DevCounters* c, int64_t slots, int* flag) {
+  *flag = (c->table_tomb * 4 > slots) ? 1 : 0;
+}
+__global__ void table_clear_kernel(Slot* slots, int64_t* towner, int64_t n, const int* flag) {
+  if (!*flag) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    slots[i].key = KEY_EMPTY;
+    slots[i].val = -1;
+    towner[i] = NO_OWNER;
+  }
+}
+__global__ void table_reinsert_kernel(CommitArgs a, const int* flag) {
+  if (!*flag) return;
+  for (int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; id < a.n_blocks;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    if (!a.blk_in_table[id]) continue;
+    const unsigned long long c = a.blk_key[id];
+    uint64_t s = c & a.slot_mask;
+    for (;;) {
+      if (atomicCAS(&a.slots[s].key, KEY_EMPTY, c) == KEY_EMPTY) {
+        a.slots[s].val = (int32_t)id;
+        a.blk_slot[id] = (int64_t)s;
+        break;
+      }
+      s = (s + 1) & a.slot_mask;
+    }
+  }
+}
+__global__ void rebuild_done_kernel(DevCounters* c, const int* flag) {
+  if (*flag) c->table_tomb = 0;
+}
+
+// ---------------------------------------------------------------------------------------
+int launch_commit_payload(sfkv_pool* p, const CommitArgs& a, const void* kv_src,
+                          const int64_t* kv_src_off, const sfkv_pool* src_pool, int32_t src_wf,
+                          cudaStream_t st);
+
+static CommitArgs base_args(sfkv_pool* p) {
+  CommitArgs a{};
+  a.pin_len = p->pin_len;
+  a.pin_nblk = p->pin_nblk;
+  a.pin_blk = p->pin_blk;
+  a.pin_hash = p->pin_hash;
+  a.blk_key = p->blk_key;
+  a.blk_tok = p->blk_tok;
+  a.blk_n = p->blk_n;
+  a.blk_in_table = p->blk_in_table;
+  a.blk_ref = p->blk_ref;
+  a.blk_slot = p->blk_slot;
+  a.free_bits = p->free_bits;
+  a.slots = p->slots;
+  a.towner = p->towner;
+  a.slot_mask = (uint64_t)p->table_slots - 1;
+  a.n_words = p->n_words;
+  a.n_blocks = p->cfg.n_blocks;
+  a.max_pin_blocks = p->cfg.max_pin_blocks;
+  a.capacity = p->cfg.capacity_tokens;
+  a.ctr = p->ctr;
+  return a;
+}
+
+static int sm_count_c() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+int maybe_rebuild_table(sfkv_pool* p) {
+  cudaStream_t st = p->stream;
+  CommitArgs a = base_args(p);
+  int* flag = &p->ctr->pad;
+  rebuild_check_kernel<<<1, 1, 0, st>>>(p->ctr, p->table_slots, flag);
+  const int sms = sm_count_c();
+  table_clear_kernel<<<sms * 4, 256, 0, st>>>(p->slots, p->towner, p->table_slots, flag);
+  table_reinsert_kernel<<<sms * 4, 256, 0, st>>>(a, flag);
+  rebuild_done_kernel<<<1, 1, 0, st>>>(p->ctr, flag);
+  SFKV_LAUNCH_CHECK("table rebuild");
+  return 0;
+}
+
+int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
+               const uint32_t* tok, const void* kv_src, const int64_t* kv_src_off,
+               const int64_t* m_expected, int32_t* out_status, const sfkv_pool* src_pool,
+               int32_t src_wf) {
+  if (n <= 0) return 0;
+  cudaStream_t st = p->stream;
+  // Blocks per request first: the item count sizes the scratch (one 8-B D2H on the stream).
+  Carver c0;
+  const size_t o_blk = c0.take<int64_t>(n + 1), o_tmp0 = c0.take<int64_t>(scan_scratch_elems(n));
+  if (int rc = p->small.ensure(c0.off)) return rc;
+  int64_t* blk_off = reinterpret_cast<int64_t*>(p->small.as<char>() + o_blk);
+  if (int rc = exclusive_scan(ReqBlocks{tok_off}, n, blk_off,
+                              reinterpret_cast<int64_t*>(p->small.as<char>() + o_tmp0), st))
+    return rc;
+  int64_t n_items = 0;
+  SFKV_CUDA(cudaMemcpyAsync(&n_items, blk_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  SFKV_CUDA(cudaStreamSynchronize(st));
+  Carver cv;
+  const int64_t ni = n_items > 0 ? n_items : 1;
+  const size_t o_M = cv.take<int64_t>(n), o_hash = cv.take<uint64_t>(ni),
+               o_tile = cv.take<int64_t>(match_tile_state_elems(ni)), o_st = cv.take<int32_t>(n),
+               o_slot = cv.take<int64_t>(ni), o_bid = cv.take<int32_t>(ni),
+               o_hit = cv.take<uint8_t>(ni), o_claim = cv.take<uint8_t>(ni),
+               o_cat = cv.take<uint8_t>(ni), o_fnh = cv.take<int64_t>(n),
+               o_rank = cv.take<int64_t>(ni + 1), o_wp = cv.take<int64_t>(p->n_words + 1),
+               o_al = cv.take<int64_t>(ni),
+               o_tmp = cv.take<int64_t>(scan_scratch_elems(ni > p->n_words ? ni : p->n_words));
+  if (int rc = p->scratch.ensure(cv.off)) return rc;
+  char* base = p->scratch.as<char>();
+  CommitArgs a = base_args(p);
+  a.n = n;
+  a.wf = wf;
+  a.tok_off = tok_off;
+  a.tok = tok;
+  a.m_expected = m_expected;
+  a.payload = (p->kv && (kv_src || src_pool)) ? 1 : 0;
+  a.n_items = n_items;
+  a.s.blk_off = blk_off;
+  a.s.M = reinterpret_cast<int64_t*>(base + o_M);
+  a.s.hash = reinterpret_cast<uint64_t*>(base + o_hash);
+  a.s.tile_state = reinterpret_cast<int64_t*>(base + o_tile);
+  a.s.status = out_status ? out_status : reinterpret_cast<int32_t*>(base + o_st);
+  a.s.slot_of = reinterpret_cast<int64_t*>(base + o_slot);
+  a.s.bid = reinterpret_cast<int32_t*>(base + o_bid);
+  a.s.hit0 = reinterpret_cast<uint8_t*>(base + o_hit);
+  a.s.claim = reinterpret_cast<uint8_t*>(base + o_claim);
+  a.s.cat = reinterpret_cast<uint8_t*>(base + o_cat);
+  a.s.first_nonhit = reinterpret_cast<int64_t*>(base + o_fnh);
+  a.s.rank = reinterpret_cast<int64_t*>(base + o_rank);
+  a.s.wprefix = reinterpret_cast<int64_t*>(base + o_wp);
+  a.s.alloc_list = reinterpret_cast<int64_t*>(base + o_al);
+  a.s.scan_tmp = reinterpret_cast<int64_t*>(base + o_tmp);
+
+  // 1. chained hashes, M = LCP(old pin, tokens)
+  MatchArgs m{};
+  m.n = n;
+  m.wf = wf;
+  m.tok_off = tok_off;
+  m.tok = tok;
+  m.blk_off = blk_off;
+  m.n_items = n_items;
+  m.out_M = a.s.M;
+  m.out_hash = a.s.hash;
+  if (int rc = launch_match(p, m, a.s.tile_state, st)) return rc;
+  // 2. admission
+  SFKV_CUDA(cudaMemsetAsync(&p->ctr->error, 0, sizeof(int), st));
+  admit_kernel<<<1, 32, 0, st>>>(a);
+  SFKV_LAUNCH_CHECK("admit_kernel");
+  const int sms = sm_count_c();
+  const int g = grid_for(n_items, 256, sms * 8);
+  if (n_items > 0) {
+    probe_kernel<<<g, 256, 0, st>>>(a);
+    resolve_kernel<<<g, 256, 0, st>>>(a);
+    categorize_kernel<<<g, 256, 0, st>>>(a);
+    SFKV_LAUNCH_CHECK("probe/resolve/categorize");
+    if (int rc = exclusive_scan(NeedAlloc{a.s.cat}, n_items, a.s.rank, a.s.scan_tmp, st)) return rc;
+    if (int rc = exclusive_scan(FreeCount{p->free_bits}, p->n_words, a.s.wprefix, a.s.scan_tmp, st)) return rc;
+    alloc_kernel<<<g, 256, 0, st>>>(a);
+    refs_kernel<<<g, 256, 0, st>>>(a);
+    clear_owner_kernel<<<g, 256, 0, st>>>(a);
+    SFKV_LAUNCH_CHECK("alloc/refs");
+    if (a.payload) {
+      if (int rc = launch_commit_payload(p, a, kv_src, kv_src_off, src_pool, src_wf, st)) return rc;
+    }
+  }
+  release_kernel<<<grid_for(n * 32, 256, sms * 8), 256, 0, st>>>(a, 0, nullptr);
+  if (n_items > 0) install_kernel<<<g, 256, 0, st>>>(a);
+  SFKV_LAUNCH_CHECK("release/install");
+  return maybe_rebuild_table(p);
+}
+
+int flush_dev(sfkv_pool* p, int64_t n, const int32_t* wf, int64_t* out_freed, bool all) {
+  cudaStream_t st = p->stream;
+  CommitArgs a = base_args(p);
+  a.n = all ? p->cfg.max_workflows : n;
+  a.wf = wf;
+  if (a.n <= 0) return 0;
+  const int sms = sm_count_c();
+  release_kernel<<<grid_for(a.n * 32, 256, sms * 8), 256, 0, st>>>(a, all ? 2 : 1, out_freed);
+  SFKV_LAUNCH_CHECK("flush release_kernel");
+  return maybe_rebuild_table(p);
+}
+
+
+int launch_payload(sfkv_pool* p, const PayloadJob& j, const void* kv_src, const int64_t* kv_src_off,
+                   const sfkv_pool* src_pool, int32_t src_wf, cudaStream_t st);
+
+int launch_commit_payload(sfkv_pool* p, const CommitArgs& a, const void* kv_src,
+                          const int64_t* kv_src_off, const sfkv_pool* src_pool, int32_t src_wf,
+                          cudaStream_t st) {
+  PayloadJob j;
+  j.n = a.n;
+  j.wf = a.wf;
+  j.tok_off = a.tok_off;
+  j.blk_off = a.s.blk_off;
+  j.M = a.s.M;
+  j.rank = a.s.rank;
+  j.alloc_list = a.s.alloc_list;
+  j.bid = a.s.bid;
+  j.n_items = a.n_items;
+  j.old_pin_blk = p->pin_blk;
+  j.max_pin_blocks = p->cfg.max_pin_blocks;
+  return launch_payload(p, j, kv_src, kv_src_off, src_pool, src_wf, st);
+}
+}  // namespace sfkv

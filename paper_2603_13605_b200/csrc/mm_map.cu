@@ -1,0 +1,344 @@
+// K6 pressure argmin (memory manager) and K7 stage-mapper scoring.
+//
+// K6 replaces pressure_actions (memory.cpp:150-169): per backend whose utilization exceeds
+// tau_pressure (strict), flush the idle (in_flight == 0) preserved entry with the least
+// last_update_ts, ties to the lexicographically smallest workflow id (the reference scans entries
+// in workflow-id order and replaces only on strict <, memory.cpp:160-161). The tracker is a
+// struct-of-arrays in HBM; the lexicographic (ts, wf_rank) minimum per backend is reduced with three
+// order-independent atomic passes (min ts, min rank among ts ties, index), so the victim is
+// deterministic. 16 B per entry per pass.
+//
+// K7 replaces map_threshold (mapper.cpp:19-31: light iff score <= threshold) and generalises it
+// to an R x C cost argmin with reroute_on_overload (orchestrator.cpp:78-87) applied in request
+// order by one warp (exact sequential semantics with a 32-request fast path).
+#include <mutex>
+#include <vector>
+
+#include "pool.cuh"
+
+namespace sfkv {
+
+__device__ __forceinline__ unsigned long long ts_order_key(double t) {
+  if (t == 0.0) t = 0.0;  // -0.0 == 0.0 in the reference's comparison
+  unsigned long long b = (unsigned long long)__double_as_longlong(t);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+struct PressArgs {
+  int64_t n;
+  const int32_t* backend;
+  const double* ts;
+  const uint32_t* rank;
+  const int32_t* in_flight;
+  const uint8_t* preserved;
+  int32_t nb;
+  const double* util;
+  double tau;
+  unsigned long long* best_ts;
+  unsigned int* best_rank;
+  long long* victim;
+};
+
+__device__ __forceinline__ bool eligible(const PressArgs& a, int64_t i, int32_t& b) {
+  b = a.backend[i];
+  return b >= 0 && b < a.nb && a.preserved[i] && a.in_flight[i] <= 0 && a.util[b] > a.tau;
+}
+
+__global__ void press_init(PressArgs a) {
+  int b = threadIdx.x + blockIdx.x * blockDim.x;
+  if (b < a.nb) {
+    a.best_ts[b] = ~0ull;
+    a.best_rank[b] = ~0u;
+    a.victim[b] = -1;
+  }
+}
+__global__ void press_pass1(PressArgs a) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t b;
+    if (eligible(a, i, b)) atomicMin(&a.best_ts[b], ts_order_key(a.ts[i]));
+  }
+}
+__global__ void press_pass2(PressArgs a) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t b;
+    if (eligible(a, i, b) && ts_order_key(a.ts[i]) == a.best_ts[b]) atomicMin(&a.best_rank[b], a.rank[i]);
+  }
+}
+__global__ void press_pass3(PressArgs a) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t b;
+    if (eligible(a, i, b) && ts_order_key(a.ts[i]) == a.best_ts[b] && a.rank[i] == a.best_rank[b])
+      atomicMin(reinterpret_cast<unsigned long long*>(&a.victim[b]), (unsigned long long)i);
+  }
+}
+__global__ void press_fix(PressArgs a) {  // victim starts at -1 (all ones) for atomicMin
+  int b = threadIdx.x + blockIdx.x * blockDim.x;
+  if (b < a.nb && a.best_ts[b] == ~0ull) a.victim[b] = -1;
+}
+
+int pressure_dev(cudaStream_t st, int64_t n, const int32_t* backend, const double* ts,
+                 const uint32_t* rank, const int32_t* in_flight, const uint8_t* preserved,
+                 int32_t nb, const double* util, double tau, unsigned long long* best_ts,
+                 unsigned int* best_rank, long long* victim, int sms) {
+  PressArgs a{n, backend, ts, rank, in_flight, preserved, nb, util, tau, best_ts, best_rank, victim};
+  const int bg = (nb + 255) / 256;
+  press_init<<<bg, 256, 0, st>>>(a);
+  if (n > 0) {
+    const int g = grid_for(n, 256, sms * 8);
+    press_pass1<<<g, 256, 0, st>>>(a);
+    press_pass2<<<g, 256, 0, st>>>(a);
+    press_pass3<<<g, 256, 0, st>>>(a);
+  }
+  press_fix<<<bg, 256, 0, st>>>(a);
+  SFKV_LAUNCH_CHECK("pressure kernels");
+  return 0;
+}
+
+// ---- mapper --------------------------------------------------------------------------------
+__global__ void threshold_kernel(int64_t n, const double* score, double thr, int32_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = score[i] <= thr ? 0 : 1;
+}
+
+struct CostArgs {
+  int64_t n;
+  int32_t c;
+  const int64_t* P;
+  const int64_t* M;
+  const int64_t* O;
+  const double* overhead;
+  const double* prefill;
+  const double* decode;
+  const double* qpen;
+  const int32_t* alternates;
+  unsigned long long* depth;  // live depth (updated by the reroute pass)
+  const unsigned long long* depth0;  // batch-start snapshot
+  unsigned long long limit;
+  int32_t* choice;
+  double* cost;
+};
+
+// Same evaluation order as the oracle, no FMA contraction: bit-identical doubles.
+__global__ void cost_kernel(CostArgs a) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < a.n; r += (int64_t)gridDim.x * blockDim.x) {
+    int32_t best = 0;
+    double bc = 0;
+    for (int32_t j = 0; j < a.c; ++j) {
+      double x = __dadd_rn(a.overhead[j], __dmul_rn(a.prefill[j], (double)(a.P[r] - a.M[r * a.c + j])));
+      x = __dadd_rn(x, __dmul_rn(a.decode[j], (double)a.O[r]));
+      x = __dadd_rn(x, __dmul_rn(a.qpen[j], (double)a.depth0[j]));
+      if (j == 0 || x < bc) {
+        bc = x;
+        best = j;
+      }
+    }
+    a.choice[r] = best;
+    a.cost[r] = bc;
+  }
+}
+
+// reroute_on_overload in request order (one warp). depth lives in shared memory (c <= 1024).
+__global__ void reroute_kernel(CostArgs a) {
+  extern __shared__ unsigned long long sdepth[];
+  const int lane = threadIdx.x;
+  for (int j = lane; j < a.c; j += 32) sdepth[j] = a.depth[j];
+  __syncwarp();
+  for (int64_t base = 0; base < a.n; base += 32) {
+    const int64_t r = base + lane;
+    const bool act = r < a.n;
+    const int32_t ch = act ? a.choice[r] : -1;
+    // fast path: no request of the chunk sees its candidate at the limit
+    const unsigned peers = __match_any_sync(0xffffffffu, ch);
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned long long live = act ? sdepth[ch] + __popc(peers & lt) : 0;
+    const bool ok = !act || a.limit == 0 || live < a.limit;
+    if (__all_sync(0xffffffffu, ok)) {
+      __syncwarp();
+      if (act && (peers & lt) == 0) sdepth[ch] += __popc(peers);  // leader of each peer group
+      __syncwarp();
+    } else {
+      for (int j = 0; j < 32; ++j) {
+        if (base + j >= a.n) break;
+        if (lane == 0) {
+          int32_t c0 = a.choice[base + j], pick = c0;
+          if (sdepth[c0] >= a.limit && a.alternates) {
+            for (int32_t t = 0; t < a.c; ++t) {
+              const int32_t alt = a.alternates[c0 * a.c + t];
+              if (alt < 0) break;
+              if (sdepth[alt] < a.limit) {
+                pick = alt;
+                break;
+              }
+            }
+          }
+          a.choice[base + j] = pick;
+          sdepth[pick] += 1;
+        }
+        __syncwarp();
+      }
+    }
+  }
+  __syncwarp();
+  for (int j = lane; j < a.c; j += 32) a.depth[j] = sdepth[j];
+}
+
+int cost_dev(cudaStream_t st, CostArgs a, int sms) {
+  if (a.n > 0) {
+    cost_kernel<<<grid_for(a.n, 256, sms * 8), 256, 0, st>>>(a);
+    reroute_kernel<<<1, 32, sizeof(unsigned long long) * (a.c > 0 ? a.c : 1), st>>>(a);
+  }
+  SFKV_LAUNCH_CHECK("mapper kernels");
+  return 0;
+}
+
+int threshold_dev(cudaStream_t st, int64_t n, const double* score, double thr, int32_t* out, int sms) {
+  if (n > 0) threshold_kernel<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(n, score, thr, out);
+  SFKV_LAUNCH_CHECK("threshold_kernel");
+  return 0;
+}
+
+}  // namespace sfkv
+
+// ---- pool-less entry points: per-device stream + scratch ----------------------------------
+namespace sfkv {
+struct DevCtx {
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+  Scratch buf;
+  int sms = 148;
+};
+static DevCtx* ctx_for(int dev) {
+  static std::mutex gmu;
+  static std::vector<DevCtx*> ctxs;
+  std::lock_guard<std::mutex> lk(gmu);
+  if ((int)ctxs.size() <= dev) ctxs.resize(dev + 1, nullptr);
+  if (!ctxs[dev]) {
+    auto* c = new DevCtx;
+    cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev);
+    ctxs[dev] = c;
+  }
+  return ctxs[dev];
+}
+}  // namespace sfkv
+
+using namespace sfkv;
+
+extern "C" int sfmm_pressure_argmin(int32_t device, int64_t n, const int32_t* backend, const double* ts,
+                                    const uint32_t* wf_rank, const int32_t* in_flight,
+                                    const uint8_t* preserved, int32_t n_backends, const double* util,
+                                    double tau, int64_t* out_victim) {
+  if (n < 0 || n_backends < 0 || (n > 0 && (!backend || !ts || !wf_rank || !in_flight || !preserved)) ||
+      (n_backends > 0 && (!util || !out_victim)))
+    return fail(SFKV_EINVAL, "pressure_argmin: bad argument");
+  if (n_backends == 0) return 0;
+  if (int rc = check_device(device)) return rc;
+  DeviceGuard g(device);
+  DevCtx* c = ctx_for(device);
+  std::lock_guard<std::mutex> lk(c->mu);
+  Carver cv;
+  const size_t o_b = cv.take<int32_t>(n), o_ts = cv.take<double>(n), o_rk = cv.take<uint32_t>(n),
+               o_if = cv.take<int32_t>(n), o_pr = cv.take<uint8_t>(n), o_u = cv.take<double>(n_backends),
+               o_bt = cv.take<unsigned long long>(n_backends), o_br = cv.take<unsigned int>(n_backends),
+               o_v = cv.take<long long>(n_backends);
+  if (int rc = c->buf.ensure(cv.off)) return rc;
+  char* b = c->buf.as<char>();
+  cudaStream_t st = c->stream;
+  if (n > 0) {
+    SFKV_CUDA(cudaMemcpyAsync(b + o_b, backend, n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    SFKV_CUDA(cudaMemcpyAsync(b + o_ts, ts, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    SFKV_CUDA(cudaMemcpyAsync(b + o_rk, wf_rank, n * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    SFKV_CUDA(cudaMemcpyAsync(b + o_if, in_flight, n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    SFKV_CUDA(cudaMemcpyAsync(b + o_pr, preserved, n, cudaMemcpyHostToDevice, st));
+  }
+  SFKV_CUDA(cudaMemcpyAsync(b + o_u, util, n_backends * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (int rc = pressure_dev(st, n, reinterpret_cast<int32_t*>(b + o_b), reinterpret_cast<double*>(b + o_ts),
+                           reinterpret_cast<uint32_t*>(b + o_rk), reinterpret_cast<int32_t*>(b + o_if),
+                           reinterpret_cast<uint8_t*>(b + o_pr), n_backends,
+                           reinterpret_cast<double*>(b + o_u), tau,
+                           reinterpret_cast<unsigned long long*>(b + o_bt),
+                           reinterpret_cast<unsigned int*>(b + o_br), reinterpret_cast<long long*>(b + o_v),
+                           c->sms))
+    return rc;
+  SFKV_CUDA(cudaMemcpyAsync(out_victim, b + o_v, n_backends * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  SFKV_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+extern "C" int sfmap_threshold_batch(int32_t device, int64_t n, const double* score, double threshold,
+                                     int32_t* out_choice) {
+  if (n < 0 || (n > 0 && (!score || !out_choice))) return fail(SFKV_EINVAL, "threshold_batch: bad argument");
+  if (n == 0) return 0;
+  if (int rc = check_device(device)) return rc;
+  DeviceGuard g(device);
+  DevCtx* c = ctx_for(device);
+  std::lock_guard<std::mutex> lk(c->mu);
+  Carver cv;
+  const size_t o_s = cv.take<double>(n), o_o = cv.take<int32_t>(n);
+  if (int rc = c->buf.ensure(cv.off)) return rc;
+  char* b = c->buf.as<char>();
+  SFKV_CUDA(cudaMemcpyAsync(b + o_s, score, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  if (int rc = threshold_dev(c->stream, n, reinterpret_cast<double*>(b + o_s), threshold,
+                            reinterpret_cast<int32_t*>(b + o_o), c->sms))
+    return rc;
+  SFKV_CUDA(cudaMemcpyAsync(out_choice, b + o_o, n * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  SFKV_CUDA(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+extern "C" int sfmap_cost_batch(int32_t device, int64_t n, int32_t cc, const int64_t* P, const int64_t* M,
+                                const int64_t* O, const double* overhead, const double* prefill,
+                                const double* decode, const double* queue_penalty,
+                                const int32_t* alternates, uint64_t* depth_inout, uint64_t limit,
+                                int32_t* out_choice, double* out_cost) {
+  if (n < 0 || cc <= 0 || cc > 1024 || !depth_inout || !overhead || !prefill || !decode || !queue_penalty ||
+      (n > 0 && (!P || !M || !O || !out_choice || !out_cost)))
+    return fail(SFKV_EINVAL, "cost_batch: bad argument");
+  if (n == 0) return 0;
+  if (int rc = check_device(device)) return rc;
+  DeviceGuard g(device);
+  DevCtx* c = ctx_for(device);
+  std::lock_guard<std::mutex> lk(c->mu);
+  Carver cv;
+  const size_t o_P = cv.take<int64_t>(n), o_M = cv.take<int64_t>(n * (int64_t)cc), o_O = cv.take<int64_t>(n),
+               o_par = cv.take<double>(4 * (size_t)cc), o_alt = cv.take<int32_t>((size_t)cc * cc),
+               o_d = cv.take<unsigned long long>(cc), o_d0 = cv.take<unsigned long long>(cc),
+               o_ch = cv.take<int32_t>(n), o_co = cv.take<double>(n);
+  if (int rc = c->buf.ensure(cv.off)) return rc;
+  char* b = c->buf.as<char>();
+  cudaStream_t st = c->stream;
+  SFKV_CUDA(cudaMemcpyAsync(b + o_P, P, n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  SFKV_CUDA(cudaMemcpyAsync(b + o_M, M, n * cc * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  SFKV_CUDA(cudaMemcpyAsync(b + o_O, O, n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  double* par = reinterpret_cast<double*>(b + o_par);
+  SFKV_CUDA(cudaMemcpyAsync(par, overhead, cc * sizeof(double), cudaMemcpyHostToDevice, st));
+  SFKV_CUDA(cudaMemcpyAsync(par + cc, prefill, cc * sizeof(double), cudaMemcpyHostToDevice, st));
+  SFKV_CUDA(cudaMemcpyAsync(par + 2 * cc, decode, cc * sizeof(double), cudaMemcpyHostToDevice, st));
+  SFKV_CUDA(cudaMemcpyAsync(par + 3 * cc, queue_penalty, cc * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (alternates)
+    SFKV_CUDA(cudaMemcpyAsync(b + o_alt, alternates, (size_t)cc * cc * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  SFKV_CUDA(cudaMemcpyAsync(b + o_d, depth_inout, cc * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+  SFKV_CUDA(cudaMemcpyAsync(b + o_d0, depth_inout, cc * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+  CostArgs a;
+  a.n = n;
+  a.c = cc;
+  a.P = reinterpret_cast<int64_t*>(b + o_P);
+  a.M = reinterpret_cast<int64_t*>(b + o_M);
+  a.O = reinterpret_cast<int64_t*>(b + o_O);
+  a.overhead = par;
+  a.prefill = par + cc;
+  a.decode = par + 2 * cc;
+  a.qpen = par + 3 * cc;
+  a.alternates = alternates ? reinterpret_cast<int32_t*>(b + o_alt) : nullptr;
+  a.depth = reinterpret_cast<unsigned long long*>(b + o_d);
+  a.depth0 = reinterpret_cast<unsigned long long*>(b + o_d0);
+  a.limit = limit;
+  a.choice = reinterpret_cast<int32_t*>(b + o_ch);
+  a.cost = reinterpret_cast<double*>(b + o_co);
+  if (int rc = cost_dev(st, a, c->sms)) return rc;
+  SFKV_CUDA(cudaMemcpyAsync(out_choice, a.choice, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  SFKV_CUDA(cudaMemcpyAsync(out_cost, a.cost, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  SFKV_CUDA(cudaMemcpyAsync(depth_inout, a.depth, cc * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  SFKV_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}

@@ -1,0 +1,121 @@
+// Internal definition of a KV pin pool (one backend's cache, resident on one GPU).
+//
+// HBM layout (all arrays device-resident, sized at pool creation):
+//   pins   pin_len[W] i64 (-1 = no pin), pin_nblk[W] i32,
+//          pin_blk[W][MB] i32 (block table), pin_hash[W][MB] u64 (chained hash per pin block,
+//          pin-major so the match kernel reads a pin's hashes coalesced)
+//   blocks blk_key[B] u64, blk_tok[B][16] u32 (tokens: verify-on-hit and LCP tails),
+//          blk_n[B] u8 (valid tokens), blk_in_table[B] u8, blk_ref[B] u32, blk_slot[B] i64,
+//          free_bits[ceil(B/32)] u32 (1 = free)
+//   table  slots[S] of 16 B {u64 key, i32 block, i32 pad} (open addressing, linear probing,
+//          S = 2^table_log2; key 0 = empty, 1 = tombstone; one sector per probe) and
+//          towner[S] i64 (lowest claiming item of a batch; commit only)
+//   kv     [B][n_slabs][16][slab_row_bytes] bytes (bf16 K/V rows), block-major so a block is
+//          one contiguous extent (2 MiB for Llama-3-8B: 64 slabs x 16 x 2 KiB)
+#pragma once
+
+#include "common.cuh"
+
+namespace sfkv {
+
+struct Slot {
+  unsigned long long key;
+  int32_t val;  // block id; -1 while a batch claim is pending
+  int32_t pad;
+};
+static_assert(sizeof(Slot) == 16, "table slot is one 16-B vector");
+
+struct DevCounters {
+  long long occupancy;            // logical tokens (sum of pin lengths)
+  unsigned long long rejections;  // capacity_rejections
+  long long table_live;
+  long long table_tomb;
+  long long blocks_in_use;
+  int error;                      // sticky device-side error (SFKV_EPOOL / SFKV_ESTALE)
+  int pad;
+};
+
+}  // namespace sfkv
+
+struct sfkv_pool {
+  sfkv_pool_config cfg;
+  int64_t block_bytes = 0;
+  int64_t n_words = 0;        // free-bitmap words
+  int64_t table_slots = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  // device state
+  int64_t* pin_len = nullptr;
+  int32_t* pin_nblk = nullptr;
+  int32_t* pin_blk = nullptr;
+  uint64_t* pin_hash = nullptr;
+  uint64_t* blk_key = nullptr;
+  uint32_t* blk_tok = nullptr;
+  uint8_t* blk_n = nullptr;
+  uint8_t* blk_in_table = nullptr;
+  uint32_t* blk_ref = nullptr;
+  int64_t* blk_slot = nullptr;
+  uint32_t* free_bits = nullptr;
+  sfkv::Slot* slots = nullptr;
+  int64_t* towner = nullptr;
+  uint8_t* kv = nullptr;
+  sfkv::DevCounters* ctr = nullptr;  // device
+  sfkv::DevCounters* ctr_host = nullptr;  // pinned mirror
+  // host-side counters (BackendStats, backend.hpp:72-80)
+  uint64_t flush_calls = 0;
+  uint64_t preserve_calls = 0;
+  // scratch
+  sfkv::Scratch scratch;       // per-call device scratch
+  sfkv::Scratch small;         // per-call offsets (sized by request count)
+  sfkv::Scratch io;            // device copies of host-pointer inputs/outputs
+  void* host_stage = nullptr;  // pinned host staging
+  size_t host_stage_bytes = 0;
+};
+
+namespace sfkv {
+
+// Outputs of the hashing/matching pass shared by match, lookup and commit.
+struct MatchArgs {
+  int64_t n;                 // requests
+  const int32_t* wf;         // nullable (lookup mode)
+  const int64_t* tok_off;
+  const uint32_t* tok;
+  const int64_t* blk_off;    // [n+1] exclusive scan of ceil(len/16)
+  int64_t n_items;
+  int64_t* out_M;            // nullable
+  uint64_t* out_hash;        // nullable
+  int32_t* out_block;        // nullable: lookup mode
+  int64_t* out_hit;          // nullable: lookup mode
+};
+
+struct PayloadJob {
+  int64_t n;
+  const int32_t* wf;
+  const int64_t* tok_off;
+  const int64_t* blk_off;
+  const int64_t* M;
+  const int64_t* rank;
+  const int64_t* alloc_list;
+  const int32_t* bid;
+  int64_t n_items;
+  const int32_t* old_pin_blk;
+  int32_t max_pin_blocks;
+};
+int launch_payload(sfkv_pool* p, const PayloadJob& j, const void* kv_src, const int64_t* kv_src_off,
+                   const sfkv_pool* src_pool, int32_t src_wf, cudaStream_t st);
+
+int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStream_t st);
+size_t match_tile_state_elems(int64_t n_items);
+
+int ensure_host_stage(sfkv_pool* p, size_t bytes);
+
+// Internal commit entry (device pointers). src_pool/src_wf: handoff payload source.
+int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
+               const uint32_t* tok, const void* kv_src, const int64_t* kv_src_off,
+               const int64_t* m_expected, int32_t* out_status, const sfkv_pool* src_pool,
+               int32_t src_wf);
+int flush_dev(sfkv_pool* p, int64_t n, const int32_t* wf, int64_t* out_freed, bool all);
+int gather_dev(sfkv_pool* p, int64_t n, const int32_t* wf, void* dst, const int64_t* dst_off);
+int maybe_rebuild_table(sfkv_pool* p);
+
+}  // namespace sfkv

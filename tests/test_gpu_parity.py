@@ -1,0 +1,236 @@
+"""GPU parity: libsfkv.so (sm_100a kernels behind the C ABI) against the CPU oracle and the
+reference's own golden streams. Integer/index outputs must be bit-exact; KV payload bytes must be
+byte-identical; mapper costs are compared as exact doubles (the kernels avoid FMA contraction),
+well inside north_star's 1e-6 relative tolerance."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import replay
+from paper_2603_13605_b200.abi import BLOCK_TOKENS, Config, Pool, csr
+from scenarios import Workload
+
+pytestmark = pytest.mark.gpu
+
+
+# ---------------------------------------------------------------- Class A: golden replays ----
+@pytest.mark.parametrize("name", replay.stream_names())
+@pytest.mark.parametrize("batched", [False, True])
+def test_gpu_replays_reference_stream(gpu_api, name, batched):
+    lines = replay.load_stream(name)
+    assert replay.replay(lines, gpu_api, batched=batched) > 0
+
+
+# ---------------------------------------------------------------- Class B: vs the oracle -----
+def _pair(gpu_api, oracle_api, cfg):
+    return Pool(gpu_api, cfg), Pool(oracle_api, cfg)
+
+
+def _assert_same_state(g, o, wfs):
+    sg, so = g.stats(), o.stats()
+    for k in ("occupancy_tokens", "capacity_rejections", "blocks_in_use", "table_live"):
+        assert sg[k] == so[k], (k, sg[k], so[k])
+    np.testing.assert_array_equal(g.refcounts(), o.refcounts())
+    for w in wfs:
+        ig, hg = g.pin_blocks(w)
+        io, ho = o.pin_blocks(w)
+        np.testing.assert_array_equal(ig, io)
+        np.testing.assert_array_equal(hg, ho)
+        assert g.pinned_token_count(w) == o.pinned_token_count(w)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_match_commit_flush_random(gpu_api, oracle_api, seed):
+    n_wf = 96
+    wl = Workload(seed, n_wf, n_sys=3, sys_len=(16, 80), ctx_len=(0, 70), append=(0, 50))
+    cfg = Config(max_workflows=n_wf, n_blocks=6000, capacity_tokens=60_000, max_pin_blocks=64,
+                 table_log2=14)
+    g, o = _pair(gpu_api, oracle_api, cfg)
+    rng = np.random.default_rng(seed + 100)
+    for step in range(12):
+        wfs = rng.choice(n_wf, size=int(rng.integers(1, n_wf)), replace=False).astype(np.int32)
+        seqs, off, tok = wl.batch(wfs)
+        Mg, hg = g.match(wfs, off, tok, want_hash=True)
+        Mo, ho = o.match(wfs, off, tok, want_hash=True)
+        np.testing.assert_array_equal(Mg, Mo)
+        np.testing.assert_array_equal(hg, ho)
+        bg, htg = g.lookup(off, tok)
+        bo, hto = o.lookup(off, tok)
+        np.testing.assert_array_equal(bg, bo)
+        np.testing.assert_array_equal(htg, hto)
+        sg = g.commit(wfs, off, tok)
+        so = o.commit(wfs, off, tok)
+        np.testing.assert_array_equal(sg, so)
+        if step % 4 == 3:
+            fl = rng.choice(n_wf, size=8, replace=False).astype(np.int32)
+            np.testing.assert_array_equal(g.flush_batch(fl), o.flush_batch(fl))
+        _assert_same_state(g, o, range(n_wf))
+    assert g.flush(-1) == o.flush(-1)
+    _assert_same_state(g, o, range(n_wf))
+
+
+def test_capacity_rejections_and_edge_lengths(gpu_api, oracle_api):
+    cfg = Config(max_workflows=8, n_blocks=512, capacity_tokens=100, max_pin_blocks=16)
+    g, o = _pair(gpu_api, oracle_api, cfg)
+    seqs = [[], [7] * 15, [7] * 16, [7] * 17, list(range(1, 61)), list(range(1, 81))]
+    wfs = np.arange(len(seqs), dtype=np.int32)
+    off, tok = csr(seqs)
+    np.testing.assert_array_equal(g.commit(wfs, off, tok), o.commit(wfs, off, tok))
+    _assert_same_state(g, o, range(8))
+    np.testing.assert_array_equal(g.match(wfs, off, tok), o.match(wfs, off, tok))
+    assert g.preserve(0) and o.preserve(0)  # an empty pin counts as present
+    assert g.cache_utilization() == o.cache_utilization()
+
+
+def test_reference_known_answers(gpu_api):
+    """test_backend_sim.cpp:89-103 (LCP) and 134-144 (capacity) on the GPU pool."""
+    g = Pool(gpu_api, Config(max_workflows=4, n_blocks=64, capacity_tokens=100, max_pin_blocks=8))
+    a, b, c, d, e, x, y = 1, 2, 3, 4, 5, 6, 7
+    off, tok = csr([[a, b, c]])
+    assert g.commit(np.array([0], np.int32), off, tok)[0] == 1
+    for seq, want, wf in (([a, b, c, d, e], 3, 0), ([x, y], 0, 0), ([a, b, c], 0, 1)):
+        o2, t2 = csr([seq])
+        assert g.match(np.array([wf], np.int32), o2, t2)[0] == want
+    g2 = Pool(gpu_api, Config(max_workflows=4, n_blocks=64, capacity_tokens=100, max_pin_blocks=8))
+    st = g2.commit(np.array([0, 1], np.int32), *csr([[1] * 60, [2] * 80]))
+    assert list(st) == [1, 0] and g2.stats()["capacity_rejections"] == 1
+    assert g2.flush(0) == 60 and g2.flush(0) == 0
+
+
+def test_payload_scatter_cow_gather(gpu_api, oracle_api):
+    torch = pytest.importorskip("torch")
+    n_wf = 24
+    cfg = Config(max_workflows=n_wf, n_blocks=1500, capacity_tokens=50_000, max_pin_blocks=40,
+                 table_log2=12, n_slabs=4, slab_row_bytes=32)
+    g, o = _pair(gpu_api, oracle_api, cfg)
+    wl = Workload(7, n_wf, n_sys=2, sys_len=(16, 48), ctx_len=(0, 40), append=(1, 30))
+    rng = np.random.default_rng(7)
+    row = cfg.slab_row_bytes
+    for step in range(6):
+        wfs = rng.choice(n_wf, size=int(rng.integers(1, n_wf)), replace=False).astype(np.int32)
+        seqs, off, tok = wl.batch(wfs)
+        M = o.match(wfs, off, tok)
+        np.testing.assert_array_equal(g.match(wfs, off, tok), M)
+        # staging rows [M, P) per request: [slab][P-M][row]
+        sizes = [cfg.n_slabs * (len(s) - int(m)) * row for s, m in zip(seqs, M)]
+        kv_off = np.zeros(len(seqs), dtype=np.int64)
+        kv_off[1:] = np.cumsum(sizes)[:-1]
+        staging = rng.integers(0, 256, size=max(int(sum(sizes)), 16), dtype=np.uint8)
+        st_o = o.commit(wfs, off, tok, kv_src=staging, kv_src_off=kv_off, m_expected=M)
+        dev = torch.from_numpy(staging).cuda()
+        st_g = g.commit(wfs, off, tok, kv_src=dev, kv_src_off=kv_off, m_expected=M)
+        np.testing.assert_array_equal(st_g, st_o)
+        _assert_same_state(g, o, range(n_wf))
+        # gather every pinned workflow and compare bytes
+        lens = [o.pinned_token_count(w) for w in range(n_wf)]
+        dst_off = np.zeros(n_wf, dtype=np.int64)
+        dst_off[1:] = np.cumsum([cfg.n_slabs * L * row for L in lens])[:-1]
+        total = int(sum(cfg.n_slabs * L * row for L in lens)) + 16
+        ho = np.zeros(total, dtype=np.uint8)
+        allw = np.arange(n_wf, dtype=np.int32)
+        oracle_api.check("gather", oracle_api.gather(o.h, n_wf, allw.ctypes.data, ho.ctypes.data,
+                                                     dst_off.ctypes.data))
+        dg = torch.zeros(total, dtype=torch.uint8, device="cuda")
+        dw = torch.from_numpy(allw).cuda()
+        doff = torch.from_numpy(dst_off).cuda()
+        gpu_api.check("gather_dev", gpu_api.gather_dev(g.h, n_wf, C.c_void_p(dw.data_ptr()),
+                                                       C.c_void_p(dg.data_ptr()),
+                                                       C.c_void_p(doff.data_ptr())))
+        gpu_api.check("pool_sync", gpu_api.pool_sync(g.h))
+        np.testing.assert_array_equal(dg.cpu().numpy(), ho)
+
+
+def test_stale_payload_commit_is_refused(gpu_api):
+    torch = pytest.importorskip("torch")
+    cfg = Config(max_workflows=4, n_blocks=64, capacity_tokens=1000, max_pin_blocks=8, n_slabs=2,
+                 slab_row_bytes=16)
+    g = Pool(gpu_api, cfg)
+    off, tok = csr([[1, 2, 3]])
+    stg = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    with pytest.raises(Exception):
+        g.commit(np.array([0], np.int32), off, tok, kv_src=stg, kv_src_off=np.zeros(1, np.int64),
+                 m_expected=np.array([2], np.int64))
+    assert g.stats()["occupancy_tokens"] == 0
+
+
+def test_handoff_between_pools(gpu_api, oracle_api):
+    cfg = Config(max_workflows=8, n_blocks=400, capacity_tokens=10_000, max_pin_blocks=32,
+                 table_log2=10, n_slabs=2, slab_row_bytes=16)
+    ga, gb = Pool(gpu_api, cfg), Pool(gpu_api, cfg)
+    oa, ob = Pool(oracle_api, cfg), Pool(oracle_api, cfg)
+    rng = np.random.default_rng(5)
+    seqs = [rng.integers(1, 1000, size=n).astype(np.uint32) for n in (70, 33, 16)]
+    wfs = np.arange(3, dtype=np.int32)
+    off, tok = csr(seqs)
+    sizes = [cfg.n_slabs * len(s) * cfg.slab_row_bytes for s in seqs]
+    kv_off = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    staging = rng.integers(0, 256, size=int(sum(sizes)), dtype=np.uint8)
+    import torch
+    for (p, stg) in ((ga, torch.from_numpy(staging).cuda()), (oa, staging)):
+        p.commit(wfs, off, tok, kv_src=stg, kv_src_off=kv_off)
+    # pre-existing partial pin on the destination for wf 5 (COW source on the dst side)
+    o5, t5 = csr([seqs[0][:40]])
+    for p in (gb, ob):
+        p.commit(np.array([5], np.int32), o5, t5)
+    for src_wf, dst_wf in ((0, 5), (1, 1), (2, 2)):
+        assert ga.handoff_to(src_wf, gb, dst_wf) == oa.handoff_to(src_wf, ob, dst_wf)
+    _assert_same_state(gb, ob, range(8))
+
+
+# ---------------------------------------------------------------- K6 / K7 ----------------
+def test_pressure_argmin_random(gpu_api, oracle_api):
+    rng = np.random.default_rng(1234)  # test_memory.cpp:131-175 uses seed 1234, 300 trials
+    pg = replay.default_pressure(gpu_api)
+    po = replay.default_pressure(oracle_api)
+    for trial in range(300):
+        nb = int(rng.integers(1, 5))
+        n = int(rng.integers(0, 60))
+        backend = rng.integers(0, nb, size=n).astype(np.int32)
+        ts = rng.integers(0, 8, size=n).astype(np.float64)  # many ties
+        wr = rng.permutation(n).astype(np.uint32)
+        inf = (rng.random(n) < 0.3).astype(np.int32) * rng.integers(1, 3, size=n).astype(np.int32)
+        pres = (rng.random(n) < 0.8).astype(np.uint8)
+        util = rng.choice([0.5, 0.85, 0.86, 1.0], size=nb).astype(np.float64)
+        np.testing.assert_array_equal(pg(backend, ts, wr, inf, pres, util, 0.85),
+                                      po(backend, ts, wr, inf, pres, util, 0.85))
+
+
+def _cost(api, dev, n, c, P, M, O, par, alt, depth, limit):
+    choice = np.zeros(n, dtype=np.int32)
+    cost = np.zeros(n, dtype=np.float64)
+    args = [n, c, P.ctypes.data, M.ctypes.data, O.ctypes.data] + [x.ctypes.data for x in par] + \
+           [alt.ctypes.data if alt is not None else None, depth.ctypes.data, limit,
+            choice.ctypes.data, cost.ctypes.data]
+    if api.kind == "gpu":
+        args = [dev] + args
+    api.check("cost_batch", api.cost_batch(*args))
+    return choice, cost
+
+
+@pytest.mark.parametrize("limit", [0, 3, 40])
+def test_mapper_cost_and_reroute(gpu_api, oracle_api, limit):
+    rng = np.random.default_rng(11)
+    n, c = 5000, 8
+    P = rng.integers(1, 4096, size=n).astype(np.int64)
+    M = (rng.random((n, c)) * P[:, None]).astype(np.int64).reshape(-1)
+    O = rng.integers(0, 512, size=n).astype(np.int64)
+    par = [rng.random(c) * 50, rng.random(c) * 2, rng.random(c) * 20, rng.random(c)]
+    alt = np.full((c, c), -1, dtype=np.int32)
+    for i in range(c):
+        alt[i, : c - 1] = [(i + j) % c for j in range(1, c)]
+    d0 = rng.integers(0, 5, size=c).astype(np.uint64)
+    dg, do = d0.copy(), d0.copy()
+    cg, kg = _cost(gpu_api, 0, n, c, P, M, O, par, alt, dg, limit)
+    co, ko = _cost(oracle_api, 0, n, c, P, M, O, par, alt, do, limit)
+    np.testing.assert_array_equal(cg, co)
+    np.testing.assert_array_equal(kg, ko)  # exact doubles
+    np.testing.assert_array_equal(dg, do)
+
+
+def test_threshold_mapper(gpu_api, oracle_api):
+    """test_mapper.cpp:54-89: 80 -> light, 100 -> light (tie), 5000 -> heavy at threshold 100."""
+    s = np.array([80, 100, 5000, 100.0000001, -1, 0], dtype=np.float64)
+    out = np.zeros(len(s), dtype=np.int32)
+    gpu_api.check("threshold", gpu_api.threshold_batch(0, len(s), s.ctypes.data, 100.0, out.ctypes.data))
+    assert list(out) == [0, 0, 1, 1, 0, 0]
