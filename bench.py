@@ -1,0 +1,567 @@
+#!/usr/bin/env python3
+"""bench.py — prefix-match blocks/s (headline) and KV gather/scatter GB/s on B200.
+
+Workload (BASELINE.json configs[1]): a synthetic 10k-workflow trace on the
+Llama-3-8B KV shape (32 layers x 8 KV heads x d=128, bf16, 16-token blocks = 2 MiB per block).
+Every workflow holds a pinned context whose length is log-uniform in [512, 8192] tokens; its next
+stage prompt is that context plus a 0..255-token append, and 10% of prompts rewrite one earlier
+token (a partial hit). One step = the stage-boundary lookup for all 10k workflows:
+sfkv_match_batch_dev (chained block hashing + exact LCP against each workflow's own pin — the
+reference's SimulatedBackend::prefix_match, simulated_backend.cpp:153-162) over ~1.9M blocks.
+
+  value  = blocks looked up per second, inputs resident in HBM, L2 flushed between steps
+  e2e    = the same through the host-pointer C ABI (sfkv_match_batch): H2D of the batch from
+           pinned memory + D2H of M inside the timed region
+  kv     = payload legs on a 64 GiB Llama-3-8B-shaped pool: gather of retained pins into
+           contiguous staging and a stage commit (copy-on-share + scatter of appended tokens)
+  roofline / cpu_baseline / clocks / gpu_launches per the driver contract.
+
+--impl reference runs the reference's own prefix_match (oracle/_ref/libsfref.so, compiled from
+/root/reference, token ids rendered to its whitespace-token strings) on all host cores over a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+BT = 16
+KV_SLABS, KV_ROW = 64, 2048  # 32 layers x {K,V}; 8 heads x 128 dims x bf16
+BLOCK_BYTES = KV_SLABS * BT * KV_ROW  # 2 MiB
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ workload ----------------
+def make_workload(seed, n_wf, lo=512, hi=8192, app_hi=256, p_rewrite=0.1):
+    rng = np.random.default_rng(seed)
+    base = np.exp(rng.uniform(math.log(lo), math.log(hi), size=n_wf)).astype(np.int64)
+    app = rng.integers(0, app_hi, size=n_wf).astype(np.int64)
+    pin_off = np.zeros(n_wf + 1, np.int64)
+    pin_off[1:] = np.cumsum(base)
+    pin_tok = rng.integers(1, 1 << 30, size=int(pin_off[-1]), dtype=np.uint32)
+    req_len = base + app
+    req_off = np.zeros(n_wf + 1, np.int64)
+    req_off[1:] = np.cumsum(req_len)
+    req_tok = np.empty(int(req_off[-1]), np.uint32)
+    appended = rng.integers(1, 1 << 30, size=int(app.sum()), dtype=np.uint32)
+    a0 = 0
+    rewrite = rng.random(n_wf) < p_rewrite
+    pos = (rng.random(n_wf) * base).astype(np.int64)
+    for w in range(n_wf):
+        b, e = req_off[w], req_off[w] + base[w]
+        req_tok[b:e] = pin_tok[pin_off[w]:pin_off[w + 1]]
+        req_tok[e:req_off[w + 1]] = appended[a0:a0 + app[w]]
+        a0 += app[w]
+        if rewrite[w]:
+            req_tok[b + pos[w]] ^= np.uint32(0x2A2A2A)
+    expect_M = np.where(rewrite, pos, base)
+    return dict(n=n_wf, pin_off=pin_off, pin_tok=pin_tok, req_off=req_off, req_tok=req_tok,
+                base=base, req_len=req_len, expect_M=expect_M)
+
+
+def blocks_of(lens):
+    return (lens + BT - 1) // BT
+
+
+# ------------------------------------------------------------------ clocks ------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------ reference arm -----------
+def ref_lib():
+    so = os.path.join(REPO, "oracle", "_ref", "libsfref.so")
+    if not os.path.exists(so):
+        return None
+    L = C.CDLL(so)
+    L.sfref_pool_create.restype = C.c_void_p
+    L.sfref_pool_create.argtypes = [C.c_longlong]
+    L.sfref_complete.restype = C.c_longlong
+    L.sfref_complete.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p, C.c_longlong, C.c_void_p]
+    L.sfref_batch_create.restype = C.c_void_p
+    L.sfref_batch_create.argtypes = [C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.sfref_prefix_match_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    L.sfref_pool_destroy.argtypes = [C.c_void_p]
+    L.sfref_batch_destroy.argtypes = [C.c_void_p]
+    return L
+
+
+def ref_shard(L, wl, idx):
+    """A reference SimulatedBackend holding the pins of workflows idx, plus their request batch."""
+    h = L.sfref_pool_create(1 << 40)
+    acc = C.c_int()
+    for w in idx:
+        t = wl["pin_tok"][wl["pin_off"][w]:wl["pin_off"][w + 1]]
+        L.sfref_complete(h, f"wf{w}".encode(), t.ctypes.data, len(t), C.byref(acc))
+    seqs = [wl["req_tok"][wl["req_off"][w]:wl["req_off"][w + 1]] for w in idx]
+    off = np.zeros(len(idx) + 1, np.int64)
+    off[1:] = np.cumsum([len(s) for s in seqs])
+    tok = np.concatenate(seqs).astype(np.uint32) if seqs else np.zeros(1, np.uint32)
+    names = (C.c_char_p * len(idx))(*[f"wf{w}".encode() for w in idx])
+    b = L.sfref_batch_create(len(idx), names, off.ctypes.data, tok.ctypes.data)
+    blocks = int(blocks_of(np.diff(off)).sum())
+    return h, b, blocks, len(idx)
+
+
+def time_ref(L, shards, steps, warmup):
+    """Concurrent prefix_match over all shards (one thread each; ctypes drops the GIL)."""
+    outs = [np.zeros(n, np.int64) for (_, _, _, n) in shards]
+
+    def one(i):
+        h, b, _, _ = shards[i]
+        L.sfref_prefix_match_batch(h, b, outs[i].ctypes.data)
+
+    times = []
+    for it in range(warmup + steps):
+        ths = [threading.Thread(target=one, args=(i,)) for i in range(len(shards))]
+        t0 = time.perf_counter()
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        dt = time.perf_counter() - t0
+        if it >= warmup:
+            times.append(dt)
+    return times, outs
+
+
+def cpu_sample_workload(seed, n):
+    return make_workload(seed, n)
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    L = ref_lib()
+    cores = os.cpu_count() or 1
+    n_sample = args.ref_sample
+    wl = cpu_sample_workload(args.seed, n_sample)
+    if L is not None:
+        kind = "reference"
+        parts = np.array_split(np.arange(n_sample), cores)
+        shards = [ref_shard(L, wl, list(p)) for p in parts if len(p)]
+        times, outs = time_ref(L, shards, args.steps, args.warmup)
+        blocks = sum(s[2] for s in shards)
+        for s in shards:
+            L.sfref_batch_destroy(s[1])
+            L.sfref_pool_destroy(s[0])
+        sample = (f"{n_sample} workflows of the C2 distribution ({blocks} blocks/step), "
+                  f"{len(shards)} threads x SimulatedBackend::prefix_match on pre-tokenized strings")
+    else:  # oracle port (the C restatement) when the reference could not be compiled here
+        sys.path.insert(0, os.path.join(REPO, "tests"))
+        import oracle_lib
+        from paper_2603_13605_b200.abi import Config, Pool
+        kind, cores = "port", 1
+        api = oracle_lib.load()
+        pool = Pool(api, Config(max_workflows=n_sample, n_blocks=int(blocks_of(wl["base"]).sum()) + 64,
+                                capacity_tokens=1 << 40, max_pin_blocks=600, table_log2=24))
+        wf = np.arange(n_sample, dtype=np.int32)
+        pool.commit(wf, wl["pin_off"], wl["pin_tok"])
+        times = []
+        for it in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            pool.match(wf, wl["req_off"], wl["req_tok"])
+            if it >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        blocks = int(blocks_of(np.diff(wl["req_off"])).sum())
+        sample = f"{n_sample} workflows, oracle C port (sfo_match_batch), 1 thread"
+    ms = 1e3 * float(np.mean(times))
+    value = blocks / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "blocks/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic", "config": config_dict(args, blocks_per_step=blocks, n_wf=n_sample),
+            "cpu_baseline": {"value": value, "unit": "blocks/s", "cores": len(parts) if kind == "reference" else 1,
+                             "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": "blocks/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+METRIC = "prefix-match blocks/s (C2 stage-boundary lookup); KV gather/scatter GB/s vs HBM peak"
+
+
+def config_dict(args, **kw):
+    d = {"workload": "C2: synthetic 10k-workflow trace, Llama-3-8B KV shape (32L, 8 KV heads, "
+                     "d=128, bf16, block=16), 1 backend pool per GPU; step = stage-prefix lookup of "
+                     "every workflow against its own pin",
+         "workflows_per_gpu": args.workflows, "context_tokens": "log-uniform [512, 8192]",
+         "append_tokens": "uniform [0, 256)", "rewrite_fraction": 0.1,
+         "l2": "flushed between timed steps (512 MiB write)", "parallelism": f"replica x{args.gpus}"}
+    d.update(kw)
+    return d
+
+
+# ------------------------------------------------------------------ our arm ----------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_2603_13605_b200 as pkg
+    from paper_2603_13605_b200.abi import Config, Pool
+
+    dev = local_rank
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream()
+    api = pkg.api()
+    wl = make_workload(args.seed + rank, args.workflows)
+    n = wl["n"]
+    req_blocks = int(blocks_of(wl["req_len"]).sum())
+    pin_blocks = int(blocks_of(wl["base"]).sum())
+    log(f"[rank {rank}] workload: {n} workflows, {len(wl['req_tok'])} request tokens, "
+        f"{req_blocks} request blocks")
+
+    # ---- metadata pool holding every workflow's pin -------------------------------------
+    mpb = int(blocks_of(wl["req_len"]).max()) + 1
+    nb = pin_blocks + 2 * mpb + 1024
+    tl = max(10, int(math.ceil(math.log2(2 * nb))) + 1)
+    pool = Pool(api, Config(max_workflows=n, n_blocks=nb, capacity_tokens=1 << 50,
+                            max_pin_blocks=mpb, table_log2=tl, device=dev))
+    wf_all = np.arange(n, dtype=np.int32)
+    t0 = time.perf_counter()
+    for c0 in range(0, n, 2000):
+        c1 = min(n, c0 + 2000)
+        off = wl["pin_off"][c0:c1 + 1] - wl["pin_off"][c0]
+        tok = wl["pin_tok"][wl["pin_off"][c0]:wl["pin_off"][c1]]
+        st = pool.commit(wf_all[c0:c1], off, tok)
+        assert st.all()
+    log(f"[rank {rank}] pinned {n} contexts ({pin_blocks} blocks) in {time.perf_counter() - t0:.1f}s")
+    api.check("set_stream", api.pool_set_stream(pool.h, C.c_void_p(stream.cuda_stream)))
+
+    d_wf = torch.from_numpy(wf_all).to(dev)
+    d_off = torch.from_numpy(wl["req_off"]).to(dev)
+    d_tok = torch.from_numpy(wl["req_tok"].view(np.int32)).to(dev)
+    d_M = torch.zeros(n, dtype=torch.int64, device=dev)
+    n_tokens = int(wl["req_off"][-1])
+    l2 = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def match_step():
+        api.check("match_dev", api.match_batch_dev(pool.h, n, C.c_void_p(d_wf.data_ptr()),
+                  C.c_void_p(d_off.data_ptr()), C.c_void_p(d_tok.data_ptr()), n_tokens,
+                  C.c_void_p(d_M.data_ptr()), None))
+
+    # correctness gate on the timed inputs: M must equal the construction's known LCP
+    match_step()
+    torch.cuda.synchronize()
+    M = d_M.cpu().numpy()
+    assert (M == wl["expect_M"]).all(), "match result differs from the workload's known LCP"
+
+    hbm_peak, peak_src = peaks()
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+    with ClockSampler(dev) as clk:
+        for _ in range(args.warmup):
+            l2.zero_()
+            match_step()
+        torch.cuda.synchronize()
+        if dist:
+            tdist.barrier()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        for s in range(args.steps):
+            l2.zero_()  # L2 flush between timed steps (not inside the events)
+            ev[s][0].record(stream)
+            match_step()
+            ev[s][1].record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            tdist.barrier()
+        step_ms = [a.elapsed_time(b) for a, b in ev]
+        ms = float(np.mean(step_ms))
+        if dist:
+            t = torch.tensor([ms], device=dev)
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            ms = float(t.item())
+
+        # ---- e2e through the host-pointer C ABI (pinned host buffers) --------------------
+        h_wf = torch.from_numpy(wf_all).pin_memory().numpy()
+        h_off = torch.from_numpy(wl["req_off"]).pin_memory().numpy()
+        h_tok = torch.from_numpy(wl["req_tok"].view(np.int32)).pin_memory().numpy().view(np.uint32)
+        h_M = torch.zeros(n, dtype=torch.int64).pin_memory().numpy()
+        api.check("set_stream", api.pool_set_stream(pool.h, None))  # private stream again
+
+        def e2e_step():
+            api.check("match", api.match_batch(pool.h, n, h_wf.ctypes.data, h_off.ctypes.data,
+                                               h_tok.ctypes.data, h_M.ctypes.data, None))
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        e2e_t = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            e2e_step()
+            e2e_t.append(time.perf_counter() - t0)
+        assert (h_M == wl["expect_M"]).all()
+        e2e_ms = 1e3 * float(np.mean(e2e_t))
+        if dist:
+            t = torch.tensor([e2e_ms], device=dev)
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+
+        kv = None if args.no_kv else kv_legs(args, api, dev, stream, hbm_peak, rank)
+    clocks = clk.summary()
+
+    # ---- roofline of the match kernel: algorithmic bytes of one launch --------------------
+    # per request block: 64 B tokens read (+8 B hash write is disabled in this step: out_hash=NULL)
+    # per overlapping pin block (k < pin blocks): 8 B pin hash; per verified block (prefix hash
+    # equal): 4 B block id + 64 B pin tokens. Per request: wf 4 B, tok_off 8 B, M 8 B, pin meta 12 B.
+    base_blocks = blocks_of(wl["base"])
+    verified = np.where(wl["expect_M"] < wl["base"], wl["expect_M"] // BT + 1, base_blocks)
+    verified = np.minimum(verified, base_blocks)
+    alg_bytes = (64 * req_blocks + 8 * int(base_blocks.sum()) + 68 * int(verified.sum())
+                 + 40 * n)
+    achieved = alg_bytes / (ms / 1e3) / 1e9
+    value = req_blocks * world / (ms / 1e3)
+    h2d = h_wf.nbytes + h_off.nbytes + 4 * n_tokens
+    d2h = h_M.nbytes
+    roof = {"bound": "hbm", "kernel": "match_kernel (+4 small scan/init launches in the step)",
+            "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+            "peak_source": peak_src, "alg_bytes_per_step": alg_bytes,
+            "alg_bytes_per_block": alg_bytes / req_blocks,
+            "traffic": args.traffic}
+    line = {"metric": METRIC, "value": value, "unit": "blocks/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (seeded token ids; KV payload random bytes)",
+            "config": config_dict(args, blocks_per_step=req_blocks, pin_blocks=pin_blocks),
+            "roofline": roof,
+            "e2e": {"value": req_blocks * world / (e2e_ms / 1e3), "unit": "blocks/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "ms_per_step": e2e_ms},
+            "gpu_launches": 6 * args.steps,
+            "clocks": clocks,
+            "step_ms_min_max": [min(step_ms), max(step_ms)]}
+    if kv:
+        line["kv"] = kv
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args)
+    pool.close()
+    return line
+
+
+def kv_legs(args, api, dev, stream, hbm_peak, rank):
+    """Llama-3-8B-shaped payload pool: gather of retained pins and a stage commit with COW."""
+    import torch
+
+    from paper_2603_13605_b200.abi import Config, Pool
+    n_wf, ctx = args.kv_workflows, args.kv_context
+    pool_blocks = args.kv_pool_gib * (1 << 30) // BLOCK_BYTES
+    cfg = Config(max_workflows=n_wf, n_blocks=pool_blocks, capacity_tokens=1 << 50,
+                 max_pin_blocks=(ctx + 512) // BT + 2, table_log2=int(math.log2(pool_blocks)) + 2,
+                 n_slabs=KV_SLABS, slab_row_bytes=KV_ROW, device=dev)
+    pool = Pool(api, cfg)
+    rng = np.random.default_rng(args.seed + 77 + rank)
+    tok_bytes = KV_SLABS * KV_ROW
+    chunk = max(1, (args.kv_staging_gib << 30) // (ctx * tok_bytes))
+    staging = torch.randint(0, 255, ((args.kv_staging_gib << 30),), dtype=torch.uint8, device=dev)
+    ctxs = [rng.integers(1, 1 << 30, size=ctx).astype(np.uint32) for _ in range(n_wf)]
+    from paper_2603_13605_b200.abi import csr
+    for c0 in range(0, n_wf, chunk):
+        ids = np.arange(c0, min(n_wf, c0 + chunk), dtype=np.int32)
+        off, tok = csr([ctxs[i] for i in ids])
+        kv_off = np.arange(len(ids), dtype=np.int64) * ctx * tok_bytes
+        st = pool.commit(ids, off, tok, kv_src=staging, kv_src_off=kv_off)
+        assert st.all()
+    api.check("set_stream", api.pool_set_stream(pool.h, C.c_void_p(stream.cuda_stream)))
+    # gather: G pins per step into contiguous staging [slab][token][row]
+    G = min(n_wf, max(1, (args.kv_staging_gib << 30) // (ctx * tok_bytes)))
+    gwf = torch.arange(G, dtype=torch.int32, device=dev)
+    goff = torch.arange(G, dtype=torch.int64, device=dev) * ctx * tok_bytes
+    l2 = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def gather():
+        api.check("gather", api.gather_dev(pool.h, G, C.c_void_p(gwf.data_ptr()),
+                                           C.c_void_p(staging.data_ptr()), C.c_void_p(goff.data_ptr())))
+    for _ in range(args.warmup):
+        gather()
+    times = []
+    for _ in range(args.steps):
+        l2.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        gather()
+        b.record(stream)
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+    g_ms = float(np.mean(times))
+    g_bytes = 2 * G * ctx * tok_bytes
+    g_gbs = g_bytes / (g_ms / 1e3) / 1e9
+    # stage commit: every workflow's next stage is its retained context plus a fresh A-token
+    # output (steady state: the previous stage's tail is replaced). The context is not block
+    # aligned, so the boundary block is copied on share (M % 16 rows from the old block) and the
+    # appended rows are scattered from staging; the old tail blocks are released.
+    A = args.kv_append
+    c_times, c_bytes = [], []
+    for it in range(args.warmup + args.steps):
+        ids = np.arange(n_wf, dtype=np.int32)
+        nxt = [np.concatenate([ctxs[i], rng.integers(1, 1 << 30, size=A).astype(np.uint32)]) for i in ids]
+        off, tok = csr(nxt)
+        M = np.array([len(c) for c in ctxs], dtype=np.int64)
+        kv_off = np.arange(n_wf, dtype=np.int64) * A * tok_bytes
+        d_wf = torch.from_numpy(ids).to(dev)
+        d_off = torch.from_numpy(off).to(dev)
+        d_tok = torch.from_numpy(tok.view(np.int32)).to(dev)
+        d_kvo = torch.from_numpy(kv_off).to(dev)
+        d_me = torch.from_numpy(M).to(dev)
+        d_st = torch.zeros(n_wf, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize()
+        l2.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        api.check("commit_dev", api.commit_batch_dev(
+            pool.h, n_wf, C.c_void_p(d_wf.data_ptr()), C.c_void_p(d_off.data_ptr()),
+            C.c_void_p(d_tok.data_ptr()), int(off[-1]), C.c_void_p(staging.data_ptr()),
+            C.c_void_p(d_kvo.data_ptr()), C.c_void_p(d_me.data_ptr()), C.c_void_p(d_st.data_ptr())))
+        b.record(stream)
+        torch.cuda.synchronize()
+        assert bool((d_st == 1).all()), "kv commit rejected"
+        # bytes: every row of every newly written block (from the boundary block M//16 on) is
+        # read once (COW rows from the old boundary block, the rest from staging) and written once
+        rows = sum(len(c) - BT * (int(m) // BT) for c, m in zip(nxt, M))
+        moved = 2 * rows * tok_bytes
+        if it >= args.warmup:
+            c_times.append(a.elapsed_time(b))
+            c_bytes.append(moved)
+    c_ms = float(np.mean(c_times))
+    c_gbs = float(np.mean(c_bytes)) / (c_ms / 1e3) / 1e9
+    pool.close()
+    del staging
+    return {"pool_gib": args.kv_pool_gib, "pool_blocks": pool_blocks,
+            "gather": {"pins_per_step": G, "tokens_per_pin": ctx, "bytes_per_step": g_bytes,
+                       "ms": g_ms, "gbps": g_gbs, "frac_of_hbm": g_gbs / hbm_peak},
+            "stage_commit": {"workflows": n_wf, "append_tokens": A, "bytes_per_step": float(np.mean(c_bytes)),
+                             "ms": c_ms, "gbps": c_gbs, "frac_of_hbm": c_gbs / hbm_peak,
+                             "note": "whole commit pipeline (metadata kernels + COW + scatter)"}}
+
+
+def cpu_baseline(args):
+    L = ref_lib()
+    n_sample = args.cpu_sample
+    wl = cpu_sample_workload(args.seed, n_sample)
+    if L is None:
+        return {"value": None, "unit": "blocks/s", "cores": 1, "kind": "port",
+                "sample": "oracle/_ref missing"}
+    sh = ref_shard(L, wl, list(range(n_sample)))
+    times, _ = time_ref(L, [sh], steps=3, warmup=1)
+    v = sh[2] / float(np.mean(times))
+    L.sfref_batch_destroy(sh[1])
+    L.sfref_pool_destroy(sh[0])
+    return {"value": v, "unit": "blocks/s", "cores": 1, "kind": "reference",
+            "sample": f"{n_sample} workflows of the same C2 distribution ({sh[2]} blocks), "
+                      "SimulatedBackend::prefix_match on pre-tokenized strings, 1 thread"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workflows", type=int, default=10_000)
+    ap.add_argument("--seed", type=int, default=0x0A1A + 2)
+    ap.add_argument("--no-kv", action="store_true")
+    ap.add_argument("--kv-pool-gib", type=int, default=64)
+    ap.add_argument("--kv-workflows", type=int, default=200)
+    ap.add_argument("--kv-context", type=int, default=2008)
+    ap.add_argument("--kv-append", type=int, default=40)
+    ap.add_argument("--kv-staging-gib", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1000)
+    ap.add_argument("--ref-sample", type=int, default=2000)
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per match launch (from profiles/), reported as-is")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.traffic is None:
+        tp = os.path.join(REPO, "profiles", "match_traffic.json")
+        if os.path.exists(tp):
+            args.traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    if args.impl == "reference":
+        rc = run_reference_arm(args, rank, world)
+    else:
+        line = run_ours(args, rank, world, local_rank)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        rc = 0
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.barrier()
+        tdist.destroy_process_group()
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())

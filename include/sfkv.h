@@ -15,7 +15,9 @@
  *   - Functions without the _dev suffix take HOST pointers: they copy inputs to the device,
  *     run the kernels and copy results back before returning (synchronous, like the reference's
  *     single-threaded calls). The _dev variants take DEVICE pointers on the pool's device and
- *     are asynchronous on the pool stream.
+ *     are asynchronous on the pool stream (no host synchronisation): they also take n_tokens,
+ *     the number of tokens the tok buffer can hold (>= tok_off[n]), which bounds the work size.
+ *     KV staging (kv_src) is always device memory, also in sfkv_commit_batch.
  *   - A workflow is a dense slot id in [0, max_workflows) chosen by the host (the host keeps the
  *     workflow_id string -> slot map, as SimulatedBackend keys pins_ by workflow_id,
  *     simulated_backend.hpp:115).
@@ -102,7 +104,7 @@ int sfkv_pool_kv(sfkv_pool* pool, void** kv, int64_t* block_bytes);
 int sfkv_match_batch(sfkv_pool* pool, int64_t n, const int32_t* wf, const int64_t* tok_off,
                      const uint32_t* tok, int64_t* out_M, uint64_t* out_hash);
 int sfkv_match_batch_dev(sfkv_pool* pool, int64_t n, const int32_t* wf, const int64_t* tok_off,
-                         const uint32_t* tok, int64_t* out_M, uint64_t* out_hash);
+                         const uint32_t* tok, int64_t n_tokens, int64_t* out_M, uint64_t* out_hash);
 
 /* ---- global lookup (new; cross-workflow dedup the reference lacks) -------------
  * For every block of every request (ceil(len/16) entries per request, request order): the id of
@@ -111,7 +113,7 @@ int sfkv_match_batch_dev(sfkv_pool* pool, int64_t n, const int32_t* wf, const in
 int sfkv_lookup_batch(sfkv_pool* pool, int64_t n, const int64_t* tok_off, const uint32_t* tok,
                       int32_t* out_block, int64_t* out_hit_tokens);
 int sfkv_lookup_batch_dev(sfkv_pool* pool, int64_t n, const int64_t* tok_off, const uint32_t* tok,
-                          int32_t* out_block, int64_t* out_hit_tokens);
+                          int64_t n_tokens, int32_t* out_block, int64_t* out_hit_tokens);
 
 /* ---- retain: replaces SimulatedBackend::pin_prompt (simulated_backend.cpp:135-151) ----------
  * Commits request r's tokens as the new pin of wf[r] (workflow slots distinct within a batch).
@@ -131,8 +133,9 @@ int sfkv_commit_batch(sfkv_pool* pool, int64_t n, const int32_t* wf, const int64
                       const uint32_t* tok, const void* kv_src, const int64_t* kv_src_off,
                       const int64_t* m_expected, int32_t* out_status);
 int sfkv_commit_batch_dev(sfkv_pool* pool, int64_t n, const int32_t* wf, const int64_t* tok_off,
-                          const uint32_t* tok, const void* kv_src, const int64_t* kv_src_off,
-                          const int64_t* m_expected, int32_t* out_status);
+                          const uint32_t* tok, int64_t n_tokens, const void* kv_src,
+                          const int64_t* kv_src_off, const int64_t* m_expected,
+                          int32_t* out_status);
 
 /* ---- evict: replaces SimulatedBackend::flush (simulated_backend.cpp:169-184) -----------------
  * wf = SFKV_FLUSH_ALL flushes every pin. *freed = tokens released (0 when nothing was pinned). */

@@ -45,9 +45,9 @@ uint64_t sfo_block_digest(uint64_t k, uint32_t n, const uint32_t* t) {
   return mix64(acc ^ mix64(k * 0xD6E8FEB86659FD93ull + n));
 }
 
-/* chain(k) = fin(sum_{i<=k} digest(i)); keys 0 and 1 are reserved (empty / tombstone). */
+/* chain(k) = fin(sum_{i<=k} digest(i) mod 2^62); keys 0 and 1 are reserved (empty / tombstone). */
 uint64_t sfo_chain_finalize(uint64_t s) {
-  uint64_t c = mix64(s ^ 0x5851F42D4C957F2Dull);
+  uint64_t c = mix64((s & ((1ull << 62) - 1)) ^ 0x5851F42D4C957F2Dull);
   return c < 2 ? c + 2 : c;
 }
 

@@ -82,9 +82,9 @@ GPU_ONLY = {
     "last_error": [],
     "pool_set_stream": [P, P],
     "pool_sync": [P],
-    "match_batch_dev": [P, i64, P, P, P, P, P],
-    "lookup_batch_dev": [P, i64, P, P, P, P],
-    "commit_batch_dev": [P, i64, P, P, P, P, P, P, P],
+    "match_batch_dev": [P, i64, P, P, P, i64, P, P],
+    "lookup_batch_dev": [P, i64, P, P, i64, P, P],
+    "commit_batch_dev": [P, i64, P, P, P, i64, P, P, P, P],
     "gather_dev": [P, i64, P, P, P],
 }
 ORACLE_ONLY = {

@@ -229,9 +229,9 @@ int sfkv_pool_kv(sfkv_pool* p, void** kv, int64_t* block_bytes) {
 // ---------------------------------------------------------------- lookup ------------------
 static int match_common(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
                         const uint32_t* tok, int64_t* out_M, uint64_t* out_hash, int32_t* out_block,
-                        int64_t* out_hit, int64_t n_items_host) {
+                        int64_t* out_hit, int64_t n_items_bound) {
   cudaStream_t st = p->stream;
-  int64_t n_items = n_items_host;
+  const int64_t n_items = n_items_bound;  // upper bound; kernels read the exact count on device
   Carver c0;
   const size_t o_blk = c0.take<int64_t>(n + 1), o_tmp = c0.take<int64_t>(scan_scratch_elems(n));
   if (int rc = p->small.ensure(c0.off)) return rc;
@@ -240,10 +240,6 @@ static int match_common(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_
   if (int rc = exclusive_scan(ReqBlocks{tok_off}, n, blk_off,
                               reinterpret_cast<int64_t*>(p->small.as<char>() + o_tmp), st))
     return rc;
-  if (n_items < 0) {
-    SFKV_CUDA(cudaMemcpyAsync(&n_items, blk_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SFKV_CUDA(cudaStreamSynchronize(st));
-  }
   Carver cv;
   const size_t o_tile = cv.take<int64_t>(match_tile_state_elems(n_items));
   if (int rc = p->scratch.ensure(cv.off)) return rc;
@@ -324,11 +320,12 @@ int sfkv_match_batch(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* 
 }
 
 int sfkv_match_batch_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
-                         const uint32_t* tok, int64_t* out_M, uint64_t* out_hash) {
-  if (!p || !wf || !tok_off || !tok || !out_M) return fail(SFKV_EINVAL, "match_batch_dev: null argument");
+                         const uint32_t* tok, int64_t n_tokens, int64_t* out_M, uint64_t* out_hash) {
+  if (!p || !wf || !tok_off || !tok || !out_M || n_tokens < 0)
+    return fail(SFKV_EINVAL, "match_batch_dev: bad argument");
   if (n <= 0) return n == 0 ? 0 : fail(SFKV_EINVAL, "negative batch");
   DeviceGuard g(p->cfg.device);
-  return match_common(p, n, wf, tok_off, tok, out_M, out_hash, nullptr, nullptr, -1);
+  return match_common(p, n, wf, tok_off, tok, out_M, out_hash, nullptr, nullptr, n + n_tokens / BT);
 }
 
 int sfkv_lookup_batch(sfkv_pool* p, int64_t n, const int64_t* tok_off, const uint32_t* tok,
@@ -356,11 +353,12 @@ int sfkv_lookup_batch(sfkv_pool* p, int64_t n, const int64_t* tok_off, const uin
 }
 
 int sfkv_lookup_batch_dev(sfkv_pool* p, int64_t n, const int64_t* tok_off, const uint32_t* tok,
-                          int32_t* out_block, int64_t* out_hit) {
-  if (!p || !tok_off || !tok || !out_block || !out_hit) return fail(SFKV_EINVAL, "lookup_batch_dev: null argument");
+                          int64_t n_tokens, int32_t* out_block, int64_t* out_hit) {
+  if (!p || !tok_off || !tok || !out_block || !out_hit || n_tokens < 0)
+    return fail(SFKV_EINVAL, "lookup_batch_dev: bad argument");
   if (n <= 0) return n == 0 ? 0 : fail(SFKV_EINVAL, "negative batch");
   DeviceGuard g(p->cfg.device);
-  return match_common(p, n, nullptr, tok_off, tok, nullptr, nullptr, out_block, out_hit, -1);
+  return match_common(p, n, nullptr, tok_off, tok, nullptr, nullptr, out_block, out_hit, n + n_tokens / BT);
 }
 
 // ---------------------------------------------------------------- retain ------------------
@@ -401,19 +399,23 @@ int sfkv_commit_batch(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t*
     dko = reinterpret_cast<int64_t*>(ex + o_ko);
     SFKV_CUDA(cudaMemcpyAsync(dko, kv_src_off, n * sizeof(int64_t), cudaMemcpyHostToDevice, p->stream));
   }
-  if (int rc = commit_dev(p, n, dwf, doff, dtok, kv_src, dko, dme, dst, nullptr, 0)) return rc;
+  if (int rc = commit_dev(p, n, dwf, doff, dtok, host_items(n, tok_off), kv_src, dko, dme, dst,
+                          nullptr, 0))
+    return rc;
   SFKV_CUDA(cudaMemcpyAsync(out_status, dst, n * sizeof(int32_t), cudaMemcpyDeviceToHost, p->stream));
   return check_sticky(p);
 }
 
 int sfkv_commit_batch_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
-                          const uint32_t* tok, const void* kv_src, const int64_t* kv_src_off,
-                          const int64_t* m_expected, int32_t* out_status) {
+                          const uint32_t* tok, int64_t n_tokens, const void* kv_src,
+                          const int64_t* kv_src_off, const int64_t* m_expected, int32_t* out_status) {
   if (!p || !wf || !tok_off || !tok || !out_status) return fail(SFKV_EINVAL, "commit_batch_dev: null argument");
   if (n <= 0) return n == 0 ? 0 : fail(SFKV_EINVAL, "negative batch");
   if (kv_src && (!kv_src_off || !p->kv)) return fail(SFKV_EINVAL, "commit_batch_dev: kv_src needs kv_src_off and a payload pool");
   DeviceGuard g(p->cfg.device);
-  return commit_dev(p, n, wf, tok_off, tok, kv_src, kv_src_off, m_expected, out_status, nullptr, 0);
+  if (n_tokens < 0) return fail(SFKV_EINVAL, "commit_batch_dev: negative n_tokens");
+  return commit_dev(p, n, wf, tok_off, tok, n + n_tokens / BT, kv_src, kv_src_off, m_expected,
+                    out_status, nullptr, 0);
 }
 
 // ---------------------------------------------------------------- evict -------------------
@@ -593,7 +595,7 @@ int sfkv_handoff(sfkv_pool* src, int32_t wf_src, sfkv_pool* dst, int32_t wf_dst,
     DeviceGuard gs(src->cfg.device);
     SFKV_CUDA(cudaStreamSynchronize(src->stream));
   }
-  if (int rc = commit_dev(dst, 1, dwf, doff, dtok, nullptr, nullptr, nullptr, dst_status,
+  if (int rc = commit_dev(dst, 1, dwf, doff, dtok, nb, nullptr, nullptr, nullptr, dst_status,
                           dst->kv ? src : nullptr, wf_src))
     return rc;
   SFKV_CUDA(cudaMemcpyAsync(status, dst_status, sizeof(int32_t), cudaMemcpyDeviceToHost, dst->stream));

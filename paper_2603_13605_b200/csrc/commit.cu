@@ -2,8 +2,8 @@
 // refcounts, deterministic allocation, capacity admission.
 //
 // Replaces SimulatedBackend::pin_prompt (simulated_backend.cpp:135-151) and ::flush (169-184).
-// A commit batch runs these launches on the pool stream (the batch semantics are defined in
-// oracle/sfkv_oracle.c, commit_impl):
+// A commit batch runs these launches on the pool stream with no host synchronisation (the batch
+// semantics are defined in oracle/sfkv_oracle.c, commit_impl):
 //   match      chained hashes of every block + M_r = LCP(old pin, tokens)           (match.cu)
 //   admit      one warp, request order: reject iff occ - old + new > capacity; warp-wide fast
 //              path when the whole 32-request chunk fits, exact sequential fallback otherwise
@@ -21,7 +21,8 @@
 //              leave the table (tombstone)
 //   install    new block tables / hashes / lengths
 // The batch is phase-ordered, so a block shared by an old and a new pin never transiently hits
-// a refcount of zero.
+// a refcount of zero. Scratch is sized by an item-count bound from the caller (token-buffer
+// size / 16 + requests); every kernel reads the exact count blk_off[n] on the device.
 #include "pool.cuh"
 
 namespace sfkv {
@@ -29,20 +30,20 @@ namespace sfkv {
 enum : uint8_t { CAT_NONE = 0, CAT_HIT = 1, CAT_DUP = 2, CAT_OWN = 3, CAT_PRIV = 4 };
 
 struct CommitScratch {
-  int64_t* blk_off;      // [n+1]
-  int64_t* M;            // [n]
-  uint64_t* hash;        // [items]
-  int64_t* tile_state;   // match look-back
-  int32_t* status;       // [n]
-  int64_t* slot_of;      // [items]
-  int32_t* bid;          // [items]
-  uint8_t* hit0;         // [items]
-  uint8_t* claim;        // [items]
-  uint8_t* cat;          // [items]
-  int64_t* first_nonhit; // [n]
-  int64_t* rank;         // [items+1]
-  int64_t* wprefix;      // [words+1]
-  int64_t* alloc_list;   // [items]
+  int64_t* blk_off;       // [n+1]
+  int64_t* M;             // [n]
+  uint64_t* hash;         // [items]
+  int64_t* tile_state;    // match look-back
+  int32_t* status;        // [n]
+  int64_t* slot_of;       // [items]
+  int32_t* bid;           // [items]
+  uint8_t* hit0;          // [items]
+  uint8_t* claim;         // [items]
+  uint8_t* cat;           // [items]
+  int64_t* first_nonhit;  // [n]
+  int64_t* rank;          // [items+1]
+  int64_t* wprefix;       // [words+1]
+  int64_t* alloc_list;    // [items]
   int64_t* scan_tmp;
 };
 
@@ -51,9 +52,9 @@ struct CommitArgs {
   const int32_t* wf;
   const int64_t* tok_off;
   const uint32_t* tok;
-  int64_t n_items;
+  int64_t n_items;  // upper bound (exact count: s.blk_off[n])
   const int64_t* m_expected;
-  int payload;               // 1 when KV bytes are written
+  int payload;  // 1 when KV bytes are written
   CommitScratch s;
   // pool
   int64_t* pin_len;
@@ -76,6 +77,11 @@ struct CommitArgs {
   int64_t capacity;
   DevCounters* ctr;
 };
+
+#define FOR_ITEMS(a, item)                                                         \
+  for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x,              \
+               n_items__ = (a).s.blk_off[(a).n];                                   \
+       item < n_items__; item += (int64_t)gridDim.x * blockDim.x)
 
 __device__ __forceinline__ void item_coords(const CommitArgs& a, int64_t item, int64_t& r,
                                             int64_t& k, int& nval) {
@@ -108,6 +114,12 @@ __device__ __forceinline__ bool blk_tokens_equal(const uint32_t* __restrict__ bl
 __global__ void admit_kernel(CommitArgs a) {
   const int lane = threadIdx.x;
   DevCounters* c = a.ctr;
+  if (lane == 0) {
+    c->error = 0;
+    c->occ_saved = c->occupancy;
+    c->rej_saved = c->rejections;
+  }
+  __syncwarp();
   // staleness / block-table checks first: a refused batch changes nothing
   bool bad_stale = false, bad_len = false;
   for (int64_t r = lane; r < a.n; r += 32) {
@@ -120,6 +132,7 @@ __global__ void admit_kernel(CommitArgs a) {
   if (bad_stale || bad_len) {
     const int code = bad_len ? SFKV_EPOOL : SFKV_ESTALE;
     for (int64_t r = lane; r < a.n; r += 32) a.s.status[r] = code;
+    __syncwarp();
     if (lane == 0) c->error = code;
     return;
   }
@@ -149,7 +162,7 @@ __global__ void admit_kernel(CommitArgs a) {
     } else {
       for (int j = 0; j < 32; ++j) {  // exact sequential rule (simulated_backend.cpp:141-150)
         const long long d = __shfl_sync(0xffffffffu, delta, j);
-        const bool aj = __shfl_sync(0xffffffffu, (int)act, j);
+        const int aj = __shfl_sync(0xffffffffu, (int)act, j);
         if (!aj) break;
         const bool ok = occ + d <= a.capacity;
         if (lane == j) a.s.status[r] = ok ? SFKV_PIN_ACCEPTED : SFKV_PIN_REJECTED;
@@ -166,8 +179,8 @@ __global__ void admit_kernel(CommitArgs a) {
 
 // ---- probe / claim ---------------------------------------------------------------------
 __global__ void probe_kernel(CommitArgs a) {
-  for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < a.n_items;
-       item += (int64_t)gridDim.x * blockDim.x) {
+  if (a.ctr->error) return;
+  FOR_ITEMS(a, item) {
     int64_t r, k;
     int nval;
     item_coords(a, item, r, k, nval);
@@ -207,8 +220,8 @@ __global__ void probe_kernel(CommitArgs a) {
 }
 
 __global__ void resolve_kernel(CommitArgs a) {
-  for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < a.n_items;
-       item += (int64_t)gridDim.x * blockDim.x) {
+  if (a.ctr->error) return;
+  FOR_ITEMS(a, item) {
     int64_t r, k;
     int nval;
     item_coords(a, item, r, k, nval);
@@ -233,18 +246,23 @@ __global__ void resolve_kernel(CommitArgs a) {
   }
 }
 
+// Runs over the whole bound so the rank scan can use it as its length.
 __global__ void categorize_kernel(CommitArgs a) {
+  const int64_t NI = a.s.blk_off[a.n];
+  const bool err = a.ctr->error != 0;
   for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < a.n_items;
        item += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = upper_index(a.s.blk_off, a.n, item);
-    const int64_t k = item - a.s.blk_off[r];
     uint8_t cat = CAT_NONE;
-    if (a.s.status[r] == SFKV_PIN_ACCEPTED) {
-      if (k < a.s.first_nonhit[r]) {
-        cat = a.s.hit0[item] ? CAT_HIT : CAT_DUP;
-      } else {
-        const bool own = a.s.claim[item] && a.towner[a.s.slot_of[item]] == item;
-        cat = own ? CAT_OWN : CAT_PRIV;
+    if (item < NI && !err) {
+      const int64_t r = upper_index(a.s.blk_off, a.n, item);
+      const int64_t k = item - a.s.blk_off[r];
+      if (a.s.status[r] == SFKV_PIN_ACCEPTED) {
+        if (k < a.s.first_nonhit[r]) {
+          cat = a.s.hit0[item] ? CAT_HIT : CAT_DUP;
+        } else {
+          const bool own = a.s.claim[item] && a.towner[a.s.slot_of[item]] == item;
+          cat = own ? CAT_OWN : CAT_PRIV;
+        }
       }
     }
     a.s.cat[item] = cat;
@@ -253,19 +271,14 @@ __global__ void categorize_kernel(CommitArgs a) {
 
 struct NeedAlloc {
   const uint8_t* cat;
-  __device__ int64_t operator()(int64_t i) const { return (cat[i] == CAT_OWN || cat[i] == CAT_PRIV) ? 1 : 0; }
+  __device__ int64_t operator()(int64_t i) const {
+    return (cat[i] == CAT_OWN || cat[i] == CAT_PRIV) ? 1 : 0;
+  }
 };
 struct FreeCount {
   const uint32_t* bits;
   __device__ int64_t operator()(int64_t i) const { return __popc(bits[i]); }
 };
-struct PinBlocks {
-  const int32_t* wf;
-  const int64_t* pin_len;
-  const int32_t* pin_nblk;
-  __device__ int64_t operator()(int64_t i) const { return pin_len[wf[i]] < 0 ? 0 : pin_nblk[wf[i]]; }
-};
-
 
 __device__ __forceinline__ int select_bit(uint32_t w, int r) {  // position of the r-th set bit
   for (int b = 0; b < 32; ++b) {
@@ -278,9 +291,13 @@ __device__ __forceinline__ int select_bit(uint32_t w, int r) {  // position of t
 }
 
 __global__ void alloc_kernel(CommitArgs a) {
+  if (a.ctr->error) return;
   const int64_t total_free = a.s.wprefix[a.n_words];
-  for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < a.n_items;
-       item += (int64_t)gridDim.x * blockDim.x) {
+  if (a.s.rank[a.n_items] > total_free) {  // exhausted: abort before any block is touched
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctr->error = SFKV_EPOOL;
+    return;
+  }
+  FOR_ITEMS(a, item) {
     const uint8_t cat = a.s.cat[item];
     if (cat != CAT_OWN && cat != CAT_PRIV) continue;
     const int64_t rk = a.s.rank[item];
@@ -293,7 +310,7 @@ __global__ void alloc_kernel(CommitArgs a) {
     const int32_t id = (int32_t)(w * 32 + bit);
     a.s.alloc_list[rk] = item;
     a.s.bid[item] = id;
-    atomicAnd(&a.free_bits[w], ~(1u << bit));
+    // the free bit is cleared by refs_kernel: selection must see the pre-batch bitmap
     int64_t r, k;
     int nval;
     item_coords(a, item, r, k, nval);
@@ -320,24 +337,24 @@ __global__ void alloc_kernel(CommitArgs a) {
 }
 
 __global__ void refs_kernel(CommitArgs a) {
-  for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < a.n_items;
-       item += (int64_t)gridDim.x * blockDim.x) {
+  if (a.ctr->error) return;
+  FOR_ITEMS(a, item) {
     const uint8_t cat = a.s.cat[item];
     if (cat == CAT_NONE) continue;
     int32_t id = a.s.bid[item];
     if (cat == CAT_DUP) {
       id = a.slots[a.s.slot_of[item]].val;
       a.s.bid[item] = id;
+    } else if (cat == CAT_OWN || cat == CAT_PRIV) {
+      atomicAnd(&a.free_bits[id >> 5], ~(1u << (id & 31)));
     }
     atomicAdd(&a.blk_ref[id], 1u);
   }
 }
 
 __global__ void clear_owner_kernel(CommitArgs a) {
-  for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < a.n_items;
-       item += (int64_t)gridDim.x * blockDim.x) {
+  FOR_ITEMS(a, item) {
     if (a.s.claim[item]) a.towner[a.s.slot_of[item]] = NO_OWNER;
-    // a claimed slot whose key never got a block (cannot happen: the owner is always OWN)
   }
 }
 
@@ -359,10 +376,10 @@ __device__ __forceinline__ void release_block(const CommitArgs& a, int32_t id) {
 // One warp per request: release the old pin; install the new length (commit) or none (flush).
 __global__ void release_kernel(CommitArgs a, int mode /*0 commit, 1 flush list, 2 flush all*/,
                                int64_t* out_freed) {
+  if (mode == 0 && a.ctr->error) return;
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t count = mode == 2 ? a.n : a.n;
-  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < count; r += warps) {
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < a.n; r += warps) {
     if (mode == 0 && a.s.status[r] != SFKV_PIN_ACCEPTED) continue;
     const int32_t w = mode == 2 ? (int32_t)r : a.wf[r];
     const int64_t pl = a.pin_len[w];
@@ -388,9 +405,25 @@ __global__ void release_kernel(CommitArgs a, int mode /*0 commit, 1 flush list, 
   }
 }
 
+// A batch that aborted after admission (physical pool or table exhausted) leaves the pool as it
+// was: pins, blocks and refcounts are untouched by then; the admission counters roll back and
+// every request reports the error. Claimed-but-unfilled table keys are reclaimed by the next
+// batch that probes them (they read as in-batch claims).
+__global__ void commit_finish_kernel(CommitArgs a) {
+  const int err = a.ctr->error;
+  if (err != SFKV_EPOOL) return;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < a.n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    a.s.status[r] = SFKV_EPOOL;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.ctr->occupancy = a.ctr->occ_saved;
+    a.ctr->rejections = a.ctr->rej_saved;
+  }
+}
+
 __global__ void install_kernel(CommitArgs a) {
-  for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < a.n_items;
-       item += (int64_t)gridDim.x * blockDim.x) {
+  if (a.ctr->error) return;
+  FOR_ITEMS(a, item) {
     if (a.s.cat[item] == CAT_NONE) continue;
     const int64_t r = upper_index(a.s.blk_off, a.n, item);
     const int64_t k = item - a.s.blk_off[r];
@@ -435,10 +468,6 @@ __global__ void rebuild_done_kernel(DevCounters* c, const int* flag) {
 }
 
 // ---------------------------------------------------------------------------------------
-int launch_commit_payload(sfkv_pool* p, const CommitArgs& a, const void* kv_src,
-                          const int64_t* kv_src_off, const sfkv_pool* src_pool, int32_t src_wf,
-                          cudaStream_t st);
-
 static CommitArgs base_args(sfkv_pool* p) {
   CommitArgs a{};
   a.pin_len = p->pin_len;
@@ -487,33 +516,42 @@ int maybe_rebuild_table(sfkv_pool* p) {
   return 0;
 }
 
+static int launch_commit_payload(sfkv_pool* p, const CommitArgs& a, const void* kv_src,
+                                 const int64_t* kv_src_off, const sfkv_pool* src_pool,
+                                 int32_t src_wf, cudaStream_t st) {
+  PayloadJob j;
+  j.n = a.n;
+  j.wf = a.wf;
+  j.tok_off = a.tok_off;
+  j.blk_off = a.s.blk_off;
+  j.M = a.s.M;
+  j.rank = a.s.rank;
+  j.alloc_list = a.s.alloc_list;
+  j.bid = a.s.bid;
+  j.n_items = a.n_items;  // rank[bound] = number of new blocks
+  j.old_pin_blk = p->pin_blk;
+  j.max_pin_blocks = p->cfg.max_pin_blocks;
+  j.error = &p->ctr->error;
+  return launch_payload(p, j, kv_src, kv_src_off, src_pool, src_wf, st);
+}
+
 int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
-               const uint32_t* tok, const void* kv_src, const int64_t* kv_src_off,
-               const int64_t* m_expected, int32_t* out_status, const sfkv_pool* src_pool,
-               int32_t src_wf) {
+               const uint32_t* tok, int64_t n_items_bound, const void* kv_src,
+               const int64_t* kv_src_off, const int64_t* m_expected, int32_t* out_status,
+               const sfkv_pool* src_pool, int32_t src_wf) {
   if (n <= 0) return 0;
   cudaStream_t st = p->stream;
-  // Blocks per request first: the item count sizes the scratch (one 8-B D2H on the stream).
-  Carver c0;
-  const size_t o_blk = c0.take<int64_t>(n + 1), o_tmp0 = c0.take<int64_t>(scan_scratch_elems(n));
-  if (int rc = p->small.ensure(c0.off)) return rc;
-  int64_t* blk_off = reinterpret_cast<int64_t*>(p->small.as<char>() + o_blk);
-  if (int rc = exclusive_scan(ReqBlocks{tok_off}, n, blk_off,
-                              reinterpret_cast<int64_t*>(p->small.as<char>() + o_tmp0), st))
-    return rc;
-  int64_t n_items = 0;
-  SFKV_CUDA(cudaMemcpyAsync(&n_items, blk_off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  SFKV_CUDA(cudaStreamSynchronize(st));
+  const int64_t ni = n_items_bound > 0 ? n_items_bound : 1;
   Carver cv;
-  const int64_t ni = n_items > 0 ? n_items : 1;
-  const size_t o_M = cv.take<int64_t>(n), o_hash = cv.take<uint64_t>(ni),
-               o_tile = cv.take<int64_t>(match_tile_state_elems(ni)), o_st = cv.take<int32_t>(n),
-               o_slot = cv.take<int64_t>(ni), o_bid = cv.take<int32_t>(ni),
-               o_hit = cv.take<uint8_t>(ni), o_claim = cv.take<uint8_t>(ni),
-               o_cat = cv.take<uint8_t>(ni), o_fnh = cv.take<int64_t>(n),
-               o_rank = cv.take<int64_t>(ni + 1), o_wp = cv.take<int64_t>(p->n_words + 1),
-               o_al = cv.take<int64_t>(ni),
-               o_tmp = cv.take<int64_t>(scan_scratch_elems(ni > p->n_words ? ni : p->n_words));
+  const size_t o_blk = cv.take<int64_t>(n + 1), o_M = cv.take<int64_t>(n),
+               o_hash = cv.take<uint64_t>(ni), o_tile = cv.take<int64_t>(match_tile_state_elems(ni)),
+               o_st = cv.take<int32_t>(n), o_slot = cv.take<int64_t>(ni),
+               o_bid = cv.take<int32_t>(ni), o_hit = cv.take<uint8_t>(ni),
+               o_claim = cv.take<uint8_t>(ni), o_cat = cv.take<uint8_t>(ni),
+               o_fnh = cv.take<int64_t>(n), o_rank = cv.take<int64_t>(ni + 1),
+               o_wp = cv.take<int64_t>(p->n_words + 1), o_al = cv.take<int64_t>(ni),
+               o_tmp = cv.take<int64_t>(scan_scratch_elems(ni > p->n_words ? ni : p->n_words) +
+                                        scan_scratch_elems(n));
   if (int rc = p->scratch.ensure(cv.off)) return rc;
   char* base = p->scratch.as<char>();
   CommitArgs a = base_args(p);
@@ -523,8 +561,8 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   a.tok = tok;
   a.m_expected = m_expected;
   a.payload = (p->kv && (kv_src || src_pool)) ? 1 : 0;
-  a.n_items = n_items;
-  a.s.blk_off = blk_off;
+  a.n_items = ni;
+  a.s.blk_off = reinterpret_cast<int64_t*>(base + o_blk);
   a.s.M = reinterpret_cast<int64_t*>(base + o_M);
   a.s.hash = reinterpret_cast<uint64_t*>(base + o_hash);
   a.s.tile_state = reinterpret_cast<int64_t*>(base + o_tile);
@@ -540,40 +578,42 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   a.s.alloc_list = reinterpret_cast<int64_t*>(base + o_al);
   a.s.scan_tmp = reinterpret_cast<int64_t*>(base + o_tmp);
 
-  // 1. chained hashes, M = LCP(old pin, tokens)
+  // 1. blocks per request, chained hashes, M = LCP(old pin, tokens)
+  if (int rc = exclusive_scan(ReqBlocks{tok_off}, n, a.s.blk_off, a.s.scan_tmp, st)) return rc;
   MatchArgs m{};
   m.n = n;
   m.wf = wf;
   m.tok_off = tok_off;
   m.tok = tok;
-  m.blk_off = blk_off;
-  m.n_items = n_items;
+  m.blk_off = a.s.blk_off;
+  m.n_items = ni;
   m.out_M = a.s.M;
   m.out_hash = a.s.hash;
   if (int rc = launch_match(p, m, a.s.tile_state, st)) return rc;
-  // 2. admission
-  SFKV_CUDA(cudaMemsetAsync(&p->ctr->error, 0, sizeof(int), st));
+  // 2. admission, classification, allocation, references
   admit_kernel<<<1, 32, 0, st>>>(a);
   SFKV_LAUNCH_CHECK("admit_kernel");
   const int sms = sm_count_c();
-  const int g = grid_for(n_items, 256, sms * 8);
-  if (n_items > 0) {
-    probe_kernel<<<g, 256, 0, st>>>(a);
-    resolve_kernel<<<g, 256, 0, st>>>(a);
-    categorize_kernel<<<g, 256, 0, st>>>(a);
-    SFKV_LAUNCH_CHECK("probe/resolve/categorize");
-    if (int rc = exclusive_scan(NeedAlloc{a.s.cat}, n_items, a.s.rank, a.s.scan_tmp, st)) return rc;
-    if (int rc = exclusive_scan(FreeCount{p->free_bits}, p->n_words, a.s.wprefix, a.s.scan_tmp, st)) return rc;
-    alloc_kernel<<<g, 256, 0, st>>>(a);
-    refs_kernel<<<g, 256, 0, st>>>(a);
-    clear_owner_kernel<<<g, 256, 0, st>>>(a);
-    SFKV_LAUNCH_CHECK("alloc/refs");
-    if (a.payload) {
-      if (int rc = launch_commit_payload(p, a, kv_src, kv_src_off, src_pool, src_wf, st)) return rc;
-    }
+  const int g = grid_for(ni, 256, sms * 8);
+  probe_kernel<<<g, 256, 0, st>>>(a);
+  resolve_kernel<<<g, 256, 0, st>>>(a);
+  categorize_kernel<<<g, 256, 0, st>>>(a);
+  SFKV_LAUNCH_CHECK("probe/resolve/categorize");
+  if (int rc = exclusive_scan(NeedAlloc{a.s.cat}, ni, a.s.rank, a.s.scan_tmp, st)) return rc;
+  if (int rc = exclusive_scan(FreeCount{p->free_bits}, p->n_words, a.s.wprefix, a.s.scan_tmp, st))
+    return rc;
+  alloc_kernel<<<g, 256, 0, st>>>(a);
+  refs_kernel<<<g, 256, 0, st>>>(a);
+  clear_owner_kernel<<<g, 256, 0, st>>>(a);
+  SFKV_LAUNCH_CHECK("alloc/refs");
+  // 3. payload (copy-on-share + staging scatter / handoff pull)
+  if (a.payload) {
+    if (int rc = launch_commit_payload(p, a, kv_src, kv_src_off, src_pool, src_wf, st)) return rc;
   }
+  // 4. release old pins, install new ones
   release_kernel<<<grid_for(n * 32, 256, sms * 8), 256, 0, st>>>(a, 0, nullptr);
-  if (n_items > 0) install_kernel<<<g, 256, 0, st>>>(a);
+  install_kernel<<<g, 256, 0, st>>>(a);
+  commit_finish_kernel<<<grid_for(n, 256, sms), 256, 0, st>>>(a);
   SFKV_LAUNCH_CHECK("release/install");
   return maybe_rebuild_table(p);
 }
@@ -590,25 +630,4 @@ int flush_dev(sfkv_pool* p, int64_t n, const int32_t* wf, int64_t* out_freed, bo
   return maybe_rebuild_table(p);
 }
 
-
-int launch_payload(sfkv_pool* p, const PayloadJob& j, const void* kv_src, const int64_t* kv_src_off,
-                   const sfkv_pool* src_pool, int32_t src_wf, cudaStream_t st);
-
-int launch_commit_payload(sfkv_pool* p, const CommitArgs& a, const void* kv_src,
-                          const int64_t* kv_src_off, const sfkv_pool* src_pool, int32_t src_wf,
-                          cudaStream_t st) {
-  PayloadJob j;
-  j.n = a.n;
-  j.wf = a.wf;
-  j.tok_off = a.tok_off;
-  j.blk_off = a.s.blk_off;
-  j.M = a.s.M;
-  j.rank = a.s.rank;
-  j.alloc_list = a.s.alloc_list;
-  j.bid = a.s.bid;
-  j.n_items = a.n_items;
-  j.old_pin_blk = p->pin_blk;
-  j.max_pin_blocks = p->cfg.max_pin_blocks;
-  return launch_payload(p, j, kv_src, kv_src_off, src_pool, src_wf, st);
-}
 }  // namespace sfkv

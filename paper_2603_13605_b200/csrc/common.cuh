@@ -40,8 +40,11 @@ __host__ __device__ __forceinline__ uint64_t block_digest_words(uint64_t k, uint
   return mix64(acc ^ mix64(k * 0xD6E8FEB86659FD93ull + n));
 }
 
+// The chain sum is taken mod 2^62 so a look-back status word can carry it next to a 2-bit flag.
+constexpr uint64_t CHAIN_MASK = (1ull << 62) - 1;
+
 __host__ __device__ __forceinline__ uint64_t chain_finalize(uint64_t s) {
-  uint64_t c = mix64(s ^ 0x5851F42D4C957F2Dull);
+  uint64_t c = mix64((s & CHAIN_MASK) ^ 0x5851F42D4C957F2Dull);
   return c < 2 ? c + 2 : c;
 }
 

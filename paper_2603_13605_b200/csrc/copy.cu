@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(256) payload_kernel(PayloadKernelArgs P) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if (*j.error) return;
   const int64_t total = j.rank[j.n_items] * P.n_slabs;
   for (int64_t u = warp; u < total; u += nwarps) {
     const int64_t a = u / P.n_slabs;

@@ -14,12 +14,15 @@
 //             LCP independent of hash collisions (M is pre-set to min(P, pin_len)).
 //   lookup  : probe the global table for c_k (full blocks), verify tokens, report the block id.
 //
-// Data movement: one thread per block. When the request's token span starts 16-B aligned (the
-// host packer guarantees it; any CSR is accepted) a thread loads its 64-B block with four 16-B
-// vector loads; a warp's loads cover 2 KiB of contiguous tokens, so DRAM sectors are fully used
-// (L1 merges the halves). Algorithmic bytes per block: 64 B tokens + 8 B hash out, + 8 B pin hash
-// (+ 4 B block id + 64 B pin tokens when verified) in match mode, + 16 B slot (+ 64 B verify) in
-// lookup mode. No tensor cores: this is integer hashing and compares.
+// Data movement: one thread per block, 256-block tiles claimed in order by persistent CTAs. A
+// tile's request metadata (block/token offsets, workflow slot, pin length and block count) is
+// staged in shared memory by all threads at once from a precomputed tile -> first-request table,
+// so no thread walks global memory serially. A thread loads its 64-B block with 16-B vector
+// loads at any alignment (a warp covers 2 KiB of contiguous tokens; L1 merges the halves) and
+// issues its pin-hash / block-id loads before the tile scan so their latency overlaps the
+// look-back. Algorithmic bytes per block: 64 B tokens (+8 B hash out when requested), + 8 B pin
+// hash for blocks inside the pin, + 4 B block id + 64 B pin tokens when verified; lookup mode:
+// + 16 B table slot (+ 64 B verify). HBM-bound integer work: no tensor cores.
 #include "pool.cuh"
 
 namespace sfkv {
@@ -36,9 +39,10 @@ struct SegOp {
   }
 };
 
+// counter + per-tile {status word, first request}
 size_t match_tile_state_elems(int64_t n_items) {
   int64_t ntiles = (n_items + MT - 1) / MT;
-  return (size_t)(1 + 3 * ntiles);
+  return (size_t)(1 + 2 * ntiles);
 }
 
 struct MatchKernelArgs {
@@ -52,12 +56,23 @@ struct MatchKernelArgs {
   const Slot* slots;
   uint64_t slot_mask;
   int32_t max_pin_blocks;
-  int64_t ntiles;
+  int64_t ntiles;  // bound
   unsigned long long* counter;
-  volatile int64_t* flag;
-  volatile uint64_t* agg;
-  volatile uint64_t* incl;
+  uint64_t* status;  // per tile: 0 = pending, ST_AGG | aggregate, ST_INCL | inclusive prefix
+  const int64_t* tile_r0;
 };
+
+constexpr uint64_t ST_AGG = 1ull << 62;
+constexpr uint64_t ST_INCL = 2ull << 62;
+
+__device__ __forceinline__ void st_status(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ void load16_aligned(const uint32_t* __restrict__ p, uint32_t* t) {
   const uint4* q = reinterpret_cast<const uint4*>(p);
@@ -120,62 +135,117 @@ __device__ __forceinline__ bool tokens_equal(const uint32_t* a, const uint32_t* 
   return eq;
 }
 
-__global__ void __launch_bounds__(MT) match_kernel(MatchKernelArgs K) {
+// tile_r0[t] = the request holding item t*MT (tiles whose first item lies in request r).
+__global__ void tile_first_kernel(const int64_t* __restrict__ blk_off, int64_t n,
+                                  int64_t* __restrict__ tile_r0) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b0 = blk_off[r], b1 = blk_off[r + 1];
+    for (int64_t t = (b0 + MT - 1) / MT; t * MT < b1; ++t) tile_r0[t] = r;
+  }
+}
+
+__global__ void __launch_bounds__(MT, 4) match_kernel(MatchKernelArgs K) {
   using BS = cub::BlockScan<SegPair, MT>;
   __shared__ typename BS::TempStorage tmp;
-  __shared__ int64_t s_off[MT + 1];
-  __shared__ int64_t s_tile, s_r0;
+  __shared__ int64_t s_off[MT + 1];   // blk_off of the tile's request window
+  __shared__ int64_t s_toff[MT + 1];  // tok_off
+  __shared__ int64_t s_pl[MT];        // pin length (-1: none)
+  __shared__ int32_t s_wf[MT];
+  __shared__ int32_t s_pnb[MT];
+  __shared__ int64_t s_tile;
   __shared__ uint64_t s_prefix;
 
   const MatchArgs& A = K.a;
   const int tid = threadIdx.x;
+  const bool match_mode = A.out_M != nullptr;
   const int64_t tok_total = A.tok_off[A.n];
+  // A.n_items is only an upper bound (it sizes the look-back state); the exact count is on device.
+  const int64_t n_items = A.blk_off[A.n];
+  const int64_t ntiles = (n_items + MT - 1) / MT;
 
   for (;;) {
+    // Take the ticket only when starting the tile: a held-but-unstarted ticket would make every
+    // later tile's look-back wait on it.
     if (tid == 0) s_tile = (int64_t)atomicAdd(K.counter, 1ull);
     __syncthreads();
     const int64_t tile = s_tile;
-    if (tile >= K.ntiles) break;
+    if (tile >= ntiles) break;
     const int64_t item0 = tile * MT;
     const int64_t item = item0 + tid;
-    const bool valid = item < A.n_items;
+    const bool valid = item < n_items;
 
-    // ---- request of each item: window of blk_off in smem, binary search ----
-    if (tid == 0) s_r0 = upper_index(A.blk_off, A.n, item0);
-    __syncthreads();
-    const int64_t r0 = s_r0;
-    for (int j = tid; j <= MT; j += MT) {
-      int64_t rr = r0 + j;
-      s_off[j] = rr <= A.n ? A.blk_off[rr] : INT64_MAX;
+    // ---- stage the request window [r0, r0 + MT] (all threads in parallel) ----
+    const int64_t r0 = K.tile_r0[tile];
+    {
+      const int64_t rr = r0 + tid;
+      s_off[tid] = rr <= A.n ? A.blk_off[rr] : INT64_MAX;
+      s_toff[tid] = rr <= A.n ? A.tok_off[rr] : 0;
+      if (match_mode && rr < A.n) {
+        const int32_t w = A.wf[rr];
+        const int64_t pl = K.pin_len[w];
+        s_wf[tid] = w;
+        s_pl[tid] = pl;
+        s_pnb[tid] = pl < 0 ? 0 : K.pin_nblk[w];
+      }
+      if (tid == 0) {
+        const int64_t re = r0 + MT;
+        s_off[MT] = re <= A.n ? A.blk_off[re] : INT64_MAX;
+        s_toff[MT] = re <= A.n ? A.tok_off[re] : 0;
+      }
     }
     __syncthreads();
-    int64_t r = r0;
+
+    // ---- my block: request (smem binary search), tokens, early pin loads ----
+    int64_t r = r0, k = 0, tb = 0, te = 0;
+    int32_t w = 0, pnb = 0;
+    int64_t pl = -1;
     if (valid) {
-      if (s_off[MT] <= item) {  // > MT requests in this tile (empty requests): global search
+      if (s_off[MT] <= item) {  // > MT requests in this tile (empty requests): global path
         r = upper_index(A.blk_off, A.n, item);
+        k = item - A.blk_off[r];
+        tb = A.tok_off[r];
+        te = A.tok_off[r + 1];
+        if (match_mode) {
+          w = A.wf[r];
+          pl = K.pin_len[w];
+          pnb = pl < 0 ? 0 : K.pin_nblk[w];
+        }
       } else {
         int lo = 0, hi = MT;  // s_off[lo] <= item < s_off[hi]
         while (hi - lo > 1) {
-          int mid = (lo + hi) >> 1;
+          const int mid = (lo + hi) >> 1;
           if (s_off[mid] <= item) lo = mid;
           else hi = mid;
         }
         r = r0 + lo;
+        k = item - s_off[lo];
+        tb = s_toff[lo];
+        te = s_toff[lo + 1];
+        if (match_mode) {
+          w = s_wf[lo];
+          pl = s_pl[lo];
+          pnb = s_pnb[lo];
+        }
       }
     }
-    int64_t k = 0, start = 0;
-    int nval = 0;
+    const int64_t rem = te - tb - k * BT;
+    const int nval = valid ? (int)(rem < BT ? rem : BT) : 0;
     uint32_t t[BT];
     if (valid) {
-      k = item - A.blk_off[r];
-      const int64_t tb = A.tok_off[r];
-      const int64_t rem = A.tok_off[r + 1] - tb - k * BT;
-      nval = (int)(rem < BT ? rem : BT);
-      start = tb + k * BT;
-      load_block(A.tok, start, nval, tok_total, t);
+      load_block(A.tok, tb + k * BT, nval, tok_total, t);
     } else {
 #pragma unroll
       for (int j = 0; j < BT; ++j) t[j] = 0u;
+    }
+    // pin metadata needed after the scan, issued now so its latency overlaps the look-back
+    const bool in_pin = match_mode && valid && pl >= 0 && k < pnb;
+    const int64_t pb = (int64_t)w * K.max_pin_blocks;
+    uint64_t prev_pin_hash = 0;
+    int32_t pin_id = 0;
+    if (in_pin) {
+      if (k > 0) prev_pin_hash = __ldg(K.pin_hash + pb + k - 1);
+      pin_id = __ldg(K.pin_blk + pb + k);
     }
     const uint64_t g = valid ? block_digest_words((uint64_t)k, (uint32_t)nval, t) : 0ull;
 
@@ -184,37 +254,22 @@ __global__ void __launch_bounds__(MT) match_kernel(MatchKernelArgs K) {
     SegPair out, total;
     BS(tmp).InclusiveScan(in, out, SegOp(), total);
     if (tid == 0) {
+      // status word = flag << 62 | (sum mod 2^62): one relaxed 64-bit store / load, no fences.
       uint64_t prefix = 0;
-      if (total.h) {
-        K.incl[tile] = total.v;
-        __threadfence();
-        K.flag[tile] = 2;
-      } else {
-        K.agg[tile] = total.v;
-        __threadfence();
-        K.flag[tile] = 1;
-      }
+      st_status(K.status + tile, (total.h ? ST_INCL : ST_AGG) | (total.v & CHAIN_MASK));
       if (!in.h && tile > 0) {
         int64_t pred = tile - 1;
         for (;;) {
-          int64_t f;
+          uint64_t s;
           do {
-            f = K.flag[pred];
-          } while (f == 0);
-          __threadfence();
-          if (f == 2) {
-            prefix += K.incl[pred];
-            break;
-          }
-          prefix += K.agg[pred];
+            s = ld_status(K.status + pred);
+          } while (s == 0);
+          prefix += s & CHAIN_MASK;
+          if ((s & ~CHAIN_MASK) == ST_INCL) break;
           --pred;
         }
       }
-      if (!total.h) {
-        K.incl[tile] = prefix + total.v;
-        __threadfence();
-        K.flag[tile] = 2;
-      }
+      if (!total.h) st_status(K.status + tile, ST_INCL | ((prefix + total.v) & CHAIN_MASK));
       s_prefix = prefix;
     }
     __syncthreads();
@@ -223,29 +278,23 @@ __global__ void __launch_bounds__(MT) match_kernel(MatchKernelArgs K) {
 
     if (valid) {
       if (A.out_hash) A.out_hash[item] = c;
-      if (A.out_M) {  // ---- pin compare (match / commit) ----
-        const int32_t w = A.wf[r];
-        const int64_t pl = K.pin_len[w];
-        if (pl >= 0 && k < K.pin_nblk[w]) {
-          const int64_t pb = (int64_t)w * K.max_pin_blocks;
-          const bool prev_ok = (k == 0) || (chain_finalize(S - g) == K.pin_hash[pb + k - 1]);
-          if (prev_ok) {
-            const int32_t id = K.pin_blk[pb + k];
-            const int pn = K.blk_n[id];
-            uint32_t q[BT];
-            load16_aligned(K.blk_tok + (int64_t)id * BT, q);
-            const int lim = nval < pn ? nval : pn;
-            int tt = 0;
-            bool run = true;
+      if (in_pin) {  // ---- pin compare (match / commit) ----
+        const bool prev_ok = (k == 0) || (chain_finalize(S - g) == prev_pin_hash);
+        if (prev_ok) {
+          const int pn = K.blk_n[pin_id];
+          uint32_t q[BT];
+          load16_aligned(K.blk_tok + (int64_t)pin_id * BT, q);
+          const int lim = nval < pn ? nval : pn;
+          int tt = 0;
+          bool run = true;
 #pragma unroll
-            for (int j = 0; j < BT; ++j) {
-              run = run && j < lim && q[j] == t[j];
-              tt += run ? 1 : 0;
-            }
-            if (tt < lim)
-              atomicMin(reinterpret_cast<unsigned long long*>(A.out_M + r),
-                        (unsigned long long)(k * BT + tt));
+          for (int j = 0; j < BT; ++j) {
+            run = run && j < lim && q[j] == t[j];
+            tt += run ? 1 : 0;
           }
+          if (tt < lim)
+            atomicMin(reinterpret_cast<unsigned long long*>(A.out_M + r),
+                      (unsigned long long)(k * BT + tt));
         }
       }
       if (A.out_block) {  // ---- global table probe (lookup) ----
@@ -274,7 +323,7 @@ __global__ void __launch_bounds__(MT) match_kernel(MatchKernelArgs K) {
                     (unsigned long long)(k * BT));
       }
     }
-    __syncthreads();  // s_off / scan storage reuse by the next tile
+    __syncthreads();  // window / scan storage reuse; s_tile (next ticket) visible
   }
 }
 
@@ -322,10 +371,11 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   K.max_pin_blocks = p->cfg.max_pin_blocks;
   K.ntiles = ntiles;
   K.counter = reinterpret_cast<unsigned long long*>(tile_state);
-  K.flag = tile_state + 1;
-  K.agg = reinterpret_cast<volatile uint64_t*>(tile_state + 1 + ntiles);
-  K.incl = reinterpret_cast<volatile uint64_t*>(tile_state + 1 + 2 * ntiles);
-  int64_t grid = (int64_t)sm_count() * 8;  // persistent: 8 x 256-thread CTAs per SM
+  K.status = reinterpret_cast<uint64_t*>(tile_state + 1);
+  int64_t* tile_r0 = tile_state + 1 + ntiles;
+  K.tile_r0 = tile_r0;
+  tile_first_kernel<<<grid_for(a.n, 256, sm_count() * 8), 256, 0, st>>>(a.blk_off, a.n, tile_r0);
+  int64_t grid = (int64_t)sm_count() * 4;  // persistent: 4 x 256-thread CTAs per SM
   if (grid > ntiles) grid = ntiles;
   match_kernel<<<(unsigned)grid, MT, 0, st>>>(K);
   SFKV_LAUNCH_CHECK("match_kernel");

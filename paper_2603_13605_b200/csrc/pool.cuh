@@ -32,7 +32,9 @@ struct DevCounters {
   long long table_tomb;
   long long blocks_in_use;
   int error;                      // sticky device-side error (SFKV_EPOOL / SFKV_ESTALE)
-  int pad;
+  int pad;                        // table-rebuild flag
+  long long occ_saved;            // admission snapshot, restored when a batch aborts
+  unsigned long long rej_saved;
 };
 
 }  // namespace sfkv
@@ -100,6 +102,7 @@ struct PayloadJob {
   int64_t n_items;
   const int32_t* old_pin_blk;
   int32_t max_pin_blocks;
+  const int* error;  // sticky batch error: no bytes move when set
 };
 int launch_payload(sfkv_pool* p, const PayloadJob& j, const void* kv_src, const int64_t* kv_src_off,
                    const sfkv_pool* src_pool, int32_t src_wf, cudaStream_t st);
@@ -107,13 +110,11 @@ int launch_payload(sfkv_pool* p, const PayloadJob& j, const void* kv_src, const 
 int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStream_t st);
 size_t match_tile_state_elems(int64_t n_items);
 
-int ensure_host_stage(sfkv_pool* p, size_t bytes);
-
 // Internal commit entry (device pointers). src_pool/src_wf: handoff payload source.
 int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
-               const uint32_t* tok, const void* kv_src, const int64_t* kv_src_off,
-               const int64_t* m_expected, int32_t* out_status, const sfkv_pool* src_pool,
-               int32_t src_wf);
+               const uint32_t* tok, int64_t n_items_bound, const void* kv_src,
+               const int64_t* kv_src_off, const int64_t* m_expected, int32_t* out_status,
+               const sfkv_pool* src_pool, int32_t src_wf);
 int flush_dev(sfkv_pool* p, int64_t n, const int32_t* wf, int64_t* out_freed, bool all);
 int gather_dev(sfkv_pool* p, int64_t n, const int32_t* wf, void* dst, const int64_t* dst_off);
 int maybe_rebuild_table(sfkv_pool* p);

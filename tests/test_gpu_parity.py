@@ -234,3 +234,28 @@ def test_threshold_mapper(gpu_api, oracle_api):
     out = np.zeros(len(s), dtype=np.int32)
     gpu_api.check("threshold", gpu_api.threshold_batch(0, len(s), s.ctypes.data, 100.0, out.ctypes.data))
     assert list(out) == [0, 0, 1, 1, 0, 0]
+
+
+def test_pool_exhaustion_aborts_batch_cleanly(gpu_api, oracle_api):
+    """A commit that needs more physical blocks than are free fails with SFKV_EPOOL and leaves
+    occupancy, pins and refcounts unchanged; the pool keeps working afterwards."""
+    cfg = Config(max_workflows=8, n_blocks=10, capacity_tokens=10_000, max_pin_blocks=16,
+                 table_log2=8)
+    g = Pool(gpu_api, cfg)
+    off, tok = csr([list(range(1, 100))])  # 7 blocks
+    assert g.commit(np.array([0], np.int32), off, tok)[0] == 1
+    before = (g.stats(), g.refcounts().copy(), g.pin_blocks(0)[0].copy())
+    off2, tok2 = csr([list(range(500, 600))])  # 7 more blocks: only 3 free
+    with pytest.raises(Exception) as ei:
+        g.commit(np.array([1], np.int32), off2, tok2)
+    assert "EPOOL" in str(ei.value)
+    after = (g.stats(), g.refcounts(), g.pin_blocks(0)[0])
+    assert after[0]["occupancy_tokens"] == before[0]["occupancy_tokens"]
+    assert after[0]["capacity_rejections"] == before[0]["capacity_rejections"]
+    np.testing.assert_array_equal(after[1], before[1])
+    np.testing.assert_array_equal(after[2], before[2])
+    assert g.flush(0) == 99
+    assert g.commit(np.array([1], np.int32), off2, tok2)[0] == 1  # the abandoned claims heal
+    assert g.match(np.array([1], np.int32), off2, tok2)[0] == 100
+    lk, hit = g.lookup(off2, tok2)
+    assert hit[0] == 96 and (lk[:6] >= 0).all()
