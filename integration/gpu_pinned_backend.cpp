@@ -1,0 +1,237 @@
+// GpuPinnedBackend implementation (see gpu_pinned_backend.hpp). The scheduling and latency rules
+// restate SimulatedBackend's documented behaviour (simulated_backend.hpp:57-76 and
+// simulated_backend.cpp:31-133); only the cache operations differ: they go to the B200 pool.
+#include "gpu_pinned_backend.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+
+namespace stageflow {
+
+namespace {
+
+std::mutex g_intern_mu;
+std::unordered_map<std::string, std::uint32_t> g_intern;
+
+std::string numbered_words(long long n) {  // "out0 out1 ... out{n-1}" placeholder reply
+  std::string s;
+  for (long long i = 0; i < n; ++i) {
+    if (i) s.push_back(' ');
+    s += "out";
+    s += std::to_string(i);
+  }
+  return s;
+}
+
+int ceil_log2(long long x) {
+  int l = 0;
+  while ((1LL << l) < x) ++l;
+  return l;
+}
+
+}  // namespace
+
+std::uint32_t intern_token(const std::string& token) {
+  std::lock_guard<std::mutex> lk(g_intern_mu);
+  auto [it, inserted] = g_intern.emplace(token, static_cast<std::uint32_t>(g_intern.size()));
+  return it->second;
+}
+
+GpuPinnedBackend::GpuPinnedBackend(EventLoop& loop, BackendDescriptor descriptor,
+                                   SimulatedBackendConfig config, GpuPoolOptions options, LogFn log)
+    : loop_(loop), descriptor_(std::move(descriptor)), config_(std::move(config)),
+      options_(options), log_(std::move(log)) {
+  if (config_.max_concurrency < 1) throw BackendError("max_concurrency must be >= 1");
+  if (config_.cache_capacity_tokens <= 0) throw BackendError("cache capacity must be positive");
+  if (config_.prefill_ms_per_token <= 0 || config_.decode_ms_per_token <= 0)
+    throw BackendError("latency parameters must be positive");
+  sfkv_pool_config pc{};
+  pc.device = options_.device;
+  pc.max_workflows = options_.max_workflows;
+  pc.capacity_tokens = config_.cache_capacity_tokens;
+  pc.max_pin_blocks = options_.max_pin_blocks;
+  // Physical blocks never bind in parity mode: every logical token once, one partial block per
+  // pin, and one maximal pin of transient headroom (a replaced pin is released after commit).
+  pc.n_blocks = config_.cache_capacity_tokens / SFKV_BLOCK_TOKENS + options_.max_workflows +
+                2LL * options_.max_pin_blocks + 64;
+  pc.table_log2 = ceil_log2(2 * pc.n_blocks) + 1;
+  pc.n_slabs = 0;  // the reference holds no KV bytes; this binding is metadata-only
+  pc.slab_row_bytes = 0;
+  check(sfkv_pool_create(&pc, &pool_), "sfkv_pool_create");
+}
+
+GpuPinnedBackend::~GpuPinnedBackend() { sfkv_pool_destroy(pool_); }
+
+void GpuPinnedBackend::check(int rc, const char* what) const {
+  if (rc != SFKV_OK)
+    throw BackendError(std::string(what) + " failed (" + std::to_string(rc) + "): " + sfkv_last_error());
+}
+
+int32_t GpuPinnedBackend::find_slot(const std::string& workflow_id) const {
+  auto it = slots_.find(workflow_id);
+  return it == slots_.end() ? -1 : it->second;
+}
+
+int32_t GpuPinnedBackend::slot_for(const std::string& workflow_id) {
+  auto it = slots_.find(workflow_id);
+  if (it != slots_.end()) return it->second;
+  const auto s = static_cast<int32_t>(slots_.size());
+  if (s >= options_.max_workflows) throw BackendError("GpuPinnedBackend: out of workflow slots");
+  slots_.emplace(workflow_id, s);
+  return s;
+}
+
+bool GpuPinnedBackend::has_capacity() const {
+  return busy_ + static_cast<int>(pending_.size()) < config_.max_concurrency;
+}
+
+void GpuPinnedBackend::complete(CompletionRequest req, CompletionCallback cb) {
+  ++stats_.completions;
+  pending_.push_back(Pending{std::move(req), std::move(cb), loop_.now_ms()});
+  pump();
+}
+
+void GpuPinnedBackend::pump() {
+  while (busy_ < config_.max_concurrency && !pending_.empty()) {
+    Pending p = std::move(pending_.front());
+    pending_.pop_front();
+    start(std::move(p));
+  }
+}
+
+ScriptedReply GpuPinnedBackend::reply_for(const CompletionRequest& req, int turn) const {
+  const auto& rule = config_.output;
+  const auto& ann = req.metadata.annotations;
+  if (rule.kind == OutputRule::Kind::Scripted) return rule.script(req, turn);
+  if (rule.kind == OutputRule::Kind::EchoAnnotation) {
+    auto it = ann.find(rule.annotation_key);
+    return {it == ann.end() ? std::string() : it->second, {}};
+  }
+  long long n = rule.constant_tokens;
+  if (rule.kind == OutputRule::Kind::FromAnnotation) {
+    auto it = ann.find(rule.annotation_key);
+    if (it != ann.end()) n = std::max(0LL, std::stoll(it->second));
+  }
+  return {numbered_words(n), {}};
+}
+
+void GpuPinnedBackend::start(Pending item) {
+  const double now = loop_.now_ms();
+  const double queue_ms = now - item.arrival_ms;
+  const std::string wf = item.req.metadata.workflow_id;
+
+  std::vector<std::uint32_t> ids;
+  for (const auto& t : context_token_sequence(item.req.messages)) ids.push_back(intern_token(t));
+  const long long P = static_cast<long long>(ids.size());
+  const int64_t off[2] = {0, P};
+  long long M = 0;
+  int32_t slot = -1;
+  if (!wf.empty()) {  // the empty workflow id never holds a pin (simulated_backend.cpp:125)
+    slot = slot_for(wf);
+    int64_t m = 0;
+    check(sfkv_match_batch(pool_, 1, &slot, off, ids.data(), &m, nullptr), "sfkv_match_batch");
+    M = m;
+  }
+  if (observer_) observer_(wf, item.req.metadata.stage_id, P, M);
+
+  const int turn = turns_[{wf, item.req.metadata.stage_id}]++;
+  ScriptedReply reply = reply_for(item.req, turn);
+  long long O = count_tokens(reply.content);
+  if (item.req.max_tokens > 0 && O > item.req.max_tokens) {
+    auto words = tokenize_whitespace(reply.content);
+    words.resize(static_cast<std::size_t>(item.req.max_tokens));
+    std::string kept;
+    for (const auto& w : words) {
+      if (!kept.empty()) kept.push_back(' ');
+      kept += w;
+    }
+    reply.content = std::move(kept);
+    O = item.req.max_tokens;
+  }
+  if (O == 0 && !reply.tool_calls.empty()) O = 1;
+
+  const double prefill = config_.fixed_overhead_ms +
+                         config_.prefill_ms_per_token * static_cast<double>(P - M);
+  const double decode = config_.decode_ms_per_token * static_cast<double>(O);
+  CompletionResponse resp;
+  resp.content = std::move(reply.content);
+  resp.tool_calls = std::move(reply.tool_calls);
+  resp.usage.prompt_tokens = P;
+  resp.usage.completion_tokens = O;
+  resp.usage.cached_prefix_tokens = M;
+  resp.timing.queue_ms = queue_ms;
+  resp.timing.ttft_ms = queue_ms + prefill;
+  resp.timing.total_ms = resp.timing.ttft_ms + decode;
+  ++busy_;
+  stats_.prompt_tokens += P;
+  stats_.completion_tokens += O;
+  stats_.cached_prefix_tokens += M;
+
+  loop_.schedule_in(prefill + decode, [this, slot, ids = std::move(ids), resp = std::move(resp),
+                                       cb = std::move(item.cb), wf]() mutable {
+    if (slot >= 0) {  // retain the served prompt (commit = pin_prompt, admission included)
+      const int64_t o2[2] = {0, static_cast<int64_t>(ids.size())};
+      int32_t status = 0;
+      check(sfkv_commit_batch(pool_, 1, &slot, o2, ids.data(), nullptr, nullptr, nullptr, &status),
+            "sfkv_commit_batch");
+      if (status != SFKV_PIN_ACCEPTED && log_)
+        log_(LogLevel::Warn, "gpu backend " + descriptor_.ref +
+                                 ": cache capacity exceeded, prefix for workflow " + wf + " not pinned");
+    }
+    --busy_;
+    pump();
+    cb(std::move(resp), nullptr);
+    notify_capacity();
+  });
+}
+
+long long GpuPinnedBackend::flush(const FlushScope& scope) {
+  ++stats_.flush_calls;
+  int64_t freed = 0;
+  if (scope.all) {
+    check(sfkv_flush(pool_, SFKV_FLUSH_ALL, &freed), "sfkv_flush");
+    return freed;
+  }
+  const int32_t slot = find_slot(scope.workflow_id);
+  if (slot < 0) return 0;
+  check(sfkv_flush(pool_, slot, &freed), "sfkv_flush");
+  return freed;
+}
+
+double GpuPinnedBackend::cache_utilization() const {
+  double u = 0;
+  check(sfkv_cache_utilization(pool_, &u), "sfkv_cache_utilization");
+  return u;
+}
+
+bool GpuPinnedBackend::preserve(const std::string& workflow_id) {
+  ++stats_.preserve_calls;
+  const int32_t slot = find_slot(workflow_id);
+  if (slot < 0) return false;
+  int32_t has = 0;
+  check(sfkv_preserve(pool_, slot, &has), "sfkv_preserve");
+  return has != 0;
+}
+
+long long GpuPinnedBackend::pinned_token_count(const std::string& workflow_id) const {
+  const int32_t slot = find_slot(workflow_id);
+  if (slot < 0) return 0;
+  int64_t n = 0;
+  check(sfkv_pinned_token_count(pool_, slot, &n), "sfkv_pinned_token_count");
+  return n;
+}
+
+long long GpuPinnedBackend::occupancy_tokens() const {
+  sfkv_pool_stats s{};
+  check(sfkv_stats(pool_, &s), "sfkv_stats");
+  return s.occupancy_tokens;
+}
+
+std::uint64_t GpuPinnedBackend::capacity_rejections() const {
+  sfkv_pool_stats s{};
+  check(sfkv_stats(pool_, &s), "sfkv_stats");
+  return s.capacity_rejections;
+}
+
+}  // namespace stageflow

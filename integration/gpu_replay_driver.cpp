@@ -1,0 +1,115 @@
+// sf_gpu_replay — the reference's own orchestrator, memory manager and harness loop driving the
+// B200 pool through GpuPinnedBackend (the drop-in). Same wiring as run_benchmark
+// (proj/src/harness.cpp:8-116) with GpuPinnedBackend in place of SimulatedBackend. Emits:
+//   {"type":"req", b, wf, stage, P, M}   per dispatch, in dispatch order (M from the GPU)
+//   {"type":"act", ...}                   the memory manager's action log (memory.cpp:389-401)
+//   {"type":"end", backends: {...}}        final counters
+// tests/test_dropin_replay.py compares this with the golden stream recorded from the unmodified
+// reference (oracle/ref_shim/replay_driver.cpp) for the same (trace, config).
+#include <fstream>
+
+#include "gpu_pinned_backend.hpp"
+#include "stageflow/config.hpp"
+#include "stageflow/harness.hpp"
+
+using namespace stageflow;
+
+int main(int argc, char** argv) {
+  std::string config_path, trace_path, out_path;
+  int device = 0;
+  for (int i = 1; i + 1 < argc; i += 2) {
+    std::string a = argv[i];
+    if (a == "--config") config_path = argv[i + 1];
+    else if (a == "--trace") trace_path = argv[i + 1];
+    else if (a == "--out") out_path = argv[i + 1];
+    else if (a == "--device") device = std::stoi(argv[i + 1]);
+  }
+  if (config_path.empty() || trace_path.empty() || out_path.empty()) {
+    std::fprintf(stderr, "usage: sf_gpu_replay --config C --trace T --out O [--device D]\n");
+    return 2;
+  }
+  auto config = load_config(config_path);
+  auto templates = build_templates(config);
+  auto trace = load_trace(trace_path, templates.names());
+  EventLoop loop(ClockMode::Virtual);
+  LogFn log = stderr_logger(LogLevel::Error);
+
+  std::vector<json> out;
+  BackendRegistry registry;
+  std::map<std::string, GpuPinnedBackend*> gpu;
+  for (const auto& b : config.backends) {
+    GpuPoolOptions opt;
+    opt.device = device;
+    opt.max_workflows = static_cast<int>(trace.size()) + 8;
+    auto be = std::make_shared<GpuPinnedBackend>(loop, b.descriptor, b.sim, opt, log);
+    const std::string ref = b.descriptor.ref;
+    be->set_dispatch_observer([&out, ref](const std::string& wf, const std::string& st,
+                                          long long P, long long M) {
+      out.push_back({{"type", "req"}, {"b", ref}, {"wf", wf}, {"stage", st}, {"P", P}, {"M", M}});
+    });
+    gpu[ref] = be.get();
+    registry.add(be);
+  }
+  ToolRegistry tools;
+  SignalBus bus;
+  MemoryManager memory(config.memory, &registry, log);
+  memory.attach(bus);
+  Orchestrator orch(loop, registry, tools, bus, config.orchestration, log);
+
+  std::size_t remaining = trace.size();
+  for (std::size_t i = 0; i < trace.size(); ++i) {
+    const auto& r = trace[i];
+    const std::string workflow_id = r.workflow_template + "-" + std::to_string(i);
+    auto spec = templates.at(r.workflow_template)(
+        r, workflow_id, config.template_params.value(r.workflow_template, json::object()));
+    if (spec.stages.empty()) {
+      --remaining;
+      continue;
+    }
+    for (auto& [_, stage] : spec.stages) {
+      if (stage.stage_scheduling_policy == "fcfs" && config.default_stage_policy != "fcfs")
+        stage.stage_scheduling_policy = config.default_stage_policy;
+      if (stage.request_scheduling_policy == "fcfs" && config.default_request_policy != "fcfs")
+        stage.request_scheduling_policy = config.default_request_policy;
+    }
+    auto validated = validate_workflow(spec, registry);
+    if (!validated.ok()) throw std::runtime_error("invalid workflow from " + r.workflow_template);
+    const auto& wf = *validated.workflow;
+    if (!wf.spec().workflow_memory_policy.empty())
+      memory.set_workflow_chain(workflow_id, wf.spec().workflow_memory_policy);
+    orch.submit_at(static_cast<double>(r.arrival_ms), wf, make_router(config, registry, wf),
+                   [&remaining](ExecutionReport) { --remaining; }, r.annotations());
+  }
+  auto tick = std::make_shared<std::function<void()>>();
+  if (config.memory.monitor_interval_ms > 0) {
+    *tick = [&, wp = std::weak_ptr<std::function<void()>>(tick)] {
+      if (remaining == 0) return;
+      memory.pressure_tick(loop.now_ms());
+      if (auto self = wp.lock()) loop.schedule_in(config.memory.monitor_interval_ms, *self);
+    };
+    loop.schedule_in(config.memory.monitor_interval_ms, *tick);
+  }
+  loop.run_until_idle();
+
+  for (const auto& r : memory.action_log()) {
+    out.push_back({{"type", "act"}, {"trigger", r.trigger}, {"ts", r.ts},
+                   {"action", cache_action_kind_name(r.action.kind)},
+                   {"workflow", r.action.workflow_id}, {"backend", r.action.backend_ref},
+                   {"reason", r.action.reason}});
+  }
+  json end_b = json::object();
+  for (auto& [ref, g] : gpu) {
+    const auto& st = g->stats();
+    end_b[ref] = {{"occupancy_tokens", g->occupancy_tokens()},
+                  {"capacity_rejections", g->capacity_rejections()},
+                  {"completions", st.completions}, {"flush_calls", st.flush_calls},
+                  {"preserve_calls", st.preserve_calls}, {"prompt_tokens", st.prompt_tokens},
+                  {"completion_tokens", st.completion_tokens},
+                  {"cached_prefix_tokens", st.cached_prefix_tokens},
+                  {"utilization", g->cache_utilization()}};
+  }
+  out.push_back({{"type", "end"}, {"now_ms", loop.now_ms()}, {"backends", end_b}});
+  std::ofstream f(out_path);
+  for (const auto& l : out) f << l.dump() << "\n";
+  return 0;
+}

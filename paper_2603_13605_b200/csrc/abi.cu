@@ -241,7 +241,7 @@ static int match_common(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_
                               reinterpret_cast<int64_t*>(p->small.as<char>() + o_tmp), st))
     return rc;
   Carver cv;
-  const size_t o_tile = cv.take<int64_t>(match_tile_state_elems(n_items));
+  const size_t o_tile = cv.take<int64_t>(match_tile_state_elems(n_items, n));
   if (int rc = p->scratch.ensure(cv.off)) return rc;
   MatchArgs a{};
   a.n = n;

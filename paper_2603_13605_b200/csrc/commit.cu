@@ -544,7 +544,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   const int64_t ni = n_items_bound > 0 ? n_items_bound : 1;
   Carver cv;
   const size_t o_blk = cv.take<int64_t>(n + 1), o_M = cv.take<int64_t>(n),
-               o_hash = cv.take<uint64_t>(ni), o_tile = cv.take<int64_t>(match_tile_state_elems(ni)),
+               o_hash = cv.take<uint64_t>(ni), o_tile = cv.take<int64_t>(match_tile_state_elems(ni, n)),
                o_st = cv.take<int32_t>(n), o_slot = cv.take<int64_t>(ni),
                o_bid = cv.take<int32_t>(ni), o_hit = cv.take<uint8_t>(ni),
                o_claim = cv.take<uint8_t>(ni), o_cat = cv.take<uint8_t>(ni),

@@ -5,7 +5,7 @@
 //
 //   items   = every 16-token block of every request (CSR batch, flattened; blk_off = scan)
 //   digest  = block_digest(k, n, tokens)                           (per item, independent)
-//   S_k     = sum_{i<=k} digest_i  (segmented by request)           (CTA scan + decoupled look-back)
+//   S_k     = sum_{i<=k} digest_i mod 2^62 (segmented by request)   (warp scan + decoupled look-back)
 //   c_k     = chain_finalize(S_k)                                   (chained block hash)
 //   match   : if c_{k-1} equals the pin's hash k-1 (or k == 0), verify block k against the pin's
 //             tokens; a differing token at t gives atomicMin(M[r], 16k + t). c_{k-1} is
@@ -14,41 +14,38 @@
 //             LCP independent of hash collisions (M is pre-set to min(P, pin_len)).
 //   lookup  : probe the global table for c_k (full blocks), verify tokens, report the block id.
 //
-// Data movement: one thread per block, 256-block tiles claimed in order by persistent CTAs. A
-// tile's request metadata (block/token offsets, workflow slot, pin length and block count) is
-// staged in shared memory by all threads at once from a precomputed tile -> first-request table,
-// so no thread walks global memory serially. A thread loads its 64-B block with 16-B vector
-// loads at any alignment (a warp covers 2 KiB of contiguous tokens; L1 merges the halves) and
-// issues its pin-hash / block-id loads before the tile scan so their latency overlaps the
-// look-back. Algorithmic bytes per block: 64 B tokens (+8 B hash out when requested), + 8 B pin
-// hash for blocks inside the pin, + 4 B block id + 64 B pin tokens when verified; lookup mode:
-// + 16 B table slot (+ 64 B verify). HBM-bound integer work: no tensor cores.
+// Execution: warp-centric and barrier-free. A warp owns a 32-block tile (one block per lane);
+// tiles are assigned statically round-robin to the resident warps of a persistent grid, so every
+// warp walks its tiles in increasing order and a tile's predecessors are always owned by warps
+// that make progress. Request metadata for the tile's window of up to 32 requests is loaded one
+// request per lane and redistributed with shuffles (5-step shuffle binary search). The chain sum
+// is a warp shuffle segmented scan; the carry across tiles is a decoupled look-back in which the
+// 32 lanes read 32 predecessor status words at once (flag and 62-bit sum packed in one word:
+// relaxed 64-bit loads/stores, no fences). A lane loads its 64-B block with 16-B vector loads at
+// any alignment (a warp covers 2 KiB of contiguous tokens) and issues its pin-hash / block-id
+// loads before the scan. Algorithmic bytes per block: 64 B tokens (+8 B hash out when requested),
+// + 8 B pin hash for blocks inside the pin, + 4 B block id + 64 B pin tokens when verified; lookup
+// mode: + 16 B table slot (+ 64 B verify). HBM-bound integer work: no tensor cores.
 #include "pool.cuh"
 
 namespace sfkv {
 
-constexpr int MT = 256;  // items (threads) per tile
+constexpr int WT = 32;  // items per warp tile
+#ifndef MATCH_MIN_CTAS
+#define MATCH_MIN_CTAS 3  // 256-thread CTAs per SM: 80 registers, no spills
+#endif
 
-struct SegPair {
-  uint64_t v;
-  int h;
-};
-struct SegOp {
-  __device__ __forceinline__ SegPair operator()(const SegPair& a, const SegPair& b) const {
-    return SegPair{b.h ? b.v : a.v + b.v, a.h | b.h};
-  }
-};
-
-// counter + per-tile {status word, first request}
-size_t match_tile_state_elems(int64_t n_items) {
-  int64_t ntiles = (n_items + MT - 1) / MT;
-  return (size_t)(1 + 2 * ntiles);
+// counter (unused) + per-tile {status word, first request} + 32-B request records [n+1]
+size_t match_tile_state_elems(int64_t n_items, int64_t n_requests) {
+  int64_t ntiles = (n_items + WT - 1) / WT;
+  return (size_t)(((1 + 2 * ntiles + 3) & ~int64_t(3)) + 4 * (n_requests + 1));
 }
+
+struct ReqRec;
 
 struct MatchKernelArgs {
   MatchArgs a;
-  const int64_t* pin_len;
-  const int32_t* pin_nblk;
+  const ReqRec* rec;
   const int32_t* pin_blk;
   const uint64_t* pin_hash;
   const uint32_t* blk_tok;
@@ -56,8 +53,6 @@ struct MatchKernelArgs {
   const Slot* slots;
   uint64_t slot_mask;
   int32_t max_pin_blocks;
-  int64_t ntiles;  // bound
-  unsigned long long* counter;
   uint64_t* status;  // per tile: 0 = pending, ST_AGG | aggregate, ST_INCL | inclusive prefix
   const int64_t* tile_r0;
 };
@@ -71,6 +66,12 @@ __device__ __forceinline__ void st_status(uint64_t* p, uint64_t v) {
 __device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
@@ -135,111 +136,141 @@ __device__ __forceinline__ bool tokens_equal(const uint32_t* a, const uint32_t* 
   return eq;
 }
 
-// tile_r0[t] = the request holding item t*MT (tiles whose first item lies in request r).
-__global__ void tile_first_kernel(const int64_t* __restrict__ blk_off, int64_t n,
-                                  int64_t* __restrict__ tile_r0) {
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+// Per-request record staged once per batch by request_prep_kernel (one request per thread, so
+// the dependent wf -> pin_len load chain runs fully parallel instead of inside every tile).
+struct __align__(32) ReqRec {
+  int64_t blk_off;   // first item of the request
+  int64_t tok_off;   // first token
+  int64_t pin_len;   // -1: the workflow has no pin (or lookup mode)
+  int32_t wf;
+  int32_t pad;
+};
+
+// rec[r] for r in [0, n] (rec[n] closes the last request) and tile_r0[t] = the request holding
+// item t*WT (tiles whose first item lies in request r).
+__global__ void request_prep_kernel(MatchArgs A, const int64_t* __restrict__ pin_len,
+                                    ReqRec* __restrict__ rec, int64_t* __restrict__ tile_r0) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= A.n;
        r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b0 = blk_off[r], b1 = blk_off[r + 1];
-    for (int64_t t = (b0 + MT - 1) / MT; t * MT < b1; ++t) tile_r0[t] = r;
+    ReqRec q;
+    q.blk_off = A.blk_off[r];
+    q.tok_off = A.tok_off[r];
+    q.wf = 0;
+    q.pin_len = -1;
+    q.pad = 0;
+    if (r < A.n && A.wf) {
+      q.wf = A.wf[r];
+      q.pin_len = pin_len[q.wf];
+    }
+    rec[r] = q;
+    if (r < A.n) {
+      const int64_t b1 = A.blk_off[r + 1];
+      for (int64_t t = (q.blk_off + WT - 1) / WT; t * WT < b1; ++t) tile_r0[t] = r;
+    }
   }
 }
 
-__global__ void __launch_bounds__(MT, 4) match_kernel(MatchKernelArgs K) {
-  using BS = cub::BlockScan<SegPair, MT>;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ int64_t s_off[MT + 1];   // blk_off of the tile's request window
-  __shared__ int64_t s_toff[MT + 1];  // tok_off
-  __shared__ int64_t s_pl[MT];        // pin length (-1: none)
-  __shared__ int32_t s_wf[MT];
-  __shared__ int32_t s_pnb[MT];
-  __shared__ int64_t s_tile;
-  __shared__ uint64_t s_prefix;
+__device__ __forceinline__ ReqRec load_rec(const ReqRec* p) {
+  const int4* q = reinterpret_cast<const int4*>(p);
+  const int4 a = __ldg(q), b = __ldg(q + 1);
+  ReqRec r;
+  r.blk_off = (int64_t)(((uint64_t)(uint32_t)a.y << 32) | (uint32_t)a.x);
+  r.tok_off = (int64_t)(((uint64_t)(uint32_t)a.w << 32) | (uint32_t)a.z);
+  r.pin_len = (int64_t)(((uint64_t)(uint32_t)b.y << 32) | (uint32_t)b.x);
+  r.wf = b.z;
+  r.pad = 0;
+  return r;
+}
 
+// Aggregate of one tile computed from scratch: (sum of digests since the tile's last segment
+// head, whether the tile holds a head). Used only when a predecessor's status stays unpublished
+// (e.g. its warp is not resident because other kernels occupy the GPU), so the look-back always
+// makes progress without relying on co-residency. Returns the status word the owner would publish.
+__device__ __forceinline__ uint64_t tile_status_fallback(const MatchKernelArgs& K, int64_t tile,
+                                                      int64_t n_items, int64_t tok_total) {
   const MatchArgs& A = K.a;
-  const int tid = threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t item = tile * WT + lane;
+  uint64_t v = 0;
+  int h = 0;
+  if (item < n_items) {
+    const int64_t r = upper_index(A.blk_off, A.n, item);
+    const int64_t k = item - A.blk_off[r];
+    const int64_t tb = A.tok_off[r];
+    const int64_t rem = A.tok_off[r + 1] - tb - k * BT;
+    const int nval = (int)(rem < BT ? rem : BT);
+    uint32_t t[BT];
+    load_block(A.tok, tb + k * BT, nval, tok_total, t);
+    v = block_digest_words((uint64_t)k, (uint32_t)nval, t);
+    h = k == 0;
+  }
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t vv = __shfl_up_sync(0xffffffffu, v, d);
+    const int hh = __shfl_up_sync(0xffffffffu, h, d);
+    if (lane >= d) {
+      if (!h) v += vv;
+      h |= hh;
+    }
+  }
+  v = __shfl_sync(0xffffffffu, v, 31);
+  h = __shfl_sync(0xffffffffu, h, 31);
+  return (h ? ST_INCL : ST_AGG) | (v & CHAIN_MASK);
+}
+
+template <bool LOOKUP>
+__global__ void __launch_bounds__(256, MATCH_MIN_CTAS) match_kernel(MatchKernelArgs K) {
+  const MatchArgs& A = K.a;
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const bool match_mode = A.out_M != nullptr;
   const int64_t tok_total = A.tok_off[A.n];
-  // A.n_items is only an upper bound (it sizes the look-back state); the exact count is on device.
+  // A.n_items is only an upper bound (it sizes the tile state); the exact count is on device.
   const int64_t n_items = A.blk_off[A.n];
-  const int64_t ntiles = (n_items + MT - 1) / MT;
+  const int64_t ntiles = (n_items + WT - 1) / WT;
 
-  for (;;) {
-    // Take the ticket only when starting the tile: a held-but-unstarted ticket would make every
-    // later tile's look-back wait on it.
-    if (tid == 0) s_tile = (int64_t)atomicAdd(K.counter, 1ull);
-    __syncthreads();
-    const int64_t tile = s_tile;
-    if (tile >= ntiles) break;
-    const int64_t item0 = tile * MT;
-    const int64_t item = item0 + tid;
+  int64_t r0_next = gwarp < ntiles ? K.tile_r0[gwarp] : 0;
+  for (int64_t tile = gwarp; tile < ntiles; tile += nwarps) {
+    const int64_t item0 = tile * WT;
+    const int64_t item = item0 + lane;
     const bool valid = item < n_items;
 
-    // ---- stage the request window [r0, r0 + MT] (all threads in parallel) ----
-    const int64_t r0 = K.tile_r0[tile];
-    {
-      const int64_t rr = r0 + tid;
-      s_off[tid] = rr <= A.n ? A.blk_off[rr] : INT64_MAX;
-      s_toff[tid] = rr <= A.n ? A.tok_off[rr] : 0;
-      if (match_mode && rr < A.n) {
-        const int32_t w = A.wf[rr];
-        const int64_t pl = K.pin_len[w];
-        s_wf[tid] = w;
-        s_pl[tid] = pl;
-        s_pnb[tid] = pl < 0 ? 0 : K.pin_nblk[w];
-      }
-      if (tid == 0) {
-        const int64_t re = r0 + MT;
-        s_off[MT] = re <= A.n ? A.blk_off[re] : INT64_MAX;
-        s_toff[MT] = re <= A.n ? A.tok_off[re] : 0;
-      }
+    // ---- request window [r0, r0 + 32]: lane j holds request r0 + j (one 32-B record) ----
+    const int64_t r0 = r0_next;
+    const int64_t rr = r0 + lane <= A.n ? r0 + lane : A.n;
+    const ReqRec rec_j = load_rec(K.rec + rr);
+    const int64_t off_32 = r0 + WT <= A.n ? K.rec[r0 + WT].blk_off : INT64_MAX;
+    const int64_t toff_32 = r0 + WT <= A.n ? K.rec[r0 + WT].tok_off : 0;
+    if (tile + nwarps < ntiles) r0_next = K.tile_r0[tile + nwarps];  // prefetch
+    const int64_t off_j = r0 + lane <= A.n ? rec_j.blk_off : INT64_MAX;
+    // largest j in [0, 31] with off_j <= item (off non-decreasing); j = 32 if off_32 <= item
+    int j = 0;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      const int64_t v = __shfl_sync(0xffffffffu, off_j, j + s);
+      if (v <= item) j += s;
     }
-    __syncthreads();
-
-    // ---- my block: request (smem binary search), tokens, early pin loads ----
-    int64_t r = r0, k = 0, tb = 0, te = 0;
-    int32_t w = 0, pnb = 0;
-    int64_t pl = -1;
-    if (valid) {
-      if (s_off[MT] <= item) {  // > MT requests in this tile (empty requests): global path
-        r = upper_index(A.blk_off, A.n, item);
-        k = item - A.blk_off[r];
-        tb = A.tok_off[r];
-        te = A.tok_off[r + 1];
-        if (match_mode) {
-          w = A.wf[r];
-          pl = K.pin_len[w];
-          pnb = pl < 0 ? 0 : K.pin_nblk[w];
-        }
-      } else {
-        int lo = 0, hi = MT;  // s_off[lo] <= item < s_off[hi]
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (s_off[mid] <= item) lo = mid;
-          else hi = mid;
-        }
-        r = r0 + lo;
-        k = item - s_off[lo];
-        tb = s_toff[lo];
-        te = s_toff[lo + 1];
-        if (match_mode) {
-          w = s_wf[lo];
-          pl = s_pl[lo];
-          pnb = s_pnb[lo];
-        }
-      }
+    const int64_t off_r = __shfl_sync(0xffffffffu, off_j, j);
+    int64_t tb = __shfl_sync(0xffffffffu, rec_j.tok_off, j);
+    const int64_t te_in = __shfl_sync(0xffffffffu, rec_j.tok_off, (j + 1) & 31);
+    int32_t w = __shfl_sync(0xffffffffu, rec_j.wf, j);
+    int64_t pl = __shfl_sync(0xffffffffu, rec_j.pin_len, j);
+    int64_t r = r0 + j, k = item - off_r, te = j == 31 ? toff_32 : te_in;
+    if (valid && off_32 <= item) {  // > 32 requests in this tile (empty requests): global path
+      r = upper_index(A.blk_off, A.n, item);
+      const ReqRec a = load_rec(K.rec + r);
+      k = item - a.blk_off;
+      tb = a.tok_off;
+      te = K.rec[r + 1].tok_off;
+      w = a.wf;
+      pl = a.pin_len;
     }
     const int64_t rem = te - tb - k * BT;
     const int nval = valid ? (int)(rem < BT ? rem : BT) : 0;
-    uint32_t t[BT];
-    if (valid) {
-      load_block(A.tok, tb + k * BT, nval, tok_total, t);
-    } else {
-#pragma unroll
-      for (int j = 0; j < BT; ++j) t[j] = 0u;
-    }
-    // pin metadata needed after the scan, issued now so its latency overlaps the look-back
-    const bool in_pin = match_mode && valid && pl >= 0 && k < pnb;
+
+    // ---- tokens + pin metadata (one round trip), then the pin block's tokens ----
+    const bool in_pin = match_mode && valid && pl >= 0 && k < (pl + BT - 1) / BT;
     const int64_t pb = (int64_t)w * K.max_pin_blocks;
     uint64_t prev_pin_hash = 0;
     int32_t pin_id = 0;
@@ -247,57 +278,103 @@ __global__ void __launch_bounds__(MT, 4) match_kernel(MatchKernelArgs K) {
       if (k > 0) prev_pin_hash = __ldg(K.pin_hash + pb + k - 1);
       pin_id = __ldg(K.pin_blk + pb + k);
     }
-    const uint64_t g = valid ? block_digest_words((uint64_t)k, (uint32_t)nval, t) : 0ull;
-
-    // ---- segmented inclusive scan over the tile + decoupled look-back ----
-    SegPair in{g, (valid && k == 0) ? 1 : 0};
-    SegPair out, total;
-    BS(tmp).InclusiveScan(in, out, SegOp(), total);
-    if (tid == 0) {
-      // status word = flag << 62 | (sum mod 2^62): one relaxed 64-bit store / load, no fences.
-      uint64_t prefix = 0;
-      st_status(K.status + tile, (total.h ? ST_INCL : ST_AGG) | (total.v & CHAIN_MASK));
-      if (!in.h && tile > 0) {
-        int64_t pred = tile - 1;
-        for (;;) {
-          uint64_t s;
-          do {
-            s = ld_status(K.status + pred);
-          } while (s == 0);
-          prefix += s & CHAIN_MASK;
-          if ((s & ~CHAIN_MASK) == ST_INCL) break;
-          --pred;
-        }
-      }
-      if (!total.h) st_status(K.status + tile, ST_INCL | ((prefix + total.v) & CHAIN_MASK));
-      s_prefix = prefix;
+    uint32_t t[BT];
+    if (valid) {
+      load_block(A.tok, tb + k * BT, nval, tok_total, t);
+    } else {
+#pragma unroll
+      for (int i = 0; i < BT; ++i) t[i] = 0u;
     }
-    __syncthreads();
-    const uint64_t S = out.h ? out.v : s_prefix + out.v;
+    const uint64_t g = valid ? block_digest_words((uint64_t)k, (uint32_t)nval, t) : 0ull;
+    // lookup mode keeps the tokens for verify-on-hit
+    uint32_t tk[BT];
+    if constexpr (LOOKUP) {
+#pragma unroll
+      for (int i = 0; i < BT; ++i) tk[i] = t[i];
+    }
+
+    // ---- warp segmented inclusive scan of (digest, head) ----
+    uint64_t v = g;
+    int h = (valid && k == 0) ? 1 : 0;
+    const int head0 = __shfl_sync(0xffffffffu, h, 0);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t vv = __shfl_up_sync(0xffffffffu, v, d);
+      const int hh = __shfl_up_sync(0xffffffffu, h, d);
+      if (lane >= d) {
+        if (!h) v += vv;
+        h |= hh;
+      }
+    }
+    const uint64_t tot_v = __shfl_sync(0xffffffffu, v, 31);
+    const int tot_h = __shfl_sync(0xffffffffu, h, 31);
+
+    // ---- decoupled look-back, 32 predecessors per round ----
+    // The aggregate is published as soon as the digests are scanned (nothing else delays the
+    // successors); the pin block's tokens are fetched now so their latency overlaps the look-back.
+    if (lane == 0) st_status(K.status + tile, (tot_h ? ST_INCL : ST_AGG) | (tot_v & CHAIN_MASK));
+    uint32_t q[BT];
+    int pn = 0;
+    if (in_pin) {
+      load16_aligned(K.blk_tok + (int64_t)pin_id * BT, q);
+      pn = K.blk_n[pin_id];
+    }
+    uint64_t prefix = 0;
+    if (!head0 && tile > 0) {
+      int64_t base = tile - 1;
+      int spins = 0;
+      for (;;) {
+        const int64_t p = base - lane;
+        uint64_t s = p >= 0 ? ld_status(K.status + p) : ST_INCL;
+        unsigned ready = __ballot_sync(0xffffffffu, s != 0);
+        unsigned incl = __ballot_sync(0xffffffffu, (s & ~CHAIN_MASK) == ST_INCL);
+        int first = incl ? __ffs(incl) - 1 : 31;
+        unsigned need = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
+        if ((ready & need) != need) {  // a needed predecessor has not published yet
+          if (++spins < 1024) continue;
+          // forward progress: compute the nearest unpublished predecessor's aggregate ourselves
+          const int miss = __ffs(~ready & need) - 1;
+          const uint64_t fs = tile_status_fallback(K, base - miss, n_items, tok_total);
+          if (lane == miss) s = fs;
+          ready = __ballot_sync(0xffffffffu, s != 0);
+          incl = __ballot_sync(0xffffffffu, (s & ~CHAIN_MASK) == ST_INCL);
+          first = incl ? __ffs(incl) - 1 : 31;
+          need = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
+          if ((ready & need) != need) continue;  // another gap further back: repeat
+        }
+        spins = 0;
+        prefix += warp_sum(lane <= first ? (s & CHAIN_MASK) : 0ull);
+        if (incl) break;
+        base -= 32;
+      }
+    }
+    if (!tot_h && lane == 0) st_status(K.status + tile, ST_INCL | ((prefix + tot_v) & CHAIN_MASK));
+    const uint64_t S = h ? v : prefix + v;
     const uint64_t c = chain_finalize(S);
 
     if (valid) {
       if (A.out_hash) A.out_hash[item] = c;
       if (in_pin) {  // ---- pin compare (match / commit) ----
+        // Only blocks whose prefix hash matches the pin's are compared token by token; the first
+        // truly differing block always qualifies, so M stays exact whatever the hash does.
         const bool prev_ok = (k == 0) || (chain_finalize(S - g) == prev_pin_hash);
         if (prev_ok) {
-          const int pn = K.blk_n[pin_id];
-          uint32_t q[BT];
-          load16_aligned(K.blk_tok + (int64_t)pin_id * BT, q);
+          uint32_t u[BT];  // request tokens again: an L1 hit, cheaper than keeping them live
+          load_block(A.tok, tb + k * BT, nval, tok_total, u);
           const int lim = nval < pn ? nval : pn;
-          int tt = 0;
+          int lcp = 0;
           bool run = true;
 #pragma unroll
-          for (int j = 0; j < BT; ++j) {
-            run = run && j < lim && q[j] == t[j];
-            tt += run ? 1 : 0;
+          for (int i = 0; i < BT; ++i) {
+            run = run && i < lim && q[i] == u[i];
+            lcp += run ? 1 : 0;
           }
-          if (tt < lim)
+          if (lcp < lim)
             atomicMin(reinterpret_cast<unsigned long long*>(A.out_M + r),
-                      (unsigned long long)(k * BT + tt));
+                      (unsigned long long)(k * BT + lcp));
         }
       }
-      if (A.out_block) {  // ---- global table probe (lookup) ----
+      if constexpr (LOOKUP) {  // ---- global table probe (lookup) ----
         int32_t id = -1;
         if (nval == BT) {
           uint64_t s = c & K.slot_mask;
@@ -309,7 +386,7 @@ __global__ void __launch_bounds__(MT, 4) match_kernel(MatchKernelArgs K) {
               if (cand >= 0 && K.blk_n[cand] == BT) {
                 uint32_t q[BT];
                 load16_aligned(K.blk_tok + (int64_t)cand * BT, q);
-                if (tokens_equal(q, t)) id = cand;
+                if (tokens_equal(q, tk)) id = cand;
               }
               break;
             }
@@ -323,7 +400,6 @@ __global__ void __launch_bounds__(MT, 4) match_kernel(MatchKernelArgs K) {
                     (unsigned long long)(k * BT));
       }
     }
-    __syncthreads();  // window / scan storage reuse; s_tile (next ticket) visible
   }
 }
 
@@ -351,7 +427,7 @@ static int sm_count() {
 }
 
 int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStream_t st) {
-  const int64_t ntiles = (a.n_items + MT - 1) / MT;
+  const int64_t ntiles = (a.n_items + WT - 1) / WT;
   if (a.n > 0 && (a.out_M || a.out_hit)) {
     match_init_kernel<<<grid_for(a.n, 256, 1 << 20), 256, 0, st>>>(a, p->pin_len);
     SFKV_LAUNCH_CHECK("match_init_kernel");
@@ -360,8 +436,6 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   SFKV_CUDA(cudaMemsetAsync(tile_state, 0, sizeof(int64_t) * (1 + ntiles), st));
   MatchKernelArgs K;
   K.a = a;
-  K.pin_len = p->pin_len;
-  K.pin_nblk = p->pin_nblk;
   K.pin_blk = p->pin_blk;
   K.pin_hash = p->pin_hash;
   K.blk_tok = p->blk_tok;
@@ -369,15 +443,21 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   K.slots = p->slots;
   K.slot_mask = (uint64_t)p->table_slots - 1;
   K.max_pin_blocks = p->cfg.max_pin_blocks;
-  K.ntiles = ntiles;
-  K.counter = reinterpret_cast<unsigned long long*>(tile_state);
   K.status = reinterpret_cast<uint64_t*>(tile_state + 1);
   int64_t* tile_r0 = tile_state + 1 + ntiles;
   K.tile_r0 = tile_r0;
-  tile_first_kernel<<<grid_for(a.n, 256, sm_count() * 8), 256, 0, st>>>(a.blk_off, a.n, tile_r0);
-  int64_t grid = (int64_t)sm_count() * 4;  // persistent: 4 x 256-thread CTAs per SM
-  if (grid > ntiles) grid = ntiles;
-  match_kernel<<<(unsigned)grid, MT, 0, st>>>(K);
+  // records start 32-B aligned after the per-tile arrays
+  int64_t rec_off = (1 + 2 * ntiles + 3) & ~int64_t(3);
+  ReqRec* rec = reinterpret_cast<ReqRec*>(tile_state + rec_off);
+  K.rec = rec;
+  request_prep_kernel<<<grid_for(a.n + 1, 256, sm_count() * 8), 256, 0, st>>>(a, p->pin_len, rec,
+                                                                             tile_r0);
+  // persistent: 4 x 256-thread CTAs per SM; tiles assigned round-robin to warps
+  int64_t grid = (int64_t)sm_count() * MATCH_MIN_CTAS;
+  const int64_t need = (ntiles + 7) / 8;
+  if (grid > need) grid = need;
+  if (a.out_block) match_kernel<true><<<(unsigned)grid, 256, 0, st>>>(K);
+  else match_kernel<false><<<(unsigned)grid, 256, 0, st>>>(K);
   SFKV_LAUNCH_CHECK("match_kernel");
   return 0;
 }

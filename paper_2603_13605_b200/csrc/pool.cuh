@@ -108,7 +108,7 @@ int launch_payload(sfkv_pool* p, const PayloadJob& j, const void* kv_src, const 
                    const sfkv_pool* src_pool, int32_t src_wf, cudaStream_t st);
 
 int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStream_t st);
-size_t match_tile_state_elems(int64_t n_items);
+size_t match_tile_state_elems(int64_t n_items, int64_t n_requests);
 
 // Internal commit entry (device pointers). src_pool/src_wf: handoff payload source.
 int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
