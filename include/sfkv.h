@@ -155,6 +155,9 @@ int sfkv_pin_blocks(sfkv_pool* pool, int32_t wf, int32_t* ids, uint64_t* hashes,
                     int32_t* n_blocks);
 /* Refcount of every physical block (n_blocks entries). */
 int sfkv_block_refcounts(sfkv_pool* pool, uint32_t* out);
+/* Token ids of a pin (cap entries max; *n_tokens = pin length, 0 without a pin). Used to ship a
+ * pin to another process (cross-rank handoff). */
+int sfkv_pin_tokens(sfkv_pool* pool, int32_t wf, uint32_t* out, int64_t cap, int64_t* n_tokens);
 
 /* ---- gather (new): assemble pins into contiguous staging ------------------------------------
  * Request r writes its pin's KV at dst + dst_off[r], layout [slab][token (pin_len)][row]. */

@@ -597,6 +597,14 @@ int sfo_pin_blocks(sfo_pool* p, int32_t wf, int32_t* ids, uint64_t* hashes, int3
   return 0;
 }
 
+int sfo_pin_tokens(sfo_pool* p, int32_t wf, uint32_t* out, int64_t cap, int64_t* n_tokens) {
+  if (bad_wf(p, wf)) return -1;
+  int64_t L = p->pin_len[wf] < 0 ? 0 : p->pin_len[wf];
+  *n_tokens = L;
+  for (int64_t i = 0; i < L && i < cap; ++i) out[i] = p->pin_tok[wf][i];
+  return 0;
+}
+
 int sfo_block_refcounts(sfo_pool* p, uint32_t* out) {
   memcpy(out, p->blk_ref, (size_t)p->cfg.n_blocks * sizeof(uint32_t));
   return 0;

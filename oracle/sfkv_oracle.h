@@ -67,6 +67,7 @@ int sfo_stats(sfo_pool* p, sfo_pool_stats* out);
 int sfo_pin_blocks(sfo_pool* p, int32_t wf, int32_t* ids, uint64_t* hashes, int32_t cap,
                    int32_t* n_blocks);
 int sfo_block_refcounts(sfo_pool* p, uint32_t* out);
+int sfo_pin_tokens(sfo_pool* p, int32_t wf, uint32_t* out, int64_t cap, int64_t* n_tokens);
 int sfo_gather(sfo_pool* p, int64_t n, const int32_t* wf, void* dst, const int64_t* dst_off);
 int sfo_handoff(sfo_pool* src, int32_t wf_src, sfo_pool* dst, int32_t wf_dst, int32_t* status);
 

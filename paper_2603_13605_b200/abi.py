@@ -72,6 +72,7 @@ SIGNATURES = {
     "stats": [P, C.POINTER(PoolStats)],
     "pin_blocks": [P, i32, P, P, i32, C.POINTER(i32)],
     "block_refcounts": [P, P],
+    "pin_tokens": [P, i32, P, i64, C.POINTER(i64)],
     "handoff": [P, i32, P, i32, C.POINTER(i32)],
     "block_digest": [u64, u32, P],
     "chain_finalize": [u64],
@@ -281,6 +282,14 @@ class Pool:
         out = np.zeros(self.cfg.n_blocks, dtype=np.uint32)
         self.api.check("block_refcounts", self.api.block_refcounts(self.h, _ptr(out)))
         return out
+
+    def pin_tokens(self, wf):
+        n = C.c_int64()
+        self.api.check("pin_tokens", self.api.pin_tokens(self.h, int(wf), None, 0, C.byref(n)))
+        out = np.zeros(max(n.value, 1), dtype=np.uint32)
+        self.api.check("pin_tokens", self.api.pin_tokens(self.h, int(wf), _ptr(out), n.value,
+                                                         C.byref(n)))
+        return out[: n.value]
 
     def handoff_to(self, wf_src, dst: "Pool", wf_dst):
         st = C.c_int32()

@@ -554,6 +554,27 @@ __global__ void pin_tokens_kernel(const int32_t* pin_blk, const uint32_t* blk_to
     out[i] = blk_tok[(int64_t)pin_blk[i / BT] * BT + (i % BT)];
 }
 
+int sfkv_pin_tokens(sfkv_pool* p, int32_t wf, uint32_t* out, int64_t cap, int64_t* n_tokens) {
+  if (!p || !n_tokens || wf < 0 || wf >= p->cfg.max_workflows || (cap > 0 && !out))
+    return fail(SFKV_EINVAL, "pin_tokens: bad argument");
+  DeviceGuard g(p->cfg.device);
+  int64_t L = -1;
+  int32_t nb = 0;
+  if (int rc = read_pin_len(p, wf, &L)) return rc;
+  *n_tokens = L < 0 ? 0 : L;
+  if (L <= 0 || cap <= 0) return 0;
+  SFKV_CUDA(cudaMemcpy(&nb, p->pin_nblk + wf, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (int rc = p->io.ensure((size_t)nb * BT * sizeof(uint32_t))) return rc;
+  uint32_t* d = p->io.as<uint32_t>();
+  pin_tokens_kernel<<<grid_for((int64_t)nb * BT, 256, 1024), 256, 0, p->stream>>>(
+      p->pin_blk + (int64_t)wf * p->cfg.max_pin_blocks, p->blk_tok, nb, d);
+  SFKV_LAUNCH_CHECK("pin_tokens_kernel");
+  const int64_t m = L < cap ? L : cap;
+  SFKV_CUDA(cudaMemcpyAsync(out, d, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, p->stream));
+  SFKV_CUDA(cudaStreamSynchronize(p->stream));
+  return 0;
+}
+
 int sfkv_handoff(sfkv_pool* src, int32_t wf_src, sfkv_pool* dst, int32_t wf_dst, int32_t* status) {
   if (!src || !dst || !status || wf_src < 0 || wf_src >= src->cfg.max_workflows || wf_dst < 0 ||
       wf_dst >= dst->cfg.max_workflows)
