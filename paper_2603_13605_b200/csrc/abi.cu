@@ -233,13 +233,9 @@ static int match_common(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_
   cudaStream_t st = p->stream;
   const int64_t n_items = n_items_bound;  // upper bound; kernels read the exact count on device
   Carver c0;
-  const size_t o_blk = c0.take<int64_t>(n + 1), o_tmp = c0.take<int64_t>(scan_scratch_elems(n));
+  const size_t o_blk = c0.take<int64_t>(n + 1);
   if (int rc = p->small.ensure(c0.off)) return rc;
-  int64_t* blk_off = reinterpret_cast<int64_t*>(p->small.as<char>() + o_blk);
-
-  if (int rc = exclusive_scan(ReqBlocks{tok_off}, n, blk_off,
-                              reinterpret_cast<int64_t*>(p->small.as<char>() + o_tmp), st))
-    return rc;
+  int64_t* blk_off = reinterpret_cast<int64_t*>(p->small.as<char>() + o_blk);  // written by prep
   Carver cv;
   const size_t o_tile = cv.take<int64_t>(match_tile_state_elems(n_items, n));
   if (int rc = p->scratch.ensure(cv.off)) return rc;

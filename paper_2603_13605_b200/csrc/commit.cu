@@ -579,8 +579,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   a.s.scan_tmp = reinterpret_cast<int64_t*>(base + o_tmp);
 
   // 1. blocks per request, chained hashes, M = LCP(old pin, tokens)
-  if (int rc = exclusive_scan(ReqBlocks{tok_off}, n, a.s.blk_off, a.s.scan_tmp, st)) return rc;
-  MatchArgs m{};
+  MatchArgs m{};  // the match launch also writes blk_off (its prep kernel scans the requests)
   m.n = n;
   m.wf = wf;
   m.tok_off = tok_off;

@@ -82,7 +82,7 @@ struct MatchArgs {
   const int32_t* wf;         // nullable (lookup mode)
   const int64_t* tok_off;
   const uint32_t* tok;
-  const int64_t* blk_off;    // [n+1] exclusive scan of ceil(len/16)
+  int64_t* blk_off;          // [n+1] exclusive scan of ceil(len/16), written by launch_match
   int64_t n_items;
   int64_t* out_M;            // nullable
   uint64_t* out_hash;        // nullable
