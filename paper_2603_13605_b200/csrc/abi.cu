@@ -82,7 +82,7 @@ static void pool_free(sfkv_pool* p) {
   cudaFree(p->pin_len);
   cudaFree(p->pin_nblk);
   cudaFree(p->pin_blk);
-  cudaFree(p->pin_hash);
+  cudaFree(p->pin_tok);
   cudaFree(p->blk_key);
   cudaFree(p->blk_tok);
   cudaFree(p->blk_n);
@@ -159,7 +159,7 @@ int sfkv_pool_create(const sfkv_pool_config* cfg, sfkv_pool** out) {
   const size_t W = cfg->max_workflows, B = cfg->n_blocks, MB = cfg->max_pin_blocks;
   int rc = 0;
   if ((rc = dalloc(&p->pin_len, W)) || (rc = dalloc(&p->pin_nblk, W)) ||
-      (rc = dalloc(&p->pin_blk, W * MB)) || (rc = dalloc(&p->pin_hash, W * MB)) ||
+      (rc = dalloc(&p->pin_blk, W * MB)) || (rc = dalloc(&p->pin_tok, W * MB * BT)) ||
       (rc = dalloc(&p->blk_key, B)) || (rc = dalloc(&p->blk_tok, B * BT)) ||
       (rc = dalloc(&p->blk_n, B)) || (rc = dalloc(&p->blk_in_table, B)) ||
       (rc = dalloc(&p->blk_ref, B)) || (rc = dalloc(&p->blk_slot, B)) ||
@@ -523,8 +523,11 @@ int sfkv_pin_blocks(sfkv_pool* p, int32_t wf, int32_t* ids, uint64_t* hashes, in
   *n_blocks = nb;
   const int32_t m = nb < cap ? nb : cap;
   const int64_t pb = (int64_t)wf * p->cfg.max_pin_blocks;
-  if (ids && m) SFKV_CUDA(cudaMemcpy(ids, p->pin_blk + pb, m * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  if (hashes && m) SFKV_CUDA(cudaMemcpy(hashes, p->pin_hash + pb, m * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  std::vector<int32_t> idv(m > 0 ? m : 1);
+  if (m) SFKV_CUDA(cudaMemcpy(idv.data(), p->pin_blk + pb, m * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (ids && m) std::copy(idv.begin(), idv.begin() + m, ids);
+  for (int32_t k = 0; hashes && k < m; ++k)  // a block's key is its chained hash
+    SFKV_CUDA(cudaMemcpy(hashes + k, p->blk_key + idv[k], sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return 0;
 }
 

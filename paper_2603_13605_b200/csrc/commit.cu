@@ -60,7 +60,7 @@ struct CommitArgs {
   int64_t* pin_len;
   int32_t* pin_nblk;
   int32_t* pin_blk;
-  uint64_t* pin_hash;
+  uint32_t* pin_tok;
   uint64_t* blk_key;
   uint32_t* blk_tok;
   uint8_t* blk_n;
@@ -429,7 +429,13 @@ __global__ void install_kernel(CommitArgs a) {
     const int64_t k = item - a.s.blk_off[r];
     const int64_t pb = (int64_t)a.wf[r] * a.max_pin_blocks;
     a.pin_blk[pb + k] = a.s.bid[item];
-    a.pin_hash[pb + k] = a.s.hash[item];
+    // pin-major token copy (zero padded), read by the match kernel without indirection
+    const int64_t rem = a.tok_off[r + 1] - a.tok_off[r] - k * BT;
+    uint32_t t[BT];
+    load_req_block(a, r, k, (int)(rem < BT ? rem : BT), t);
+    uint4* dst = reinterpret_cast<uint4*>(a.pin_tok + (pb + k) * BT);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dst[i] = make_uint4(t[4 * i], t[4 * i + 1], t[4 * i + 2], t[4 * i + 3]);
   }
 }
 
@@ -473,7 +479,7 @@ static CommitArgs base_args(sfkv_pool* p) {
   a.pin_len = p->pin_len;
   a.pin_nblk = p->pin_nblk;
   a.pin_blk = p->pin_blk;
-  a.pin_hash = p->pin_hash;
+  a.pin_tok = p->pin_tok;
   a.blk_key = p->blk_key;
   a.blk_tok = p->blk_tok;
   a.blk_n = p->blk_n;

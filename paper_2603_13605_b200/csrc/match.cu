@@ -36,7 +36,7 @@ namespace sfkv {
 constexpr int WT = 32;                        // items per warp tile
 constexpr int MATCH_THREADS = 256;
 constexpr int PREP_THREADS = 256;
-constexpr int PREP_PER_THREAD = 4;
+constexpr int PREP_PER_THREAD = 1;
 constexpr int PREP_TILE = PREP_THREADS * PREP_PER_THREAD;
 
 constexpr uint64_t ST_AGG = 1ull << 62;
@@ -106,19 +106,29 @@ __global__ void __launch_bounds__(PREP_THREADS) match_prep_kernel(PrepArgs P) {
   }
   int64_t excl, total;
   BS(tmp).ExclusiveSum(cnt, excl, total);
-  if (tid == 0) {
+  if (tid < 32) {  // warp 0: publish, then look back 32 predecessor tiles per read
+    const int lane = tid;
+    if (lane == 0) st_status(P.pstatus + tile, (tile == 0 ? ST_INCL : ST_AGG) | (uint64_t)total);
     uint64_t prefix = 0;
-    st_status(P.pstatus + tile, (tile == 0 ? ST_INCL : ST_AGG) | (uint64_t)total);
-    for (int64_t p = tile - 1; p >= 0; --p) {
+    for (int64_t base = tile - 1; base >= 0; base -= 32) {
+      const int64_t p = base - lane;
       uint64_t s;
-      do {
-        s = ld_status(P.pstatus + p);
-      } while (s == 0);
-      prefix += s & CHAIN_MASK;
-      if ((s & ~CHAIN_MASK) == ST_INCL) break;
+      unsigned incl;
+      int first;
+      for (;;) {  // predecessors hold earlier tickets, so they are running: plain spin
+        s = p >= 0 ? ld_status(P.pstatus + p) : ST_INCL;
+        incl = __ballot_sync(0xffffffffu, (s & ~CHAIN_MASK) == ST_INCL);
+        first = incl ? __ffs(incl) - 1 : 31;
+        const unsigned need = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
+        if ((__ballot_sync(0xffffffffu, s != 0) & need) == need) break;
+      }
+      prefix += warp_sum(lane <= first ? (s & CHAIN_MASK) : 0ull);
+      if (incl) break;
     }
-    if (tile > 0) st_status(P.pstatus + tile, ST_INCL | (prefix + (uint64_t)total));
-    s_prefix = (int64_t)prefix;
+    if (lane == 0) {
+      if (tile > 0) st_status(P.pstatus + tile, ST_INCL | (prefix + (uint64_t)total));
+      s_prefix = (int64_t)prefix;
+    }
   }
   __syncthreads();
   int64_t b = s_prefix + excl;
@@ -160,7 +170,7 @@ __global__ void __launch_bounds__(PREP_THREADS) match_prep_kernel(PrepArgs P) {
 struct MatchKernelArgs {
   MatchArgs a;
   const ReqRec* rec;
-  const int32_t* pin_blk;
+  const uint32_t* pin_tok;
   const uint32_t* blk_tok;
   const uint8_t* blk_n;
   const Slot* slots;
@@ -178,7 +188,7 @@ struct Win {  // lane j holds request r0 + j of a tile's window
 };
 
 struct Ctx {  // one lane's block of one tile
-  int64_t item, r, k, start, pin_base;
+  int64_t item, r, k, start, pin_base, pin_len;
   int32_t nval;
   bool valid, in_pin;
 };
@@ -245,6 +255,7 @@ __device__ __forceinline__ Ctx resolve(const MatchKernelArgs& K, const Win& w, i
   c.start = tb + c.k * BT;
   c.in_pin = match_mode && c.valid && pl >= 0 && c.k < (pl + BT - 1) / BT;
   c.pin_base = (int64_t)wf * K.max_pin_blocks;
+  c.pin_len = pl;
   return c;
 }
 
@@ -301,6 +312,10 @@ __device__ __forceinline__ void load_block(const uint32_t* __restrict__ tok, int
     if (j >= nval) t[j] = 0u;
 }
 
+// One warp per 32-block tile, one block per lane, non-persistent: at 46 registers ~40 warps per SM
+// keep enough tiles in flight to cover the window -> tokens/pin-tokens round trips. (A persistent
+// cp.async-pipelined variant measured slower: with the inter-warp dependencies gone, occupancy and
+// not load latency decides; see profiles/round1/README.md.)
 __global__ void __launch_bounds__(MATCH_THREADS) match_block_kernel(MatchKernelArgs K) {
   const MatchArgs& A = K.a;
   const int lane = threadIdx.x & 31;
@@ -311,8 +326,6 @@ __global__ void __launch_bounds__(MATCH_THREADS) match_block_kernel(MatchKernelA
   const bool match_mode = A.out_M != nullptr;
   const Ctx c = resolve(K, load_win(K, K.tile_r0[tile]), tile, n_items, match_mode);
 
-  int32_t pid = 0;
-  if (c.in_pin) pid = __ldg(K.pin_blk + c.pin_base + c.k);
   uint32_t t[BT];
   if (c.valid) {
     load_block(A.tok, c.start, c.nval, tok_total, t);
@@ -324,10 +337,11 @@ __global__ void __launch_bounds__(MATCH_THREADS) match_block_kernel(MatchKernelA
   // ---- M: first differing token against the pin's block, warp segmented min, one atomic ----
   if (match_mode) {
     unsigned long long m = ~0ull;
-    if (c.in_pin) {
+    if (c.in_pin) {  // the pin's block k from its pin-major token copy (coalesced, no indirection)
       uint32_t q[BT];
-      load16_aligned(K.blk_tok + (int64_t)pid * BT, q);
-      const int pn = K.blk_n[pid];
+      load16_aligned(K.pin_tok + (c.pin_base + c.k) * BT, q);
+      const int64_t prem = c.pin_len - c.k * BT;
+      const int pn = (int)(prem < BT ? prem : BT);
       const int lim = c.nval < pn ? c.nval : pn;
       int lcp = 0;
       bool run = true;
@@ -378,6 +392,10 @@ __global__ void __launch_bounds__(MATCH_THREADS) match_chain_kernel(MatchKernelA
   const int64_t item = tile * WT + lane;
   const bool valid = item < n_items;
   const uint64_t loc = valid ? K.local[item] : 0ull;
+  // the first 32 predecessor statuses are read together with the local sums (speculatively:
+  // unused when the tile starts with a segment head)
+  const int64_t p0 = tile - 1 - lane;
+  const uint64_t st0 = p0 >= 0 ? K.status[p0] : ST_INCL;
   const int h = (int)(loc >> 63);
   const uint64_t v = loc & CHAIN_MASK;
   // carry into the tile's first segment: every status is final, walk back 32 tiles per read
@@ -385,7 +403,7 @@ __global__ void __launch_bounds__(MATCH_THREADS) match_chain_kernel(MatchKernelA
   if (!__shfl_sync(0xffffffffu, h, 0) && tile > 0) {
     for (int64_t base = tile - 1;; base -= 32) {
       const int64_t p = base - lane;
-      const uint64_t st = p >= 0 ? K.status[p] : ST_INCL;
+      const uint64_t st = base == tile - 1 ? st0 : (p >= 0 ? K.status[p] : ST_INCL);
       const unsigned incl = __ballot_sync(0xffffffffu, (st & ~CHAIN_MASK) == ST_INCL);
       const int first = incl ? __ffs(incl) - 1 : 31;
       prefix += warp_sum(lane <= first ? (st & CHAIN_MASK) : 0ull);
@@ -461,7 +479,7 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   MatchKernelArgs K;
   K.a = a;
   K.rec = rec;
-  K.pin_blk = p->pin_blk;
+  K.pin_tok = p->pin_tok;
   K.blk_tok = p->blk_tok;
   K.blk_n = p->blk_n;
   K.slots = p->slots;

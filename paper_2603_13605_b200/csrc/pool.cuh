@@ -2,9 +2,10 @@
 //
 // HBM layout (all arrays device-resident, sized at pool creation):
 //   pins   pin_len[W] i64 (-1 = no pin), pin_nblk[W] i32,
-//          pin_blk[W][MB] i32 (block table), pin_hash[W][MB] u64 (chained hash per pin block,
-//          pin-major so the match kernel reads a pin's hashes coalesced)
-//   blocks blk_key[B] u64, blk_tok[B][16] u32 (tokens: verify-on-hit and LCP tails),
+//          pin_blk[W][MB] i32 (block table), pin_tok[W][MB][16] u32 (the pin's tokens block by
+//          block, pin-major: the match kernel compares a request against its pin with coalesced
+//          reads and no block-id indirection; the block's chained hash is blk_key[pin_blk])
+//   blocks blk_key[B] u64, blk_tok[B][16] u32 (tokens: verify-on-hit for shared blocks),
 //          blk_n[B] u8 (valid tokens), blk_in_table[B] u8, blk_ref[B] u32, blk_slot[B] i64,
 //          free_bits[ceil(B/32)] u32 (1 = free)
 //   table  slots[S] of 16 B {u64 key, i32 block, i32 pad} (open addressing, linear probing,
@@ -50,7 +51,7 @@ struct sfkv_pool {
   int64_t* pin_len = nullptr;
   int32_t* pin_nblk = nullptr;
   int32_t* pin_blk = nullptr;
-  uint64_t* pin_hash = nullptr;
+  uint32_t* pin_tok = nullptr;  // [W][MB][16] a pin's tokens, block by block (pin-major copy)
   uint64_t* blk_key = nullptr;
   uint32_t* blk_tok = nullptr;
   uint8_t* blk_n = nullptr;
