@@ -363,6 +363,8 @@ def run_ours(args, rank, world, local_rank):
         e2e_value = sfdist.aggregate_rate(req_blocks, local_e2e_ms, dev)
 
         kv = None if args.no_kv else kv_legs(args, api, dev, stream, hbm_peak, rank)
+        c5 = None if args.no_c5 else lookup_leg(args, api, dev, stream, hbm_peak, rank)
+        c4 = None if args.no_c4 else long_context_leg(args, api, dev, stream, hbm_peak, rank)
     clocks = clk.summary()
 
     # ---- roofline of the match kernel: algorithmic bytes of one launch --------------------
@@ -395,6 +397,10 @@ def run_ours(args, rank, world, local_rank):
             "step_ms_min_max": [min(step_ms), max(step_ms)]}
     if kv:
         line["kv"] = kv
+    if c5:
+        line["c5_lookup"] = c5
+    if c4:
+        line["c4_long_context"] = c4
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
     pool.close()
@@ -496,6 +502,207 @@ def kv_legs(args, api, dev, stream, hbm_peak, rank):
                              "note": "whole commit pipeline (metadata kernels + COW + scatter)"}}
 
 
+def lookup_leg(args, api, dev, stream, hbm_peak, rank):
+    """C5 (BASELINE configs[4]): heavy prefix sharing. Resident: 8,192 system prompts of 64 blocks
+    plus 32,768 workflows = a system prompt + 16 private blocks, i.e. 1,048,576 distinct resident
+    blocks in the dedup table (every workflow pin shares its prompt's 64 blocks). One step =
+    sfkv_lookup_batch_dev over 100k stage prefixes = a system prompt + 1..63 private blocks, half
+    continuing a resident workflow's private context: ~9.6 M chained-hash probes, token-verified on
+    every key hit (a global lookup the reference has no counterpart for)."""
+    import torch
+
+    from paper_2603_13605_b200.abi import Config, Pool
+    rng = np.random.default_rng(args.seed + 5 + rank)
+    n_sys, sys_blocks, n_wf, priv_blocks = 8192, 64, 32768, 16
+    sys_tok = rng.integers(1, 1 << 30, size=(n_sys, sys_blocks * BT), dtype=np.uint32)
+    priv_tok = rng.integers(1, 1 << 30, size=(n_wf, priv_blocks * BT), dtype=np.uint32)
+    W = n_sys + n_wf
+    cfg = Config(max_workflows=W, n_blocks=1 << 21, capacity_tokens=1 << 50,
+                 max_pin_blocks=sys_blocks + priv_blocks + 1, table_log2=23, device=dev)
+    pool = Pool(api, cfg)
+    t0 = time.perf_counter()
+    for c0 in range(0, n_sys, 4096):  # owners of the system prompts
+        ids = np.arange(c0, min(n_sys, c0 + 4096))
+        off = np.arange(len(ids) + 1, dtype=np.int64) * sys_blocks * BT
+        assert pool.commit(ids.astype(np.int32), off, np.ascontiguousarray(sys_tok[ids]).ravel()).all()
+    wlen = (sys_blocks + priv_blocks) * BT
+    for c0 in range(0, n_wf, 4096):  # workflows: prompt + private context
+        ids = np.arange(c0, min(n_wf, c0 + 4096))
+        tok = np.concatenate([sys_tok[ids % n_sys], priv_tok[ids]], axis=1).ravel()
+        off = np.arange(len(ids) + 1, dtype=np.int64) * wlen
+        assert pool.commit((n_sys + ids).astype(np.int32), off, tok).all()
+    st = pool.stats()
+    log(f"[rank {rank}] c5: {st['table_live']} resident blocks in the table "
+        f"({time.perf_counter() - t0:.1f}s)")
+    # the batch
+    P = args.c5_prefixes
+    s = rng.integers(0, n_sys, size=P)
+    npriv = rng.integers(1, 64, size=P)
+    cont = rng.random(P) < 0.5
+    wsel = s + n_sys * rng.integers(0, n_wf // n_sys, size=P)  # a resident workflow on prompt s
+    lens = (sys_blocks + npriv) * BT
+    off = np.zeros(P + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    tok = np.empty(int(off[-1]), np.uint32)
+    fresh = rng.integers(1, 1 << 30, size=int((npriv * BT).sum()), dtype=np.uint32)
+    f0 = 0
+    for i in range(P):
+        b = off[i]
+        tok[b:b + sys_blocks * BT] = sys_tok[s[i]]
+        b += sys_blocks * BT
+        npt = npriv[i] * BT
+        tok[b:b + npt] = fresh[f0:f0 + npt]
+        f0 += npt
+        if cont[i]:
+            k = min(npriv[i], priv_blocks) * BT
+            tok[b:b + k] = priv_tok[wsel[i], :k]
+    expect_hit = BT * (sys_blocks + np.where(cont, np.minimum(npriv, priv_blocks), 0))
+    n_blocks = int(off[-1] // BT)
+    d_off = torch.from_numpy(off).to(dev)
+    d_tok = torch.from_numpy(tok.view(np.int32)).to(dev)
+    d_blk = torch.zeros(n_blocks, dtype=torch.int32, device=dev)
+    d_hit = torch.zeros(P, dtype=torch.int64, device=dev)
+    api.check("set_stream", api.pool_set_stream(pool.h, C.c_void_p(stream.cuda_stream)))
+
+    def step():
+        api.check("lookup_dev", api.lookup_batch_dev(pool.h, P, C.c_void_p(d_off.data_ptr()),
+                  C.c_void_p(d_tok.data_ptr()), int(off[-1]), C.c_void_p(d_blk.data_ptr()),
+                  C.c_void_p(d_hit.data_ptr())))
+    step()
+    torch.cuda.synchronize()
+    assert (d_hit.cpu().numpy() == expect_hit).all(), "lookup hit lengths differ from construction"
+    l2 = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        l2.zero_()
+        step()
+    times = []
+    for _ in range(args.steps):
+        l2.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+    ms = float(np.mean(times))
+    hits = int(expect_hit.sum() // BT)
+    # per block: 64 B tokens + 16 B table slot + 4 B block id out, + 64 B token verify per key
+    # hit; per request 32 B record + 8 B tok_off + 8 B hit length
+    alg = 84 * n_blocks + 64 * hits + 48 * P
+    pool.close()
+    return {"workload": "C5: 1,048,576 resident blocks (8,192 shared 64-block system prompts + "
+                        "32,768 x 16 private), lookup of 100k prefixes (prompt + 1..63 blocks)",
+            "prefixes": P, "blocks_per_step": n_blocks, "hit_blocks": hits, "ms": ms,
+            "blocks_per_s": n_blocks / (ms / 1e3),
+            "roofline": {"bound": "hbm", "alg_bytes_per_step": alg,
+                         "achieved": alg / (ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": alg / (ms / 1e3) / 1e9 / hbm_peak}}
+
+
+def long_context_leg(args, api, dev, stream, hbm_peak, rank):
+    """C4 (BASELINE configs[3]): long-context retention under eviction pressure. A Llama-3-8B pool
+    sized to ~90 % of the GPU's HBM (77,247 x 2 MiB blocks when it fits: 1,235,952 tokens of logical
+    capacity) holds nine 131,064-token contexts (utilization 95 % > tau' = 0.85).
+    Measured: gather of a whole 16 GiB pin into contiguous staging; a stage wave (every resident
+    workflow appends 100 tokens: copy-on-share of the 8-row boundary block + scatter); the pressure
+    step (sfmm_pressure_argmin over the tracker, then sfkv_flush of the LRU victim: 8,192 blocks
+    released); and admission of a new 16 GiB context (commit + scatter from staging)."""
+    import torch
+
+    from paper_2603_13605_b200.abi import Config, Pool, csr
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    ctx = 131_072 - 8
+    tok_bytes = KV_SLABS * KV_ROW
+    stage_bytes = (ctx + 128) * tok_bytes
+    free, total = torch.cuda.mem_get_info(dev)
+    budget = free - stage_bytes - (3 << 30)
+    pool_blocks = int(min(77_247, budget // BLOCK_BYTES))
+    if pool_blocks < 9 * (ctx // BT + 8) + 256:  # nine residents + append headroom
+        return {"skipped": f"needs ~150 GiB free HBM, {free / 2**30:.1f} GiB available"}
+    W = 16
+    cfg = Config(max_workflows=W, n_blocks=pool_blocks, capacity_tokens=pool_blocks * BT,
+                 max_pin_blocks=(ctx + 256) // BT + 2, table_log2=int(math.log2(pool_blocks)) + 2,
+                 n_slabs=KV_SLABS, slab_row_bytes=KV_ROW, device=dev)
+    pool = Pool(api, cfg)
+    staging = torch.empty(stage_bytes, dtype=torch.uint8, device=dev)
+    rng = np.random.default_rng(args.seed + 4 + rank)
+    ctxs = [rng.integers(1, 1 << 30, size=ctx).astype(np.uint32) for _ in range(W)]
+    zero = np.zeros(1, np.int64)
+
+    def timed(fn):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
+
+    def admit(w):  # a new 131,064-token context: prefill KV scattered into fresh blocks
+        off, tok = csr([ctxs[w]])
+        st = []
+        ms = timed(lambda: st.append(pool.commit(np.array([w], np.int32), off, tok, kv_src=staging,
+                                                 kv_src_off=zero)))
+        assert st[0][0] == 1, "admission rejected"
+        return ms
+
+    admit_ms = [admit(w) for w in range(9)]
+    util = pool.cache_utilization()
+    # gather a whole pin (16 GiB read + 16 GiB write)
+    gw = torch.tensor([0], dtype=torch.int32, device=dev)
+    go = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def gather():
+        api.check("gather", api.gather_dev(pool.h, 1, C.c_void_p(gw.data_ptr()),
+                                           C.c_void_p(staging.data_ptr()), C.c_void_p(go.data_ptr())))
+        api.check("sync", api.pool_sync(pool.h))
+    gather()
+    g_ms = float(np.median([timed(gather) for _ in range(max(3, min(args.steps, 5)))]))
+    g_bytes = 2 * ctx * tok_bytes
+    # stage wave: 100-token appends for the nine residents (M = ctx: 8 COW rows + 100 scattered)
+    wave_ms = []
+    for it in range(3):
+        seqs = [np.concatenate([ctxs[w], rng.integers(1, 1 << 30, size=100).astype(np.uint32)])
+                for w in range(9)]
+        off, tok = csr(seqs)
+        kvo = np.arange(9, dtype=np.int64) * 100 * tok_bytes
+        me = np.full(9, ctx, np.int64)
+        wave_ms.append(timed(lambda: pool.commit(np.arange(9, dtype=np.int32), off, tok,
+                                                 kv_src=staging, kv_src_off=kvo, m_expected=me)))
+    wave_bytes = 9 * 2 * (100 + ctx % BT) * tok_bytes
+    # pressure: tracker entries (ts = last StageComplete), LRU victim on the GPU, then evict + admit
+    ts = np.array([5.0, 3.0, 9.0, 7.0, 4.0, 8.0, 6.0, 2.5, 10.0])  # workflow 7 is the oldest
+    victim = np.full(1, -1, np.int64)
+    backend, rank_, infl = np.zeros(9, np.int32), np.arange(9, dtype=np.uint32), np.zeros(9, np.int32)
+    pres, utilv = np.ones(9, np.uint8), np.array([util])
+    api.check("pressure", api.pressure_argmin(
+        dev, 9, backend.ctypes.data, ts.ctypes.data, rank_.ctypes.data, infl.ctypes.data,
+        pres.ctypes.data, 1, utilv.ctypes.data, 0.85, victim.ctypes.data))
+    assert victim[0] == 7, f"pressure victim {victim[0]} != LRU 7"
+    freed = []
+    flush_ms = timed(lambda: freed.append(pool.flush(int(victim[0]))))
+    readmit_ms = admit(9)
+    adm_bytes = 2 * ctx * tok_bytes
+    pool.close()
+    del staging
+    torch.cuda.empty_cache()
+    a_ms = float(np.median(admit_ms))
+    return {"pool_blocks": pool_blocks, "pool_gb": pool_blocks * BLOCK_BYTES / 1e9,
+            "pool_frac_of_180gb": pool_blocks * BLOCK_BYTES / 180e9,
+            "pool_frac_of_device_memory": pool_blocks * BLOCK_BYTES / total,
+            "utilization_after_fill": util, "context_tokens": ctx,
+            "gather_16gib": {"ms": g_ms, "gbps": g_bytes / (g_ms / 1e3) / 1e9,
+                             "frac_of_hbm": g_bytes / (g_ms / 1e3) / 1e9 / hbm_peak},
+            "admit_commit": {"ms": a_ms, "gbps": adm_bytes / (a_ms / 1e3) / 1e9,
+                             "frac_of_hbm": adm_bytes / (a_ms / 1e3) / 1e9 / hbm_peak,
+                             "readmit_after_evict_ms": readmit_ms},
+            "stage_wave_9x100": {"ms": float(np.median(wave_ms)),
+                                 "gbps": wave_bytes / (np.median(wave_ms) / 1e3) / 1e9},
+            "evict": {"victim": int(victim[0]), "expected_lru": 7, "freed_tokens": freed[0],
+                      "flush_ms": flush_ms}}
+
+
 def cpu_baseline(args):
     L = ref_lib()
     n_sample = args.cpu_sample
@@ -522,6 +729,9 @@ def main():
     ap.add_argument("--workflows", type=int, default=10_000)
     ap.add_argument("--seed", type=int, default=0x0A1A + 2)
     ap.add_argument("--no-kv", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-c4", action="store_true")
+    ap.add_argument("--c5-prefixes", type=int, default=100_000)
     ap.add_argument("--kv-pool-gib", type=int, default=64)
     ap.add_argument("--kv-workflows", type=int, default=200)
     ap.add_argument("--kv-context", type=int, default=2008)
