@@ -13,7 +13,7 @@
 //   lookup  : probe the global table for c_k (full blocks), verify tokens, report the block id.
 //
 // Launches (no kernel ever waits on another CTA or warp):
-//   match_prep_kernel   single-pass request scan (decoupled look-back over 1024-request tiles):
+//   match_prep_kernel   single-pass request scan (decoupled look-back over 256-request tiles):
 //                       blk_off, a 32-B record per request {blk_off, tok_off, pin_len, wf}, the
 //                       tile -> first-request map, M / hit initial values.
 //   match_block_kernel  one warp per 32-block tile, one block per lane: request window (one record
