@@ -203,7 +203,12 @@ int sfmap_cost_batch(int32_t device, int64_t n, int32_t c, const int64_t* P, con
                      int32_t* out_choice, double* out_cost);
 
 /* ---- the chained block hash (shared by the GPU kernels and the CPU oracle) -------------------
- * digest(k, n, t) of block k with n valid tokens t[0..n); chain(k) = fin(sum_{i<=k} digest(i)).
+ * digest(k, n, t) of block k with n valid tokens t[0..n) (t[j] = 0 for j >= n):
+ *   K_s[j]  = bits [32s, 32s+32) of mix64(16 s + j + 1)            (s = 0, 1; j < 16)
+ *   acc_s   = sum_{i<8} (t[2i] + K_s[2i]) * (t[2i+1] + K_s[2i+1])  (u32 adds, u64 products/sum)
+ *   digest  = mix64(acc_0 ^ rotl64(acc_1, 32) ^ (k * 0xD6E8FEB86659FD93 + n))
+ * mix64 = splitmix64's finaliser. chain(k) = fin(sum_{i<=k} digest(i) mod 2^62),
+ * fin(s) = mix64(s ^ 0x5851F42D4C957F2D), raised to >= 2 (keys 0/1 are reserved).
  * Exposed for tests and for hosts that precompute keys. */
 uint64_t sfkv_block_digest(uint64_t k, uint32_t n, const uint32_t* t);
 uint64_t sfkv_chain_finalize(uint64_t prefix_sum);

@@ -32,17 +32,28 @@ static uint64_t mix64(uint64_t x) {
   return x;
 }
 
-/* digest(k, n, t): words w_i = t[2i] | t[2i+1] << 32 (tokens at i >= n read as 0),
- * acc = sum_i mix64(w_i ^ (i+1)*G), digest = mix64(acc ^ mix64(k*H + n)). */
+/* digest(k, n, t) (the definition in include/sfkv.h): tokens at i >= n read as 0;
+ * K_s[j] = 32-bit slice s (0 = low, 1 = high) of mix64(16 s + j + 1);
+ * acc_s = sum_{i<8} (t[2i] + K_s[2i] mod 2^32) * (t[2i+1] + K_s[2i+1] mod 2^32) mod 2^64;
+ * digest = mix64(acc_0 ^ rotl64(acc_1, 32) ^ (k*H + n)). */
+static uint32_t nh_key(int set, int j) {
+  uint64_t m = mix64((uint64_t)(set * 16 + j + 1));
+  return (uint32_t)(set ? m >> 32 : m);
+}
+
 uint64_t sfo_block_digest(uint64_t k, uint32_t n, const uint32_t* t) {
-  uint64_t acc = 0;
-  for (uint32_t i = 0; i < 8; ++i) {
-    uint64_t lo = (2 * i < n) ? t[2 * i] : 0;
-    uint64_t hi = (2 * i + 1 < n) ? t[2 * i + 1] : 0;
-    uint64_t w = lo | (hi << 32);
-    acc += mix64(w ^ ((uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull));
+  uint64_t acc[2] = {0, 0};
+  for (int s = 0; s < 2; ++s) {
+    for (uint32_t i = 0; i < 8; ++i) {
+      uint32_t lo = (2 * i < n) ? t[2 * i] : 0;
+      uint32_t hi = (2 * i + 1 < n) ? t[2 * i + 1] : 0;
+      uint32_t a = lo + nh_key(s, (int)(2 * i));
+      uint32_t b = hi + nh_key(s, (int)(2 * i + 1));
+      acc[s] += (uint64_t)a * (uint64_t)b;
+    }
   }
-  return mix64(acc ^ mix64(k * 0xD6E8FEB86659FD93ull + n));
+  uint64_t rot = (acc[1] << 32) | (acc[1] >> 32);
+  return mix64(acc[0] ^ rot ^ (k * 0xD6E8FEB86659FD93ull + n));
 }
 
 /* chain(k) = fin(sum_{i<=k} digest(i) mod 2^62); keys 0 and 1 are reserved (empty / tombstone). */

@@ -143,7 +143,7 @@ uint64_t sfkv_chain_finalize(uint64_t s) { return chain_finalize(s); }
 int sfkv_pool_create(const sfkv_pool_config* cfg, sfkv_pool** out) {
   if (!cfg || !out) return fail(SFKV_EINVAL, "pool_create: null argument");
   if (cfg->max_workflows <= 0 || cfg->n_blocks <= 0 || cfg->capacity_tokens <= 0 ||
-      cfg->max_pin_blocks <= 0 || cfg->table_log2 < 4 || cfg->table_log2 > 40 || cfg->n_slabs < 0 ||
+      cfg->max_pin_blocks <= 0 || cfg->max_pin_blocks > (1 << 26) || cfg->table_log2 < 4 || cfg->table_log2 > 40 || cfg->n_slabs < 0 ||
       (cfg->n_slabs > 0 && (cfg->slab_row_bytes <= 0 || cfg->slab_row_bytes % 16 != 0)) ||
       cfg->n_blocks >= INT32_MAX)
     return fail(SFKV_EINVAL, "pool_create: invalid configuration");
@@ -159,7 +159,7 @@ int sfkv_pool_create(const sfkv_pool_config* cfg, sfkv_pool** out) {
   const size_t W = cfg->max_workflows, B = cfg->n_blocks, MB = cfg->max_pin_blocks;
   int rc = 0;
   if ((rc = dalloc(&p->pin_len, W)) || (rc = dalloc(&p->pin_nblk, W)) ||
-      (rc = dalloc(&p->pin_blk, W * MB)) || (rc = dalloc(&p->pin_tok, W * MB * BT)) ||
+      (rc = dalloc(&p->pin_blk, W * MB)) || (rc = dalloc(&p->pin_tok, W * (size_t)pin_groups(*cfg) * 32 * BT)) ||
       (rc = dalloc(&p->blk_key, B)) || (rc = dalloc(&p->blk_tok, B * BT)) ||
       (rc = dalloc(&p->blk_n, B)) || (rc = dalloc(&p->blk_in_table, B)) ||
       (rc = dalloc(&p->blk_ref, B)) || (rc = dalloc(&p->blk_slot, B)) ||

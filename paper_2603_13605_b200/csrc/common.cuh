@@ -19,7 +19,7 @@ constexpr uint64_t KEY_TOMB = 1ull;            // table key: deleted
 constexpr int64_t NO_OWNER = INT64_MAX;
 
 // ---- the chained block hash (include/sfkv.h; identical to the oracle's restatement) ----------
-__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+__host__ __device__ constexpr uint64_t mix64(uint64_t x) {
   x ^= x >> 30;
   x *= 0xbf58476d1ce4e5b9ull;
   x ^= x >> 27;
@@ -28,16 +28,28 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x;
 }
 
+// NH keys (UMAC-style pair hash): key j of set s is a 32-bit slice of mix64(s * 16 + j + 1).
+__host__ __device__ constexpr uint32_t nh_key(int set, int j) {
+  return (uint32_t)(mix64((uint64_t)(set * 16 + j + 1)) >> (set ? 32 : 0));
+}
+
 // digest of block k with n valid tokens; t[i] for i >= n must already be zero.
+//   acc_s = sum_{i<8} (t[2i] + K_s[2i]) * (t[2i+1] + K_s[2i+1])   (32-bit adds, 64-bit products)
+//   digest = mix64(acc_0 ^ rotl(acc_1, 32) ^ (k * H + n))
+// Two NH passes (each 2^-32-almost-universal on 32-bit words) under one 64-bit finaliser: a
+// 64-bit non-cryptographic key at ~50 integer instructions per block. M never depends on it
+// (it is token-compared); the dedup table verifies the block's tokens on every key hit.
 __host__ __device__ __forceinline__ uint64_t block_digest_words(uint64_t k, uint32_t n,
                                                                 const uint32_t* t) {
-  uint64_t acc = 0;
+  uint64_t a0 = 0, a1 = 0;
 #pragma unroll
-  for (uint32_t i = 0; i < 8; ++i) {
-    uint64_t w = (uint64_t)t[2 * i] | ((uint64_t)t[2 * i + 1] << 32);
-    acc += mix64(w ^ ((uint64_t)(i + 1) * 0x9E3779B97F4A7C15ull));
+  for (int i = 0; i < 8; ++i) {
+    a0 += (uint64_t)(uint32_t)(t[2 * i] + nh_key(0, 2 * i)) *
+          (uint64_t)(uint32_t)(t[2 * i + 1] + nh_key(0, 2 * i + 1));
+    a1 += (uint64_t)(uint32_t)(t[2 * i] + nh_key(1, 2 * i)) *
+          (uint64_t)(uint32_t)(t[2 * i + 1] + nh_key(1, 2 * i + 1));
   }
-  return mix64(acc ^ mix64(k * 0xD6E8FEB86659FD93ull + n));
+  return mix64(a0 ^ ((a1 << 32) | (a1 >> 32)) ^ (k * 0xD6E8FEB86659FD93ull + n));
 }
 
 // The chain sum is taken mod 2^62 so a look-back status word can carry it next to a 2-bit flag.

@@ -8,55 +8,93 @@
 //             token of block k against the pin's block k (blocks that match contribute nothing; M
 //             starts at min(P, pin_len)). Every in-pin block is compared, so the minimum — the
 //             first truly differing block — is exact with no dependence on hashing.
-//   digest  = block_digest(k, n, tokens), per block
+//   digest  = block_digest(k, n, tokens), per block (include/sfkv.h)
 //   c_k     = chain_finalize(sum_{i<=k} digest_i mod 2^62)   (chained block hash, segmented scan)
 //   lookup  : probe the global table for c_k (full blocks), verify tokens, report the block id.
 //
-// Launches (no kernel ever waits on another CTA or warp):
+// Launches (no kernel ever waits on another CTA or warp; consecutive launches overlap their
+// prologues with the predecessor's tail through programmatic dependent launch):
 //   match_prep_kernel   single-pass request scan (decoupled look-back over 256-request tiles):
-//                       blk_off, a 32-B record per request {blk_off, tok_off, pin_len, wf}, the
-//                       tile -> first-request map, M / hit initial values.
-//   match_block_kernel  one warp per 32-block tile, one block per lane: request window (one record
-//                       per lane + shuffle search), 16-B vector token loads at any alignment, block
-//                       id + pin-block tokens, in-block LCP, warp segmented-min and one atomicMin per
-//                       (warp, request). When hashes are wanted it also runs the warp segmented scan
-//                       of digests and writes each block's local inclusive sum (with its segment-head
-//                       bit) and the tile's aggregate — final values, nobody waits for them.
-//   match_chain_kernel  (hashes / lookup only) one warp per tile: carry = sum of the preceding
-//                       tiles' aggregates back to the nearest tile holding the request's head (32
-//                       status words per read), chained hashes out, table probe in lookup mode.
-// Algorithmic bytes per block: 64 B tokens + 4 B block id + 64 B pin tokens (blocks inside the pin)
-// + 8 B hash out when requested; lookup mode + 16 B table slot (+ 64 B verify on a key hit);
-// + 32 B per request. Implementation traffic on top: 8 B written + read per block (local sums)
-// when hashes are wanted. HBM-bound integer work: no tensor cores.
+//                       blk_off, a 32-B record per request {blk_off, tok_off, len, pin_len, wf}
+//                       (the dependent wf -> pin_len load happens once per request), a 32-B tile
+//                       record per 32-block tile (the request holding its first block, in
+//                       tile-relative coordinates), M / hit initial values.
+//   match_block_kernel  one warp per 32-block tile, one block per lane. Lanes resolve their block
+//                       from the tile record (one broadcast load) or, for tiles crossing a request
+//                       boundary, from the request window (one record per lane + a 5-step
+//                       shuffle search). Match mode stages the tile's token range (contiguous in
+//                       the CSR batch) into shared memory with one cp.async.bulk per warp and
+//                       reads it with bank-rotated 16-B loads; the pin's blocks come from the
+//                       token-major pin copy, one or two 128-B lines per warp load. (Lane-per-block
+//                       16-B global loads are 64 B apart: 16 lines per warp instruction, which
+//                       made L1 the limiter at 81 %.) M: a block whose 16 words all agree with
+//                       the pin's has no mismatch; only differing blocks compute the exact first
+//                       mismatch, and only the first mismatching lane of each request segment
+//                       issues an atomicMin (ballot arithmetic). Hashes: NH digest per block, one
+//                       warp inclusive scan, segment correction from the head ballot; each
+//                       block's local sum and the tile aggregate are final when written.
+//   match_chain_kernel  (hashes / lookup only) one warp per 8 (hash) / 4 (lookup) consecutive
+//                       tiles: the carry into the first tile walks back over the predecessors'
+//                       final aggregates (32 per read); carries between the warp's own tiles come
+//                       from its own loads. Lookup mode probes the table for every full block (the
+//                       warp's probes in flight together) and verifies tokens on a key hit.
+// Algorithmic bytes per block: 64 B tokens + 64 B pin tokens (blocks inside the pin) + 8 B hash
+// out when requested; lookup mode + 16 B table slot (+ 64 B verify on a key hit); + 32 B per
+// request. Implementation traffic on top: 8 B written + read per block (local sums) when hashes
+// are wanted, + 4 B written + read per block (request id) in lookup mode. HBM-bound integer work:
+// no tensor cores.
 #include "pool.cuh"
 
 namespace sfkv {
 
 constexpr int WT = 32;                        // items per warp tile
 constexpr int MATCH_THREADS = 256;
+// chain pass tiles per warp: hash-only warps are latency-bound on one look-back, lookup warps
+// also carry the table probes
+#ifndef SFKV_CH_TPW_HASH
+#define SFKV_CH_TPW_HASH 8
+#endif
+constexpr int CH_TPW_HASH = SFKV_CH_TPW_HASH;
+constexpr int CH_TPW_LOOKUP = 4;
 constexpr int PREP_THREADS = 256;
-constexpr int PREP_PER_THREAD = 1;
-constexpr int PREP_TILE = PREP_THREADS * PREP_PER_THREAD;
+constexpr int PREP_TILE = PREP_THREADS;
 
 constexpr uint64_t ST_AGG = 1ull << 62;
 constexpr uint64_t ST_INCL = 2ull << 62;
+constexpr uint32_t RK_FULL = 1u << 31;        // lookup mode: request id | full-block flag
+
+
 
 struct __align__(32) ReqRec {
   int64_t blk_off;  // first item of the request
   int64_t tok_off;  // first token
-  int64_t pin_len;  // -1: no pin (or lookup mode)
+  int32_t len;      // tokens
+  int32_t pin_len;  // -1: no pin (or lookup mode)
   int32_t wf;
   int32_t pad;
 };
 
+// Per tile (written by the prep kernel): the request holding the tile's first block, in the
+// block kernel's tile-relative coordinates (see resolve()). One 32-B broadcast load resolves every
+// lane of a tile that lies inside one request (most tiles: requests average ~6 tiles).
+struct __align__(32) TileRec {
+  int64_t s;    // token start of the tile's first block
+  int32_t r;    // its request
+  int32_t kb;   // its block index inside the request
+  int32_t rem;  // tokens from s to the request's end
+  int32_t wf;
+  int32_t pl;   // pin length of wf (-1: none / lookup mode)
+  int32_t pad;
+};
+
 // Scratch layout (int64 units): [prep ticket][prep status x nprep][tile status x ntiles]
-// [tile_r0 x ntiles][pad to 4][records x (n+1) x 4][local sums x n_items]
+// [pad to 4][tile records x ntiles x 4][records x (n+1) x 4][local sums x n_items][rk x n_items/2]
 static int64_t prep_tiles(int64_t n) { return (n + PREP_TILE - 1) / PREP_TILE; }
+static int64_t tile_head(int64_t np, int64_t ntiles) { return (1 + np + ntiles + 3) & ~int64_t(3); }
 size_t match_tile_state_elems(int64_t n_items, int64_t n_requests) {
   const int64_t ntiles = (n_items + WT - 1) / WT;
-  const int64_t head = 1 + prep_tiles(n_requests) + 2 * ntiles;
-  return (size_t)(((head + 3) & ~int64_t(3)) + 4 * (n_requests + 1) + n_items);
+  const int64_t head = tile_head(prep_tiles(n_requests), ntiles) + 4 * ntiles;
+  return (size_t)(head + 4 * (n_requests + 1) + n_items + (n_items + 1) / 2 + 1);
 }
 
 __device__ __forceinline__ void st_status(uint64_t* p, uint64_t v) {
@@ -72,6 +110,14 @@ __device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+// Programmatic dependent launch: the next kernel on the stream may start its prologue now; a
+// dependent kernel waits here until its predecessor grid has completed and its writes are visible.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+__device__ __forceinline__ int32_t clamp32(int64_t v) {
+  return (int32_t)(v < -(1ll << 30) ? -(1ll << 30) : (v > (1ll << 30) ? (1ll << 30) : v));
+}
 
 // ---------------------------------------------------------------- prep ----------------------
 struct PrepArgs {
@@ -81,7 +127,7 @@ struct PrepArgs {
   const int64_t* pin_len;
   int64_t* blk_off;   // out [n+1]
   ReqRec* rec;        // out [n+1]
-  int64_t* tile_r0;   // out
+  TileRec* trec;      // out
   int64_t* out_M;     // nullable: min(P, pin_len) or 0
   int64_t* out_hit;   // nullable: 16 * blocks
   unsigned long long* ticket;
@@ -92,20 +138,22 @@ __global__ void __launch_bounds__(PREP_THREADS) match_prep_kernel(PrepArgs P) {
   using BS = cub::BlockScan<int64_t, PREP_THREADS>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ int64_t s_tile, s_prefix;
+  pdl_trigger();
   const int tid = threadIdx.x;
   if (tid == 0) s_tile = (int64_t)atomicAdd(P.ticket, 1ull);
   __syncthreads();
   const int64_t tile = s_tile;
-  const int64_t r_base = tile * PREP_TILE + (int64_t)tid * PREP_PER_THREAD;
-  int64_t len[PREP_PER_THREAD], cnt = 0;
-#pragma unroll
-  for (int i = 0; i < PREP_PER_THREAD; ++i) {
-    const int64_t r = r_base + i;
-    len[i] = r < P.n ? P.tok_off[r + 1] - P.tok_off[r] : 0;
-    cnt += (len[i] + BT - 1) / BT;
+  const int64_t r = tile * PREP_TILE + tid;
+  const int64_t len = r < P.n ? P.tok_off[r + 1] - P.tok_off[r] : 0;
+  const int64_t nb = (len + BT - 1) / BT;
+  int32_t wf = 0;
+  int64_t pl = -1;
+  if (P.wf && r < P.n) {  // issued before the scan: the dependent pin_len load overlaps it
+    wf = P.wf[r];
+    pl = P.pin_len[wf];
   }
   int64_t excl, total;
-  BS(tmp).ExclusiveSum(cnt, excl, total);
+  BS(tmp).ExclusiveSum(nb, excl, total);
   if (tid < 32) {  // warp 0: publish, then look back 32 predecessor tiles per read
     const int lane = tid;
     if (lane == 0) st_status(P.pstatus + tile, (tile == 0 ? ST_INCL : ST_AGG) | (uint64_t)total);
@@ -131,38 +179,40 @@ __global__ void __launch_bounds__(PREP_THREADS) match_prep_kernel(PrepArgs P) {
     }
   }
   __syncthreads();
-  int64_t b = s_prefix + excl;
-#pragma unroll
-  for (int i = 0; i < PREP_PER_THREAD; ++i) {
-    const int64_t r = r_base + i;
-    if (r >= P.n) break;
-    const int64_t nb = (len[i] + BT - 1) / BT;
-    ReqRec q;
-    q.blk_off = b;
-    q.tok_off = P.tok_off[r];
-    q.pin_len = -1;
-    q.wf = 0;
-    q.pad = 0;
-    if (P.wf) {
-      q.wf = P.wf[r];
-      q.pin_len = P.pin_len[q.wf];
-    }
-    P.rec[r] = q;
-    P.blk_off[r] = b;
-    for (int64_t t = (b + WT - 1) / WT; t * WT < b + nb; ++t) P.tile_r0[t] = r;
-    if (P.out_M) P.out_M[r] = q.pin_len < 0 ? 0 : (len[i] < q.pin_len ? len[i] : q.pin_len);
-    if (P.out_hit) P.out_hit[r] = nb * BT;
-    b += nb;
-    if (r == P.n - 1) {  // closing record
-      ReqRec e;
-      e.blk_off = b;
-      e.tok_off = P.tok_off[P.n];
-      e.pin_len = -1;
-      e.wf = 0;
-      e.pad = 0;
-      P.rec[P.n] = e;
-      P.blk_off[P.n] = b;
-    }
+  if (r >= P.n) return;
+  const int64_t b = s_prefix + excl;
+  ReqRec q;
+  q.blk_off = b;
+  q.tok_off = P.tok_off[r];
+  q.len = (int32_t)len;
+  q.pin_len = (int32_t)pl;
+  q.wf = wf;
+  q.pad = 0;
+  P.rec[r] = q;
+  P.blk_off[r] = b;
+  for (int64_t t = (b + WT - 1) / WT; t * WT < b + nb; ++t) {
+    TileRec tr;
+    tr.kb = (int32_t)(t * WT - b);
+    tr.s = q.tok_off + (int64_t)tr.kb * BT;
+    tr.r = (int32_t)r;
+    tr.rem = (int32_t)(len - (int64_t)tr.kb * BT);
+    tr.wf = wf;
+    tr.pl = (int32_t)pl;
+    tr.pad = 0;
+    P.trec[t] = tr;
+  }
+  if (P.out_M) P.out_M[r] = pl < 0 ? 0 : (len < pl ? len : pl);
+  if (P.out_hit) P.out_hit[r] = nb * BT;
+  if (r == P.n - 1) {  // closing record
+    ReqRec e;
+    e.blk_off = b + nb;
+    e.tok_off = P.tok_off[P.n];
+    e.len = 0;
+    e.pin_len = -1;
+    e.wf = 0;
+    e.pad = 0;
+    P.rec[P.n] = e;
+    P.blk_off[P.n] = b + nb;
   }
 }
 
@@ -175,87 +225,98 @@ struct MatchKernelArgs {
   const uint8_t* blk_n;
   const Slot* slots;
   uint64_t slot_mask;
-  int32_t max_pin_blocks;
+  int64_t pin_groups;
   uint64_t* status;  // per tile: flag | aggregate since the tile's last segment head (final)
   uint64_t* local;   // per block: bit 63 = a segment head at or before it in the tile | local sum
-  const int64_t* tile_r0;
+  uint32_t* rk;      // lookup mode: per block request id | RK_FULL
+  const TileRec* trec;
   int hashes;        // chained hashes (or lookup) requested
 };
 
-struct Win {  // lane j holds request r0 + j of a tile's window
-  int64_t r0, off_j, toff_j, pl_j, off32, toff32;
-  int32_t wf_j;
-};
-
 struct Ctx {  // one lane's block of one tile
-  int64_t item, r, k, start, pin_base, pin_len;
-  int32_t nval;
-  bool valid, in_pin;
+  int64_t r, start;
+  int32_t k, nval, pin_len, wf;
+  bool valid;
 };
 
-__device__ __forceinline__ Win load_win(const MatchKernelArgs& K, int64_t r0) {
-  const int lane = threadIdx.x & 31;
-  const int64_t n = K.a.n;
-  Win w;
-  w.r0 = r0;
-  w.off_j = INT64_MAX;
-  w.toff_j = 0;
-  w.pl_j = -1;
-  w.wf_j = 0;
-  w.off32 = INT64_MAX;
-  w.toff32 = 0;
-  const int64_t rr = r0 + lane;
-  if (rr <= n) {
-    const int4* q = reinterpret_cast<const int4*>(K.rec + rr);
-    const int4 a = __ldg(q), b = __ldg(q + 1);
-    w.off_j = (int64_t)(((uint64_t)(uint32_t)a.y << 32) | (uint32_t)a.x);
-    w.toff_j = (int64_t)(((uint64_t)(uint32_t)a.w << 32) | (uint32_t)a.z);
-    w.pl_j = (int64_t)(((uint64_t)(uint32_t)b.y << 32) | (uint32_t)b.x);
-    w.wf_j = b.z;
-  }
-  if (r0 + WT <= n) {
-    w.off32 = __ldg(&K.rec[r0 + WT].blk_off);
-    w.toff32 = __ldg(&K.rec[r0 + WT].tok_off);
-  }
-  return w;
+__device__ __forceinline__ void unpack_rec(const ReqRec* q, int64_t& blk_off, int64_t& tok_off,
+                                           int32_t& len, int32_t& pl, int32_t& wf) {
+  const int4* p = reinterpret_cast<const int4*>(q);
+  const int4 a = __ldg(p), b = __ldg(p + 1);
+  blk_off = (int64_t)(((uint64_t)(uint32_t)a.y << 32) | (uint32_t)a.x);
+  tok_off = (int64_t)(((uint64_t)(uint32_t)a.w << 32) | (uint32_t)a.z);
+  len = b.x;
+  pl = b.y;
+  wf = b.z;
 }
 
-__device__ __forceinline__ Ctx resolve(const MatchKernelArgs& K, const Win& w, int64_t tile,
-                                       int64_t n_items, bool match_mode) {
+// Lane L of tile `tile` resolves item tile*32 + L. The tile record gives the request r0 holding
+// the tile's first block as (s0, kb0, rem0): when r0 covers the whole tile (rem0 > 16*31) every
+// lane resolves from that one broadcast load: k = kb0 + L, start = s0 + 16 L,
+// nval = clamp(rem0 - 16 L, 0, 16). Otherwise the window (requests r0 .. r0+31) is one record per
+// lane, reduced to the same tile-relative coordinates before the shuffles:
+//   kb_j  = tile*32 - blk_off_j   (block index of the tile's first item inside request j)
+//   s_j   = tok_off_j + 16 kb_j   (token start of that block)
+//   rem_j = len_j - 16 kb_j       (tokens from there to the request's end)
+// and lane L belongs to the largest j with kb_j >= -L. Tiles covering > 32 requests (empty
+// requests) fall back to a binary search over blk_off for the lanes past the window.
+__device__ __forceinline__ Ctx resolve(const MatchKernelArgs& K, int64_t tile, int64_t n_items) {
   const int lane = threadIdx.x & 31;
+  const int64_t n = K.a.n;
+  const int64_t T0 = tile * WT;
+  const int4* tp = reinterpret_cast<const int4*>(K.trec + tile);
+  const int4 ta = __ldg(tp), tb = __ldg(tp + 1);
+  const int64_t s0 = (int64_t)(((uint64_t)(uint32_t)ta.y << 32) | (uint32_t)ta.x);
+  const int64_t r0 = ta.z;
   Ctx c;
-  c.item = tile * WT + lane;
-  c.valid = c.item < n_items;
-  int j = 0;  // largest j in [0, 31] with off_j <= item
+  const int64_t item = T0 + lane;
+  c.valid = item < n_items;
+  if (tb.x > (WT - 1) * BT) {  // the whole tile lies inside request r0
+    c.r = r0;
+    c.k = ta.w + lane;
+    c.start = s0 + (int64_t)lane * BT;
+    c.wf = tb.y;
+    c.pin_len = tb.z;
+    const int32_t nv = tb.x - lane * BT;
+    c.nval = c.valid ? (nv > BT ? BT : nv) : 0;
+    return c;
+  }
+  const int64_t rr = r0 + lane;
+  int32_t kb = -(1 << 30), rem = 0, pl = -1, wf = 0;
+  int64_t s = 0;
+  if (rr <= n) {
+    int64_t bo, to;
+    int32_t len;
+    unpack_rec(K.rec + rr, bo, to, len, pl, wf);
+    kb = clamp32(T0 - bo);
+    s = to + (int64_t)kb * BT;
+    rem = clamp32((int64_t)len - (int64_t)kb * BT);
+  }
+  const int64_t off32 = r0 + WT <= n ? __ldg(&K.rec[r0 + WT].blk_off) : INT64_MAX;
+  int j = 0;
 #pragma unroll
-  for (int s = 16; s > 0; s >>= 1) {
-    const int64_t v = __shfl_sync(0xffffffffu, w.off_j, j + s);
-    if (v <= c.item) j += s;
+  for (int st = 16; st > 0; st >>= 1) {
+    const int32_t v = __shfl_sync(0xffffffffu, kb, j + st);
+    if (v >= -lane) j += st;
   }
-  const int64_t off_r = __shfl_sync(0xffffffffu, w.off_j, j);
-  int64_t tb = __shfl_sync(0xffffffffu, w.toff_j, j);
-  const int64_t te_in = __shfl_sync(0xffffffffu, w.toff_j, (j + 1) & 31);
-  int32_t wf = __shfl_sync(0xffffffffu, w.wf_j, j);
-  int64_t pl = __shfl_sync(0xffffffffu, w.pl_j, j);
-  c.r = w.r0 + j;
-  c.k = c.item - off_r;
-  int64_t te = j == 31 ? w.toff32 : te_in;
-  if (c.valid && w.off32 <= c.item) {  // > 32 requests in this tile (empty requests)
-    c.r = upper_index(K.a.blk_off, K.a.n, c.item);
-    const ReqRec& q = K.rec[c.r];
-    c.k = c.item - q.blk_off;
-    tb = q.tok_off;
-    te = K.rec[c.r + 1].tok_off;
-    wf = q.wf;
-    pl = q.pin_len;
+  const int32_t kbj = __shfl_sync(0xffffffffu, kb, j);
+  const int32_t remj = __shfl_sync(0xffffffffu, rem, j);
+  c.start = __shfl_sync(0xffffffffu, s, j) + (int64_t)lane * BT;
+  c.pin_len = __shfl_sync(0xffffffffu, pl, j);
+  c.wf = __shfl_sync(0xffffffffu, wf, j);
+  c.k = kbj + lane;
+  c.r = r0 + j;
+  int32_t nv = remj - lane * BT;
+  if (c.valid && off32 <= item) {  // > 32 requests in this tile
+    c.r = upper_index(K.a.blk_off, n, item);
+    int64_t bo, to;
+    int32_t len;
+    unpack_rec(K.rec + c.r, bo, to, len, c.pin_len, c.wf);
+    c.k = (int32_t)(item - bo);
+    c.start = to + (int64_t)c.k * BT;
+    nv = len - c.k * BT;
   }
-  if (!c.valid) c.r = -1 - lane;  // never merges with a real request in segmented reductions
-  const int64_t rem = te - tb - c.k * BT;
-  c.nval = c.valid ? (int32_t)(rem < BT ? rem : BT) : 0;
-  c.start = tb + c.k * BT;
-  c.in_pin = match_mode && c.valid && pl >= 0 && c.k < (pl + BT - 1) / BT;
-  c.pin_base = (int64_t)wf * K.max_pin_blocks;
-  c.pin_len = pl;
+  c.nval = c.valid ? (nv < 0 ? 0 : (nv > BT ? BT : nv)) : 0;
   return c;
 }
 
@@ -271,21 +332,14 @@ __device__ __forceinline__ void load16_aligned(const uint32_t* __restrict__ p, u
   }
 }
 
-template <int SH>
-__device__ __forceinline__ void take16(const uint32_t* w, uint32_t* t) {
-#pragma unroll
-  for (int j = 0; j < BT; ++j) t[j] = w[j + SH];
-}
-
 // Block tokens [start, start+nval) zero-padded to 16: five 16-B loads from the aligned-down
-// address and a static funnel by (start & 3) at any alignment; scalar only at the array end.
+// address and a branch-free two-stage funnel by (start & 3) (lanes of different requests have
+// different alignments, so a switch would diverge); scalar only at the array end.
 __device__ __forceinline__ void load_block(const uint32_t* __restrict__ tok, int64_t start, int nval,
                                            int64_t tok_total, uint32_t* t) {
   const int64_t a0 = start & ~int64_t(3);
   const int sh = (int)(start & 3);
-  if (sh == 0 && start + BT <= tok_total) {
-    load16_aligned(tok + start, t);
-  } else if (a0 + 20 <= tok_total) {
+  if (a0 + 20 <= tok_total) {
     uint32_t w[20];
     const uint4* q = reinterpret_cast<const uint4*>(tok + a0);
 #pragma unroll
@@ -296,155 +350,324 @@ __device__ __forceinline__ void load_block(const uint32_t* __restrict__ tok, int
       w[4 * i + 2] = v.z;
       w[4 * i + 3] = v.w;
     }
-    switch (sh) {
-      case 0: take16<0>(w, t); break;
-      case 1: take16<1>(w, t); break;
-      case 2: take16<2>(w, t); break;
-      default: take16<3>(w, t); break;
-    }
+    uint32_t u[17];
+#pragma unroll
+    for (int i = 0; i < 17; ++i) u[i] = (sh & 2) ? w[i + 2] : w[i];
+#pragma unroll
+    for (int i = 0; i < BT; ++i) t[i] = (sh & 1) ? u[i + 1] : u[i];
   } else {
 #pragma unroll
     for (int j = 0; j < BT; ++j) t[j] = j < nval ? __ldg(tok + start + j) : 0u;
-    return;
   }
+  if (nval < BT) {
 #pragma unroll
-  for (int j = 0; j < BT; ++j)
-    if (j >= nval) t[j] = 0u;
+    for (int j = 0; j < BT; ++j)
+      if (j >= nval) t[j] = 0u;
+  }
 }
 
-// One warp per 32-block tile, one block per lane, non-persistent: at 46 registers ~40 warps per SM
-// keep enough tiles in flight to cover the window -> tokens/pin-tokens round trips. (A persistent
-// cp.async-pipelined variant measured slower: with the inter-warp dependencies gone, occupancy and
-// not load latency decides; see profiles/round1/README.md.)
-__global__ void __launch_bounds__(MATCH_THREADS) match_block_kernel(MatchKernelArgs K) {
+// ---- TMA bulk staging of a tile's request tokens ----------------------------------------
+// A tile's 32 blocks are one contiguous token range of the CSR batch (blocks partition requests
+// and requests are consecutive), so one cp.async.bulk per warp brings all of it (<= 2.1 KB)
+// into shared memory without touching the LSU. Lanes then read their block with rotated
+// 16-B shared loads: lane L starts at chunk (i + r_L) mod 5 with r_L = (L >> 1) & 3, which puts
+// the 8 lanes of each quarter-warp phase on distinct bank groups (lanes of one request are 64 B
+// apart, so unrotated reads would be 4-way conflicted); two select stages undo the rotation.
+constexpr int STAGE_WORDS = 544;  // >= 31*16 + 3 + 20 words (last lane's 5-chunk window), 128-B multiple
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+// Block tokens of a lane whose block starts at word o of the staged range (o >= 0).
+__device__ __forceinline__ void load_block_staged(const uint32_t* s, int o, int nval, uint32_t* t) {
+  const int lane = threadIdx.x & 31;
+  const int c0 = o >> 2, sh = o & 3, rr = (lane >> 1) & 3;
+  uint4 v[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    int x = i + rr;
+    x = x >= 5 ? x - 5 : x;
+    v[i] = *reinterpret_cast<const uint4*>(s + 4 * (c0 + x));
+  }
+  uint4 u[5];
+#pragma unroll
+  for (int x = 0; x < 5; ++x) u[x] = (rr & 1) ? v[(x + 4) % 5] : v[x];
+  uint32_t w[20];
+#pragma unroll
+  for (int x = 0; x < 5; ++x) {
+    const uint4 q = (rr & 2) ? u[(x + 3) % 5] : u[x];
+    w[4 * x] = q.x;
+    w[4 * x + 1] = q.y;
+    w[4 * x + 2] = q.z;
+    w[4 * x + 3] = q.w;
+  }
+  uint32_t y[17];
+#pragma unroll
+  for (int i = 0; i < 17; ++i) y[i] = (sh & 2) ? w[i + 2] : w[i];
+#pragma unroll
+  for (int i = 0; i < BT; ++i) t[i] = (sh & 1) ? y[i + 1] : y[i];
+  if (nval < BT) {
+#pragma unroll
+    for (int j = 0; j < BT; ++j)
+      if (j >= nval) t[j] = 0u;
+  }
+}
+
+// M and chained-hash work of one tile once every lane holds its block's tokens t (zero padded)
+// and, for blocks inside the pin, the pin's block q.
+__device__ __forceinline__ void tile_finish(const MatchKernelArgs& K, int64_t tile, const Ctx& c,
+                                            bool in_pin, const uint32_t* t, const uint32_t* q) {
   const MatchArgs& A = K.a;
   const int lane = threadIdx.x & 31;
+  const bool match_mode = A.out_M != nullptr;
+  const unsigned below = (1u << lane) - 1u;
+  // request heads (first block of a request) and segment starts (heads, lane 0, invalid lanes)
+  const unsigned heads = __ballot_sync(0xffffffffu, c.valid && c.k == 0);
+  const unsigned segs = heads | 1u | __ballot_sync(0xffffffffu, !c.valid);
+  const int seg0 = 31 - __clz(segs & (below | (1u << lane)));
+
+  // ---- M: first differing token against the pin's block; the first mismatching lane of each
+  //      request segment issues the only atomic --------------------------------------------
+  if (match_mode) {
+    int lcp = BT, lim = 0;
+    if (in_pin) {
+      // both sides are zero padded past their ends, so a block whose 16 words all agree has no
+      // mismatch below lim; only a differing block (the first diverging block of a request, or a
+      // boundary block whose padding differs) takes the exact first-mismatch path
+      uint32_t d = 0;
+#pragma unroll
+      for (int j = 0; j < BT; ++j) d |= q[j] ^ t[j];
+      if (d) {
+        const int pn = min(c.pin_len - c.k * BT, BT);
+        lim = min(c.nval, pn);
+        unsigned ne = 1u << lim;
+#pragma unroll
+        for (int j = 0; j < BT; ++j) ne |= (q[j] != t[j]) ? (1u << j) : 0u;
+        lcp = __ffs(ne) - 1;
+      }
+    }
+    const bool mism = in_pin && lcp < lim;
+    const unsigned mm = __ballot_sync(0xffffffffu, mism);
+    if (mism && (mm & below & ~((1u << seg0) - 1u)) == 0)
+      atomicMin(reinterpret_cast<unsigned long long*>(A.out_M + c.r),
+                (unsigned long long)((int64_t)c.k * BT + lcp));
+  }
+
+  // ---- chained hashes: warp inclusive scan of digests, corrected to segment-local sums; the
+  //      tile aggregate is final (read by the chain pass) ------------------------------------
+  if (K.hashes) {
+    uint64_t v = c.valid ? block_digest_words((uint64_t)c.k, (uint32_t)c.nval, t) : 0ull;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t u = __shfl_up_sync(0xffffffffu, v, d);
+      if (lane >= d) v += u;
+    }
+    const unsigned hl = heads & (below | (1u << lane));
+    const int hs = 31 - __clz(hl | 1u);  // last real head at or before this lane (if any)
+    const uint64_t base = __shfl_sync(0xffffffffu, v, hs > 0 ? hs - 1 : 0);
+    const uint64_t h = hl ? 1ull : 0ull;
+    if (hl && hs > 0) v -= base;
+    const int64_t item = tile * WT + lane;
+    if (c.valid) {
+      K.local[item] = (h << 63) | (v & CHAIN_MASK);
+      if (K.rk) K.rk[item] = (uint32_t)c.r | (c.nval == BT ? RK_FULL : 0u);
+    }
+    if (lane == 31) K.status[tile] = (h ? ST_INCL : ST_AGG) | (v & CHAIN_MASK);
+  }
+}
+
+
+// One warp per 32-block tile, one block per lane, non-persistent: enough tiles in flight per SM to
+// cover the window -> tokens/pin-tokens round trips.
+template <bool STAGED>
+__global__ void __launch_bounds__(MATCH_THREADS) match_block_kernel(MatchKernelArgs K) {
+  __shared__ __align__(128) uint32_t s_tok[STAGED ? MATCH_THREADS / 32 : 1][STAGED ? STAGE_WORDS : 4];
+  __shared__ __align__(8) uint64_t s_bar[MATCH_THREADS / 32];
+  const MatchArgs& A = K.a;
+  const int lane = threadIdx.x & 31;
+  [[maybe_unused]] const int warp = threadIdx.x >> 5;
   const int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if constexpr (STAGED) {
+    if (lane == 0) mbar_init(&s_bar[warp]);
+    __syncwarp();
+  }
+  pdl_trigger();
+  pdl_wait();
   const int64_t n_items = K.rec[A.n].blk_off;
   if (tile * WT >= n_items) return;
   const int64_t tok_total = K.rec[A.n].tok_off;
   const bool match_mode = A.out_M != nullptr;
-  const Ctx c = resolve(K, load_win(K, K.tile_r0[tile]), tile, n_items, match_mode);
+  const Ctx c = resolve(K, tile, n_items);
 
+  // the pin's block k (token-major 32-block groups: each load is one or two 128-B lines per
+  // warp), issued before the staging wait so both round trips overlap
+  const bool in_pin = match_mode && c.valid && c.pin_len >= 0 && c.k < (c.pin_len + BT - 1) / BT;
+  uint32_t q[BT];
+  if (in_pin) {
+    const uint32_t* pp = K.pin_tok + pin_tok_index(c.wf, c.k, 0, K.pin_groups);
+#pragma unroll
+    for (int j = 0; j < BT; ++j) q[j] = __ldg(pp + (j << 5));
+  }
   uint32_t t[BT];
-  if (c.valid) {
+  if constexpr (STAGED) {
+    // the tile's token range: lane 0's block to the end of the last valid lane's 5-chunk window
+    const int nv = __popc(__ballot_sync(0xffffffffu, c.valid));
+    const int64_t a0 = __shfl_sync(0xffffffffu, c.start, 0) & ~int64_t(3);
+    const int64_t a1 = __shfl_sync(0xffffffffu, (c.start & ~int64_t(3)) + 20, nv - 1);
+    if (a1 <= (tok_total & ~int64_t(3))) {  // all but the batch's last tile
+      if (lane == 0) bulk_load(s_tok[warp], A.tok + a0, (uint32_t)(a1 - a0) * 4u, &s_bar[warp]);
+      mbar_wait0(&s_bar[warp]);
+      if (c.valid) load_block_staged(s_tok[warp], (int)(c.start - a0), c.nval, t);
+    } else if (c.valid) {
+      load_block(A.tok, c.start, c.nval, tok_total, t);
+    }
+  } else if (c.valid) {
     load_block(A.tok, c.start, c.nval, tok_total, t);
-  } else {
+  }
+  if (!c.valid) {
 #pragma unroll
     for (int j = 0; j < BT; ++j) t[j] = 0u;
   }
-
-  // ---- M: first differing token against the pin's block, warp segmented min, one atomic ----
-  if (match_mode) {
-    unsigned long long m = ~0ull;
-    if (c.in_pin) {  // the pin's block k from its pin-major token copy (coalesced, no indirection)
-      uint32_t q[BT];
-      load16_aligned(K.pin_tok + (c.pin_base + c.k) * BT, q);
-      const int64_t prem = c.pin_len - c.k * BT;
-      const int pn = (int)(prem < BT ? prem : BT);
-      const int lim = c.nval < pn ? c.nval : pn;
-      int lcp = 0;
-      bool run = true;
-#pragma unroll
-      for (int j = 0; j < BT; ++j) {
-        run = run && j < lim && q[j] == t[j];
-        lcp += run ? 1 : 0;
-      }
-      if (lcp < lim) m = (unsigned long long)(c.k * BT + lcp);
-    }
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const unsigned long long o = __shfl_down_sync(0xffffffffu, m, d);
-      const int64_t orr = __shfl_down_sync(0xffffffffu, c.r, d);
-      if (lane + d < 32 && orr == c.r && o < m) m = o;
-    }
-    const int64_t prev_r = __shfl_up_sync(0xffffffffu, c.r, 1);
-    if (c.valid && (lane == 0 || prev_r != c.r) && m != ~0ull)
-      atomicMin(reinterpret_cast<unsigned long long*>(A.out_M + c.r), m);
-  }
-
-  // ---- chained hashes: local segmented scan; tile aggregate (final, read by the chain pass) --
-  if (K.hashes) {
-    uint64_t v = c.valid ? block_digest_words((uint64_t)c.k, (uint32_t)c.nval, t) : 0ull;
-    int h = (c.valid && c.k == 0) ? 1 : 0;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint64_t vv = __shfl_up_sync(0xffffffffu, v, d);
-      const int hh = __shfl_up_sync(0xffffffffu, h, d);
-      if (lane >= d) {
-        if (!h) v += vv;
-        h |= hh;
-      }
-    }
-    if (c.valid) K.local[c.item] = ((uint64_t)h << 63) | (v & CHAIN_MASK);
-    if (lane == 31) K.status[tile] = (h ? ST_INCL : ST_AGG) | (v & CHAIN_MASK);
-  }
+  tile_finish(K, tile, c, in_pin, t, q);
 }
 
 // ---------------------------------------------------------------- chain pass ---------------
 template <bool LOOKUP>
 __global__ void __launch_bounds__(MATCH_THREADS) match_chain_kernel(MatchKernelArgs K) {
+  constexpr int CH_TPW = LOOKUP ? CH_TPW_LOOKUP : CH_TPW_HASH;
   const MatchArgs& A = K.a;
   const int lane = threadIdx.x & 31;
-  const int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * CH_TPW;
+  pdl_trigger();
+  pdl_wait();
   const int64_t n_items = K.rec[A.n].blk_off;
-  if (tile * WT >= n_items) return;
-  const int64_t item = tile * WT + lane;
-  const bool valid = item < n_items;
-  const uint64_t loc = valid ? K.local[item] : 0ull;
+  if (t0 * WT >= n_items) return;
+  uint64_t loc[CH_TPW];
+  uint32_t rk[CH_TPW];
+#pragma unroll
+  for (int i = 0; i < CH_TPW; ++i) {
+    const int64_t item = (t0 + i) * WT + lane;
+    loc[i] = item < n_items ? K.local[item] : 0ull;
+    if constexpr (LOOKUP) rk[i] = item < n_items ? K.rk[item] : 0u;
+  }
   // the first 32 predecessor statuses are read together with the local sums (speculatively:
-  // unused when the tile starts with a segment head)
-  const int64_t p0 = tile - 1 - lane;
+  // unused when the first tile starts with a segment head)
+  const int64_t p0 = t0 - 1 - lane;
   const uint64_t st0 = p0 >= 0 ? K.status[p0] : ST_INCL;
-  const int h = (int)(loc >> 63);
-  const uint64_t v = loc & CHAIN_MASK;
-  // carry into the tile's first segment: every status is final, walk back 32 tiles per read
-  uint64_t prefix = 0;
-  if (!__shfl_sync(0xffffffffu, h, 0) && tile > 0) {
-    for (int64_t base = tile - 1;; base -= 32) {
+  // carry into the first tile's first segment: every status is final, walk back 32 tiles per read
+  uint64_t carry = 0;
+  if (!__shfl_sync(0xffffffffu, (uint32_t)(loc[0] >> 63), 0) && t0 > 0) {
+    for (int64_t base = t0 - 1;; base -= 32) {
       const int64_t p = base - lane;
-      const uint64_t st = base == tile - 1 ? st0 : (p >= 0 ? K.status[p] : ST_INCL);
+      const uint64_t st = base == t0 - 1 ? st0 : (p >= 0 ? K.status[p] : ST_INCL);
       const unsigned incl = __ballot_sync(0xffffffffu, (st & ~CHAIN_MASK) == ST_INCL);
       const int first = incl ? __ffs(incl) - 1 : 31;
-      prefix += warp_sum(lane <= first ? (st & CHAIN_MASK) : 0ull);
+      carry += warp_sum(lane <= first ? (st & CHAIN_MASK) : 0ull);
       if (incl) break;
     }
   }
-  const uint64_t c = chain_finalize(h ? v : prefix + v);
-  if (valid && A.out_hash) A.out_hash[item] = c;
-  if constexpr (LOOKUP) {  // global table probe, token-verified
-    const int64_t tok_total = K.rec[A.n].tok_off;
-    const Ctx x = resolve(K, load_win(K, K.tile_r0[tile]), tile, n_items, false);
-    int32_t id = -1;
-    if (x.valid && x.nval == BT) {
-      uint64_t sl = c & K.slot_mask;
-      for (;;) {
-        const uint4 raw = __ldg(reinterpret_cast<const uint4*>(K.slots + sl));
-        const uint64_t key = (uint64_t)raw.x | ((uint64_t)raw.y << 32);
-        if (key == c) {
-          const int32_t cand = (int32_t)raw.z;
-          if (cand >= 0 && K.blk_n[cand] == BT) {
-            uint32_t t[BT], q[BT];
-            load_block(A.tok, x.start, x.nval, tok_total, t);
-            load16_aligned(K.blk_tok + (int64_t)cand * BT, q);
-            bool eq = true;
+  uint64_t c[CH_TPW];
 #pragma unroll
-            for (int j = 0; j < BT; ++j) eq &= q[j] == t[j];
-            if (eq) id = cand;
+  for (int i = 0; i < CH_TPW; ++i) {
+    const bool h = loc[i] >> 63;
+    const uint64_t sum = h ? (loc[i] & CHAIN_MASK) : carry + (loc[i] & CHAIN_MASK);
+    carry = __shfl_sync(0xffffffffu, sum, 31);
+    c[i] = chain_finalize(sum);
+    const int64_t item = (t0 + i) * WT + lane;
+    if (item < n_items && A.out_hash) A.out_hash[item] = c[i];
+  }
+  if constexpr (LOOKUP) {  // global table probe, token-verified; all probes of the warp in flight
+    const int64_t tok_total = K.rec[A.n].tok_off;
+    uint4 raw[CH_TPW];
+#pragma unroll
+    for (int i = 0; i < CH_TPW; ++i) {
+      const int64_t item = (t0 + i) * WT + lane;
+      raw[i] = make_uint4(0, 0, 0xffffffffu, 0);
+      if (item < n_items && (rk[i] & RK_FULL))
+        raw[i] = __ldg(reinterpret_cast<const uint4*>(K.slots + (c[i] & K.slot_mask)));
+    }
+#pragma unroll
+    for (int i = 0; i < CH_TPW; ++i) {
+      const int64_t item = (t0 + i) * WT + lane;
+      const bool valid = item < n_items;
+      const int64_t r = (int64_t)(rk[i] & ~RK_FULL);
+      int32_t id = -1;
+      if (valid && (rk[i] & RK_FULL)) {
+        uint64_t sl = c[i] & K.slot_mask;
+        uint4 w = raw[i];
+        for (;;) {
+          const uint64_t key = (uint64_t)w.x | ((uint64_t)w.y << 32);
+          if (key == c[i]) {
+            const int32_t cand = (int32_t)w.z;
+            if (cand >= 0 && K.blk_n[cand] == BT) {
+              int64_t bo, to;
+              int32_t len, pl, wf;
+              unpack_rec(K.rec + r, bo, to, len, pl, wf);
+              uint32_t t[BT], q[BT];
+              load_block(A.tok, to + (item - bo) * BT, BT, tok_total, t);
+              load16_aligned(K.blk_tok + (int64_t)cand * BT, q);
+              bool eq = true;
+#pragma unroll
+              for (int j = 0; j < BT; ++j) eq &= q[j] == t[j];
+              if (eq) id = cand;
+            }
+            break;
           }
-          break;
+          if (key == KEY_EMPTY) break;
+          sl = (sl + 1) & K.slot_mask;
+          w = __ldg(reinterpret_cast<const uint4*>(K.slots + sl));
         }
-        if (key == KEY_EMPTY) break;
-        sl = (sl + 1) & K.slot_mask;
+      }
+      if (valid) A.out_block[item] = id;
+      // leading hit length: the first miss of each request segment in the tile lowers out_hit
+      const uint32_t prev = __shfl_up_sync(0xffffffffu, rk[i] & ~RK_FULL, 1);
+      const unsigned segs = __ballot_sync(0xffffffffu, lane == 0 || !valid || prev != (uint32_t)r);
+      const unsigned below = (1u << lane) - 1u;
+      const int seg0 = 31 - __clz(segs & (below | (1u << lane)));
+      const bool miss = valid && id < 0;
+      const unsigned mm = __ballot_sync(0xffffffffu, miss);
+      if (miss && (mm & below & ~((1u << seg0) - 1u)) == 0) {
+        const int64_t bo = __ldg(&K.rec[r].blk_off);
+        atomicMin(reinterpret_cast<unsigned long long*>(A.out_hit + r),
+                  (unsigned long long)((item - bo) * BT));
       }
     }
-    if (x.valid) {
-      A.out_block[item] = id;
-      if (id < 0)
-        atomicMin(reinterpret_cast<unsigned long long*>(A.out_hit + x.r),
-                  (unsigned long long)(x.k * BT));
-    }
   }
+}
+
+template <class Kern, class Arg>
+static cudaError_t launch_pdl(Kern kern, unsigned grid, unsigned block, cudaStream_t st, const Arg& arg) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, arg);
 }
 
 int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStream_t st) {
@@ -454,10 +677,12 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   unsigned long long* ticket = reinterpret_cast<unsigned long long*>(tile_state);
   uint64_t* pstatus = reinterpret_cast<uint64_t*>(tile_state + 1);
   uint64_t* status = reinterpret_cast<uint64_t*>(tile_state + 1 + np);
-  int64_t* tile_r0 = tile_state + 1 + np + ntiles;
-  const int64_t head = (1 + np + 2 * ntiles + 3) & ~int64_t(3);
+  const int64_t th = tile_head(np, ntiles);
+  TileRec* trec = reinterpret_cast<TileRec*>(tile_state + th);
+  const int64_t head = th + 4 * ntiles;
   ReqRec* rec = reinterpret_cast<ReqRec*>(tile_state + head);
   uint64_t* local = reinterpret_cast<uint64_t*>(tile_state + head + 4 * (a.n + 1));
+  uint32_t* rk = reinterpret_cast<uint32_t*>(tile_state + head + 4 * (a.n + 1) + a.n_items);
 
   SFKV_CUDA(cudaMemsetAsync(tile_state, 0, sizeof(int64_t) * (1 + np), st));
   PrepArgs P;
@@ -467,7 +692,7 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   P.pin_len = p->pin_len;
   P.blk_off = a.blk_off;
   P.rec = rec;
-  P.tile_r0 = tile_r0;
+  P.trec = trec;
   P.out_M = a.out_M;
   P.out_hit = a.out_hit;
   P.ticket = ticket;
@@ -484,18 +709,21 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   K.blk_n = p->blk_n;
   K.slots = p->slots;
   K.slot_mask = (uint64_t)p->table_slots - 1;
-  K.max_pin_blocks = p->cfg.max_pin_blocks;
+  K.pin_groups = pin_groups(p->cfg);
   K.status = status;
   K.local = local;
-  K.tile_r0 = tile_r0;
+  K.rk = a.out_block ? rk : nullptr;
+  K.trec = trec;
   K.hashes = (a.out_hash || a.out_block) ? 1 : 0;
   const int64_t grid = (ntiles + MATCH_THREADS / 32 - 1) / (MATCH_THREADS / 32);
-  match_block_kernel<<<(unsigned)grid, MATCH_THREADS, 0, st>>>(K);
-  SFKV_LAUNCH_CHECK("match_block_kernel");
+  if (a.out_M) SFKV_CUDA(launch_pdl(match_block_kernel<true>, (unsigned)grid, MATCH_THREADS, st, K));
+  else SFKV_CUDA(launch_pdl(match_block_kernel<false>, (unsigned)grid, MATCH_THREADS, st, K));
   if (K.hashes) {
-    if (a.out_block) match_chain_kernel<true><<<(unsigned)grid, MATCH_THREADS, 0, st>>>(K);
-    else match_chain_kernel<false><<<(unsigned)grid, MATCH_THREADS, 0, st>>>(K);
-    SFKV_LAUNCH_CHECK("match_chain_kernel");
+    const int tpw = a.out_block ? CH_TPW_LOOKUP : CH_TPW_HASH;
+    const int64_t cwarps = (ntiles + tpw - 1) / tpw;
+    const unsigned cgrid = (unsigned)((cwarps + MATCH_THREADS / 32 - 1) / (MATCH_THREADS / 32));
+    if (a.out_block) SFKV_CUDA(launch_pdl(match_chain_kernel<true>, cgrid, MATCH_THREADS, st, K));
+    else SFKV_CUDA(launch_pdl(match_chain_kernel<false>, cgrid, MATCH_THREADS, st, K));
   }
   return 0;
 }
