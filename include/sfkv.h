@@ -171,6 +171,38 @@ int sfkv_gather_dev(sfkv_pool* pool, int64_t n, const int32_t* wf, void* dst,
  * GPU. *status = SFKV_PIN_ACCEPTED / SFKV_PIN_REJECTED (dst capacity), unchanged dst on reject. */
 int sfkv_handoff(sfkv_pool* src, int32_t wf_src, sfkv_pool* dst, int32_t wf_dst, int32_t* status);
 
+/* ---- cross-process stage handoff over NVLink (one process per GPU; new) ---------
+ * The sending rank exports its pool's KV region once (CUDA IPC); every receiving rank maps it
+ * (sfkv_peer_open), so the receiver's commit kernel pulls the source blocks' rows directly over
+ * NVLink (or from the same device) with no staging copy. The sender ships only metadata per
+ * workflow: its pin's tokens and block ids (sfkv_pin_export); the sender must keep those blocks
+ * resident until the receiver's handoff call has completed.
+ * sfkv_handoff_recv_batch commits request r's tokens as the pin of wf[r] in `dst` exactly like
+ * sfkv_commit_batch (admission, dedup, copy-on-share against dst's old pin), with the payload of
+ * new blocks read from the source blocks src_blocks[blk_off[r] + k] (ceil(len_r/16) ids per
+ * request, concatenated in request order) of the mapped region. */
+typedef struct sfkv_ipc_handle {
+  char handle[64];           /* cudaIpcMemHandle_t of the pool's KV region */
+  int64_t kv_bytes;
+  int64_t block_bytes;
+  int32_t n_slabs;
+  int32_t slab_row_bytes;
+} sfkv_ipc_handle;
+typedef struct sfkv_peer sfkv_peer;
+
+int sfkv_pool_export(sfkv_pool* pool, sfkv_ipc_handle* out);
+int sfkv_peer_open(const sfkv_ipc_handle* handle, int32_t device, sfkv_peer** out);
+int sfkv_peer_close(sfkv_peer* peer);
+/* Tokens (cap entries max) and block ids (ceil(L/16) entries; written when cap >= L) of a pin. */
+int sfkv_pin_export(sfkv_pool* pool, int32_t wf, uint32_t* tok, int32_t* block_ids, int64_t cap,
+                    int64_t* n_tokens);
+int sfkv_handoff_recv_batch(sfkv_pool* dst, const sfkv_peer* src, int64_t n, const int32_t* wf,
+                            const int64_t* tok_off, const uint32_t* tok, const int32_t* src_blocks,
+                            int32_t* out_status);
+int sfkv_handoff_recv_batch_dev(sfkv_pool* dst, const sfkv_peer* src, int64_t n, const int32_t* wf,
+                                const int64_t* tok_off, const uint32_t* tok, int64_t n_tokens,
+                                const int32_t* src_blocks, int32_t* out_status);
+
 /* ---- memory manager: replaces pressure_actions (memory.cpp:150-169) -------------------------
  * Entries are the tracker's (workflow, backend) records as SoA: backend index, last_update_ts,
  * wf_rank (rank of workflow_id in std::string order), in_flight, preserved. For every backend b

@@ -37,6 +37,16 @@ class PoolConfig(C.Structure):
     ]
 
 
+class IpcHandle(C.Structure):  # sfkv_ipc_handle
+    _fields_ = [
+        ("handle", C.c_char * 64),
+        ("kv_bytes", C.c_int64),
+        ("block_bytes", C.c_int64),
+        ("n_slabs", C.c_int32),
+        ("slab_row_bytes", C.c_int32),
+    ]
+
+
 class PoolStats(C.Structure):
     _fields_ = [
         ("occupancy_tokens", C.c_int64),
@@ -87,6 +97,12 @@ GPU_ONLY = {
     "lookup_batch_dev": [P, i64, P, P, i64, P, P],
     "commit_batch_dev": [P, i64, P, P, P, i64, P, P, P, P],
     "gather_dev": [P, i64, P, P, P],
+    "pool_export": [P, C.POINTER(IpcHandle)],
+    "peer_open": [C.POINTER(IpcHandle), i32, C.POINTER(P)],
+    "peer_close": [P],
+    "pin_export": [P, i32, P, P, i64, C.POINTER(i64)],
+    "handoff_recv_batch": [P, P, i64, P, P, P, P, P],
+    "handoff_recv_batch_dev": [P, P, i64, P, P, P, i64, P, P],
 }
 ORACLE_ONLY = {
     "gather": [P, i64, P, P, P],
@@ -297,7 +313,49 @@ class Pool:
                                                    C.byref(st)))
         return st.value
 
+    # -- cross-process handoff (GPU pools only) ----------------------------------------------
+    def export(self) -> bytes:
+        """The pool's KV region as a CUDA IPC handle (sfkv_ipc_handle bytes)."""
+        h = IpcHandle()
+        self.api.check("pool_export", self.api.pool_export(self.h, C.byref(h)))
+        return bytes(C.string_at(C.addressof(h), C.sizeof(h)))
+
+    def pin_export(self, wf):
+        """(tokens uint32[L], block ids int32[ceil(L/16)]) of workflow wf's pin."""
+        n = C.c_int64()
+        self.api.check("pin_export", self.api.pin_export(self.h, int(wf), None, None, 0, C.byref(n)))
+        L = n.value
+        tok = np.zeros(max(L, 1), dtype=np.uint32)
+        ids = np.zeros(max((L + BLOCK_TOKENS - 1) // BLOCK_TOKENS, 1), dtype=np.int32)
+        self.api.check("pin_export", self.api.pin_export(self.h, int(wf), _ptr(tok), _ptr(ids), L,
+                                                         C.byref(n)))
+        return tok[:L], ids[: (L + BLOCK_TOKENS - 1) // BLOCK_TOKENS]
+
+    def handoff_recv(self, peer: "Peer", wf, tok_off, tok, src_blocks):
+        """Commit a batch of contexts whose payload is pulled from `peer`'s blocks."""
+        wf = np.ascontiguousarray(wf, dtype=np.int32)
+        st = np.zeros(len(wf), dtype=np.int32)
+        src_blocks = np.ascontiguousarray(src_blocks, dtype=np.int32)
+        self.api.check("handoff_recv_batch", self.api.handoff_recv_batch(
+            self.h, peer.h, len(wf), _ptr(wf), _ptr(tok_off), _ptr(tok), _ptr(src_blocks), _ptr(st)))
+        return st
+
     def kv_ptr(self):
         p, bb = C.c_void_p(), C.c_int64()
         self.api.check("pool_kv", self.api.pool_kv(self.h, C.byref(p), C.byref(bb)))
         return p.value, bb.value
+
+
+class Peer:
+    """Another process's pool payload mapped into this one (sfkv_peer_open over CUDA IPC)."""
+
+    def __init__(self, api: Api, handle: bytes, device: int):
+        h = IpcHandle.from_buffer_copy(handle)
+        self.api = api
+        self.h = C.c_void_p()
+        api.check("peer_open", api.peer_open(C.byref(h), int(device), C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            self.api.peer_close(self.h)
+            self.h = None

@@ -396,7 +396,7 @@ int sfkv_commit_batch(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t*
     SFKV_CUDA(cudaMemcpyAsync(dko, kv_src_off, n * sizeof(int64_t), cudaMemcpyHostToDevice, p->stream));
   }
   if (int rc = commit_dev(p, n, dwf, doff, dtok, host_items(n, tok_off), kv_src, dko, dme, dst,
-                          nullptr, 0))
+                          nullptr))
     return rc;
   SFKV_CUDA(cudaMemcpyAsync(out_status, dst, n * sizeof(int32_t), cudaMemcpyDeviceToHost, p->stream));
   return check_sticky(p);
@@ -411,7 +411,7 @@ int sfkv_commit_batch_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int6
   DeviceGuard g(p->cfg.device);
   if (n_tokens < 0) return fail(SFKV_EINVAL, "commit_batch_dev: negative n_tokens");
   return commit_dev(p, n, wf, tok_off, tok, n + n_tokens / BT, kv_src, kv_src_off, m_expected,
-                    out_status, nullptr, 0);
+                    out_status, nullptr);
 }
 
 // ---------------------------------------------------------------- evict -------------------
@@ -615,11 +615,130 @@ int sfkv_handoff(sfkv_pool* src, int32_t wf_src, sfkv_pool* dst, int32_t wf_dst,
     DeviceGuard gs(src->cfg.device);
     SFKV_CUDA(cudaStreamSynchronize(src->stream));
   }
+  PayloadSource ps;
+  ps.kv = src->kv;
+  ps.blk = src->pin_blk + (int64_t)wf_src * src->cfg.max_pin_blocks;  // item k = block k
+  ps.block_bytes = src->block_bytes;
   if (int rc = commit_dev(dst, 1, dwf, doff, dtok, nb, nullptr, nullptr, nullptr, dst_status,
-                          dst->kv ? src : nullptr, wf_src))
+                          dst->kv ? &ps : nullptr))
     return rc;
   SFKV_CUDA(cudaMemcpyAsync(status, dst_status, sizeof(int32_t), cudaMemcpyDeviceToHost, dst->stream));
   return check_sticky(dst);
+}
+
+
+// ---------------------------------------------------------------- cross-process handoff ---
+int sfkv_pool_export(sfkv_pool* p, sfkv_ipc_handle* out) {
+  if (!p || !out) return fail(SFKV_EINVAL, "pool_export: null argument");
+  if (!p->kv) return fail(SFKV_EINVAL, "pool_export: pool has no KV payload (n_slabs == 0)");
+  DeviceGuard g(p->cfg.device);
+  static_assert(sizeof(cudaIpcMemHandle_t) <= sizeof(out->handle), "ipc handle size");
+  cudaIpcMemHandle_t h;
+  SFKV_CUDA(cudaIpcGetMemHandle(&h, p->kv));
+  memset(out, 0, sizeof(*out));
+  memcpy(out->handle, &h, sizeof(h));
+  out->kv_bytes = p->cfg.n_blocks * p->block_bytes;
+  out->block_bytes = p->block_bytes;
+  out->n_slabs = p->cfg.n_slabs;
+  out->slab_row_bytes = p->cfg.slab_row_bytes;
+  return 0;
+}
+
+int sfkv_peer_open(const sfkv_ipc_handle* h, int32_t device, sfkv_peer** out) {
+  if (!h || !out) return fail(SFKV_EINVAL, "peer_open: null argument");
+  if (int rc = check_device(device)) return rc;
+  DeviceGuard g(device);
+  cudaIpcMemHandle_t ih;
+  memcpy(&ih, h->handle, sizeof(ih));
+  void* ptr = nullptr;
+  SFKV_CUDA(cudaIpcOpenMemHandle(&ptr, ih, cudaIpcMemLazyEnablePeerAccess));
+  auto* peer = new sfkv_peer;
+  peer->device = device;
+  peer->kv = static_cast<uint8_t*>(ptr);
+  peer->kv_bytes = h->kv_bytes;
+  peer->block_bytes = h->block_bytes;
+  peer->n_slabs = h->n_slabs;
+  peer->slab_row_bytes = h->slab_row_bytes;
+  *out = peer;
+  return 0;
+}
+
+int sfkv_peer_close(sfkv_peer* peer) {
+  if (!peer) return fail(SFKV_EINVAL, "peer_close: null peer");
+  DeviceGuard g(peer->device);
+  cudaError_t e = cudaIpcCloseMemHandle(peer->kv);
+  delete peer;
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
+  return 0;
+}
+
+int sfkv_pin_export(sfkv_pool* p, int32_t wf, uint32_t* tok, int32_t* block_ids, int64_t cap,
+                    int64_t* n_tokens) {
+  if (!p || !n_tokens || wf < 0 || wf >= p->cfg.max_workflows || (cap > 0 && (!tok || !block_ids)))
+    return fail(SFKV_EINVAL, "pin_export: bad argument");
+  if (int rc = sfkv_pin_tokens(p, wf, tok, cap, n_tokens)) return rc;
+  const int64_t L = *n_tokens;
+  if (L <= 0 || cap < L) return 0;
+  DeviceGuard g(p->cfg.device);
+  const int64_t nb = (L + BT - 1) / BT;
+  SFKV_CUDA(cudaMemcpy(block_ids, p->pin_blk + (int64_t)wf * p->cfg.max_pin_blocks,
+                       nb * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+static int handoff_shape_ok(const sfkv_pool* dst, const sfkv_peer* src) {
+  if (!dst->kv) return fail(SFKV_EINVAL, "handoff_recv: destination pool has no KV payload");
+  if (src->n_slabs != dst->cfg.n_slabs || src->slab_row_bytes != dst->cfg.slab_row_bytes)
+    return fail(SFKV_EINVAL, "handoff_recv: pools have different KV shapes");
+  return 0;
+}
+
+int sfkv_handoff_recv_batch(sfkv_pool* dst, const sfkv_peer* src, int64_t n, const int32_t* wf,
+                            const int64_t* tok_off, const uint32_t* tok, const int32_t* src_blocks,
+                            int32_t* out_status) {
+  if (!dst || !src || !out_status || (n > 0 && (!wf || !tok_off || !src_blocks)))
+    return fail(SFKV_EINVAL, "handoff_recv_batch: null argument");
+  if (n == 0) return 0;
+  if (int rc = handoff_shape_ok(dst, src)) return rc;
+  if (int rc = validate_batch_host(dst, n, wf, tok_off)) return rc;
+  DeviceGuard g(dst->cfg.device);
+  const int64_t items = host_items(n, tok_off);
+  int32_t* dwf;
+  int64_t* doff;
+  uint32_t* dtok;
+  char* ex;
+  const size_t o_blk = (n * sizeof(int32_t) + 255) & ~size_t(255);
+  if (int rc = stage_batch(dst, n, wf, tok_off, tok, o_blk + items * sizeof(int32_t) + 16, &dwf, &doff,
+                           &dtok, &ex))
+    return rc;
+  int32_t* dstatus = reinterpret_cast<int32_t*>(ex);
+  int32_t* dblk = reinterpret_cast<int32_t*>(ex + o_blk);
+  if (items > 0)
+    SFKV_CUDA(cudaMemcpyAsync(dblk, src_blocks, items * sizeof(int32_t), cudaMemcpyHostToDevice, dst->stream));
+  PayloadSource ps;
+  ps.kv = src->kv;
+  ps.blk = dblk;
+  ps.block_bytes = src->block_bytes;
+  if (int rc = commit_dev(dst, n, dwf, doff, dtok, items, nullptr, nullptr, nullptr, dstatus, &ps))
+    return rc;
+  SFKV_CUDA(cudaMemcpyAsync(out_status, dstatus, n * sizeof(int32_t), cudaMemcpyDeviceToHost, dst->stream));
+  return check_sticky(dst);
+}
+
+int sfkv_handoff_recv_batch_dev(sfkv_pool* dst, const sfkv_peer* src, int64_t n, const int32_t* wf,
+                                const int64_t* tok_off, const uint32_t* tok, int64_t n_tokens,
+                                const int32_t* src_blocks, int32_t* out_status) {
+  if (!dst || !src || !out_status || (n > 0 && (!wf || !tok_off || !tok || !src_blocks)))
+    return fail(SFKV_EINVAL, "handoff_recv_batch_dev: null argument");
+  if (n <= 0) return n == 0 ? 0 : fail(SFKV_EINVAL, "negative batch");
+  if (n_tokens < 0) return fail(SFKV_EINVAL, "handoff_recv_batch_dev: negative n_tokens");
+  if (int rc = handoff_shape_ok(dst, src)) return rc;
+  DeviceGuard g(dst->cfg.device);
+  PayloadSource ps;
+  ps.kv = src->kv;
+  ps.blk = src_blocks;
+  ps.block_bytes = src->block_bytes;
+  return commit_dev(dst, n, wf, tok_off, tok, n + n_tokens / BT, nullptr, nullptr, nullptr, out_status, &ps);
 }
 
 }  // extern "C"

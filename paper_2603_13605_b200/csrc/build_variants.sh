@@ -1,7 +1,7 @@
 #!/bin/bash
 # builds libsfkv variants with different compile-time switches into exp/
 set -e
-cd "$(dirname "$0")/../paper_2603_13605_b200/csrc"
+cd "$(dirname "$0")"; mkdir -p ../../exp
 NVCC=/usr/local/cuda/bin/nvcc
 FLAGS="-O3 -std=c++17 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC,-O2 --expt-relaxed-constexpr"
 for v in "$@"; do

@@ -526,8 +526,8 @@ int maybe_rebuild_table(sfkv_pool* p) {
 }
 
 static int launch_commit_payload(sfkv_pool* p, const CommitArgs& a, const void* kv_src,
-                                 const int64_t* kv_src_off, const sfkv_pool* src_pool,
-                                 int32_t src_wf, cudaStream_t st) {
+                                 const int64_t* kv_src_off, const PayloadSource* src,
+                                 cudaStream_t st) {
   PayloadJob j;
   j.n = a.n;
   j.wf = a.wf;
@@ -541,13 +541,13 @@ static int launch_commit_payload(sfkv_pool* p, const CommitArgs& a, const void* 
   j.old_pin_blk = p->pin_blk;
   j.max_pin_blocks = p->cfg.max_pin_blocks;
   j.error = &p->ctr->error;
-  return launch_payload(p, j, kv_src, kv_src_off, src_pool, src_wf, st);
+  return launch_payload(p, j, kv_src, kv_src_off, src, st);
 }
 
 int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
                const uint32_t* tok, int64_t n_items_bound, const void* kv_src,
                const int64_t* kv_src_off, const int64_t* m_expected, int32_t* out_status,
-               const sfkv_pool* src_pool, int32_t src_wf) {
+               const PayloadSource* src) {
   if (n <= 0) return 0;
   cudaStream_t st = p->stream;
   const int64_t ni = n_items_bound > 0 ? n_items_bound : 1;
@@ -569,7 +569,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   a.tok_off = tok_off;
   a.tok = tok;
   a.m_expected = m_expected;
-  a.payload = (p->kv && (kv_src || src_pool)) ? 1 : 0;
+  a.payload = (p->kv && (kv_src || src)) ? 1 : 0;
   a.n_items = ni;
   a.s.blk_off = reinterpret_cast<int64_t*>(base + o_blk);
   a.s.M = reinterpret_cast<int64_t*>(base + o_M);
@@ -616,7 +616,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   SFKV_LAUNCH_CHECK("alloc/refs");
   // 3. payload (copy-on-share + staging scatter / handoff pull)
   if (a.payload) {
-    if (int rc = launch_commit_payload(p, a, kv_src, kv_src_off, src_pool, src_wf, st)) return rc;
+    if (int rc = launch_commit_payload(p, a, kv_src, kv_src_off, src, st)) return rc;
   }
   // 4. release old pins, install new ones
   release_kernel<<<grid_for(n * 32, 256, sms * 8), 256, 0, st>>>(a, 0, nullptr);

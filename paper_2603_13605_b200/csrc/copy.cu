@@ -54,8 +54,8 @@ struct PayloadKernelArgs {
   int64_t row;
   const uint8_t* staging;
   const int64_t* staging_off;
-  const uint8_t* src_kv;   // handoff source pool payload (may be a peer device's memory)
-  const int32_t* src_blk;  // handoff source pin's block table
+  const uint8_t* src_kv;   // handoff source payload (another pool, or a peer rank's over NVLink)
+  const int32_t* src_blk;  // handoff source block of every batch item
   int64_t src_block_bytes;
 };
 
@@ -86,8 +86,8 @@ __global__ void __launch_bounds__(256) payload_kernel(PayloadKernelArgs P) {
     }
     if (nval > j0) {
       const uint8_t* src;
-      if (P.src_kv) {  // handoff: same rows of the source pin's block k
-        src = P.src_kv + (int64_t)P.src_blk[k] * P.src_block_bytes + ((int64_t)s * BT + j0) * P.row;
+      if (P.src_kv) {  // handoff: same rows of the source block of this item
+        src = P.src_kv + (int64_t)P.src_blk[item] * P.src_block_bytes + ((int64_t)s * BT + j0) * P.row;
       } else {  // staging rows [M, P): row index (k*16 + j0 - M)
         src = P.staging + P.staging_off[r] + ((int64_t)s * (len - M) + k * BT + j0 - M) * P.row;
       }
@@ -108,7 +108,7 @@ static int sm_count_p() {
 }
 
 int launch_payload(sfkv_pool* p, const PayloadJob& j, const void* kv_src, const int64_t* kv_src_off,
-                   const sfkv_pool* src_pool, int32_t src_wf, cudaStream_t st) {
+                   const PayloadSource* src, cudaStream_t st) {
   PayloadKernelArgs P;
   P.j = j;
   P.kv = p->kv;
@@ -117,9 +117,9 @@ int launch_payload(sfkv_pool* p, const PayloadJob& j, const void* kv_src, const 
   P.row = p->cfg.slab_row_bytes;
   P.staging = static_cast<const uint8_t*>(kv_src);
   P.staging_off = kv_src_off;
-  P.src_kv = src_pool ? src_pool->kv : nullptr;
-  P.src_blk = src_pool ? src_pool->pin_blk + (int64_t)src_wf * src_pool->cfg.max_pin_blocks : nullptr;
-  P.src_block_bytes = src_pool ? src_pool->block_bytes : 0;
+  P.src_kv = src ? src->kv : nullptr;
+  P.src_blk = src ? src->blk : nullptr;
+  P.src_block_bytes = src ? src->block_bytes : 0;
   payload_kernel<<<sm_count_p() * 8, 256, 0, st>>>(P);
   SFKV_LAUNCH_CHECK("payload_kernel");
   return 0;

@@ -42,6 +42,16 @@ struct DevCounters {
 
 }  // namespace sfkv
 
+// A peer rank's pool payload mapped into this process (CUDA IPC).
+struct sfkv_peer {
+  int32_t device = 0;
+  uint8_t* kv = nullptr;
+  int64_t kv_bytes = 0;
+  int64_t block_bytes = 0;
+  int32_t n_slabs = 0;
+  int32_t slab_row_bytes = 0;
+};
+
 struct sfkv_pool {
   sfkv_pool_config cfg;
   int64_t block_bytes = 0;
@@ -114,17 +124,25 @@ struct PayloadJob {
   int32_t max_pin_blocks;
   const int* error;  // sticky batch error: no bytes move when set
 };
+// Handoff payload source: rows of batch item `item` (request r's block k) come from block
+// blk[item] of the source region kv (another pool of this process, or a peer rank's pool mapped
+// over CUDA IPC: reads then travel over NVLink).
+struct PayloadSource {
+  const uint8_t* kv = nullptr;
+  const int32_t* blk = nullptr;
+  int64_t block_bytes = 0;
+};
 int launch_payload(sfkv_pool* p, const PayloadJob& j, const void* kv_src, const int64_t* kv_src_off,
-                   const sfkv_pool* src_pool, int32_t src_wf, cudaStream_t st);
+                   const PayloadSource* src, cudaStream_t st);
 
 int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStream_t st);
 size_t match_tile_state_elems(int64_t n_items, int64_t n_requests);
 
-// Internal commit entry (device pointers). src_pool/src_wf: handoff payload source.
+// Internal commit entry (device pointers). src: handoff payload source (nullable).
 int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
                const uint32_t* tok, int64_t n_items_bound, const void* kv_src,
                const int64_t* kv_src_off, const int64_t* m_expected, int32_t* out_status,
-               const sfkv_pool* src_pool, int32_t src_wf);
+               const PayloadSource* src);
 int flush_dev(sfkv_pool* p, int64_t n, const int32_t* wf, int64_t* out_freed, bool all);
 int gather_dev(sfkv_pool* p, int64_t n, const int32_t* wf, void* dst, const int64_t* dst_off);
 int maybe_rebuild_table(sfkv_pool* p);

@@ -6,10 +6,16 @@ mapped to another backend ships the workflow's retained context to that backend'
 
     header (pin length L)  ->  token ids [L] (u32)  ->  KV rows [slab][L][row] (payload pools)
 
-sent point to point with torch.distributed (NCCL over NVLink between B200 ranks, gloo on CPU). The
-receiver commits it as its own pin: M = LCP(its old pin, tokens) rows come from its old pin by
-copy-on-share inside sfkv_commit_batch, only rows [M, L) are read from the message. Within one
-process that owns several GPUs, sfkv_handoff does the same transfer as a single peer-pull kernel.
+sent point to point with torch.distributed (the portable message path: `send_pin` / `recv_pin`,
+also what the CPU oracle pools run under gloo). The receiver commits it as its own pin: M =
+LCP(its old pin, tokens) rows come from its old pin by copy-on-share inside sfkv_commit_batch, only
+rows [M, L) are read from the message.
+
+The B200 path is `PeerLink`: every rank exports its pool's KV region once as a CUDA IPC handle and
+maps its peers' regions, so a handoff ships only metadata (tokens + the source pin's block ids)
+and the receiver's commit kernel pulls the payload rows straight out of the sender's HBM over
+NVLink (sfkv_handoff_recv_batch): one kernel, no gather, no staging buffer, no NCCL payload copy.
+Within one process that owns several GPUs, sfkv_handoff does the same transfer.
 
 `max_over_ranks` / `aggregate_rate` implement bench.py's timing rule (max time over ranks, whole-job
 units / that time).
@@ -96,6 +102,99 @@ def recv_pin(pool: Pool, wf: int, src: int, device=None, group=None):
     st = pool.commit(wfa, off, t, kv_src=staging, kv_src_off=np.zeros(1, dtype=np.int64),
                      m_expected=np.array([M], dtype=np.int64))
     return int(st[0])
+
+
+def _meta_device(group=None):
+    """Metadata tensors live on the GPU for NCCL groups, on the CPU for gloo."""
+    import torch
+    dist = _dist()
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+class PeerLink:
+    """CUDA-IPC links between the ranks' pools (one process per GPU).
+
+    send(wfs, dst) ships the pins' metadata to rank dst and waits for its ack (the blocks must stay
+    resident until the receiver has pulled them); recv(wf_dst, src) commits the incoming contexts
+    into this rank's pool with the payload pulled from rank src's pool over NVLink."""
+
+    def __init__(self, pool: Pool, device: int, group=None):
+        import ctypes as C
+
+        from .abi import Peer
+        dist = _dist()
+        self.pool, self.group = pool, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, (pool.export(), device), group=group)
+        self.peers = {}
+        for r, (h, _dev) in enumerate(handles):
+            if r != self.rank:
+                self.peers[r] = Peer(pool.api, h, device)
+        self._C = C
+
+    def close(self):
+        for p in self.peers.values():
+            p.close()
+        self.peers = {}
+
+    def metadata(self, wfs):
+        """CSR (tok_off, tok, src_blocks) of the pins of `wfs` in this rank's pool."""
+        toks, blks = [], []
+        for w in wfs:
+            t, b = self.pool.pin_export(int(w))
+            toks.append(t)
+            blks.append(b)
+        off, tok = csr(toks)
+        blocks = np.concatenate(blks).astype(np.int32) if blks else np.zeros(0, np.int32)
+        return off, tok, blocks
+
+    def send(self, wfs, dst: int):
+        import torch
+        dist = _dist()
+        dev = _meta_device(self.group)
+        off, tok, blocks = self.metadata(wfs)
+        hdr = torch.tensor([len(wfs), int(off[-1]), len(blocks)], dtype=torch.int64)
+        dist.send(hdr.to(dev), dst, group=self.group)
+        dist.send(torch.from_numpy(off).to(dev), dst, group=self.group)
+        if off[-1]:
+            dist.send(torch.from_numpy(tok[: off[-1]].view(np.int32).copy()).to(dev), dst, group=self.group)
+            dist.send(torch.from_numpy(blocks).to(dev), dst, group=self.group)
+        ack = torch.zeros(1, dtype=torch.int64, device=dev)
+        dist.recv(ack, dst, group=self.group)  # the receiver has pulled every block
+        return int(ack.item())
+
+    def recv_metadata(self, src: int):
+        import torch
+        dist = _dist()
+        dev = _meta_device(self.group)
+        hdr = torch.zeros(3, dtype=torch.int64, device=dev)
+        dist.recv(hdr, src, group=self.group)
+        n, T, B = (int(x) for x in hdr.cpu())
+        off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        dist.recv(off, src, group=self.group)
+        tok = torch.zeros(max(T, 1), dtype=torch.int32, device=dev)
+        blocks = torch.zeros(max(B, 1), dtype=torch.int32, device=dev)
+        if T:
+            dist.recv(tok[:T], src, group=self.group)
+            dist.recv(blocks[:B], src, group=self.group)
+        return (off.cpu().numpy(), tok.cpu().numpy().view(np.uint32), blocks.cpu().numpy())
+
+    def ack(self, src: int, value: int = 1):
+        import torch
+        _dist().send(torch.tensor([value], dtype=torch.int64, device=_meta_device(self.group)), src,
+                     group=self.group)
+
+    def recv(self, wf_dst, src: int):
+        """Receive a batch from rank src, pull its payload over NVLink, ack. Returns statuses."""
+        off, tok, blocks = self.recv_metadata(src)
+        wf_dst = np.ascontiguousarray(wf_dst, dtype=np.int32)
+        assert len(wf_dst) == len(off) - 1
+        st = self.pool.handoff_recv(self.peers[src], wf_dst, off, tok, blocks)
+        self.ack(src)
+        return st
 
 
 def max_over_ranks(x: float, device=None) -> float:
