@@ -365,6 +365,7 @@ def run_ours(args, rank, world, local_rank):
         kv = None if args.no_kv else kv_legs(args, api, dev, stream, hbm_peak, rank)
         c5 = None if args.no_c5 else lookup_leg(args, api, dev, stream, hbm_peak, rank)
         c4 = None if args.no_c4 else long_context_leg(args, api, dev, stream, hbm_peak, rank)
+        c3 = handoff_leg(args, api, dev, stream, rank, world) if (dist and not args.no_c3) else None
     clocks = clk.summary()
 
     # ---- roofline of the match kernel: algorithmic bytes of one launch --------------------
@@ -401,6 +402,8 @@ def run_ours(args, rank, world, local_rank):
         line["c5_lookup"] = c5
     if c4:
         line["c4_long_context"] = c4
+    if c3:
+        line["c3_handoff"] = c3
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
     pool.close()
@@ -703,6 +706,103 @@ def long_context_leg(args, api, dev, stream, hbm_peak, rank):
                       "flush_ms": flush_ms}}
 
 
+NVLINK_GBPS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md; 900 nominal)
+
+
+def handoff_leg(args, api, dev, stream, rank, world):
+    """C3: cross-GPU stage handoff, one backend pool per GPU (BASELINE configs[2]).
+
+    Every rank pins H Llama-3-8B contexts, then each step every rank takes over the H retained
+    contexts of rank (r-1) mod N as new pins of its own: sfkv_handoff_recv_batch pulls the
+    source blocks' rows straight out of the peer's HBM over NVLink (CUDA-IPC-mapped pool) inside
+    the commit's payload kernel. All ranks pull concurrently (a ring: every GPU sends and
+    receives H contexts per step). The received pins are flushed between steps (untimed) so every
+    step moves every byte."""
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2603_13605_b200 import dist as sfdist
+    from paper_2603_13605_b200.abi import Config, Pool, csr
+    H, ctx = args.c3_workflows, args.kv_context
+    nblk = (ctx + BT - 1) // BT
+    cfg = Config(max_workflows=2 * H, n_blocks=2 * H * nblk + 64, capacity_tokens=1 << 50,
+                 max_pin_blocks=nblk + 2, table_log2=int(math.log2(2 * H * nblk + 64)) + 2,
+                 n_slabs=KV_SLABS, slab_row_bytes=KV_ROW, device=dev)
+    pool = Pool(api, cfg)
+    tok_bytes = KV_SLABS * KV_ROW
+    rng = np.random.default_rng(args.seed + 1000 + rank)
+    ctxs = [rng.integers(1, 1 << 30, size=ctx).astype(np.uint32) for _ in range(H)]
+    staging = torch.randint(0, 255, (ctx * tok_bytes,), dtype=torch.uint8, device=dev)
+    for i in range(H):  # each context's KV comes from its prefill (staging)
+        off, tok = csr([ctxs[i]])
+        assert pool.commit(np.array([i], np.int32), off, tok, kv_src=staging,
+                           kv_src_off=np.zeros(1, np.int64))[0] == 1
+    del staging
+    link = sfdist.PeerLink(pool, dev)
+    src, dst = (rank - 1) % world, (rank + 1) % world
+    off, tok, blocks = link.metadata(range(H))  # what this rank ships to dst
+    mdev = sfdist._meta_device()  # metadata travels over NCCL (GPU tensors) or gloo (CPU)
+    t_out = torch.from_numpy(tok.view(np.int32).copy()).to(mdev)
+    b_out = torch.from_numpy(blocks).to(mdev)
+    t_in, b_in = torch.empty_like(t_out), torch.empty_like(b_out)  # src's: same shapes by construction
+    ops = [tdist.P2POp(tdist.isend, t_out, dst), tdist.P2POp(tdist.isend, b_out, dst),
+           tdist.P2POp(tdist.irecv, t_in, src), tdist.P2POp(tdist.irecv, b_in, src)]
+    for w in tdist.batch_isend_irecv(ops):
+        w.wait()
+    d_tok, d_blk = t_in.to(dev), b_in.to(dev)
+    torch.cuda.synchronize()
+    d_off = torch.from_numpy(off).to(dev)
+    wf_in = np.arange(H, 2 * H, dtype=np.int32)
+    d_wf = torch.from_numpy(wf_in).to(dev)
+    d_st = torch.zeros(H, dtype=torch.int32, device=dev)
+    peer = link.peers[src]
+    api.check("set_stream", api.pool_set_stream(pool.h, C.c_void_p(stream.cuda_stream)))
+
+    def pull():
+        api.check("handoff_recv_batch_dev", api.handoff_recv_batch_dev(
+            pool.h, peer.h, H, C.c_void_p(d_wf.data_ptr()), C.c_void_p(d_off.data_ptr()),
+            C.c_void_p(d_tok.data_ptr()), int(off[-1]), C.c_void_p(d_blk.data_ptr()),
+            C.c_void_p(d_st.data_ptr())))
+
+    times = []
+    for it in range(args.warmup + args.steps):
+        tdist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        pull()
+        b.record(stream)
+        torch.cuda.synchronize()
+        assert bool((d_st == 1).all()), "handoff rejected"
+        if it >= args.warmup:
+            times.append(a.elapsed_time(b))
+        if it == 0:  # the received context is src's first one (tokens)
+            got = pool.pin_tokens(H)
+            assert (got == d_tok[:ctx].cpu().numpy().view(np.uint32)).all()
+        pool.flush_batch(wf_in)  # untimed: the next step moves every byte again
+    local_ms = float(np.mean(times))
+    ms = sfdist.max_over_ranks(local_ms, dev)
+    moved = H * ctx * tok_bytes  # bytes pulled over NVLink per rank per step (= egress per GPU)
+    gbps = moved / (ms / 1e3) / 1e9
+    tdist.barrier()
+    link.close()
+    pool.close()
+    if args.same_device:  # test mode: the "peer" is the same HBM, the pull is a local copy
+        hbm = peaks()[0]
+        roof = {"bound": "hbm (same-device test mode)", "achieved": 2 * gbps * world, "peak": hbm,
+                "unit": "GB/s", "frac": 2 * gbps * world / hbm}
+    else:
+        roof = {"bound": "nvlink", "achieved": gbps, "peak": NVLINK_GBPS, "unit": "GB/s",
+                "frac": gbps / NVLINK_GBPS,
+                "peak_source": "measured peer copy per direction (B200_PROFILING.md); 900 nominal"}
+    return {"workload": f"C3: ring of {world} pools, each step every GPU takes over the {H} "
+                        f"retained {ctx}-token Llama-3-8B contexts of its predecessor "
+                        "(CUDA-IPC pull inside the commit kernel)",
+            "contexts_per_gpu": H, "bytes_per_gpu_per_step": moved, "ms": ms,
+            "per_gpu_gbps": gbps, "aggregate_gbps": gbps * world, "roofline": roof}
+
+
+
 def cpu_baseline(args):
     L = ref_lib()
     n_sample = args.cpu_sample
@@ -732,6 +832,10 @@ def main():
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--c5-prefixes", type=int, default=100_000)
+    ap.add_argument("--no-c3", action="store_true")
+    ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--dist-backend", default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--c3-workflows", type=int, default=32)
     ap.add_argument("--kv-pool-gib", type=int, default=64)
     ap.add_argument("--kv-workflows", type=int, default=200)
     ap.add_argument("--kv-context", type=int, default=2008)
@@ -750,11 +854,14 @@ def main():
         tp = os.path.join(REPO, "profiles", "match_traffic.json")
         if os.path.exists(tp):
             args.traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    if args.same_device:  # test mode: every rank on device 0 (CUDA IPC within one GPU; gloo)
+        local_rank = 0
     if world > 1:
         import torch
         import torch.distributed as tdist
         torch.cuda.set_device(local_rank)
-        tdist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        backend = args.dist_backend or ("nccl" if args.impl == "ours" else "gloo")
+        tdist.init_process_group(backend)
     if args.impl == "reference":
         rc = run_reference_arm(args, rank, world)
     else:

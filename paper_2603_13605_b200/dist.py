@@ -203,7 +203,7 @@ def max_over_ranks(x: float, device=None) -> float:
     dist = _dist()
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(x)
-    t = torch.tensor([float(x)], dtype=torch.float64, device=device or "cpu")
+    t = torch.tensor([float(x)], dtype=torch.float64, device=_meta_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -215,7 +215,7 @@ def aggregate_rate(local_units: float, local_ms: float, device=None) -> float:
     ms = max_over_ranks(local_ms, device)
     units = float(local_units)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        t = torch.tensor([units], dtype=torch.float64, device=device or "cpu")
+        t = torch.tensor([units], dtype=torch.float64, device=_meta_device())
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         units = float(t.item())
     return units / (ms / 1e3)
