@@ -213,6 +213,105 @@ int sfmm_pressure_argmin(int32_t device, int64_t n, const int32_t* backend, cons
                          const uint8_t* preserved, int32_t n_backends, const double* util,
                          double tau, int64_t* out_victim);
 
+/* ---- memory manager: batched MemoryManager::on_signal and pressure_tick on a GPU-resident
+ *      WorkflowTracker (memory.cpp:256-387) ------------------------------------
+ * The tracker (memory.hpp:49-72: cache entries, in-flight counts, last stage, completion, plus
+ * the manager's started/open stage sets and per-workflow chains) lives in HBM as dense arrays
+ * over (workflow slot, backend index). Workflow ids, stage ids, backend refs and models are
+ * interned by the host: backends are indexed in sorted-ref order (BackendRegistry::refs), stage
+ * ids are dense per workflow (< SFMM_MAX_STAGES), models are dense ids.
+ * sfmm_on_signal_batch applies a batch of lifecycle signals exactly as n sequential on_signal
+ * calls would: policies read only their own workflow's state, so the batch is processed in
+ * parallel across workflows and in order within each. Signal i's log records (on_signal logs
+ * every returned action, noops included, memory.cpp:312-328) are written at
+ * [i * n_backends, i * n_backends + count[i]); the action log of the batch is the concatenation
+ * in signal order. Flushes are recorded as applied (the sfkv pools cannot fail a flush), so the
+ * tracker erases the entry (memory.cpp:319-321); the host issues the pool flushes / preserves
+ * (sfkv_flush_batch / sfkv_preserve) from the records. A signal that the reference would reject
+ * (OutOfOrderSignalError, memory.cpp:256-285) gets status SFMM_SIG_OUT_OF_ORDER and produces no
+ * records; the rest of that workflow's signals in the batch are SFMM_SIG_SKIPPED.
+ * sfmm_pressure_tick replaces MemoryManager::pressure_tick (memory.cpp:372-387): per backend with
+ * util > tau_pressure, the idle preserved entry with least (last_update_ts, workflow rank) is
+ * flushed (recorded with reason flush_under_pressure) and erased from the tracker. */
+#define SFMM_MAX_STAGES 64
+#define SFMM_MAX_CHAIN 8
+/* LifecycleSignal::Kind (signals.hpp:13-15) */
+#define SFMM_STAGE_START 0
+#define SFMM_STAGE_COMPLETE 1
+#define SFMM_WORKFLOW_COMPLETE 2
+/* CachePolicyOverride (workflow.hpp:16) */
+#define SFMM_OVERRIDE_NONE 0
+#define SFMM_OVERRIDE_PRESERVE 1
+#define SFMM_OVERRIDE_FLUSH 2
+/* memory_policy_by_name (memory.cpp:171-183) */
+#define SFMM_POLICY_PRESERVE_SMALL_INCREMENT 1
+#define SFMM_POLICY_FLUSH_AT_BOUNDARY 2
+/* CacheAction::Kind (memory.hpp:20) */
+#define SFMM_ACT_PRESERVE 0
+#define SFMM_ACT_FLUSH 1
+#define SFMM_ACT_NOOP 2
+/* CacheAction::reason values the built-in code produces */
+#define SFMM_REASON_OVERRIDE 0
+#define SFMM_REASON_PRESERVE_SMALL_INCREMENT 1
+#define SFMM_REASON_FLUSH_AT_BOUNDARY 2
+#define SFMM_REASON_FLUSH_UNDER_PRESSURE 3
+#define SFMM_REASON_CHAIN_EXHAUSTED 4
+/* per-signal status */
+#define SFMM_SIG_OK 0
+#define SFMM_SIG_OUT_OF_ORDER 1     /* OutOfOrderSignalError */
+#define SFMM_SIG_SKIPPED 2          /* an earlier signal of the workflow in this batch failed */
+#define SFMM_SIG_NEGATIVE_IN_FLIGHT 3 /* logic_error("in-flight count went negative") */
+
+typedef struct sfmm_tracker sfmm_tracker;
+
+typedef struct sfmm_config {
+  int32_t device;
+  int32_t max_workflows;
+  int32_t n_backends;
+  int32_t chain_len;                 /* default policy chain (MemoryConfig::policy_chain) */
+  uint8_t chain[SFMM_MAX_CHAIN];
+  int64_t tau;                       /* MemoryConfig::tau (memory.hpp:74-79) */
+  double tau_pressure;               /* MemoryConfig::tau_pressure */
+} sfmm_config;
+
+typedef struct sfmm_signals {        /* n signals, struct of arrays */
+  const uint8_t* kind;
+  const int32_t* wf;
+  const int32_t* stage;              /* dense per workflow; ignored for WorkflowComplete */
+  const int32_t* backend;            /* ignored for WorkflowComplete */
+  const int32_t* model;
+  const int64_t* tokens;             /* context_tokens */
+  const double* ts;
+  const uint8_t* override_;          /* cache_override */
+} sfmm_signals;
+
+typedef struct sfmm_records {        /* outputs: n signals x n_backends record slots */
+  int32_t* count;                    /* [n] records of signal i */
+  uint8_t* status;                   /* [n] SFMM_SIG_* */
+  uint8_t* kind;                     /* [n * n_backends] SFMM_ACT_* */
+  int32_t* backend;                  /* [n * n_backends] -1 for noops */
+  uint8_t* reason;                   /* [n * n_backends] SFMM_REASON_* */
+} sfmm_records;
+
+int sfmm_tracker_create(const sfmm_config* cfg, sfmm_tracker** out);
+int sfmm_tracker_destroy(sfmm_tracker* t);
+int sfmm_tracker_set_stream(sfmm_tracker* t, void* cuda_stream);
+int sfmm_tracker_sync(sfmm_tracker* t);
+/* Forget every workflow (a fresh MemoryManager with the same configuration). */
+int sfmm_tracker_reset(sfmm_tracker* t);
+/* MemoryManager::set_workflow_chain (memory.cpp:246-250); len 0 = no-op, as the reference. */
+int sfmm_set_workflow_chain(sfmm_tracker* t, int32_t wf, int32_t len, const uint8_t* policies);
+/* Rank of every workflow slot in workflow-id string order (pressure tie-break). */
+int sfmm_set_workflow_ranks(sfmm_tracker* t, int64_t n, const uint32_t* rank);
+int sfmm_on_signal_batch(sfmm_tracker* t, int64_t n, const sfmm_signals* sig, const sfmm_records* out);
+int sfmm_on_signal_batch_dev(sfmm_tracker* t, int64_t n, const sfmm_signals* sig,
+                             const sfmm_records* out);
+/* util[n_backends] (sorted-ref order) -> out_victim[n_backends] workflow slot or -1. */
+int sfmm_pressure_tick(sfmm_tracker* t, const double* util, int32_t* out_victim);
+/* Tracker snapshot (inspection / parity): per (wf, backend) entry and in-flight count. */
+int sfmm_tracker_entries(sfmm_tracker* t, uint8_t* present, uint8_t* preserved, int64_t* tokens,
+                         double* ts, int32_t* in_flight);
+
 /* ---- stage mapper: replaces map_threshold (mapper.cpp:19-31) and reroute_on_overload
  *      (orchestrator.cpp:78-87) -----------------------------------------------------------------
  * Threshold: out_choice[r] = 0 (light) iff score[r] <= threshold, else 1 (heavy).

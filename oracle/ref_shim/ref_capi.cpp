@@ -9,6 +9,9 @@
 //                                       WorkflowTracker built with its public mutators
 //   sfref_map_threshold               -> map_threshold (mapper.cpp:19-31)
 //   sfref_reroute                     -> reroute_on_overload (orchestrator.cpp:78-87)
+//   sfref_mm_*                        -> MemoryManager::{on_signal, pressure_tick,
+//                                       set_workflow_chain, action_log} (memory.cpp:246-401),
+//                                       no backends attached (every action "applies")
 // Token ids are rendered to whitespace tokens "t<id>", the same text the reference tokenizes.
 #include <cstring>
 
@@ -173,6 +176,74 @@ int sfref_reroute(int n, const unsigned long long* depth, unsigned long long lim
       [&](const std::string& s) { return static_cast<std::size_t>(depth[std::stoi(s)]); },
       static_cast<std::size_t>(limit));
   return std::stoi(pick);
+}
+
+// ---- MemoryManager ------------------------------------------------------------------------
+void* sfref_mm_create(long long tau, double tau_pressure, int chain_len, const char* const* chain) {
+  MemoryConfig cfg;
+  cfg.tau = tau;
+  cfg.tau_pressure = tau_pressure;
+  cfg.policy_chain.assign(chain, chain + chain_len);
+  return new MemoryManager(cfg);
+}
+void sfref_mm_destroy(void* h) { delete static_cast<MemoryManager*>(h); }
+
+void sfref_mm_set_chain(void* h, const char* wf, int len, const char* const* names) {
+  std::vector<std::string> v(names, names + len);
+  static_cast<MemoryManager*>(h)->set_workflow_chain(wf, v);
+}
+
+// kind 0/1/2 = StageStart/StageComplete/WorkflowComplete; override 0/1/2 = None/Preserve/Flush.
+// Returns 0, 1 (OutOfOrderSignalError) or 3 (logic_error: in-flight went negative).
+int sfref_mm_on_signal(void* h, int kind, const char* wf, const char* stage, const char* backend,
+                       const char* model, long long tokens, double ts, int override_) {
+  LifecycleSignal sig;
+  sig.kind = static_cast<LifecycleSignal::Kind>(kind);
+  sig.workflow_id = wf;
+  if (kind != 2) {
+    sig.stage_id = stage;
+    sig.backend_ref = backend;
+    sig.model = model;
+    sig.context_tokens = tokens;
+  }
+  sig.ts = ts;
+  sig.cache_override = static_cast<CachePolicyOverride>(override_);
+  try {
+    static_cast<MemoryManager*>(h)->on_signal(sig);
+  } catch (const OutOfOrderSignalError&) {
+    return 1;
+  } catch (const std::logic_error&) {
+    return 3;
+  }
+  return 0;
+}
+
+int sfref_mm_pressure_tick(void* h, int n, const char* const* refs, const double* util, double now) {
+  std::map<std::string, double> u;
+  for (int i = 0; i < n; ++i) u[refs[i]] = util[i];
+  return static_cast<int>(static_cast<MemoryManager*>(h)->pressure_tick(u, now).size());
+}
+
+long long sfref_mm_log_size(void* h) {
+  return static_cast<long long>(static_cast<MemoryManager*>(h)->action_log().size());
+}
+
+// Record i of the action log: kind 0/1/2 = Preserve/Flush/NoOp; strings copied (NUL-terminated,
+// truncated to cap bytes).
+void sfref_mm_log_get(void* h, long long i, int* kind, char* wf, char* backend, char* reason,
+                      char* trigger, int cap, double* ts) {
+  const auto& r = static_cast<MemoryManager*>(h)->action_log().at(static_cast<std::size_t>(i));
+  *kind = static_cast<int>(r.action.kind);
+  *ts = r.ts;
+  auto put = [cap](char* dst, const std::string& s) {
+    std::size_t n = std::min<std::size_t>(s.size(), static_cast<std::size_t>(cap - 1));
+    std::memcpy(dst, s.data(), n);
+    dst[n] = 0;
+  };
+  put(wf, r.action.workflow_id);
+  put(backend, r.action.backend_ref);
+  put(reason, r.action.reason);
+  put(trigger, r.trigger);
 }
 
 }  // extern "C"

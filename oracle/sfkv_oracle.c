@@ -720,3 +720,274 @@ int sfo_cost_batch(int64_t n, int32_t c, const int64_t* P, const int64_t* M, con
   free(depth0);
   return 0;
 }
+
+
+/* ================================================================ memory manager tracker ====
+ * Restates MemoryManager (memory.cpp:233-387) over dense ids: workflow slots, backends in sorted
+ * ref order (map iteration order of entries_ / utilization), per-workflow dense stage ids, model
+ * ids. Signals are applied one at a time in batch order, exactly as on_signal. */
+enum { K_START = 0, K_COMPLETE = 1, K_WF_COMPLETE = 2 };
+enum { O_NONE = 0, O_PRESERVE = 1, O_FLUSH = 2 };
+enum { P_PSI = 1, P_FAB = 2 };
+enum { A_PRESERVE = 0, A_FLUSH = 1, A_NOOP = 2 };
+enum { R_OVERRIDE = 0, R_PSI = 1, R_FAB = 2, R_PRESSURE = 3, R_EXHAUSTED = 4 };
+#define MAXCH 8
+
+struct sfo_tracker {
+  sfo_mm_config cfg;
+  int32_t W, NB;
+  uint8_t* completed;
+  uint64_t* started; /* started_ever_ (memory.hpp:165) */
+  uint64_t* open_;   /* open_stages_ */
+  uint8_t* last_valid;
+  int32_t* last_b;
+  int32_t* last_model;
+  int64_t* last_tokens;
+  int32_t* chain_len; /* -1: default chain (workflow_chains_ has no entry) */
+  uint8_t* chain;
+  uint8_t* present; /* entries_ [(wf, backend)] */
+  uint8_t* preserved;
+  int64_t* tokens;
+  double* ts;
+  int32_t* inflight; /* in_flight_ [backend][wf] */
+  uint32_t* rank;
+  uint8_t* failed; /* per batch */
+};
+
+int sfo_tracker_create(const sfo_mm_config* cfg, sfo_tracker** out) {
+  if (!cfg || !out || cfg->max_workflows <= 0 || cfg->n_backends <= 0 || cfg->chain_len < 0 ||
+      cfg->chain_len > MAXCH || cfg->tau <= 0 || !(cfg->tau_pressure > 0) || cfg->tau_pressure > 1)
+    return -1; /* memory.cpp:240-243 */
+  sfo_tracker* t = (sfo_tracker*)calloc(1, sizeof(*t));
+  t->cfg = *cfg;
+  t->W = cfg->max_workflows;
+  t->NB = cfg->n_backends;
+  size_t W = (size_t)t->W, E = W * (size_t)t->NB;
+  t->completed = calloc(W, 1);
+  t->started = calloc(W, 8);
+  t->open_ = calloc(W, 8);
+  t->last_valid = calloc(W, 1);
+  t->last_b = calloc(W, 4);
+  t->last_model = calloc(W, 4);
+  t->last_tokens = calloc(W, 8);
+  t->chain_len = malloc(W * 4);
+  for (size_t w = 0; w < W; ++w) t->chain_len[w] = -1;
+  t->chain = calloc(W * MAXCH, 1);
+  t->present = calloc(E, 1);
+  t->preserved = calloc(E, 1);
+  t->tokens = calloc(E, 8);
+  t->ts = calloc(E, 8);
+  t->inflight = calloc(E, 4);
+  t->rank = calloc(W, 4);
+  for (size_t w = 0; w < W; ++w) t->rank[w] = (uint32_t)w;
+  t->failed = calloc(W, 1);
+  *out = t;
+  return 0;
+}
+
+int sfo_tracker_destroy(sfo_tracker* t) {
+  if (!t) return -1;
+  free(t->completed); free(t->started); free(t->open_); free(t->last_valid); free(t->last_b);
+  free(t->last_model); free(t->last_tokens); free(t->chain_len); free(t->chain); free(t->present);
+  free(t->preserved); free(t->tokens); free(t->ts); free(t->inflight); free(t->rank); free(t->failed);
+  free(t);
+  return 0;
+}
+
+int sfo_set_workflow_chain(sfo_tracker* t, int32_t wf, int32_t len, const uint8_t* policies) {
+  if (!t || wf < 0 || wf >= t->W || len < 0 || len > MAXCH || (len && !policies)) return -1;
+  if (len == 0) return 0; /* memory.cpp:248 */
+  for (int32_t i = 0; i < len; ++i) {
+    if (policies[i] != P_PSI && policies[i] != P_FAB) return -1; /* unknown policy */
+    t->chain[(size_t)wf * MAXCH + i] = policies[i];
+  }
+  t->chain_len[wf] = len;
+  return 0;
+}
+
+int sfo_set_workflow_ranks(sfo_tracker* t, int64_t n, const uint32_t* rank) {
+  if (!t || n < 0 || n > t->W || (n && !rank)) return -1;
+  for (int64_t w = 0; w < n; ++w) t->rank[w] = rank[w];
+  return 0;
+}
+
+typedef struct { uint8_t kind; int32_t b; uint8_t reason; } act_t;
+
+/* policy_preserve_small_increment (memory.cpp:116-125) */
+static int pol_psi(const sfo_tracker* t, int w, uint8_t kind, int32_t b, int32_t m, int64_t T, act_t* a) {
+  if (kind != K_START || !t->last_valid[w]) return 0;
+  if (t->last_b[w] != b || t->last_model[w] != m) return 0;
+  if (T - t->last_tokens[w] >= t->cfg.tau) return 0;
+  a[0].kind = A_PRESERVE;
+  a[0].b = b;
+  a[0].reason = R_PSI;
+  return 1;
+}
+
+/* policy_flush_at_boundary (memory.cpp:127-148) */
+static int pol_fab(const sfo_tracker* t, int w, uint8_t kind, int32_t b, int32_t m, act_t* a) {
+  int n = 0;
+  size_t e0 = (size_t)w * t->NB;
+  if (kind == K_WF_COMPLETE) {
+    for (int32_t bb = 0; bb < t->NB; ++bb)
+      if (t->present[e0 + bb] && t->preserved[e0 + bb]) {
+        a[n].kind = A_FLUSH;
+        a[n].b = bb;
+        a[n].reason = R_FAB;
+        ++n;
+      }
+    return n;
+  }
+  if (kind == K_START && t->last_valid[w] && (t->last_b[w] != b || t->last_model[w] != m)) {
+    int32_t lb = t->last_b[w];
+    if (t->present[e0 + lb] && t->preserved[e0 + lb]) {
+      a[0].kind = A_FLUSH;
+      a[0].b = lb;
+      a[0].reason = R_FAB;
+      n = 1;
+    }
+  }
+  return n;
+}
+
+int sfo_on_signal_batch(sfo_tracker* t, int64_t n, const sfo_signals* sg, const sfo_records* out) {
+  if (!t || !sg || !out || n < 0) return -1;
+  const int32_t NB = t->NB;
+  act_t* acts = (act_t*)malloc(sizeof(act_t) * (size_t)(NB > 1 ? NB : 1));
+  memset(t->failed, 0, (size_t)t->W);
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t w = sg->wf[i];
+    const uint8_t kind = sg->kind[i];
+    const int32_t s = kind == K_WF_COMPLETE ? 0 : sg->stage[i];
+    const int32_t b = kind == K_WF_COMPLETE ? -1 : sg->backend[i];
+    const int32_t m = kind == K_WF_COMPLETE ? -1 : sg->model[i];
+    const int64_t T = kind == K_WF_COMPLETE ? 0 : sg->tokens[i];
+    const double ts = sg->ts[i];
+    const uint8_t ov = sg->override_ ? sg->override_[i] : O_NONE;
+    out->count[i] = 0;
+    if (w < 0 || w >= t->W || kind > 2 || (kind != K_WF_COMPLETE && (b < 0 || b >= NB || s < 0 || s >= 64))) {
+      free(acts);
+      return -1;
+    }
+    if (t->failed[w]) {
+      out->status[i] = 2;
+      continue;
+    }
+    /* check_order (memory.cpp:256-285) */
+    const uint64_t bit = 1ull << s;
+    int bad = t->completed[w] || (kind == K_START && (t->started[w] & bit)) ||
+              (kind == K_COMPLETE && !(t->open_[w] & bit)) ||
+              (kind == K_WF_COMPLETE && t->open_[w] != 0);
+    if (!bad && kind == K_COMPLETE && t->inflight[(size_t)w * NB + b] <= 0) {
+      /* adjust_in_flight(-1) would go negative: logic_error (memory.cpp:92) after logging */
+      bad = 3;
+    }
+    if (bad == 1) { /* OutOfOrderSignalError: nothing resolved, applied or logged */
+      out->status[i] = 1;
+      t->failed[w] = 1;
+      continue;
+    }
+    /* resolve (memory.cpp:287-310) */
+    int na = 0;
+    if (kind == K_START && ov != O_NONE) {
+      if (!t->last_valid[w]) {
+        acts[0].kind = A_NOOP; acts[0].b = -1; acts[0].reason = R_OVERRIDE;
+      } else {
+        acts[0].kind = ov == O_FLUSH ? A_FLUSH : A_PRESERVE;
+        acts[0].b = t->last_b[w];
+        acts[0].reason = R_OVERRIDE;
+      }
+      na = 1;
+    } else {
+      const int32_t len = t->chain_len[w] >= 0 ? t->chain_len[w] : t->cfg.chain_len;
+      const uint8_t* ch = t->chain_len[w] >= 0 ? t->chain + (size_t)w * MAXCH : t->cfg.chain;
+      for (int32_t p = 0; p < len && na == 0; ++p)
+        na = ch[p] == P_PSI ? pol_psi(t, w, kind, b, m, T, acts) : pol_fab(t, w, kind, b, m, acts);
+      if (na == 0) {
+        acts[0].kind = A_NOOP; acts[0].b = -1; acts[0].reason = R_EXHAUSTED;
+        na = 1;
+      }
+    }
+    /* apply_and_record (memory.cpp:312-328): flushes succeed -> mark_flushed */
+    for (int a = 0; a < na; ++a) {
+      out->kind[(size_t)i * NB + a] = acts[a].kind;
+      out->backend[(size_t)i * NB + a] = acts[a].b;
+      out->reason[(size_t)i * NB + a] = acts[a].reason;
+      if (acts[a].kind == A_FLUSH) t->present[(size_t)w * NB + acts[a].b] = 0;
+    }
+    out->count[i] = na;
+    if (bad == 3) { /* the records were logged, then update_tracker threw */
+      out->status[i] = 3;
+      t->failed[w] = 1;
+      /* update_tracker erased the open stage, then adjust_in_flight stored -1 and threw
+       * (memory.cpp:338-339, 90-92) */
+      t->open_[w] &= ~bit;
+      t->inflight[(size_t)w * NB + b] -= 1;
+      continue;
+    }
+    out->status[i] = 0;
+    /* update_tracker (memory.cpp:330-360) */
+    const size_t e = (size_t)w * NB + (b < 0 ? 0 : b);
+    if (kind == K_START) {
+      t->started[w] |= bit;
+      t->open_[w] |= bit;
+      t->inflight[e] += 1;
+    } else if (kind == K_COMPLETE) {
+      t->open_[w] &= ~bit;
+      t->inflight[e] -= 1;
+      t->present[e] = 1;
+      t->preserved[e] = T > 0;
+      t->tokens[e] = T;
+      t->ts[e] = ts;
+      t->last_valid[w] = 1;
+      t->last_b[w] = b;
+      t->last_model[w] = m;
+      t->last_tokens[w] = T;
+    } else {
+      t->completed[w] = 1;
+      for (int32_t bb = 0; bb < NB; ++bb) {
+        t->present[(size_t)w * NB + bb] = 0;
+        t->inflight[(size_t)w * NB + bb] = 0;
+      }
+      t->last_valid[w] = 0;
+      t->started[w] = 0;
+      t->open_[w] = 0;
+      t->chain_len[w] = -1;
+    }
+  }
+  free(acts);
+  return 0;
+}
+
+/* pressure_tick -> pressure_actions (memory.cpp:150-169, 382-387) */
+int sfo_pressure_tick(sfo_tracker* t, const double* util, int32_t* out_victim) {
+  if (!t || !util || !out_victim) return -1;
+  for (int32_t b = 0; b < t->NB; ++b) {
+    out_victim[b] = -1;
+    if (!(util[b] > t->cfg.tau_pressure)) continue;
+    int32_t best = -1;
+    for (int32_t w = 0; w < t->W; ++w) {
+      size_t e = (size_t)w * t->NB + b;
+      if (!t->present[e] || !t->preserved[e] || t->inflight[e] > 0) continue;
+      size_t eb = (size_t)best * t->NB + b;
+      if (best < 0 || t->ts[e] < t->ts[eb] || (t->ts[e] == t->ts[eb] && t->rank[w] < t->rank[best]))
+        best = w;
+    }
+    out_victim[b] = best;
+  }
+  for (int32_t b = 0; b < t->NB; ++b)
+    if (out_victim[b] >= 0) t->present[(size_t)out_victim[b] * t->NB + b] = 0; /* mark_flushed */
+  return 0;
+}
+
+int sfo_tracker_entries(sfo_tracker* t, uint8_t* present, uint8_t* preserved, int64_t* tokens,
+                        double* ts, int32_t* in_flight) {
+  if (!t) return -1;
+  size_t E = (size_t)t->W * t->NB;
+  if (present) memcpy(present, t->present, E);
+  if (preserved) memcpy(preserved, t->preserved, E);
+  if (tokens) memcpy(tokens, t->tokens, E * 8);
+  if (ts) memcpy(ts, t->ts, E * 8);
+  if (in_flight) memcpy(in_flight, t->inflight, E * 4);
+  return 0;
+}

@@ -81,4 +81,41 @@ int sfo_cost_batch(int64_t n, int32_t c, const int64_t* P, const int64_t* M, con
                    const double* queue_penalty, const int32_t* alternates, uint64_t* depth_inout,
                    uint64_t limit, int32_t* out_choice, double* out_cost);
 
+/* ---- memory manager tracker (restates MemoryManager::on_signal / pressure_tick) ---------- */
+typedef struct sfo_tracker sfo_tracker;
+typedef struct sfo_mm_config { /* same layout as sfmm_config */
+  int32_t device;
+  int32_t max_workflows;
+  int32_t n_backends;
+  int32_t chain_len;
+  uint8_t chain[8];
+  int64_t tau;
+  double tau_pressure;
+} sfo_mm_config;
+typedef struct sfo_signals {
+  const uint8_t* kind;
+  const int32_t* wf;
+  const int32_t* stage;
+  const int32_t* backend;
+  const int32_t* model;
+  const int64_t* tokens;
+  const double* ts;
+  const uint8_t* override_;
+} sfo_signals;
+typedef struct sfo_records {
+  int32_t* count;
+  uint8_t* status;
+  uint8_t* kind;
+  int32_t* backend;
+  uint8_t* reason;
+} sfo_records;
+int sfo_tracker_create(const sfo_mm_config* cfg, sfo_tracker** out);
+int sfo_tracker_destroy(sfo_tracker* t);
+int sfo_set_workflow_chain(sfo_tracker* t, int32_t wf, int32_t len, const uint8_t* policies);
+int sfo_set_workflow_ranks(sfo_tracker* t, int64_t n, const uint32_t* rank);
+int sfo_on_signal_batch(sfo_tracker* t, int64_t n, const sfo_signals* sig, const sfo_records* out);
+int sfo_pressure_tick(sfo_tracker* t, const double* util, int32_t* out_victim);
+int sfo_tracker_entries(sfo_tracker* t, uint8_t* present, uint8_t* preserved, int64_t* tokens,
+                        double* ts, int32_t* in_flight);
+
 #endif

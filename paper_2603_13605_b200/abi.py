@@ -113,6 +113,22 @@ GLOBAL_FNS = {  # prefix differs: sfmm_/sfmap_ on the GPU, sfo_ in the oracle
     "threshold_batch": [P, i64, P, f64, P],
     "cost_batch": [P, i64, i32, P, P, P, P, P, P, P, P, P, u64, P, P],
 }
+# memory-manager tracker: sfmm_* on the GPU, sfo_* in the oracle (same argument lists)
+MM_FNS = {
+    "tracker_create": [P, C.POINTER(P)],
+    "tracker_destroy": [P],
+    "set_workflow_chain": [P, i32, i32, P],
+    "set_workflow_ranks": [P, i64, P],
+    "on_signal_batch": [P, i64, P, P],
+    "pressure_tick": [P, P, P],
+    "tracker_entries": [P, P, P, P, P, P],
+}
+MM_GPU_ONLY = {
+    "tracker_set_stream": [P, P],
+    "tracker_sync": [P],
+    "tracker_reset": [P],
+    "on_signal_batch_dev": [P, i64, P, P],
+}
 _RESTYPES = {
     "block_digest": u64,
     "chain_finalize": u64,
@@ -138,6 +154,11 @@ class Api:
         table.update(GPU_ONLY if kind == "gpu" else ORACLE_ONLY)
         for name, argt in table.items():
             self._bind(pre + name, name, argt)
+        for name, argt in MM_FNS.items():
+            self._bind(("sfmm_" if kind == "gpu" else "sfo_") + name, "mm_" + name, argt)
+        if kind == "gpu":
+            for name, argt in MM_GPU_ONLY.items():
+                self._bind("sfmm_" + name, "mm_" + name, argt)
         for name, argt in GLOBAL_FNS.items():
             if kind == "gpu":
                 sym = ("sfmm_" if name == "pressure_argmin" else "sfmap_") + name
@@ -359,3 +380,102 @@ class Peer:
         if self.h:
             self.api.peer_close(self.h)
             self.h = None
+
+
+# ---------------------------------------------------------------- memory-manager tracker ----
+MM_START, MM_COMPLETE, MM_WF_COMPLETE = 0, 1, 2
+MM_OVERRIDE = {"none": 0, "preserve": 1, "flush": 2}
+MM_POLICY = {"preserve_small_increment": 1, "flush_at_boundary": 2}
+MM_ACT = ["preserve", "flush", "noop"]
+MM_REASON = ["override", "preserve_small_increment", "flush_at_boundary", "flush_under_pressure",
+             "chain_exhausted"]
+
+
+class MmConfig(C.Structure):  # sfmm_config / sfo_mm_config
+    _fields_ = [
+        ("device", C.c_int32),
+        ("max_workflows", C.c_int32),
+        ("n_backends", C.c_int32),
+        ("chain_len", C.c_int32),
+        ("chain", C.c_uint8 * 8),
+        ("tau", C.c_int64),
+        ("tau_pressure", C.c_double),
+    ]
+
+
+class MmSignals(C.Structure):
+    _fields_ = [(f, C.c_void_p) for f in
+                ("kind", "wf", "stage", "backend", "model", "tokens", "ts", "override_")]
+
+
+class MmRecords(C.Structure):
+    _fields_ = [(f, C.c_void_p) for f in ("count", "status", "kind", "backend", "reason")]
+
+
+class Tracker:
+    """GPU-resident (or oracle) MemoryManager tracker over dense ids (host-pointer entry points)."""
+
+    def __init__(self, api: Api, max_workflows: int, n_backends: int, chain=("preserve_small_increment",
+                 "flush_at_boundary"), tau=512, tau_pressure=0.85, device=0):
+        cfg = MmConfig()
+        cfg.device, cfg.max_workflows, cfg.n_backends = device, max_workflows, n_backends
+        cfg.chain_len = len(chain)
+        for i, c in enumerate(chain):
+            cfg.chain[i] = MM_POLICY[c]
+        cfg.tau, cfg.tau_pressure = tau, tau_pressure
+        self.api, self.W, self.NB = api, max_workflows, n_backends
+        self.h = C.c_void_p()
+        api.check("tracker_create", api.mm_tracker_create(C.byref(cfg), C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            self.api.mm_tracker_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_chain(self, wf, names):
+        codes = np.array([MM_POLICY[n] for n in names] or [0], dtype=np.uint8)
+        self.api.check("set_workflow_chain", self.api.mm_set_workflow_chain(
+            self.h, int(wf), len(names), _ptr(codes)))
+
+    def set_ranks(self, rank):
+        rank = np.ascontiguousarray(rank, dtype=np.uint32)
+        self.api.check("set_workflow_ranks", self.api.mm_set_workflow_ranks(self.h, len(rank), _ptr(rank)))
+
+    def on_signals(self, kind, wf, stage, backend, model, tokens, ts, override):
+        """Arrays of n signals -> (count[n], status[n], kind[n,NB], backend[n,NB], reason[n,NB])."""
+        n = len(kind)
+        arrs = [np.ascontiguousarray(kind, np.uint8), np.ascontiguousarray(wf, np.int32),
+                np.ascontiguousarray(stage, np.int32), np.ascontiguousarray(backend, np.int32),
+                np.ascontiguousarray(model, np.int32), np.ascontiguousarray(tokens, np.int64),
+                np.ascontiguousarray(ts, np.float64), np.ascontiguousarray(override, np.uint8)]
+        sig = MmSignals(*[a.ctypes.data for a in arrs])
+        cnt = np.zeros(n, np.int32)
+        st = np.zeros(n, np.uint8)
+        k = np.zeros(max(n * self.NB, 1), np.uint8)
+        b = np.zeros(max(n * self.NB, 1), np.int32)
+        r = np.zeros(max(n * self.NB, 1), np.uint8)
+        rec = MmRecords(cnt.ctypes.data, st.ctypes.data, k.ctypes.data, b.ctypes.data, r.ctypes.data)
+        self.api.check("on_signal_batch", self.api.mm_on_signal_batch(self.h, n, C.byref(sig), C.byref(rec)))
+        nb = self.NB
+        return cnt, st, k[: n * nb].reshape(n, nb), b[: n * nb].reshape(n, nb), r[: n * nb].reshape(n, nb)
+
+    def pressure_tick(self, util):
+        util = np.ascontiguousarray(util, np.float64)
+        out = np.zeros(self.NB, np.int32)
+        self.api.check("pressure_tick", self.api.mm_pressure_tick(self.h, _ptr(util), _ptr(out)))
+        return out
+
+    def entries(self):
+        E = self.W * self.NB
+        pres, keep = np.zeros(E, np.uint8), np.zeros(E, np.uint8)
+        tok, ts, inf = np.zeros(E, np.int64), np.zeros(E, np.float64), np.zeros(E, np.int32)
+        self.api.check("tracker_entries", self.api.mm_tracker_entries(
+            self.h, _ptr(pres), _ptr(keep), _ptr(tok), _ptr(ts), _ptr(inf)))
+        shp = (self.W, self.NB)
+        return (pres.reshape(shp), keep.reshape(shp), tok.reshape(shp), ts.reshape(shp), inf.reshape(shp))

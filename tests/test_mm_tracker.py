@@ -1,0 +1,82 @@
+"""Batched MemoryManager (§8f-1): the tracker restatement against the reference.
+
+CPU: the oracle tracker (oracle/sfkv_oracle.c, sfo_tracker_*) reproduces (1) every golden
+stream's action log — trigger, ts, action, workflow, backend, reason, in order, pressure ticks
+included — recorded from the reference harness, and (2) the reference's own MemoryManager
+(oracle/_ref/libsfref.so) on seeded random streams with overrides, per-workflow chains,
+concurrent stages, pressure ticks and out-of-order signals, one signal at a time.
+GPU (`-m gpu`): the sm_100a tracker (sfmm_*) equals the oracle on the same streams in large
+batches (parallel across workflows) and reproduces the golden logs."""
+import os
+
+import pytest
+
+import replay
+from mm_stream import Interner, RefManager, golden_events, random_stream, run_stream
+from paper_2603_13605_b200.abi import Tracker
+
+REF_LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                       "libsfref.so")
+
+
+def _golden(api, name, batched, device=0):
+    lines = replay.load_stream(name)
+    meta, events, acts, backends, wfs = golden_events(lines)
+    intern = Interner(backends, wfs)
+    tr = Tracker(api, max_workflows=len(set(wfs)) + 1, n_backends=len(backends), chain=meta["chain"],
+                 tau=meta["tau"], tau_pressure=meta["tau_pressure"], device=device)
+    log, statuses = run_stream(tr, intern, events, batch_between_ticks=batched)
+    tr.close()
+    want = [{k: a[k] for k in ("trigger", "ts", "action", "workflow", "backend", "reason")} for a in acts]
+    return log, want, statuses
+
+
+@pytest.mark.parametrize("name", replay.stream_names())
+@pytest.mark.parametrize("batched", [False, True])
+def test_oracle_tracker_reproduces_golden_action_log(oracle_api, name, batched):
+    log, want, statuses = _golden(oracle_api, name, batched)
+    assert all(s == 0 for s in statuses)
+    assert log == want
+
+
+@pytest.mark.skipif(not os.path.exists(REF_LIB), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
+def test_oracle_tracker_matches_reference_memory_manager(oracle_api, seed):
+    events, backends, wfs = random_stream(seed)
+    chain = ["preserve_small_increment", "flush_at_boundary"] if seed % 2 else ["flush_at_boundary"]
+    ref = RefManager(512, 0.85, chain)
+    want_log, want_st = ref.run(events, backends)
+    ref.close()
+    intern = Interner(backends, wfs)
+    tr = Tracker(oracle_api, max_workflows=len(wfs), n_backends=len(backends), chain=chain)
+    log, st = run_stream(tr, intern, events, batch_between_ticks=False)
+    assert st == want_st
+    assert any(s != 0 for s in st), "stream should exercise out-of-order signals"
+    assert log == want_log
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", replay.stream_names())
+def test_gpu_tracker_reproduces_golden_action_log(gpu_api, name):
+    log, want, statuses = _golden(gpu_api, name, batched=True)
+    assert all(s == 0 for s in statuses)
+    assert log == want
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed,n_wf", [(11, 60), (12, 500), (13, 3000)])
+def test_gpu_tracker_matches_oracle_in_large_batches(gpu_api, oracle_api, seed, n_wf):
+    events, backends, wfs = random_stream(seed, n_wf=n_wf, backends=("A", "B", "C", "D", "E"),
+                                          p_tick=0.002)
+    out = []
+    for api in (oracle_api, gpu_api):
+        intern = Interner(backends, wfs)
+        tr = Tracker(api, max_workflows=len(wfs), n_backends=len(backends))
+        log, st = run_stream(tr, intern, events, batch_between_ticks=True)
+        out.append((log, st, tr.entries()))
+        tr.close()
+    (lo, so, eo), (lg, sg, eg) = out
+    assert sg == so
+    assert lg == lo
+    for a, b in zip(eo, eg):  # tracker state after the stream
+        assert (a == b).all()
