@@ -366,6 +366,7 @@ def run_ours(args, rank, world, local_rank):
         c5 = None if args.no_c5 else lookup_leg(args, api, dev, stream, hbm_peak, rank)
         c4 = None if args.no_c4 else long_context_leg(args, api, dev, stream, hbm_peak, rank)
         c3 = handoff_leg(args, api, dev, stream, rank, world) if (dist and not args.no_c3) else None
+        mm = None if args.no_mm else mm_leg(args, api, dev, stream)
     clocks = clk.summary()
 
     # ---- roofline of the match kernel: algorithmic bytes of one launch --------------------
@@ -404,6 +405,8 @@ def run_ours(args, rank, world, local_rank):
         line["c4_long_context"] = c4
     if c3:
         line["c3_handoff"] = c3
+    if mm:
+        line["mm_signals"] = mm
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
     pool.close()
@@ -803,6 +806,110 @@ def handoff_leg(args, api, dev, stream, rank, world):
 
 
 
+def signal_stream(seed, n_wf, k=5, n_backends=2, p_alt=0.3):
+    """C2-shaped lifecycle-signal stream (vectorised): n_wf math_chain workflows of k stages, base
+    context log-uniform [512, 8192] tokens, +256 per stage; 30 % alternate between two backends
+    (their boundary flushes exercise flush_at_boundary). Per workflow: S0 C0 S1 C1 ... WFC;
+    workflows interleaved round-robin (ts = position)."""
+    rng = np.random.default_rng(seed)
+    per = 2 * k + 1
+    base = np.exp(rng.uniform(np.log(512), np.log(8192), n_wf)).astype(np.int64)
+    alt = rng.random(n_wf) < p_alt
+    b0 = rng.integers(0, n_backends, n_wf)
+    pos = np.arange(per)
+    stage = np.minimum(pos // 2, k - 1)
+    kind = np.where(pos == per - 1, 2, pos % 2).astype(np.uint8)
+    W = np.repeat(np.arange(n_wf, dtype=np.int32), per).reshape(n_wf, per)
+    ST = np.broadcast_to(stage, (n_wf, per))
+    K = np.broadcast_to(kind, (n_wf, per))
+    B = (b0[:, None] + np.where(alt[:, None], ST % 2, 0)) % n_backends
+    T = base[:, None] + 256 * ST
+    order = np.argsort(np.broadcast_to(pos, (n_wf, per)).ravel(), kind="stable")  # round-robin
+    f = lambda a: np.ascontiguousarray(np.asarray(a).ravel()[order])
+    n = n_wf * per
+    return {"kind": f(K), "wf": f(W), "stage": f(ST).astype(np.int32), "backend": f(B).astype(np.int32),
+            "model": np.zeros(n, np.int32), "tokens": f(T).astype(np.int64),
+            "ts": np.arange(n, dtype=np.float64), "override": np.zeros(n, np.uint8), "n": n,
+            "n_wf": n_wf, "n_backends": n_backends}
+
+
+def mm_leg(args, api, dev, stream):
+    """§8f-1: batched MemoryManager::on_signal on the GPU tracker; C2 scale (10k workflows,
+    110k signals per batch)."""
+    import torch
+
+    from paper_2603_13605_b200.abi import MmRecords, MmSignals, Tracker
+    sg = signal_stream(args.seed + 5, args.workflows)
+    n, NB = sg["n"], sg["n_backends"]
+    tr = Tracker(api, max_workflows=sg["n_wf"], n_backends=NB)
+    api.check("tracker_set_stream", api.mm_tracker_set_stream(tr.h, C.c_void_p(stream.cuda_stream)))
+    d = {k: torch.from_numpy(sg[k]).to(dev) for k in ("kind", "wf", "stage", "backend", "model", "tokens", "ts", "override")}
+    sig = MmSignals(*[d[k].data_ptr() for k in ("kind", "wf", "stage", "backend", "model", "tokens", "ts", "override")])
+    cnt = torch.zeros(n, dtype=torch.int32, device=dev)
+    st = torch.zeros(n, dtype=torch.uint8, device=dev)
+    rk = torch.zeros(n * NB, dtype=torch.uint8, device=dev)
+    rb = torch.zeros(n * NB, dtype=torch.int32, device=dev)
+    rr = torch.zeros(n * NB, dtype=torch.uint8, device=dev)
+    rec = MmRecords(cnt.data_ptr(), st.data_ptr(), rk.data_ptr(), rb.data_ptr(), rr.data_ptr())
+    times = []
+    for it in range(args.warmup + args.steps):
+        api.check("tracker_reset", api.mm_tracker_reset(tr.h))  # untimed: a fresh manager
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        api.check("on_signal_batch_dev", api.mm_on_signal_batch_dev(tr.h, n, C.byref(sig), C.byref(rec)))
+        b.record(stream)
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            times.append(a.elapsed_time(b))
+    assert int(st.sum()) == 0
+    c = cnt.cpu().numpy()
+    kinds = rk.view(n, NB).cpu().numpy()[:, 0]
+    preserves = int(((kinds == 0) & (c > 0)).sum())
+    flushes = int(np.where(np.arange(NB)[None, :] < c[:, None], rk.view(n, NB).cpu().numpy() == 1, False).sum())
+    tr.close()
+    ms = float(np.mean(times))
+    out = {"workload": f"{sg['n_wf']} math_chain workflows x 5 stages on {NB} backends (30 % alternating): "
+                       f"{n} lifecycle signals resolved per batch",
+           "signals_per_step": n, "ms": ms, "signals_per_s": n / (ms / 1e3),
+           "preserves": preserves, "flushes": flushes}
+    L = ref_lib()
+    if L is not None and not args.no_cpu_baseline:
+        out["cpu_reference"] = mm_reference(L, args)
+    return out
+
+
+def mm_reference(L, args, n_wf=1000):
+    """The reference's MemoryManager::on_signal on a bounded sample (1 thread, C++ loop)."""
+    sg = signal_stream(args.seed + 5, n_wf)
+    n = sg["n"]
+    enc = lambda xs: (C.c_char_p * n)(*[x.encode() for x in xs])
+    wf = enc([f"wf-{w:06d}" for w in sg["wf"]])
+    stage = enc([f"s{s}" if k != 2 else "" for s, k in zip(sg["stage"], sg["kind"])])
+    backend = enc(["" if k == 2 else "b" + str(b) for b, k in zip(sg["backend"], sg["kind"])])
+    model = enc(["" if k == 2 else "m" for k in sg["kind"]])
+    kind = (C.c_int * n)(*sg["kind"].tolist())
+    toks = (C.c_longlong * n)(*sg["tokens"].tolist())
+    ts = (C.c_double * n)(*sg["ts"].tolist())
+    L.sfref_mm_create.restype = C.c_void_p
+    L.sfref_mm_create.argtypes = [C.c_longlong, C.c_double, C.c_int, C.POINTER(C.c_char_p)]
+    L.sfref_mm_destroy.argtypes = [C.c_void_p]
+    L.sfref_mm_on_signal_batch.restype = C.c_longlong
+    L.sfref_mm_on_signal_batch.argtypes = [C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    chain = (C.c_char_p * 2)(b"preserve_small_increment", b"flush_at_boundary")
+    times = []
+    for _ in range(3):
+        h = L.sfref_mm_create(512, 0.85, 2, chain)
+        t0 = time.perf_counter()
+        bad = L.sfref_mm_on_signal_batch(h, n, kind, wf, stage, backend, model, toks, ts, None)
+        times.append(time.perf_counter() - t0)
+        L.sfref_mm_destroy(h)
+        assert bad == 0
+    return {"value": n / float(np.median(times)), "unit": "signals/s", "cores": 1, "kind": "reference",
+            "sample": f"{n_wf} workflows of the same stream ({n} signals), MemoryManager::on_signal, 1 thread"}
+
+
+
 def cpu_baseline(args):
     L = ref_lib()
     n_sample = args.cpu_sample
@@ -833,6 +940,7 @@ def main():
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--c5-prefixes", type=int, default=100_000)
     ap.add_argument("--no-c3", action="store_true")
+    ap.add_argument("--no-mm", action="store_true")
     ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--dist-backend", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--c3-workflows", type=int, default=32)

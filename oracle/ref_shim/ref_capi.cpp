@@ -218,6 +218,19 @@ int sfref_mm_on_signal(void* h, int kind, const char* wf, const char* stage, con
   return 0;
 }
 
+// n signals through MemoryManager::on_signal in order (the CPU baseline: the loop stays in C++).
+// Returns the number of signals the reference rejected.
+long long sfref_mm_on_signal_batch(void* h, long long n, const int* kind, const char* const* wf,
+                                   const char* const* stage, const char* const* backend,
+                                   const char* const* model, const long long* tokens,
+                                   const double* ts, const int* override_) {
+  long long bad = 0;
+  for (long long i = 0; i < n; ++i)
+    bad += sfref_mm_on_signal(h, kind[i], wf[i], stage[i], backend[i], model[i], tokens[i], ts[i],
+                              override_ ? override_[i] : 0) != 0;
+  return bad;
+}
+
 int sfref_mm_pressure_tick(void* h, int n, const char* const* refs, const double* util, double now) {
   std::map<std::string, double> u;
   for (int i = 0; i < n; ++i) u[refs[i]] = util[i];
