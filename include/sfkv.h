@@ -46,6 +46,7 @@ extern "C" {
 #define SFKV_EPOOL -5     /* physical pool exhausted (logical capacity admitted the pin, but the
                              physical block pool or a pin's block table is too small) */
 #define SFKV_ESTALE -6    /* payload commit whose staging assumed a different cached prefix */
+#define SFKV_ECOLLIDE -7  /* two different token strings share a 64-bit hash (interner) */
 
 #define SFKV_FLUSH_ALL (-1)        /* FlushScope::everything() (backend.hpp:65-70) */
 #define SFKV_BLOCK_TOKENS 16       /* tokens per KV block */
@@ -202,6 +203,33 @@ int sfkv_handoff_recv_batch(sfkv_pool* dst, const sfkv_peer* src, int64_t n, con
 int sfkv_handoff_recv_batch_dev(sfkv_pool* dst, const sfkv_peer* src, int64_t n, const int32_t* wf,
                                 const int64_t* tok_off, const uint32_t* tok, int64_t n_tokens,
                                 const int32_t* src_blocks, int32_t* out_status);
+
+/* ---- tokenizer + interner: replaces tokenize_whitespace /
+ *      context_token_sequence (backend.cpp:60-91) on the dispatch path ------------------------
+ * Tokens are maximal runs of non-space bytes (std::isspace, C locale); each message is split
+ * separately and the request's tokens are the concatenation (roles ignored). Every token string
+ * is interned into a u32 id: equal strings get equal ids for the interner's lifetime; strings new
+ * to the interner are numbered in order of first occurrence in the batch (deterministic). Text is
+ * a CSR of messages (msg_off over text bytes) and requests are ranges of messages (req_msg_off).
+ * Output: the token CSR the match / commit entry points take (tok_off[n+1], tok). tok must hold
+ * (n_bytes + 1) / 2 ids. A batch that would overflow the interner or that meets a 64-bit hash
+ * collision between different strings fails without changing the interner (SFKV_EPOOL /
+ * SFKV_ECOLLIDE). */
+typedef struct sfkv_interner sfkv_interner;
+int sfkv_interner_create(int32_t device, int32_t table_log2, int64_t arena_bytes, sfkv_interner** out);
+int sfkv_interner_destroy(sfkv_interner* it);
+int sfkv_interner_set_stream(sfkv_interner* it, void* cuda_stream);
+int sfkv_interner_size(sfkv_interner* it, int64_t* n_ids);
+int sfkv_interner_token(sfkv_interner* it, uint32_t id, char* out, int32_t cap, int32_t* len);
+int sfkv_tokenize_batch(sfkv_interner* it, int64_t n, const int64_t* req_msg_off, const int64_t* msg_off,
+                        const uint8_t* text, int64_t* tok_off, uint32_t* tok, int64_t tok_cap,
+                        int64_t* n_tokens);
+/* Device pointers, asynchronous on the interner's stream; *n_tokens is a device scalar.
+ * sfkv_interner_check reports (and clears) a failed device batch. */
+int sfkv_tokenize_batch_dev(sfkv_interner* it, int64_t n, const int64_t* req_msg_off, int64_t n_msg,
+                            const int64_t* msg_off, const uint8_t* text, int64_t n_bytes, int64_t* tok_off,
+                            uint32_t* tok, int64_t* n_tokens);
+int sfkv_interner_check(sfkv_interner* it);
 
 /* ---- memory manager: replaces pressure_actions (memory.cpp:150-169) -------------------------
  * Entries are the tracker's (workflow, backend) records as SoA: backend index, last_update_ts,

@@ -15,6 +15,7 @@
 // Token ids are rendered to whitespace tokens "t<id>", the same text the reference tokenizes.
 #include <cstring>
 
+#include "stageflow/backend.hpp"
 #include "stageflow/memory.hpp"
 #include "stageflow/mapper.hpp"
 #include "stageflow/orchestrator.hpp"
@@ -176,6 +177,30 @@ int sfref_reroute(int n, const unsigned long long* depth, unsigned long long lim
       [&](const std::string& s) { return static_cast<std::size_t>(depth[std::stoi(s)]); },
       static_cast<std::size_t>(limit));
   return std::stoi(pick);
+}
+
+// ---- tokenizer --------------------------------------------------------------------------
+// context_token_sequence (backend.cpp:83-91) over n messages (content only). Writes the tokens
+// concatenated into out (cap bytes) with their lengths into out_len (cap_tokens); returns the
+// token count (or -1 when a buffer is too small).
+long long sfref_context_tokens(int n, const char* const* msg, const long long* msg_len, char* out,
+                               long long cap, long long* out_len, long long cap_tokens) {
+  Context ctx;
+  for (int i = 0; i < n; ++i) {
+    Message m;
+    m.content.assign(msg[i], static_cast<std::size_t>(msg_len[i]));
+    ctx.push_back(std::move(m));
+  }
+  auto toks = context_token_sequence(ctx);
+  if (static_cast<long long>(toks.size()) > cap_tokens) return -1;
+  long long o = 0;
+  for (std::size_t i = 0; i < toks.size(); ++i) {
+    if (o + static_cast<long long>(toks[i].size()) > cap) return -1;
+    std::memcpy(out + o, toks[i].data(), toks[i].size());
+    o += static_cast<long long>(toks[i].size());
+    out_len[i] = static_cast<long long>(toks[i].size());
+  }
+  return static_cast<long long>(toks.size());
 }
 
 // ---- MemoryManager ------------------------------------------------------------------------

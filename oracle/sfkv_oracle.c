@@ -991,3 +991,122 @@ int sfo_tracker_entries(sfo_tracker* t, uint8_t* present, uint8_t* preserved, in
   if (in_flight) memcpy(in_flight, t->inflight, E * 4);
   return 0;
 }
+
+
+/* ================================================================ tokenizer + interner ======
+ * tokenize_whitespace (backend.cpp:60-70): skip std::isspace bytes (C locale), take the maximal
+ * run of non-space bytes as a token; context_token_sequence (backend.cpp:83-91) concatenates the
+ * tokens of each message. Interning: a token string seen for the first time gets the next id,
+ * in token order. (A plain open-addressing map over the strings themselves: no hashing shortcut
+ * can make two different strings equal here.) */
+struct sfo_interner {
+  int64_t cap;      /* slots (power of two) */
+  int64_t* slot;    /* id + 1, 0 = empty */
+  uint8_t* arena;
+  int64_t arena_cap, arena_used;
+  int64_t* off;
+  int32_t* len;
+  int64_t n, max_ids;
+};
+
+static int sp(uint8_t c) { return c == ' ' || (c >= '\t' && c <= '\r'); }
+
+static uint64_t str_hash(const uint8_t* p, int64_t n) { /* FNV-1a: only the map layout uses it */
+  uint64_t h = 1469598103934665603ull;
+  for (int64_t i = 0; i < n; ++i) h = (h ^ p[i]) * 1099511628211ull;
+  return h;
+}
+
+int sfo_interner_create(int32_t device, int32_t table_log2, int64_t arena_bytes, sfo_interner** out) {
+  (void)device;
+  if (!out || table_log2 < 4 || table_log2 > 34 || arena_bytes <= 0) return -1;
+  sfo_interner* it = (sfo_interner*)calloc(1, sizeof(*it));
+  it->cap = (int64_t)1 << table_log2;
+  it->max_ids = it->cap / 2;
+  it->slot = (int64_t*)calloc((size_t)it->cap, sizeof(int64_t));
+  it->arena = (uint8_t*)malloc((size_t)arena_bytes);
+  it->arena_cap = arena_bytes;
+  it->off = (int64_t*)malloc((size_t)it->max_ids * sizeof(int64_t));
+  it->len = (int32_t*)malloc((size_t)it->max_ids * sizeof(int32_t));
+  *out = it;
+  return 0;
+}
+
+int sfo_interner_destroy(sfo_interner* it) {
+  if (!it) return -1;
+  free(it->slot); free(it->arena); free(it->off); free(it->len); free(it);
+  return 0;
+}
+
+int sfo_interner_size(sfo_interner* it, int64_t* n_ids) {
+  if (!it || !n_ids) return -1;
+  *n_ids = it->n;
+  return 0;
+}
+
+int sfo_interner_token(sfo_interner* it, uint32_t id, char* out, int32_t cap, int32_t* len) {
+  if (!it || !len || (int64_t)id >= it->n) return -1;
+  *len = it->len[id];
+  if (cap > 0) memcpy(out, it->arena + it->off[id], (size_t)(it->len[id] < cap ? it->len[id] : cap));
+  return 0;
+}
+
+/* id of p[0..n), inserting it (next id) when new; -1 when the interner is full */
+static int64_t intern(sfo_interner* it, const uint8_t* p, int64_t n) {
+  uint64_t m = (uint64_t)it->cap - 1, s = str_hash(p, n) & m;
+  for (;;) {
+    int64_t v = it->slot[s];
+    if (!v) break;
+    int64_t id = v - 1;
+    if (it->len[id] == n && !memcmp(it->arena + it->off[id], p, (size_t)n)) return id;
+    s = (s + 1) & m;
+  }
+  if (it->n >= it->max_ids || it->arena_used + n > it->arena_cap) return -1;
+  int64_t id = it->n++;
+  memcpy(it->arena + it->arena_used, p, (size_t)n);
+  it->off[id] = it->arena_used;
+  it->len[id] = (int32_t)n;
+  it->arena_used += n;
+  it->slot[s] = id + 1;
+  return id;
+}
+
+int sfo_tokenize_batch(sfo_interner* it, int64_t n, const int64_t* req_msg_off, const int64_t* msg_off,
+                       const uint8_t* text, int64_t* tok_off, uint32_t* tok, int64_t tok_cap,
+                       int64_t* n_tokens) {
+  if (!it || n < 0 || !req_msg_off || !tok_off || !n_tokens) return -1;
+  /* all-or-nothing like the GPU: work on a copy of the interner state */
+  int64_t n0 = it->n, used0 = it->arena_used;
+  int64_t* slot0 = (int64_t*)malloc((size_t)it->cap * sizeof(int64_t));
+  memcpy(slot0, it->slot, (size_t)it->cap * sizeof(int64_t));
+  int64_t k = 0;
+  int rc = 0;
+  for (int64_t r = 0; r < n && !rc; ++r) {
+    tok_off[r] = k;
+    for (int64_t m = req_msg_off[r]; m < req_msg_off[r + 1] && !rc; ++m) {
+      int64_t i = msg_off[m], e = msg_off[m + 1];
+      while (i < e) {
+        while (i < e && sp(text[i])) ++i;
+        int64_t s0 = i;
+        while (i < e && !sp(text[i])) ++i;
+        if (i > s0) {
+          int64_t id = intern(it, text + s0, i - s0);
+          if (id < 0 || k >= tok_cap) {
+            rc = id < 0 ? -5 : -1;
+            break;
+          }
+          tok[k++] = (uint32_t)id;
+        }
+      }
+    }
+  }
+  tok_off[n] = k;
+  *n_tokens = k;
+  if (rc) { /* roll back */
+    memcpy(it->slot, slot0, (size_t)it->cap * sizeof(int64_t));
+    it->n = n0;
+    it->arena_used = used0;
+  }
+  free(slot0);
+  return rc;
+}

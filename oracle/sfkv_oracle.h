@@ -118,4 +118,15 @@ int sfo_pressure_tick(sfo_tracker* t, const double* util, int32_t* out_victim);
 int sfo_tracker_entries(sfo_tracker* t, uint8_t* present, uint8_t* preserved, int64_t* tokens,
                         double* ts, int32_t* in_flight);
 
+
+/* ---- tokenizer + interner (restates tokenize_whitespace / context_token_sequence) -------- */
+typedef struct sfo_interner sfo_interner;
+int sfo_interner_create(int32_t device, int32_t table_log2, int64_t arena_bytes, sfo_interner** out);
+int sfo_interner_destroy(sfo_interner* it);
+int sfo_interner_size(sfo_interner* it, int64_t* n_ids);
+int sfo_interner_token(sfo_interner* it, uint32_t id, char* out, int32_t cap, int32_t* len);
+int sfo_tokenize_batch(sfo_interner* it, int64_t n, const int64_t* req_msg_off, const int64_t* msg_off,
+                       const uint8_t* text, int64_t* tok_off, uint32_t* tok, int64_t tok_cap,
+                       int64_t* n_tokens);
+
 #endif

@@ -85,6 +85,11 @@ SIGNATURES = {
     "pin_tokens": [P, i32, P, i64, C.POINTER(i64)],
     "handoff": [P, i32, P, i32, C.POINTER(i32)],
     "block_digest": [u64, u32, P],
+    "interner_create": [i32, i32, i64, C.POINTER(P)],
+    "interner_destroy": [P],
+    "interner_size": [P, C.POINTER(i64)],
+    "interner_token": [P, u32, P, i32, C.POINTER(i32)],
+    "tokenize_batch": [P, i64, P, P, P, P, P, i64, C.POINTER(i64)],
     "chain_finalize": [u64],
 }
 # entry points whose name differs between the GPU ABI and the oracle
@@ -97,6 +102,9 @@ GPU_ONLY = {
     "lookup_batch_dev": [P, i64, P, P, i64, P, P],
     "commit_batch_dev": [P, i64, P, P, P, i64, P, P, P, P],
     "gather_dev": [P, i64, P, P, P],
+    "interner_set_stream": [P, P],
+    "interner_check": [P],
+    "tokenize_batch_dev": [P, i64, P, i64, P, P, i64, P, P, P],
     "pool_export": [P, C.POINTER(IpcHandle)],
     "peer_open": [C.POINTER(IpcHandle), i32, C.POINTER(P)],
     "peer_close": [P],
@@ -479,3 +487,63 @@ class Tracker:
             self.h, _ptr(pres), _ptr(keep), _ptr(tok), _ptr(ts), _ptr(inf)))
         shp = (self.W, self.NB)
         return (pres.reshape(shp), keep.reshape(shp), tok.reshape(shp), ts.reshape(shp), inf.reshape(shp))
+
+
+# ---------------------------------------------------------------- tokenizer + interner ------
+def text_batch(requests):
+    """requests: list of lists of message byte strings -> (req_msg_off, msg_off, text u8)."""
+    req = np.zeros(len(requests) + 1, np.int64)
+    msgs = []
+    for i, r in enumerate(requests):
+        req[i + 1] = req[i] + len(r)
+        msgs.extend(r)
+    moff = np.zeros(len(msgs) + 1, np.int64)
+    for i, m in enumerate(msgs):
+        moff[i + 1] = moff[i] + len(m)
+    text = np.frombuffer(b"".join(msgs) + b"\0" * 16, dtype=np.uint8).copy()
+    return req, moff, text
+
+
+class Interner:
+    """Token-string interner + whitespace tokenizer (host-pointer entry points)."""
+
+    def __init__(self, api: Api, table_log2=20, arena_bytes=64 << 20, device=0):
+        self.api = api
+        self.h = C.c_void_p()
+        api.check("interner_create", api.interner_create(device, table_log2, arena_bytes, C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            self.api.interner_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def tokenize(self, requests):
+        """-> (tok_off int64[n+1], tok uint32[T]) for a list of requests (lists of messages)."""
+        req, moff, text = text_batch(requests)
+        nbytes = int(moff[-1])
+        cap = max((nbytes + 1) // 2, 1)
+        tok_off = np.zeros(len(requests) + 1, np.int64)
+        tok = np.zeros(cap, np.uint32)
+        nt = C.c_int64()
+        self.api.check("tokenize_batch", self.api.tokenize_batch(
+            self.h, len(requests), _ptr(req), _ptr(moff), _ptr(text), _ptr(tok_off), _ptr(tok), cap,
+            C.byref(nt)))
+        return tok_off, tok[: nt.value]
+
+    def size(self):
+        n = C.c_int64()
+        self.api.check("interner_size", self.api.interner_size(self.h, C.byref(n)))
+        return n.value
+
+    def token(self, i):
+        ln = C.c_int32()
+        self.api.check("interner_token", self.api.interner_token(self.h, int(i), None, 0, C.byref(ln)))
+        buf = C.create_string_buffer(max(ln.value, 1))
+        self.api.check("interner_token", self.api.interner_token(self.h, int(i), buf, ln.value, C.byref(ln)))
+        return buf.raw[: ln.value]

@@ -1,0 +1,555 @@
+// §8f-2: whitespace tokenizer + token interner on the GPU, feeding the match / commit kernels.
+//
+// Replaces tokenize_whitespace / context_token_sequence (backend.cpp:60-91): tokens are maximal
+// runs of non-space bytes (std::isspace in the C locale: ' ', '\t', '\n', '\v', '\f', '\r'),
+// messages are tokenized separately and concatenated (a token never spans two messages), roles
+// are ignored. The reference keeps tokens as std::string; the pools key on u32 ids, so every token
+// string is interned: the same bytes always get the same id for the interner's lifetime, and new
+// strings are numbered in order of first occurrence (batch position), which makes ids
+// deterministic and equal to a sequential restatement's.
+//
+// Launches for a batch (text is a CSR of messages, requests are ranges of messages):
+//   msg_mark_kernel    flags the first byte of every message (a forced token boundary)
+//   chunk_count_kernel token starts per 4 KiB chunk (start: non-space byte after a space or at a
+//                      message start)
+//   exclusive scan     over chunks
+//   chunk_emit_kernel  CTA-wide scan inside each chunk: token start positions, in order
+//   tok_probe_kernel   per token: length (to the next space / message start), 64-bit hash, probe
+//                      the interner table: a verified hit is the id; a miss claims a slot (CAS)
+//                      and competes for ownership with atomicMin(position) — lowest position wins
+//   tok_resolve_kernel claimers that lost compare their bytes with the owner's (a 64-bit hash
+//                      collision between different strings fails the batch loudly)
+//   exclusive scan     over owner flags -> new ids in first-occurrence order
+//   tok_publish_kernel owners copy their bytes into the arena and publish the id in the slot
+//   tok_final_kernel   every token reads its id; per-request token offsets by binary search
+// Byte-stream work, HBM/latency-bound; no tensor cores.
+#include "pool.cuh"
+
+struct sfkv_interner {
+  int32_t device = 0;
+  int64_t slots_n = 0;   // power of two
+  int64_t arena_cap = 0;
+  int64_t max_ids = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  struct TSlot* slots = nullptr;
+  int64_t* owner = nullptr;       // per slot: lowest claiming token of the current batch
+  uint8_t* arena = nullptr;
+  int64_t* id_off = nullptr;      // id -> arena offset
+  int32_t* id_len = nullptr;
+  unsigned long long* ctr = nullptr;  // [0] ids, [1] arena cursor, [2] error flag
+  unsigned long long* ctr_host = nullptr;
+  sfkv::Scratch scratch;
+  sfkv::Scratch io;
+};
+
+struct TSlot {
+  unsigned long long key;  // 0 = empty
+  uint32_t id;             // TOK_PENDING while a batch claim is unresolved
+  uint32_t pad;
+};
+
+namespace sfkv {
+
+constexpr uint32_t TOK_PENDING = 0xffffffffu;
+constexpr int CHUNK = 4096;
+constexpr int CHUNK_THREADS = 256;
+constexpr int PER_THREAD = CHUNK / CHUNK_THREADS;  // 16 bytes per thread
+enum : int { TERR_COLLISION = 1, TERR_ARENA = 2, TERR_IDS = 4, TERR_TABLE = 8 };
+
+__device__ __forceinline__ bool is_space(uint8_t c) { return c == ' ' || (c >= '\t' && c <= '\r'); }
+
+__device__ __forceinline__ unsigned long long tok_hash(const uint8_t* p, int len) {
+  unsigned long long h = 0x9E3779B97F4A7C15ull ^ (unsigned long long)len;
+  int i = 0;
+  for (; i + 8 <= len; i += 8) {
+    unsigned long long w = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w |= (unsigned long long)p[i + k] << (8 * k);
+    h = mix64(h + w * 0xD6E8FEB86659FD93ull);
+  }
+  if (i < len) {
+    unsigned long long w = 0;
+    for (int k = 0; i + k < len; ++k) w |= (unsigned long long)p[i + k] << (8 * k);
+    h = mix64(h + w * 0xD6E8FEB86659FD93ull);
+  }
+  h = mix64(h);
+  return h ? h : 1;
+}
+
+struct TokArgs {
+  int64_t n_req;
+  const int64_t* req_msg_off;
+  const int64_t* msg_off;
+  int64_t n_msg;
+  const uint8_t* text;
+  int64_t n_bytes;
+  uint8_t* mstart;       // [n_bytes + 1]
+  int64_t* chunk_off;    // [nchunks + 1]
+  int64_t* tstart;       // [token bound]
+  int32_t* tlen;
+  int64_t* tslot;
+  uint8_t* tnew;
+  int64_t* new_rank;     // [token bound + 1]
+  int64_t* tok_off;      // out [n_req + 1]
+  uint32_t* tok;         // out
+  int64_t* n_tokens;     // out (device scalar)
+  // interner
+  TSlot* slots;
+  uint64_t mask;
+  int64_t* owner;
+  uint8_t* arena;
+  int64_t arena_cap;
+  int64_t* id_off;
+  int32_t* id_len;
+  int64_t max_ids;
+  unsigned long long* ctr;
+};
+
+__global__ void msg_mark_kernel(TokArgs a) {
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < a.n_msg; m += (int64_t)gridDim.x * blockDim.x)
+    if (a.msg_off[m] < a.n_bytes) a.mstart[a.msg_off[m]] = 1;
+}
+
+__device__ __forceinline__ bool tok_start(const TokArgs& a, int64_t i) {
+  const uint8_t c = a.text[i];
+  return !is_space(c) && (i == 0 || a.mstart[i] || is_space(a.text[i - 1]));
+}
+
+__global__ void __launch_bounds__(CHUNK_THREADS) chunk_count_kernel(TokArgs a, int64_t* counts) {
+  using BR = cub::BlockReduce<int, CHUNK_THREADS>;
+  __shared__ typename BR::TempStorage tmp;
+  const int64_t base = (int64_t)blockIdx.x * CHUNK;
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < PER_THREAD; ++k) {
+    const int64_t i = base + (int64_t)k * CHUNK_THREADS + threadIdx.x;
+    if (i < a.n_bytes && tok_start(a, i)) ++c;
+  }
+  c = BR(tmp).Sum(c);
+  if (threadIdx.x == 0) counts[blockIdx.x] = c;
+}
+
+struct ChunkCount {
+  const int64_t* counts;
+  __device__ int64_t operator()(int64_t c) const { return counts[c]; }
+};
+
+__global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
+  using BS = cub::BlockScan<int, CHUNK_THREADS>;
+  __shared__ typename BS::TempStorage tmp;
+  const int64_t base = (int64_t)blockIdx.x * CHUNK + (int64_t)threadIdx.x * PER_THREAD;  // blocked
+  bool f[PER_THREAD];
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < PER_THREAD; ++k) {
+    const int64_t i = base + k;
+    f[k] = i < a.n_bytes && tok_start(a, i);
+    c += f[k];
+  }
+  int excl;
+  BS(tmp).ExclusiveSum(c, excl);
+  int64_t o = a.chunk_off[blockIdx.x] + excl;
+#pragma unroll
+  for (int k = 0; k < PER_THREAD; ++k)
+    if (f[k]) a.tstart[o++] = base + k;
+}
+
+__device__ __forceinline__ bool bytes_equal(const uint8_t* x, const uint8_t* y, int len) {
+  for (int i = 0; i < len; ++i)
+    if (x[i] != y[i]) return false;
+  return true;
+}
+
+__global__ void tok_probe_kernel(TokArgs a) {
+  const int64_t nt = *a.n_tokens;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = a.tstart[t];
+    int64_t e = s + 1;
+    while (e < a.n_bytes && !is_space(a.text[e]) && !a.mstart[e]) ++e;
+    const int len = (int)(e - s);
+    a.tlen[t] = len;
+    const unsigned long long h = tok_hash(a.text + s, len);
+    uint64_t sl = h & a.mask;
+    int64_t found = -1;
+    for (uint64_t probes = 0; probes <= a.mask; ++probes) {
+      TSlot* p = a.slots + sl;
+      unsigned long long k = p->key;
+      if (k == 0) {
+        k = atomicCAS(&p->key, 0ull, h);
+        if (k == 0) k = h;  // claimed it (its id is TOK_PENDING until published)
+      }
+      if (k == h) {
+        found = (int64_t)sl;
+        break;
+      }
+      sl = (sl + 1) & a.mask;
+    }
+    if (found < 0) {
+      atomicOr(a.ctr + 2, (unsigned long long)TERR_TABLE);
+      a.tslot[t] = -1;
+      continue;
+    }
+    a.tslot[t] = found;
+    const uint32_t id = *(volatile uint32_t*)&a.slots[found].id;
+    if (id == TOK_PENDING) atomicMin(reinterpret_cast<unsigned long long*>(a.owner + found), (unsigned long long)t);
+  }
+}
+
+// Settle every token: verified hit (id published before this batch), owner of a new string, or
+// a duplicate of a new string (bytes compared with the owner's).
+__global__ void tok_resolve_kernel(TokArgs a) {
+  const int64_t nt = *a.n_tokens;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sl = a.tslot[t];
+    uint8_t isnew = 0;
+    if (sl >= 0) {
+      const uint32_t id = a.slots[sl].id;
+      const uint8_t* mine = a.text + a.tstart[t];
+      const int len = a.tlen[t];
+      if (id != TOK_PENDING) {  // existing string: verify against the arena copy
+        if (a.id_len[id] != len || !bytes_equal(mine, a.arena + a.id_off[id], len))
+          atomicOr(a.ctr + 2, (unsigned long long)TERR_COLLISION);
+      } else {
+        const int64_t o = a.owner[sl];
+        if (o == t) {
+          isnew = 1;
+          atomicAdd(a.ctr + 3, (unsigned long long)len);  // arena bytes this batch needs
+        } else if (a.tlen[o] != len || !bytes_equal(mine, a.text + a.tstart[o], len)) {
+          atomicOr(a.ctr + 2, (unsigned long long)TERR_COLLISION);
+        }
+      }
+    }
+    a.tnew[t] = isnew;
+  }
+}
+
+struct NewFlag {
+  const uint8_t* f;
+  __device__ int64_t operator()(int64_t t) const { return f[t]; }
+};
+
+// Capacity check before anything is published: a failing batch leaves the interner unchanged.
+__global__ void tok_check_kernel(TokArgs a) {
+  if (threadIdx.x || blockIdx.x || a.ctr[2]) return;
+  if ((int64_t)(a.ctr[0] + a.new_rank[*a.n_tokens]) > a.max_ids) a.ctr[2] |= TERR_IDS;
+  if ((int64_t)(a.ctr[1] + a.ctr[3]) > a.arena_cap) a.ctr[2] |= TERR_ARENA;
+}
+
+__global__ void tok_publish_kernel(TokArgs a) {
+  const int64_t nt = *a.n_tokens;
+  const unsigned long long base_id = a.ctr[0];
+  if (a.ctr[2]) return;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
+    if (!a.tnew[t]) continue;
+    const int64_t id = (int64_t)base_id + a.new_rank[t];
+    const int len = a.tlen[t];
+    const unsigned long long off = atomicAdd(a.ctr + 1, (unsigned long long)len);
+    const uint8_t* src = a.text + a.tstart[t];
+    for (int i = 0; i < len; ++i) a.arena[off + i] = src[i];
+    a.id_off[id] = (int64_t)off;
+    a.id_len[id] = len;
+  }
+}
+
+__global__ void tok_final_kernel(TokArgs a) {
+  const int64_t nt = *a.n_tokens;
+  const unsigned long long base_id = a.ctr[0];
+  const bool failed = a.ctr[2] != 0;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sl = a.tslot[t];
+    if (sl < 0 || !a.tnew[t]) continue;
+    if (failed) {  // roll the batch's claims back: the table returns to its pre-batch state
+      a.slots[sl].key = 0;  // (claims sit at the first empty slot of their probe path)
+    } else {
+      const uint32_t id = (uint32_t)(base_id + a.new_rank[t]);
+      a.tok[t] = id;
+      a.slots[sl].id = id;
+    }
+    a.owner[sl] = INT64_MAX;
+  }
+}
+
+__global__ void tok_final2_kernel(TokArgs a) {  // duplicates read the published ids
+  const int64_t nt = *a.n_tokens;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sl = a.tslot[t];
+    if (sl >= 0 && !a.tnew[t]) a.tok[t] = a.slots[sl].id;
+  }
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= a.n_req; r += (int64_t)gridDim.x * blockDim.x) {
+    // first token at or after the request's first byte (tstart is sorted)
+    const int64_t b = r < a.n_req ? a.msg_off[a.req_msg_off[r]] : a.n_bytes;
+    int64_t lo = 0, hi = nt;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (a.tstart[mid] < b) lo = mid + 1;
+      else hi = mid;
+    }
+    a.tok_off[r] = lo;
+  }
+}
+
+__global__ void tok_commit_kernel(TokArgs a) {  // advance the id counter once per batch
+  if (threadIdx.x == 0 && blockIdx.x == 0 && !a.ctr[2]) a.ctr[0] += a.new_rank[*a.n_tokens];
+}
+
+__global__ void copy_count_kernel(const int64_t* chunk_off, int64_t nchunks, int64_t* n_tokens) {
+  *n_tokens = chunk_off[nchunks];
+}
+
+static int sm_count_k() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+__global__ void interner_init_kernel(TSlot* slots, int64_t* owner, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    slots[i].key = 0;
+    slots[i].id = TOK_PENDING;
+    slots[i].pad = 0;
+    owner[i] = INT64_MAX;
+  }
+}
+
+// Device-pointer batch. tok must hold (n_bytes + 1) / 2 ids (the most a byte string can split into).
+static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg_off, int64_t n_msg,
+                        const int64_t* msg_off, const uint8_t* text, int64_t n_bytes, int64_t* tok_off,
+                        uint32_t* tok, int64_t* n_tokens) {
+  cudaStream_t st = it->stream;
+  const int64_t nchunks = (n_bytes + CHUNK - 1) / CHUNK;
+  const int64_t tb = (n_bytes + 1) / 2 + 1;  // token bound
+  Carver cv;
+  const size_t o_ms = cv.take<uint8_t>(n_bytes + 1), o_cnt = cv.take<int64_t>(nchunks + 1),
+               o_co = cv.take<int64_t>(nchunks + 1), o_ts = cv.take<int64_t>(tb), o_tl = cv.take<int32_t>(tb),
+               o_sl = cv.take<int64_t>(tb), o_nw = cv.take<uint8_t>(tb), o_nr = cv.take<int64_t>(tb + 1),
+               o_tmp = cv.take<int64_t>(scan_scratch_elems(tb > nchunks ? tb : nchunks));
+  if (int rc = it->scratch.ensure(cv.off)) return rc;
+  char* base = it->scratch.as<char>();
+  TokArgs a;
+  a.n_req = n_req;
+  a.req_msg_off = req_msg_off;
+  a.msg_off = msg_off;
+  a.n_msg = n_msg;
+  a.text = text;
+  a.n_bytes = n_bytes;
+  a.mstart = reinterpret_cast<uint8_t*>(base + o_ms);
+  a.chunk_off = reinterpret_cast<int64_t*>(base + o_co);
+  a.tstart = reinterpret_cast<int64_t*>(base + o_ts);
+  a.tlen = reinterpret_cast<int32_t*>(base + o_tl);
+  a.tslot = reinterpret_cast<int64_t*>(base + o_sl);
+  a.tnew = reinterpret_cast<uint8_t*>(base + o_nw);
+  a.new_rank = reinterpret_cast<int64_t*>(base + o_nr);
+  a.tok_off = tok_off;
+  a.tok = tok;
+  a.n_tokens = n_tokens;
+  a.slots = it->slots;
+  a.mask = (uint64_t)it->slots_n - 1;
+  a.owner = it->owner;
+  a.arena = it->arena;
+  a.arena_cap = it->arena_cap;
+  a.id_off = it->id_off;
+  a.id_len = it->id_len;
+  a.max_ids = it->max_ids;
+  a.ctr = it->ctr;
+  int64_t* counts = reinterpret_cast<int64_t*>(base + o_cnt);
+  int64_t* tmp = reinterpret_cast<int64_t*>(base + o_tmp);
+  const int sms = sm_count_k();
+  SFKV_CUDA(cudaMemsetAsync(a.mstart, 0, n_bytes + 1, st));
+  SFKV_CUDA(cudaMemsetAsync(it->ctr + 3, 0, sizeof(unsigned long long), st));
+  if (n_msg > 0) msg_mark_kernel<<<grid_for(n_msg, 256, sms * 4), 256, 0, st>>>(a);
+  if (nchunks > 0) chunk_count_kernel<<<(unsigned)nchunks, CHUNK_THREADS, 0, st>>>(a, counts);
+  SFKV_LAUNCH_CHECK("msg_mark/chunk_count");
+  if (int rc = exclusive_scan(ChunkCount{counts}, nchunks, a.chunk_off, tmp, st)) return rc;
+  if (nchunks > 0) chunk_emit_kernel<<<(unsigned)nchunks, CHUNK_THREADS, 0, st>>>(a);
+  copy_count_kernel<<<1, 1, 0, st>>>(a.chunk_off, nchunks, n_tokens);
+  const int g = grid_for(tb, 256, sms * 8);
+  tok_probe_kernel<<<g, 256, 0, st>>>(a);
+  tok_resolve_kernel<<<g, 256, 0, st>>>(a);
+  SFKV_LAUNCH_CHECK("chunk_emit/probe/resolve");
+  if (int rc = exclusive_scan(NewFlag{a.tnew}, tb, a.new_rank, tmp, st)) return rc;
+  tok_check_kernel<<<1, 32, 0, st>>>(a);
+  tok_publish_kernel<<<g, 256, 0, st>>>(a);
+  tok_final_kernel<<<g, 256, 0, st>>>(a);
+  tok_final2_kernel<<<g, 256, 0, st>>>(a);
+  tok_commit_kernel<<<1, 32, 0, st>>>(a);
+  SFKV_LAUNCH_CHECK("publish/final");
+  return 0;
+}
+
+}  // namespace sfkv
+
+using namespace sfkv;
+
+static void interner_free(sfkv_interner* it) {
+  cudaFree(it->slots);
+  cudaFree(it->owner);
+  cudaFree(it->arena);
+  cudaFree(it->id_off);
+  cudaFree(it->id_len);
+  cudaFree(it->ctr);
+  if (it->ctr_host) cudaFreeHost(it->ctr_host);
+  it->scratch.release();
+  it->io.release();
+  if (it->own_stream && it->stream) cudaStreamDestroy(it->stream);
+}
+
+static int interner_check(sfkv_interner* it) {
+  SFKV_CUDA(cudaMemcpyAsync(it->ctr_host, it->ctr, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, it->stream));
+  SFKV_CUDA(cudaStreamSynchronize(it->stream));
+  const unsigned long long e = it->ctr_host[2];
+  if (!e) return 0;
+  // the failed batch published nothing; clear the flag so the interner stays usable
+  SFKV_CUDA(cudaMemsetAsync(it->ctr + 2, 0, sizeof(unsigned long long), it->stream));
+  if (e & TERR_COLLISION) return fail(SFKV_ECOLLIDE, "tokenize: 64-bit hash collision between different tokens");
+  if (e & TERR_TABLE) return fail(SFKV_EPOOL, "tokenize: interner table full");
+  if (e & TERR_IDS) return fail(SFKV_EPOOL, "tokenize: interner id space full");
+  return fail(SFKV_EPOOL, "tokenize: interner arena full");
+}
+
+extern "C" {
+
+int sfkv_interner_create(int32_t device, int32_t table_log2, int64_t arena_bytes, sfkv_interner** out) {
+  if (!out || table_log2 < 4 || table_log2 > 34 || arena_bytes <= 0)
+    return fail(SFKV_EINVAL, "interner_create: bad argument");
+  if (int rc = check_device(device)) return rc;
+  DeviceGuard g(device);
+  auto* it = new sfkv_interner;
+  it->device = device;
+  it->slots_n = int64_t(1) << table_log2;
+  it->arena_cap = arena_bytes;
+  it->max_ids = it->slots_n / 2;  // load factor <= 0.5
+  cudaError_t e;
+  if ((e = cudaMalloc(&it->slots, it->slots_n * sizeof(TSlot))) != cudaSuccess ||
+      (e = cudaMalloc(&it->owner, it->slots_n * sizeof(int64_t))) != cudaSuccess ||
+      (e = cudaMalloc(&it->arena, arena_bytes)) != cudaSuccess ||
+      (e = cudaMalloc(&it->id_off, it->max_ids * sizeof(int64_t))) != cudaSuccess ||
+      (e = cudaMalloc(&it->id_len, it->max_ids * sizeof(int32_t))) != cudaSuccess ||
+      (e = cudaMalloc(&it->ctr, 4 * sizeof(unsigned long long))) != cudaSuccess ||
+      (e = cudaMallocHost(&it->ctr_host, 4 * sizeof(unsigned long long))) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&it->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+    interner_free(it);
+    delete it;
+    return cuda_fail(e, "interner_create");
+  }
+  it->own_stream = true;
+  interner_init_kernel<<<grid_for(it->slots_n, 256, 4096), 256, 0, it->stream>>>(it->slots, it->owner, it->slots_n);
+  cudaMemsetAsync(it->ctr, 0, 4 * sizeof(unsigned long long), it->stream);
+  if ((e = cudaStreamSynchronize(it->stream)) != cudaSuccess) {
+    interner_free(it);
+    delete it;
+    return cuda_fail(e, "interner init");
+  }
+  *out = it;
+  return 0;
+}
+
+int sfkv_interner_destroy(sfkv_interner* it) {
+  if (!it) return fail(SFKV_EINVAL, "interner_destroy: null interner");
+  DeviceGuard g(it->device);
+  cudaStreamSynchronize(it->stream);
+  interner_free(it);
+  delete it;
+  return 0;
+}
+
+int sfkv_interner_set_stream(sfkv_interner* it, void* stream) {
+  if (!it) return fail(SFKV_EINVAL, "interner_set_stream: null interner");
+  DeviceGuard g(it->device);
+  SFKV_CUDA(cudaStreamSynchronize(it->stream));
+  if (it->own_stream) cudaStreamDestroy(it->stream);
+  if (stream) {
+    it->stream = static_cast<cudaStream_t>(stream);
+    it->own_stream = false;
+  } else {
+    SFKV_CUDA(cudaStreamCreateWithFlags(&it->stream, cudaStreamNonBlocking));
+    it->own_stream = true;
+  }
+  return 0;
+}
+
+int sfkv_interner_size(sfkv_interner* it, int64_t* n_ids) {
+  if (!it || !n_ids) return fail(SFKV_EINVAL, "interner_size: null argument");
+  DeviceGuard g(it->device);
+  SFKV_CUDA(cudaMemcpyAsync(it->ctr_host, it->ctr, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, it->stream));
+  SFKV_CUDA(cudaStreamSynchronize(it->stream));
+  *n_ids = (int64_t)it->ctr_host[0];
+  return 0;
+}
+
+int sfkv_interner_token(sfkv_interner* it, uint32_t id, char* out, int32_t cap, int32_t* len) {
+  if (!it || !len || (cap > 0 && !out)) return fail(SFKV_EINVAL, "interner_token: bad argument");
+  int64_t n = 0;
+  if (int rc = sfkv_interner_size(it, &n)) return rc;
+  if ((int64_t)id >= n) return fail(SFKV_EINVAL, "interner_token: unknown id");
+  DeviceGuard g(it->device);
+  int64_t off = 0;
+  int32_t l = 0;
+  SFKV_CUDA(cudaMemcpy(&off, it->id_off + id, sizeof(off), cudaMemcpyDeviceToHost));
+  SFKV_CUDA(cudaMemcpy(&l, it->id_len + id, sizeof(l), cudaMemcpyDeviceToHost));
+  *len = l;
+  if (cap > 0) SFKV_CUDA(cudaMemcpy(out, it->arena + off, (size_t)(l < cap ? l : cap), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int sfkv_tokenize_batch_dev(sfkv_interner* it, int64_t n, const int64_t* req_msg_off, int64_t n_msg,
+                            const int64_t* msg_off, const uint8_t* text, int64_t n_bytes, int64_t* tok_off,
+                            uint32_t* tok, int64_t* n_tokens) {
+  if (!it || n < 0 || n_msg < 0 || n_bytes < 0 || !tok_off || !n_tokens || (n > 0 && !req_msg_off) ||
+      (n_msg > 0 && !msg_off) || (n_bytes > 0 && (!text || !tok)))
+    return fail(SFKV_EINVAL, "tokenize_batch_dev: bad argument");
+  DeviceGuard g(it->device);
+  return tokenize_dev(it, n, req_msg_off, n_msg, msg_off, text, n_bytes, tok_off, tok, n_tokens);
+}
+
+int sfkv_tokenize_batch(sfkv_interner* it, int64_t n, const int64_t* req_msg_off, const int64_t* msg_off,
+                        const uint8_t* text, int64_t* tok_off, uint32_t* tok, int64_t tok_cap,
+                        int64_t* n_tokens) {
+  if (!it || n < 0 || !req_msg_off || !tok_off || !n_tokens) return fail(SFKV_EINVAL, "tokenize_batch: bad argument");
+  const int64_t n_msg = req_msg_off[n];
+  if (req_msg_off[0] != 0) return fail(SFKV_EINVAL, "tokenize_batch: req_msg_off[0] must be 0");
+  for (int64_t r = 0; r < n; ++r)
+    if (req_msg_off[r + 1] < req_msg_off[r]) return fail(SFKV_EINVAL, "tokenize_batch: req_msg_off decreasing");
+  if (n_msg > 0 && !msg_off) return fail(SFKV_EINVAL, "tokenize_batch: null msg_off");
+  const int64_t n_bytes = n_msg > 0 ? msg_off[n_msg] : 0;
+  if (n_msg > 0 && msg_off[0] != 0) return fail(SFKV_EINVAL, "tokenize_batch: msg_off[0] must be 0");
+  for (int64_t m = 0; m < n_msg; ++m)
+    if (msg_off[m + 1] < msg_off[m]) return fail(SFKV_EINVAL, "tokenize_batch: msg_off decreasing");
+  if (tok_cap < (n_bytes + 1) / 2) return fail(SFKV_EINVAL, "tokenize_batch: tok_cap < (n_bytes + 1) / 2");
+  DeviceGuard g(it->device);
+  cudaStream_t st = it->stream;
+  const int64_t tb = (n_bytes + 1) / 2 + 1;
+  Carver cv;
+  const size_t o_rm = cv.take<int64_t>(n + 1), o_mo = cv.take<int64_t>(n_msg + 1), o_tx = cv.take<uint8_t>(n_bytes + 16),
+               o_to = cv.take<int64_t>(n + 1), o_tk = cv.take<uint32_t>(tb), o_nt = cv.take<int64_t>(1);
+  if (int rc = it->io.ensure(cv.off)) return rc;
+  char* b = it->io.as<char>();
+  SFKV_CUDA(cudaMemcpyAsync(b + o_rm, req_msg_off, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+  if (n_msg > 0) SFKV_CUDA(cudaMemcpyAsync(b + o_mo, msg_off, (n_msg + 1) * 8, cudaMemcpyHostToDevice, st));
+  else SFKV_CUDA(cudaMemsetAsync(b + o_mo, 0, 8, st));
+  if (n_bytes > 0) SFKV_CUDA(cudaMemcpyAsync(b + o_tx, text, n_bytes, cudaMemcpyHostToDevice, st));
+  if (int rc = tokenize_dev(it, n, reinterpret_cast<int64_t*>(b + o_rm), n_msg, reinterpret_cast<int64_t*>(b + o_mo),
+                            reinterpret_cast<uint8_t*>(b + o_tx), n_bytes, reinterpret_cast<int64_t*>(b + o_to),
+                            reinterpret_cast<uint32_t*>(b + o_tk), reinterpret_cast<int64_t*>(b + o_nt)))
+    return rc;
+  if (int rc = interner_check(it)) return rc;
+  SFKV_CUDA(cudaMemcpyAsync(n_tokens, b + o_nt, 8, cudaMemcpyDeviceToHost, st));
+  SFKV_CUDA(cudaStreamSynchronize(st));
+  SFKV_CUDA(cudaMemcpyAsync(tok_off, b + o_to, (n + 1) * 8, cudaMemcpyDeviceToHost, st));
+  if (*n_tokens > 0) SFKV_CUDA(cudaMemcpyAsync(tok, b + o_tk, *n_tokens * 4, cudaMemcpyDeviceToHost, st));
+  SFKV_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int sfkv_interner_check(sfkv_interner* it) {
+  if (!it) return fail(SFKV_EINVAL, "interner_check: null interner");
+  DeviceGuard g(it->device);
+  return interner_check(it);
+}
+
+}  // extern "C"
