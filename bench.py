@@ -367,6 +367,7 @@ def run_ours(args, rank, world, local_rank):
         c4 = None if args.no_c4 else long_context_leg(args, api, dev, stream, hbm_peak, rank)
         c3 = handoff_leg(args, api, dev, stream, rank, world) if (dist and not args.no_c3) else None
         mm = None if args.no_mm else mm_leg(args, api, dev, stream)
+        tk = None if args.no_tok else tokenize_leg(args, api, dev, stream, hbm_peak)
     clocks = clk.summary()
 
     # ---- roofline of the match kernel: algorithmic bytes of one launch --------------------
@@ -407,6 +408,8 @@ def run_ours(args, rank, world, local_rank):
         line["c3_handoff"] = c3
     if mm:
         line["mm_signals"] = mm
+    if tk:
+        line["tokenize"] = tk
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
     pool.close()
@@ -910,6 +913,103 @@ def mm_reference(L, args, n_wf=1000):
 
 
 
+def render_text(tok_ids, vocab=100_000):
+    """Token ids -> whitespace text over a vocab-word dictionary ("t<k>", k = id mod vocab),
+    single spaces: the string form the reference's tokenizer consumes. Returns (text bytes,
+    byte offset of every token plus the end)."""
+    W = 8
+    mat = np.zeros((vocab, W), np.uint8)  # word bytes, a space, zero padding
+    wlen = np.zeros(vocab, np.int64)
+    for k in range(vocab):
+        w = b"t%d " % k
+        mat[k, :len(w)] = np.frombuffer(w, np.uint8)
+        wlen[k] = len(w)
+    k = tok_ids.astype(np.int64) % vocab
+    rows = mat[k].ravel()
+    text = rows[rows != 0]
+    off = np.zeros(len(k) + 1, np.int64)
+    np.cumsum(wlen[k], out=off[1:])
+    return text, off
+
+
+def tokenize_leg(args, api, dev, stream, hbm_peak):
+    """§8f-2: whitespace tokenizer + interner over the C2 requests rendered to text (one message
+    per request, 100k-word vocabulary); steady state (every word already interned)."""
+    import torch
+
+    from paper_2603_13605_b200.abi import Interner
+    wl = make_workload(args.seed, args.workflows)
+    text, tok_byte_off = render_text(wl["req_tok"])
+    n = wl["n"]
+    msg_off = tok_byte_off[wl["req_off"]]  # each request is one message
+    req_msg_off = np.arange(n + 1, dtype=np.int64)
+    nbytes = int(msg_off[-1])
+    it = Interner(api, table_log2=20, arena_bytes=16 << 20, device=dev)
+    api.check("interner_set_stream", api.interner_set_stream(it.h, C.c_void_p(stream.cuda_stream)))
+    d_req = torch.from_numpy(req_msg_off).to(dev)
+    d_moff = torch.from_numpy(msg_off).to(dev)
+    d_text = torch.from_numpy(np.concatenate([text, np.zeros(16, np.uint8)])).to(dev)
+    d_off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    d_tok = torch.zeros((nbytes + 1) // 2 + 1, dtype=torch.int32, device=dev)
+    d_nt = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def step():
+        api.check("tokenize_batch_dev", api.tokenize_batch_dev(
+            it.h, n, C.c_void_p(d_req.data_ptr()), n, C.c_void_p(d_moff.data_ptr()),
+            C.c_void_p(d_text.data_ptr()), nbytes, C.c_void_p(d_off.data_ptr()),
+            C.c_void_p(d_tok.data_ptr()), C.c_void_p(d_nt.data_ptr())))
+    times = []
+    for i in range(args.warmup + args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            times.append(a.elapsed_time(b))
+    api.check("interner_check", api.interner_check(it.h))
+    nt = int(d_nt.item())
+    assert nt == len(wl["req_tok"])
+    off = d_off.cpu().numpy()
+    assert (off == wl["req_off"]).all()
+    vocab_ids = d_tok[:nt].cpu().numpy()
+    # the same word always has the same id (and distinct words distinct ids)
+    k = wl["req_tok"].astype(np.int64) % 100_000
+    first = {}
+    assert all(first.setdefault(int(w), int(t)) == int(t) for w, t in zip(k[:200000], vocab_ids[:200000]))
+    ms = float(np.mean(times))
+    out = {"workload": f"{n} C2 requests rendered to text ({nbytes / 1e6:.0f} MB, {nt} tokens, 100k-word "
+                       "vocabulary, one message each); steady state: every word already interned",
+           "tokens_per_step": nt, "bytes_per_step": nbytes, "ms": ms, "tokens_per_s": nt / (ms / 1e3),
+           "text_gbps": nbytes / (ms / 1e3) / 1e9, "interned": it.size()}
+    it.close()
+    L = ref_lib()
+    if L is not None and not args.no_cpu_baseline:
+        out["cpu_reference"] = tokenize_reference(L, text, msg_off, min(n, 300))
+    return out
+
+
+def tokenize_reference(L, text, msg_off, n_req):
+    """The reference's context_token_sequence on a bounded sample (1 thread)."""
+    L.sfref_context_tokens.restype = C.c_longlong
+    L.sfref_context_tokens.argtypes = [C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_longlong), C.c_char_p,
+                                       C.c_longlong, C.POINTER(C.c_longlong), C.c_longlong]
+    msgs = [bytes(text[msg_off[r]:msg_off[r + 1]]) for r in range(n_req)]
+    cap = max(len(m) for m in msgs) + 1
+    out = C.create_string_buffer(cap)
+    out_len = (C.c_longlong * cap)()
+    toks = 0
+    t0 = time.perf_counter()
+    for m in msgs:
+        arr = (C.c_char_p * 1)(m)
+        ln = (C.c_longlong * 1)(len(m))
+        toks += L.sfref_context_tokens(1, arr, ln, out, cap, out_len, cap)
+    dt = time.perf_counter() - t0
+    return {"value": toks / dt, "unit": "tokens/s", "cores": 1, "kind": "reference",
+            "sample": f"{n_req} requests ({toks} tokens), context_token_sequence, 1 thread"}
+
+
+
 def cpu_baseline(args):
     L = ref_lib()
     n_sample = args.cpu_sample
@@ -941,6 +1041,7 @@ def main():
     ap.add_argument("--c5-prefixes", type=int, default=100_000)
     ap.add_argument("--no-c3", action="store_true")
     ap.add_argument("--no-mm", action="store_true")
+    ap.add_argument("--no-tok", action="store_true")
     ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--dist-backend", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--c3-workflows", type=int, default=32)

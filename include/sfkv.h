@@ -218,7 +218,7 @@ int sfkv_handoff_recv_batch_dev(sfkv_pool* dst, const sfkv_peer* src, int64_t n,
 typedef struct sfkv_interner sfkv_interner;
 int sfkv_interner_create(int32_t device, int32_t table_log2, int64_t arena_bytes, sfkv_interner** out);
 int sfkv_interner_destroy(sfkv_interner* it);
-int sfkv_interner_set_stream(sfkv_interner* it, void* cuda_stream);
+int sfkv_interner_set_stream(sfkv_interner* it, void* cuda_stream);  /* NULL = legacy default stream */
 int sfkv_interner_size(sfkv_interner* it, int64_t* n_ids);
 int sfkv_interner_token(sfkv_interner* it, uint32_t id, char* out, int32_t cap, int32_t* len);
 int sfkv_tokenize_batch(sfkv_interner* it, int64_t n, const int64_t* req_msg_off, const int64_t* msg_off,
@@ -323,7 +323,7 @@ typedef struct sfmm_records {        /* outputs: n signals x n_backends record s
 
 int sfmm_tracker_create(const sfmm_config* cfg, sfmm_tracker** out);
 int sfmm_tracker_destroy(sfmm_tracker* t);
-int sfmm_tracker_set_stream(sfmm_tracker* t, void* cuda_stream);
+int sfmm_tracker_set_stream(sfmm_tracker* t, void* cuda_stream);  /* NULL = legacy default stream */
 int sfmm_tracker_sync(sfmm_tracker* t);
 /* Forget every workflow (a fresh MemoryManager with the same configuration). */
 int sfmm_tracker_reset(sfmm_tracker* t);

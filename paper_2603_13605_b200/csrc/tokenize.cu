@@ -463,13 +463,8 @@ int sfkv_interner_set_stream(sfkv_interner* it, void* stream) {
   DeviceGuard g(it->device);
   SFKV_CUDA(cudaStreamSynchronize(it->stream));
   if (it->own_stream) cudaStreamDestroy(it->stream);
-  if (stream) {
-    it->stream = static_cast<cudaStream_t>(stream);
-    it->own_stream = false;
-  } else {
-    SFKV_CUDA(cudaStreamCreateWithFlags(&it->stream, cudaStreamNonBlocking));
-    it->own_stream = true;
-  }
+  it->stream = static_cast<cudaStream_t>(stream);  // NULL: the legacy default stream (as pools)
+  it->own_stream = false;
   return 0;
 }
 

@@ -517,13 +517,8 @@ int sfmm_tracker_set_stream(sfmm_tracker* t, void* stream) {
   DeviceGuard g(t->cfg.device);
   SFKV_CUDA(cudaStreamSynchronize(t->stream));
   if (t->own_stream) cudaStreamDestroy(t->stream);
-  if (stream) {
-    t->stream = static_cast<cudaStream_t>(stream);
-    t->own_stream = false;
-  } else {
-    SFKV_CUDA(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
-    t->own_stream = true;
-  }
+  t->stream = static_cast<cudaStream_t>(stream);  // NULL: the legacy default stream (as pools)
+  t->own_stream = false;
   return 0;
 }
 
