@@ -9,19 +9,23 @@
 // deterministic and equal to a sequential restatement's.
 //
 // Launches for a batch (text is a CSR of messages, requests are ranges of messages):
-//   msg_mark_kernel    flags the first byte of every message (a forced token boundary)
-//   chunk_count_kernel token starts per 4 KiB chunk (start: non-space byte after a space or at a
-//                      message start)
-//   exclusive scan     over chunks
-//   chunk_emit_kernel  CTA-wide scan inside each chunk: token start positions, in order
-//   tok_probe_kernel   per token: length (to the next space / message start), 64-bit hash, probe
-//                      the interner table: a verified hit is the id; a miss claims a slot (CAS)
-//                      and competes for ownership with atomicMin(position) — lowest position wins
-//   tok_resolve_kernel claimers that lost compare their bytes with the owner's (a 64-bit hash
-//                      collision between different strings fails the batch loudly)
-//   exclusive scan     over owner flags -> new ids in first-occurrence order
-//   tok_publish_kernel owners copy their bytes into the arena and publish the id in the slot
-//   tok_final_kernel   every token reads its id; per-request token offsets by binary search
+//   msg_mark_kernel     message-start bitmap (a message start is a forced token boundary)
+//   chunk_count_kernel  token starts per 4 KiB chunk: 16-B loads, C-locale space test on 4 bytes
+//                       at a time (__vcmpeq4 / __vcmpleu4), start = non-space & (prev space |
+//                       message start)
+//   exclusive scan      over chunks
+//   chunk_emit_kernel   CTA scan inside each chunk: token start positions, in order
+//   tok_probe_kernel    per token: length, key, probe. Tokens of <= 7 bytes key on their own bytes
+//                       (exact); longer ones on a 63-bit hash verified against the arena. A string
+//                       published by an earlier batch resolves here; claims (CAS into an empty
+//                       slot + atomicMin(position): the lowest position owns the new string) and
+//                       duplicates of this batch's new strings go to a pending list
+//   tok_resolve_kernel  pending tokens: owners flagged; long duplicates compare bytes with the owner
+//                       (a 64-bit hash collision fails the batch loudly)
+//   rank_* kernels      owners ranked by position (tile counts, scan, in-tile scan) -> new ids in
+//                       first-occurrence order; bytes copied to the arena. They exit at once when
+//                       the batch brings no new string (steady state).
+//   tok_final* kernels  duplicates read the published ids; per-request token offsets
 // Byte-stream work, HBM/latency-bound; no tensor cores.
 #include "pool.cuh"
 
@@ -37,7 +41,9 @@ struct sfkv_interner {
   uint8_t* arena = nullptr;
   int64_t* id_off = nullptr;      // id -> arena offset
   int32_t* id_len = nullptr;
-  unsigned long long* ctr = nullptr;  // [0] ids, [1] arena cursor, [2] error flag
+  unsigned long long* ctr = nullptr;  // [0] ids, [1] arena cursor, [2] error flag, [3..5] batch
+  uint8_t* tnew = nullptr;         // per-token owner flags, zero between batches
+  size_t tnew_cap = 0;
   unsigned long long* ctr_host = nullptr;
   sfkv::Scratch scratch;
   sfkv::Scratch io;
@@ -53,13 +59,27 @@ namespace sfkv {
 
 constexpr uint32_t TOK_PENDING = 0xffffffffu;
 constexpr int CHUNK = 4096;
-constexpr int CHUNK_THREADS = 256;
-constexpr int PER_THREAD = CHUNK / CHUNK_THREADS;  // 16 bytes per thread
+constexpr int CHUNK_THREADS = 256;  // 16 bytes (one 16-B load) per thread
+constexpr int RANK_TILE = 8192;     // tokens per CTA of the rank pass (256 threads x 32)
 enum : int { TERR_COLLISION = 1, TERR_ARENA = 2, TERR_IDS = 4, TERR_TABLE = 8 };
+// ctr: [0] ids, [1] arena cursor, [2] error, [3] new bytes, [4] pending, [5] new ids (batch)
 
 __device__ __forceinline__ bool is_space(uint8_t c) { return c == ' ' || (c >= '\t' && c <= '\r'); }
 
-__device__ __forceinline__ unsigned long long tok_hash(const uint8_t* p, int len) {
+// 4 bytes -> 4-bit mask (bit j = byte j is a C-locale space)
+__device__ __forceinline__ uint32_t space_mask4(uint32_t w) {
+  const uint32_t sp = __vcmpeq4(w, 0x20202020u) | __vcmpleu4(__vsub4(w, 0x09090909u), 0x04040404u);
+  return ((sp & 0x01010101u) * 0x01020408u) >> 24;
+}
+
+// Table keys: tokens of <= 7 bytes are their own key (tag bit 63 | length | bytes): exact, no
+// verification. Longer tokens key on a 63-bit hash and are verified against the arena / owner.
+__device__ __forceinline__ unsigned long long tok_key(const uint8_t* p, int len) {
+  if (len <= 7) {
+    unsigned long long w = 0;
+    for (int k = 0; k < len; ++k) w |= (unsigned long long)p[k] << (8 * k);
+    return (1ull << 63) | ((unsigned long long)len << 56) | w;
+  }
   unsigned long long h = 0x9E3779B97F4A7C15ull ^ (unsigned long long)len;
   int i = 0;
   for (; i + 8 <= len; i += 8) {
@@ -73,7 +93,7 @@ __device__ __forceinline__ unsigned long long tok_hash(const uint8_t* p, int len
     for (int k = 0; i + k < len; ++k) w |= (unsigned long long)p[i + k] << (8 * k);
     h = mix64(h + w * 0xD6E8FEB86659FD93ull);
   }
-  h = mix64(h);
+  h = mix64(h) & ~(1ull << 63);
   return h ? h : 1;
 }
 
@@ -84,16 +104,18 @@ struct TokArgs {
   int64_t n_msg;
   const uint8_t* text;
   int64_t n_bytes;
-  uint8_t* mstart;       // [n_bytes + 1]
+  uint32_t* mbits;       // message-start bitmap
   int64_t* chunk_off;    // [nchunks + 1]
   int64_t* tstart;       // [token bound]
-  int32_t* tlen;
-  int64_t* tslot;
-  uint8_t* tnew;
-  int64_t* new_rank;     // [token bound + 1]
+  int64_t* pend_t;       // pending tokens (claims / duplicates of new strings)
+  int64_t* pend_slot;
+  int32_t* pend_len;
+  uint8_t* tnew;         // [token bound] owner flags (kept zero between batches)
+  int64_t* tile_cnt;     // [rank tiles + 1]
   int64_t* tok_off;      // out [n_req + 1]
   uint32_t* tok;         // out
   int64_t* n_tokens;     // out (device scalar)
+  int64_t n_rank_tiles;
   // interner
   TSlot* slots;
   uint64_t mask;
@@ -107,26 +129,35 @@ struct TokArgs {
 };
 
 __global__ void msg_mark_kernel(TokArgs a) {
-  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < a.n_msg; m += (int64_t)gridDim.x * blockDim.x)
-    if (a.msg_off[m] < a.n_bytes) a.mstart[a.msg_off[m]] = 1;
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < a.n_msg; m += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = a.msg_off[m];
+    if (i < a.n_bytes) atomicOr(a.mbits + (i >> 5), 1u << (i & 31));
+  }
 }
 
-__device__ __forceinline__ bool tok_start(const TokArgs& a, int64_t i) {
-  const uint8_t c = a.text[i];
-  return !is_space(c) && (i == 0 || a.mstart[i] || is_space(a.text[i - 1]));
+// 16-bit mask of token starts among bytes [base, base + 16) (base 16-aligned): a non-space byte
+// whose predecessor is a space or which starts a message (or the text).
+__device__ __forceinline__ uint32_t start_mask16(const TokArgs& a, int64_t base) {
+  if (base >= a.n_bytes) return 0;
+  uint32_t sp;
+  if (base + 16 <= a.n_bytes) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(a.text + base));
+    sp = space_mask4(v.x) | (space_mask4(v.y) << 4) | (space_mask4(v.z) << 8) | (space_mask4(v.w) << 12);
+  } else {
+    sp = 0xffffu;
+    for (int j = 0; base + j < a.n_bytes; ++j)
+      if (!is_space(a.text[base + j])) sp &= ~(1u << j);
+  }
+  const uint32_t prev_sp = base == 0 ? 1u : (is_space(a.text[base - 1]) ? 1u : 0u);
+  const uint32_t ms = (__ldg(a.mbits + (base >> 5)) >> (base & 31)) & 0xffffu;
+  return ~sp & (((sp << 1) | prev_sp) | ms) & 0xffffu;
 }
 
 __global__ void __launch_bounds__(CHUNK_THREADS) chunk_count_kernel(TokArgs a, int64_t* counts) {
   using BR = cub::BlockReduce<int, CHUNK_THREADS>;
   __shared__ typename BR::TempStorage tmp;
-  const int64_t base = (int64_t)blockIdx.x * CHUNK;
-  int c = 0;
-#pragma unroll
-  for (int k = 0; k < PER_THREAD; ++k) {
-    const int64_t i = base + (int64_t)k * CHUNK_THREADS + threadIdx.x;
-    if (i < a.n_bytes && tok_start(a, i)) ++c;
-  }
-  c = BR(tmp).Sum(c);
+  const int64_t base = (int64_t)blockIdx.x * CHUNK + (int64_t)threadIdx.x * 16;
+  const int c = BR(tmp).Sum(__popc(start_mask16(a, base)));
   if (threadIdx.x == 0) counts[blockIdx.x] = c;
 }
 
@@ -138,21 +169,16 @@ struct ChunkCount {
 __global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
   using BS = cub::BlockScan<int, CHUNK_THREADS>;
   __shared__ typename BS::TempStorage tmp;
-  const int64_t base = (int64_t)blockIdx.x * CHUNK + (int64_t)threadIdx.x * PER_THREAD;  // blocked
-  bool f[PER_THREAD];
-  int c = 0;
-#pragma unroll
-  for (int k = 0; k < PER_THREAD; ++k) {
-    const int64_t i = base + k;
-    f[k] = i < a.n_bytes && tok_start(a, i);
-    c += f[k];
-  }
+  const int64_t base = (int64_t)blockIdx.x * CHUNK + (int64_t)threadIdx.x * 16;
+  uint32_t m = start_mask16(a, base);
   int excl;
-  BS(tmp).ExclusiveSum(c, excl);
+  BS(tmp).ExclusiveSum(__popc(m), excl);
   int64_t o = a.chunk_off[blockIdx.x] + excl;
-#pragma unroll
-  for (int k = 0; k < PER_THREAD; ++k)
-    if (f[k]) a.tstart[o++] = base + k;
+  while (m) {
+    const int j = __ffs(m) - 1;
+    m &= m - 1;
+    a.tstart[o++] = base + j;
+  }
 }
 
 __device__ __forceinline__ bool bytes_equal(const uint8_t* x, const uint8_t* y, int len) {
@@ -161,120 +187,179 @@ __device__ __forceinline__ bool bytes_equal(const uint8_t* x, const uint8_t* y, 
   return true;
 }
 
+__device__ __forceinline__ bool is_mstart(const TokArgs& a, int64_t i) {
+  return (a.mbits[i >> 5] >> (i & 31)) & 1u;
+}
+
+// Per token: length, key, probe. Published strings resolve here (short keys exactly, long keys
+// verified against the arena); claims and duplicates of this batch's new strings go to the
+// pending list.
 __global__ void tok_probe_kernel(TokArgs a) {
   const int64_t nt = *a.n_tokens;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = a.tstart[t];
     int64_t e = s + 1;
-    while (e < a.n_bytes && !is_space(a.text[e]) && !a.mstart[e]) ++e;
+    while (e < a.n_bytes && !is_space(a.text[e]) && !is_mstart(a, e)) ++e;
     const int len = (int)(e - s);
-    a.tlen[t] = len;
-    const unsigned long long h = tok_hash(a.text + s, len);
-    uint64_t sl = h & a.mask;
+    const uint8_t* mine = a.text + s;
+    const unsigned long long key = tok_key(mine, len);
+    uint64_t sl = mix64(key) & a.mask;  // short keys are raw bytes: spread them before placing
     int64_t found = -1;
+    uint32_t id = TOK_PENDING;
     for (uint64_t probes = 0; probes <= a.mask; ++probes) {
       TSlot* p = a.slots + sl;
       unsigned long long k = p->key;
       if (k == 0) {
-        k = atomicCAS(&p->key, 0ull, h);
-        if (k == 0) k = h;  // claimed it (its id is TOK_PENDING until published)
+        k = atomicCAS(&p->key, 0ull, key);
+        if (k == 0) k = key;  // claimed: its id stays TOK_PENDING until published
       }
-      if (k == h) {
+      if (k == key) {
         found = (int64_t)sl;
+        id = *(volatile uint32_t*)&p->id;
         break;
       }
       sl = (sl + 1) & a.mask;
     }
     if (found < 0) {
       atomicOr(a.ctr + 2, (unsigned long long)TERR_TABLE);
-      a.tslot[t] = -1;
       continue;
     }
-    a.tslot[t] = found;
-    const uint32_t id = *(volatile uint32_t*)&a.slots[found].id;
-    if (id == TOK_PENDING) atomicMin(reinterpret_cast<unsigned long long*>(a.owner + found), (unsigned long long)t);
-  }
-}
-
-// Settle every token: verified hit (id published before this batch), owner of a new string, or
-// a duplicate of a new string (bytes compared with the owner's).
-__global__ void tok_resolve_kernel(TokArgs a) {
-  const int64_t nt = *a.n_tokens;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t sl = a.tslot[t];
-    uint8_t isnew = 0;
-    if (sl >= 0) {
-      const uint32_t id = a.slots[sl].id;
-      const uint8_t* mine = a.text + a.tstart[t];
-      const int len = a.tlen[t];
-      if (id != TOK_PENDING) {  // existing string: verify against the arena copy
-        if (a.id_len[id] != len || !bytes_equal(mine, a.arena + a.id_off[id], len))
-          atomicOr(a.ctr + 2, (unsigned long long)TERR_COLLISION);
-      } else {
-        const int64_t o = a.owner[sl];
-        if (o == t) {
-          isnew = 1;
-          atomicAdd(a.ctr + 3, (unsigned long long)len);  // arena bytes this batch needs
-        } else if (a.tlen[o] != len || !bytes_equal(mine, a.text + a.tstart[o], len)) {
-          atomicOr(a.ctr + 2, (unsigned long long)TERR_COLLISION);
-        }
-      }
+    if (id != TOK_PENDING) {  // published before this batch
+      if (!(key >> 63) && (a.id_len[id] != len || !bytes_equal(mine, a.arena + a.id_off[id], len)))
+        atomicOr(a.ctr + 2, (unsigned long long)TERR_COLLISION);
+      a.tok[t] = id;
+      continue;
     }
-    a.tnew[t] = isnew;
+    atomicMin(reinterpret_cast<unsigned long long*>(a.owner + found), (unsigned long long)t);
+    const unsigned long long j = atomicAdd(a.ctr + 4, 1ull);
+    a.pend_t[j] = t;
+    a.pend_slot[j] = found;
+    a.pend_len[j] = len;
   }
 }
 
-struct NewFlag {
-  const uint8_t* f;
-  __device__ int64_t operator()(int64_t t) const { return f[t]; }
-};
+// Pending tokens: the lowest position owns a new string; the others are duplicates (long keys
+// compare bytes with the owner's: a 64-bit hash collision fails the batch loudly).
+__global__ void tok_resolve_kernel(TokArgs a) {
+  const int64_t np = (int64_t)a.ctr[4];
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = a.pend_t[j], sl = a.pend_slot[j];
+    const int len = a.pend_len[j];
+    const int64_t o = a.owner[sl];
+    if (o == t) {
+      a.tnew[t] = 1;
+      atomicAdd(a.ctr + 5, 1ull);
+      atomicAdd(a.ctr + 3, (unsigned long long)len);
+    } else if (!(a.slots[sl].key >> 63) && !bytes_equal(a.text + a.tstart[t], a.text + a.tstart[o], len)) {
+      atomicOr(a.ctr + 2, (unsigned long long)TERR_COLLISION);
+    }
+  }
+}
 
 // Capacity check before anything is published: a failing batch leaves the interner unchanged.
 __global__ void tok_check_kernel(TokArgs a) {
   if (threadIdx.x || blockIdx.x || a.ctr[2]) return;
-  if ((int64_t)(a.ctr[0] + a.new_rank[*a.n_tokens]) > a.max_ids) a.ctr[2] |= TERR_IDS;
+  if ((int64_t)(a.ctr[0] + a.ctr[5]) > a.max_ids) a.ctr[2] |= TERR_IDS;
   if ((int64_t)(a.ctr[1] + a.ctr[3]) > a.arena_cap) a.ctr[2] |= TERR_ARENA;
 }
 
-__global__ void tok_publish_kernel(TokArgs a) {
+// New ids in first-occurrence order: owners are ranked by token position (tile counts, a scan
+// over tiles, an in-tile block scan). Every pass exits at once when the batch has no new string.
+__global__ void __launch_bounds__(256) rank_count_kernel(TokArgs a) {
+  using BR = cub::BlockReduce<int, 256>;
+  __shared__ typename BR::TempStorage tmp;
   const int64_t nt = *a.n_tokens;
-  const unsigned long long base_id = a.ctr[0];
-  if (a.ctr[2]) return;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
-    if (!a.tnew[t]) continue;
-    const int64_t id = (int64_t)base_id + a.new_rank[t];
-    const int len = a.tlen[t];
+  const int64_t t0 = (int64_t)blockIdx.x * RANK_TILE;
+  if (a.ctr[5] == 0 || a.ctr[2] || t0 >= nt) return;
+  int c = 0;
+  for (int k = 0; k < RANK_TILE / 256; ++k) {
+    const int64_t t = t0 + (int64_t)k * 256 + threadIdx.x;
+    if (t < nt) c += a.tnew[t];
+  }
+  c = BR(tmp).Sum(c);
+  if (threadIdx.x == 0) a.tile_cnt[blockIdx.x] = c;
+}
+
+__global__ void __launch_bounds__(1024) rank_scan_kernel(TokArgs a) {
+  using BS = cub::BlockScan<int64_t, 1024>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ int64_t carry;
+  const int64_t nt = *a.n_tokens;
+  if (a.ctr[5] == 0 || a.ctr[2]) return;
+  const int64_t ntiles = (nt + RANK_TILE - 1) / RANK_TILE;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t b = 0; b < ntiles; b += 1024) {
+    const int64_t i = b + threadIdx.x;
+    int64_t v = i < ntiles ? a.tile_cnt[i] : 0, ex, tot;
+    BS(tmp).ExclusiveSum(v, ex, tot);
+    if (i < ntiles) a.tile_cnt[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) rank_publish_kernel(TokArgs a) {
+  using BS = cub::BlockScan<int, 256>;
+  __shared__ typename BS::TempStorage tmp;
+  const int64_t nt = *a.n_tokens;
+  const int64_t t0 = (int64_t)blockIdx.x * RANK_TILE;
+  if (a.ctr[5] == 0 || a.ctr[2] || t0 >= nt) return;
+  constexpr int PT = RANK_TILE / 256;
+  const int64_t tb = t0 + (int64_t)threadIdx.x * PT;  // blocked
+  int c = 0;
+  uint32_t f = 0;
+  for (int k = 0; k < PT; ++k)
+    if (tb + k < nt && a.tnew[tb + k]) {
+      f |= 1u << k;
+      ++c;
+    }
+  int ex;
+  BS(tmp).ExclusiveSum(c, ex);
+  int64_t id = (int64_t)a.ctr[0] + a.tile_cnt[blockIdx.x] + ex;
+  while (f) {
+    const int k = __ffs(f) - 1;
+    f &= f - 1;
+    const int64_t t = tb + k;
+    a.tnew[t] = 0;
+    const int64_t s = a.tstart[t];
+    int64_t e = s + 1;
+    while (e < a.n_bytes && !is_space(a.text[e]) && !is_mstart(a, e)) ++e;
+    const int len = (int)(e - s);
     const unsigned long long off = atomicAdd(a.ctr + 1, (unsigned long long)len);
-    const uint8_t* src = a.text + a.tstart[t];
-    for (int i = 0; i < len; ++i) a.arena[off + i] = src[i];
+    for (int i = 0; i < len; ++i) a.arena[off + i] = a.text[s + i];
     a.id_off[id] = (int64_t)off;
     a.id_len[id] = len;
+    a.tok[t] = (uint32_t)id;
+    ++id;
   }
 }
 
+// Pending tokens take their ids from the published slots (or, when the batch failed, the claims
+// are rolled back: the table returns to its pre-batch state — claims sit at the first empty slot
+// of their probe path, so clearing them restores every chain).
 __global__ void tok_final_kernel(TokArgs a) {
-  const int64_t nt = *a.n_tokens;
-  const unsigned long long base_id = a.ctr[0];
+  const int64_t np = (int64_t)a.ctr[4];
   const bool failed = a.ctr[2] != 0;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t sl = a.tslot[t];
-    if (sl < 0 || !a.tnew[t]) continue;
-    if (failed) {  // roll the batch's claims back: the table returns to its pre-batch state
-      a.slots[sl].key = 0;  // (claims sit at the first empty slot of their probe path)
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = a.pend_t[j], sl = a.pend_slot[j];
+    if (a.owner[sl] != t) continue;
+    if (failed) {
+      a.slots[sl].key = 0;
+      a.tnew[t] = 0;
     } else {
-      const uint32_t id = (uint32_t)(base_id + a.new_rank[t]);
-      a.tok[t] = id;
-      a.slots[sl].id = id;
+      a.slots[sl].id = a.tok[t];
     }
-    a.owner[sl] = INT64_MAX;
   }
 }
 
-__global__ void tok_final2_kernel(TokArgs a) {  // duplicates read the published ids
+__global__ void tok_final2_kernel(TokArgs a) {
+  const int64_t np = (int64_t)a.ctr[4];
   const int64_t nt = *a.n_tokens;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t sl = a.tslot[t];
-    if (sl >= 0 && !a.tnew[t]) a.tok[t] = a.slots[sl].id;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = a.pend_t[j], sl = a.pend_slot[j];
+    if (a.owner[sl] != t) a.tok[t] = a.slots[sl].id;  // duplicates of new strings
   }
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= a.n_req; r += (int64_t)gridDim.x * blockDim.x) {
     // first token at or after the request's first byte (tstart is sorted)
@@ -289,8 +374,14 @@ __global__ void tok_final2_kernel(TokArgs a) {  // duplicates read the published
   }
 }
 
+__global__ void tok_owner_reset_kernel(TokArgs a) {
+  const int64_t np = (int64_t)a.ctr[4];
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x)
+    a.owner[a.pend_slot[j]] = INT64_MAX;
+}
+
 __global__ void tok_commit_kernel(TokArgs a) {  // advance the id counter once per batch
-  if (threadIdx.x == 0 && blockIdx.x == 0 && !a.ctr[2]) a.ctr[0] += a.new_rank[*a.n_tokens];
+  if (threadIdx.x == 0 && blockIdx.x == 0 && !a.ctr[2]) a.ctr[0] += a.ctr[5];
 }
 
 __global__ void copy_count_kernel(const int64_t* chunk_off, int64_t nchunks, int64_t* n_tokens) {
@@ -317,19 +408,31 @@ __global__ void interner_init_kernel(TSlot* slots, int64_t* owner, int64_t n) {
   }
 }
 
-// Device-pointer batch. tok must hold (n_bytes + 1) / 2 ids (the most a byte string can split into).
+// Device-pointer batch. tok must hold (n_bytes + 1) / 2 ids (the most a byte string can split
+// into); text must be 16-B aligned.
 static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg_off, int64_t n_msg,
                         const int64_t* msg_off, const uint8_t* text, int64_t n_bytes, int64_t* tok_off,
                         uint32_t* tok, int64_t* n_tokens) {
+  if (reinterpret_cast<uintptr_t>(text) & 15) return fail(SFKV_EINVAL, "tokenize: text must be 16-B aligned");
   cudaStream_t st = it->stream;
   const int64_t nchunks = (n_bytes + CHUNK - 1) / CHUNK;
   const int64_t tb = (n_bytes + 1) / 2 + 1;  // token bound
+  const int64_t nrt = (tb + RANK_TILE - 1) / RANK_TILE;
+  const int64_t nwords = n_bytes / 32 + 2;
   Carver cv;
-  const size_t o_ms = cv.take<uint8_t>(n_bytes + 1), o_cnt = cv.take<int64_t>(nchunks + 1),
-               o_co = cv.take<int64_t>(nchunks + 1), o_ts = cv.take<int64_t>(tb), o_tl = cv.take<int32_t>(tb),
-               o_sl = cv.take<int64_t>(tb), o_nw = cv.take<uint8_t>(tb), o_nr = cv.take<int64_t>(tb + 1),
-               o_tmp = cv.take<int64_t>(scan_scratch_elems(tb > nchunks ? tb : nchunks));
+  const size_t o_mb = cv.take<uint32_t>(nwords), o_cnt = cv.take<int64_t>(nchunks + 1),
+               o_co = cv.take<int64_t>(nchunks + 1), o_ts = cv.take<int64_t>(tb), o_pt = cv.take<int64_t>(tb),
+               o_ps = cv.take<int64_t>(tb), o_pl = cv.take<int32_t>(tb), o_tc = cv.take<int64_t>(nrt + 1),
+               o_tmp = cv.take<int64_t>(scan_scratch_elems(nchunks));
   if (int rc = it->scratch.ensure(cv.off)) return rc;
+  if ((size_t)tb > it->tnew_cap) {  // owner flags stay zero between batches
+    if (it->tnew) cudaFree(it->tnew);
+    it->tnew = nullptr;
+    it->tnew_cap = 0;
+    SFKV_CUDA(cudaMalloc(&it->tnew, (size_t)tb));
+    SFKV_CUDA(cudaMemsetAsync(it->tnew, 0, (size_t)tb, st));
+    it->tnew_cap = (size_t)tb;
+  }
   char* base = it->scratch.as<char>();
   TokArgs a;
   a.n_req = n_req;
@@ -338,16 +441,18 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   a.n_msg = n_msg;
   a.text = text;
   a.n_bytes = n_bytes;
-  a.mstart = reinterpret_cast<uint8_t*>(base + o_ms);
+  a.mbits = reinterpret_cast<uint32_t*>(base + o_mb);
   a.chunk_off = reinterpret_cast<int64_t*>(base + o_co);
   a.tstart = reinterpret_cast<int64_t*>(base + o_ts);
-  a.tlen = reinterpret_cast<int32_t*>(base + o_tl);
-  a.tslot = reinterpret_cast<int64_t*>(base + o_sl);
-  a.tnew = reinterpret_cast<uint8_t*>(base + o_nw);
-  a.new_rank = reinterpret_cast<int64_t*>(base + o_nr);
+  a.pend_t = reinterpret_cast<int64_t*>(base + o_pt);
+  a.pend_slot = reinterpret_cast<int64_t*>(base + o_ps);
+  a.pend_len = reinterpret_cast<int32_t*>(base + o_pl);
+  a.tnew = it->tnew;
+  a.tile_cnt = reinterpret_cast<int64_t*>(base + o_tc);
   a.tok_off = tok_off;
   a.tok = tok;
   a.n_tokens = n_tokens;
+  a.n_rank_tiles = nrt;
   a.slots = it->slots;
   a.mask = (uint64_t)it->slots_n - 1;
   a.owner = it->owner;
@@ -360,8 +465,8 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   int64_t* counts = reinterpret_cast<int64_t*>(base + o_cnt);
   int64_t* tmp = reinterpret_cast<int64_t*>(base + o_tmp);
   const int sms = sm_count_k();
-  SFKV_CUDA(cudaMemsetAsync(a.mstart, 0, n_bytes + 1, st));
-  SFKV_CUDA(cudaMemsetAsync(it->ctr + 3, 0, sizeof(unsigned long long), st));
+  SFKV_CUDA(cudaMemsetAsync(a.mbits, 0, nwords * sizeof(uint32_t), st));
+  SFKV_CUDA(cudaMemsetAsync(it->ctr + 3, 0, 3 * sizeof(unsigned long long), st));
   if (n_msg > 0) msg_mark_kernel<<<grid_for(n_msg, 256, sms * 4), 256, 0, st>>>(a);
   if (nchunks > 0) chunk_count_kernel<<<(unsigned)nchunks, CHUNK_THREADS, 0, st>>>(a, counts);
   SFKV_LAUNCH_CHECK("msg_mark/chunk_count");
@@ -371,14 +476,16 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   const int g = grid_for(tb, 256, sms * 8);
   tok_probe_kernel<<<g, 256, 0, st>>>(a);
   tok_resolve_kernel<<<g, 256, 0, st>>>(a);
-  SFKV_LAUNCH_CHECK("chunk_emit/probe/resolve");
-  if (int rc = exclusive_scan(NewFlag{a.tnew}, tb, a.new_rank, tmp, st)) return rc;
   tok_check_kernel<<<1, 32, 0, st>>>(a);
-  tok_publish_kernel<<<g, 256, 0, st>>>(a);
+  SFKV_LAUNCH_CHECK("chunk_emit/probe/resolve");
+  rank_count_kernel<<<(unsigned)nrt, 256, 0, st>>>(a);
+  rank_scan_kernel<<<1, 1024, 0, st>>>(a);
+  rank_publish_kernel<<<(unsigned)nrt, 256, 0, st>>>(a);
   tok_final_kernel<<<g, 256, 0, st>>>(a);
   tok_final2_kernel<<<g, 256, 0, st>>>(a);
+  tok_owner_reset_kernel<<<g, 256, 0, st>>>(a);
   tok_commit_kernel<<<1, 32, 0, st>>>(a);
-  SFKV_LAUNCH_CHECK("publish/final");
+  SFKV_LAUNCH_CHECK("rank/publish/final");
   return 0;
 }
 
@@ -393,6 +500,7 @@ static void interner_free(sfkv_interner* it) {
   cudaFree(it->id_off);
   cudaFree(it->id_len);
   cudaFree(it->ctr);
+  cudaFree(it->tnew);
   if (it->ctr_host) cudaFreeHost(it->ctr_host);
   it->scratch.release();
   it->io.release();
@@ -430,8 +538,8 @@ int sfkv_interner_create(int32_t device, int32_t table_log2, int64_t arena_bytes
       (e = cudaMalloc(&it->arena, arena_bytes)) != cudaSuccess ||
       (e = cudaMalloc(&it->id_off, it->max_ids * sizeof(int64_t))) != cudaSuccess ||
       (e = cudaMalloc(&it->id_len, it->max_ids * sizeof(int32_t))) != cudaSuccess ||
-      (e = cudaMalloc(&it->ctr, 4 * sizeof(unsigned long long))) != cudaSuccess ||
-      (e = cudaMallocHost(&it->ctr_host, 4 * sizeof(unsigned long long))) != cudaSuccess ||
+      (e = cudaMalloc(&it->ctr, 8 * sizeof(unsigned long long))) != cudaSuccess ||
+      (e = cudaMallocHost(&it->ctr_host, 8 * sizeof(unsigned long long))) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&it->stream, cudaStreamNonBlocking)) != cudaSuccess) {
     interner_free(it);
     delete it;
@@ -439,7 +547,7 @@ int sfkv_interner_create(int32_t device, int32_t table_log2, int64_t arena_bytes
   }
   it->own_stream = true;
   interner_init_kernel<<<grid_for(it->slots_n, 256, 4096), 256, 0, it->stream>>>(it->slots, it->owner, it->slots_n);
-  cudaMemsetAsync(it->ctr, 0, 4 * sizeof(unsigned long long), it->stream);
+  cudaMemsetAsync(it->ctr, 0, 8 * sizeof(unsigned long long), it->stream);
   if ((e = cudaStreamSynchronize(it->stream)) != cudaSuccess) {
     interner_free(it);
     delete it;
