@@ -1,5 +1,6 @@
 // sf_gpu_replay — the reference's own orchestrator, memory manager and harness loop driving the
-// B200 pool through GpuPinnedBackend (the drop-in). Same wiring as run_benchmark
+// B200 pool through GpuPinnedBackend (the drop-in). With --gpu-memory the reference's
+// MemoryManager is replaced by GpuMemoryManager (policy resolution and the tracker on the B200). Same wiring as run_benchmark
 // (proj/src/harness.cpp:8-116) with GpuPinnedBackend in place of SimulatedBackend. Emits:
 //   {"type":"req", b, wf, stage, P, M}   per dispatch, in dispatch order (M from the GPU)
 //   {"type":"act", ...}                   the memory manager's action log (memory.cpp:389-401)
@@ -8,6 +9,7 @@
 // reference (oracle/ref_shim/replay_driver.cpp) for the same (trace, config).
 #include <fstream>
 
+#include "gpu_memory_manager.hpp"
 #include "gpu_pinned_backend.hpp"
 #include "stageflow/config.hpp"
 #include "stageflow/harness.hpp"
@@ -17,8 +19,15 @@ using namespace stageflow;
 int main(int argc, char** argv) {
   std::string config_path, trace_path, out_path;
   int device = 0;
+  bool gpu_memory = false;
+  for (int i = 1; i < argc; ++i)
+    if (std::string(argv[i]) == "--gpu-memory") gpu_memory = true;
   for (int i = 1; i + 1 < argc; i += 2) {
     std::string a = argv[i];
+    if (a == "--gpu-memory") {
+      --i;
+      continue;
+    }
     if (a == "--config") config_path = argv[i + 1];
     else if (a == "--trace") trace_path = argv[i + 1];
     else if (a == "--out") out_path = argv[i + 1];
@@ -52,8 +61,24 @@ int main(int argc, char** argv) {
   }
   ToolRegistry tools;
   SignalBus bus;
-  MemoryManager memory(config.memory, &registry, log);
-  memory.attach(bus);
+  std::unique_ptr<MemoryManager> cpu_mem;
+  std::unique_ptr<GpuMemoryManager> gpu_mem;
+  if (gpu_memory) {
+    gpu_mem = std::make_unique<GpuMemoryManager>(config.memory, &registry,
+                                                 static_cast<int>(trace.size()) + 8, device, log);
+    gpu_mem->attach(bus);
+  } else {
+    cpu_mem = std::make_unique<MemoryManager>(config.memory, &registry, log);
+    cpu_mem->attach(bus);
+  }
+  auto set_chain = [&](const std::string& wf, const std::vector<std::string>& names) {
+    if (gpu_mem) gpu_mem->set_workflow_chain(wf, names);
+    else cpu_mem->set_workflow_chain(wf, names);
+  };
+  auto pressure_tick = [&](double now) {
+    if (gpu_mem) gpu_mem->pressure_tick(now);
+    else cpu_mem->pressure_tick(now);
+  };
   Orchestrator orch(loop, registry, tools, bus, config.orchestration, log);
 
   std::size_t remaining = trace.size();
@@ -76,7 +101,7 @@ int main(int argc, char** argv) {
     if (!validated.ok()) throw std::runtime_error("invalid workflow from " + r.workflow_template);
     const auto& wf = *validated.workflow;
     if (!wf.spec().workflow_memory_policy.empty())
-      memory.set_workflow_chain(workflow_id, wf.spec().workflow_memory_policy);
+      set_chain(workflow_id, wf.spec().workflow_memory_policy);
     orch.submit_at(static_cast<double>(r.arrival_ms), wf, make_router(config, registry, wf),
                    [&remaining](ExecutionReport) { --remaining; }, r.annotations());
   }
@@ -84,14 +109,14 @@ int main(int argc, char** argv) {
   if (config.memory.monitor_interval_ms > 0) {
     *tick = [&, wp = std::weak_ptr<std::function<void()>>(tick)] {
       if (remaining == 0) return;
-      memory.pressure_tick(loop.now_ms());
+      pressure_tick(loop.now_ms());
       if (auto self = wp.lock()) loop.schedule_in(config.memory.monitor_interval_ms, *self);
     };
     loop.schedule_in(config.memory.monitor_interval_ms, *tick);
   }
   loop.run_until_idle();
 
-  for (const auto& r : memory.action_log()) {
+  for (const auto& r : gpu_mem ? gpu_mem->action_log() : cpu_mem->action_log()) {
     out.push_back({{"type", "act"}, {"trigger", r.trigger}, {"ts", r.ts},
                    {"action", cache_action_kind_name(r.action.kind)},
                    {"workflow", r.action.workflow_id}, {"backend", r.action.backend_ref},

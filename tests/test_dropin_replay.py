@@ -82,16 +82,19 @@ SCENARIOS = {
 }
 
 
+@pytest.mark.parametrize("gpu_memory", [False, True], ids=["ref-memory", "gpu-memory"])
 @pytest.mark.parametrize("name", sorted(SCENARIOS))
-def test_reference_harness_on_gpu_pool_matches_golden(tmp_path, name):
+def test_reference_harness_on_gpu_pool_matches_golden(tmp_path, name, gpu_memory):
+    """gpu-memory: the reference's MemoryManager is replaced by GpuMemoryManager (integration/),
+    so pin cache, policy resolution, tracker and pressure ticks all run on the B200."""
     if not os.path.exists(DRIVER):
         pytest.fail("oracle/_ref/sf_gpu_replay missing: build it where /root/reference exists")
     cfg, trace = SCENARIOS[name]()
     cp, tp, op = tmp_path / "c.json", tmp_path / "t.jsonl", tmp_path / "o.jsonl"
     cp.write_text(json.dumps(cfg))
     tp.write_text("".join(json.dumps(r) + "\n" for r in trace))
-    subprocess.run([DRIVER, "--config", str(cp), "--trace", str(tp), "--out", str(op)],
-                   check=True, timeout=600)
+    subprocess.run([DRIVER, "--config", str(cp), "--trace", str(tp), "--out", str(op)] +
+                   (["--gpu-memory"] if gpu_memory else []), check=True, timeout=600)
     got = [json.loads(l) for l in op.read_text().splitlines()]
     gold = replay.load_stream(name)
 
