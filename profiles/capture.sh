@@ -1,0 +1,19 @@
+#!/bin/bash
+# Profiling recipe for one round (run under gpurun from the repo root; one GPU, never multi-rank):
+#   bash profiles/capture.sh <tag>
+# Outputs into gpurun_out/<tag>/: the bench line, the launch list of a short bench run and full
+# ncu captures of the kernels DESIGN.md reports on (summarised by profiles/ncu_summary.py).
+set -u
+T=${1:-round}
+O=gpurun_out/$T
+mkdir -p $O
+python bench.py > $O/bench.log 2>&1
+tail -1 $O/bench.log > $O/bench_line.json
+B="python bench.py --steps 3 --warmup 1 --no-cpu-baseline"
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $B > /dev/null 2>&1
+Q="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-kv --no-c4"
+ncu --set full --clock-control none --import-source on -k regex:match_block --launch-skip 6 --launch-count 1 -o $O/match_block $Q > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"match_chain_kernel<0>" --launch-skip 6 --launch-count 1 -o $O/match_chain $Q > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:tok_probe --launch-skip 1 --launch-count 1 -o $O/tok_probe $Q > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:sig_resolve --launch-skip 1 --launch-count 1 -o $O/sig_resolve $Q > /dev/null 2>&1
+ls -la $O
