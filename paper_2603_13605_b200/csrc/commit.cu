@@ -430,14 +430,13 @@ __global__ void install_kernel(CommitArgs a) {
     const int64_t k = item - a.s.blk_off[r];
     const int64_t pb = (int64_t)a.wf[r] * a.max_pin_blocks;
     a.pin_blk[pb + k] = a.s.bid[item];
-    // pin-major token copy (zero padded, 32-block groups token-major: consecutive items write
-    // consecutive words), read by the match kernel without indirection
+    // pin-major token copy (zero padded), read by the match kernel without indirection
     const int64_t rem = a.tok_off[r + 1] - a.tok_off[r] - k * BT;
     uint32_t t[BT];
     load_req_block(a, r, k, (int)(rem < BT ? rem : BT), t);
-    uint32_t* dst = a.pin_tok + pin_tok_index(a.wf[r], k, 0, a.pin_groups);
+    uint4* dst = reinterpret_cast<uint4*>(a.pin_tok + pin_tok_index(a.wf[r], k, 0, a.pin_groups));
 #pragma unroll
-    for (int j = 0; j < BT; ++j) dst[j * PIN_TOK_STRIDE] = t[j];
+    for (int i = 0; i < 4; ++i) dst[i] = make_uint4(t[4 * i], t[4 * i + 1], t[4 * i + 2], t[4 * i + 3]);
   }
 }
 

@@ -24,8 +24,9 @@
 //                       boundary, from the request window (one record per lane + a 5-step
 //                       shuffle search). Match mode stages the tile's token range (contiguous in
 //                       the CSR batch) into shared memory with one cp.async.bulk per warp and
-//                       reads it with bank-rotated 16-B loads; the pin's blocks come from the
-//                       token-major pin copy, one or two 128-B lines per warp load. (Lane-per-block
+//                       reads it with bank-rotated 16-B loads; the pin's blocks of each request
+//                       segment (pin-major copy: one extent) arrive by a second bulk copy on the
+//                       same mbarrier phase, so nothing is held in registers across the wait. (Lane-per-block
 //                       16-B global loads are 64 B apart: 16 lines per warp instruction, which
 //                       made L1 the limiter at 81 %.) M: a block whose 16 words all agree with
 //                       the pin's has no mismatch; only differing blocks compute the exact first
@@ -399,6 +400,38 @@ __device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// Pin block of a lane staged at lane * 64 B: rotated 16-B reads (chunk (i + r_L) & 3 with
+// r_L = (L >> 1) & 3 puts a quarter-warp's 8 lanes on distinct bank groups), then un-rotated.
+__device__ __forceinline__ void load_pin_staged(const uint32_t* s, uint32_t* q) {
+  const int lane = threadIdx.x & 31;
+  const int rr = (lane >> 1) & 3;
+  uint4 v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = *reinterpret_cast<const uint4*>(s + lane * BT + 4 * ((i + rr) & 3));
+  uint4 u[4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) u[x] = (rr & 1) ? v[(x + 3) & 3] : v[x];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const uint4 w = (rr & 2) ? u[(x + 2) & 3] : u[x];
+    q[4 * x] = w.x;
+    q[4 * x + 1] = w.y;
+    q[4 * x + 2] = w.z;
+    q[4 * x + 3] = w.w;
+  }
+}
+
 // Block tokens of a lane whose block starts at word o of the staged range (o >= 0).
 __device__ __forceinline__ void load_block_staged(const uint32_t* s, int o, int nval, uint32_t* t) {
   const int lane = threadIdx.x & 31;
@@ -500,9 +533,11 @@ __device__ __forceinline__ void tile_finish(const MatchKernelArgs& K, int64_t ti
 
 // One warp per 32-block tile, one block per lane, non-persistent: enough tiles in flight per SM to
 // cover the window -> tokens/pin-tokens round trips.
+// 5 CTAs (40 warps) per SM: the register cap (48) trades a few spilled bytes for occupancy.
 template <bool STAGED>
-__global__ void __launch_bounds__(MATCH_THREADS) match_block_kernel(MatchKernelArgs K) {
+__global__ void __launch_bounds__(MATCH_THREADS, 5) match_block_kernel(MatchKernelArgs K) {
   __shared__ __align__(128) uint32_t s_tok[STAGED ? MATCH_THREADS / 32 : 1][STAGED ? STAGE_WORDS : 4];
+  __shared__ __align__(128) uint32_t s_pin[STAGED ? MATCH_THREADS / 32 : 1][STAGED ? WT * BT : 4];
   __shared__ __align__(8) uint64_t s_bar[MATCH_THREADS / 32];
   const MatchArgs& A = K.a;
   const int lane = threadIdx.x & 31;
@@ -520,28 +555,41 @@ __global__ void __launch_bounds__(MATCH_THREADS) match_block_kernel(MatchKernelA
   const bool match_mode = A.out_M != nullptr;
   const Ctx c = resolve(K, tile, n_items);
 
-  // the pin's block k (token-major 32-block groups: each load is one or two 128-B lines per
-  // warp), issued before the staging wait so both round trips overlap
   const bool in_pin = match_mode && c.valid && c.pin_len >= 0 && c.k < (c.pin_len + BT - 1) / BT;
   uint32_t q[BT];
-  if (in_pin) {
-    const uint32_t* pp = K.pin_tok + pin_tok_index(c.wf, c.k, 0, K.pin_groups);
-#pragma unroll
-    for (int j = 0; j < BT; ++j) q[j] = __ldg(pp + (j << 5));
-  }
   uint32_t t[BT];
   if constexpr (STAGED) {
-    // the tile's token range: lane 0's block to the end of the last valid lane's 5-chunk window
+    // one mbarrier phase for the tile: its token range (one bulk copy) and, per request segment
+    // of in-pin blocks, that segment's pin blocks (pin-major: one extent, placed at lane * 64 B)
     const int nv = __popc(__ballot_sync(0xffffffffu, c.valid));
     const int64_t a0 = __shfl_sync(0xffffffffu, c.start, 0) & ~int64_t(3);
     const int64_t a1 = __shfl_sync(0xffffffffu, (c.start & ~int64_t(3)) + 20, nv - 1);
-    if (a1 <= (tok_total & ~int64_t(3))) {  // all but the batch's last tile
-      if (lane == 0) bulk_load(s_tok[warp], A.tok + a0, (uint32_t)(a1 - a0) * 4u, &s_bar[warp]);
-      mbar_wait0(&s_bar[warp]);
-      if (c.valid) load_block_staged(s_tok[warp], (int)(c.start - a0), c.nval, t);
-    } else if (c.valid) {
-      load_block(A.tok, c.start, c.nval, tok_total, t);
+    const bool staged = a1 <= (tok_total & ~int64_t(3));  // all but the batch's last tile
+    const unsigned pin_m = __ballot_sync(0xffffffffu, in_pin);
+    const int64_t prev_r = __shfl_up_sync(0xffffffffu, c.r, 1);
+    const bool head = in_pin && (lane == 0 || !((pin_m >> (lane - 1)) & 1u) || prev_r != c.r);
+    const unsigned heads = __ballot_sync(0xffffffffu, head);
+    uint32_t pin_bytes = 0;
+    if (head) {
+      const unsigned after = ~((2u << lane) - 1u);
+      const unsigned stop = (heads | ~pin_m) & after;
+      const int end = stop ? __ffs(stop) - 1 : 32;
+      pin_bytes = (uint32_t)(end - lane) * (BT * 4);
     }
+    const uint32_t total = __reduce_add_sync(0xffffffffu, pin_bytes) + (staged ? (uint32_t)(a1 - a0) * 4u : 0u);
+    if (total) {
+      if (lane == 0) mbar_expect_tx(&s_bar[warp], total);
+      __syncwarp();
+      if (staged && lane == 0) bulk_copy(s_tok[warp], A.tok + a0, (uint32_t)(a1 - a0) * 4u, &s_bar[warp]);
+      if (head) bulk_copy(s_pin[warp] + lane * BT, K.pin_tok + pin_tok_index(c.wf, c.k, 0, K.pin_groups),
+                          pin_bytes, &s_bar[warp]);
+      mbar_wait0(&s_bar[warp]);
+    }
+    if (c.valid) {
+      if (staged) load_block_staged(s_tok[warp], (int)(c.start - a0), c.nval, t);
+      else load_block(A.tok, c.start, c.nval, tok_total, t);
+    }
+    if (in_pin) load_pin_staged(s_pin[warp], q);
   } else if (c.valid) {
     load_block(A.tok, c.start, c.nval, tok_total, t);
   }

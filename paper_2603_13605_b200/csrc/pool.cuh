@@ -2,11 +2,10 @@
 //
 // HBM layout (all arrays device-resident, sized at pool creation):
 //   pins   pin_len[W] i64 (-1 = no pin), pin_nblk[W] i32,
-//          pin_blk[W][MB] i32 (block table), pin_tok[W][G][16][32] u32 with G = ceil(MB/32): the
-//          pin's tokens in groups of 32 blocks, token-major inside a group (word j of block k at
-//          [wf][k/32][j][k%32]), so the match kernel's lanes — consecutive blocks of one pin —
-//          read token j of their blocks in one or two 128-B lines, with no block-id indirection;
-//          the block's chained hash is blk_key[pin_blk]
+//          pin_blk[W][MB] i32 (block table), pin_tok[W][32 G][16] u32 with G = ceil(MB/32): the
+//          pin's tokens block by block (pin-major), so the blocks of one request segment of a
+//          match tile are one contiguous extent that a single bulk copy (TMA) stages, with no
+//          block-id indirection; the block's chained hash is blk_key[pin_blk]
 //   blocks blk_key[B] u64, blk_tok[B][16] u32 (tokens: verify-on-hit for shared blocks),
 //          blk_n[B] u8 (valid tokens), blk_in_table[B] u8, blk_ref[B] u32, blk_slot[B] i64,
 //          free_bits[ceil(B/32)] u32 (1 = free)
@@ -91,9 +90,8 @@ namespace sfkv {
 
 // Word index of token j of pin block k of workflow wf in pin_tok (see the layout above).
 __host__ __device__ __forceinline__ int64_t pin_tok_index(int64_t wf, int64_t k, int j, int64_t groups) {
-  return (((wf * groups + (k >> 5)) * BT + j) << 5) + (k & 31);
+  return ((wf * (groups << 5) + k) << 4) + j;
 }
-constexpr int PIN_TOK_STRIDE = 32;  // words between tokens j and j+1 of a block
 inline int64_t pin_groups(const sfkv_pool_config& c) { return (c.max_pin_blocks + 31) / 32; }
 
 // Outputs of the hashing/matching pass shared by match, lookup and commit.
