@@ -159,7 +159,7 @@ int sfkv_pool_create(const sfkv_pool_config* cfg, sfkv_pool** out) {
   const size_t W = cfg->max_workflows, B = cfg->n_blocks, MB = cfg->max_pin_blocks;
   int rc = 0;
   if ((rc = dalloc(&p->pin_len, W)) || (rc = dalloc(&p->pin_nblk, W)) ||
-      (rc = dalloc(&p->pin_blk, W * MB)) || (rc = dalloc(&p->pin_tok, W * (size_t)pin_groups(*cfg) * 32 * BT)) ||
+      (rc = dalloc(&p->pin_blk, W * MB)) || (rc = dalloc(&p->pin_tok, W * (size_t)pin_groups(*cfg) * 32 * PIN_STRIDE)) ||
       (rc = dalloc(&p->blk_key, B)) || (rc = dalloc(&p->blk_tok, B * BT)) ||
       (rc = dalloc(&p->blk_n, B)) || (rc = dalloc(&p->blk_in_table, B)) ||
       (rc = dalloc(&p->blk_ref, B)) || (rc = dalloc(&p->blk_slot, B)) ||

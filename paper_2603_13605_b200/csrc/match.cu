@@ -411,10 +411,21 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-// Pin block of a lane staged at lane * 64 B: rotated 16-B reads (chunk (i + r_L) & 3 with
-// r_L = (L >> 1) & 3 puts a quarter-warp's 8 lanes on distinct bank groups), then un-rotated.
+// Pin block of a lane staged at lane * PIN_STRIDE words. With the padded 80-B stride the 8 lanes of
+// a quarter-warp read 8 distinct bank groups: plain 16-B loads. (The unpadded 64-B stride needs a
+// per-lane chunk rotation and two select stages to undo it.)
 __device__ __forceinline__ void load_pin_staged(const uint32_t* s, uint32_t* q) {
   const int lane = threadIdx.x & 31;
+#if SFKV_PIN_PAD
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const uint4 w = *reinterpret_cast<const uint4*>(s + lane * PIN_STRIDE + 4 * x);
+    q[4 * x] = w.x;
+    q[4 * x + 1] = w.y;
+    q[4 * x + 2] = w.z;
+    q[4 * x + 3] = w.w;
+  }
+#else
   const int rr = (lane >> 1) & 3;
   uint4 v[4];
 #pragma unroll
@@ -430,6 +441,7 @@ __device__ __forceinline__ void load_pin_staged(const uint32_t* s, uint32_t* q) 
     q[4 * x + 2] = w.z;
     q[4 * x + 3] = w.w;
   }
+#endif
 }
 
 // Block tokens of a lane whose block starts at word o of the staged range (o >= 0).
@@ -537,7 +549,7 @@ __device__ __forceinline__ void tile_finish(const MatchKernelArgs& K, int64_t ti
 template <bool STAGED>
 __global__ void __launch_bounds__(MATCH_THREADS, 5) match_block_kernel(MatchKernelArgs K) {
   __shared__ __align__(128) uint32_t s_tok[STAGED ? MATCH_THREADS / 32 : 1][STAGED ? STAGE_WORDS : 4];
-  __shared__ __align__(128) uint32_t s_pin[STAGED ? MATCH_THREADS / 32 : 1][STAGED ? WT * BT : 4];
+  __shared__ __align__(128) uint32_t s_pin[STAGED ? MATCH_THREADS / 32 : 1][STAGED ? WT * PIN_STRIDE : 4];
   __shared__ __align__(8) uint64_t s_bar[MATCH_THREADS / 32];
   const MatchArgs& A = K.a;
   const int lane = threadIdx.x & 31;
@@ -574,14 +586,14 @@ __global__ void __launch_bounds__(MATCH_THREADS, 5) match_block_kernel(MatchKern
       const unsigned after = ~((2u << lane) - 1u);
       const unsigned stop = (heads | ~pin_m) & after;
       const int end = stop ? __ffs(stop) - 1 : 32;
-      pin_bytes = (uint32_t)(end - lane) * (BT * 4);
+      pin_bytes = (uint32_t)(end - lane) * (PIN_STRIDE * 4);
     }
     const uint32_t total = __reduce_add_sync(0xffffffffu, pin_bytes) + (staged ? (uint32_t)(a1 - a0) * 4u : 0u);
     if (total) {
       if (lane == 0) mbar_expect_tx(&s_bar[warp], total);
       __syncwarp();
       if (staged && lane == 0) bulk_copy(s_tok[warp], A.tok + a0, (uint32_t)(a1 - a0) * 4u, &s_bar[warp]);
-      if (head) bulk_copy(s_pin[warp] + lane * BT, K.pin_tok + pin_tok_index(c.wf, c.k, 0, K.pin_groups),
+      if (head) bulk_copy(s_pin[warp] + lane * PIN_STRIDE, K.pin_tok + pin_tok_index(c.wf, c.k, 0, K.pin_groups),
                           pin_bytes, &s_bar[warp]);
       mbar_wait0(&s_bar[warp]);
     }

@@ -88,9 +88,13 @@ struct sfkv_pool {
 
 namespace sfkv {
 
+#ifndef SFKV_PIN_PAD
+#define SFKV_PIN_PAD 1
+#endif
+constexpr int PIN_STRIDE = SFKV_PIN_PAD ? 20 : 16;  // words per pin block (16 tokens + padding)
 // Word index of token j of pin block k of workflow wf in pin_tok (see the layout above).
 __host__ __device__ __forceinline__ int64_t pin_tok_index(int64_t wf, int64_t k, int j, int64_t groups) {
-  return ((wf * (groups << 5) + k) << 4) + j;
+  return (wf * (groups << 5) + k) * PIN_STRIDE + j;
 }
 inline int64_t pin_groups(const sfkv_pool_config& c) { return (c.max_pin_blocks + 31) / 32; }
 
