@@ -99,6 +99,7 @@ static void pool_free(sfkv_pool* p) {
   p->scratch.release();
   p->small.release();
   p->io.release();
+  p->prep_status.release();
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   delete p;
 }

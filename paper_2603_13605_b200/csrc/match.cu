@@ -131,9 +131,17 @@ struct PrepArgs {
   TileRec* trec;      // out
   int64_t* out_M;     // nullable: min(P, pin_len) or 0
   int64_t* out_hit;   // nullable: 16 * blocks
-  unsigned long long* ticket;
-  uint64_t* pstatus;  // prep tile status (zeroed by the host)
+  unsigned long long* ticket;  // null: CTAs are co-resident, blockIdx order
+  uint64_t* pstatus;  // prep tile status (epoch-tagged, per-pool buffer)
+  uint32_t epoch;
 };
+
+// Prep look-back status: flag (2 bits) | launch epoch (14 bits) | block count (48 bits). Statuses
+// live in a per-pool buffer that nothing else writes, so a status is current iff its epoch is
+// this launch's: no memset between launches (the host clears the buffer when the epoch wraps).
+constexpr int PE_SHIFT = 48;
+constexpr uint64_t PE_SUM = (1ull << PE_SHIFT) - 1;
+constexpr uint64_t PE_FLAG = 3ull << 62;
 
 __global__ void __launch_bounds__(PREP_THREADS) match_prep_kernel(PrepArgs P) {
   using BS = cub::BlockScan<int64_t, PREP_THREADS>;
@@ -141,41 +149,45 @@ __global__ void __launch_bounds__(PREP_THREADS) match_prep_kernel(PrepArgs P) {
   __shared__ int64_t s_tile, s_prefix;
   pdl_trigger();
   const int tid = threadIdx.x;
-  if (tid == 0) s_tile = (int64_t)atomicAdd(P.ticket, 1ull);
+  // With every prep CTA co-resident (the usual case) the launch order is the tile order; a
+  // ticket (zeroed by the host) orders CTAs otherwise, so a predecessor is always running.
+  if (tid == 0) s_tile = P.ticket ? (int64_t)atomicAdd(P.ticket, 1ull) : (int64_t)blockIdx.x;
   __syncthreads();
   const int64_t tile = s_tile;
   const int64_t r = tile * PREP_TILE + tid;
   const int64_t len = r < P.n ? P.tok_off[r + 1] - P.tok_off[r] : 0;
-  const int64_t nb = (len + BT - 1) / BT;
   int32_t wf = 0;
   int64_t pl = -1;
   if (P.wf && r < P.n) {  // issued before the scan: the dependent pin_len load overlaps it
     wf = P.wf[r];
     pl = P.pin_len[wf];
   }
+  const int64_t nb = (len + BT - 1) / BT;
   int64_t excl, total;
   BS(tmp).ExclusiveSum(nb, excl, total);
   if (tid < 32) {  // warp 0: publish, then look back 32 predecessor tiles per read
     const int lane = tid;
-    if (lane == 0) st_status(P.pstatus + tile, (tile == 0 ? ST_INCL : ST_AGG) | (uint64_t)total);
+    const uint64_t ep = (uint64_t)P.epoch << PE_SHIFT;
+    if (lane == 0) st_status(P.pstatus + tile, (tile == 0 ? ST_INCL : ST_AGG) | ep | (uint64_t)total);
     uint64_t prefix = 0;
     for (int64_t base = tile - 1; base >= 0; base -= 32) {
       const int64_t p = base - lane;
       uint64_t s;
       unsigned incl;
       int first;
-      for (;;) {  // predecessors hold earlier tickets, so they are running: plain spin
-        s = p >= 0 ? ld_status(P.pstatus + p) : ST_INCL;
-        incl = __ballot_sync(0xffffffffu, (s & ~CHAIN_MASK) == ST_INCL);
+      for (;;) {  // predecessors run (co-resident, or earlier tickets): plain spin
+        s = p >= 0 ? ld_status(P.pstatus + p) : (ST_INCL | ep);
+        const bool cur = (s & ~(PE_FLAG | PE_SUM)) == ep && (s & PE_FLAG);
+        incl = __ballot_sync(0xffffffffu, cur && (s & PE_FLAG) == ST_INCL);
         first = incl ? __ffs(incl) - 1 : 31;
         const unsigned need = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
-        if ((__ballot_sync(0xffffffffu, s != 0) & need) == need) break;
+        if ((__ballot_sync(0xffffffffu, cur) & need) == need) break;
       }
-      prefix += warp_sum(lane <= first ? (s & CHAIN_MASK) : 0ull);
+      prefix += warp_sum(lane <= first ? (s & PE_SUM) : 0ull);
       if (incl) break;
     }
     if (lane == 0) {
-      if (tile > 0) st_status(P.pstatus + tile, ST_INCL | (prefix + (uint64_t)total));
+      if (tile > 0) st_status(P.pstatus + tile, ST_INCL | ep | (prefix + (uint64_t)total));
       s_prefix = (int64_t)prefix;
     }
   }
@@ -735,7 +747,6 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   const int64_t ntiles = (a.n_items + WT - 1) / WT;
   const int64_t np = prep_tiles(a.n);
   unsigned long long* ticket = reinterpret_cast<unsigned long long*>(tile_state);
-  uint64_t* pstatus = reinterpret_cast<uint64_t*>(tile_state + 1);
   uint64_t* status = reinterpret_cast<uint64_t*>(tile_state + 1 + np);
   const int64_t th = tile_head(np, ntiles);
   TileRec* trec = reinterpret_cast<TileRec*>(tile_state + th);
@@ -744,7 +755,28 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   uint64_t* local = reinterpret_cast<uint64_t*>(tile_state + head + 4 * (a.n + 1));
   uint32_t* rk = reinterpret_cast<uint32_t*>(tile_state + head + 4 * (a.n + 1) + a.n_items);
 
-  SFKV_CUDA(cudaMemsetAsync(tile_state, 0, sizeof(int64_t) * (1 + np), st));
+  // prep statuses: a per-pool buffer, epoch-tagged (cleared only when it grows or the epoch wraps)
+  const size_t need = sizeof(uint64_t) * (size_t)(np + 1);
+  if (p->prep_status.bytes < need) {
+    if (int rc = p->prep_status.ensure(need)) return rc;
+    SFKV_CUDA(cudaMemsetAsync(p->prep_status.ptr, 0, p->prep_status.bytes, st));
+    p->prep_epoch = 0;
+  }
+  p->prep_epoch = (p->prep_epoch + 1) & 0x3FFF;
+  if (p->prep_epoch == 0) {
+    SFKV_CUDA(cudaMemsetAsync(p->prep_status.ptr, 0, p->prep_status.bytes, st));
+    p->prep_epoch = 1;
+  }
+  static int prep_resident = 0;  // prep CTAs that can be resident at once (same for every pool)
+  if (!prep_resident) {
+    int per_sm = 0, dev = 0, sms = 0;
+    SFKV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, match_prep_kernel, PREP_THREADS, 0));
+    SFKV_CUDA(cudaGetDevice(&dev));
+    SFKV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    prep_resident = per_sm * sms;
+  }
+  const bool use_ticket = np > prep_resident / 2;  // leave room for co-running kernels
+  if (use_ticket) SFKV_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st));
   PrepArgs P;
   P.n = a.n;
   P.tok_off = a.tok_off;
@@ -755,8 +787,9 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   P.trec = trec;
   P.out_M = a.out_M;
   P.out_hit = a.out_hit;
-  P.ticket = ticket;
-  P.pstatus = pstatus;
+  P.ticket = use_ticket ? ticket : nullptr;
+  P.pstatus = p->prep_status.as<uint64_t>();
+  P.epoch = p->prep_epoch;
   match_prep_kernel<<<(unsigned)np, PREP_THREADS, 0, st>>>(P);
   SFKV_LAUNCH_CHECK("match_prep_kernel");
   if (ntiles == 0) return 0;

@@ -82,6 +82,8 @@ struct sfkv_pool {
   sfkv::Scratch scratch;       // per-call device scratch
   sfkv::Scratch small;         // per-call offsets (sized by request count)
   sfkv::Scratch io;            // device copies of host-pointer inputs/outputs
+  sfkv::Scratch prep_status;   // match prep look-back statuses (epoch-tagged)
+  uint32_t prep_epoch = 0;
   void* host_stage = nullptr;  // pinned host staging
   size_t host_stage_bytes = 0;
 };
