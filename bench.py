@@ -10,10 +10,15 @@ sfkv_match_batch_dev (chained block hashing + exact LCP against each workflow's 
 reference's SimulatedBackend::prefix_match, simulated_backend.cpp:153-162) over ~1.9M blocks.
 
   value  = blocks looked up per second, inputs resident in HBM, L2 flushed between steps
-  e2e    = the same through the host-pointer C ABI (sfkv_match_batch): H2D of the batch from
-           pinned memory + D2H of M inside the timed region
+           (M + the chained hash of every block: SURVEY §8 K1+K2, the keys the commit needs)
+  m_only = the same with M only (exactly prefix_match's output; what e2e computes)
+  e2e    = M through the host-pointer C ABI (sfkv_match_batch): H2D of the batch from
+           pinned memory + D2H of M inside the timed region (PCIe-bound)
   kv     = payload legs on a 64 GiB Llama-3-8B-shaped pool: gather of retained pins into
            contiguous staging and a stage commit (copy-on-share + scatter of appended tokens)
+  c4_long_context / c5_lookup = BASELINE configs[3] / configs[4] legs; c3_handoff (N > 1) =
+           configs[2]: every GPU pulls its predecessor's retained contexts over NVLink
+  mm_signals / tokenize = SURVEY §8f-1 / §8f-2 legs (batched MemoryManager, tokenizer+interner)
   roofline / cpu_baseline / clocks / gpu_launches per the driver contract.
 
 --impl reference runs the reference's own prefix_match (oracle/_ref/libsfref.so, compiled from
@@ -340,6 +345,25 @@ def run_ours(args, rank, world, local_rank):
         ms = sfdist.max_over_ranks(local_ms, dev)  # max over ranks (NCCL all-reduce)
         value = sfdist.aggregate_rate(req_blocks, local_ms, dev)  # sum of blocks / max time
 
+        # ---- M only (the reference's prefix_match output, no chained hashes) ---------------
+        def m_only_step():
+            api.check("match_dev", api.match_batch_dev(pool.h, n, C.c_void_p(d_wf.data_ptr()),
+                      C.c_void_p(d_off.data_ptr()), C.c_void_p(d_tok.data_ptr()), n_tokens,
+                      C.c_void_p(d_M.data_ptr()), None))
+        for _ in range(args.warmup):
+            l2.zero_()
+            m_only_step()
+        mo_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                 for _ in range(args.steps)]
+        for s_ in range(args.steps):
+            l2.zero_()
+            mo_ev[s_][0].record(stream)
+            m_only_step()
+            mo_ev[s_][1].record(stream)
+        torch.cuda.synchronize()
+        assert (d_M.cpu().numpy() == wl["expect_M"]).all()
+        mo_ms = sfdist.max_over_ranks(float(np.mean([a.elapsed_time(b) for a, b in mo_ev])), dev)
+
         # ---- e2e through the host-pointer C ABI (pinned host buffers) --------------------
         h_wf = torch.from_numpy(wf_all).pin_memory().numpy()
         h_off = torch.from_numpy(wl["req_off"]).pin_memory().numpy()
@@ -386,6 +410,11 @@ def run_ours(args, rank, world, local_rank):
             "peak_source": peak_src, "alg_bytes_per_step": alg_bytes,
             "alg_bytes_per_block": alg_bytes / req_blocks,
             "traffic": args.traffic}
+    mo_bytes = 64 * req_blocks + 68 * int(base_blocks.sum()) + 60 * n
+    m_only = {"what": "M only (no chained hashes): the reference prefix_match's output, as e2e",
+              "ms": mo_ms, "blocks_per_s": req_blocks / (mo_ms / 1e3) * world,
+              "alg_bytes_per_step": mo_bytes,
+              "frac_of_hbm": mo_bytes / (mo_ms / 1e3) / 1e9 / hbm_peak}
     line = {"metric": METRIC, "value": value, "unit": "blocks/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
@@ -395,7 +424,8 @@ def run_ours(args, rank, world, local_rank):
             "e2e": {"value": e2e_value, "unit": "blocks/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "ms_per_step": e2e_ms},
-            "gpu_launches": 2 * args.steps,  # match_prep_kernel + match_kernel per step
+            "gpu_launches": 3 * args.steps,  # match_prep + match_block + match_chain per step
+            "m_only": m_only,
             "clocks": clocks,
             "step_ms_min_max": [min(step_ms), max(step_ms)]}
     if kv:

@@ -57,7 +57,10 @@ constexpr int MATCH_THREADS = 256;
 #endif
 constexpr int CH_TPW_HASH = SFKV_CH_TPW_HASH;
 constexpr int CH_TPW_LOOKUP = 4;
-constexpr int PREP_THREADS = 256;
+#ifndef SFKV_PREP_THREADS
+#define SFKV_PREP_THREADS 256
+#endif
+constexpr int PREP_THREADS = SFKV_PREP_THREADS;
 constexpr int PREP_TILE = PREP_THREADS;
 
 constexpr uint64_t ST_AGG = 1ull << 62;
