@@ -14,8 +14,9 @@
 //                       at a time (__vcmpeq4 / __vcmpleu4), start = non-space & (prev space |
 //                       message start)
 //   exclusive scan      over chunks
-//   chunk_emit_kernel   CTA scan inside each chunk: token start positions, in order
-//   tok_probe_kernel    per token: length, key, probe. Tokens of <= 7 bytes key on their own bytes
+//   chunk_emit_kernel   CTA scan inside each chunk: token start positions, in order; the chunk (+256 B)
+//                       is staged in shared memory and every token is probed right there: length,
+//                       key, probe. Tokens of <= 7 bytes key on their own bytes
 //                       (exact); longer ones on a 63-bit hash verified against the arena. A string
 //                       published by an earlier batch resolves here; claims (CAS into an empty
 //                       slot + atomicMin(position): the lowest position owns the new string) and
@@ -166,76 +167,142 @@ struct ChunkCount {
   __device__ int64_t operator()(int64_t c) const { return counts[c]; }
 };
 
-__global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
-  using BS = cub::BlockScan<int, CHUNK_THREADS>;
-  __shared__ typename BS::TempStorage tmp;
-  const int64_t base = (int64_t)blockIdx.x * CHUNK + (int64_t)threadIdx.x * 16;
-  uint32_t m = start_mask16(a, base);
-  int excl;
-  BS(tmp).ExclusiveSum(__popc(m), excl);
-  int64_t o = a.chunk_off[blockIdx.x] + excl;
-  while (m) {
-    const int j = __ffs(m) - 1;
-    m &= m - 1;
-    a.tstart[o++] = base + j;
-  }
-}
-
 __device__ __forceinline__ bool bytes_equal(const uint8_t* x, const uint8_t* y, int len) {
   for (int i = 0; i < len; ++i)
     if (x[i] != y[i]) return false;
   return true;
 }
-
 __device__ __forceinline__ bool is_mstart(const TokArgs& a, int64_t i) {
   return (a.mbits[i >> 5] >> (i & 31)) & 1u;
 }
+__device__ void probe_token(const TokArgs& a, int64_t t, const uint8_t* p, int len);
+__device__ void probe_key(const TokArgs& a, int64_t t, unsigned long long key, const uint8_t* p, int len);
 
-// Per token: length, key, probe. Published strings resolve here (short keys exactly, long keys
-// verified against the arena); claims and duplicates of this batch's new strings go to the
-// pending list.
-__global__ void tok_probe_kernel(TokArgs a) {
-  const int64_t nt = *a.n_tokens;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = a.tstart[t];
-    int64_t e = s + 1;
-    while (e < a.n_bytes && !is_space(a.text[e]) && !is_mstart(a, e)) ++e;
-    const int len = (int)(e - s);
-    const uint8_t* mine = a.text + s;
-    const unsigned long long key = tok_key(mine, len);
-    uint64_t sl = mix64(key) & a.mask;  // short keys are raw bytes: spread them before placing
-    int64_t found = -1;
-    uint32_t id = TOK_PENDING;
-    for (uint64_t probes = 0; probes <= a.mask; ++probes) {
-      TSlot* p = a.slots + sl;
-      unsigned long long k = p->key;
-      if (k == 0) {
-        k = atomicCAS(&p->key, 0ull, key);
-        if (k == 0) k = key;  // claimed: its id stays TOK_PENDING until published
-      }
-      if (k == key) {
-        found = (int64_t)sl;
-        id = *(volatile uint32_t*)&p->id;
-        break;
-      }
-      sl = (sl + 1) & a.mask;
-    }
-    if (found < 0) {
-      atomicOr(a.ctr + 2, (unsigned long long)TERR_TABLE);
-      continue;
-    }
-    if (id != TOK_PENDING) {  // published before this batch
-      if (!(key >> 63) && (a.id_len[id] != len || !bytes_equal(mine, a.arena + a.id_off[id], len)))
-        atomicOr(a.ctr + 2, (unsigned long long)TERR_COLLISION);
-      a.tok[t] = id;
-      continue;
-    }
-    atomicMin(reinterpret_cast<unsigned long long*>(a.owner + found), (unsigned long long)t);
-    const unsigned long long j = atomicAdd(a.ctr + 4, 1ull);
-    a.pend_t[j] = t;
-    a.pend_slot[j] = found;
-    a.pend_len[j] = len;
+// Token starts of the chunk in order (CTA scan), and every token probed right here: the chunk's
+// 4 KiB plus OVER bytes of the next chunk and their message-start bits are staged in shared memory,
+// so a token's end, key and probe need no second pass over the text (tokens running past the
+// staged window fall back to global reads).
+constexpr int OVER = 256;
+__global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
+  using BS = cub::BlockScan<int, CHUNK_THREADS>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ __align__(16) uint8_t sb[CHUNK + OVER];
+  __shared__ uint32_t sbits[(CHUNK + OVER) / 32];
+  const int64_t c0 = (int64_t)blockIdx.x * CHUNK;
+  const int64_t base = c0 + (int64_t)threadIdx.x * 16;
+  const int64_t lim = a.n_bytes - c0;  // valid staged bytes: [0, min(lim, CHUNK + OVER))
+  // stage bytes (16 B per thread, OVER / 16 threads take the overflow) and bits
+  if (base + 16 <= a.n_bytes) {
+    *reinterpret_cast<uint4*>(sb + threadIdx.x * 16) = __ldg(reinterpret_cast<const uint4*>(a.text + base));
+  } else {
+    for (int j = 0; j < 16; ++j) sb[threadIdx.x * 16 + j] = base + j < a.n_bytes ? a.text[base + j] : ' ';
   }
+  if (threadIdx.x < OVER / 16) {
+    const int64_t ob = c0 + CHUNK + threadIdx.x * 16;
+    if (ob + 16 <= a.n_bytes) {
+      *reinterpret_cast<uint4*>(sb + CHUNK + threadIdx.x * 16) = __ldg(reinterpret_cast<const uint4*>(a.text + ob));
+    } else {
+      for (int j = 0; j < 16; ++j) sb[CHUNK + threadIdx.x * 16 + j] = ob + j < a.n_bytes ? a.text[ob + j] : ' ';
+    }
+  }
+  if (threadIdx.x < (CHUNK + OVER) / 32) {
+    const int64_t w = (c0 >> 5) + threadIdx.x;
+    sbits[threadIdx.x] = (c0 + threadIdx.x * 32 < a.n_bytes) ? a.mbits[w] : 0xffffffffu;
+  }
+  uint32_t m = start_mask16(a, base);
+  int excl;
+  BS(tmp).ExclusiveSum(__popc(m), excl);  // (its barrier also publishes the staged bytes)
+  int64_t t = a.chunk_off[blockIdx.x] + excl;
+  const int stage_end = (int)(lim < CHUNK + OVER ? lim : CHUNK + OVER);
+  if (!m) return;
+  // token boundaries (space or message start) for the 64 staged bytes from this thread's window:
+  // a token's end is one find-first-set away (no per-byte loop)
+  const int w0 = threadIdx.x * 16;
+  unsigned long long bnd = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 v = *reinterpret_cast<const uint4*>(sb + w0 + 16 * q);
+    const uint32_t sp = space_mask4(v.x) | (space_mask4(v.y) << 4) | (space_mask4(v.z) << 8) |
+                        (space_mask4(v.w) << 12);
+    bnd |= (unsigned long long)sp << (16 * q);
+  }
+  {  // message starts: 64 bits from bit offset w0 (w0 is a multiple of 16)
+    const int wi = w0 >> 5, sh = w0 & 31;
+    const unsigned long long lo = sbits[wi] | ((unsigned long long)sbits[wi + 1] << 32);
+    const unsigned long long hi = sbits[wi + 2];
+    bnd |= sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+  }
+  const bool window_is_text_end = stage_end - w0 <= 64 && stage_end == lim;
+  if (stage_end - w0 < 64) bnd |= ~0ull << (stage_end - w0);  // nothing staged past stage_end
+  while (m) {
+    const int j = __ffs(m) - 1;
+    m &= m - 1;
+    const int s0 = w0 + j;  // chunk-relative start
+    a.tstart[t] = c0 + s0;
+    const unsigned long long rest = bnd >> (j + 1);  // boundaries after the start
+    const int span = rest ? __ffsll((long long)rest) : 64 - j;  // token length if found here
+    if (rest && (w0 + j + span < stage_end || window_is_text_end)) {
+      const int len = span;
+      if (len <= 7) {  // exact short key from two aligned 8-B shared loads
+        const int a8 = s0 & ~7, b8 = (s0 & 7) * 8;
+        const unsigned long long lo = *reinterpret_cast<const unsigned long long*>(sb + a8);
+        const unsigned long long hi = *reinterpret_cast<const unsigned long long*>(sb + a8 + 8);
+        unsigned long long raw = b8 ? (lo >> b8) | (hi << (64 - b8)) : lo;
+        raw &= (1ull << (8 * len)) - 1;
+        probe_key(a, t, (1ull << 63) | ((unsigned long long)len << 56) | raw, sb + s0, len);
+      } else {
+        probe_token(a, t, sb + s0, len);
+      }
+    } else {  // the token runs past the staged window: finish it from global memory
+      int64_t g = c0 + s0 + 1;
+      while (g < a.n_bytes && !is_space(a.text[g]) && !is_mstart(a, g)) ++g;
+      probe_token(a, t, a.text + c0 + s0, (int)(g - (c0 + s0)));
+    }
+    ++t;
+  }
+}
+
+// Probe one token (bytes p[0..len), position t): published strings resolve here (short keys
+// exactly, long keys verified against the arena); claims and duplicates of this batch's new
+// strings go to the pending list.
+__device__ void probe_key(const TokArgs& a, int64_t t, unsigned long long key, const uint8_t* p, int len);
+__device__ void probe_token(const TokArgs& a, int64_t t, const uint8_t* p, int len) {
+  probe_key(a, t, tok_key(p, len), p, len);
+}
+
+__device__ void probe_key(const TokArgs& a, int64_t t, unsigned long long key, const uint8_t* p, int len) {
+  uint64_t sl = mix64(key) & a.mask;  // short keys are raw bytes: spread them before placing
+  int64_t found = -1;
+  uint32_t id = TOK_PENDING;
+  for (uint64_t probes = 0; probes <= a.mask; ++probes) {
+    TSlot* q = a.slots + sl;
+    unsigned long long k = q->key;
+    if (k == 0) {
+      k = atomicCAS(&q->key, 0ull, key);
+      if (k == 0) k = key;  // claimed: its id stays TOK_PENDING until published
+    }
+    if (k == key) {
+      found = (int64_t)sl;
+      id = *(volatile uint32_t*)&q->id;
+      break;
+    }
+    sl = (sl + 1) & a.mask;
+  }
+  if (found < 0) {
+    atomicOr(a.ctr + 2, (unsigned long long)TERR_TABLE);
+    return;
+  }
+  if (id != TOK_PENDING) {  // published before this batch
+    if (!(key >> 63) && (a.id_len[id] != len || !bytes_equal(p, a.arena + a.id_off[id], len)))
+      atomicOr(a.ctr + 2, (unsigned long long)TERR_COLLISION);
+    a.tok[t] = id;
+    return;
+  }
+  atomicMin(reinterpret_cast<unsigned long long*>(a.owner + found), (unsigned long long)t);
+  const unsigned long long j = atomicAdd(a.ctr + 4, 1ull);
+  a.pend_t[j] = t;
+  a.pend_slot[j] = found;
+  a.pend_len[j] = len;
 }
 
 // Pending tokens: the lowest position owns a new string; the others are duplicates (long keys
@@ -474,7 +541,6 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   if (nchunks > 0) chunk_emit_kernel<<<(unsigned)nchunks, CHUNK_THREADS, 0, st>>>(a);
   copy_count_kernel<<<1, 1, 0, st>>>(a.chunk_off, nchunks, n_tokens);
   const int g = grid_for(tb, 256, sms * 8);
-  tok_probe_kernel<<<g, 256, 0, st>>>(a);
   tok_resolve_kernel<<<g, 256, 0, st>>>(a);
   tok_check_kernel<<<1, 32, 0, st>>>(a);
   SFKV_LAUNCH_CHECK("chunk_emit/probe/resolve");
