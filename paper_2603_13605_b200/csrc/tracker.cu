@@ -206,7 +206,7 @@ __device__ void sort_segment(int32_t* x, int64_t c) {
   }
 }
 
-__global__ void __launch_bounds__(128) sig_resolve_kernel(SigArgs a, TrackerView v) {
+__global__ void __launch_bounds__(32) sig_resolve_kernel(SigArgs a, TrackerView v) {
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= v.W) return;
   const int32_t c = v.cnt[w];
@@ -224,15 +224,36 @@ __global__ void __launch_bounds__(128) sig_resolve_kernel(SigArgs a, TrackerView
   int64_t lt = v.last_tokens[w];
   int32_t clen = v.chain_len[w];
   bool failed = false;
+  // signal fields are prefetched one signal ahead, so the next signal's loads overlap this one's
+  // resolution (each workflow's signals are a sequential dependency chain)
+  struct Sig {
+    int64_t i, T;
+    int32_t s, b, m;
+    uint8_t kind, ov;
+  };
+  auto load = [&](int64_t i) {
+    Sig x;
+    x.i = i;
+    x.kind = a.s.kind[i];
+    x.s = a.s.stage[i];
+    x.b = a.s.backend[i];
+    x.m = a.s.model[i];
+    x.T = a.s.tokens[i];
+    x.ov = a.s.override_ ? a.s.override_[i] : O_NONE;
+    return x;
+  };
+  Sig nx = load(seg[0]);
   for (int32_t q = 0; q < c; ++q) {
-    const int64_t i = seg[q];
-    const uint8_t kind = a.s.kind[i];
+    const Sig cur = nx;
+    if (q + 1 < c) nx = load(seg[q + 1]);
+    const int64_t i = cur.i;
+    const uint8_t kind = cur.kind;
     const bool wfc = kind == K_WF_COMPLETE;
-    const int32_t s = wfc ? 0 : a.s.stage[i];
-    const int32_t b = wfc ? -1 : a.s.backend[i];
-    const int32_t m = wfc ? -1 : a.s.model[i];
-    const int64_t T = wfc ? 0 : a.s.tokens[i];
-    const uint8_t ov = a.s.override_ ? a.s.override_[i] : O_NONE;
+    const int32_t s = wfc ? 0 : cur.s;
+    const int32_t b = wfc ? -1 : cur.b;
+    const int32_t m = wfc ? -1 : cur.m;
+    const int64_t T = wfc ? 0 : cur.T;
+    const uint8_t ov = wfc ? O_NONE : cur.ov;
     a.r.count[i] = 0;
     if (failed) {
       a.r.status[i] = SFMM_SIG_SKIPPED;
@@ -408,7 +429,7 @@ static int on_signals_dev(sfmm_tracker* t, int64_t n, const sfmm_signals& s, con
   if (int rc = exclusive_scan(CntOf{t->cnt}, t->W, a.seg_off, reinterpret_cast<int64_t*>(base + o_tmp), st))
     return rc;
   sig_scatter_kernel<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(a);
-  sig_resolve_kernel<<<(unsigned)((t->W + 127) / 128), 128, 0, st>>>(a, v);
+  sig_resolve_kernel<<<(unsigned)((t->W + 31) / 32), 32, 0, st>>>(a, v);  // spread over every SM
   SFKV_LAUNCH_CHECK("sig_scatter/resolve");
   return 0;
 }
@@ -563,6 +584,9 @@ int sfmm_set_workflow_ranks(sfmm_tracker* t, int64_t n, const uint32_t* rank) {
 int sfmm_on_signal_batch_dev(sfmm_tracker* t, int64_t n, const sfmm_signals* sig, const sfmm_records* out) {
   if (!t || !sig || !out || n < 0) return fail(SFKV_EINVAL, "on_signal_batch_dev: bad argument");
   if (n > INT32_MAX) return fail(SFKV_EINVAL, "on_signal_batch_dev: batch too large");
+  if (n > 0 && (!sig->kind || !sig->wf || !sig->stage || !sig->backend || !sig->model || !sig->tokens ||
+                !sig->ts || !out->count || !out->status || !out->kind || !out->backend || !out->reason))
+    return fail(SFKV_EINVAL, "on_signal_batch_dev: null array (only override_ may be null)");
   DeviceGuard g(t->cfg.device);
   return on_signals_dev(t, n, *sig, *out);
 }
