@@ -25,6 +25,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 }
 
 __global__ void __launch_bounds__(1024) scan_tiles_kernel(int64_t* tile_sums, int64_t ntiles) {
+  pdl_enter();
   using BS = cub::BlockScan<int64_t, 1024>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ int64_t carry;

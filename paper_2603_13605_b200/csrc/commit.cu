@@ -113,6 +113,7 @@ __device__ __forceinline__ bool blk_tokens_equal(const uint32_t* __restrict__ bl
 
 // ---- admission: one warp, exact reference order ----------------------------------------
 __global__ void admit_kernel(CommitArgs a) {
+  pdl_enter();
   const int lane = threadIdx.x;
   DevCounters* c = a.ctr;
   if (lane == 0) {
@@ -180,6 +181,7 @@ __global__ void admit_kernel(CommitArgs a) {
 
 // ---- probe / claim ---------------------------------------------------------------------
 __global__ void probe_kernel(CommitArgs a) {
+  pdl_enter();
   if (a.ctr->error) return;
   FOR_ITEMS(a, item) {
     int64_t r, k;
@@ -221,6 +223,7 @@ __global__ void probe_kernel(CommitArgs a) {
 }
 
 __global__ void resolve_kernel(CommitArgs a) {
+  pdl_enter();
   if (a.ctr->error) return;
   FOR_ITEMS(a, item) {
     int64_t r, k;
@@ -249,6 +252,7 @@ __global__ void resolve_kernel(CommitArgs a) {
 
 // Runs over the whole bound so the rank scan can use it as its length.
 __global__ void categorize_kernel(CommitArgs a) {
+  pdl_enter();
   const int64_t NI = a.s.blk_off[a.n];
   const bool err = a.ctr->error != 0;
   for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < a.n_items;
@@ -292,6 +296,7 @@ __device__ __forceinline__ int select_bit(uint32_t w, int r) {  // position of t
 }
 
 __global__ void alloc_kernel(CommitArgs a) {
+  pdl_enter();
   if (a.ctr->error) return;
   const int64_t total_free = a.s.wprefix[a.n_words];
   if (a.s.rank[a.n_items] > total_free) {  // exhausted: abort before any block is touched
@@ -338,6 +343,7 @@ __global__ void alloc_kernel(CommitArgs a) {
 }
 
 __global__ void refs_kernel(CommitArgs a) {
+  pdl_enter();
   if (a.ctr->error) return;
   FOR_ITEMS(a, item) {
     const uint8_t cat = a.s.cat[item];
@@ -354,6 +360,7 @@ __global__ void refs_kernel(CommitArgs a) {
 }
 
 __global__ void clear_owner_kernel(CommitArgs a) {
+  pdl_enter();
   FOR_ITEMS(a, item) {
     if (a.s.claim[item]) a.towner[a.s.slot_of[item]] = NO_OWNER;
   }
@@ -377,6 +384,7 @@ __device__ __forceinline__ void release_block(const CommitArgs& a, int32_t id) {
 // One warp per request: release the old pin; install the new length (commit) or none (flush).
 __global__ void release_kernel(CommitArgs a, int mode /*0 commit, 1 flush list, 2 flush all*/,
                                int64_t* out_freed) {
+  pdl_enter();
   if (mode == 0 && a.ctr->error) return;
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -411,6 +419,7 @@ __global__ void release_kernel(CommitArgs a, int mode /*0 commit, 1 flush list, 
 // every request reports the error. Claimed-but-unfilled table keys are reclaimed by the next
 // batch that probes them (they read as in-batch claims).
 __global__ void commit_finish_kernel(CommitArgs a) {
+  pdl_enter();
   const int err = a.ctr->error;
   if (err != SFKV_EPOOL) return;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < a.n;
@@ -423,6 +432,7 @@ __global__ void commit_finish_kernel(CommitArgs a) {
 }
 
 __global__ void install_kernel(CommitArgs a) {
+  pdl_enter();
   if (a.ctr->error) return;
   FOR_ITEMS(a, item) {
     if (a.s.cat[item] == CAT_NONE) continue;
@@ -442,9 +452,11 @@ __global__ void install_kernel(CommitArgs a) {
 
 // ---- table maintenance: rebuild when tombstones exceed a quarter of the slots ------------
 __global__ void rebuild_check_kernel(DevCounters* c, int64_t slots, int* flag) {
+  pdl_enter();
   *flag = (c->table_tomb * 4 > slots) ? 1 : 0;
 }
 __global__ void table_clear_kernel(Slot* slots, int64_t* towner, int64_t n, const int* flag) {
+  pdl_enter();
   if (!*flag) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -454,6 +466,7 @@ __global__ void table_clear_kernel(Slot* slots, int64_t* towner, int64_t n, cons
   }
 }
 __global__ void table_reinsert_kernel(CommitArgs a, const int* flag) {
+  pdl_enter();
   if (!*flag) return;
   for (int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; id < a.n_blocks;
        id += (int64_t)gridDim.x * blockDim.x) {
@@ -471,6 +484,7 @@ __global__ void table_reinsert_kernel(CommitArgs a, const int* flag) {
   }
 }
 __global__ void rebuild_done_kernel(DevCounters* c, const int* flag) {
+  pdl_enter();
   if (*flag) c->table_tomb = 0;
 }
 
@@ -515,11 +529,11 @@ int maybe_rebuild_table(sfkv_pool* p) {
   cudaStream_t st = p->stream;
   CommitArgs a = base_args(p);
   int* flag = &p->ctr->pad;
-  rebuild_check_kernel<<<1, 1, 0, st>>>(p->ctr, p->table_slots, flag);
+  SFKV_CUDA(launch_pdl(rebuild_check_kernel, dim3(1), dim3(1), st, p->ctr, p->table_slots, flag));
   const int sms = sm_count_c();
-  table_clear_kernel<<<sms * 4, 256, 0, st>>>(p->slots, p->towner, p->table_slots, flag);
-  table_reinsert_kernel<<<sms * 4, 256, 0, st>>>(a, flag);
-  rebuild_done_kernel<<<1, 1, 0, st>>>(p->ctr, flag);
+  SFKV_CUDA(launch_pdl(table_clear_kernel, dim3(sms * 4), dim3(256), st, p->slots, p->towner, p->table_slots, (const int*)flag));
+  SFKV_CUDA(launch_pdl(table_reinsert_kernel, dim3(sms * 4), dim3(256), st, a, (const int*)flag));
+  SFKV_CUDA(launch_pdl(rebuild_done_kernel, dim3(1), dim3(1), st, p->ctr, (const int*)flag));
   SFKV_LAUNCH_CHECK("table rebuild");
   return 0;
 }
@@ -598,29 +612,29 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   m.out_hash = a.s.hash;
   if (int rc = launch_match(p, m, a.s.tile_state, st)) return rc;
   // 2. admission, classification, allocation, references
-  admit_kernel<<<1, 32, 0, st>>>(a);
+  SFKV_CUDA(launch_pdl(admit_kernel, dim3(1), dim3(32), st, a));
   SFKV_LAUNCH_CHECK("admit_kernel");
   const int sms = sm_count_c();
   const int g = grid_for(ni, 256, sms * 8);
-  probe_kernel<<<g, 256, 0, st>>>(a);
-  resolve_kernel<<<g, 256, 0, st>>>(a);
-  categorize_kernel<<<g, 256, 0, st>>>(a);
+  SFKV_CUDA(launch_pdl(probe_kernel, dim3(g), dim3(256), st, a));
+  SFKV_CUDA(launch_pdl(resolve_kernel, dim3(g), dim3(256), st, a));
+  SFKV_CUDA(launch_pdl(categorize_kernel, dim3(g), dim3(256), st, a));
   SFKV_LAUNCH_CHECK("probe/resolve/categorize");
   if (int rc = exclusive_scan(NeedAlloc{a.s.cat}, ni, a.s.rank, a.s.scan_tmp, st)) return rc;
   if (int rc = exclusive_scan(FreeCount{p->free_bits}, p->n_words, a.s.wprefix, a.s.scan_tmp, st))
     return rc;
-  alloc_kernel<<<g, 256, 0, st>>>(a);
-  refs_kernel<<<g, 256, 0, st>>>(a);
-  clear_owner_kernel<<<g, 256, 0, st>>>(a);
+  SFKV_CUDA(launch_pdl(alloc_kernel, dim3(g), dim3(256), st, a));
+  SFKV_CUDA(launch_pdl(refs_kernel, dim3(g), dim3(256), st, a));
+  SFKV_CUDA(launch_pdl(clear_owner_kernel, dim3(g), dim3(256), st, a));
   SFKV_LAUNCH_CHECK("alloc/refs");
   // 3. payload (copy-on-share + staging scatter / handoff pull)
   if (a.payload) {
     if (int rc = launch_commit_payload(p, a, kv_src, kv_src_off, src, st)) return rc;
   }
   // 4. release old pins, install new ones
-  release_kernel<<<grid_for(n * 32, 256, sms * 8), 256, 0, st>>>(a, 0, nullptr);
-  install_kernel<<<g, 256, 0, st>>>(a);
-  commit_finish_kernel<<<grid_for(n, 256, sms), 256, 0, st>>>(a);
+  SFKV_CUDA(launch_pdl(release_kernel, dim3(grid_for(n * 32, 256, sms * 8)), dim3(256), st, a, 0, (int64_t*)nullptr));
+  SFKV_CUDA(launch_pdl(install_kernel, dim3(g), dim3(256), st, a));
+  SFKV_CUDA(launch_pdl(commit_finish_kernel, dim3(grid_for(n, 256, sms)), dim3(256), st, a));
   SFKV_LAUNCH_CHECK("release/install");
   return maybe_rebuild_table(p);
 }

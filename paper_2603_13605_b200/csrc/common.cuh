@@ -8,6 +8,7 @@
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 #include <string>
+#include <utility>
 
 #include "../../include/sfkv.h"
 
@@ -115,6 +116,32 @@ struct Carver {
   }
 };
 
+// ---- programmatic dependent launch -------------------------------------------------------
+// Kernels of one pipeline on a stream are launched with programmatic stream serialization: the
+// next kernel's CTAs may be scheduled while the previous grid drains; every kernel waits at its
+// top (griddepcontrol.wait) until its predecessor has completed and its writes are visible, so
+// the data dependencies are exactly those of plain stream order. Launch latency is hidden.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter() {
+  pdl_wait();
+  pdl_trigger();
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // ---- device-wide exclusive scan (three phases, cub::BlockScan inside each CTA) --------------
 // out[i] = sum_{j<i} f(j) for i in [0, n], out[n] = total. f is a device functor (int64 result).
 constexpr int SCAN_THREADS = 512;
@@ -125,6 +152,7 @@ template <class F>
 __global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(F f, int64_t n, int64_t* tile_sums) {
   using BS = cub::BlockReduce<int64_t, SCAN_THREADS>;
   __shared__ typename BS::TempStorage tmp;
+  pdl_enter();
   int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
   int64_t s = 0;
 #pragma unroll
@@ -143,6 +171,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_apply_kernel(F f, int64_t n
                                                           int64_t* out) {
   using BS = cub::BlockScan<int64_t, SCAN_THREADS>;
   __shared__ typename BS::TempStorage tmp;
+  pdl_enter();
   int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
   int64_t v[SCAN_ITEMS];
 #pragma unroll
@@ -174,10 +203,10 @@ int exclusive_scan(F f, int64_t n, int64_t* out, int64_t* tile_scratch, cudaStre
     SFKV_LAUNCH_CHECK("scan (empty)");
     return 0;
   }
-  scan_reduce_kernel<<<(unsigned)ntiles, SCAN_THREADS, 0, st>>>(f, n, tile_scratch);
-  scan_tiles_kernel<<<1, 1024, 0, st>>>(tile_scratch, ntiles);
-  scan_apply_kernel<<<(unsigned)ntiles, SCAN_THREADS, 0, st>>>(f, n, tile_scratch, out);
-  SFKV_LAUNCH_CHECK("exclusive_scan");
+  SFKV_CUDA(launch_pdl(scan_reduce_kernel<F>, dim3((unsigned)ntiles), dim3(SCAN_THREADS), st, f, n, tile_scratch));
+  SFKV_CUDA(launch_pdl(scan_tiles_kernel, dim3(1), dim3(1024), st, tile_scratch, ntiles));
+  SFKV_CUDA(launch_pdl(scan_apply_kernel<F>, dim3((unsigned)ntiles), dim3(SCAN_THREADS), st, f, n,
+                       (const int64_t*)tile_scratch, out));
   return 0;
 }
 

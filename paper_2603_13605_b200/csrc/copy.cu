@@ -60,6 +60,7 @@ struct PayloadKernelArgs {
 };
 
 __global__ void __launch_bounds__(256) payload_kernel(PayloadKernelArgs P) {
+  pdl_enter();
   const PayloadJob& j = P.j;
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -120,8 +121,7 @@ int launch_payload(sfkv_pool* p, const PayloadJob& j, const void* kv_src, const 
   P.src_kv = src ? src->kv : nullptr;
   P.src_blk = src ? src->blk : nullptr;
   P.src_block_bytes = src ? src->block_bytes : 0;
-  payload_kernel<<<sm_count_p() * 8, 256, 0, st>>>(P);
-  SFKV_LAUNCH_CHECK("payload_kernel");
+  SFKV_CUDA(launch_pdl(payload_kernel, dim3(sm_count_p() * 8), dim3(256), st, P));
   return 0;
 }
 

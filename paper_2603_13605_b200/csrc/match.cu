@@ -114,10 +114,6 @@ __device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-// Programmatic dependent launch: the next kernel on the stream may start its prologue now; a
-// dependent kernel waits here until its predecessor grid has completed and its writes are visible.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ int32_t clamp32(int64_t v) {
   return (int32_t)(v < -(1ll << 30) ? -(1ll << 30) : (v > (1ll << 30) ? (1ll << 30) : v));
@@ -731,20 +727,6 @@ __global__ void __launch_bounds__(MATCH_THREADS) match_chain_kernel(MatchKernelA
   }
 }
 
-template <class Kern, class Arg>
-static cudaError_t launch_pdl(Kern kern, unsigned grid, unsigned block, cudaStream_t st, const Arg& arg) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, arg);
-}
-
 int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStream_t st) {
   if (a.n <= 0) return 0;
   const int64_t ntiles = (a.n_items + WT - 1) / WT;
@@ -813,14 +795,14 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   K.hashes = (a.out_hash || a.out_block) ? 1 : 0;
   const int64_t grid = (ntiles + MATCH_THREADS / 32 - 1) / (MATCH_THREADS / 32);
   // lookup mode (no pins) keeps plain 16-B loads: staging measured slower there (C5 607 vs 510 us)
-  if (a.out_M) SFKV_CUDA(launch_pdl(match_block_kernel<true>, (unsigned)grid, MATCH_THREADS, st, K));
-  else SFKV_CUDA(launch_pdl(match_block_kernel<false>, (unsigned)grid, MATCH_THREADS, st, K));
+  if (a.out_M) SFKV_CUDA(launch_pdl(match_block_kernel<true>, dim3((unsigned)grid), dim3(MATCH_THREADS), st, K));
+  else SFKV_CUDA(launch_pdl(match_block_kernel<false>, dim3((unsigned)grid), dim3(MATCH_THREADS), st, K));
   if (K.hashes) {
     const int tpw = a.out_block ? CH_TPW_LOOKUP : CH_TPW_HASH;
     const int64_t cwarps = (ntiles + tpw - 1) / tpw;
     const unsigned cgrid = (unsigned)((cwarps + MATCH_THREADS / 32 - 1) / (MATCH_THREADS / 32));
-    if (a.out_block) SFKV_CUDA(launch_pdl(match_chain_kernel<true>, cgrid, MATCH_THREADS, st, K));
-    else SFKV_CUDA(launch_pdl(match_chain_kernel<false>, cgrid, MATCH_THREADS, st, K));
+    if (a.out_block) SFKV_CUDA(launch_pdl(match_chain_kernel<true>, dim3(cgrid), dim3(MATCH_THREADS), st, K));
+    else SFKV_CUDA(launch_pdl(match_chain_kernel<false>, dim3(cgrid), dim3(MATCH_THREADS), st, K));
   }
   return 0;
 }
