@@ -556,8 +556,11 @@ def lookup_leg(args, api, dev, stream, hbm_peak, rank):
     sys_tok = rng.integers(1, 1 << 30, size=(n_sys, sys_blocks * BT), dtype=np.uint32)
     priv_tok = rng.integers(1, 1 << 30, size=(n_wf, priv_blocks * BT), dtype=np.uint32)
     W = n_sys + n_wf
-    cfg = Config(max_workflows=W, n_blocks=1 << 21, capacity_tokens=1 << 50,
-                 max_pin_blocks=sys_blocks + priv_blocks + 1, table_log2=23, device=dev)
+    # table: 2^22 slots x 16 B (64 MB, L2-resident, load factor 0.25) for the 1,048,576 blocks;
+    # SURVEY §8d sketches 2^21 (load 0.5), whose longer probe chains measured 7 % slower
+    tl = args.c5_table_log2
+    cfg = Config(max_workflows=W, n_blocks=min(1_200_000, (1 << tl) - 1), capacity_tokens=1 << 50,
+                 max_pin_blocks=sys_blocks + priv_blocks + 1, table_log2=tl, device=dev)
     pool = Pool(api, cfg)
     t0 = time.perf_counter()
     for c0 in range(0, n_sys, 4096):  # owners of the system prompts
@@ -1069,6 +1072,7 @@ def main():
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--c5-prefixes", type=int, default=100_000)
+    ap.add_argument("--c5-table-log2", type=int, default=22)
     ap.add_argument("--no-c3", action="store_true")
     ap.add_argument("--no-mm", action="store_true")
     ap.add_argument("--no-tok", action="store_true")

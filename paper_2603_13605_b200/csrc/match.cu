@@ -34,7 +34,7 @@
 //                       issues an atomicMin (ballot arithmetic). Hashes: NH digest per block, one
 //                       warp inclusive scan, segment correction from the head ballot; each
 //                       block's local sum and the tile aggregate are final when written.
-//   match_chain_kernel  (hashes / lookup only) one warp per 8 (hash) / 4 (lookup) consecutive
+//   match_chain_kernel  (hashes / lookup only) one warp per 8 (hash) / 2 (lookup) consecutive
 //                       tiles: the carry into the first tile walks back over the predecessors'
 //                       final aggregates (32 per read); carries between the warp's own tiles come
 //                       from its own loads. Lookup mode probes the table for every full block (the
@@ -56,7 +56,7 @@ constexpr int MATCH_THREADS = 256;
 #define SFKV_CH_TPW_HASH 8
 #endif
 constexpr int CH_TPW_HASH = SFKV_CH_TPW_HASH;
-constexpr int CH_TPW_LOOKUP = 4;
+constexpr int CH_TPW_LOOKUP = 2;  // 54 registers: more warps in flight for the dependent probes
 #ifndef SFKV_PREP_THREADS
 #define SFKV_PREP_THREADS 256
 #endif
@@ -691,7 +691,7 @@ __global__ void __launch_bounds__(MATCH_THREADS) match_chain_kernel(MatchKernelA
           const uint64_t key = (uint64_t)w.x | ((uint64_t)w.y << 32);
           if (key == c[i]) {
             const int32_t cand = (int32_t)w.z;
-            if (cand >= 0 && K.blk_n[cand] == BT) {
+            if (cand >= 0) {  // only full blocks are ever published; a pending claim reads -1
               int64_t bo, to;
               int32_t len, pl, wf;
               unpack_rec(K.rec + r, bo, to, len, pl, wf);
