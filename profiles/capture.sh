@@ -12,8 +12,10 @@ tail -1 $O/bench.log > $O/bench_line.json
 B="python bench.py --steps 3 --warmup 1 --no-cpu-baseline"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $B > /dev/null 2>&1
 Q="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-kv --no-c4"
+# C5 lookup chain pass: the 20th match_chain launch of this command (19 hash-mode ones precede it)
+ncu --set full --clock-control none --import-source on -k regex:match_chain --launch-skip 19 --launch-count 1 -o $O/c5_chain $Q > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:match_block --launch-skip 6 --launch-count 1 -o $O/match_block $Q > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:match_chain --launch-skip 6 --launch-count 1 -o $O/match_chain $Q > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:tok_probe --launch-skip 1 --launch-count 1 -o $O/tok_probe $Q > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:chunk_emit --launch-skip 1 --launch-count 1 -o $O/chunk_emit $Q > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:sig_resolve --launch-skip 1 --launch-count 1 -o $O/sig_resolve $Q > /dev/null 2>&1
 ls -la $O
