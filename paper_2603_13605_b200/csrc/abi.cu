@@ -231,7 +231,7 @@ int sfkv_pool_kv(sfkv_pool* p, void** kv, int64_t* block_bytes) {
 // ---------------------------------------------------------------- lookup ------------------
 static int match_common(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
                         const uint32_t* tok, int64_t* out_M, uint64_t* out_hash, int32_t* out_block,
-                        int64_t* out_hit, int64_t n_items_bound) {
+                        int64_t* out_hit, int64_t n_items_bound, int64_t n_tok_bound) {
   cudaStream_t st = p->stream;
   const int64_t n_items = n_items_bound;  // upper bound; kernels read the exact count on device
   Carver c0;
@@ -248,6 +248,7 @@ static int match_common(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_
   a.tok = tok;
   a.blk_off = blk_off;
   a.n_items = n_items;
+  a.n_tok_bound = n_tok_bound;
   a.out_M = out_M;
   a.out_hash = out_hash;
   a.out_block = out_block;
@@ -309,7 +310,7 @@ int sfkv_match_batch(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* 
   if (int rc = stage_batch(p, n, wf, tok_off, tok, out_bytes, &dwf, &doff, &dtok, &ex)) return rc;
   int64_t* dM = reinterpret_cast<int64_t*>(ex);
   uint64_t* dh = out_hash ? reinterpret_cast<uint64_t*>(ex + ((n * sizeof(int64_t) + 255) & ~size_t(255))) : nullptr;
-  if (int rc = match_common(p, n, dwf, doff, dtok, dM, dh, nullptr, nullptr, items)) return rc;
+  if (int rc = match_common(p, n, dwf, doff, dtok, dM, dh, nullptr, nullptr, items, tok_off[n])) return rc;
   SFKV_CUDA(cudaMemcpyAsync(out_M, dM, n * sizeof(int64_t), cudaMemcpyDeviceToHost, p->stream));
   if (out_hash && items)
     SFKV_CUDA(cudaMemcpyAsync(out_hash, dh, items * sizeof(uint64_t), cudaMemcpyDeviceToHost, p->stream));
@@ -323,7 +324,7 @@ int sfkv_match_batch_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64
     return fail(SFKV_EINVAL, "match_batch_dev: bad argument");
   if (n <= 0) return n == 0 ? 0 : fail(SFKV_EINVAL, "negative batch");
   DeviceGuard g(p->cfg.device);
-  return match_common(p, n, wf, tok_off, tok, out_M, out_hash, nullptr, nullptr, n + n_tokens / BT);
+  return match_common(p, n, wf, tok_off, tok, out_M, out_hash, nullptr, nullptr, n + n_tokens / BT, n_tokens);
 }
 
 int sfkv_lookup_batch(sfkv_pool* p, int64_t n, const int64_t* tok_off, const uint32_t* tok,
@@ -342,7 +343,7 @@ int sfkv_lookup_batch(sfkv_pool* p, int64_t n, const int64_t* tok_off, const uin
     return rc;
   int64_t* dhit = reinterpret_cast<int64_t*>(ex);
   int32_t* dblk = reinterpret_cast<int32_t*>(ex + o2);
-  if (int rc = match_common(p, n, nullptr, doff, dtok, nullptr, nullptr, dblk, dhit, items)) return rc;
+  if (int rc = match_common(p, n, nullptr, doff, dtok, nullptr, nullptr, dblk, dhit, items, tok_off[n])) return rc;
   SFKV_CUDA(cudaMemcpyAsync(out_hit, dhit, n * sizeof(int64_t), cudaMemcpyDeviceToHost, p->stream));
   if (items)
     SFKV_CUDA(cudaMemcpyAsync(out_block, dblk, items * sizeof(int32_t), cudaMemcpyDeviceToHost, p->stream));
@@ -356,7 +357,8 @@ int sfkv_lookup_batch_dev(sfkv_pool* p, int64_t n, const int64_t* tok_off, const
     return fail(SFKV_EINVAL, "lookup_batch_dev: bad argument");
   if (n <= 0) return n == 0 ? 0 : fail(SFKV_EINVAL, "negative batch");
   DeviceGuard g(p->cfg.device);
-  return match_common(p, n, nullptr, tok_off, tok, nullptr, nullptr, out_block, out_hit, n + n_tokens / BT);
+  return match_common(p, n, nullptr, tok_off, tok, nullptr, nullptr, out_block, out_hit, n + n_tokens / BT,
+                      n_tokens);
 }
 
 // ---------------------------------------------------------------- retain ------------------
@@ -397,7 +399,7 @@ int sfkv_commit_batch(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t*
     dko = reinterpret_cast<int64_t*>(ex + o_ko);
     SFKV_CUDA(cudaMemcpyAsync(dko, kv_src_off, n * sizeof(int64_t), cudaMemcpyHostToDevice, p->stream));
   }
-  if (int rc = commit_dev(p, n, dwf, doff, dtok, host_items(n, tok_off), kv_src, dko, dme, dst,
+  if (int rc = commit_dev(p, n, dwf, doff, dtok, host_items(n, tok_off), tok_off[n], kv_src, dko, dme, dst,
                           nullptr))
     return rc;
   SFKV_CUDA(cudaMemcpyAsync(out_status, dst, n * sizeof(int32_t), cudaMemcpyDeviceToHost, p->stream));
@@ -412,7 +414,7 @@ int sfkv_commit_batch_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int6
   if (kv_src && (!kv_src_off || !p->kv)) return fail(SFKV_EINVAL, "commit_batch_dev: kv_src needs kv_src_off and a payload pool");
   DeviceGuard g(p->cfg.device);
   if (n_tokens < 0) return fail(SFKV_EINVAL, "commit_batch_dev: negative n_tokens");
-  return commit_dev(p, n, wf, tok_off, tok, n + n_tokens / BT, kv_src, kv_src_off, m_expected,
+  return commit_dev(p, n, wf, tok_off, tok, n + n_tokens / BT, n_tokens, kv_src, kv_src_off, m_expected,
                     out_status, nullptr);
 }
 
@@ -621,7 +623,7 @@ int sfkv_handoff(sfkv_pool* src, int32_t wf_src, sfkv_pool* dst, int32_t wf_dst,
   ps.kv = src->kv;
   ps.blk = src->pin_blk + (int64_t)wf_src * src->cfg.max_pin_blocks;  // item k = block k
   ps.block_bytes = src->block_bytes;
-  if (int rc = commit_dev(dst, 1, dwf, doff, dtok, nb, nullptr, nullptr, nullptr, dst_status,
+  if (int rc = commit_dev(dst, 1, dwf, doff, dtok, nb, (int64_t)nb * BT, nullptr, nullptr, nullptr, dst_status,
                           dst->kv ? &ps : nullptr))
     return rc;
   SFKV_CUDA(cudaMemcpyAsync(status, dst_status, sizeof(int32_t), cudaMemcpyDeviceToHost, dst->stream));
@@ -721,7 +723,7 @@ int sfkv_handoff_recv_batch(sfkv_pool* dst, const sfkv_peer* src, int64_t n, con
   ps.kv = src->kv;
   ps.blk = dblk;
   ps.block_bytes = src->block_bytes;
-  if (int rc = commit_dev(dst, n, dwf, doff, dtok, items, nullptr, nullptr, nullptr, dstatus, &ps))
+  if (int rc = commit_dev(dst, n, dwf, doff, dtok, items, tok_off[n], nullptr, nullptr, nullptr, dstatus, &ps))
     return rc;
   SFKV_CUDA(cudaMemcpyAsync(out_status, dstatus, n * sizeof(int32_t), cudaMemcpyDeviceToHost, dst->stream));
   return check_sticky(dst);
@@ -740,7 +742,8 @@ int sfkv_handoff_recv_batch_dev(sfkv_pool* dst, const sfkv_peer* src, int64_t n,
   ps.kv = src->kv;
   ps.blk = src_blocks;
   ps.block_bytes = src->block_bytes;
-  return commit_dev(dst, n, wf, tok_off, tok, n + n_tokens / BT, nullptr, nullptr, nullptr, out_status, &ps);
+  return commit_dev(dst, n, wf, tok_off, tok, n + n_tokens / BT, n_tokens, nullptr, nullptr, nullptr, out_status,
+                    &ps);
 }
 
 }  // extern "C"

@@ -558,7 +558,7 @@ static int launch_commit_payload(sfkv_pool* p, const CommitArgs& a, const void* 
 }
 
 int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
-               const uint32_t* tok, int64_t n_items_bound, const void* kv_src,
+               const uint32_t* tok, int64_t n_items_bound, int64_t n_tok_bound, const void* kv_src,
                const int64_t* kv_src_off, const int64_t* m_expected, int32_t* out_status,
                const PayloadSource* src) {
   if (n <= 0) return 0;
@@ -608,6 +608,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   m.tok = tok;
   m.blk_off = a.s.blk_off;
   m.n_items = ni;
+  m.n_tok_bound = n_tok_bound;
   m.out_M = a.s.M;
   m.out_hash = a.s.hash;
   if (int rc = launch_match(p, m, a.s.tile_state, st)) return rc;

@@ -23,8 +23,8 @@
 //                       from the tile record (one broadcast load) or, for tiles crossing a request
 //                       boundary, from the request window (one record per lane + a 5-step
 //                       shuffle search). Match mode stages the tile's token range (contiguous in
-//                       the CSR batch) into shared memory with one cp.async.bulk per warp and
-//                       reads it with bank-rotated 16-B loads; the pin's blocks of each request
+//                       the CSR batch) into shared memory with one 2D tensor-map TMA load per warp
+//                       (rows of 32 ids, 128-B swizzle: conflict-free 16-B reads, no rotation); the pin's blocks of each request
 //                       segment (pin-major copy: one extent) arrive by a second bulk copy on the
 //                       same mbarrier phase, so nothing is held in registers across the wait. (Lane-per-block
 //                       16-B global loads are 64 B apart: 16 lines per warp instruction, which
@@ -44,12 +44,16 @@
 // request. Implementation traffic on top: 8 B written + read per block (local sums) when hashes
 // are wanted, + 4 B written + read per block (request id) in lookup mode. HBM-bound integer work:
 // no tensor cores.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "pool.cuh"
 
 namespace sfkv {
 
 constexpr int WT = 32;                        // items per warp tile
 constexpr int MATCH_THREADS = 256;
+constexpr int BLOCK_THREADS = 128;  // block pass: 4 warps per CTA, so the per-warp staging fits 10 CTAs/SM
 // chain pass tiles per warp: hash-only warps are latency-bound on one look-back, lookup warps
 // also carry the table probes
 #ifndef SFKV_CH_TPW_HASH
@@ -243,6 +247,7 @@ struct MatchKernelArgs {
   uint32_t* rk;      // lookup mode: per block request id | RK_FULL
   const TileRec* trec;
   int hashes;        // chained hashes (or lookup) requested
+  int64_t tok_rows;  // full 32-id rows of the token buffer (the tensor map's height)
 };
 
 struct Ctx {  // one lane's block of one tile
@@ -378,30 +383,13 @@ __device__ __forceinline__ void load_block(const uint32_t* __restrict__ tok, int
   }
 }
 
-// ---- TMA bulk staging of a tile's request tokens ----------------------------------------
-// A tile's 32 blocks are one contiguous token range of the CSR batch (blocks partition requests
-// and requests are consecutive), so one cp.async.bulk per warp brings all of it (<= 2.1 KB)
-// into shared memory without touching the LSU. Lanes then read their block with rotated
-// 16-B shared loads: lane L starts at chunk (i + r_L) mod 5 with r_L = (L >> 1) & 3, which puts
-// the 8 lanes of each quarter-warp phase on distinct bank groups (lanes of one request are 64 B
-// apart, so unrotated reads would be 4-way conflicted); two select stages undo the rotation.
-constexpr int STAGE_WORDS = 544;  // >= 31*16 + 3 + 20 words (last lane's 5-chunk window), 128-B multiple
-
+// ---- TMA staging (tokens: a 2D tensor-map box with the 128-B swizzle; pins: bulk copies) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
 }
 __device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
   asm volatile(
@@ -455,28 +443,30 @@ __device__ __forceinline__ void load_pin_staged(const uint32_t* s, uint32_t* q) 
 #endif
 }
 
-// Block tokens of a lane whose block starts at word o of the staged range (o >= 0).
-__device__ __forceinline__ void load_block_staged(const uint32_t* s, int o, int nval, uint32_t* t) {
-  const int lane = threadIdx.x & 31;
-  const int c0 = o >> 2, sh = o & 3, rr = (lane >> 1) & 3;
-  uint4 v[5];
-#pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    int x = i + rr;
-    x = x >= 5 ? x - 5 : x;
-    v[i] = *reinterpret_cast<const uint4*>(s + 4 * (c0 + x));
-  }
-  uint4 u[5];
-#pragma unroll
-  for (int x = 0; x < 5; ++x) u[x] = (rr & 1) ? v[(x + 4) % 5] : v[x];
+// Tensor-map staging of the token range: the token buffer viewed as rows of 32 ids (128 B); a
+// tile's range is TMAP_ROWS rows from the row holding its first token, loaded with the 128-B
+// swizzle (16-B chunk c of row r lands at chunk c ^ (r & 7)), so the lanes of a quarter-warp —
+// whose blocks are 4 chunks apart — read distinct bank groups with no per-lane rotation to undo.
+constexpr int TMAP_ROWS = 18;  // >= (3 + 31*16 + 20 + 31) / 32 rows
+__device__ __forceinline__ void bulk_tensor_2d(void* dst, const CUtensorMap* tm, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+// Block tokens of a lane whose block starts at word o of a swizzled staged range.
+__device__ __forceinline__ void load_block_swz(const uint32_t* s, int o, int nval, uint32_t* t) {
+  const int c0 = o >> 2, sh = o & 3;
   uint32_t w[20];
 #pragma unroll
-  for (int x = 0; x < 5; ++x) {
-    const uint4 q = (rr & 2) ? u[(x + 3) % 5] : u[x];
-    w[4 * x] = q.x;
-    w[4 * x + 1] = q.y;
-    w[4 * x + 2] = q.z;
-    w[4 * x + 3] = q.w;
+  for (int i = 0; i < 5; ++i) {
+    const int g = c0 + i;
+    const uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(s) + ((g ^ ((g >> 3) & 7)) << 4));
+    w[4 * i] = v.x;
+    w[4 * i + 1] = v.y;
+    w[4 * i + 2] = v.z;
+    w[4 * i + 3] = v.w;
   }
   uint32_t y[17];
 #pragma unroll
@@ -489,6 +479,7 @@ __device__ __forceinline__ void load_block_staged(const uint32_t* s, int o, int 
       if (j >= nval) t[j] = 0u;
   }
 }
+
 
 // M and chained-hash work of one tile once every lane holds its block's tokens t (zero padded)
 // and, for blocks inside the pin, the pin's block q.
@@ -558,10 +549,11 @@ __device__ __forceinline__ void tile_finish(const MatchKernelArgs& K, int64_t ti
 // cover the window -> tokens/pin-tokens round trips.
 // 5 CTAs (40 warps) per SM: the register cap (48) trades a few spilled bytes for occupancy.
 template <bool STAGED>
-__global__ void __launch_bounds__(MATCH_THREADS, 5) match_block_kernel(MatchKernelArgs K) {
-  __shared__ __align__(128) uint32_t s_tok[STAGED ? MATCH_THREADS / 32 : 1][STAGED ? STAGE_WORDS : 4];
-  __shared__ __align__(128) uint32_t s_pin[STAGED ? MATCH_THREADS / 32 : 1][STAGED ? WT * PIN_STRIDE : 4];
-  __shared__ __align__(8) uint64_t s_bar[MATCH_THREADS / 32];
+__global__ void __launch_bounds__(BLOCK_THREADS, 10) match_block_kernel(MatchKernelArgs K,
+                                                                       const __grid_constant__ CUtensorMap tmap) {
+  __shared__ __align__(1024) uint32_t s_tok[STAGED ? BLOCK_THREADS / 32 : 1][STAGED ? 768 : 4];  // 18 rows, 1 KB-aligned
+  __shared__ __align__(128) uint32_t s_pin[STAGED ? BLOCK_THREADS / 32 : 1][STAGED ? WT * PIN_STRIDE : 4];
+  __shared__ __align__(8) uint64_t s_bar[BLOCK_THREADS / 32];
   const MatchArgs& A = K.a;
   const int lane = threadIdx.x & 31;
   [[maybe_unused]] const int warp = threadIdx.x >> 5;
@@ -585,9 +577,10 @@ __global__ void __launch_bounds__(MATCH_THREADS, 5) match_block_kernel(MatchKern
     // one mbarrier phase for the tile: its token range (one bulk copy) and, per request segment
     // of in-pin blocks, that segment's pin blocks (pin-major: one extent, placed at lane * 64 B)
     const int nv = __popc(__ballot_sync(0xffffffffu, c.valid));
-    const int64_t a0 = __shfl_sync(0xffffffffu, c.start, 0) & ~int64_t(3);
+    const int64_t row0 = __shfl_sync(0xffffffffu, c.start, 0) >> 5;
+    const int64_t a0 = row0 << 5;
     const int64_t a1 = __shfl_sync(0xffffffffu, (c.start & ~int64_t(3)) + 20, nv - 1);
-    const bool staged = a1 <= (tok_total & ~int64_t(3));  // all but the batch's last tile
+    const bool staged = a1 <= K.tok_rows * 32;  // all but the tiles touching the last partial row
     const unsigned pin_m = __ballot_sync(0xffffffffu, in_pin);
     const int64_t prev_r = __shfl_up_sync(0xffffffffu, c.r, 1);
     const bool head = in_pin && (lane == 0 || !((pin_m >> (lane - 1)) & 1u) || prev_r != c.r);
@@ -599,17 +592,18 @@ __global__ void __launch_bounds__(MATCH_THREADS, 5) match_block_kernel(MatchKern
       const int end = stop ? __ffs(stop) - 1 : 32;
       pin_bytes = (uint32_t)(end - lane) * (PIN_STRIDE * 4);
     }
-    const uint32_t total = __reduce_add_sync(0xffffffffu, pin_bytes) + (staged ? (uint32_t)(a1 - a0) * 4u : 0u);
+    const uint32_t tok_bytes = staged ? (uint32_t)(TMAP_ROWS * 128) : 0u;
+    const uint32_t total = __reduce_add_sync(0xffffffffu, pin_bytes) + tok_bytes;
     if (total) {
       if (lane == 0) mbar_expect_tx(&s_bar[warp], total);
       __syncwarp();
-      if (staged && lane == 0) bulk_copy(s_tok[warp], A.tok + a0, (uint32_t)(a1 - a0) * 4u, &s_bar[warp]);
+      if (staged && lane == 0) bulk_tensor_2d(s_tok[warp], &tmap, 0, (int)row0, &s_bar[warp]);
       if (head) bulk_copy(s_pin[warp] + lane * PIN_STRIDE, K.pin_tok + pin_tok_index(c.wf, c.k, 0, K.pin_groups),
                           pin_bytes, &s_bar[warp]);
       mbar_wait0(&s_bar[warp]);
     }
     if (c.valid) {
-      if (staged) load_block_staged(s_tok[warp], (int)(c.start - a0), c.nval, t);
+      if (staged) load_block_swz(s_tok[warp], (int)(c.start - a0), c.nval, t);
       else load_block(A.tok, c.start, c.nval, tok_total, t);
     }
     if (in_pin) load_pin_staged(s_pin[warp], q);
@@ -793,10 +787,34 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   K.rk = a.out_block ? rk : nullptr;
   K.trec = trec;
   K.hashes = (a.out_hash || a.out_block) ? 1 : 0;
-  const int64_t grid = (ntiles + MATCH_THREADS / 32 - 1) / (MATCH_THREADS / 32);
+  const int64_t grid = (ntiles + BLOCK_THREADS / 32 - 1) / (BLOCK_THREADS / 32);
   // lookup mode (no pins) keeps plain 16-B loads: staging measured slower there (C5 607 vs 510 us)
-  if (a.out_M) SFKV_CUDA(launch_pdl(match_block_kernel<true>, dim3((unsigned)grid), dim3(MATCH_THREADS), st, K));
-  else SFKV_CUDA(launch_pdl(match_block_kernel<false>, dim3((unsigned)grid), dim3(MATCH_THREADS), st, K));
+  // token tensor map (rows of 32 ids); a batch smaller than one row stages nothing
+  CUtensorMap tm;
+  memset(&tm, 0, sizeof(tm));
+  K.tok_rows = a.n_tok_bound / 32;
+  if (a.out_M && K.tok_rows > 0) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      void* fn = nullptr;
+      SFKV_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+      if (q != cudaDriverEntryPointSuccess || !fn) return fail(SFKV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {32, (cuuint64_t)K.tok_rows};
+    const cuuint64_t strides[1] = {128};
+    const cuuint32_t box[2] = {32, TMAP_ROWS};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(a.tok), dims, strides,
+                              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SFKV_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  } else {
+    K.tok_rows = 0;
+  }
+  if (a.out_M) SFKV_CUDA(launch_pdl(match_block_kernel<true>, dim3((unsigned)grid), dim3(BLOCK_THREADS), st, K, tm));
+  else SFKV_CUDA(launch_pdl(match_block_kernel<false>, dim3((unsigned)grid), dim3(BLOCK_THREADS), st, K, tm));
   if (K.hashes) {
     const int tpw = a.out_block ? CH_TPW_LOOKUP : CH_TPW_HASH;
     const int64_t cwarps = (ntiles + tpw - 1) / tpw;

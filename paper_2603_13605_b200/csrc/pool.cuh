@@ -108,6 +108,7 @@ struct MatchArgs {
   const uint32_t* tok;
   int64_t* blk_off;          // [n+1] exclusive scan of ceil(len/16), written by launch_match
   int64_t n_items;
+  int64_t n_tok_bound;       // token-buffer capacity (ids) the tok pointer may be read up to
   int64_t* out_M;            // nullable
   uint64_t* out_hash;        // nullable
   int32_t* out_block;        // nullable: lookup mode
@@ -144,7 +145,7 @@ size_t match_tile_state_elems(int64_t n_items, int64_t n_requests);
 
 // Internal commit entry (device pointers). src: handoff payload source (nullable).
 int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_off,
-               const uint32_t* tok, int64_t n_items_bound, const void* kv_src,
+               const uint32_t* tok, int64_t n_items_bound, int64_t n_tok_bound, const void* kv_src,
                const int64_t* kv_src_off, const int64_t* m_expected, int32_t* out_status,
                const PayloadSource* src);
 int flush_dev(sfkv_pool* p, int64_t n, const int32_t* wf, int64_t* out_freed, bool all);
