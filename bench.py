@@ -18,7 +18,8 @@ reference's SimulatedBackend::prefix_match, simulated_backend.cpp:153-162) over 
            contiguous staging and a stage commit (copy-on-share + scatter of appended tokens)
   c4_long_context / c5_lookup = BASELINE configs[3] / configs[4] legs; c3_handoff (N > 1) =
            configs[2]: every GPU pulls its predecessor's retained contexts over NVLink
-  mm_signals / tokenize = SURVEY §8f-1 / §8f-2 legs (batched MemoryManager, tokenizer+interner)
+  mm_signals / tokenize / latency_metrics = SURVEY §8f-1 / -2 / -3 legs (batched MemoryManager,
+           tokenizer+interner, latency model + TTFT CDF)
   roofline / cpu_baseline / clocks / gpu_launches per the driver contract.
 
 --impl reference runs the reference's own prefix_match (oracle/_ref/libsfref.so, compiled from
@@ -392,6 +393,7 @@ def run_ours(args, rank, world, local_rank):
         c3 = handoff_leg(args, api, dev, stream, rank, world) if (dist and not args.no_c3) else None
         mm = None if args.no_mm else mm_leg(args, api, dev, stream)
         tk = None if args.no_tok else tokenize_leg(args, api, dev, stream, hbm_peak)
+        lat = None if args.no_lat else latency_leg(args, api, dev, stream)
     clocks = clk.summary()
 
     # ---- roofline of the match kernel: algorithmic bytes of one launch --------------------
@@ -440,6 +442,8 @@ def run_ours(args, rank, world, local_rank):
         line["mm_signals"] = mm
     if tk:
         line["tokenize"] = tk
+    if lat:
+        line["latency_metrics"] = lat
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
     pool.close()
@@ -1043,6 +1047,51 @@ def tokenize_reference(L, text, msg_off, n_req):
 
 
 
+def latency_leg(args, api, dev, stream):
+    """§8f-3: SimulatedBackend::start's timing arithmetic for a batch of 1M stage requests over 8
+    backends (device-resident), and the 99-point nearest-rank TTFT CDF of the batch."""
+    import torch
+
+    from paper_2603_13605_b200.abi import nearest_rank
+    n, nb = 1_000_000, 8
+    rng = np.random.default_rng(args.seed + 9)
+    P = rng.integers(512, 8448, size=n)
+    M = (P * rng.random(n)).astype(np.int64)
+    host = {"backend": rng.integers(0, nb, size=n).astype(np.int32), "queue": rng.exponential(30.0, size=n),
+            "P": P, "M": M, "O": rng.integers(16, 512, size=n).astype(np.int64)}
+    d = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in host.items()}
+    par = [torch.from_numpy(rng.random(nb) * s).to(dev) for s in (20.0, 0.5, 20.0)]
+    out = [torch.zeros(n, dtype=torch.float64, device=dev) for _ in range(3)]
+    fn = api.lib.sfmet_latency_batch_dev
+    fn.argtypes = [C.c_int32, C.c_int64] + [C.c_void_p] * 12
+    ptr = lambda t: C.c_void_p(t.data_ptr())
+
+    def step():
+        api.check("latency_batch_dev", fn(dev, n, ptr(d["backend"]), ptr(d["queue"]), ptr(d["P"]), ptr(d["M"]),
+                                          ptr(d["O"]), ptr(par[0]), ptr(par[1]), ptr(par[2]), ptr(out[0]),
+                                          ptr(out[1]), ptr(out[2]), C.c_void_p(stream.cuda_stream)))
+    times = []
+    for i in range(args.warmup + args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            times.append(a.elapsed_time(b))
+    ms = float(np.mean(times))
+    ttft = out[0].cpu().numpy()
+    t0 = time.perf_counter()
+    cdf = nearest_rank(api, ttft, np.arange(1, 100, dtype=np.int32), device=dev)
+    cdf_ms = 1e3 * (time.perf_counter() - t0)
+    alg = n * (4 + 8 * 4 + 8 * 3)
+    return {"workload": f"{n} stage requests over {nb} backends: ttft / total / service delay, then the 99-point TTFT CDF",
+            "requests": n, "ms": ms, "requests_per_s": n / (ms / 1e3),
+            "hbm_frac": alg / (ms / 1e3) / 1e9 / peaks()[0], "cdf_ms_host_api": cdf_ms,
+            "ttft_p50_p99": [float(cdf[49]), float(cdf[98])]}
+
+
+
 def cpu_baseline(args):
     L = ref_lib()
     n_sample = args.cpu_sample
@@ -1076,6 +1125,7 @@ def main():
     ap.add_argument("--no-c3", action="store_true")
     ap.add_argument("--no-mm", action="store_true")
     ap.add_argument("--no-tok", action="store_true")
+    ap.add_argument("--no-lat", action="store_true")
     ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--dist-backend", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--c3-workflows", type=int, default=32)

@@ -340,6 +340,26 @@ int sfmm_pressure_tick(sfmm_tracker* t, const double* util, int32_t* out_victim)
 int sfmm_tracker_entries(sfmm_tracker* t, uint8_t* present, uint8_t* preserved, int64_t* tokens,
                          double* ts, int32_t* in_flight);
 
+/* ---- batched latency model and TTFT percentiles: SimulatedBackend::start's
+ *      timing arithmetic (simulated_backend.cpp:99-112) and MetricsReport's nearest-rank
+ *      percentiles (metrics.cpp:22-28, 57-67) ---------------------------------------------------
+ * Per request r on backend b = backend[r]:
+ *   prefill = overhead[b] + prefill[b] * (P[r] - M[r]);  decode = decode[b] * O[r]
+ *   ttft = queue_ms[r] + prefill;  total = ttft + decode;  service = prefill + decode
+ *   (the completion event's delay) — bit-identical doubles (no FMA contraction).
+ * out_total / out_service nullable. The _dev variant takes device pointers and a stream. */
+int sfmet_latency_batch(int32_t device, int64_t n, const int32_t* backend, const double* queue_ms, const int64_t* P,
+                        const int64_t* M, const int64_t* O, int32_t n_backends, const double* overhead,
+                        const double* prefill, const double* decode, double* out_ttft, double* out_total,
+                        double* out_service);
+int sfmet_latency_batch_dev(int32_t device, int64_t n, const int32_t* backend, const double* queue_ms,
+                            const int64_t* P, const int64_t* M, const int64_t* O, const double* overhead,
+                            const double* prefill, const double* decode, double* out_ttft, double* out_total,
+                            double* out_service, void* cuda_stream);
+/* out[i] = the pct[i]-th nearest-rank percentile of the n samples (n >= 1; sorted on the device):
+ * sorted[max(1, ceil(pct[i] / 100 * n)) - 1]. MetricsReport::ttft_cdf is pct = 1..99. */
+int sfmet_nearest_rank(int32_t device, int64_t n, const double* samples, int32_t k, const int32_t* pct, double* out);
+
 /* ---- stage mapper: replaces map_threshold (mapper.cpp:19-31) and reroute_on_overload
  *      (orchestrator.cpp:78-87) -----------------------------------------------------------------
  * Threshold: out_choice[r] = 0 (light) iff score[r] <= threshold, else 1 (heavy).

@@ -17,6 +17,7 @@
 
 #include "stageflow/backend.hpp"
 #include "stageflow/memory.hpp"
+#include "stageflow/metrics.hpp"
 #include "stageflow/mapper.hpp"
 #include "stageflow/orchestrator.hpp"
 #include "stageflow/simulated_backend.hpp"
@@ -177,6 +178,50 @@ int sfref_reroute(int n, const unsigned long long* depth, unsigned long long lim
       [&](const std::string& s) { return static_cast<std::size_t>(depth[std::stoi(s)]); },
       static_cast<std::size_t>(limit));
   return std::stoi(pick);
+}
+
+// ---- latency model and metrics --------------------------------------------------------------
+// n requests submitted at virtual time 0 to one SimulatedBackend (max_concurrency slots, constant
+// output of out_tokens): the reference's own CompletionResponse timing and usage per request
+// (simulated_backend.cpp:72-133). wf[i] = "" for unpinned (routing-style) calls.
+void sfref_sim_timing(double prefill, double decode, double overhead, int max_conc, long long out_tokens, int n,
+                      const char* const* wf, const char* const* text, double* queue, double* ttft, double* total,
+                      long long* P, long long* M, long long* O) {
+  EventLoop loop(ClockMode::Virtual);
+  SimulatedBackendConfig cfg;
+  cfg.prefill_ms_per_token = prefill;
+  cfg.decode_ms_per_token = decode;
+  cfg.fixed_overhead_ms = overhead;
+  cfg.max_concurrency = max_conc;
+  cfg.cache_capacity_tokens = 1LL << 40;
+  cfg.output = OutputRule::constant(out_tokens);
+  BackendDescriptor d;
+  d.ref = "ref";
+  d.model = "ref-model";
+  SimulatedBackend be(loop, d, cfg);
+  for (int i = 0; i < n; ++i) {
+    CompletionRequest req;
+    req.model = "ref-model";
+    Message m;
+    m.content = text[i];
+    req.messages.push_back(std::move(m));
+    req.metadata.workflow_id = wf[i];
+    req.metadata.stage_id = "s";
+    be.complete(std::move(req), [=](CompletionResponse r, std::exception_ptr) {
+      queue[i] = r.timing.queue_ms;
+      ttft[i] = r.timing.ttft_ms;
+      total[i] = r.timing.total_ms;
+      P[i] = r.usage.prompt_tokens;
+      M[i] = r.usage.cached_prefix_tokens;
+      O[i] = r.usage.completion_tokens;
+    });
+  }
+  loop.run_until_idle();
+}
+
+// percentile_nearest_rank over the (already sorted) samples (metrics.cpp:22-28).
+double sfref_percentile(long long n, const double* sorted, int pct) {
+  return percentile_nearest_rank(std::vector<double>(sorted, sorted + n), pct);
 }
 
 // ---- tokenizer --------------------------------------------------------------------------

@@ -15,6 +15,7 @@
  */
 #include "sfkv_oracle.h"
 
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -1109,4 +1110,47 @@ int sfo_tokenize_batch(sfo_interner* it, int64_t n, const int64_t* req_msg_off, 
   }
   free(slot0);
   return rc;
+}
+
+
+/* ================================================================ latency model ==========
+ * SimulatedBackend::start (simulated_backend.cpp:99-112): prefill = overhead + prefill_ms * (P -
+ * M), decode = decode_ms * O, ttft = queue + prefill, total = ttft + decode; the completion event
+ * fires prefill + decode after dispatch (line 121). Plain C doubles, no contraction (x86-64 -O2). */
+int sfo_latency_batch(int64_t n, const int32_t* backend, const double* queue_ms, const int64_t* P,
+                      const int64_t* M, const int64_t* O, int32_t n_backends, const double* overhead,
+                      const double* prefill, const double* decode, double* out_ttft, double* out_total,
+                      double* out_service) {
+  if (n < 0 || n_backends <= 0) return -1;
+  for (int64_t r = 0; r < n; ++r) {
+    const int32_t b = backend[r];
+    if (b < 0 || b >= n_backends) return -1;
+    const double pf = overhead[b] + prefill[b] * (double)(P[r] - M[r]);
+    const double dc = decode[b] * (double)O[r];
+    out_ttft[r] = queue_ms[r] + pf;
+    if (out_total) out_total[r] = out_ttft[r] + dc;
+    if (out_service) out_service[r] = pf + dc;
+  }
+  return 0;
+}
+
+static int cmp_double(const void* a, const void* b) {
+  const double x = *(const double*)a, y = *(const double*)b;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* percentile_nearest_rank (metrics.cpp:22-28): rank = max(1, ceil(pct / 100.0 * n)). */
+int sfo_nearest_rank(int64_t n, const double* samples, int32_t k, const int32_t* pct, double* out) {
+  if (n <= 0 || k < 0) return -1;
+  double* s = (double*)malloc((size_t)n * sizeof(double));
+  memcpy(s, samples, (size_t)n * sizeof(double));
+  qsort(s, (size_t)n, sizeof(double), cmp_double);
+  for (int32_t i = 0; i < k; ++i) {
+    int64_t rank = (int64_t)ceil((double)pct[i] / 100.0 * (double)n);
+    if (rank < 1) rank = 1;
+    if (rank > n) rank = n;
+    out[i] = s[rank - 1];
+  }
+  free(s);
+  return 0;
 }

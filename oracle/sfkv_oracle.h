@@ -129,4 +129,13 @@ int sfo_tokenize_batch(sfo_interner* it, int64_t n, const int64_t* req_msg_off, 
                        const uint8_t* text, int64_t* tok_off, uint32_t* tok, int64_t tok_cap,
                        int64_t* n_tokens);
 
+
+/* ---- latency model and nearest-rank percentiles (restates simulated_backend.cpp:99-112,
+ *      metrics.cpp:22-28) ------------------------------------------------------------------ */
+int sfo_latency_batch(int64_t n, const int32_t* backend, const double* queue_ms, const int64_t* P,
+                      const int64_t* M, const int64_t* O, int32_t n_backends, const double* overhead,
+                      const double* prefill, const double* decode, double* out_ttft, double* out_total,
+                      double* out_service);
+int sfo_nearest_rank(int64_t n, const double* samples, int32_t k, const int32_t* pct, double* out);
+
 #endif

@@ -116,6 +116,10 @@ ORACLE_ONLY = {
     "gather": [P, i64, P, P, P],
     "chain_hashes": [P, i64, P],
 }
+MET_FNS = {  # sfmet_* on the GPU (first argument: device), sfo_* in the oracle
+    "latency_batch": [P, i64, P, P, P, P, P, i32, P, P, P, P, P, P],
+    "nearest_rank": [P, i64, P, i32, P, P],
+}
 GLOBAL_FNS = {  # prefix differs: sfmm_/sfmap_ on the GPU, sfo_ in the oracle
     "pressure_argmin": [P, i64, P, P, P, P, P, i32, P, f64, P],
     "threshold_batch": [P, i64, P, f64, P],
@@ -167,6 +171,11 @@ class Api:
         if kind == "gpu":
             for name, argt in MM_GPU_ONLY.items():
                 self._bind("sfmm_" + name, "mm_" + name, argt)
+        for name, argt in MET_FNS.items():
+            if kind == "gpu":
+                self._bind("sfmet_" + name, name, [i32] + argt[1:])
+            else:
+                self._bind("sfo_" + name, name, argt[1:])
         for name, argt in GLOBAL_FNS.items():
             if kind == "gpu":
                 sym = ("sfmm_" if name == "pressure_argmin" else "sfmap_") + name
@@ -547,3 +556,29 @@ class Interner:
         buf = C.create_string_buffer(max(ln.value, 1))
         self.api.check("interner_token", self.api.interner_token(self.h, int(i), buf, ln.value, C.byref(ln)))
         return buf.raw[: ln.value]
+
+
+# ---------------------------------------------------------------- latency model / metrics ---
+def latency_batch(api: Api, backend, queue_ms, P, M, O, overhead, prefill, decode, device=0):
+    """(ttft, total, service) per request: SimulatedBackend::start's timing, batched."""
+    n = len(backend)
+    arrs = [np.ascontiguousarray(backend, np.int32), np.ascontiguousarray(queue_ms, np.float64),
+            np.ascontiguousarray(P, np.int64), np.ascontiguousarray(M, np.int64), np.ascontiguousarray(O, np.int64)]
+    par = [np.ascontiguousarray(x, np.float64) for x in (overhead, prefill, decode)]
+    ttft, total, svc = np.zeros(n), np.zeros(n), np.zeros(n)
+    args = [n] + [_ptr(a) for a in arrs] + [len(par[0])] + [_ptr(x) for x in par] + [_ptr(ttft), _ptr(total), _ptr(svc)]
+    if api.kind == "gpu":
+        args = [device] + args
+    api.check("latency_batch", api.latency_batch(*args))
+    return ttft, total, svc
+
+
+def nearest_rank(api: Api, samples, pct, device=0):
+    samples = np.ascontiguousarray(samples, np.float64)
+    pct = np.ascontiguousarray(pct, np.int32)
+    out = np.zeros(len(pct))
+    args = [len(samples), _ptr(samples), len(pct), _ptr(pct), _ptr(out)]
+    if api.kind == "gpu":
+        args = [device] + args
+    api.check("nearest_rank", api.nearest_rank(*args))
+    return out

@@ -224,14 +224,19 @@ struct DeviceGuard {
 };
 
 inline int check_device(int dev) {
+  // cached per device: cudaGetDeviceProperties costs milliseconds, entry points call this often
+  static int ok[64] = {0};
+  if (dev >= 0 && dev < 64 && ok[dev]) return 0;
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
   if (e != cudaSuccess || n == 0) return fail(SFKV_ENODEV, "no CUDA device visible");
   if (dev < 0 || dev >= n) return fail(SFKV_ENODEV, "device ordinal out of range");
-  cudaDeviceProp prop;
-  SFKV_CUDA(cudaGetDeviceProperties(&prop, dev));
-  if (prop.major != 10) return fail(SFKV_ENODEV, "libsfkv is built for sm_100a (B200); device is sm_" +
-                                                       std::to_string(prop.major * 10 + prop.minor));
+  int major = 0, minor = 0;
+  SFKV_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  SFKV_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+  if (major != 10) return fail(SFKV_ENODEV, "libsfkv is built for sm_100a (B200); device is sm_" +
+                                                std::to_string(major * 10 + minor));
+  if (dev < 64) ok[dev] = 1;
   return 0;
 }
 
