@@ -14,6 +14,7 @@
 //                                       no backends attached (every action "applies")
 // Token ids are rendered to whitespace tokens "t<id>", the same text the reference tokenizes.
 #include <cstring>
+#include <sstream>
 
 #include "stageflow/backend.hpp"
 #include "stageflow/memory.hpp"
@@ -305,6 +306,15 @@ int sfref_mm_pressure_tick(void* h, int n, const char* const* refs, const double
   std::map<std::string, double> u;
   for (int i = 0; i < n; ++i) u[refs[i]] = util[i];
   return static_cast<int>(static_cast<MemoryManager*>(h)->pressure_tick(u, now).size());
+}
+
+// MemoryManager::export_action_log (memory.cpp:389-401) into buf (cap bytes); returns its length.
+long long sfref_mm_export(void* h, char* buf, long long cap) {
+  std::ostringstream os;
+  static_cast<MemoryManager*>(h)->export_action_log(os);
+  const std::string s = os.str();
+  if (static_cast<long long>(s.size()) <= cap) std::memcpy(buf, s.data(), s.size());
+  return static_cast<long long>(s.size());
 }
 
 long long sfref_mm_log_size(void* h) {

@@ -80,3 +80,30 @@ def test_gpu_tracker_matches_oracle_in_large_batches(gpu_api, oracle_api, seed, 
     assert lg == lo
     for a, b in zip(eo, eg):  # tracker state after the stream
         assert (a == b).all()
+
+
+@pytest.mark.skipif(not os.path.exists(REF_LIB), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed", [7, 8])
+def test_action_log_jsonl_byte_identical_to_reference_export(oracle_api, seed):
+    """§8f-4: the JSONL the GPU path writes (paper_2603_13605_b200.sim_server.action_log_jsonl over
+    the tracker's records) equals MemoryManager::export_action_log byte for byte."""
+    import ctypes as C
+
+    from paper_2603_13605_b200.sim_server import action_log_jsonl
+    events, backends, wfs = random_stream(seed)
+    chain = ["preserve_small_increment", "flush_at_boundary"]
+    ref = RefManager(512, 0.85, chain)
+    ref.run(events, backends)
+    L = ref.L
+    L.sfref_mm_export.restype = C.c_longlong
+    L.sfref_mm_export.argtypes = [C.c_void_p, C.c_char_p, C.c_longlong]
+    n = L.sfref_mm_export(ref.h, None, 0)
+    buf = C.create_string_buffer(n + 1)
+    L.sfref_mm_export(ref.h, buf, n + 1)
+    want = buf.raw[:n].decode()
+    ref.close()
+    tr = Tracker(oracle_api, max_workflows=len(wfs), n_backends=len(backends), chain=chain)
+    log, _ = run_stream(tr, Interner(backends, wfs), events, batch_between_ticks=False)
+    got = action_log_jsonl(log)
+    assert got.count("\n") > 100
+    assert got == want
