@@ -1081,9 +1081,12 @@ def latency_leg(args, api, dev, stream):
             times.append(a.elapsed_time(b))
     ms = float(np.mean(times))
     ttft = out[0].cpu().numpy()
+    pct = np.arange(1, 100, dtype=np.int32)
+    nearest_rank(api, ttft, pct, device=dev)  # first call loads the sort kernels (lazy module loading)
     t0 = time.perf_counter()
-    cdf = nearest_rank(api, ttft, np.arange(1, 100, dtype=np.int32), device=dev)
-    cdf_ms = 1e3 * (time.perf_counter() - t0)
+    for _ in range(3):
+        cdf = nearest_rank(api, ttft, pct, device=dev)
+    cdf_ms = 1e3 * (time.perf_counter() - t0) / 3
     alg = n * (4 + 8 * 4 + 8 * 3)
     return {"workload": f"{n} stage requests over {nb} backends: ttft / total / service delay, then the 99-point TTFT CDF",
             "requests": n, "ms": ms, "requests_per_s": n / (ms / 1e3),
