@@ -383,6 +383,19 @@ def run_ours(args, rank, world, local_rank):
             e2e_step()
             e2e_t.append(time.perf_counter() - t0)
         assert (h_M == wl["expect_M"]).all()
+        # the host link the e2e number is bound by: a plain pinned H2D copy of the same bytes
+        h_probe = torch.empty(h_wf.nbytes + h_off.nbytes + h_tok.nbytes, dtype=torch.uint8).pin_memory()
+        d_probe = torch.empty_like(h_probe, device=dev)
+        pcie = []
+        for _ in range(4):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            d_probe.copy_(h_probe, non_blocking=True)
+            b.record()
+            torch.cuda.synchronize()
+            pcie.append(h_probe.numel() / (a.elapsed_time(b) / 1e3) / 1e9)
+        pcie_gbps = max(pcie[1:])
+        del h_probe, d_probe
         local_e2e_ms = 1e3 * float(np.mean(e2e_t))
         e2e_ms = sfdist.max_over_ranks(local_e2e_ms, dev)
         e2e_value = sfdist.aggregate_rate(req_blocks, local_e2e_ms, dev)
@@ -425,7 +438,9 @@ def run_ours(args, rank, world, local_rank):
             "roofline": roof,
             "e2e": {"value": e2e_value, "unit": "blocks/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                    "ms_per_step": e2e_ms},
+                    "ms_per_step": e2e_ms, "h2d_gbps": h2d / (e2e_ms / 1e3) / 1e9,
+                    "pinned_h2d_copy_gbps": pcie_gbps,
+                    "frac_of_host_link": h2d / (e2e_ms / 1e3) / 1e9 / pcie_gbps},
             "gpu_launches": 3 * args.steps,  # match_prep + match_block + match_chain per step
             "m_only": m_only,
             "clocks": clocks,
