@@ -1002,7 +1002,7 @@ def tokenize_leg(args, api, dev, stream, hbm_peak):
     d_moff = torch.from_numpy(msg_off).to(dev)
     d_text = torch.from_numpy(np.concatenate([text, np.zeros(16, np.uint8)])).to(dev)
     d_off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-    d_tok = torch.zeros((nbytes + 1) // 2 + 1, dtype=torch.int32, device=dev)
+    d_tok = torch.zeros((nbytes + n + 1) // 2 + 1, dtype=torch.int32, device=dev)  # (n_bytes + n_msg + 1) / 2
     d_nt = torch.zeros(1, dtype=torch.int64, device=dev)
 
     def step():
@@ -1034,6 +1034,11 @@ def tokenize_leg(args, api, dev, stream, hbm_peak):
                        "vocabulary, one message each); steady state: every word already interned",
            "tokens_per_step": nt, "bytes_per_step": nbytes, "ms": ms, "tokens_per_s": nt / (ms / 1e3),
            "text_gbps": nbytes / (ms / 1e3) / 1e9, "interned": it.size()}
+    # HBM roofline: text in (1 B/byte) + ids out (4 B/token) + offsets; the interner table
+    # (16 B slot per token probe) is L2-resident and not counted
+    alg = nbytes + 4 * nt + 8 * (n + 1) * 3
+    out["roofline"] = {"bound": "hbm", "alg_bytes_per_step": alg, "achieved": alg / (ms / 1e3) / 1e9,
+                       "peak": hbm_peak, "unit": "GB/s", "frac": alg / (ms / 1e3) / 1e9 / hbm_peak}
     it.close()
     L = ref_lib()
     if L is not None and not args.no_cpu_baseline:

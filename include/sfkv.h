@@ -212,7 +212,7 @@ int sfkv_handoff_recv_batch_dev(sfkv_pool* dst, const sfkv_peer* src, int64_t n,
  * to the interner are numbered in order of first occurrence in the batch (deterministic). Text is
  * a CSR of messages (msg_off over text bytes) and requests are ranges of messages (req_msg_off).
  * Output: the token CSR the match / commit entry points take (tok_off[n+1], tok). tok must hold
- * (n_bytes + 1) / 2 ids. A batch that would overflow the interner or that meets a 64-bit hash
+ * (n_bytes + n_msg + 1) / 2 ids (a message of L bytes splits into at most (L + 1) / 2 tokens). A batch that would overflow the interner or that meets a 64-bit hash
  * collision between different strings fails without changing the interner (SFKV_EPOOL /
  * SFKV_ECOLLIDE). */
 typedef struct sfkv_interner sfkv_interner;

@@ -536,7 +536,7 @@ class Interner:
         """-> (tok_off int64[n+1], tok uint32[T]) for a list of requests (lists of messages)."""
         req, moff, text = text_batch(requests)
         nbytes = int(moff[-1])
-        cap = max((nbytes + 1) // 2, 1)
+        cap = max((nbytes + len(moff) - 1 + 1) // 2, 1)  # (n_bytes + n_msg + 1) / 2
         tok_off = np.zeros(len(requests) + 1, np.int64)
         tok = np.zeros(cap, np.uint32)
         nt = C.c_int64()

@@ -336,15 +336,18 @@ __global__ void __launch_bounds__(256) rank_count_kernel(TokArgs a) {
   using BR = cub::BlockReduce<int, 256>;
   __shared__ typename BR::TempStorage tmp;
   const int64_t nt = *a.n_tokens;
-  const int64_t t0 = (int64_t)blockIdx.x * RANK_TILE;
-  if (a.ctr[5] == 0 || a.ctr[2] || t0 >= nt) return;
-  int c = 0;
-  for (int k = 0; k < RANK_TILE / 256; ++k) {
-    const int64_t t = t0 + (int64_t)k * 256 + threadIdx.x;
-    if (t < nt) c += a.tnew[t];
+  if (a.ctr[5] == 0 || a.ctr[2]) return;  // steady state: no new string
+  for (int64_t tile = blockIdx.x; tile * RANK_TILE < nt; tile += gridDim.x) {
+    const int64_t t0 = tile * RANK_TILE;
+    int c = 0;
+    for (int k = 0; k < RANK_TILE / 256; ++k) {
+      const int64_t t = t0 + (int64_t)k * 256 + threadIdx.x;
+      if (t < nt) c += a.tnew[t];
+    }
+    c = BR(tmp).Sum(c);
+    if (threadIdx.x == 0) a.tile_cnt[tile] = c;
+    __syncthreads();  // tmp reused
   }
-  c = BR(tmp).Sum(c);
-  if (threadIdx.x == 0) a.tile_cnt[blockIdx.x] = c;
 }
 
 __global__ void __launch_bounds__(1024) rank_scan_kernel(TokArgs a) {
@@ -367,12 +370,10 @@ __global__ void __launch_bounds__(1024) rank_scan_kernel(TokArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(256) rank_publish_kernel(TokArgs a) {
+__device__ void rank_publish_tile(const TokArgs& a, int64_t tile, int64_t nt,
+                                  typename cub::BlockScan<int, 256>::TempStorage& tmp) {
   using BS = cub::BlockScan<int, 256>;
-  __shared__ typename BS::TempStorage tmp;
-  const int64_t nt = *a.n_tokens;
-  const int64_t t0 = (int64_t)blockIdx.x * RANK_TILE;
-  if (a.ctr[5] == 0 || a.ctr[2] || t0 >= nt) return;
+  const int64_t t0 = tile * RANK_TILE;
   constexpr int PT = RANK_TILE / 256;
   const int64_t tb = t0 + (int64_t)threadIdx.x * PT;  // blocked
   int c = 0;
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(256) rank_publish_kernel(TokArgs a) {
     }
   int ex;
   BS(tmp).ExclusiveSum(c, ex);
-  int64_t id = (int64_t)a.ctr[0] + a.tile_cnt[blockIdx.x] + ex;
+  int64_t id = (int64_t)a.ctr[0] + a.tile_cnt[tile] + ex;
   while (f) {
     const int k = __ffs(f) - 1;
     f &= f - 1;
@@ -400,6 +401,16 @@ __global__ void __launch_bounds__(256) rank_publish_kernel(TokArgs a) {
     a.id_len[id] = len;
     a.tok[t] = (uint32_t)id;
     ++id;
+  }
+}
+
+__global__ void __launch_bounds__(256) rank_publish_kernel(TokArgs a) {
+  __shared__ typename cub::BlockScan<int, 256>::TempStorage tmp;
+  const int64_t nt = *a.n_tokens;
+  if (a.ctr[5] == 0 || a.ctr[2]) return;  // steady state: no new string
+  for (int64_t tile = blockIdx.x; tile * RANK_TILE < nt; tile += gridDim.x) {
+    rank_publish_tile(a, tile, nt, tmp);
+    __syncthreads();  // tmp reused
   }
 }
 
@@ -475,15 +486,15 @@ __global__ void interner_init_kernel(TSlot* slots, int64_t* owner, int64_t n) {
   }
 }
 
-// Device-pointer batch. tok must hold (n_bytes + 1) / 2 ids (the most a byte string can split
-// into); text must be 16-B aligned.
+// Device-pointer batch. tok must hold (n_bytes + n_msg + 1) / 2 ids (a message of L bytes splits
+// into at most (L + 1) / 2 tokens); text must be 16-B aligned.
 static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg_off, int64_t n_msg,
                         const int64_t* msg_off, const uint8_t* text, int64_t n_bytes, int64_t* tok_off,
                         uint32_t* tok, int64_t* n_tokens) {
   if (reinterpret_cast<uintptr_t>(text) & 15) return fail(SFKV_EINVAL, "tokenize: text must be 16-B aligned");
   cudaStream_t st = it->stream;
   const int64_t nchunks = (n_bytes + CHUNK - 1) / CHUNK;
-  const int64_t tb = (n_bytes + 1) / 2 + 1;  // token bound
+  const int64_t tb = (n_bytes + n_msg + 1) / 2 + 1;  // token bound
   const int64_t nrt = (tb + RANK_TILE - 1) / RANK_TILE;
   const int64_t nwords = n_bytes / 32 + 2;
   Carver cv;
@@ -544,9 +555,10 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   tok_resolve_kernel<<<g, 256, 0, st>>>(a);
   tok_check_kernel<<<1, 32, 0, st>>>(a);
   SFKV_LAUNCH_CHECK("chunk_emit/probe/resolve");
-  rank_count_kernel<<<(unsigned)nrt, 256, 0, st>>>(a);
+  const unsigned rg = (unsigned)(nrt < sms * 4 ? (nrt > 0 ? nrt : 1) : sms * 4);  // grid-stride over tiles
+  rank_count_kernel<<<rg, 256, 0, st>>>(a);
   rank_scan_kernel<<<1, 1024, 0, st>>>(a);
-  rank_publish_kernel<<<(unsigned)nrt, 256, 0, st>>>(a);
+  rank_publish_kernel<<<rg, 256, 0, st>>>(a);
   tok_final_kernel<<<g, 256, 0, st>>>(a);
   tok_final2_kernel<<<g, 256, 0, st>>>(a);
   tok_owner_reset_kernel<<<g, 256, 0, st>>>(a);
@@ -689,10 +701,11 @@ int sfkv_tokenize_batch(sfkv_interner* it, int64_t n, const int64_t* req_msg_off
   if (n_msg > 0 && msg_off[0] != 0) return fail(SFKV_EINVAL, "tokenize_batch: msg_off[0] must be 0");
   for (int64_t m = 0; m < n_msg; ++m)
     if (msg_off[m + 1] < msg_off[m]) return fail(SFKV_EINVAL, "tokenize_batch: msg_off decreasing");
-  if (tok_cap < (n_bytes + 1) / 2) return fail(SFKV_EINVAL, "tokenize_batch: tok_cap < (n_bytes + 1) / 2");
+  if (tok_cap < (n_bytes + n_msg + 1) / 2)
+    return fail(SFKV_EINVAL, "tokenize_batch: tok_cap < (n_bytes + n_msg + 1) / 2");
   DeviceGuard g(it->device);
   cudaStream_t st = it->stream;
-  const int64_t tb = (n_bytes + 1) / 2 + 1;
+  const int64_t tb = (n_bytes + n_msg + 1) / 2 + 1;
   Carver cv;
   const size_t o_rm = cv.take<int64_t>(n + 1), o_mo = cv.take<int64_t>(n_msg + 1), o_tx = cv.take<uint8_t>(n_bytes + 16),
                o_to = cv.take<int64_t>(n + 1), o_tk = cv.take<uint32_t>(tb), o_nt = cv.take<int64_t>(1);

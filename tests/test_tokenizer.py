@@ -106,3 +106,38 @@ def test_gpu_interner_overflow_fails_without_change(gpu_api):
     assert g.size() == n0
     off, tok = g.tokenize([[b"c a b d"]])  # still usable, old ids intact
     assert tok.tolist() == [2, 0, 1, 3]
+
+
+def _edge_batches():
+    rng = np.random.default_rng(5)
+    one_byte = [[bytes([97 + i % 26]) for i in range(5000)], [b"x"] * 3 + [b" "], []]  # 4096 tokens in a chunk
+    long_words = []
+    for _ in range(6):  # tokens up to 600 bytes: across chunk boundaries and past the staged window
+        words = [bytes(int(x) for x in rng.integers(33, 127, size=int(rng.integers(1, 600)))) for _ in range(40)]
+        long_words.append([b" ".join(words), b"\t".join(words[:7])])
+    return [one_byte, long_words]
+
+
+@pytest.mark.skipif(not os.path.exists(REF_LIB), reason="oracle/_ref not built")
+def test_oracle_tokenizer_edge_batches_match_reference(oracle_api):
+    L = C.CDLL(REF_LIB)
+    L.sfref_context_tokens.restype = C.c_longlong
+    L.sfref_context_tokens.argtypes = [C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_longlong), C.c_char_p,
+                                       C.c_longlong, C.POINTER(C.c_longlong), C.c_longlong]
+    it = Interner(oracle_api, table_log2=16, arena_bytes=1 << 20)
+    for reqs in _edge_batches():
+        off, tok = it.tokenize(reqs)
+        for r, msgs in enumerate(reqs):
+            assert [it.token(i) for i in tok[off[r]:off[r + 1]]] == ref_tokens(L, msgs), r
+
+
+@pytest.mark.gpu
+def test_gpu_tokenizer_edge_batches_match_oracle(gpu_api, oracle_api):
+    g = Interner(gpu_api, table_log2=16, arena_bytes=1 << 20)
+    o = Interner(oracle_api, table_log2=16, arena_bytes=1 << 20)
+    for reqs in _edge_batches():
+        go, gt = g.tokenize(reqs)
+        oo, ot = o.tokenize(reqs)
+        np.testing.assert_array_equal(go, oo)
+        np.testing.assert_array_equal(gt, ot)
+    assert g.size() == o.size()
