@@ -20,6 +20,8 @@ reference's SimulatedBackend::prefix_match, simulated_backend.cpp:153-162) over 
            configs[2]: every GPU pulls its predecessor's retained contexts over NVLink
   mm_signals / tokenize / latency_metrics = SURVEY §8f-1 / -2 / -3 legs (batched MemoryManager,
            tokenizer+interner, latency model + TTFT CDF)
+  c1_dropin = configs[0]: the support demo through the reference's harness, unmodified vs over
+           the B200 pool (+ GPU memory manager): wall time and REQ/ACT parity
   roofline / cpu_baseline / clocks / gpu_launches per the driver contract.
 
 --impl reference runs the reference's own prefix_match (oracle/_ref/libsfref.so, compiled from
@@ -387,7 +389,7 @@ def run_ours(args, rank, world, local_rank):
         h_probe = torch.empty(h_wf.nbytes + h_off.nbytes + h_tok.nbytes, dtype=torch.uint8).pin_memory()
         d_probe = torch.empty_like(h_probe, device=dev)
         pcie = []
-        for _ in range(4):
+        for _ in range(8):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             d_probe.copy_(h_probe, non_blocking=True)
@@ -407,6 +409,7 @@ def run_ours(args, rank, world, local_rank):
         mm = None if args.no_mm else mm_leg(args, api, dev, stream)
         tk = None if args.no_tok else tokenize_leg(args, api, dev, stream, hbm_peak)
         lat = None if args.no_lat else latency_leg(args, api, dev, stream)
+        c1 = None if (args.no_c1 or rank != 0) else c1_leg(dev)
     clocks = clk.summary()
 
     # ---- roofline of the match kernel: algorithmic bytes of one launch --------------------
@@ -459,6 +462,8 @@ def run_ours(args, rank, world, local_rank):
         line["tokenize"] = tk
     if lat:
         line["latency_metrics"] = lat
+    if c1:
+        line["c1_dropin"] = c1
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args)
     pool.close()
@@ -1067,6 +1072,60 @@ def tokenize_reference(L, text, msg_off, n_req):
 
 
 
+def c1_leg(dev):
+    """the support demo (4 workflows, 2 backends, 28 stage requests) through the
+    reference's own harness, three ways: the unmodified reference (oracle/_ref/sf_ref_replay), the
+    reference harness over the B200 pool (sf_gpu_replay) and with the GPU memory manager as well
+    (--gpu-memory). Reported: process wall time of each replay (median of 3; the GPU drivers' time
+    includes CUDA context creation) and REQ (P, M) / ACT-log parity against the reference run."""
+    import tempfile
+
+    sys.path.insert(0, os.path.join(REPO, "tests"))
+    from dropin_scenarios import SCENARIOS
+    ref_drv = os.path.join(REPO, "oracle", "_ref", "sf_ref_replay")
+    gpu_drv = os.path.join(REPO, "oracle", "_ref", "sf_gpu_replay")
+    if not (os.path.exists(ref_drv) and os.path.exists(gpu_drv)):
+        return {"unavailable": "oracle/_ref replay drivers not built"}
+    cfg, trace = SCENARIOS["support_demo"]()
+    keys = ("trigger", "ts", "action", "workflow", "backend", "reason")
+    with tempfile.TemporaryDirectory() as d:
+        cp, tp = os.path.join(d, "c.json"), os.path.join(d, "t.jsonl")
+        with open(cp, "w") as f:
+            json.dump(cfg, f)
+        with open(tp, "w") as f:
+            f.write("".join(json.dumps(r) + "\n" for r in trace))
+
+        def run(drv, extra, tag):
+            times, lines = [], None
+            for i in range(3):
+                op = os.path.join(d, f"{tag}{i}.jsonl")
+                t0 = time.perf_counter()
+                subprocess.run([drv, "--config", cp, "--trace", tp, "--out", op] + extra, check=True,
+                               timeout=300, env=dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get(
+                                   "CUDA_VISIBLE_DEVICES", str(dev))) if drv == gpu_drv else None)
+                times.append(1e3 * (time.perf_counter() - t0))
+                with open(op) as f:
+                    lines = [json.loads(l) for l in f]
+            return float(np.median(times)), lines
+
+        ref_ms, ref_out = run(ref_drv, [], "r")
+        gpu_ms, gpu_out = run(gpu_drv, [], "g")
+        gmm_ms, gmm_out = run(gpu_drv, ["--gpu-memory"], "m")
+    want_req = [(l["b"], l["wf"], l["stage"], l["P"], l["M"]) for l in ref_out if l.get("op") == "match"]
+    want_act = [tuple(l[k] for k in keys) for l in ref_out if l["type"] == "act"]
+
+    def parity(out):
+        req = [(l["b"], l["wf"], l["stage"], l["P"], l["M"]) for l in out if l["type"] == "req"]
+        act = [tuple(l[k] for k in keys) for l in out if l["type"] == "act"]
+        return req == want_req and act == want_act
+    return {"workload": "C1: support demo (4 workflows, 2 backends, capacity 200k tokens each, tau 512, "
+                        "tau' 0.85, 100 ms tick, 40 ms tools) through the reference harness",
+            "stage_requests": len(want_req), "actions": len(want_act),
+            "reference_ms": ref_ms, "gpu_pool_ms": gpu_ms, "gpu_pool_and_memory_ms": gmm_ms,
+            "parity_req_act": {"gpu_pool": parity(gpu_out), "gpu_pool_and_memory": parity(gmm_out)},
+            "note": "process wall time incl. startup (GPU: CUDA context); a parity config, not a throughput one"}
+
+
 def latency_leg(args, api, dev, stream):
     """§8f-3: SimulatedBackend::start's timing arithmetic for a batch of 1M stage requests over 8
     backends (device-resident), and the 99-point nearest-rank TTFT CDF of the batch."""
@@ -1149,6 +1208,7 @@ def main():
     ap.add_argument("--no-mm", action="store_true")
     ap.add_argument("--no-tok", action="store_true")
     ap.add_argument("--no-lat", action="store_true")
+    ap.add_argument("--no-c1", action="store_true")
     ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--dist-backend", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--c3-workflows", type=int, default=32)
