@@ -29,12 +29,17 @@ struct LatArgs {
   double* service;
 };
 
-__global__ void latency_kernel(LatArgs a) {
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < a.n; r += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t b = a.backend[r];
-    const double pf = __dadd_rn(a.overhead[b], __dmul_rn(a.prefill[b], (double)(a.P[r] - a.M[r])));
-    const double dc = __dmul_rn(a.decode[b], (double)a.O[r]);
-    const double t = __dadd_rn(a.queue[r], pf);
+// One thread per request (no grid-stride loop: every request's loads are in flight at once; the
+// per-backend parameters are a dependent gather of a few cached lines).
+__global__ void __launch_bounds__(256) latency_kernel(LatArgs a) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < a.n) {
+    const int32_t b = __ldg(a.backend + r);
+    const double q = __ldg(a.queue + r);
+    const int64_t P = __ldg(a.P + r), M = __ldg(a.M + r), O = __ldg(a.O + r);
+    const double pf = __dadd_rn(__ldg(a.overhead + b), __dmul_rn(__ldg(a.prefill + b), (double)(P - M)));
+    const double dc = __dmul_rn(__ldg(a.decode + b), (double)O);
+    const double t = __dadd_rn(q, pf);
     a.ttft[r] = t;
     if (a.total) a.total[r] = __dadd_rn(t, dc);
     if (a.service) a.service[r] = __dadd_rn(pf, dc);
@@ -51,17 +56,6 @@ __global__ void nearest_rank_kernel(const double* sorted, int64_t n, int32_t k, 
   out[i] = sorted[rank - 1];
 }
 
-static int sm_count_m() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
-
 }  // namespace sfkv
 
 using namespace sfkv;
@@ -75,11 +69,12 @@ int sfmet_latency_batch_dev(int32_t device, int64_t n, const int32_t* backend, c
   if (n < 0 || (n > 0 && (!backend || !queue_ms || !P || !M || !O || !overhead || !prefill || !decode || !out_ttft)))
     return fail(SFKV_EINVAL, "latency_batch_dev: bad argument");
   if (n == 0) return 0;
+  if (n > (int64_t)INT32_MAX * 256) return fail(SFKV_EINVAL, "latency_batch_dev: too many requests");
   if (int rc = check_device(device)) return rc;
   DeviceGuard g(device);
   LatArgs a{n, backend, queue_ms, P, M, O, overhead, prefill, decode, out_ttft, out_total, out_service};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  latency_kernel<<<grid_for(n, 256, sm_count_m() * 8), 256, 0, st>>>(a);
+  latency_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a);
   SFKV_LAUNCH_CHECK("latency_kernel");
   return 0;
 }
