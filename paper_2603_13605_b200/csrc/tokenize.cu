@@ -107,7 +107,7 @@ struct TokArgs {
   int64_t n_bytes;
   uint32_t* mbits;       // message-start bitmap
   int64_t* chunk_off;    // [nchunks + 1]
-  int64_t* tstart;       // [token bound]
+  int64_t* tstart;       // [token bound] byte start of pending tokens (claims / duplicates)
   int64_t* pend_t;       // pending tokens (claims / duplicates of new strings)
   int64_t* pend_slot;
   int32_t* pend_len;
@@ -175,8 +175,9 @@ __device__ __forceinline__ bool bytes_equal(const uint8_t* x, const uint8_t* y, 
 __device__ __forceinline__ bool is_mstart(const TokArgs& a, int64_t i) {
   return (a.mbits[i >> 5] >> (i & 31)) & 1u;
 }
-__device__ void probe_token(const TokArgs& a, int64_t t, const uint8_t* p, int len);
-__device__ void probe_key(const TokArgs& a, int64_t t, unsigned long long key, const uint8_t* p, int len);
+__device__ void probe_token(const TokArgs& a, int64_t t, int64_t start, const uint8_t* p, int len);
+__device__ void probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned long long key, const uint8_t* p,
+                          int len);
 
 // Token starts of the chunk in order (CTA scan), and every token probed right here: the chunk's
 // 4 KiB plus OVER bytes of the next chunk and their message-start bits are staged in shared memory,
@@ -238,7 +239,6 @@ __global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
     const int j = __ffs(m) - 1;
     m &= m - 1;
     const int s0 = w0 + j;  // chunk-relative start
-    a.tstart[t] = c0 + s0;
     const unsigned long long rest = bnd >> (j + 1);  // boundaries after the start
     const int span = rest ? __ffsll((long long)rest) : 64 - j;  // token length if found here
     if (rest && (w0 + j + span < stage_end || window_is_text_end)) {
@@ -249,14 +249,14 @@ __global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
         const unsigned long long hi = *reinterpret_cast<const unsigned long long*>(sb + a8 + 8);
         unsigned long long raw = b8 ? (lo >> b8) | (hi << (64 - b8)) : lo;
         raw &= (1ull << (8 * len)) - 1;
-        probe_key(a, t, (1ull << 63) | ((unsigned long long)len << 56) | raw, sb + s0, len);
+        probe_key(a, t, c0 + s0, (1ull << 63) | ((unsigned long long)len << 56) | raw, sb + s0, len);
       } else {
-        probe_token(a, t, sb + s0, len);
+        probe_token(a, t, c0 + s0, sb + s0, len);
       }
     } else {  // the token runs past the staged window: finish it from global memory
       int64_t g = c0 + s0 + 1;
       while (g < a.n_bytes && !is_space(a.text[g]) && !is_mstart(a, g)) ++g;
-      probe_token(a, t, a.text + c0 + s0, (int)(g - (c0 + s0)));
+      probe_token(a, t, c0 + s0, a.text + c0 + s0, (int)(g - (c0 + s0)));
     }
     ++t;
   }
@@ -265,25 +265,31 @@ __global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
 // Probe one token (bytes p[0..len), position t): published strings resolve here (short keys
 // exactly, long keys verified against the arena); claims and duplicates of this batch's new
 // strings go to the pending list.
-__device__ void probe_key(const TokArgs& a, int64_t t, unsigned long long key, const uint8_t* p, int len);
-__device__ void probe_token(const TokArgs& a, int64_t t, const uint8_t* p, int len) {
-  probe_key(a, t, tok_key(p, len), p, len);
+__device__ void probe_token(const TokArgs& a, int64_t t, int64_t start, const uint8_t* p, int len) {
+  probe_key(a, t, start, tok_key(p, len), p, len);
 }
 
-__device__ void probe_key(const TokArgs& a, int64_t t, unsigned long long key, const uint8_t* p, int len) {
+// (start: the token's byte position, recorded only for pending tokens)
+__device__ void probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned long long key, const uint8_t* p,
+                          int len) {
   uint64_t sl = mix64(key) & a.mask;  // short keys are raw bytes: spread them before placing
   int64_t found = -1;
   uint32_t id = TOK_PENDING;
   for (uint64_t probes = 0; probes <= a.mask; ++probes) {
     TSlot* q = a.slots + sl;
-    unsigned long long k = q->key;
+    // key and id in one 16-B load: ids change only between batches (a slot claimed during this
+    // batch keeps TOK_PENDING until the publish pass), so the pair is consistent
+    const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(q);
+    unsigned long long k = w.x;
+    uint32_t qid = (uint32_t)w.y;
     if (k == 0) {
       k = atomicCAS(&q->key, 0ull, key);
       if (k == 0) k = key;  // claimed: its id stays TOK_PENDING until published
+      qid = TOK_PENDING;    // (a slot claimed by anyone during this batch is pending)
     }
     if (k == key) {
       found = (int64_t)sl;
-      id = *(volatile uint32_t*)&q->id;
+      id = qid;
       break;
     }
     sl = (sl + 1) & a.mask;
@@ -298,6 +304,7 @@ __device__ void probe_key(const TokArgs& a, int64_t t, unsigned long long key, c
     a.tok[t] = id;
     return;
   }
+  a.tstart[t] = start;
   atomicMin(reinterpret_cast<unsigned long long*>(a.owner + found), (unsigned long long)t);
   const unsigned long long j = atomicAdd(a.ctr + 4, 1ull);
   a.pend_t[j] = t;
@@ -432,23 +439,35 @@ __global__ void tok_final_kernel(TokArgs a) {
   }
 }
 
-__global__ void tok_final2_kernel(TokArgs a) {
+__global__ void tok_final2_kernel(TokArgs a) {  // duplicates of new strings
   const int64_t np = (int64_t)a.ctr[4];
-  const int64_t nt = *a.n_tokens;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = a.pend_t[j], sl = a.pend_slot[j];
-    if (a.owner[sl] != t) a.tok[t] = a.slots[sl].id;  // duplicates of new strings
+    if (a.owner[sl] != t) a.tok[t] = a.slots[sl].id;
   }
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= a.n_req; r += (int64_t)gridDim.x * blockDim.x) {
-    // first token at or after the request's first byte (tstart is sorted)
+}
+
+// tok_off[r]: tokens before request r's first byte b = its chunk's offset + the token starts in
+// [chunk start, b) (one warp per request, every load of the <= 4 KiB prefix in flight at once).
+__global__ void req_tokoff_kernel(TokArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r <= a.n_req; r += warps) {
     const int64_t b = r < a.n_req ? a.msg_off[a.req_msg_off[r]] : a.n_bytes;
-    int64_t lo = 0, hi = nt;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (a.tstart[mid] < b) lo = mid + 1;
-      else hi = mid;
+    const int64_t c = b / CHUNK;
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < CHUNK / 512; ++k) {
+      const int64_t w = c * CHUNK + 16 * lane + 512 * k;
+      if (w < b) {
+        uint32_t m = start_mask16(a, w);
+        if (b - w < 16) m &= (1u << (b - w)) - 1u;
+        cnt += __popc(m);
+      }
     }
-    a.tok_off[r] = lo;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+    if (lane == 0) a.tok_off[r] = a.chunk_off[c] + cnt;
   }
 }
 
@@ -561,6 +580,7 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   rank_publish_kernel<<<rg, 256, 0, st>>>(a);
   tok_final_kernel<<<g, 256, 0, st>>>(a);
   tok_final2_kernel<<<g, 256, 0, st>>>(a);
+  req_tokoff_kernel<<<grid_for((n_req + 1) * 32, 256, sms * 8), 256, 0, st>>>(a);
   tok_owner_reset_kernel<<<g, 256, 0, st>>>(a);
   tok_commit_kernel<<<1, 32, 0, st>>>(a);
   SFKV_LAUNCH_CHECK("rank/publish/final");
