@@ -14,10 +14,11 @@
 //                       at a time (__vcmpeq4 / __vcmpleu4), start = non-space & (prev space |
 //                       message start)
 //   exclusive scan      over chunks
-//   chunk_emit_kernel   CTA scan inside each chunk: token start positions, in order; the chunk (+256 B)
-//                       is staged in shared memory and every token is probed right there: length,
-//                       key, probe. Tokens of <= 7 bytes key on their own bytes
-//                       (exact); longer ones on a 63-bit hash verified against the arena. A string
+//   chunk_emit_kernel   CTA scan inside each chunk: token start positions, in order, in a shared
+//                       list; the chunk (+256 B) and a boundary bitmap are staged in shared memory
+//                       and the list is probed one token per thread: length, key, probe. Tokens
+//                       of <= 7 bytes key on their own bytes (exact); longer ones on a 63-bit
+//                       hash verified against the arena. A string
 //                       published by an earlier batch resolves here; claims (CAS into an empty
 //                       slot + atomicMin(position): the lowest position owns the new string) and
 //                       duplicates of this batch's new strings go to a pending list
@@ -179,10 +180,11 @@ __device__ void probe_token(const TokArgs& a, int64_t t, int64_t start, const ui
 __device__ void probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned long long key, const uint8_t* p,
                           int len);
 
-// Token starts of the chunk in order (CTA scan), and every token probed right here: the chunk's
-// 4 KiB plus OVER bytes of the next chunk and their message-start bits are staged in shared memory,
-// so a token's end, key and probe need no second pass over the text (tokens running past the
-// staged window fall back to global reads).
+// Token starts of the chunk in order (CTA scan) into a shared list, and every token probed right
+// here, one token per thread (no per-thread token-count divergence): the chunk's 4 KiB plus OVER
+// bytes of the next chunk and their message-start bits are staged in shared memory with a
+// chunk-wide boundary bitmap (space | message start), so a token's end is the next set bit and its
+// key comes from the staged bytes (tokens running past the staged window fall back to global reads).
 constexpr int OVER = 256;
 __global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
   using BS = cub::BlockScan<int, CHUNK_THREADS>;
@@ -211,54 +213,45 @@ __global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
     sbits[threadIdx.x] = (c0 + threadIdx.x * 32 < a.n_bytes) ? a.mbits[w] : 0xffffffffu;
   }
   uint32_t m = start_mask16(a, base);
-  int excl;
-  BS(tmp).ExclusiveSum(__popc(m), excl);  // (its barrier also publishes the staged bytes)
-  int64_t t = a.chunk_off[blockIdx.x] + excl;
+  __shared__ uint16_t slist[CHUNK];
+  __shared__ uint32_t sbnd[(CHUNK + OVER) / 32 + 1];
+  int excl, total;
+  BS(tmp).ExclusiveSum(__popc(m), excl, total);  // (its barrier also publishes the staged bytes)
+  {
+    int k = excl;
+    for (uint32_t mm = m; mm; mm &= mm - 1) slist[k++] = (uint16_t)(threadIdx.x * 16 + __ffs(mm) - 1);
+  }
+  for (int o = threadIdx.x * 16; o < CHUNK + OVER; o += CHUNK_THREADS * 16) {
+    const uint4 v = *reinterpret_cast<const uint4*>(sb + o);
+    const uint32_t sp = space_mask4(v.x) | (space_mask4(v.y) << 4) | (space_mask4(v.z) << 8) | (space_mask4(v.w) << 12);
+    reinterpret_cast<uint16_t*>(sbnd)[o >> 4] = (uint16_t)(sp | ((sbits[o >> 5] >> (o & 31)) & 0xffffu));
+  }
+  __syncthreads();
   const int stage_end = (int)(lim < CHUNK + OVER ? lim : CHUNK + OVER);
-  if (!m) return;
-  // token boundaries (space or message start) for the 64 staged bytes from this thread's window:
-  // a token's end is one find-first-set away (no per-byte loop)
-  const int w0 = threadIdx.x * 16;
-  unsigned long long bnd = 0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const uint4 v = *reinterpret_cast<const uint4*>(sb + w0 + 16 * q);
-    const uint32_t sp = space_mask4(v.x) | (space_mask4(v.y) << 4) | (space_mask4(v.z) << 8) |
-                        (space_mask4(v.w) << 12);
-    bnd |= (unsigned long long)sp << (16 * q);
-  }
-  {  // message starts: 64 bits from bit offset w0 (w0 is a multiple of 16)
-    const int wi = w0 >> 5, sh = w0 & 31;
-    const unsigned long long lo = sbits[wi] | ((unsigned long long)sbits[wi + 1] << 32);
-    const unsigned long long hi = sbits[wi + 2];
-    bnd |= sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
-  }
-  const bool window_is_text_end = stage_end - w0 <= 64 && stage_end == lim;
-  if (stage_end - w0 < 64) bnd |= ~0ull << (stage_end - w0);  // nothing staged past stage_end
-  while (m) {
-    const int j = __ffs(m) - 1;
-    m &= m - 1;
-    const int s0 = w0 + j;  // chunk-relative start
-    const unsigned long long rest = bnd >> (j + 1);  // boundaries after the start
-    const int span = rest ? __ffsll((long long)rest) : 64 - j;  // token length if found here
-    if (rest && (w0 + j + span < stage_end || window_is_text_end)) {
-      const int len = span;
-      if (len <= 7) {  // exact short key from two aligned 8-B shared loads
+  const int64_t tb0 = a.chunk_off[blockIdx.x];
+  for (int i = threadIdx.x; i < total; i += CHUNK_THREADS) {
+    const int s0 = slist[i];
+    int w = (s0 + 1) >> 5;
+    uint32_t bits = sbnd[w] & (~0u << ((s0 + 1) & 31));
+    while (!bits && (w + 1) * 32 < stage_end) bits = sbnd[++w];
+    const int e = bits ? w * 32 + __ffs(bits) - 1 : CHUNK + OVER;
+    if (e < stage_end || (bits && stage_end == lim)) {
+      const int len = e - s0;
+      if (len <= 7) {
         const int a8 = s0 & ~7, b8 = (s0 & 7) * 8;
         const unsigned long long lo = *reinterpret_cast<const unsigned long long*>(sb + a8);
         const unsigned long long hi = *reinterpret_cast<const unsigned long long*>(sb + a8 + 8);
         unsigned long long raw = b8 ? (lo >> b8) | (hi << (64 - b8)) : lo;
         raw &= (1ull << (8 * len)) - 1;
-        probe_key(a, t, c0 + s0, (1ull << 63) | ((unsigned long long)len << 56) | raw, sb + s0, len);
+        probe_key(a, tb0 + i, c0 + s0, (1ull << 63) | ((unsigned long long)len << 56) | raw, sb + s0, len);
       } else {
-        probe_token(a, t, c0 + s0, sb + s0, len);
+        probe_token(a, tb0 + i, c0 + s0, sb + s0, len);
       }
-    } else {  // the token runs past the staged window: finish it from global memory
+    } else {
       int64_t g = c0 + s0 + 1;
       while (g < a.n_bytes && !is_space(a.text[g]) && !is_mstart(a, g)) ++g;
-      probe_token(a, t, c0 + s0, a.text + c0 + s0, (int)(g - (c0 + s0)));
+      probe_token(a, tb0 + i, c0 + s0, a.text + c0 + s0, (int)(g - (c0 + s0)));
     }
-    ++t;
   }
 }
 
