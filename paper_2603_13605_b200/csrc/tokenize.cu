@@ -212,19 +212,28 @@ __global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
     const int64_t w = (c0 >> 5) + threadIdx.x;
     sbits[threadIdx.x] = (c0 + threadIdx.x * 32 < a.n_bytes) ? a.mbits[w] : 0xffffffffu;
   }
-  uint32_t m = start_mask16(a, base);
   __shared__ uint16_t slist[CHUNK];
   __shared__ uint32_t sbnd[(CHUNK + OVER) / 32 + 1];
-  int excl, total;
-  BS(tmp).ExclusiveSum(__popc(m), excl, total);  // (its barrier also publishes the staged bytes)
-  {
-    int k = excl;
-    for (uint32_t mm = m; mm; mm &= mm - 1) slist[k++] = (uint16_t)(threadIdx.x * 16 + __ffs(mm) - 1);
-  }
+  __syncthreads();
+  // from the staged bytes: 16 boundary bits (space | message start) per thread into the bitmap, and
+  // the thread's token starts (non-space after a space or at a message start)
+  uint32_t m = 0;
   for (int o = threadIdx.x * 16; o < CHUNK + OVER; o += CHUNK_THREADS * 16) {
     const uint4 v = *reinterpret_cast<const uint4*>(sb + o);
     const uint32_t sp = space_mask4(v.x) | (space_mask4(v.y) << 4) | (space_mask4(v.z) << 8) | (space_mask4(v.w) << 12);
-    reinterpret_cast<uint16_t*>(sbnd)[o >> 4] = (uint16_t)(sp | ((sbits[o >> 5] >> (o & 31)) & 0xffffu));
+    const uint32_t ms = (sbits[o >> 5] >> (o & 31)) & 0xffffu;
+    reinterpret_cast<uint16_t*>(sbnd)[o >> 4] = (uint16_t)(sp | ms);
+    if (o < CHUNK && base < a.n_bytes) {
+      const uint32_t prev_sp = o > 0 ? (uint32_t)is_space(sb[o - 1])
+                                     : (c0 == 0 ? 1u : (uint32_t)is_space(a.text[c0 - 1]));
+      m = ~sp & (((sp << 1) | prev_sp) | ms) & 0xffffu;
+    }
+  }
+  int excl, total;
+  BS(tmp).ExclusiveSum(__popc(m), excl, total);
+  {
+    int k = excl;
+    for (uint32_t mm = m; mm; mm &= mm - 1) slist[k++] = (uint16_t)(threadIdx.x * 16 + __ffs(mm) - 1);
   }
   __syncthreads();
   const int stage_end = (int)(lim < CHUNK + OVER ? lim : CHUNK + OVER);
