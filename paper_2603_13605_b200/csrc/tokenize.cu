@@ -10,9 +10,9 @@
 //
 // Launches for a batch (text is a CSR of messages, requests are ranges of messages):
 //   msg_mark_kernel     message-start bitmap (a message start is a forced token boundary)
-//   chunk_count_kernel  token starts per 4 KiB chunk: 16-B loads, C-locale space test on 4 bytes
-//                       at a time (__vcmpeq4 / __vcmpleu4), start = non-space & (prev space |
-//                       message start)
+//   chunk_count_kernel  token starts per 4 KiB chunk (a warp each): 16-B loads, C-locale space
+//                       test on 4 bytes at a time (__vcmpeq4 / __vcmpleu4), start = non-space &
+//                       (prev space | message start)
 //   exclusive scan      over chunks
 //   chunk_emit_kernel   CTA scan inside each chunk: token start positions, in order, in a shared
 //                       list; the chunk (+256 B) and a boundary bitmap are staged in shared memory
@@ -155,12 +155,19 @@ __device__ __forceinline__ uint32_t start_mask16(const TokArgs& a, int64_t base)
   return ~sp & (((sp << 1) | prev_sp) | ms) & 0xffffu;
 }
 
-__global__ void __launch_bounds__(CHUNK_THREADS) chunk_count_kernel(TokArgs a, int64_t* counts) {
-  using BR = cub::BlockReduce<int, CHUNK_THREADS>;
-  __shared__ typename BR::TempStorage tmp;
-  const int64_t base = (int64_t)blockIdx.x * CHUNK + (int64_t)threadIdx.x * 16;
-  const int c = BR(tmp).Sum(__popc(start_mask16(a, base)));
-  if (threadIdx.x == 0) counts[blockIdx.x] = c;
+// One warp per chunk: every lane's CHUNK / 512 windows (16-B text + previous byte + start bits)
+// are loaded together, then a warp reduction; no block barrier.
+constexpr int COUNT_WARPS = 8;
+__global__ void __launch_bounds__(COUNT_WARPS * 32) chunk_count_kernel(TokArgs a, int64_t* counts, int64_t nchunks) {
+  const int lane = threadIdx.x & 31;
+  const int64_t chunk = (int64_t)blockIdx.x * COUNT_WARPS + (threadIdx.x >> 5);
+  if (chunk >= nchunks) return;
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < CHUNK / 512; ++k) c += __popc(start_mask16(a, chunk * CHUNK + 512 * k + 16 * lane));
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+  if (lane == 0) counts[chunk] = c;
 }
 
 struct ChunkCount {
@@ -567,7 +574,8 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   SFKV_CUDA(cudaMemsetAsync(a.mbits, 0, nwords * sizeof(uint32_t), st));
   SFKV_CUDA(cudaMemsetAsync(it->ctr + 3, 0, 3 * sizeof(unsigned long long), st));
   if (n_msg > 0) msg_mark_kernel<<<grid_for(n_msg, 256, sms * 4), 256, 0, st>>>(a);
-  if (nchunks > 0) chunk_count_kernel<<<(unsigned)nchunks, CHUNK_THREADS, 0, st>>>(a, counts);
+  if (nchunks > 0)
+    chunk_count_kernel<<<(unsigned)((nchunks + COUNT_WARPS - 1) / COUNT_WARPS), COUNT_WARPS * 32, 0, st>>>(a, counts, nchunks);
   SFKV_LAUNCH_CHECK("msg_mark/chunk_count");
   if (int rc = exclusive_scan(ChunkCount{counts}, nchunks, a.chunk_off, tmp, st)) return rc;
   if (nchunks > 0) chunk_emit_kernel<<<(unsigned)nchunks, CHUNK_THREADS, 0, st>>>(a);
