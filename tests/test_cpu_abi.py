@@ -10,6 +10,7 @@ import pytest
 
 import oracle_lib
 import paper_2603_13605_b200 as pkg
+from paper_2603_13605_b200.abi import Config, Pool
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -175,3 +176,18 @@ def test_oracle_threshold_matches_reference(oracle_api):
     oracle_api.check("thr", oracle_api.threshold_batch(len(s), s.ctypes.data, 100.0, out.ctypes.data))
     for x, o in zip(s, out):
         assert (o == 0) == bool(ref.sfref_map_threshold(float(x), 100.0))
+
+
+def test_oracle_hashes_full_c2_size_fast(oracle_api):
+    """The oracle's chained hashes for the full C2 batch (10k requests, 1.78 M blocks) in seconds:
+    the checker of tests/test_gpu_parity.py::test_full_c2_size_match."""
+    import time
+    import bench
+    wl = bench.make_workload(0x0A1A + 1, 10_000)
+    n = wl["n"]
+    o = Pool(oracle_api, Config(max_workflows=n, n_blocks=1024, capacity_tokens=1 << 40,
+                                max_pin_blocks=int(bench.blocks_of(wl["req_len"]).max()) + 1, table_log2=12))
+    t0 = time.perf_counter()
+    M, h = o.match(np.arange(n, dtype=np.int32), wl["req_off"], wl["req_tok"], want_hash=True)
+    assert time.perf_counter() - t0 < 60
+    assert (M == 0).all() and len(h) == int(bench.blocks_of(wl["req_len"]).sum())

@@ -259,3 +259,32 @@ def test_pool_exhaustion_aborts_batch_cleanly(gpu_api, oracle_api):
     assert g.match(np.array([1], np.int32), off2, tok2)[0] == 100
     lk, hit = g.lookup(off2, tok2)
     assert hit[0] == 96 and (lk[:6] >= 0).all()
+
+
+def _c2_full():
+    import bench
+    return bench, bench.make_workload(0x0A1A + 1, 10_000)
+
+
+def test_full_c2_size_match(gpu_api, oracle_api):
+    """BASELINE configs[1] at full size (10k workflows, 1.7 M pinned blocks, 1.78 M request blocks):
+    M equals the construction's known LCP (a size-independent property: append-only prompts match
+    their whole pin, rewritten ones stop at the rewrite) and every chained block hash equals the
+    oracle's."""
+    bench, wl = _c2_full()
+    n = wl["n"]
+    mpb = int(bench.blocks_of(wl["req_len"]).max()) + 1
+    nb = int(bench.blocks_of(wl["base"]).sum()) + 2 * mpb + 1024
+    g = Pool(gpu_api, Config(max_workflows=n, n_blocks=nb, capacity_tokens=1 << 50, max_pin_blocks=mpb,
+                             table_log2=int(np.ceil(np.log2(2 * nb))) + 1))
+    wf = np.arange(n, dtype=np.int32)
+    for c0 in range(0, n, 2000):
+        c1 = min(n, c0 + 2000)
+        off = wl["pin_off"][c0:c1 + 1] - wl["pin_off"][c0]
+        assert g.commit(wf[c0:c1], off, wl["pin_tok"][wl["pin_off"][c0]:wl["pin_off"][c1]]).all()
+    Mg, hg = g.match(wf, wl["req_off"], wl["req_tok"], want_hash=True)
+    np.testing.assert_array_equal(Mg, wl["expect_M"])
+    o = Pool(oracle_api, Config(max_workflows=n, n_blocks=1024, capacity_tokens=1 << 40, max_pin_blocks=mpb,
+                                table_log2=12))
+    _, ho = o.match(wf, wl["req_off"], wl["req_tok"], want_hash=True)
+    np.testing.assert_array_equal(hg, ho)
