@@ -20,6 +20,7 @@ reference's SimulatedBackend::prefix_match, simulated_backend.cpp:153-162) over 
            configs[2]: every GPU pulls its predecessor's retained contexts over NVLink
   mm_signals / tokenize / latency_metrics = SURVEY §8f-1 / -2 / -3 legs (batched MemoryManager,
            tokenizer+interner, latency model + TTFT CDF)
+  mapper = SURVEY §8 a14: cost argmin + in-order reroute over 100k requests x 8 candidates
   c1_dropin = configs[0]: the support demo through the reference's harness, unmodified vs over
            the B200 pool (+ GPU memory manager): wall time and REQ/ACT parity
   roofline / cpu_baseline / clocks / gpu_launches per the driver contract.
@@ -409,6 +410,7 @@ def run_ours(args, rank, world, local_rank):
         mm = None if args.no_mm else mm_leg(args, api, dev, stream)
         tk = None if args.no_tok else tokenize_leg(args, api, dev, stream, hbm_peak)
         lat = None if args.no_lat else latency_leg(args, api, dev, stream)
+        mp = None if args.no_map else mapper_leg(api, dev, stream, hbm_peak)
         c1 = None if (args.no_c1 or rank != 0) else c1_leg(dev)
     clocks = clk.summary()
 
@@ -462,6 +464,8 @@ def run_ours(args, rank, world, local_rank):
         line["tokenize"] = tk
     if lat:
         line["latency_metrics"] = lat
+    if mp:
+        line["mapper"] = mp
     if c1:
         line["c1_dropin"] = c1
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -1126,6 +1130,52 @@ def c1_leg(dev):
             "note": "process wall time incl. startup (GPU: CUDA context); a parity config, not a throughput one"}
 
 
+def mapper_leg(api, dev, stream, hbm_peak):
+    """stage-mapper cost scoring of R = 100k stage requests x C = 8 candidate
+    (model, backend) pairs (cost = overhead + prefill (P - M) + decode O + queue penalty depth,
+    exact doubles, argmin) followed by reroute_on_overload in request order, through
+    sfmap_cost_batch_dev. Two queue limits: none (pure scoring) and one that saturates candidates
+    part-way through the batch (the in-order reroute walk)."""
+    import torch
+    rng = np.random.default_rng(0x0A1A + 7)
+    n, c = 100_000, 8
+    P = rng.integers(512, 8192, size=n).astype(np.int64)
+    M = (rng.random((n, c)) * P[:, None]).astype(np.int64).reshape(-1)
+    O = rng.integers(0, 512, size=n).astype(np.int64)
+    par = [rng.random(c) * 50, rng.random(c) * 0.02, rng.random(c) * 20, rng.random(c)]
+    alt = np.full((c, c), -1, dtype=np.int32)
+    for i in range(c):
+        alt[i, : c - 1] = [(i + j) % c for j in range(1, c)]
+    t = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in dict(
+        P=P, M=M, O=O, alt=alt, oh=par[0], pf=par[1], dc=par[2], qp=par[3]).items()}
+    d = torch.zeros(c, dtype=torch.int64, device=dev)
+    och = torch.zeros(n, dtype=torch.int32, device=dev)
+    oco = torch.zeros(n, dtype=torch.float64, device=dev)
+    ptr = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+    out = {"workload": f"{n} stage requests x {c} candidates: cost argmin + in-order reroute",
+           "requests": n, "candidates": c}
+    for name, limit in (("no_limit", 0), ("limit_12000", 12_000)):
+        times = []
+        for i in range(8):
+            d.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            api.check("cost_batch_dev", api.cost_batch_dev(
+                dev, n, c, ptr(t["P"]), ptr(t["M"]), ptr(t["O"]), ptr(t["oh"]), ptr(t["pf"]), ptr(t["dc"]),
+                ptr(t["qp"]), ptr(t["alt"]), ptr(d), limit, ptr(och), ptr(oco), C.c_void_p(stream.cuda_stream)))
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i >= 3:
+                times.append(a.elapsed_time(b))
+        ms = float(np.mean(times))
+        rerouted = int((och.cpu().numpy() != np.argmin(
+            (par[0][None, :] + par[1][None, :] * (P[:, None] - M.reshape(n, c)) + par[2][None, :] * O[:, None]), axis=1)).sum())
+        alg = n * (8 * c + 20)  # SURVEY §8d: R x (8 C + 20) B
+        out[name] = {"ms": ms, "requests_per_s": n / (ms / 1e3), "rerouted": rerouted,
+                     "hbm_frac": alg / (ms / 1e3) / 1e9 / hbm_peak}
+    return out
+
+
 def latency_leg(args, api, dev, stream):
     """§8f-3: SimulatedBackend::start's timing arithmetic for a batch of 1M stage requests over 8
     backends (device-resident), and the 99-point nearest-rank TTFT CDF of the batch."""
@@ -1209,6 +1259,7 @@ def main():
     ap.add_argument("--no-tok", action="store_true")
     ap.add_argument("--no-lat", action="store_true")
     ap.add_argument("--no-c1", action="store_true")
+    ap.add_argument("--no-map", action="store_true")
     ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--dist-backend", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--c3-workflows", type=int, default=32)

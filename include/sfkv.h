@@ -380,6 +380,12 @@ int sfmap_cost_batch(int32_t device, int64_t n, int32_t c, const int64_t* P, con
                      const double* decode, const double* queue_penalty,
                      const int32_t* alternates, uint64_t* depth_inout, uint64_t limit,
                      int32_t* out_choice, double* out_cost);
+/* Device pointers (depth_inout too), asynchronous on cuda_stream (NULL = legacy default stream). */
+int sfmap_cost_batch_dev(int32_t device, int64_t n, int32_t c, const int64_t* P, const int64_t* M,
+                         const int64_t* O, const double* overhead, const double* prefill,
+                         const double* decode, const double* queue_penalty,
+                         const int32_t* alternates, uint64_t* depth_inout, uint64_t limit,
+                         int32_t* out_choice, double* out_cost, void* cuda_stream);
 
 /* ---- the chained block hash (shared by the GPU kernels and the CPU oracle) -------------------
  * digest(k, n, t) of block k with n valid tokens t[0..n) (t[j] = 0 for j >= n):

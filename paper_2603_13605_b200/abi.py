@@ -182,6 +182,8 @@ class Api:
                 self._bind(sym, name, [i32] + argt[1:])  # first arg: device ordinal
             else:
                 self._bind("sfo_" + name, name, argt[1:])
+        if kind == "gpu":  # device-pointer mapper batch (+ stream)
+            self._bind("sfmap_cost_batch_dev", "cost_batch_dev", [i32] + GLOBAL_FNS["cost_batch"][1:] + [P])
 
     def _bind(self, sym, name, argt):
         fn = getattr(self.lib, sym)

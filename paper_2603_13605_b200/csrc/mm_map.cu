@@ -15,6 +15,8 @@
 #include <vector>
 
 #include "pool.cuh"
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
 
 namespace sfkv {
 
@@ -138,43 +140,58 @@ __global__ void cost_kernel(CostArgs a) {
 }
 
 // reroute_on_overload in request order (one warp). depth lives in shared memory (c <= 1024).
+// The first choices of RG chunks of 32 requests are loaded together (the pass is a sequential
+// walk: without the prefetch every chunk paid a dependent global round trip).
+constexpr int RG = 8;
 __global__ void reroute_kernel(CostArgs a) {
   extern __shared__ unsigned long long sdepth[];
   const int lane = threadIdx.x;
   for (int j = lane; j < a.c; j += 32) sdepth[j] = a.depth[j];
   __syncwarp();
-  for (int64_t base = 0; base < a.n; base += 32) {
-    const int64_t r = base + lane;
-    const bool act = r < a.n;
-    const int32_t ch = act ? a.choice[r] : -1;
-    // fast path: no request of the chunk sees its candidate at the limit
-    const unsigned peers = __match_any_sync(0xffffffffu, ch);
-    const unsigned lt = (1u << lane) - 1u;
-    const unsigned long long live = act ? sdepth[ch] + __popc(peers & lt) : 0;
-    const bool ok = !act || a.limit == 0 || live < a.limit;
-    if (__all_sync(0xffffffffu, ok)) {
-      __syncwarp();
-      if (act && (peers & lt) == 0) sdepth[ch] += __popc(peers);  // leader of each peer group
-      __syncwarp();
-    } else {
-      for (int j = 0; j < 32; ++j) {
-        if (base + j >= a.n) break;
-        if (lane == 0) {
-          int32_t c0 = a.choice[base + j], pick = c0;
-          if (sdepth[c0] >= a.limit && a.alternates) {
-            for (int32_t t = 0; t < a.c; ++t) {
-              const int32_t alt = a.alternates[c0 * a.c + t];
-              if (alt < 0) break;
-              if (sdepth[alt] < a.limit) {
-                pick = alt;
-                break;
+  for (int64_t group = 0; group < a.n; group += RG * 32) {
+    int32_t chs[RG];
+#pragma unroll
+    for (int u = 0; u < RG; ++u) {
+      const int64_t r = group + u * 32 + lane;
+      chs[u] = r < a.n ? a.choice[r] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < RG; ++u) {
+      const int64_t base = group + u * 32;
+      if (base >= a.n) break;
+      const int64_t r = base + lane;
+      const bool act = r < a.n;
+      const int32_t ch = chs[u];
+      // fast path: no request of the chunk sees its candidate at the limit
+      const unsigned peers = __match_any_sync(0xffffffffu, ch);
+      const unsigned lt = (1u << lane) - 1u;
+      const unsigned long long live = act ? sdepth[ch] + __popc(peers & lt) : 0;
+      const bool ok = !act || a.limit == 0 || live < a.limit;
+      if (__all_sync(0xffffffffu, ok)) {
+        __syncwarp();
+        if (act && (peers & lt) == 0) sdepth[ch] += __popc(peers);  // leader of each peer group
+        __syncwarp();
+      } else {
+        for (int j = 0; j < 32; ++j) {
+          if (base + j >= a.n) break;
+          const int32_t c0 = __shfl_sync(0xffffffffu, ch, j);
+          if (lane == 0) {
+            int32_t pick = c0;
+            if (sdepth[c0] >= a.limit && a.alternates) {
+              for (int32_t t = 0; t < a.c; ++t) {
+                const int32_t alt = a.alternates[c0 * a.c + t];
+                if (alt < 0) break;
+                if (sdepth[alt] < a.limit) {
+                  pick = alt;
+                  break;
+                }
               }
             }
+            if (pick != c0) a.choice[base + j] = pick;
+            sdepth[pick] += 1;
           }
-          a.choice[base + j] = pick;
-          sdepth[pick] += 1;
+          __syncwarp();
         }
-        __syncwarp();
       }
     }
   }
@@ -182,10 +199,159 @@ __global__ void reroute_kernel(CostArgs a) {
   for (int j = lane; j < a.c; j += 32) a.depth[j] = sdepth[j];
 }
 
+// No queue limit: nothing is rerouted, the depths just count the choices (a parallel histogram).
+__global__ void depth_count_kernel(CostArgs a) {
+  extern __shared__ unsigned int scount[];
+  for (int j = threadIdx.x; j < a.c; j += blockDim.x) scount[j] = 0;
+  __syncthreads();
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < a.n; r += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&scount[a.choice[r]], 1u);
+  __syncthreads();
+  for (int j = threadIdx.x; j < a.c; j += blockDim.x)
+    if (scount[j]) atomicAdd(a.depth + j, (unsigned long long)scount[j]);
+}
+
+// reroute_on_overload for c <= 16 candidates, one CTA, in windows of RWIN requests. Depths only grow,
+// so the saturated set S = {j : depth[j] >= limit} grows monotonically (at most c times) and a
+// request's pick is a pure function of (its choice, S): the first unsaturated of (choice,
+// alternates...), else the choice. A window computes every pick under the current S in parallel,
+// scans the picks' one-hot counts (16-bit counters packed four to a u64 word: window counts stay
+// below 2^16, so plain u64 adds never carry across counters), and finds the first request whose
+// increment saturates an unsaturated candidate. Requests up to it are final; S grows and the
+// window restarts after it. Windows: n / RWIN + (saturation events <= c). Alternates live in shared
+// memory; each window's choices are loaded during the previous window.
+template <int W>
+struct PackN {
+  unsigned long long w[W];
+};
+template <int W>
+struct PackAdd {
+  __device__ __forceinline__ PackN<W> operator()(const PackN<W>& x, const PackN<W>& y) const {
+    PackN<W> z;
+#pragma unroll
+    for (int i = 0; i < W; ++i) z.w[i] = x.w[i] + y.w[i];
+    return z;
+  }
+};
+template <int W>
+__device__ __forceinline__ unsigned lane16(const PackN<W>& p, int j) {
+  return (unsigned)((p.w[j >> 2] >> (16 * (j & 3))) & 0xffffu);
+}
+constexpr int RWT = 512;         // threads of the window kernel
+constexpr int RK = 8;            // consecutive requests per thread
+constexpr int RWIN = RWT * RK;   // requests per window (< 2^16: 16-bit counters cannot overflow)
+template <int W>  // W u64 words = 4 W candidates
+__global__ void __launch_bounds__(RWT) reroute_window_kernel(CostArgs a) {
+  using P = PackN<W>;
+  using BS = cub::BlockScan<P, RWT>;
+  using BR = cub::BlockReduce<int, RWT>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ typename BR::TempStorage rtmp;
+  __shared__ unsigned long long sdepth[4 * W];
+  __shared__ int32_t salt[4 * W * 4 * W];
+  __shared__ unsigned ssat;
+  __shared__ int s_p;
+  __shared__ P s_incl;
+  const int tid = threadIdx.x;
+  const int c = a.c;
+  if (tid < c) sdepth[tid] = a.depth[tid];
+  for (int i = tid; i < c * c; i += RWT) salt[i] = a.alternates ? a.alternates[i] : -1;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned m = 0;
+    for (int j = 0; j < c; ++j)
+      if (sdepth[j] >= a.limit) m |= 1u << j;
+    ssat = m;
+  }
+  __syncthreads();
+  int64_t base = 0;
+  int32_t cn[RK];  // this thread's choices in the next window
+#pragma unroll
+  for (int k = 0; k < RK; ++k) cn[k] = (int64_t)tid * RK + k < a.n ? a.choice[tid * RK + k] : 0;
+  while (base < a.n) {
+    const unsigned sat = ssat;
+    const int64_t r0 = base + (int64_t)tid * RK;
+    int32_t c0[RK], pick[RK];
+    P loc;  // this thread's one-hot counts
+#pragma unroll
+    for (int i = 0; i < W; ++i) loc.w[i] = 0ull;
+#pragma unroll
+    for (int k = 0; k < RK; ++k) {
+      c0[k] = cn[k];
+      pick[k] = c0[k];
+      if (r0 + k < a.n && ((sat >> c0[k]) & 1u)) {
+        for (int32_t t = 0; t < c; ++t) {
+          const int32_t alt = salt[c0[k] * c + t];
+          if (alt < 0) break;
+          if (!((sat >> alt) & 1u)) {
+            pick[k] = alt;
+            break;
+          }
+        }
+      }
+      if (r0 + k < a.n) loc.w[pick[k] >> 2] += 1ull << (16 * (pick[k] & 3));
+      // the following window's choice, assuming no saturation event here (else reloaded below)
+      cn[k] = r0 + RWIN + k < a.n ? a.choice[r0 + RWIN + k] : 0;
+    }
+    P zero;
+#pragma unroll
+    for (int i = 0; i < W; ++i) zero.w[i] = 0ull;
+    P pre, total;
+    BS(tmp).ExclusiveScan(loc, pre, zero, PackAdd<W>(), total);
+    int ev = RWIN;  // first request of this thread that saturates an unsaturated candidate
+    {
+      P run = pre;
+#pragma unroll
+      for (int k = 0; k < RK; ++k) {
+        if (ev == RWIN && r0 + k < a.n && !((sat >> pick[k]) & 1u) &&
+            sdepth[pick[k]] + lane16<W>(run, pick[k]) + 1 >= a.limit)
+          ev = tid * RK + k;
+        if (r0 + k < a.n) run.w[pick[k] >> 2] += 1ull << (16 * (pick[k] & 3));
+      }
+    }
+    const int p = BR(rtmp).Reduce(ev, cub::Min());
+    if (tid == 0) s_p = p;
+    __syncthreads();
+    const int pp = s_p;
+#pragma unroll
+    for (int k = 0; k < RK; ++k)
+      if (r0 + k < a.n && tid * RK + k <= pp && pick[k] != c0[k]) a.choice[r0 + k] = pick[k];
+    if (pp < RWIN && tid == pp / RK) {
+      P incl = pre;
+#pragma unroll
+      for (int k = 0; k < RK; ++k)
+        if (tid * RK + k <= pp) incl.w[pick[k] >> 2] += 1ull << (16 * (pick[k] & 3));
+      s_incl = incl;
+      ssat |= 1u << pick[pp % RK];
+    }
+    __syncthreads();
+    if (tid < c) sdepth[tid] += lane16<W>(pp < RWIN ? s_incl : total, tid);
+    if (pp < RWIN) {  // the window restarts after the event: reload
+      base += pp + 1;
+#pragma unroll
+      for (int k = 0; k < RK; ++k) {
+        const int64_t r = base + (int64_t)tid * RK + k;
+        cn[k] = r < a.n ? a.choice[r] : 0;
+      }
+    } else {
+      base += RWIN;
+    }
+    __syncthreads();
+  }
+  if (tid < c) a.depth[tid] = sdepth[tid];
+}
+
 int cost_dev(cudaStream_t st, CostArgs a, int sms) {
   if (a.n > 0) {
     cost_kernel<<<grid_for(a.n, 256, sms * 8), 256, 0, st>>>(a);
-    reroute_kernel<<<1, 32, sizeof(unsigned long long) * (a.c > 0 ? a.c : 1), st>>>(a);
+    if (a.limit == 0)
+      depth_count_kernel<<<grid_for(a.n, 256, sms * 2), 256, sizeof(unsigned) * a.c, st>>>(a);
+    else if (a.c <= 8)
+      reroute_window_kernel<2><<<1, RWT, 0, st>>>(a);
+    else if (a.c <= 16)
+      reroute_window_kernel<4><<<1, RWT, 0, st>>>(a);
+    else
+      reroute_kernel<<<1, 32, sizeof(unsigned long long) * (a.c > 0 ? a.c : 1), st>>>(a);
   }
   SFKV_LAUNCH_CHECK("mapper kernels");
   return 0;
@@ -341,4 +507,37 @@ extern "C" int sfmap_cost_batch(int32_t device, int64_t n, int32_t cc, const int
   SFKV_CUDA(cudaMemcpyAsync(depth_inout, a.depth, cc * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   SFKV_CUDA(cudaStreamSynchronize(st));
   return 0;
+}
+
+// Device pointers, asynchronous on `stream` (NULL: the legacy default stream). The scoring kernel
+// reads depth_inout before the reroute pass (stream-ordered after it) updates it, so the batch-start
+// snapshot needs no copy.
+extern "C" int sfmap_cost_batch_dev(int32_t device, int64_t n, int32_t cc, const int64_t* P, const int64_t* M,
+                                    const int64_t* O, const double* overhead, const double* prefill,
+                                    const double* decode, const double* queue_penalty,
+                                    const int32_t* alternates, uint64_t* depth_inout, uint64_t limit,
+                                    int32_t* out_choice, double* out_cost, void* stream) {
+  if (n < 0 || cc <= 0 || cc > 1024 || !depth_inout || !overhead || !prefill || !decode || !queue_penalty ||
+      (n > 0 && (!P || !M || !O || !out_choice || !out_cost)))
+    return fail(SFKV_EINVAL, "cost_batch_dev: bad argument");
+  if (n == 0) return 0;
+  if (int rc = check_device(device)) return rc;
+  DeviceGuard g(device);
+  CostArgs a;
+  a.n = n;
+  a.c = cc;
+  a.P = P;
+  a.M = M;
+  a.O = O;
+  a.overhead = overhead;
+  a.prefill = prefill;
+  a.decode = decode;
+  a.qpen = queue_penalty;
+  a.alternates = alternates;
+  a.depth = reinterpret_cast<unsigned long long*>(depth_inout);
+  a.depth0 = reinterpret_cast<const unsigned long long*>(depth_inout);
+  a.limit = limit;
+  a.choice = out_choice;
+  a.cost = out_cost;
+  return cost_dev(static_cast<cudaStream_t>(stream), a, ctx_for(device)->sms);
 }

@@ -228,6 +228,42 @@ def test_mapper_cost_and_reroute(gpu_api, oracle_api, limit):
     np.testing.assert_array_equal(dg, do)
 
 
+@pytest.mark.parametrize("c", [8, 12, 20])  # the window pass for c <= 8 / <= 16, the warp walk above
+@pytest.mark.parametrize("limit", [0, 3, 40, 700])
+def test_mapper_device_entry_matches_oracle(gpu_api, oracle_api, limit, c):
+    """sfmap_cost_batch_dev (device pointers, one stream) and sfmap_cost_batch both equal the
+    oracle over 20k requests (many reroute windows, every candidate saturating at limit 700)."""
+    import torch
+    rng = np.random.default_rng(limit + 5 + c)
+    n = 20_000
+    P = rng.integers(1, 4096, size=n).astype(np.int64)
+    M = (rng.random((n, c)) * P[:, None]).astype(np.int64).reshape(-1)
+    O = rng.integers(0, 512, size=n).astype(np.int64)
+    par = [rng.random(c) * 50, rng.random(c) * 2, rng.random(c) * 20, rng.random(c)]
+    alt = np.full((c, c), -1, dtype=np.int32)
+    for i in range(c):
+        alt[i, : c - 1] = [(i + j) % c for j in range(1, c)]
+    d0 = rng.integers(0, 5, size=c).astype(np.uint64)
+    dh, do = d0.copy(), d0.copy()
+    ch, co = _cost(gpu_api, 0, n, c, P, M, O, par, alt, dh, limit)
+    cho, coo = _cost(oracle_api, 0, n, c, P, M, O, par, alt, do, limit)
+    np.testing.assert_array_equal(ch, cho)
+    np.testing.assert_array_equal(co, coo)
+    np.testing.assert_array_equal(dh, do)
+    t = {k: torch.from_numpy(v).cuda() for k, v in dict(P=P, M=M, O=O, alt=alt, d=d0.view(np.int64),
+                                                          oh=par[0], pf=par[1], dc=par[2], qp=par[3]).items()}
+    och = torch.zeros(n, dtype=torch.int32, device="cuda")
+    oco = torch.zeros(n, dtype=torch.float64, device="cuda")
+    ptr = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+    gpu_api.check("cost_batch_dev", gpu_api.cost_batch_dev(
+        0, n, c, ptr(t["P"]), ptr(t["M"]), ptr(t["O"]), ptr(t["oh"]), ptr(t["pf"]), ptr(t["dc"]), ptr(t["qp"]),
+        ptr(t["alt"]), ptr(t["d"]), limit, ptr(och), ptr(oco), None))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(och.cpu().numpy(), ch)
+    np.testing.assert_array_equal(oco.cpu().numpy(), co)
+    np.testing.assert_array_equal(t["d"].cpu().numpy().view(np.uint64), dh)
+
+
 def test_threshold_mapper(gpu_api, oracle_api):
     """test_mapper.cpp:54-89: 80 -> light, 100 -> light (tie), 5000 -> heavy at threshold 100."""
     s = np.array([80, 100, 5000, 100.0000001, -1, 0], dtype=np.float64)
