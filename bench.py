@@ -411,7 +411,7 @@ def run_ours(args, rank, world, local_rank):
         tk = None if args.no_tok else tokenize_leg(args, api, dev, stream, hbm_peak)
         lat = None if args.no_lat else latency_leg(args, api, dev, stream)
         mp = None if args.no_map else mapper_leg(api, dev, stream, hbm_peak)
-        c1 = None if (args.no_c1 or rank != 0) else c1_leg(dev)
+        c1 = None if (args.no_c1 or world > 1) else c1_leg(dev)  # configs[0] is a 1-GPU replay
     clocks = clk.summary()
 
     # ---- roofline of the match kernel: algorithmic bytes of one launch --------------------
