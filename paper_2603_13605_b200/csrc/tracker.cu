@@ -206,6 +206,53 @@ __device__ void sort_segment(int32_t* x, int64_t c) {
   }
 }
 
+// A workflow's (wf, b) tracker entries during its signal replay: for NB <= N they are loaded once
+// into thread-local arrays and written back at the end (every signal used to pay dependent global
+// round trips on them); N = 0 accesses global memory directly.
+template <int N>
+struct Ents {
+  uint8_t pr[N], pv[N];
+  int32_t inf[N];
+  int64_t tok[N];
+  double t[N];
+  __device__ Ents(const TrackerView& v, int64_t e0, int32_t nb) {
+    for (int32_t b = 0; b < nb; ++b) {
+      pr[b] = v.present[e0 + b];
+      pv[b] = v.preserved[e0 + b];
+      inf[b] = v.inflight[e0 + b];
+      tok[b] = v.tokens[e0 + b];
+      t[b] = v.ts[e0 + b];
+    }
+  }
+  __device__ void store(const TrackerView& v, int64_t e0, int32_t nb) const {
+    for (int32_t b = 0; b < nb; ++b) {
+      v.present[e0 + b] = pr[b];
+      v.preserved[e0 + b] = pv[b];
+      v.inflight[e0 + b] = inf[b];
+      v.tokens[e0 + b] = tok[b];
+      v.ts[e0 + b] = t[b];
+    }
+  }
+  __device__ uint8_t& present(int32_t b) { return pr[b]; }
+  __device__ uint8_t& preserved(int32_t b) { return pv[b]; }
+  __device__ int32_t& inflight(int32_t b) { return inf[b]; }
+  __device__ int64_t& tokens(int32_t b) { return tok[b]; }
+  __device__ double& ts(int32_t b) { return t[b]; }
+};
+template <>
+struct Ents<0> {
+  const TrackerView& v;
+  int64_t e0;
+  __device__ Ents(const TrackerView& vv, int64_t e, int32_t) : v(vv), e0(e) {}
+  __device__ void store(const TrackerView&, int64_t, int32_t) const {}
+  __device__ uint8_t& present(int32_t b) { return v.present[e0 + b]; }
+  __device__ uint8_t& preserved(int32_t b) { return v.preserved[e0 + b]; }
+  __device__ int32_t& inflight(int32_t b) { return v.inflight[e0 + b]; }
+  __device__ int64_t& tokens(int32_t b) { return v.tokens[e0 + b]; }
+  __device__ double& ts(int32_t b) { return v.ts[e0 + b]; }
+};
+
+template <int NBC>
 __global__ void __launch_bounds__(32) sig_resolve_kernel(SigArgs a, TrackerView v) {
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= v.W) return;
@@ -213,9 +260,19 @@ __global__ void __launch_bounds__(32) sig_resolve_kernel(SigArgs a, TrackerView 
   if (c == 0) return;
   v.cnt[w] = 0;  // ready for the next batch
   int32_t* seg = a.seg + a.seg_off[w];
-  sort_segment(seg, c);
+  // the usual handful of signal indices sorted in (L1-resident) local memory, longer segments in place
+  constexpr int SMALL = 32;
+  int32_t sx[SMALL];
+  const bool small = c <= SMALL;
+  if (small) {
+    for (int32_t q = 0; q < c; ++q) sx[q] = seg[q];
+    sort_segment(sx, c);
+  } else {
+    sort_segment(seg, c);
+  }
   const int32_t NB = v.NB;
   const int64_t e0 = w * NB;
+  Ents<NBC> E(v, e0, NB);  // the workflow's (wf, b) entries: registers / local memory when NB <= NBC
   // workflow state in registers for the whole segment
   uint8_t completed = v.completed[w];
   unsigned long long started = v.started[w], open = v.open_[w];
@@ -242,10 +299,10 @@ __global__ void __launch_bounds__(32) sig_resolve_kernel(SigArgs a, TrackerView 
     x.ov = a.s.override_ ? a.s.override_[i] : O_NONE;
     return x;
   };
-  Sig nx = load(seg[0]);
+  Sig nx = load(small ? sx[0] : seg[0]);
   for (int32_t q = 0; q < c; ++q) {
     const Sig cur = nx;
-    if (q + 1 < c) nx = load(seg[q + 1]);
+    if (q + 1 < c) nx = load(small ? sx[q + 1] : seg[q + 1]);
     const int64_t i = cur.i;
     const uint8_t kind = cur.kind;
     const bool wfc = kind == K_WF_COMPLETE;
@@ -291,12 +348,12 @@ __global__ void __launch_bounds__(32) sig_resolve_kernel(SigArgs a, TrackerView 
         } else {  // policy_flush_at_boundary (memory.cpp:127-148)
           if (wfc) {
             for (int32_t bb = 0; bb < NB; ++bb)
-              if (v.present[e0 + bb] && v.preserved[e0 + bb]) {
+              if (E.present(bb) && E.preserved(bb)) {
                 rk[na] = A_FLUSH, rb[na] = bb, rr[na] = R_FAB;
                 ++na;
               }
-          } else if (kind == K_START && lvalid && (lb != b || lm != m) && v.present[e0 + lb] &&
-                     v.preserved[e0 + lb]) {
+          } else if (kind == K_START && lvalid && (lb != b || lm != m) && E.present(lb) &&
+                     E.preserved(lb)) {
             rk[0] = A_FLUSH, rb[0] = lb, rr[0] = R_FAB;
             na = 1;
           }
@@ -309,37 +366,38 @@ __global__ void __launch_bounds__(32) sig_resolve_kernel(SigArgs a, TrackerView 
     }
     // apply_and_record (memory.cpp:312-328): a flush that applied erases the entry
     for (int j = 0; j < na; ++j)
-      if (rk[j] == A_FLUSH) v.present[e0 + rb[j]] = 0;
+      if (rk[j] == A_FLUSH) E.present(rb[j]) = 0;
     a.r.count[i] = na;
     // update_tracker (memory.cpp:330-360)
     if (kind == K_START) {
       started |= bit;
       open |= bit;
-      v.inflight[e0 + b] += 1;
+      E.inflight(b) += 1;
     } else if (kind == K_COMPLETE) {
       open &= ~bit;
-      const int32_t f = v.inflight[e0 + b] - 1;
-      v.inflight[e0 + b] = f;
+      const int32_t f = E.inflight(b) - 1;
+      E.inflight(b) = f;
       if (f < 0) {  // adjust_in_flight threw after storing the count (memory.cpp:90-92)
         a.r.status[i] = SFMM_SIG_NEGATIVE_IN_FLIGHT;
         failed = true;
         continue;
       }
-      v.present[e0 + b] = 1;
-      v.preserved[e0 + b] = T > 0;
-      v.tokens[e0 + b] = T;
-      v.ts[e0 + b] = a.s.ts[i];
+      E.present(b) = 1;
+      E.preserved(b) = T > 0;
+      E.tokens(b) = T;
+      E.ts(b) = a.s.ts[i];
       lvalid = 1, lb = b, lm = m, lt = T;
     } else {
       completed = 1;
       for (int32_t bb = 0; bb < NB; ++bb) {
-        v.present[e0 + bb] = 0;
-        v.inflight[e0 + bb] = 0;
+        E.present(bb) = 0;
+        E.inflight(bb) = 0;
       }
       lvalid = 0, started = 0, open = 0, clen = -1;
     }
     a.r.status[i] = SFMM_SIG_OK;
   }
+  E.store(v, e0, NB);
   v.completed[w] = completed;
   v.started[w] = started;
   v.open_[w] = open;
@@ -429,7 +487,10 @@ static int on_signals_dev(sfmm_tracker* t, int64_t n, const sfmm_signals& s, con
   if (int rc = exclusive_scan(CntOf{t->cnt}, t->W, a.seg_off, reinterpret_cast<int64_t*>(base + o_tmp), st))
     return rc;
   sig_scatter_kernel<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(a);
-  sig_resolve_kernel<<<(unsigned)((t->W + 31) / 32), 32, 0, st>>>(a, v);  // spread over every SM
+  if (t->NB <= 8)  // spread over every SM
+    sig_resolve_kernel<8><<<(unsigned)((t->W + 31) / 32), 32, 0, st>>>(a, v);
+  else
+    sig_resolve_kernel<0><<<(unsigned)((t->W + 31) / 32), 32, 0, st>>>(a, v);
   SFKV_LAUNCH_CHECK("sig_scatter/resolve");
   return 0;
 }
