@@ -102,6 +102,9 @@ static void pool_free(sfkv_pool* p) {
   p->io.release();
   p->prep_status.release();
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+  if (p->aux) cudaStreamDestroy(p->aux);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
   delete p;
 }
 

@@ -44,6 +44,7 @@ struct CommitScratch {
   int64_t* rank;          // [items+1]
   int64_t* wprefix;       // [words+1]
   int64_t* alloc_list;    // [items]
+  int32_t* cow_src;       // [items] by alloc rank: the old pin's block at the same index (or -1)
   int64_t* scan_tmp;
 };
 
@@ -320,6 +321,10 @@ __global__ void alloc_kernel(CommitArgs a) {
     int64_t r, k;
     int nval;
     item_coords(a, item, r, k, nval);
+    {  // copy-on-share source, read before install_kernel replaces the pin table
+      const int32_t w = a.wf[r];
+      a.s.cow_src[rk] = a.pin_len[w] >= 0 && k < a.pin_nblk[w] ? a.pin_blk[(int64_t)w * a.max_pin_blocks + k] : -1;
+    }
     uint32_t t[BT];
     load_req_block(a, r, k, nval, t);
     uint4* dst = reinterpret_cast<uint4*>(a.blk_tok + (int64_t)id * BT);
@@ -551,8 +556,7 @@ static int launch_commit_payload(sfkv_pool* p, const CommitArgs& a, const void* 
   j.alloc_list = a.s.alloc_list;
   j.bid = a.s.bid;
   j.n_items = a.n_items;  // rank[bound] = number of new blocks
-  j.old_pin_blk = p->pin_blk;
-  j.max_pin_blocks = p->cfg.max_pin_blocks;
+  j.cow_src = a.s.cow_src;
   j.error = &p->ctr->error;
   return launch_payload(p, j, kv_src, kv_src_off, src, st);
 }
@@ -571,7 +575,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
                o_bid = cv.take<int32_t>(ni), o_hit = cv.take<uint8_t>(ni),
                o_claim = cv.take<uint8_t>(ni), o_cat = cv.take<uint8_t>(ni),
                o_fnh = cv.take<int64_t>(n), o_rank = cv.take<int64_t>(ni + 1),
-               o_wp = cv.take<int64_t>(p->n_words + 1), o_al = cv.take<int64_t>(ni),
+               o_wp = cv.take<int64_t>(p->n_words + 1), o_al = cv.take<int64_t>(ni), o_cow = cv.take<int32_t>(ni),
                o_tmp = cv.take<int64_t>(scan_scratch_elems(ni > p->n_words ? ni : p->n_words) +
                                         scan_scratch_elems(n));
   if (int rc = p->scratch.ensure(cv.off)) return rc;
@@ -598,6 +602,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   a.s.rank = reinterpret_cast<int64_t*>(base + o_rank);
   a.s.wprefix = reinterpret_cast<int64_t*>(base + o_wp);
   a.s.alloc_list = reinterpret_cast<int64_t*>(base + o_al);
+  a.s.cow_src = reinterpret_cast<int32_t*>(base + o_cow);
   a.s.scan_tmp = reinterpret_cast<int64_t*>(base + o_tmp);
 
   // 1. blocks per request, chained hashes, M = LCP(old pin, tokens)
@@ -628,15 +633,30 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   SFKV_CUDA(launch_pdl(refs_kernel, dim3(g), dim3(256), st, a));
   SFKV_CUDA(launch_pdl(clear_owner_kernel, dim3(g), dim3(256), st, a));
   SFKV_LAUNCH_CHECK("alloc/refs");
-  // 3. payload (copy-on-share + staging scatter / handoff pull)
+  // 3. payload (copy-on-share + staging scatter / handoff pull) on the pool stream while
+  // 4. the old pins are released and the new ones installed on the aux stream: the payload reads
+  //    only the batch's own arrays (copy-on-share sources were snapshotted by alloc_kernel), and
+  //    freed blocks cannot be reallocated before the join
+  cudaStream_t meta = st;
   if (a.payload) {
+    if (!p->aux) {
+      SFKV_CUDA(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
+      SFKV_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+      SFKV_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+    }
+    SFKV_CUDA(cudaEventRecord(p->ev_fork, st));
+    SFKV_CUDA(cudaStreamWaitEvent(p->aux, p->ev_fork, 0));
+    meta = p->aux;
     if (int rc = launch_commit_payload(p, a, kv_src, kv_src_off, src, st)) return rc;
   }
-  // 4. release old pins, install new ones
-  SFKV_CUDA(launch_pdl(release_kernel, dim3(grid_for(n * 32, 256, sms * 8)), dim3(256), st, a, 0, (int64_t*)nullptr));
-  SFKV_CUDA(launch_pdl(install_kernel, dim3(g), dim3(256), st, a));
-  SFKV_CUDA(launch_pdl(commit_finish_kernel, dim3(grid_for(n, 256, sms)), dim3(256), st, a));
+  SFKV_CUDA(launch_pdl(release_kernel, dim3(grid_for(n * 32, 256, sms * 8)), dim3(256), meta, a, 0, (int64_t*)nullptr));
+  SFKV_CUDA(launch_pdl(install_kernel, dim3(g), dim3(256), meta, a));
+  SFKV_CUDA(launch_pdl(commit_finish_kernel, dim3(grid_for(n, 256, sms)), dim3(256), meta, a));
   SFKV_LAUNCH_CHECK("release/install");
+  if (meta != st) {
+    SFKV_CUDA(cudaEventRecord(p->ev_join, meta));
+    SFKV_CUDA(cudaStreamWaitEvent(st, p->ev_join, 0));
+  }
   return maybe_rebuild_table(p);
 }
 

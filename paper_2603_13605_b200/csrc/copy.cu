@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256) payload_kernel(PayloadKernelArgs P) {
     j0 = j0 < 0 ? 0 : (j0 > nval ? nval : j0);
     uint8_t* dst = P.kv + (int64_t)j.bid[item] * P.block_bytes + (int64_t)s * BT * P.row;
     if (j0 > 0) {  // copy-on-share: cached rows of the old pin's boundary block
-      const int32_t old = j.old_pin_blk[(int64_t)j.wf[r] * j.max_pin_blocks + k];
+      const int32_t old = j.cow_src[a];
       const uint8_t* src = P.kv + (int64_t)old * P.block_bytes + (int64_t)s * BT * P.row;
       warp_copy(dst, src, j0 * P.row, lane);
     }

@@ -58,6 +58,10 @@ struct sfkv_pool {
   int64_t table_slots = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // commit: the old pins' release and the new pins' install run on `aux` while the payload copy
+  // runs on `stream` (forked after allocation, joined before the call returns its work)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // device state
   int64_t* pin_len = nullptr;
   int32_t* pin_nblk = nullptr;
@@ -125,8 +129,8 @@ struct PayloadJob {
   const int64_t* alloc_list;
   const int32_t* bid;
   int64_t n_items;
-  const int32_t* old_pin_blk;
-  int32_t max_pin_blocks;
+  const int32_t* cow_src;  // per allocated block (alloc order): the old pin's block at the same
+                           // index, snapshotted before the install overwrites the pin table
   const int* error;  // sticky batch error: no bytes move when set
 };
 // Handoff payload source: rows of batch item `item` (request r's block k) come from block
