@@ -9,6 +9,8 @@
 // reference's bit for bit. Percentiles: the samples are radix-sorted on the device and
 // percentile p is sorted[max(1, ceil(p / 100 * n)) - 1], the reference's rank rule.
 #include <cub/device/device_radix_sort.cuh>
+#include <mutex>
+#include <vector>
 
 #include "pool.cuh"
 
@@ -58,6 +60,28 @@ __global__ void nearest_rank_kernel(const double* sorted, int64_t n, int32_t k, 
 
 }  // namespace sfkv
 
+namespace sfkv {
+// Host-pointer entry points: a per-device scratch buffer and stream reused across calls (a
+// cudaMalloc / cudaFree pair per call cost milliseconds: cudaFree synchronizes the device).
+struct MetCtx {
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+  Scratch buf;
+};
+static MetCtx* met_ctx(int dev) {
+  static std::mutex gmu;
+  static std::vector<MetCtx*> ctxs;
+  std::lock_guard<std::mutex> lk(gmu);
+  if ((int)ctxs.size() <= dev) ctxs.resize(dev + 1, nullptr);
+  if (!ctxs[dev]) {
+    auto* c = new MetCtx;
+    cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    ctxs[dev] = c;
+  }
+  return ctxs[dev];
+}
+}  // namespace sfkv
+
 using namespace sfkv;
 
 extern "C" {
@@ -96,15 +120,19 @@ int sfmet_latency_batch(int32_t device, int64_t n, const int32_t* backend, const
                o_m = cv.take<int64_t>(n), o_o = cv.take<int64_t>(n), o_oh = cv.take<double>(n_backends),
                o_pf = cv.take<double>(n_backends), o_dc = cv.take<double>(n_backends), o_t = cv.take<double>(n),
                o_tt = cv.take<double>(n), o_sv = cv.take<double>(n);
-  char* d = nullptr;
-  SFKV_CUDA(cudaMalloc(&d, cv.off));
-  auto up = [&](size_t off, const void* src, size_t bytes) { return cudaMemcpy(d + off, src, bytes, cudaMemcpyHostToDevice); };
+  MetCtx* mc = met_ctx(device);
+  std::lock_guard<std::mutex> lk(mc->mu);
+  if (int rc = mc->buf.ensure(cv.off)) return rc;
+  char* d = mc->buf.as<char>();
+  cudaStream_t st = mc->stream;
+  auto up = [&](size_t off, const void* src, size_t bytes) {
+    return cudaMemcpyAsync(d + off, src, bytes, cudaMemcpyHostToDevice, st);
+  };
   cudaError_t e = cudaSuccess;
   if ((e = up(o_b, backend, n * 4)) != cudaSuccess || (e = up(o_q, queue_ms, n * 8)) != cudaSuccess ||
       (e = up(o_p, P, n * 8)) != cudaSuccess || (e = up(o_m, M, n * 8)) != cudaSuccess ||
       (e = up(o_o, O, n * 8)) != cudaSuccess || (e = up(o_oh, overhead, n_backends * 8)) != cudaSuccess ||
       (e = up(o_pf, prefill, n_backends * 8)) != cudaSuccess || (e = up(o_dc, decode, n_backends * 8)) != cudaSuccess) {
-    cudaFree(d);
     return cuda_fail(e, "latency_batch H2D");
   }
   int rc = sfmet_latency_batch_dev(device, n, reinterpret_cast<int32_t*>(d + o_b), reinterpret_cast<double*>(d + o_q),
@@ -112,14 +140,14 @@ int sfmet_latency_batch(int32_t device, int64_t n, const int32_t* backend, const
                                    reinterpret_cast<int64_t*>(d + o_o), reinterpret_cast<double*>(d + o_oh),
                                    reinterpret_cast<double*>(d + o_pf), reinterpret_cast<double*>(d + o_dc),
                                    reinterpret_cast<double*>(d + o_t), out_total ? reinterpret_cast<double*>(d + o_tt) : nullptr,
-                                   out_service ? reinterpret_cast<double*>(d + o_sv) : nullptr, nullptr);
+                                   out_service ? reinterpret_cast<double*>(d + o_sv) : nullptr, st);
   if (!rc) {
-    if ((e = cudaMemcpy(out_ttft, d + o_t, n * 8, cudaMemcpyDeviceToHost)) != cudaSuccess ||
-        (out_total && (e = cudaMemcpy(out_total, d + o_tt, n * 8, cudaMemcpyDeviceToHost)) != cudaSuccess) ||
-        (out_service && (e = cudaMemcpy(out_service, d + o_sv, n * 8, cudaMemcpyDeviceToHost)) != cudaSuccess))
+    if ((e = cudaMemcpyAsync(out_ttft, d + o_t, n * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess ||
+        (out_total && (e = cudaMemcpyAsync(out_total, d + o_tt, n * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) ||
+        (out_service && (e = cudaMemcpyAsync(out_service, d + o_sv, n * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) ||
+        (e = cudaStreamSynchronize(st)) != cudaSuccess)
       rc = cuda_fail(e, "latency_batch D2H");
   }
-  cudaFree(d);
   return rc;
 }
 
@@ -135,20 +163,24 @@ int sfmet_nearest_rank(int32_t device, int64_t n, const double* samples, int32_t
   Carver cv;
   const size_t o_in = cv.take<double>(n), o_out = cv.take<double>(n), o_p = cv.take<int32_t>(k + 1),
                o_r = cv.take<double>(k + 1), o_tmp = cv.take<char>(tmp_bytes);
-  char* d = nullptr;
-  SFKV_CUDA(cudaMalloc(&d, cv.off));
-  cudaError_t e = cudaMemcpy(d + o_in, samples, n * 8, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && k) e = cudaMemcpy(d + o_p, pct, k * 4, cudaMemcpyHostToDevice);
+  MetCtx* mc = met_ctx(device);
+  std::lock_guard<std::mutex> lk(mc->mu);
+  if (int rc = mc->buf.ensure(cv.off)) return rc;
+  char* d = mc->buf.as<char>();
+  cudaStream_t st = mc->stream;
+  cudaError_t e = cudaMemcpyAsync(d + o_in, samples, n * 8, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && k) e = cudaMemcpyAsync(d + o_p, pct, k * 4, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess)
     e = cub::DeviceRadixSort::SortKeys(d + o_tmp, tmp_bytes, reinterpret_cast<const double*>(d + o_in),
-                                       reinterpret_cast<double*>(d + o_out), (int)n);
+                                       reinterpret_cast<double*>(d + o_out), (int)n, 0, 64, st);
   if (e == cudaSuccess && k) {
-    nearest_rank_kernel<<<(k + 127) / 128, 128>>>(reinterpret_cast<double*>(d + o_out), n, k,
-                                                  reinterpret_cast<int32_t*>(d + o_p), reinterpret_cast<double*>(d + o_r));
+    nearest_rank_kernel<<<(k + 127) / 128, 128, 0, st>>>(reinterpret_cast<double*>(d + o_out), n, k,
+                                                         reinterpret_cast<int32_t*>(d + o_p),
+                                                         reinterpret_cast<double*>(d + o_r));
     e = cudaGetLastError();
   }
-  if (e == cudaSuccess && k) e = cudaMemcpy(out, d + o_r, k * 8, cudaMemcpyDeviceToHost);
-  cudaFree(d);
+  if (e == cudaSuccess && k) e = cudaMemcpyAsync(out, d + o_r, k * 8, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "nearest_rank");
   return 0;
 }
