@@ -17,6 +17,12 @@ and the receiver's commit kernel pulls the payload rows straight out of the send
 NVLink (sfkv_handoff_recv_batch): one kernel, no gather, no staging buffer, no NCCL payload copy.
 Within one process that owns several GPUs, sfkv_handoff does the same transfer.
 
+The second exchange is the **routing step** (`route_step`): every rank computes its pool's M column
+for the whole batch of R stage requests (sfkv_match_batch against the workflows' pins on that
+backend), one all-gather of R x 8 B per rank assembles the R x C matrix, and every rank runs the
+stage mapper (sfmap_cost_batch: cost argmin + in-order reroute) on it, so all ranks agree on the
+assignment without another collective.
+
 `max_over_ranks` / `aggregate_rate` implement bench.py's timing rule (max time over ranks, whole-job
 units / that time).
 """
@@ -195,6 +201,64 @@ class PeerLink:
         st = self.pool.handoff_recv(self.peers[src], wf_dst, off, tok, blocks)
         self.ack(src)
         return st
+
+
+def route_step(api, pool: Pool, wf, tok_off, tok, P, O, overhead, prefill, decode, qpen, alternates, depth,
+               limit: int, device: int = 0, group=None):
+    """SURVEY §8e exchange 2: this rank's backend is candidate `rank`; returns (choice[R], cost[R],
+    depth[C]) — identical on every rank. GPU pools: the M column, the gathered matrix and the mapper
+    stay on the device (sfkv_match_batch_dev, all_gather_into_tensor — in place under NCCL, through
+    the host under gloo — and sfmap_cost_batch_dev); oracle pools run the host entry points with the
+    same exchange."""
+    import ctypes as C
+
+    import torch
+    dist = _dist()
+    world = dist.get_world_size(group)
+    R = len(wf)
+    wf = np.ascontiguousarray(wf, dtype=np.int32)
+    tok_off = np.ascontiguousarray(tok_off, dtype=np.int64)
+    par = [np.ascontiguousarray(x, dtype=np.float64) for x in (overhead, prefill, decode, qpen)]
+    alt = None if alternates is None else np.ascontiguousarray(alternates, dtype=np.int32)
+    P = np.ascontiguousarray(P, dtype=np.int64)
+    O = np.ascontiguousarray(O, dtype=np.int64)
+    depth = np.ascontiguousarray(depth, dtype=np.uint64).copy()
+    if api.kind == "gpu":
+        dev = torch.device("cuda", device)
+        t = lambda x: torch.from_numpy(x).to(dev)  # noqa: E731
+        ptr = lambda x: C.c_void_p(x.data_ptr()) if x is not None else None  # noqa: E731
+        d_wf, d_off, d_tok = t(wf), t(tok_off), t(np.ascontiguousarray(tok, dtype=np.uint32).view(np.int32))
+        m_col = torch.empty(R, dtype=torch.int64, device=dev)
+        api.check("match_dev", api.match_batch_dev(pool.h, R, ptr(d_wf), ptr(d_off), ptr(d_tok), int(tok_off[-1]),
+                                                   ptr(m_col), None))
+        api.check("sync", api.pool_sync(pool.h))
+        mdev = _meta_device(group)  # NCCL: gathered in place on the GPU; gloo: through the host
+        m_all = torch.empty(world * R, dtype=torch.int64, device=mdev)
+        dist.all_gather_into_tensor(m_all, m_col.to(mdev), group=group)
+        M = m_all.to(dev).view(world, R).t().contiguous()  # R x C, request-major
+        d = {k: t(v) for k, v in dict(P=P, O=O, oh=par[0], pf=par[1], dc=par[2], qp=par[3],
+                                      dp=depth.view(np.int64)).items()}
+        d_alt = t(alt) if alt is not None else None
+        choice = torch.empty(R, dtype=torch.int32, device=dev)
+        cost = torch.empty(R, dtype=torch.float64, device=dev)
+        stream = torch.cuda.current_stream(dev)
+        api.check("cost_batch_dev", api.cost_batch_dev(
+            device, R, world, ptr(d["P"]), ptr(M), ptr(d["O"]), ptr(d["oh"]), ptr(d["pf"]), ptr(d["dc"]),
+            ptr(d["qp"]), ptr(d_alt), ptr(d["dp"]), int(limit), ptr(choice), ptr(cost),
+            C.c_void_p(stream.cuda_stream)))
+        stream.synchronize()
+        return choice.cpu().numpy(), cost.cpu().numpy(), d["dp"].cpu().numpy().view(np.uint64)
+    # oracle pools (CPU, gloo): the same exchange through the host entry points
+    m_col = torch.from_numpy(pool.match(wf, tok_off, np.ascontiguousarray(tok, dtype=np.uint32)).astype(np.int64))
+    parts = [torch.empty(R, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(parts, m_col, group=group)
+    M = np.ascontiguousarray(torch.stack(parts, 1).numpy())  # R x C
+    choice = np.zeros(R, np.int32)
+    cost = np.zeros(R, np.float64)
+    api.check("cost_batch", api.cost_batch(R, world, P.ctypes.data, M.ctypes.data, O.ctypes.data,
+                                           *[x.ctypes.data for x in par], alt.ctypes.data if alt is not None else None,
+                                           depth.ctypes.data, int(limit), choice.ctypes.data, cost.ctypes.data))
+    return choice, cost, depth
 
 
 def max_over_ranks(x: float, device=None) -> float:

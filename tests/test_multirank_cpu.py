@@ -98,3 +98,110 @@ def test_two_rank_handoff_and_timing_rule():
     for r in (0, 1):
         assert out[r]["max"] == 2.0
         assert out[r]["rate"] == pytest.approx(200 / 2e-3)
+
+
+def _route_inputs(world):
+    """A shared batch of 64 stage requests and, per backend rank, pins holding different prefixes
+    of them (so every candidate column of M differs)."""
+    rng = np.random.default_rng(9)
+    R = 64
+    base = [rng.integers(1, 1 << 20, size=int(rng.integers(20, 200))).astype(np.uint32) for _ in range(R)]
+    reqs = [np.concatenate([b, rng.integers(1, 1 << 20, size=int(rng.integers(0, 40))).astype(np.uint32)])
+            for b in base]
+    pins = [[b[: int(len(b) * f)] for b, f in zip(base, rng.random(R))] for _ in range(world)]
+    P = np.array([len(x) for x in reqs], np.int64)
+    O = rng.integers(0, 64, size=R).astype(np.int64)
+    par = [rng.random(world) * 5, rng.random(world) * 0.5, rng.random(world), rng.random(world) * 3]
+    alt = np.full((world, world), -1, np.int32)
+    for i in range(world):
+        alt[i, : world - 1] = [(i + j) % world for j in range(1, world)]
+    return reqs, pins, P, O, par, alt
+
+
+def _route_worker(rank, world, port, q, kind="oracle"):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    sys.path.insert(0, os.path.dirname(here))
+    import torch.distributed as dist
+
+    import oracle_lib
+    from paper_2603_13605_b200 import dist as sfdist
+    from paper_2603_13605_b200.abi import Config, Pool, csr
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        if kind == "gpu":  # B200 pools (both ranks on device 0 here: gpurun gives one GPU)
+            import torch
+            torch.cuda.set_device(0)
+            import paper_2603_13605_b200 as pkg
+            api = pkg.api()
+        else:
+            api = oracle_lib.load()
+        reqs, pins, P, O, par, alt = _route_inputs(world)
+        R = len(reqs)
+        pool = Pool(api, Config(max_workflows=R, n_blocks=4096, capacity_tokens=1 << 30, max_pin_blocks=32,
+                                table_log2=14))
+        wf = np.arange(R, dtype=np.int32)
+        assert pool.commit(wf, *csr(pins[rank])).all()
+        off, tok = csr(reqs)
+        res = sfdist.route_step(api, pool, wf, off, tok, P, O, *par, alt, np.zeros(world, np.uint64), limit=20)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, res, None))
+    except Exception:  # pragma: no cover - surfaced by the parent
+        import traceback
+        q.put((rank, None, traceback.format_exc()))
+
+
+def _route_check(oracle_api, kind):
+    from paper_2603_13605_b200.abi import Config, Pool, csr
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_route_worker, args=(r, world, port, q, kind)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        rank, res, err = q.get(timeout=240)
+        assert err is None, err
+        out[rank] = res
+    for p in procs:
+        p.join(timeout=60)
+    reqs, pins, P, O, par, alt = _route_inputs(world)
+    R = len(reqs)
+    wf = np.arange(R, dtype=np.int32)
+    off, tok = csr(reqs)
+    cols = []
+    for b in range(world):
+        pool = Pool(oracle_api, Config(max_workflows=R, n_blocks=4096, capacity_tokens=1 << 30, max_pin_blocks=32,
+                                       table_log2=14))
+        pool.commit(wf, *csr(pins[b]))
+        cols.append(pool.match(wf, off, tok))
+    M = np.ascontiguousarray(np.stack(cols, 1))
+    assert (M[:, 0] != M[:, 1]).any()
+    choice, cost, depth = np.zeros(R, np.int32), np.zeros(R, np.float64), np.zeros(world, np.uint64)
+    oracle_api.check("cost", oracle_api.cost_batch(R, world, P.ctypes.data, M.ctypes.data, O.ctypes.data,
+                                                   *[x.ctypes.data for x in par], alt.ctypes.data,
+                                                   depth.ctypes.data, 20, choice.ctypes.data, cost.ctypes.data))
+    assert depth.max() >= 20  # the queue limit re-routed part of the batch
+    for r in range(world):
+        np.testing.assert_array_equal(out[r][0], choice)
+        np.testing.assert_array_equal(out[r][1], cost)
+        np.testing.assert_array_equal(out[r][2], depth)
+
+
+def test_two_rank_route_step_matches_single_process(oracle_api):
+    """SURVEY §8e exchange 2: each rank's M column + one all-gather + the mapper on every rank gives
+    the assignment one process computes from the full R x C matrix (and all ranks agree)."""
+    _route_check(oracle_api, "oracle")
+
+
+@pytest.mark.gpu
+def test_two_rank_route_step_on_b200_pools(oracle_api):
+    """The same exchange with libsfkv pools: sfkv_match_batch_dev per rank, the all-gather, then
+    sfmap_cost_batch_dev on every rank; equal to the oracle's single-process assignment."""
+    _route_check(oracle_api, "gpu")
