@@ -17,7 +17,8 @@ reference's SimulatedBackend::prefix_match, simulated_backend.cpp:153-162) over 
   kv     = payload legs on a 64 GiB Llama-3-8B-shaped pool: gather of retained pins into
            contiguous staging and a stage commit (copy-on-share + scatter of appended tokens)
   c4_long_context / c5_lookup = BASELINE configs[3] / configs[4] legs; c3_handoff (N > 1) =
-           configs[2]: every GPU pulls its predecessor's retained contexts over NVLink
+           configs[2]: every GPU pulls its predecessor's retained contexts over NVLink;
+           c3_route (N > 1): the distributed routing step (M columns + all-gather + mapper)
   mm_signals / tokenize / latency_metrics = SURVEY §8f-1 / -2 / -3 legs (batched MemoryManager,
            tokenizer+interner, latency model + TTFT CDF)
   mapper = SURVEY §8 a14: cost argmin + in-order reroute over 100k requests x 8 candidates
@@ -407,6 +408,7 @@ def run_ours(args, rank, world, local_rank):
         c5 = None if args.no_c5 else lookup_leg(args, api, dev, stream, hbm_peak, rank)
         c4 = None if args.no_c4 else long_context_leg(args, api, dev, stream, hbm_peak, rank)
         c3 = handoff_leg(args, api, dev, stream, rank, world) if (dist and not args.no_c3) else None
+        route = route_leg(args, api, pool, dev, rank, world) if (dist and not args.no_c3) else None
         mm = None if args.no_mm else mm_leg(args, api, dev, stream)
         tk = None if args.no_tok else tokenize_leg(args, api, dev, stream, hbm_peak)
         lat = None if args.no_lat else latency_leg(args, api, dev, stream)
@@ -458,6 +460,8 @@ def run_ours(args, rank, world, local_rank):
         line["c4_long_context"] = c4
     if c3:
         line["c3_handoff"] = c3
+    if route:
+        line["c3_route"] = route
     if mm:
         line["mm_signals"] = mm
     if tk:
@@ -774,6 +778,44 @@ def long_context_leg(args, api, dev, stream, hbm_peak, rank):
 
 
 NVLINK_GBPS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md; 900 nominal)
+
+
+def route_leg(args, api, pool, dev, rank, world):
+    """BASELINE configs[2] / SURVEY §8e exchange 2 (N > 1): one routing step for the C2 batch of
+    rank 0's workload (10k stage requests, the same on every rank): each rank's M column against its
+    own pool's pins (sfkv_match_batch_dev), one all-gather of R x 8 B, the stage mapper on every rank
+    (sfmap_cost_batch_dev, C = N candidates, queue limit R / N). Wall time per step, max over ranks."""
+    import torch
+
+    from paper_2603_13605_b200 import dist as sfdist
+    wl = make_workload(args.seed, args.workflows)
+    n = wl["n"]
+    rng = np.random.default_rng(args.seed + 5)
+    wf = np.arange(n, dtype=np.int32)
+    P = np.diff(wl["req_off"]).astype(np.int64)
+    O = rng.integers(0, 512, size=n).astype(np.int64)
+    par = [rng.random(world) * 5, rng.random(world) * 0.01, rng.random(world), rng.random(world) * 0.1]
+    alt = np.full((world, world), -1, np.int32)
+    for i in range(world):
+        alt[i, : world - 1] = [(i + j) % world for j in range(1, world)]
+
+    def step():
+        return sfdist.route_step(api, pool, wf, wl["req_off"], wl["req_tok"], P, O, *par, alt,
+                                 np.zeros(world, np.uint64), limit=n // world, device=dev)
+    for _ in range(2):
+        ch, _, _ = step()
+    ts = []
+    for _ in range(5):
+        torch.cuda.synchronize()
+        sfdist._dist().barrier()
+        t0 = time.perf_counter()
+        step()
+        ts.append(1e3 * (time.perf_counter() - t0))
+    ms = sfdist.max_over_ranks(float(np.median(ts)), dev)
+    return {"workload": f"route {n} stage requests over {world} backend ranks (M column per rank + all-gather "
+                        "+ mapper on every rank)", "requests": n, "ms": ms, "requests_per_s": n / (ms / 1e3),
+            "choices_per_rank": np.bincount(ch, minlength=world).tolist(),
+            "note": "host wall time per step incl. H2D of the batch (route_step's public API)"}
 
 
 def handoff_leg(args, api, dev, stream, rank, world):
