@@ -893,6 +893,52 @@ def handoff_leg(args, api, dev, stream, rank, world):
     ms = sfdist.max_over_ranks(local_ms, dev)
     moved = H * ctx * tok_bytes  # bytes pulled over NVLink per rank per step (= egress per GPU)
     gbps = moved / (ms / 1e3) / 1e9
+    baseline = None
+
+    def nccl_baseline():
+        # SURVEY §8e baseline: gather the H pins into a contiguous buffer, ncclSend/ncclRecv it
+        # around the ring, commit from the received buffer (three passes over the bytes)
+        stg_out = torch.empty(moved, dtype=torch.uint8, device=dev)
+        stg_in = torch.empty_like(stg_out)
+        d_src = torch.arange(H, dtype=torch.int32, device=dev)
+        d_goff = torch.arange(H, dtype=torch.int64, device=dev) * (ctx * tok_bytes)
+        b_times = []
+        for it in range(args.warmup + args.steps):
+            tdist.barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            api.check("gather_dev", api.gather_dev(pool.h, H, C.c_void_p(d_src.data_ptr()),
+                                                   C.c_void_p(stg_out.data_ptr()), C.c_void_p(d_goff.data_ptr())))
+            api.check("sync", api.pool_sync(pool.h))
+            if mdev.type == "cuda":  # NCCL: device buffers
+                for w in tdist.batch_isend_irecv([tdist.P2POp(tdist.isend, stg_out, dst),
+                                                  tdist.P2POp(tdist.irecv, stg_in, src)]):
+                    w.wait()
+            else:  # gloo (same-device smoke of this path): through the host
+                h_out, h_in = stg_out.cpu(), torch.empty(moved, dtype=torch.uint8)
+                for w in tdist.batch_isend_irecv([tdist.P2POp(tdist.isend, h_out, dst),
+                                                  tdist.P2POp(tdist.irecv, h_in, src)]):
+                    w.wait()
+                stg_in.copy_(h_in)
+            api.check("commit_dev", api.commit_batch_dev(
+                pool.h, H, C.c_void_p(d_wf.data_ptr()), C.c_void_p(d_off.data_ptr()), C.c_void_p(d_tok.data_ptr()),
+                int(off[-1]), C.c_void_p(stg_in.data_ptr()), C.c_void_p(d_goff.data_ptr()), None,
+                C.c_void_p(d_st.data_ptr())))
+            b.record(stream)
+            torch.cuda.synchronize()
+            assert bool((d_st == 1).all()), "baseline commit rejected"
+            if it >= args.warmup:
+                b_times.append(a.elapsed_time(b))
+            pool.flush_batch(wf_in)
+        b_ms = sfdist.max_over_ranks(float(np.mean(b_times)), dev)
+        return {"what": "gather -> NCCL send/recv ring -> commit from the received buffer",
+                "ms": b_ms, "per_gpu_gbps": moved / (b_ms / 1e3) / 1e9}
+    if tdist.get_backend() == "nccl" or os.environ.get("SFKV_C3_BASELINE_ANY"):
+        try:
+            baseline = nccl_baseline()
+        except Exception as e:  # a baseline must not take the product's numbers down with it
+            baseline = {"error": f"{type(e).__name__}: {e}"[:300]}
     tdist.barrier()
     link.close()
     pool.close()
@@ -908,7 +954,8 @@ def handoff_leg(args, api, dev, stream, rank, world):
                         f"retained {ctx}-token Llama-3-8B contexts of its predecessor "
                         "(CUDA-IPC pull inside the commit kernel)",
             "contexts_per_gpu": H, "bytes_per_gpu_per_step": moved, "ms": ms,
-            "per_gpu_gbps": gbps, "aggregate_gbps": gbps * world, "roofline": roof}
+            "per_gpu_gbps": gbps, "aggregate_gbps": gbps * world, "roofline": roof,
+            "nccl_baseline": baseline}
 
 
 
