@@ -22,6 +22,7 @@ $F -k regex:match_chain --launch-skip 19 --launch-count 1 -o $O/c5_chain $Q > /d
 $F -k regex:chunk_emit --launch-skip 1 --launch-count 1 -o $O/chunk_emit $Q > /dev/null 2>&1
 $F -k regex:sig_resolve --launch-skip 1 --launch-count 1 -o $O/sig_resolve $Q > /dev/null 2>&1
 $F -k regex:latency_kernel --launch-skip 1 --launch-count 1 -o $O/latency $Q > /dev/null 2>&1
+$F -k regex:reroute_window --launch-skip 4 --launch-count 1 -o $O/reroute_window $Q > /dev/null 2>&1
 # KV legs: the last payload launch of this command is a timed 200-workflow stage commit, the
 # last gather launch a timed 32-pin gather
 K="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-c4 --no-c5 --no-mm --no-tok --no-lat --no-c1"
