@@ -132,6 +132,7 @@ struct TokArgs {
 };
 
 __global__ void msg_mark_kernel(TokArgs a) {
+  pdl_enter();
   for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < a.n_msg; m += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = a.msg_off[m];
     if (i < a.n_bytes) atomicOr(a.mbits + (i >> 5), 1u << (i & 31));
@@ -160,6 +161,7 @@ __device__ __forceinline__ uint32_t start_mask16(const TokArgs& a, int64_t base)
 // are loaded together, then a warp reduction; no block barrier.
 constexpr int COUNT_WARPS = 8;
 __global__ void __launch_bounds__(COUNT_WARPS * 32) chunk_count_kernel(TokArgs a, int64_t* counts, int64_t nchunks) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t chunk = (int64_t)blockIdx.x * COUNT_WARPS + (threadIdx.x >> 5);
   if (chunk >= nchunks) return;
@@ -195,6 +197,7 @@ __device__ void probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned l
 // key comes from the staged bytes (tokens running past the staged window fall back to global reads).
 constexpr int OVER = 256;
 __global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
+  pdl_enter();
   using BS = cub::BlockScan<int, CHUNK_THREADS>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ __align__(16) uint8_t sb[CHUNK + OVER];
@@ -327,6 +330,7 @@ __device__ void probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned l
 // Pending tokens: the lowest position owns a new string; the others are duplicates (long keys
 // compare bytes with the owner's: a 64-bit hash collision fails the batch loudly).
 __global__ void tok_resolve_kernel(TokArgs a) {
+  pdl_enter();
   const int64_t np = (int64_t)a.ctr[4];
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = a.pend_t[j], sl = a.pend_slot[j];
@@ -344,6 +348,7 @@ __global__ void tok_resolve_kernel(TokArgs a) {
 
 // Capacity check before anything is published: a failing batch leaves the interner unchanged.
 __global__ void tok_check_kernel(TokArgs a) {
+  pdl_enter();
   if (threadIdx.x || blockIdx.x || a.ctr[2]) return;
   if ((int64_t)(a.ctr[0] + a.ctr[5]) > a.max_ids) a.ctr[2] |= TERR_IDS;
   if ((int64_t)(a.ctr[1] + a.ctr[3]) > a.arena_cap) a.ctr[2] |= TERR_ARENA;
@@ -352,6 +357,7 @@ __global__ void tok_check_kernel(TokArgs a) {
 // New ids in first-occurrence order: owners are ranked by token position (tile counts, a scan
 // over tiles, an in-tile block scan). Every pass exits at once when the batch has no new string.
 __global__ void __launch_bounds__(256) rank_count_kernel(TokArgs a) {
+  pdl_enter();
   using BR = cub::BlockReduce<int, 256>;
   __shared__ typename BR::TempStorage tmp;
   const int64_t nt = *a.n_tokens;
@@ -370,6 +376,7 @@ __global__ void __launch_bounds__(256) rank_count_kernel(TokArgs a) {
 }
 
 __global__ void __launch_bounds__(1024) rank_scan_kernel(TokArgs a) {
+  pdl_enter();
   using BS = cub::BlockScan<int64_t, 1024>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ int64_t carry;
@@ -424,6 +431,7 @@ __device__ void rank_publish_tile(const TokArgs& a, int64_t tile, int64_t nt,
 }
 
 __global__ void __launch_bounds__(256) rank_publish_kernel(TokArgs a) {
+  pdl_enter();
   __shared__ typename cub::BlockScan<int, 256>::TempStorage tmp;
   const int64_t nt = *a.n_tokens;
   if (a.ctr[5] == 0 || a.ctr[2]) return;  // steady state: no new string
@@ -437,6 +445,7 @@ __global__ void __launch_bounds__(256) rank_publish_kernel(TokArgs a) {
 // are rolled back: the table returns to its pre-batch state — claims sit at the first empty slot
 // of their probe path, so clearing them restores every chain).
 __global__ void tok_final_kernel(TokArgs a) {
+  pdl_enter();
   const int64_t np = (int64_t)a.ctr[4];
   const bool failed = a.ctr[2] != 0;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x) {
@@ -452,6 +461,7 @@ __global__ void tok_final_kernel(TokArgs a) {
 }
 
 __global__ void tok_final2_kernel(TokArgs a) {  // duplicates of new strings
+  pdl_enter();
   const int64_t np = (int64_t)a.ctr[4];
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = a.pend_t[j], sl = a.pend_slot[j];
@@ -462,6 +472,7 @@ __global__ void tok_final2_kernel(TokArgs a) {  // duplicates of new strings
 // tok_off[r]: tokens before request r's first byte b = its chunk's offset + the token starts in
 // [chunk start, b) (one warp per request, every load of the <= 4 KiB prefix in flight at once).
 __global__ void req_tokoff_kernel(TokArgs a) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r <= a.n_req; r += warps) {
@@ -484,16 +495,19 @@ __global__ void req_tokoff_kernel(TokArgs a) {
 }
 
 __global__ void tok_owner_reset_kernel(TokArgs a) {
+  pdl_enter();
   const int64_t np = (int64_t)a.ctr[4];
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x)
     a.owner[a.pend_slot[j]] = INT64_MAX;
 }
 
 __global__ void tok_commit_kernel(TokArgs a) {  // advance the id counter once per batch
+  pdl_enter();
   if (threadIdx.x == 0 && blockIdx.x == 0 && !a.ctr[2]) a.ctr[0] += a.ctr[5];
 }
 
 __global__ void copy_count_kernel(const int64_t* chunk_off, int64_t nchunks, int64_t* n_tokens) {
+  pdl_enter();
   *n_tokens = chunk_off[nchunks];
 }
 
@@ -577,26 +591,26 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   const int sms = sm_count_k();
   SFKV_CUDA(cudaMemsetAsync(a.mbits, 0, nwords * sizeof(uint32_t), st));
   SFKV_CUDA(cudaMemsetAsync(it->ctr + 3, 0, 3 * sizeof(unsigned long long), st));
-  if (n_msg > 0) msg_mark_kernel<<<grid_for(n_msg, 256, sms * 4), 256, 0, st>>>(a);
+  if (n_msg > 0) SFKV_CUDA(launch_pdl(msg_mark_kernel, dim3(grid_for(n_msg, 256, sms * 4)), dim3(256), st, a));
   if (nchunks > 0)
-    chunk_count_kernel<<<(unsigned)((nchunks + COUNT_WARPS - 1) / COUNT_WARPS), COUNT_WARPS * 32, 0, st>>>(a, counts, nchunks);
+    SFKV_CUDA(launch_pdl(chunk_count_kernel, dim3((unsigned)((nchunks + COUNT_WARPS - 1) / COUNT_WARPS)), dim3(COUNT_WARPS * 32), st, a, counts, nchunks));
   SFKV_LAUNCH_CHECK("msg_mark/chunk_count");
   if (int rc = exclusive_scan(ChunkCount{counts}, nchunks, a.chunk_off, tmp, st)) return rc;
-  if (nchunks > 0) chunk_emit_kernel<<<(unsigned)nchunks, CHUNK_THREADS, 0, st>>>(a);
-  copy_count_kernel<<<1, 1, 0, st>>>(a.chunk_off, nchunks, n_tokens);
+  if (nchunks > 0) SFKV_CUDA(launch_pdl(chunk_emit_kernel, dim3((unsigned)nchunks), dim3(CHUNK_THREADS), st, a));
+  SFKV_CUDA(launch_pdl(copy_count_kernel, dim3(1), dim3(1), st, a.chunk_off, nchunks, n_tokens));
   const int g = grid_for(tb, 256, sms * 8);
-  tok_resolve_kernel<<<g, 256, 0, st>>>(a);
-  tok_check_kernel<<<1, 32, 0, st>>>(a);
+  SFKV_CUDA(launch_pdl(tok_resolve_kernel, dim3(g), dim3(256), st, a));
+  SFKV_CUDA(launch_pdl(tok_check_kernel, dim3(1), dim3(32), st, a));
   SFKV_LAUNCH_CHECK("chunk_emit/probe/resolve");
   const unsigned rg = (unsigned)(nrt < sms * 4 ? (nrt > 0 ? nrt : 1) : sms * 4);  // grid-stride over tiles
-  rank_count_kernel<<<rg, 256, 0, st>>>(a);
-  rank_scan_kernel<<<1, 1024, 0, st>>>(a);
-  rank_publish_kernel<<<rg, 256, 0, st>>>(a);
-  tok_final_kernel<<<g, 256, 0, st>>>(a);
-  tok_final2_kernel<<<g, 256, 0, st>>>(a);
-  req_tokoff_kernel<<<grid_for((n_req + 1) * 32, 256, sms * 8), 256, 0, st>>>(a);
-  tok_owner_reset_kernel<<<g, 256, 0, st>>>(a);
-  tok_commit_kernel<<<1, 32, 0, st>>>(a);
+  SFKV_CUDA(launch_pdl(rank_count_kernel, dim3(rg), dim3(256), st, a));
+  SFKV_CUDA(launch_pdl(rank_scan_kernel, dim3(1), dim3(1024), st, a));
+  SFKV_CUDA(launch_pdl(rank_publish_kernel, dim3(rg), dim3(256), st, a));
+  SFKV_CUDA(launch_pdl(tok_final_kernel, dim3(g), dim3(256), st, a));
+  SFKV_CUDA(launch_pdl(tok_final2_kernel, dim3(g), dim3(256), st, a));
+  SFKV_CUDA(launch_pdl(req_tokoff_kernel, dim3(grid_for((n_req + 1) * 32, 256, sms * 8)), dim3(256), st, a));
+  SFKV_CUDA(launch_pdl(tok_owner_reset_kernel, dim3(g), dim3(256), st, a));
+  SFKV_CUDA(launch_pdl(tok_commit_kernel, dim3(1), dim3(32), st, a));
   SFKV_LAUNCH_CHECK("rank/publish/final");
   return 0;
 }
