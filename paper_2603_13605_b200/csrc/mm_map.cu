@@ -122,6 +122,7 @@ struct CostArgs {
 
 // Same evaluation order as the oracle, no FMA contraction: bit-identical doubles.
 __global__ void cost_kernel(CostArgs a) {
+  pdl_enter();
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < a.n; r += (int64_t)gridDim.x * blockDim.x) {
     int32_t best = 0;
     double bc = 0;
@@ -144,6 +145,7 @@ __global__ void cost_kernel(CostArgs a) {
 // walk: without the prefetch every chunk paid a dependent global round trip).
 constexpr int RG = 8;
 __global__ void reroute_kernel(CostArgs a) {
+  pdl_enter();
   extern __shared__ unsigned long long sdepth[];
   const int lane = threadIdx.x;
   for (int j = lane; j < a.c; j += 32) sdepth[j] = a.depth[j];
@@ -201,6 +203,7 @@ __global__ void reroute_kernel(CostArgs a) {
 
 // No queue limit: nothing is rerouted, the depths just count the choices (a parallel histogram).
 __global__ void depth_count_kernel(CostArgs a) {
+  pdl_enter();
   extern __shared__ unsigned int scount[];
   for (int j = threadIdx.x; j < a.c; j += blockDim.x) scount[j] = 0;
   __syncthreads();
@@ -242,6 +245,7 @@ constexpr int RK = 8;            // consecutive requests per thread
 constexpr int RWIN = RWT * RK;   // requests per window (< 2^16: 16-bit counters cannot overflow)
 template <int W>  // W u64 words = 4 W candidates
 __global__ void __launch_bounds__(RWT) reroute_window_kernel(CostArgs a) {
+  pdl_enter();
   using P = PackN<W>;
   using BS = cub::BlockScan<P, RWT>;
   using BR = cub::BlockReduce<int, RWT>;
@@ -343,13 +347,13 @@ __global__ void __launch_bounds__(RWT) reroute_window_kernel(CostArgs a) {
 
 int cost_dev(cudaStream_t st, CostArgs a, int sms) {
   if (a.n > 0) {
-    cost_kernel<<<grid_for(a.n, 256, sms * 8), 256, 0, st>>>(a);
+    SFKV_CUDA(launch_pdl(cost_kernel, dim3(grid_for(a.n, 256, sms * 8)), dim3(256), st, a));
     if (a.limit == 0)
       depth_count_kernel<<<grid_for(a.n, 256, sms * 2), 256, sizeof(unsigned) * a.c, st>>>(a);
     else if (a.c <= 8)
-      reroute_window_kernel<2><<<1, RWT, 0, st>>>(a);
+      SFKV_CUDA(launch_pdl(reroute_window_kernel<2>, dim3(1), dim3(RWT), st, a));
     else if (a.c <= 16)
-      reroute_window_kernel<4><<<1, RWT, 0, st>>>(a);
+      SFKV_CUDA(launch_pdl(reroute_window_kernel<4>, dim3(1), dim3(RWT), st, a));
     else
       reroute_kernel<<<1, 32, sizeof(unsigned long long) * (a.c > 0 ? a.c : 1), st>>>(a);
   }

@@ -157,6 +157,7 @@ __global__ void tracker_init_kernel(TrackerView v) {
 }
 
 __global__ void sig_count_kernel(SigArgs a, TrackerView v) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
     a.slot[i] = atomicAdd(&v.cnt[a.s.wf[i]], 1);
 }
@@ -167,6 +168,7 @@ struct CntOf {
 };
 
 __global__ void sig_scatter_kernel(SigArgs a) {
+  pdl_enter();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
     a.seg[a.seg_off[a.s.wf[i]] + a.slot[i]] = (int32_t)i;
 }
@@ -254,6 +256,7 @@ struct Ents<0> {
 
 template <int NBC>
 __global__ void __launch_bounds__(32) sig_resolve_kernel(SigArgs a, TrackerView v) {
+  pdl_enter();
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= v.W) return;
   const int32_t c = v.cnt[w];
@@ -418,6 +421,7 @@ __device__ __forceinline__ bool idle_preserved(const TrackerView& v, int64_t e) 
   return v.present[e] && v.preserved[e] && v.inflight[e] <= 0 && v.util[e % v.NB] > v.tau_p;
 }
 __global__ void tp_init(TrackerView v) {
+  pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < v.NB) {
     v.best_ts[b] = ~0ull;
@@ -426,17 +430,20 @@ __global__ void tp_init(TrackerView v) {
   }
 }
 __global__ void tp_pass1(TrackerView v) {
+  pdl_enter();
   const int64_t E = (int64_t)v.W * v.NB;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
     if (idle_preserved(v, e)) atomicMin(&v.best_ts[e % v.NB], ts_key(v.ts[e]));
 }
 __global__ void tp_pass2(TrackerView v) {
+  pdl_enter();
   const int64_t E = (int64_t)v.W * v.NB;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
     if (idle_preserved(v, e) && ts_key(v.ts[e]) == v.best_ts[e % v.NB])
       atomicMin(&v.best_rank[e % v.NB], v.rank[e / v.NB]);
 }
 __global__ void tp_pass3(TrackerView v) {
+  pdl_enter();
   const int64_t E = (int64_t)v.W * v.NB;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
     const int b = (int)(e % v.NB);
@@ -445,6 +452,7 @@ __global__ void tp_pass3(TrackerView v) {
   }
 }
 __global__ void tp_apply(TrackerView v) {  // victim starts at -1 (all ones) for atomicMin
+  pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= v.NB) return;
   if (v.best_ts[b] == ~0ull) {
@@ -482,15 +490,15 @@ static int on_signals_dev(sfmm_tracker* t, int64_t n, const sfmm_signals& s, con
   a.seg = reinterpret_cast<int32_t*>(base + o_seg);
   const TrackerView v = view(t);
   const int sms = sm_count_t();
-  sig_count_kernel<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(a, v);
+  SFKV_CUDA(launch_pdl(sig_count_kernel, dim3(grid_for(n, 256, sms * 8)), dim3(256), st, a, v));
   SFKV_LAUNCH_CHECK("sig_count_kernel");
   if (int rc = exclusive_scan(CntOf{t->cnt}, t->W, a.seg_off, reinterpret_cast<int64_t*>(base + o_tmp), st))
     return rc;
-  sig_scatter_kernel<<<grid_for(n, 256, sms * 8), 256, 0, st>>>(a);
+  SFKV_CUDA(launch_pdl(sig_scatter_kernel, dim3(grid_for(n, 256, sms * 8)), dim3(256), st, a));
   if (t->NB <= 8)  // spread over every SM
-    sig_resolve_kernel<8><<<(unsigned)((t->W + 31) / 32), 32, 0, st>>>(a, v);
+    SFKV_CUDA(launch_pdl(sig_resolve_kernel<8>, dim3((unsigned)((t->W + 31) / 32)), dim3(32), st, a, v));
   else
-    sig_resolve_kernel<0><<<(unsigned)((t->W + 31) / 32), 32, 0, st>>>(a, v);
+    SFKV_CUDA(launch_pdl(sig_resolve_kernel<0>, dim3((unsigned)((t->W + 31) / 32)), dim3(32), st, a, v));
   SFKV_LAUNCH_CHECK("sig_scatter/resolve");
   return 0;
 }
@@ -713,11 +721,11 @@ int sfmm_pressure_tick(sfmm_tracker* t, const double* util, int32_t* out_victim)
   const TrackerView v = view(t);
   const int bg = (t->NB + 255) / 256;
   const int g2 = grid_for((int64_t)t->W * t->NB, 256, sm_count_t() * 8);
-  tp_init<<<bg, 256, 0, st>>>(v);
-  tp_pass1<<<g2, 256, 0, st>>>(v);
-  tp_pass2<<<g2, 256, 0, st>>>(v);
-  tp_pass3<<<g2, 256, 0, st>>>(v);
-  tp_apply<<<bg, 256, 0, st>>>(v);
+  SFKV_CUDA(launch_pdl(tp_init, dim3(bg), dim3(256), st, v));
+  SFKV_CUDA(launch_pdl(tp_pass1, dim3(g2), dim3(256), st, v));
+  SFKV_CUDA(launch_pdl(tp_pass2, dim3(g2), dim3(256), st, v));
+  SFKV_CUDA(launch_pdl(tp_pass3, dim3(g2), dim3(256), st, v));
+  SFKV_CUDA(launch_pdl(tp_apply, dim3(bg), dim3(256), st, v));
   SFKV_LAUNCH_CHECK("pressure tick kernels");
   SFKV_CUDA(cudaMemcpyAsync(out_victim, t->victim, t->NB * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   SFKV_CUDA(cudaStreamSynchronize(st));
