@@ -157,17 +157,47 @@ __device__ __forceinline__ uint32_t start_mask16(const TokArgs& a, int64_t base)
   return ~sp & (((sp << 1) | prev_sp) | ms) & 0xffffu;
 }
 
-// One warp per chunk: every lane's CHUNK / 512 windows (16-B text + previous byte + start bits)
-// are loaded together, then a warp reduction; no block barrier.
+// One warp per chunk: every lane's CHUNK / 512 windows of 16 bytes are loaded together (predicated
+// loads, no branch between them), the previous byte of a window comes from the neighbouring lane
+// (or the previous round's last lane) instead of another load, then a warp reduction.
 constexpr int COUNT_WARPS = 8;
 __global__ void __launch_bounds__(COUNT_WARPS * 32) chunk_count_kernel(TokArgs a, int64_t* counts, int64_t nchunks) {
   pdl_enter();
+  constexpr int KW = CHUNK / 512;
   const int lane = threadIdx.x & 31;
   const int64_t chunk = (int64_t)blockIdx.x * COUNT_WARPS + (threadIdx.x >> 5);
   if (chunk >= nchunks) return;
+  const int64_t c0 = chunk * CHUNK;
+  uint4 v[KW];
+  uint32_t mw[KW];
+#pragma unroll
+  for (int k = 0; k < KW; ++k) {
+    const int64_t w = c0 + 512 * k + 16 * lane;
+    v[k] = make_uint4(0x20202020u, 0x20202020u, 0x20202020u, 0x20202020u);
+    if (w + 16 <= a.n_bytes) v[k] = __ldg(reinterpret_cast<const uint4*>(a.text + w));
+    mw[k] = w < a.n_bytes ? __ldg(a.mbits + (w >> 5)) : 0u;
+  }
+  uint32_t prev_last = c0 == 0 ? 1u : (uint32_t)is_space(a.text[c0 - 1]);  // before lane 0, round 0
   int c = 0;
 #pragma unroll
-  for (int k = 0; k < CHUNK / 512; ++k) c += __popc(start_mask16(a, chunk * CHUNK + 512 * k + 16 * lane));
+  for (int k = 0; k < KW; ++k) {
+    const int64_t w = c0 + 512 * k + 16 * lane;
+    if (w < a.n_bytes && w + 16 > a.n_bytes) {  // the text's last, partial window: bytes past the end are spaces
+      uint32_t q[4] = {0x20202020u, 0x20202020u, 0x20202020u, 0x20202020u};
+      for (int j = 0; w + j < a.n_bytes; ++j)
+        q[j >> 2] = (q[j >> 2] & ~(0xffu << (8 * (j & 3)))) | ((uint32_t)a.text[w + j] << (8 * (j & 3)));
+      v[k] = make_uint4(q[0], q[1], q[2], q[3]);
+    }
+    const uint32_t sp = space_mask4(v[k].x) | (space_mask4(v[k].y) << 4) | (space_mask4(v[k].z) << 8) |
+                        (space_mask4(v[k].w) << 12);
+    const uint32_t last = (sp >> 15) & 1u;
+    uint32_t prev = __shfl_up_sync(0xffffffffu, last, 1);
+    if (lane == 0) prev = prev_last;
+    prev_last = __shfl_sync(0xffffffffu, last, 31);
+    const uint32_t ms = (mw[k] >> (w & 31)) & 0xffffu;
+    const uint32_t m = w < a.n_bytes ? (~sp & (((sp << 1) | prev) | ms) & 0xffffu) : 0u;
+    c += __popc(m);
+  }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
   if (lane == 0) counts[chunk] = c;
