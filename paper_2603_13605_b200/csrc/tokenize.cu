@@ -49,6 +49,7 @@ struct sfkv_interner {
   unsigned long long* ctr_host = nullptr;
   sfkv::Scratch scratch;
   sfkv::Scratch io;
+  sfkv::Scratch mbits;  // message-start bitmap: all zero between batches (each batch clears its bits)
 };
 
 struct TSlot {
@@ -524,16 +525,23 @@ __global__ void req_tokoff_kernel(TokArgs a) {
   }
 }
 
-__global__ void tok_owner_reset_kernel(TokArgs a) {
+__global__ void tok_owner_reset_kernel(TokArgs a) {  // and the message-start bits of this batch
   pdl_enter();
   const int64_t np = (int64_t)a.ctr[4];
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x)
     a.owner[a.pend_slot[j]] = INT64_MAX;
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < a.n_msg; m += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = a.msg_off[m];
+    if (i < a.n_bytes) a.mbits[i >> 5] = 0u;
+  }
 }
 
 __global__ void tok_commit_kernel(TokArgs a) {  // advance the id counter once per batch
   pdl_enter();
-  if (threadIdx.x == 0 && blockIdx.x == 0 && !a.ctr[2]) a.ctr[0] += a.ctr[5];
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (!a.ctr[2]) a.ctr[0] += a.ctr[5];
+    a.ctr[3] = a.ctr[4] = a.ctr[5] = 0;  // batch counters zero for the next batch
+  }
 }
 
 __global__ void copy_count_kernel(const int64_t* chunk_off, int64_t nchunks, int64_t* n_tokens) {
@@ -573,11 +581,15 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   const int64_t nrt = (tb + RANK_TILE - 1) / RANK_TILE;
   const int64_t nwords = n_bytes / 32 + 2;
   Carver cv;
-  const size_t o_mb = cv.take<uint32_t>(nwords), o_cnt = cv.take<int64_t>(nchunks + 1),
+  const size_t o_cnt = cv.take<int64_t>(nchunks + 1),
                o_co = cv.take<int64_t>(nchunks + 1), o_ts = cv.take<int64_t>(tb), o_pt = cv.take<int64_t>(tb),
                o_ps = cv.take<int64_t>(tb), o_pl = cv.take<int32_t>(tb), o_tc = cv.take<int64_t>(nrt + 1),
                o_tmp = cv.take<int64_t>(scan_scratch_elems(nchunks));
   if (int rc = it->scratch.ensure(cv.off)) return rc;
+  if (it->mbits.bytes < nwords * sizeof(uint32_t)) {  // grown: zero once, then kept zero
+    if (int rc = it->mbits.ensure(nwords * sizeof(uint32_t))) return rc;
+    SFKV_CUDA(cudaMemsetAsync(it->mbits.ptr, 0, it->mbits.bytes, st));
+  }
   if ((size_t)tb > it->tnew_cap) {  // owner flags stay zero between batches
     if (it->tnew) cudaFree(it->tnew);
     it->tnew = nullptr;
@@ -594,7 +606,7 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   a.n_msg = n_msg;
   a.text = text;
   a.n_bytes = n_bytes;
-  a.mbits = reinterpret_cast<uint32_t*>(base + o_mb);
+  a.mbits = it->mbits.as<uint32_t>();
   a.chunk_off = reinterpret_cast<int64_t*>(base + o_co);
   a.tstart = reinterpret_cast<int64_t*>(base + o_ts);
   a.pend_t = reinterpret_cast<int64_t*>(base + o_pt);
@@ -619,8 +631,7 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   int64_t* counts = reinterpret_cast<int64_t*>(base + o_cnt);
   int64_t* tmp = reinterpret_cast<int64_t*>(base + o_tmp);
   const int sms = sm_count_k();
-  SFKV_CUDA(cudaMemsetAsync(a.mbits, 0, nwords * sizeof(uint32_t), st));
-  SFKV_CUDA(cudaMemsetAsync(it->ctr + 3, 0, 3 * sizeof(unsigned long long), st));
+  // (the bitmap and the batch counters ctr[3..5] were left zero by the previous batch's last kernels)
   if (n_msg > 0) SFKV_CUDA(launch_pdl(msg_mark_kernel, dim3(grid_for(n_msg, 256, sms * 4)), dim3(256), st, a));
   if (nchunks > 0)
     SFKV_CUDA(launch_pdl(chunk_count_kernel, dim3((unsigned)((nchunks + COUNT_WARPS - 1) / COUNT_WARPS)), dim3(COUNT_WARPS * 32), st, a, counts, nchunks));
@@ -660,6 +671,7 @@ static void interner_free(sfkv_interner* it) {
   if (it->ctr_host) cudaFreeHost(it->ctr_host);
   it->scratch.release();
   it->io.release();
+  it->mbits.release();
   if (it->own_stream && it->stream) cudaStreamDestroy(it->stream);
 }
 
