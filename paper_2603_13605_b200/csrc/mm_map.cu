@@ -272,8 +272,27 @@ __global__ void __launch_bounds__(RWT) reroute_window_kernel(CostArgs a) {
   int32_t cn[RK];  // this thread's choices in the next window
 #pragma unroll
   for (int k = 0; k < RK; ++k) cn[k] = (int64_t)tid * RK + k < a.n ? a.choice[tid * RK + k] : 0;
+  __shared__ int32_t spick[4 * W];  // pick of each first choice under the current S
+  unsigned sat_done = ~0u;
   while (base < a.n) {
     const unsigned sat = ssat;
+    if (sat != sat_done) {  // S changed (at most c times): rebuild the pick table
+      if (tid < c) {
+        int32_t pk = tid;
+        if ((sat >> tid) & 1u)
+          for (int32_t t = 0; t < c; ++t) {
+            const int32_t alt = salt[tid * c + t];
+            if (alt < 0) break;
+            if (!((sat >> alt) & 1u)) {
+              pk = alt;
+              break;
+            }
+          }
+        spick[tid] = pk;
+      }
+      __syncthreads();
+      sat_done = sat;
+    }
     const int64_t r0 = base + (int64_t)tid * RK;
     int32_t c0[RK], pick[RK];
     P loc;  // this thread's one-hot counts
@@ -282,17 +301,7 @@ __global__ void __launch_bounds__(RWT) reroute_window_kernel(CostArgs a) {
 #pragma unroll
     for (int k = 0; k < RK; ++k) {
       c0[k] = cn[k];
-      pick[k] = c0[k];
-      if (r0 + k < a.n && ((sat >> c0[k]) & 1u)) {
-        for (int32_t t = 0; t < c; ++t) {
-          const int32_t alt = salt[c0[k] * c + t];
-          if (alt < 0) break;
-          if (!((sat >> alt) & 1u)) {
-            pick[k] = alt;
-            break;
-          }
-        }
-      }
+      pick[k] = spick[c0[k]];
       if (r0 + k < a.n) loc.w[pick[k] >> 2] += 1ull << (16 * (pick[k] & 3));
       // the following window's choice, assuming no saturation event here (else reloaded below)
       cn[k] = r0 + RWIN + k < a.n ? a.choice[r0 + RWIN + k] : 0;
