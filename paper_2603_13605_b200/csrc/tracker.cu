@@ -337,6 +337,7 @@ __global__ void __launch_bounds__(32) sig_resolve_kernel(SigArgs a, TrackerView 
         rk[0] = A_NOOP, rb[0] = -1, rr[0] = R_OVERRIDE;
       } else {
         rk[0] = ov == O_FLUSH ? A_FLUSH : A_PRESERVE, rb[0] = lb, rr[0] = R_OVERRIDE;
+        if (ov == O_FLUSH) E.present(lb) = 0;  // applied (erases the entry)
       }
       na = 1;
     } else {
@@ -353,11 +354,13 @@ __global__ void __launch_bounds__(32) sig_resolve_kernel(SigArgs a, TrackerView 
             for (int32_t bb = 0; bb < NB; ++bb)
               if (E.present(bb) && E.preserved(bb)) {
                 rk[na] = A_FLUSH, rb[na] = bb, rr[na] = R_FAB;
+                E.present(bb) = 0;  // applied
                 ++na;
               }
           } else if (kind == K_START && lvalid && (lb != b || lm != m) && E.present(lb) &&
                      E.preserved(lb)) {
             rk[0] = A_FLUSH, rb[0] = lb, rr[0] = R_FAB;
+            E.present(lb) = 0;  // applied
             na = 1;
           }
         }
@@ -367,9 +370,8 @@ __global__ void __launch_bounds__(32) sig_resolve_kernel(SigArgs a, TrackerView 
         na = 1;
       }
     }
-    // apply_and_record (memory.cpp:312-328): a flush that applied erases the entry
-    for (int j = 0; j < na; ++j)
-      if (rk[j] == A_FLUSH) E.present(rb[j]) = 0;
+    // apply_and_record (memory.cpp:312-328): a flush that applied erases the entry — done as each
+    // flush is recorded above (the records are write-only here: no read-back round trip)
     a.r.count[i] = na;
     // update_tracker (memory.cpp:330-360)
     if (kind == K_START) {
