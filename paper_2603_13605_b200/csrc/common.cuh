@@ -190,6 +190,39 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_apply_kernel(F f, int64_t n
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = t0 + agg;
 }
 
+// Small scans (<= 4 tiles): one CTA walks the tiles in order with a running carry — one launch
+// instead of three (the free-bitmap scan of a commit, the tracker's per-workflow counts). At 8
+// tiles the serial walk already cost more than the three-kernel scan.
+#ifndef SFKV_SCAN_SINGLE
+#define SFKV_SCAN_SINGLE 4
+#endif
+constexpr int64_t SCAN_SINGLE_MAX_TILES = SFKV_SCAN_SINGLE;
+template <class F>
+__global__ void __launch_bounds__(SCAN_THREADS) scan_single_kernel(F f, int64_t n, int64_t* out) {
+  using BS = cub::BlockScan<int64_t, SCAN_THREADS>;
+  __shared__ typename BS::TempStorage tmp;
+  pdl_enter();
+  int64_t carry = 0;
+  for (int64_t base = 0; base < n; base += SCAN_TILE) {
+    int64_t v[SCAN_ITEMS];
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+      const int64_t idx = base + (int64_t)threadIdx.x * SCAN_ITEMS + i;  // blocked arrangement
+      v[i] = idx < n ? f(idx) : 0;
+    }
+    int64_t agg;
+    BS(tmp).ExclusiveSum(v, v, agg);
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+      const int64_t idx = base + (int64_t)threadIdx.x * SCAN_ITEMS + i;
+      if (idx < n) out[idx] = carry + v[i];
+    }
+    carry += agg;
+    __syncthreads();  // tmp reused
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+}
+
 // Scratch needed by exclusive_scan for n items (tile sums).
 inline size_t scan_scratch_elems(int64_t n) { return (size_t)((n + SCAN_TILE - 1) / SCAN_TILE) + 1; }
 
@@ -201,6 +234,10 @@ int exclusive_scan(F f, int64_t n, int64_t* out, int64_t* tile_scratch, cudaStre
   if (ntiles == 0) {
     cudaMemsetAsync(out, 0, sizeof(int64_t), st);
     SFKV_LAUNCH_CHECK("scan (empty)");
+    return 0;
+  }
+  if (ntiles <= SCAN_SINGLE_MAX_TILES) {
+    SFKV_CUDA(launch_pdl(scan_single_kernel<F>, dim3(1), dim3(SCAN_THREADS), st, f, n, out));
     return 0;
   }
   SFKV_CUDA(launch_pdl(scan_reduce_kernel<F>, dim3((unsigned)ntiles), dim3(SCAN_THREADS), st, f, n, tile_scratch));
