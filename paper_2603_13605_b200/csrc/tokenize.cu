@@ -10,7 +10,7 @@
 //
 // Launches for a batch (text is a CSR of messages, requests are ranges of messages):
 //   msg_mark_kernel     message-start bitmap (a message start is a forced token boundary)
-//   chunk_count_kernel  token starts per 4 KiB chunk (a warp each): 16-B loads, C-locale space
+//   chunk_count_kernel  token starts per 2 KiB chunk (a warp each): 16-B loads, C-locale space
 //                       test on 4 bytes at a time (__vcmpeq4 / __vcmpleu4), start = non-space &
 //                       (prev space | message start)
 //   exclusive scan      over chunks
@@ -61,8 +61,13 @@ struct TSlot {
 namespace sfkv {
 
 constexpr uint32_t TOK_PENDING = 0xffffffffu;
-constexpr int CHUNK = 4096;
-constexpr int CHUNK_THREADS = 256;  // 16 bytes (one 16-B load) per thread
+#ifndef SFKV_TOK_CHUNK_THREADS
+#define SFKV_TOK_CHUNK_THREADS 128
+#endif
+// 2 KiB chunks: 128 threads, 16 bytes (one 16-B load) each (measured: 1 KiB 0.419 ms, 2 KiB 0.367,
+// 4 KiB 0.380, 8 KiB 0.465 per C2 batch)
+constexpr int CHUNK_THREADS = SFKV_TOK_CHUNK_THREADS;
+constexpr int CHUNK = CHUNK_THREADS * 16;
 constexpr int RANK_TILE = 8192;     // tokens per CTA of the rank pass (256 threads x 32)
 enum : int { TERR_COLLISION = 1, TERR_ARENA = 2, TERR_IDS = 4, TERR_TABLE = 8 };
 // ctr: [0] ids, [1] arena cursor, [2] error, [3] new bytes, [4] pending, [5] new ids (batch)
@@ -222,7 +227,7 @@ __device__ void probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned l
                           int len);
 
 // Token starts of the chunk in order (CTA scan) into a shared list, and every token probed right
-// here, one token per thread (no per-thread token-count divergence): the chunk's 4 KiB plus OVER
+// here, one token per thread (no per-thread token-count divergence): the chunk's 2 KiB plus OVER
 // bytes of the next chunk and their message-start bits are staged in shared memory with a
 // chunk-wide boundary bitmap (space | message start), so a token's end is the next set bit and its
 // key comes from the staged bytes (tokens running past the staged window fall back to global reads).
@@ -501,7 +506,7 @@ __global__ void tok_final2_kernel(TokArgs a) {  // duplicates of new strings
 }
 
 // tok_off[r]: tokens before request r's first byte b = its chunk's offset + the token starts in
-// [chunk start, b) (one warp per request, every load of the <= 4 KiB prefix in flight at once).
+// [chunk start, b) (one warp per request, every load of the <= 2 KiB prefix in flight at once).
 __global__ void req_tokoff_kernel(TokArgs a) {
   pdl_enter();
   const int lane = threadIdx.x & 31;
