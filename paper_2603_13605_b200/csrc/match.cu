@@ -60,7 +60,10 @@ constexpr int BLOCK_THREADS = 128;  // block pass: 4 warps per CTA, so the per-w
 #define SFKV_CH_TPW_HASH 8
 #endif
 constexpr int CH_TPW_HASH = SFKV_CH_TPW_HASH;
-constexpr int CH_TPW_LOOKUP = 2;  // 54 registers: more warps in flight for the dependent probes
+#ifndef SFKV_CH_TPW_LOOKUP
+#define SFKV_CH_TPW_LOOKUP 2
+#endif
+constexpr int CH_TPW_LOOKUP = SFKV_CH_TPW_LOOKUP;  // 54 registers: more warps in flight for the dependent probes
 #ifndef SFKV_PREP_THREADS
 #define SFKV_PREP_THREADS 256
 #endif
