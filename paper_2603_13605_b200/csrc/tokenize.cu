@@ -231,7 +231,10 @@ __device__ void probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned l
 // bytes of the next chunk and their message-start bits are staged in shared memory with a
 // chunk-wide boundary bitmap (space | message start), so a token's end is the next set bit and its
 // key comes from the staged bytes (tokens running past the staged window fall back to global reads).
-constexpr int OVER = 256;
+#ifndef SFKV_TOK_OVER
+#define SFKV_TOK_OVER 256
+#endif
+constexpr int OVER = SFKV_TOK_OVER;
 __global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
   pdl_enter();
   using BS = cub::BlockScan<int, CHUNK_THREADS>;
