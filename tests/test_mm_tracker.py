@@ -64,9 +64,11 @@ def test_gpu_tracker_reproduces_golden_action_log(gpu_api, name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("seed,n_wf", [(11, 60), (12, 500), (13, 3000)])
-def test_gpu_tracker_matches_oracle_in_large_batches(gpu_api, oracle_api, seed, n_wf):
-    events, backends, wfs = random_stream(seed, n_wf=n_wf, backends=("A", "B", "C", "D", "E"),
+@pytest.mark.parametrize("seed,n_wf,nb", [(11, 60, 5), (12, 500, 5), (13, 3000, 5), (14, 400, 12)])
+def test_gpu_tracker_matches_oracle_in_large_batches(gpu_api, oracle_api, seed, n_wf, nb):
+    """nb = 12 backends exercises the replay with (wf, b) entries in global memory (the
+    thread-local cache covers <= 8)."""
+    events, backends, wfs = random_stream(seed, n_wf=n_wf, backends=tuple("ABCDEFGHIJKL"[:nb]),
                                           p_tick=0.002)
     out = []
     for api in (oracle_api, gpu_api):
