@@ -512,24 +512,51 @@ __global__ void tok_final2_kernel(TokArgs a) {  // duplicates of new strings
 // [chunk start, b) (one warp per request, every load of the <= 2 KiB prefix in flight at once).
 __global__ void req_tokoff_kernel(TokArgs a) {
   pdl_enter();
+  constexpr int KW = CHUNK / 512;
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r <= a.n_req; r += warps) {
     const int64_t b = r < a.n_req ? a.msg_off[a.req_msg_off[r]] : a.n_bytes;
     const int64_t c = b / CHUNK;
+    const int64_t c0 = c * CHUNK;
+    // every window's loads issued together (predicated), the previous byte from the neighbouring
+    // lane, as in the count pass
+    const int64_t coff = a.chunk_off[c];
+    uint4 v[KW];
+    uint32_t mw[KW];
+#pragma unroll
+    for (int k = 0; k < KW; ++k) {
+      const int64_t w = c0 + 512 * k + 16 * lane;
+      v[k] = make_uint4(0x20202020u, 0x20202020u, 0x20202020u, 0x20202020u);
+      if (w < b && w + 16 <= a.n_bytes) v[k] = __ldg(reinterpret_cast<const uint4*>(a.text + w));
+      mw[k] = w < b ? __ldg(a.mbits + (w >> 5)) : 0u;
+    }
+    uint32_t prev_last = c0 == 0 ? 1u : (uint32_t)is_space(a.text[c0 - 1]);
     int cnt = 0;
 #pragma unroll
-    for (int k = 0; k < CHUNK / 512; ++k) {
-      const int64_t w = c * CHUNK + 16 * lane + 512 * k;
+    for (int k = 0; k < KW; ++k) {
+      const int64_t w = c0 + 512 * k + 16 * lane;
+      if (w < b && w + 16 > a.n_bytes) {  // the text's last, partial window
+        uint32_t q[4] = {0x20202020u, 0x20202020u, 0x20202020u, 0x20202020u};
+        for (int j = 0; w + j < a.n_bytes; ++j)
+          q[j >> 2] = (q[j >> 2] & ~(0xffu << (8 * (j & 3)))) | ((uint32_t)a.text[w + j] << (8 * (j & 3)));
+        v[k] = make_uint4(q[0], q[1], q[2], q[3]);
+      }
+      const uint32_t sp = space_mask4(v[k].x) | (space_mask4(v[k].y) << 4) | (space_mask4(v[k].z) << 8) |
+                          (space_mask4(v[k].w) << 12);
+      const uint32_t last = (sp >> 15) & 1u;
+      uint32_t prev = __shfl_up_sync(0xffffffffu, last, 1);
+      if (lane == 0) prev = prev_last;
+      prev_last = __shfl_sync(0xffffffffu, last, 31);
       if (w < b) {
-        uint32_t m = start_mask16(a, w);
+        uint32_t m = ~sp & (((sp << 1) | prev) | ((mw[k] >> (w & 31)) & 0xffffu)) & 0xffffu;
         if (b - w < 16) m &= (1u << (b - w)) - 1u;
         cnt += __popc(m);
       }
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-    if (lane == 0) a.tok_off[r] = a.chunk_off[c] + cnt;
+    if (lane == 0) a.tok_off[r] = coff + cnt;
   }
 }
 
