@@ -74,10 +74,18 @@ enum : int { TERR_COLLISION = 1, TERR_ARENA = 2, TERR_IDS = 4, TERR_TABLE = 8 };
 
 __device__ __forceinline__ bool is_space(uint8_t c) { return c == ' ' || (c >= '\t' && c <= '\r'); }
 
-// 4 bytes -> 4-bit mask (bit j = byte j is a C-locale space)
+// 4 bytes -> 4-bit mask (bit j = byte j is a C-locale space: 0x20 or 0x09..0x0D). Exact per-byte
+// SWAR with no borrow or carry crossing a byte (the high bit is cleared before each add):
+//   ge9 / ge14: (b & 0x7F) + (0x80 - 9 / 14) sets bit 7 iff b & 0x7F >= 9 / 14
+//   eq20:       ((b & 0x7F) ^ 0x20) + 0x7F leaves bit 7 clear iff the byte is 0x20
+// bytes >= 0x80 are never spaces. (The __vcmp*4 intrinsics are emulated on sm_100: ~3x the
+// instructions; the count pass was issue-bound on them.)
 __device__ __forceinline__ uint32_t space_mask4(uint32_t w) {
-  const uint32_t sp = __vcmpeq4(w, 0x20202020u) | __vcmpleu4(__vsub4(w, 0x09090909u), 0x04040404u);
-  return ((sp & 0x01010101u) * 0x01020408u) >> 24;
+  const uint32_t lo7 = w & 0x7F7F7F7Fu;
+  const uint32_t ge9 = lo7 + 0x77777777u, ge14 = lo7 + 0x72727272u;
+  const uint32_t ne20 = (lo7 ^ 0x20202020u) + 0x7F7F7F7Fu;
+  const uint32_t sp = ((ge9 & ~ge14) | ~ne20) & ~w & 0x80808080u;
+  return (((sp >> 7) * 0x01020408u) >> 24) & 0xFu;
 }
 
 // Table keys: tokens of <= 7 bytes are their own key (tag bit 63 | length | bytes): exact, no
