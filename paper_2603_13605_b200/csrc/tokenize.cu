@@ -11,7 +11,7 @@
 // Launches for a batch (text is a CSR of messages, requests are ranges of messages):
 //   msg_mark_kernel     message-start bitmap (a message start is a forced token boundary)
 //   chunk_count_kernel  token starts per 2 KiB chunk (a warp each): 16-B loads, C-locale space
-//                       test on 4 bytes at a time (__vcmpeq4 / __vcmpleu4), start = non-space &
+//                       test on 4 bytes at a time (per-byte SWAR), start = non-space &
 //                       (prev space | message start)
 //   exclusive scan      over chunks
 //   chunk_emit_kernel   CTA scan inside each chunk: token start positions, in order, in a shared
