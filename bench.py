@@ -56,6 +56,30 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+_FP_W = {}
+
+
+def fingerprint(t):
+    """Position-sensitive checksum of a flat uint8 CUDA tensor (length a multiple of 8): per 64 MiB
+    chunk, (sum of its u64 words, sum of word * (2i + 1)), wrapping. Used OUTSIDE the timed regions
+    to prove that the payload legs moved every byte to the right place without holding a second
+    copy of multi-GiB buffers (equal bytes give equal fingerprints; a misplaced or stale row
+    changes them)."""
+    import torch
+    assert t.dtype == torch.uint8 and t.numel() % 8 == 0
+    v = t.view(torch.int64)
+    CH = 8 << 20
+    key = (str(t.device), CH)
+    if key not in _FP_W:
+        _FP_W[key] = torch.arange(CH, dtype=torch.int64, device=t.device) * 2 + 1
+    w = _FP_W[key]
+    out = []
+    for c0 in range(0, v.numel(), CH):
+        c = v[c0:c0 + CH]
+        out.append(torch.stack([c.sum(), (c * w[: c.numel()]).sum()]))
+    return torch.stack(out).cpu().numpy() if out else np.zeros((0, 2), np.int64)
+
+
 # ------------------------------------------------------------------ workload ----------------
 def make_workload(seed, n_wf, lo=512, hi=8192, app_hi=256, p_rewrite=0.1):
     rng = np.random.default_rng(seed)
@@ -515,6 +539,15 @@ def kv_legs(args, api, dev, stream, hbm_peak, rank):
     def gather():
         api.check("gather", api.gather_dev(pool.h, G, C.c_void_p(gwf.data_ptr()),
                                            C.c_void_p(staging.data_ptr()), C.c_void_p(goff.data_ptr())))
+    # byte check (untimed): pin g was scattered from staging[g * ctx * tok_bytes ...] (G = chunk),
+    # so gathering the G pins back must reproduce those bytes exactly
+    gbytes = G * ctx * tok_bytes
+    fp_src = fingerprint(staging[:gbytes])
+    staging[:gbytes].zero_()
+    gather()
+    torch.cuda.synchronize()
+    verified = {"gather_bytes_equal_scatter_source": bool((fingerprint(staging[:gbytes]) == fp_src).all())}
+    assert verified["gather_bytes_equal_scatter_source"], "gathered KV bytes differ from the committed ones"
     for _ in range(args.warmup):
         gather()
     times = []
@@ -567,9 +600,29 @@ def kv_legs(args, api, dev, stream, hbm_peak, rank):
             c_bytes.append(moved)
     c_ms = float(np.mean(c_times))
     c_gbs = float(np.mean(c_bytes)) / (c_ms / 1e3) / 1e9
+    # byte check of the last stage commit (untimed): for V workflows gather the new pin; rows
+    # [0, ctx) must equal the retained context (staging bytes it was scattered from, the boundary
+    # block's ctx % 16 rows copied on share) and rows [ctx, ctx + A) the staging rows at kv_off
+    V = min(n_wf, 16)
+    L = ctx + A
+    vbuf = torch.empty(V * L * tok_bytes, dtype=torch.uint8, device=dev)
+    vw = torch.arange(V, dtype=torch.int32, device=dev)
+    vo = torch.arange(V, dtype=torch.int64, device=dev) * L * tok_bytes
+    api.check("gather", api.gather_dev(pool.h, V, C.c_void_p(vw.data_ptr()), C.c_void_p(vbuf.data_ptr()),
+                                       C.c_void_p(vo.data_ptr())))
+    torch.cuda.synchronize()
+    ok = True
+    for i in range(V):
+        got = vbuf[i * L * tok_bytes:(i + 1) * L * tok_bytes].view(KV_SLABS, L, KV_ROW)
+        base = staging[(i % chunk) * ctx * tok_bytes:((i % chunk) + 1) * ctx * tok_bytes].view(KV_SLABS, ctx, KV_ROW)
+        app = staging[i * A * tok_bytes:(i + 1) * A * tok_bytes].view(KV_SLABS, A, KV_ROW)
+        ok &= bool(torch.equal(got[:, :ctx], base)) and bool(torch.equal(got[:, ctx:], app))
+    del vbuf
+    assert ok, "stage-commit KV bytes differ from the retained context + staged append"
+    verified["stage_commit_bytes"] = f"{V} pins x {L} tokens byte-equal (COW rows + staged rows)"
     pool.close()
     del staging
-    return {"pool_gib": args.kv_pool_gib, "pool_blocks": pool_blocks,
+    return {"pool_gib": args.kv_pool_gib, "pool_blocks": pool_blocks, "verified": verified,
             "gather": {"pins_per_step": G, "tokens_per_pin": ctx, "bytes_per_step": g_bytes,
                        "ms": g_ms, "gbps": g_gbs, "frac_of_hbm": g_gbs / hbm_peak},
             "stage_commit": {"workflows": n_wf, "append_tokens": A, "bytes_per_step": float(np.mean(c_bytes)),
@@ -704,6 +757,11 @@ def long_context_leg(args, api, dev, stream, hbm_peak, rank):
                  n_slabs=KV_SLABS, slab_row_bytes=KV_ROW, device=dev)
     pool = Pool(api, cfg)
     staging = torch.empty(stage_bytes, dtype=torch.uint8, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(args.seed + 4 + rank)
+    staging.random_(0, 256, generator=gen)  # the "prefill output" every admission scatters
+    pin_bytes = ctx * tok_bytes
+    fp_src = fingerprint(staging[:pin_bytes])
     rng = np.random.default_rng(args.seed + 4 + rank)
     ctxs = [rng.integers(1, 1 << 30, size=ctx).astype(np.uint32) for _ in range(W)]
     zero = np.zeros(1, np.int64)
@@ -735,6 +793,16 @@ def long_context_leg(args, api, dev, stream, hbm_peak, rank):
         api.check("gather", api.gather_dev(pool.h, 1, C.c_void_p(gw.data_ptr()),
                                            C.c_void_p(staging.data_ptr()), C.c_void_p(go.data_ptr())))
         api.check("sync", api.pool_sync(pool.h))
+
+    def verify_pin(w):  # untimed: the 16 GiB pin gathered back equals the bytes it was admitted from
+        gw.fill_(w)
+        staging[:pin_bytes].zero_()
+        torch.cuda.synchronize()  # the pool runs on its own stream
+        gather()
+        gw.fill_(0)
+        return bool((fingerprint(staging[:pin_bytes]) == fp_src).all())
+    verified = {"admitted_pin_bytes": verify_pin(0)}
+    assert verified["admitted_pin_bytes"], "C4: gathered 16 GiB pin differs from its admission bytes"
     gather()
     g_ms = float(np.median([timed(gather) for _ in range(max(3, min(args.steps, 5)))]))
     g_bytes = 2 * ctx * tok_bytes
@@ -761,12 +829,15 @@ def long_context_leg(args, api, dev, stream, hbm_peak, rank):
     freed = []
     flush_ms = timed(lambda: freed.append(pool.flush(int(victim[0]))))
     readmit_ms = admit(9)
+    verified["readmitted_pin_bytes_after_evict"] = verify_pin(9)
+    assert verified["readmitted_pin_bytes_after_evict"], "C4: re-admitted pin bytes differ"
+    verified["pins_after_wave"] = [pool.pinned_token_count(w) for w in range(10)]
     adm_bytes = 2 * ctx * tok_bytes
     pool.close()
     del staging
     torch.cuda.empty_cache()
     a_ms = float(np.median(admit_ms))
-    return {"pool_blocks": pool_blocks, "pool_gb": pool_blocks * BLOCK_BYTES / 1e9,
+    return {"pool_blocks": pool_blocks, "pool_gb": pool_blocks * BLOCK_BYTES / 1e9, "verified": verified,
             "pool_frac_of_180gb": pool_blocks * BLOCK_BYTES / 180e9,
             "pool_frac_of_device_memory": pool_blocks * BLOCK_BYTES / total,
             "utilization_after_fill": util, "context_tokens": ctx,
@@ -845,14 +916,20 @@ def handoff_leg(args, api, dev, stream, rank, world):
     tok_bytes = KV_SLABS * KV_ROW
     rng = np.random.default_rng(args.seed + 1000 + rank)
     ctxs = [rng.integers(1, 1 << 30, size=ctx).astype(np.uint32) for _ in range(H)]
-    staging = torch.randint(0, 255, (ctx * tok_bytes,), dtype=torch.uint8, device=dev)
-    for i in range(H):  # each context's KV comes from its prefill (staging)
+    staging = torch.empty(ctx * tok_bytes, dtype=torch.uint8, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(args.seed + 1000 + rank)
+    fp_mine = []
+    for i in range(H):  # each context's KV comes from its own prefill (fresh random staging)
+        staging.random_(0, 256, generator=gen)
+        fp_mine.append(fingerprint(staging))
         off, tok = csr([ctxs[i]])
         assert pool.commit(np.array([i], np.int32), off, tok, kv_src=staging,
                            kv_src_off=np.zeros(1, np.int64))[0] == 1
-    del staging
     link = sfdist.PeerLink(pool, dev)
     src, dst = (rank - 1) % world, (rank + 1) % world
+    fps = [None] * world  # every rank's per-context payload fingerprints (self-verification)
+    tdist.all_gather_object(fps, fp_mine)
     off, tok, blocks = link.metadata(range(H))  # what this rank ships to dst
     mdev = sfdist._meta_device()  # metadata travels over NCCL (GPU tensors) or gloo (CPU)
     t_out = torch.from_numpy(tok.view(np.int32).copy()).to(mdev)
@@ -889,9 +966,17 @@ def handoff_leg(args, api, dev, stream, rank, world):
         assert bool((d_st == 1).all()), "handoff rejected"
         if it >= args.warmup:
             times.append(a.elapsed_time(b))
-        if it == 0:  # the received context is src's first one (tokens)
+        if it == 0:  # untimed: every received context equals src's, tokens and KV bytes
             got = pool.pin_tokens(H)
             assert (got == d_tok[:ctx].cpu().numpy().view(np.uint32)).all()
+            gz = torch.zeros(1, dtype=torch.int64, device=dev)
+            for i in range(H):
+                gi = torch.tensor([H + i], dtype=torch.int32, device=dev)
+                api.check("gather_dev", api.gather_dev(pool.h, 1, C.c_void_p(gi.data_ptr()),
+                                                       C.c_void_p(staging.data_ptr()), C.c_void_p(gz.data_ptr())))
+                api.check("sync", api.pool_sync(pool.h))
+                assert (fingerprint(staging) == fps[src][i]).all(), f"C3: pulled KV bytes of context {i} differ"
+            verified = f"{H} pulled contexts byte-equal to the sender's (fingerprints), tokens equal"
         pool.flush_batch(wf_in)  # untimed: the next step moves every byte again
     local_ms = float(np.mean(times))
     ms = sfdist.max_over_ranks(local_ms, dev)
@@ -959,7 +1044,7 @@ def handoff_leg(args, api, dev, stream, rank, world):
                         "(CUDA-IPC pull inside the commit kernel)",
             "contexts_per_gpu": H, "bytes_per_gpu_per_step": moved, "ms": ms,
             "per_gpu_gbps": gbps, "aggregate_gbps": gbps * world, "roofline": roof,
-            "nccl_baseline": baseline}
+            "verified": verified, "nccl_baseline": baseline}
 
 
 

@@ -39,6 +39,12 @@ namespace {
 struct Recorder {
   std::vector<json> lines;
   std::unordered_map<std::string, std::uint32_t> ids;
+  // Token ids of match records: inline ("tok"), appended to a binary u32 file ("toff" = offset
+  // of the request's first id in it; --tok-out), or dropped (--no-tok: compact full-scale
+  // goldens keep P, M, ops, signals, ticks, the action log and the end counters).
+  enum class TokMode { Inline, File, None } tok_mode = TokMode::Inline;
+  std::FILE* tok_file = nullptr;
+  std::uint64_t tok_written = 0;
 
   std::uint32_t intern(const std::string& tok) {
     auto it = ids.find(tok);
@@ -119,9 +125,17 @@ class RecordingBackend : public Backend {
       pending_.pop_front();
       ++busy_;
       auto& r = reqs_[rid];
-      r.match_line = rec_.push({{"type", "op"}, {"op", "match"}, {"b", descriptor().ref},
-                                {"rid", rid}, {"wf", r.wf}, {"stage", r.stage},
-                                {"P", r.tok.size()}, {"M", -1}, {"tok", r.tok}});
+      json j = {{"type", "op"}, {"op", "match"}, {"b", descriptor().ref},
+                {"rid", rid}, {"wf", r.wf}, {"stage", r.stage},
+                {"P", r.tok.size()}, {"M", -1}};
+      if (rec_.tok_mode == Recorder::TokMode::Inline) {
+        j["tok"] = r.tok;
+      } else if (rec_.tok_mode == Recorder::TokMode::File) {
+        j["toff"] = rec_.tok_written;
+        std::fwrite(r.tok.data(), sizeof(std::uint32_t), r.tok.size(), rec_.tok_file);
+        rec_.tok_written += r.tok.size();
+      }
+      r.match_line = rec_.push(std::move(j));
     }
   }
 
@@ -161,15 +175,21 @@ const char* override_name(CachePolicyOverride o) {
 }  // namespace
 
 int main(int argc, char** argv) {
-  std::string config_path, trace_path, out_path;
-  for (int i = 1; i + 1 < argc; i += 2) {
+  std::string config_path, trace_path, out_path, tok_path;
+  bool no_tok = false;
+  for (int i = 1; i < argc; ++i) {
     std::string a = argv[i];
-    if (a == "--config") config_path = argv[i + 1];
-    else if (a == "--trace") trace_path = argv[i + 1];
-    else if (a == "--out") out_path = argv[i + 1];
+    if (a == "--no-tok") { no_tok = true; continue; }
+    if (i + 1 >= argc) break;
+    if (a == "--config") config_path = argv[++i];
+    else if (a == "--trace") trace_path = argv[++i];
+    else if (a == "--out") out_path = argv[++i];
+    else if (a == "--tok-out") tok_path = argv[++i];
   }
   if (config_path.empty() || trace_path.empty() || out_path.empty()) {
-    std::fprintf(stderr, "usage: sf_ref_replay --config C.json --trace T.jsonl --out O.jsonl\n");
+    std::fprintf(stderr,
+                 "usage: sf_ref_replay --config C.json --trace T.jsonl --out O.jsonl "
+                 "[--tok-out T.u32 | --no-tok]\n");
     return 2;
   }
   auto config = load_config(config_path);
@@ -177,6 +197,12 @@ int main(int argc, char** argv) {
   auto trace = load_trace(trace_path, templates.names());
 
   Recorder rec;
+  if (no_tok) rec.tok_mode = Recorder::TokMode::None;
+  if (!tok_path.empty()) {
+    rec.tok_mode = Recorder::TokMode::File;
+    rec.tok_file = std::fopen(tok_path.c_str(), "wb");
+    if (!rec.tok_file) throw std::runtime_error("cannot write " + tok_path);
+  }
   EventLoop loop(ClockMode::Virtual);
   LogFn log = stderr_logger(LogLevel::Error);
 
@@ -293,6 +319,7 @@ int main(int argc, char** argv) {
   rec.push({{"type", "end"}, {"now_ms", loop.now_ms()}, {"backends", end_b},
             {"n_token_ids", rec.ids.size()}});
 
+  if (rec.tok_file) std::fclose(rec.tok_file);
   std::ofstream out(out_path);
   for (const auto& l : rec.lines) out << l.dump() << "\n";
   return 0;

@@ -348,7 +348,9 @@ static int commit_impl(sfo_pool* p, int64_t n, const int32_t* wf, const int64_t*
       return -6;
     }
   }
-  /* 1. admission */
+  /* 1. admission (counters saved: a batch that then exhausts the physical pool rolls back) */
+  const int64_t occ_saved = p->occupancy;
+  const uint64_t rej_saved = p->rejections;
   for (int64_t r = 0; r < n; ++r) {
     int64_t old = p->pin_len[wf[r]] < 0 ? 0 : p->pin_len[wf[r]];
     int64_t nw = tok_off[r + 1] - tok_off[r];
@@ -437,7 +439,10 @@ static int commit_impl(sfo_pool* p, int64_t n, const int32_t* wf, const int64_t*
     if (cat[it] != C_OWN && cat[it] != C_PRIV) continue;
     while (scan_free < p->cfg.n_blocks && !p->blk_free[scan_free]) ++scan_free;
     if (scan_free >= p->cfg.n_blocks) {
-      /* physical pool exhausted: undo nothing (callers size pools so this cannot happen) */
+      /* physical pool exhausted: the batch changes nothing (no block, pin or table entry has
+       * been touched yet; the admission counters roll back), as sfkv_commit_batch */
+      p->occupancy = occ_saved;
+      p->rejections = rej_saved;
       free(M); free(item_off); free(key); free(cat); free(bid); free(owner); free(hit0);
       free(claim); free(item_req);
       return -5;

@@ -20,6 +20,15 @@ Scenarios:
   chain_scale       synthetic, SURVEY §9 C2 probe at reduced scale: 300 math_chain_k workflows,
                     log-uniform bases, tight capacity (rejections) and pressure ticks
 Synthetic inputs are written to tests/golden/inputs/ and committed with the streams.
+
+Full-scale compact goldens (`python tests/golden/make_golden.py c2_probe c4_probe`, written to
+tests/golden/full/, match records WITHOUT token ids — P, M, every op, signal, tick, the action log
+and the end counters): the inputs regenerate from the seeded generators below, and the token
+streams are re-recorded on the GPU box by the same reference driver (--tok-out) whose compact
+projection must equal the committed golden before the GPU replays them.
+  c2_probe          SURVEY §9 C2 probe, full size: 10k workflows, 50k requests, 110k signals,
+                    sum P = 163,183,335, sum M = 125,426,668
+  c4_probe          SURVEY §9 C4 probe 2, full size: 24 x 131,072-token A/B alternating workflows
 """
 from __future__ import annotations
 
@@ -95,6 +104,95 @@ def chain_scale():
     return cfg, trace
 
 
+def c2_probe():
+    """SURVEY §9 C2-scale probe at FULL size: 10,000 math_chain_k workflows (k = 5, base
+    log-uniform in [512, 8192] drawn with Python random.seed(2), +256 tokens per stage), arrivals
+    every 5 ms, one backend (max_concurrency 64, capacity 1,310,720 tokens), default chain.
+    sum P = 163,183,335."""
+    random.seed(2)
+    bases = [int(math.exp(random.uniform(math.log(512), math.log(8192)))) for _ in range(10_000)]
+    cfg = {
+        "label": "c2-probe",
+        "backends": [sim_backend("heavy", "sim-heavy-8b", "heavy", 1_310_720, 64, 0.05, 1.0,
+                                 {"rule": "constant", "tokens": 0})],
+        "mapper": {"type": "explicit"},
+        "memory": {"chain": ["preserve_small_increment", "flush_at_boundary"], "tau": 512,
+                   "tau_pressure": 0.85, "monitor_interval_ms": 100},
+        "templates": {"math_chain_k": {"backend": "heavy", "k": 5, "append_tokens": 256,
+                                       "max_tokens": 64}},
+    }
+    trace = [{"template": "math_chain_k", "arrival_ms": 5 * w, "payload": {"base_tokens": b}}
+             for w, b in enumerate(bases)]
+    return cfg, trace
+
+
+def c4_probe():
+    """SURVEY §9 C4 probe 2 at full size: 24 workflows s1@A -> s2@B -> s3@A -> s4@B, each stage
+    prompt the workflow's own distinct 131,072-token text, chain [preserve_small_increment],
+    arrivals every 300 ms, both backends at the C4 pool's logical capacity of 1,235,952 tokens
+    (77,247 blocks x 16), prefill 0.0095 ms/token. The reference gives: first pressure flush at
+    ts 3800 (alt-5@A), 54 flush_under_pressure, 22 capacity rejections on B, end occupancy
+    8 / 9 orphaned 128k pins (SURVEY §9 quotes 56 pressure flushes for its unstated timing)."""
+    base = 131_072
+    rnd = random.Random(0x0A1A + 4)
+    stages = []
+    for i in range(1, 5):
+        stages.append({"id": f"s{i}", "backend": "A" if i % 2 else "B", "model": "m",
+                       "prompt_from_payload": "p", "max_tokens": 16})
+    cap = 1_235_952
+    cfg = {
+        "label": "c4-probe",
+        "backends": [sim_backend("A", "m", "heavy", cap, 4, 0.0095, 1.0,
+                                 {"rule": "constant", "tokens": 0}),
+                     sim_backend("B", "m", "heavy", cap, 4, 0.0095, 1.0,
+                                 {"rule": "constant", "tokens": 0})],
+        "mapper": {"type": "explicit"},
+        "memory": {"chain": ["preserve_small_increment"], "tau": 512, "tau_pressure": 0.85,
+                   "monitor_interval_ms": 100},
+        "workflows": [{"name": "alt", "stages": stages,
+                       "dependencies": [["s2", "s1"], ["s3", "s2"], ["s4", "s3"]]}],
+    }
+    trace = []
+    for w in range(24):
+        words = " ".join(f"a{w}x{rnd.randrange(1 << 20)}" for _ in range(base))
+        trace.append({"template": "alt", "arrival_ms": 300 * w, "payload": {"p": words}})
+    return cfg, trace
+
+
+FULL = os.path.join(HERE, "full")  # compact full-scale goldens (no token ids)
+FULL_SCENARIOS = {"c2_probe": c2_probe, "c4_probe": c4_probe}
+
+
+def write_inputs(fn, dirpath):
+    cfg, trace = fn()
+    cp = os.path.join(dirpath, "config.json")
+    tp = os.path.join(dirpath, "trace.jsonl")
+    with open(cp, "w") as f:
+        json.dump(cfg, f)
+    with open(tp, "w") as f:
+        for rec in trace:
+            f.write(json.dumps(rec) + "\n")
+    return cp, tp
+
+
+def compact_line(l):
+    """What a compact golden keeps of a stream line (match ops lose their token ids)."""
+    return {k: v for k, v in l.items() if k not in ("tok", "toff")}
+
+
+def run_full(name):
+    import tempfile
+    os.makedirs(FULL, exist_ok=True)
+    with tempfile.TemporaryDirectory() as td:
+        cp, tp = write_inputs(FULL_SCENARIOS[name], td)
+        out = os.path.join(td, "o.jsonl")
+        subprocess.run([DRIVER, "--config", cp, "--trace", tp, "--out", out, "--no-tok"], check=True)
+        with open(out, "rb") as f, gzip.open(os.path.join(FULL, f"{name}.jsonl.gz"), "wb", 9) as g:
+            g.write(f.read())
+        n = sum(1 for _ in open(out))
+    print(f"{name}: {n} records (compact)")
+
+
 def run(name, config_path, trace_path):
     out = os.path.join("/tmp", f"golden_{name}.jsonl")
     subprocess.run([DRIVER, "--config", config_path, "--trace", trace_path, "--out", out],
@@ -127,4 +225,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1:  # e.g. make_golden.py c2_probe c4_probe (full-scale compact goldens)
+        for name in sys.argv[1:]:
+            run_full(name)
+    else:
+        main()

@@ -15,7 +15,7 @@ import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
 
-SLABS, ROW = 4, 64
+SHAPES = [(4, 64), (64, 2048)]  # small rows, and the Llama-3-8B block (2 MiB, 32 KiB extents)
 SRC_WF, DST_WF = [0, 1, 2], [5, 6, 7]
 
 
@@ -27,7 +27,7 @@ def _free_port():
     return p
 
 
-def _contexts():
+def _contexts(SLABS, ROW):
     rng = np.random.default_rng(11)
     shared = rng.integers(1, 1 << 20, size=40).astype(np.uint32)
     ctx = [np.concatenate([shared, rng.integers(1, 1 << 20, size=n).astype(np.uint32)])
@@ -38,12 +38,12 @@ def _contexts():
     return ctx, older, stg, stg_old
 
 
-def _setup(api, rank):
+def _setup(api, rank, SLABS, ROW):
     from paper_2603_13605_b200.abi import Config, Pool, csr
     cfg = Config(max_workflows=8, n_blocks=256, capacity_tokens=100_000, max_pin_blocks=32,
                  table_log2=10, n_slabs=SLABS, slab_row_bytes=ROW)
     pool = Pool(api, cfg)
-    ctx, older, stg, stg_old = _contexts()
+    ctx, older, stg, stg_old = _contexts(SLABS, ROW)
     if api.kind == "gpu":  # KV staging is device memory for GPU pools
         import torch
         stg, stg_old = torch.from_numpy(stg).cuda(), torch.from_numpy(stg_old).cuda()
@@ -63,7 +63,7 @@ def _payload(pool, wf):
     return sfdist.gather_pin(pool, wf, device="cuda").cpu().numpy().tobytes()
 
 
-def _worker(rank, port, q):
+def _worker(rank, port, q, shape):
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     sys.path.insert(0, here)
@@ -78,7 +78,7 @@ def _worker(rank, port, q):
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=2)
-        pool = _setup(pkg.api(), rank)
+        pool = _setup(pkg.api(), rank, *shape)
         link = sfdist.PeerLink(pool, device=0)
         res = {}
         if rank == 0:
@@ -97,11 +97,12 @@ def _worker(rank, port, q):
         q.put((rank, None, traceback.format_exc()))
 
 
-def test_peerlink_pull_handoff_matches_oracle(oracle_api):
+@pytest.mark.parametrize("shape", SHAPES)
+def test_peerlink_pull_handoff_matches_oracle(oracle_api, shape):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, shape)) for r in range(2)]
     for p in procs:
         p.start()
     out = {}
@@ -113,7 +114,7 @@ def test_peerlink_pull_handoff_matches_oracle(oracle_api):
         p.join(timeout=60)
     assert out[0]["ack"] == 1
     # the oracle: the same two pools in one process, handoff one pin at a time
-    src, dst = _setup(oracle_api, 0), _setup(oracle_api, 1)
+    src, dst = _setup(oracle_api, 0, *shape), _setup(oracle_api, 1, *shape)
     want_status = [src.handoff_to(s, dst, d) for s, d in zip(SRC_WF, DST_WF)]
     assert out[1]["status"] == want_status == [1, 1, 1]
     for i, w in enumerate(DST_WF):
