@@ -630,43 +630,35 @@ def kv_legs(args, api, dev, stream, hbm_peak, rank):
                              "note": "whole commit pipeline (metadata kernels + COW + scatter)"}}
 
 
-def lookup_leg(args, api, dev, stream, hbm_peak, rank):
-    """C5 (BASELINE configs[4]): heavy prefix sharing. Resident: 8,192 system prompts of 64 blocks
-    plus 32,768 workflows = a system prompt + 16 private blocks, i.e. 1,048,576 distinct resident
-    blocks in the dedup table (every workflow pin shares its prompt's 64 blocks). One step =
-    sfkv_lookup_batch_dev over 100k stage prefixes = a system prompt + 1..63 private blocks, half
-    continuing a resident workflow's private context: ~9.6 M chained-hash probes, token-verified on
-    every key hit (SURVEY §8d C5; a global lookup the reference has no counterpart for)."""
-    import torch
-
-    from paper_2603_13605_b200.abi import Config, Pool
-    rng = np.random.default_rng(args.seed + 5 + rank)
+def c5_workload(seed, n_prefixes=100_000, table_log2=22, device=0):
+    """C5 (BASELINE configs[4]): 8,192 system prompts of 64 blocks, each owned by a
+    workflow, plus 32,768 workflows = a system prompt + 16 private blocks -> 1,048,576 distinct
+    resident blocks in the dedup table. The batch: n_prefixes stage prefixes = a system prompt +
+    1..63 private blocks, half continuing a resident workflow's private context.
+    Returns (pool Config, resident commits [(wf, tok_off, tok)], (tok_off, tok, expected hit
+    tokens per prefix)). Shared by bench.py's c5_lookup leg and tests/test_full_scale.py."""
+    from paper_2603_13605_b200.abi import Config
+    rng = np.random.default_rng(seed)
     n_sys, sys_blocks, n_wf, priv_blocks = 8192, 64, 32768, 16
     sys_tok = rng.integers(1, 1 << 30, size=(n_sys, sys_blocks * BT), dtype=np.uint32)
     priv_tok = rng.integers(1, 1 << 30, size=(n_wf, priv_blocks * BT), dtype=np.uint32)
     W = n_sys + n_wf
     # table: 2^22 slots x 16 B (64 MB, L2-resident, load factor 0.25) for the 1,048,576 blocks;
     # SURVEY §8d sketches 2^21 (load 0.5), whose longer probe chains measured 7 % slower
-    tl = args.c5_table_log2
-    cfg = Config(max_workflows=W, n_blocks=min(1_200_000, (1 << tl) - 1), capacity_tokens=1 << 50,
-                 max_pin_blocks=sys_blocks + priv_blocks + 1, table_log2=tl, device=dev)
-    pool = Pool(api, cfg)
-    t0 = time.perf_counter()
+    cfg = Config(max_workflows=W, n_blocks=min(1_200_000, (1 << table_log2) - 1), capacity_tokens=1 << 50,
+                 max_pin_blocks=sys_blocks + priv_blocks + 1, table_log2=table_log2, device=device)
+    resident = []
     for c0 in range(0, n_sys, 4096):  # owners of the system prompts
         ids = np.arange(c0, min(n_sys, c0 + 4096))
         off = np.arange(len(ids) + 1, dtype=np.int64) * sys_blocks * BT
-        assert pool.commit(ids.astype(np.int32), off, np.ascontiguousarray(sys_tok[ids]).ravel()).all()
+        resident.append((ids.astype(np.int32), off, np.ascontiguousarray(sys_tok[ids]).ravel()))
     wlen = (sys_blocks + priv_blocks) * BT
     for c0 in range(0, n_wf, 4096):  # workflows: prompt + private context
         ids = np.arange(c0, min(n_wf, c0 + 4096))
         tok = np.concatenate([sys_tok[ids % n_sys], priv_tok[ids]], axis=1).ravel()
         off = np.arange(len(ids) + 1, dtype=np.int64) * wlen
-        assert pool.commit((n_sys + ids).astype(np.int32), off, tok).all()
-    st = pool.stats()
-    log(f"[rank {rank}] c5: {st['table_live']} resident blocks in the table "
-        f"({time.perf_counter() - t0:.1f}s)")
-    # the batch
-    P = args.c5_prefixes
+        resident.append(((n_sys + ids).astype(np.int32), off, tok))
+    P = n_prefixes
     s = rng.integers(0, n_sys, size=P)
     npriv = rng.integers(1, 64, size=P)
     cont = rng.random(P) < 0.5
@@ -688,6 +680,30 @@ def lookup_leg(args, api, dev, stream, hbm_peak, rank):
             k = min(npriv[i], priv_blocks) * BT
             tok[b:b + k] = priv_tok[wsel[i], :k]
     expect_hit = BT * (sys_blocks + np.where(cont, np.minimum(npriv, priv_blocks), 0))
+    return cfg, resident, (off, tok, expect_hit)
+
+
+def lookup_leg(args, api, dev, stream, hbm_peak, rank):
+    """C5 (BASELINE configs[4]): heavy prefix sharing. Resident: 8,192 system prompts of 64 blocks
+    plus 32,768 workflows = a system prompt + 16 private blocks, i.e. 1,048,576 distinct resident
+    blocks in the dedup table (every workflow pin shares its prompt's 64 blocks). One step =
+    sfkv_lookup_batch_dev over 100k stage prefixes = a system prompt + 1..63 private blocks, half
+    continuing a resident workflow's private context: ~9.6 M chained-hash probes, token-verified on
+    every key hit (SURVEY §8d C5; a global lookup the reference has no counterpart for)."""
+    import torch
+
+    from paper_2603_13605_b200.abi import Pool
+    tl = args.c5_table_log2
+    t0 = time.perf_counter()
+    cfg, resident, batch = c5_workload(args.seed + 5 + rank, args.c5_prefixes, tl, dev)
+    pool = Pool(api, cfg)
+    for wf, off, tok in resident:
+        assert pool.commit(wf, off, tok).all()
+    st = pool.stats()
+    log(f"[rank {rank}] c5: {st['table_live']} resident blocks in the table "
+        f"({time.perf_counter() - t0:.1f}s)")
+    off, tok, expect_hit = batch
+    P = args.c5_prefixes
     n_blocks = int(off[-1] // BT)
     d_off = torch.from_numpy(off).to(dev)
     d_tok = torch.from_numpy(tok.view(np.int32)).to(dev)

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SFKV_ABI_VERSION 1
+#define SFKV_ABI_VERSION 2
 
 #define SFKV_OK 0
 #define SFKV_EINVAL -1    /* bad argument (null pointer, out-of-range slot, unaligned buffer) */
@@ -90,6 +90,15 @@ int sfkv_abi_version(void);
 /* Replaces the SimulatedBackend constructor's cache state (simulated_backend.cpp:20-29). */
 int sfkv_pool_create(const sfkv_pool_config* cfg, sfkv_pool** out);
 int sfkv_pool_destroy(sfkv_pool* pool);
+/* Grows the pool in place (never shrinks): workflow slots, the per-pin block-table length and
+ * the physical block count (the dedup table is re-indexed at load factor <= 1/2 when it grows).
+ * Pins, blocks, refcounts and KV bytes are preserved. The reference's pin cache is unbounded
+ * (std::map pins_, simulated_backend.hpp:115), so a binding starts small and reserves on demand
+ * (prompts longer than max_pin_blocks * 16 tokens, more live workflows than slots). Synchronises
+ * the pool stream. The KV region cannot move once exported (sfkv_pool_export): SFKV_EINVAL. */
+int sfkv_pool_reserve(sfkv_pool* pool, int32_t max_workflows, int32_t max_pin_blocks, int64_t n_blocks);
+/* The pool's current configuration (after any reserve). */
+int sfkv_pool_config_get(sfkv_pool* pool, sfkv_pool_config* out);
 int sfkv_pool_set_stream(sfkv_pool* pool, void* cuda_stream);
 int sfkv_pool_sync(sfkv_pool* pool);
 /* Device pointer of the KV payload (n_blocks * block_bytes), block-major
@@ -240,29 +249,41 @@ int sfmm_pressure_argmin(int32_t device, int64_t n, const int32_t* backend, cons
                          const uint32_t* wf_rank, const int32_t* in_flight,
                          const uint8_t* preserved, int32_t n_backends, const double* util,
                          double tau, int64_t* out_victim);
+/* Device pointers, asynchronous on cuda_stream (NULL = legacy default stream). One launch. */
+int sfmm_pressure_argmin_dev(int32_t device, int64_t n, const int32_t* backend, const double* ts,
+                             const uint32_t* wf_rank, const int32_t* in_flight,
+                             const uint8_t* preserved, int32_t n_backends, const double* util,
+                             double tau, int64_t* out_victim, void* cuda_stream);
 
 /* ---- memory manager: batched MemoryManager::on_signal and pressure_tick on a GPU-resident
  *      WorkflowTracker (memory.cpp:256-387) ------------------------------------
  * The tracker (memory.hpp:49-72: cache entries, in-flight counts, last stage, completion, plus
  * the manager's started/open stage sets and per-workflow chains) lives in HBM as dense arrays
  * over (workflow slot, backend index). Workflow ids, stage ids, backend refs and models are
- * interned by the host: backends are indexed in sorted-ref order (BackendRegistry::refs), stage
- * ids are dense per workflow (< SFMM_MAX_STAGES), models are dense ids.
+ * interned by the host: stage ids are dense per workflow, models are dense ids, backends are
+ * dense ids in any order (sfmm_set_backend_order gives their std::string order, the order
+ * flush_at_boundary flushes a finished workflow's entries in, memory.cpp:137-141). Nothing is
+ * capped: sfmm_tracker_reserve grows slots, backends and stage ids in place (the reference's
+ * std::maps are unbounded), and policy chains have any length.
  * sfmm_on_signal_batch applies a batch of lifecycle signals exactly as n sequential on_signal
  * calls would: policies read only their own workflow's state, so the batch is processed in
  * parallel across workflows and in order within each. Signal i's log records (on_signal logs
  * every returned action, noops included, memory.cpp:312-328) are written at
  * [i * n_backends, i * n_backends + count[i]); the action log of the batch is the concatenation
- * in signal order. Flushes are recorded as applied (the sfkv pools cannot fail a flush), so the
- * tracker erases the entry (memory.cpp:319-321); the host issues the pool flushes / preserves
- * (sfkv_flush_batch / sfkv_preserve) from the records. A signal that the reference would reject
+ * in signal order. Flushes are recorded as applied (the tracker erases the entry,
+ * memory.cpp:319-321); the host then applies every record to its backends (apply_action,
+ * memory.cpp:185-220: a flush is retried once) and reports each flush that failed twice with
+ * sfmm_flush_failed before the next batch or tick: the entry becomes present but unpreserved
+ * (mark_unpreserved, memory.cpp:322-324) unless a later signal of the same batch re-wrote or
+ * erased it (exactly the reference's end state; no policy reads an unpreserved entry, so no other
+ * decision of the batch depends on the outcome). A signal that the reference would reject
  * (OutOfOrderSignalError, memory.cpp:256-285) gets status SFMM_SIG_OUT_OF_ORDER and produces no
  * records; the rest of that workflow's signals in the batch are SFMM_SIG_SKIPPED.
  * sfmm_pressure_tick replaces MemoryManager::pressure_tick (memory.cpp:372-387): per backend with
  * util > tau_pressure, the idle preserved entry with least (last_update_ts, workflow rank) is
- * flushed (recorded with reason flush_under_pressure) and erased from the tracker. */
-#define SFMM_MAX_STAGES 64
-#define SFMM_MAX_CHAIN 8
+ * flushed (recorded with reason flush_under_pressure) and erased from the tracker (one kernel:
+ * a segmented warp-shuffle argmin); a victim whose flush failed twice is reported with
+ * sfmm_flush_failed (sig = -1). */
 /* LifecycleSignal::Kind (signals.hpp:13-15) */
 #define SFMM_STAGE_START 0
 #define SFMM_STAGE_COMPLETE 1
@@ -294,10 +315,11 @@ typedef struct sfmm_tracker sfmm_tracker;
 
 typedef struct sfmm_config {
   int32_t device;
-  int32_t max_workflows;
-  int32_t n_backends;
-  int32_t chain_len;                 /* default policy chain (MemoryConfig::policy_chain) */
-  uint8_t chain[SFMM_MAX_CHAIN];
+  int32_t max_workflows;             /* initial workflow slots */
+  int32_t n_backends;                /* initial backends */
+  int32_t max_stages;                /* initial stage ids per workflow (0 = 64) */
+  int32_t chain_len;                 /* default policy chain (MemoryConfig::policy_chain), */
+  const uint8_t* chain;              /*   any length, SFMM_POLICY_* codes; copied */
   int64_t tau;                       /* MemoryConfig::tau (memory.hpp:74-79) */
   double tau_pressure;               /* MemoryConfig::tau_pressure */
 } sfmm_config;
@@ -323,19 +345,33 @@ typedef struct sfmm_records {        /* outputs: n signals x n_backends record s
 
 int sfmm_tracker_create(const sfmm_config* cfg, sfmm_tracker** out);
 int sfmm_tracker_destroy(sfmm_tracker* t);
+/* Grows slots / backends / stage ids in place (never shrinks); state is preserved. */
+int sfmm_tracker_reserve(sfmm_tracker* t, int32_t max_workflows, int32_t n_backends, int32_t max_stages);
+int sfmm_tracker_shape(sfmm_tracker* t, int32_t* max_workflows, int32_t* n_backends, int32_t* max_stages);
 int sfmm_tracker_set_stream(sfmm_tracker* t, void* cuda_stream);  /* NULL = legacy default stream */
 int sfmm_tracker_sync(sfmm_tracker* t);
 /* Forget every workflow (a fresh MemoryManager with the same configuration). */
 int sfmm_tracker_reset(sfmm_tracker* t);
+/* Forget the listed workflow slots (a host recycling slots of finished workflows). */
+int sfmm_reset_workflows(sfmm_tracker* t, int64_t n, const int32_t* wf);
 /* MemoryManager::set_workflow_chain (memory.cpp:246-250); len 0 = no-op, as the reference. */
 int sfmm_set_workflow_chain(sfmm_tracker* t, int32_t wf, int32_t len, const uint8_t* policies);
 /* Rank of every workflow slot in workflow-id string order (pressure tie-break). */
 int sfmm_set_workflow_ranks(sfmm_tracker* t, int64_t n, const uint32_t* rank);
+/* order[k] = backend index of the k-th backend ref in std::string order (n = n_backends);
+ * default: identity. */
+int sfmm_set_backend_order(sfmm_tracker* t, int32_t n, const int32_t* order);
 int sfmm_on_signal_batch(sfmm_tracker* t, int64_t n, const sfmm_signals* sig, const sfmm_records* out);
 int sfmm_on_signal_batch_dev(sfmm_tracker* t, int64_t n, const sfmm_signals* sig,
                              const sfmm_records* out);
-/* util[n_backends] (sorted-ref order) -> out_victim[n_backends] workflow slot or -1. */
+/* Flush records the host could not apply (apply_action failed twice): (workflow slot, backend,
+ * signal index in the last sfmm_on_signal_batch, or -1 for the last sfmm_pressure_tick). */
+int sfmm_flush_failed(sfmm_tracker* t, int64_t n, const int32_t* wf, const int32_t* backend,
+                      const int64_t* sig);
+/* util[n_backends] -> out_victim[n_backends] workflow slot or -1. */
 int sfmm_pressure_tick(sfmm_tracker* t, const double* util, int32_t* out_victim);
+/* Device pointers, asynchronous on the tracker's stream (no host synchronisation). */
+int sfmm_pressure_tick_dev(sfmm_tracker* t, const double* util, int32_t* out_victim);
 /* Tracker snapshot (inspection / parity): per (wf, backend) entry and in-flight count. */
 int sfmm_tracker_entries(sfmm_tracker* t, uint8_t* present, uint8_t* preserved, int64_t* tokens,
                          double* ts, int32_t* in_flight);

@@ -5,14 +5,10 @@
 
 #include <algorithm>
 #include <cmath>
-#include <mutex>
 
 namespace stageflow {
 
 namespace {
-
-std::mutex g_intern_mu;
-std::unordered_map<std::string, std::uint32_t> g_intern;
 
 std::string numbered_words(long long n) {  // "out0 out1 ... out{n-1}" placeholder reply
   std::string s;
@@ -30,13 +26,13 @@ int ceil_log2(long long x) {
   return l;
 }
 
-}  // namespace
-
-std::uint32_t intern_token(const std::string& token) {
-  std::lock_guard<std::mutex> lk(g_intern_mu);
-  auto [it, inserted] = g_intern.emplace(token, static_cast<std::uint32_t>(g_intern.size()));
-  return it->second;
+// Physical blocks never bind in parity mode: every logical token once, one partial block per
+// pin, and one maximal pin of transient headroom (a replaced pin is released after commit).
+long long blocks_for(long long capacity, int32_t slots, int32_t pin_blocks) {
+  return capacity / SFKV_BLOCK_TOKENS + slots + 2LL * pin_blocks + 64;
 }
+
+}  // namespace
 
 GpuPinnedBackend::GpuPinnedBackend(EventLoop& loop, BackendDescriptor descriptor,
                                    SimulatedBackendConfig config, GpuPoolOptions options, LogFn log)
@@ -46,22 +42,47 @@ GpuPinnedBackend::GpuPinnedBackend(EventLoop& loop, BackendDescriptor descriptor
   if (config_.cache_capacity_tokens <= 0) throw BackendError("cache capacity must be positive");
   if (config_.prefill_ms_per_token <= 0 || config_.decode_ms_per_token <= 0)
     throw BackendError("latency parameters must be positive");
+  slot_cap_ = std::max(1, options_.max_workflows);
+  pin_blocks_cap_ = std::max(1, options_.max_pin_blocks);
   sfkv_pool_config pc{};
   pc.device = options_.device;
-  pc.max_workflows = options_.max_workflows;
+  pc.max_workflows = slot_cap_;
   pc.capacity_tokens = config_.cache_capacity_tokens;
-  pc.max_pin_blocks = options_.max_pin_blocks;
-  // Physical blocks never bind in parity mode: every logical token once, one partial block per
-  // pin, and one maximal pin of transient headroom (a replaced pin is released after commit).
-  pc.n_blocks = config_.cache_capacity_tokens / SFKV_BLOCK_TOKENS + options_.max_workflows +
-                2LL * options_.max_pin_blocks + 64;
+  pc.max_pin_blocks = pin_blocks_cap_;
+  pc.n_blocks = blocks_for(config_.cache_capacity_tokens, slot_cap_, pin_blocks_cap_);
   pc.table_log2 = ceil_log2(2 * pc.n_blocks) + 1;
   pc.n_slabs = 0;  // the reference holds no KV bytes; this binding is metadata-only
   pc.slab_row_bytes = 0;
   check(sfkv_pool_create(&pc, &pool_), "sfkv_pool_create");
+  slot_requests_.assign(slot_cap_, 0);
+  slot_pinned_.assign(slot_cap_, 0);
+  slot_names_.assign(slot_cap_, std::string());
+  for (int32_t s = slot_cap_ - 1; s >= 0; --s) free_slots_.push_back(s);
 }
 
 GpuPinnedBackend::~GpuPinnedBackend() { sfkv_pool_destroy(pool_); }
+
+std::uint32_t GpuPinnedBackend::intern(const std::string& token) {
+  auto [it, inserted] = intern_.emplace(token, static_cast<std::uint32_t>(intern_.size()));
+  return it->second;
+}
+
+bool GpuPinnedBackend::reserve(int32_t slots, int32_t pin_blocks) {
+  const int32_t s1 = std::max(slot_cap_, slots), b1 = std::max(pin_blocks_cap_, pin_blocks);
+  if (s1 == slot_cap_ && b1 == pin_blocks_cap_) return true;
+  const int rc = sfkv_pool_reserve(pool_, s1, b1, blocks_for(config_.cache_capacity_tokens, s1, b1));
+  if (rc != SFKV_OK) {
+    if (log_) log_(LogLevel::Error, "gpu backend " + descriptor_.ref + ": sfkv_pool_reserve failed: " + sfkv_last_error());
+    return false;
+  }
+  for (int32_t s = s1 - 1; s >= slot_cap_; --s) free_slots_.push_back(s);
+  slot_requests_.resize(s1, 0);
+  slot_pinned_.resize(s1, 0);
+  slot_names_.resize(s1);
+  slot_cap_ = s1;
+  pin_blocks_cap_ = b1;
+  return true;
+}
 
 void GpuPinnedBackend::check(int rc, const char* what) const {
   if (rc != SFKV_OK)
@@ -76,10 +97,22 @@ int32_t GpuPinnedBackend::find_slot(const std::string& workflow_id) const {
 int32_t GpuPinnedBackend::slot_for(const std::string& workflow_id) {
   auto it = slots_.find(workflow_id);
   if (it != slots_.end()) return it->second;
-  const auto s = static_cast<int32_t>(slots_.size());
-  if (s >= options_.max_workflows) throw BackendError("GpuPinnedBackend: out of workflow slots");
+  if (free_slots_.empty() && !reserve(2 * slot_cap_, pin_blocks_cap_))
+    throw BackendError("GpuPinnedBackend: cannot grow the workflow slots");
+  const int32_t s = free_slots_.back();
+  free_slots_.pop_back();
   slots_.emplace(workflow_id, s);
+  slot_names_[s] = workflow_id;
   return s;
+}
+
+// A slot without a pin and without requests here carries no state: back to the free list (the
+// pool already reads it as "no pin", pin_len = -1, exactly like a never-seen workflow).
+void GpuPinnedBackend::maybe_release(int32_t slot) {
+  if (slot < 0 || slot_requests_[slot] > 0 || slot_pinned_[slot]) return;
+  slots_.erase(slot_names_[slot]);
+  slot_names_[slot].clear();
+  free_slots_.push_back(slot);
 }
 
 bool GpuPinnedBackend::has_capacity() const {
@@ -88,6 +121,7 @@ bool GpuPinnedBackend::has_capacity() const {
 
 void GpuPinnedBackend::complete(CompletionRequest req, CompletionCallback cb) {
   ++stats_.completions;
+  if (!req.metadata.workflow_id.empty()) ++slot_requests_[slot_for(req.metadata.workflow_id)];
   pending_.push_back(Pending{std::move(req), std::move(cb), loop_.now_ms()});
   pump();
 }
@@ -122,13 +156,13 @@ void GpuPinnedBackend::start(Pending item) {
   const std::string wf = item.req.metadata.workflow_id;
 
   std::vector<std::uint32_t> ids;
-  for (const auto& t : context_token_sequence(item.req.messages)) ids.push_back(intern_token(t));
+  for (const auto& t : context_token_sequence(item.req.messages)) ids.push_back(intern(t));
   const long long P = static_cast<long long>(ids.size());
   const int64_t off[2] = {0, P};
   long long M = 0;
   int32_t slot = -1;
   if (!wf.empty()) {  // the empty workflow id never holds a pin (simulated_backend.cpp:125)
-    slot = slot_for(wf);
+    slot = find_slot(wf);  // held since complete()
     int64_t m = 0;
     check(sfkv_match_batch(pool_, 1, &slot, off, ids.data(), &m, nullptr), "sfkv_match_batch");
     M = m;
@@ -171,13 +205,27 @@ void GpuPinnedBackend::start(Pending item) {
   loop_.schedule_in(prefill + decode, [this, slot, ids = std::move(ids), resp = std::move(resp),
                                        cb = std::move(item.cb), wf]() mutable {
     if (slot >= 0) {  // retain the served prompt (commit = pin_prompt, admission included)
+      // Never throw out of the event loop: a failed commit is logged and leaves the old pin,
+      // like a capacity rejection (the reference cannot fail here; this is a device error).
       const int64_t o2[2] = {0, static_cast<int64_t>(ids.size())};
-      int32_t status = 0;
-      check(sfkv_commit_batch(pool_, 1, &slot, o2, ids.data(), nullptr, nullptr, nullptr, &status),
-            "sfkv_commit_batch");
-      if (status != SFKV_PIN_ACCEPTED && log_)
+      int32_t status = SFKV_PIN_REJECTED;
+      const int32_t need = static_cast<int32_t>((o2[1] + SFKV_BLOCK_TOKENS - 1) / SFKV_BLOCK_TOKENS);
+      int32_t grow = pin_blocks_cap_;
+      while (grow < need) grow *= 2;
+      int rc = SFKV_EPOOL;
+      if (reserve(slot_cap_, grow))
+        rc = sfkv_commit_batch(pool_, 1, &slot, o2, ids.data(), nullptr, nullptr, nullptr, &status);
+      if (rc != SFKV_OK) {
+        if (log_) log_(LogLevel::Error, "gpu backend " + descriptor_.ref + ": sfkv_commit_batch failed (" +
+                                            std::to_string(rc) + "): " + sfkv_last_error());
+      } else if (status == SFKV_PIN_ACCEPTED) {
+        slot_pinned_[slot] = 1;
+      } else if (log_) {
         log_(LogLevel::Warn, "gpu backend " + descriptor_.ref +
                                  ": cache capacity exceeded, prefix for workflow " + wf + " not pinned");
+      }
+      --slot_requests_[slot];
+      maybe_release(slot);
     }
     --busy_;
     pump();
@@ -191,11 +239,19 @@ long long GpuPinnedBackend::flush(const FlushScope& scope) {
   int64_t freed = 0;
   if (scope.all) {
     check(sfkv_flush(pool_, SFKV_FLUSH_ALL, &freed), "sfkv_flush");
+    std::vector<int32_t> held;
+    for (const auto& [name, s] : slots_) held.push_back(s);
+    for (int32_t s : held) {
+      slot_pinned_[s] = 0;
+      maybe_release(s);
+    }
     return freed;
   }
   const int32_t slot = find_slot(scope.workflow_id);
   if (slot < 0) return 0;
   check(sfkv_flush(pool_, slot, &freed), "sfkv_flush");
+  slot_pinned_[slot] = 0;
+  maybe_release(slot);
   return freed;
 }
 

@@ -19,16 +19,21 @@
 #include <functional>
 #include <map>
 #include <unordered_map>
+#include <vector>
 
 #include "sfkv.h"
 #include "stageflow/simulated_backend.hpp"
 
 namespace stageflow {
 
+// Initial pool sizes. The reference's cache is unbounded (std::map pins_), so the pool starts at
+// these sizes and grows on demand (sfkv_pool_reserve): more live workflows than slots, or a
+// prompt longer than max_pin_blocks * 16 tokens. A workflow's slot returns to a free list once it
+// holds no pin and has no request in this backend.
 struct GpuPoolOptions {
   int device = 0;
-  int max_workflows = 1 << 14;
-  int max_pin_blocks = 4096;  // 65,536-token pins
+  int max_workflows = 256;
+  int max_pin_blocks = 256;  // 4,096-token pins before the first reserve
 };
 
 class GpuPinnedBackend : public Backend {
@@ -70,18 +75,25 @@ class GpuPinnedBackend : public Backend {
   int busy_ = 0;
   std::deque<Pending> pending_;
   std::map<std::pair<std::string, std::string>, int> turns_;
+  // workflow id -> slot while the workflow holds a pin or has a request here
   std::unordered_map<std::string, int32_t> slots_;
+  std::vector<int32_t> free_slots_;
+  std::vector<int32_t> slot_requests_;  // requests of the slot's workflow queued or running here
+  std::vector<char> slot_pinned_;       // host mirror of "the pool holds a pin for this slot"
+  std::vector<std::string> slot_names_;
+  int32_t slot_cap_ = 0, pin_blocks_cap_ = 0;
+  std::unordered_map<std::string, std::uint32_t> intern_;  // this backend's token ids
   DispatchObserver observer_;
 
   void pump();
   void start(Pending item);
   ScriptedReply reply_for(const CompletionRequest& req, int turn) const;
-  int32_t slot_for(const std::string& workflow_id);  // creates
-  int32_t find_slot(const std::string& workflow_id) const;  // -1 when never seen
+  int32_t slot_for(const std::string& workflow_id);  // creates (grows the pool if needed)
+  int32_t find_slot(const std::string& workflow_id) const;  // -1 when none is held
+  void maybe_release(int32_t slot);
+  bool reserve(int32_t slots, int32_t pin_blocks);
+  std::uint32_t intern(const std::string& token);
   void check(int rc, const char* what) const;
 };
-
-/// Token-string interner shared by all GPU backends of a process (token id = first appearance).
-std::uint32_t intern_token(const std::string& token);
 
 }  // namespace stageflow

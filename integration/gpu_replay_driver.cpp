@@ -16,22 +16,61 @@
 
 using namespace stageflow;
 
+namespace {
+
+// --flaky REF:MODE (test double, the same rule as oracle/ref_shim/replay_driver.cpp): the
+// backend's flush throws on the first attempt of every flush action (mode 1) or always (2).
+class FlakyFlush : public Backend {
+ public:
+  FlakyFlush(std::shared_ptr<GpuPinnedBackend> inner, int mode) : inner_(std::move(inner)), mode_(mode) {}
+  const BackendDescriptor& descriptor() const override { return inner_->descriptor(); }
+  bool has_capacity() const override { return inner_->has_capacity(); }
+  void complete(CompletionRequest req, CompletionCallback cb) override { inner_->complete(std::move(req), std::move(cb)); }
+  long long flush(const FlushScope& scope) override {
+    ++attempts_;
+    if (mode_ == 2 || (mode_ == 1 && attempts_ % 2 == 1)) throw BackendError("flush failed (flaky test backend)");
+    return inner_->flush(scope);
+  }
+  double cache_utilization() const override { return inner_->cache_utilization(); }
+  bool preserve(const std::string& wf) override { return inner_->preserve(wf); }
+  const BackendStats& stats() const override { return inner_->stats(); }
+  void set_capacity_listener(std::function<void()> fn) override { inner_->set_capacity_listener(std::move(fn)); }
+
+ private:
+  std::shared_ptr<GpuPinnedBackend> inner_;
+  int mode_;
+  long long attempts_ = 0;
+};
+
+std::map<std::string, int> parse_flaky(const std::string& spec) {
+  std::map<std::string, int> m;
+  std::size_t i = 0;
+  while (i < spec.size()) {
+    std::size_t j = spec.find(',', i);
+    if (j == std::string::npos) j = spec.size();
+    const std::string item = spec.substr(i, j - i);
+    const std::size_t c = item.find(':');
+    if (c != std::string::npos) m[item.substr(0, c)] = std::stoi(item.substr(c + 1));
+    i = j + 1;
+  }
+  return m;
+}
+
+}  // namespace
+
 int main(int argc, char** argv) {
-  std::string config_path, trace_path, out_path;
+  std::string config_path, trace_path, out_path, flaky_spec;
   int device = 0;
   bool gpu_memory = false;
-  for (int i = 1; i < argc; ++i)
-    if (std::string(argv[i]) == "--gpu-memory") gpu_memory = true;
-  for (int i = 1; i + 1 < argc; i += 2) {
+  for (int i = 1; i < argc; ++i) {
     std::string a = argv[i];
-    if (a == "--gpu-memory") {
-      --i;
-      continue;
-    }
-    if (a == "--config") config_path = argv[i + 1];
-    else if (a == "--trace") trace_path = argv[i + 1];
-    else if (a == "--out") out_path = argv[i + 1];
-    else if (a == "--device") device = std::stoi(argv[i + 1]);
+    if (a == "--gpu-memory") { gpu_memory = true; continue; }
+    if (i + 1 >= argc) break;
+    if (a == "--config") config_path = argv[++i];
+    else if (a == "--trace") trace_path = argv[++i];
+    else if (a == "--out") out_path = argv[++i];
+    else if (a == "--device") device = std::stoi(argv[++i]);
+    else if (a == "--flaky") flaky_spec = argv[++i];
   }
   if (config_path.empty() || trace_path.empty() || out_path.empty()) {
     std::fprintf(stderr, "usage: sf_gpu_replay --config C --trace T --out O [--device D]\n");
@@ -45,11 +84,11 @@ int main(int argc, char** argv) {
 
   std::vector<json> out;
   BackendRegistry registry;
+  auto flaky = parse_flaky(flaky_spec);
   std::map<std::string, GpuPinnedBackend*> gpu;
   for (const auto& b : config.backends) {
-    GpuPoolOptions opt;
+    GpuPoolOptions opt;  // default sizes: the pool grows on demand (sfkv_pool_reserve)
     opt.device = device;
-    opt.max_workflows = static_cast<int>(trace.size()) + 8;
     auto be = std::make_shared<GpuPinnedBackend>(loop, b.descriptor, b.sim, opt, log);
     const std::string ref = b.descriptor.ref;
     be->set_dispatch_observer([&out, ref](const std::string& wf, const std::string& st,
@@ -57,15 +96,15 @@ int main(int argc, char** argv) {
       out.push_back({{"type", "req"}, {"b", ref}, {"wf", wf}, {"stage", st}, {"P", P}, {"M", M}});
     });
     gpu[ref] = be.get();
-    registry.add(be);
+    if (int mode = flaky[ref]) registry.add(std::make_shared<FlakyFlush>(be, mode));
+    else registry.add(be);
   }
   ToolRegistry tools;
   SignalBus bus;
   std::unique_ptr<MemoryManager> cpu_mem;
   std::unique_ptr<GpuMemoryManager> gpu_mem;
   if (gpu_memory) {
-    gpu_mem = std::make_unique<GpuMemoryManager>(config.memory, &registry,
-                                                 static_cast<int>(trace.size()) + 8, device, log);
+    gpu_mem = std::make_unique<GpuMemoryManager>(config.memory, &registry, 256, device, log);
     gpu_mem->attach(bus);
   } else {
     cpu_mem = std::make_unique<MemoryManager>(config.memory, &registry, log);

@@ -11,8 +11,11 @@
 //   sfref_reroute                     -> reroute_on_overload (orchestrator.cpp:78-87)
 //   sfref_mm_*                        -> MemoryManager::{on_signal, pressure_tick,
 //                                       set_workflow_chain, action_log} (memory.cpp:246-401),
-//                                       no backends attached (every action "applies")
+//                                       no backends attached (every action "applies"), or a
+//                                       registry of flaky test backends (sfref_mm_create_flaky)
 // Token ids are rendered to whitespace tokens "t<id>", the same text the reference tokenizes.
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -47,6 +50,39 @@ std::string render(const std::uint32_t* tok, long long n) {
   }
   return s;
 }
+
+// A test backend for the memory manager's apply_action (memory.cpp:185-220): only flush and
+// preserve are exercised; flush throws per its mode (see sfref_mm_create_flaky).
+class FlakyBackend : public Backend {
+ public:
+  FlakyBackend(std::string ref, int mode) : mode_(mode) {
+    desc_.ref = std::move(ref);
+    desc_.kind = BackendKind::Simulated;
+  }
+  const BackendDescriptor& descriptor() const override { return desc_; }
+  bool has_capacity() const override { return true; }
+  void complete(CompletionRequest, CompletionCallback) override { throw BackendError("not a serving backend"); }
+  long long flush(const FlushScope&) override {
+    ++attempts;
+    if (mode_ == 2 || (mode_ == 1 && attempts % 2 == 1)) throw BackendError("flush failed");
+    return 0;
+  }
+  double cache_utilization() const override { return 0; }
+  bool preserve(const std::string&) override { return true; }
+  const BackendStats& stats() const override { return stats_; }
+  long long attempts = 0;
+
+ private:
+  int mode_;
+  BackendDescriptor desc_;
+  BackendStats stats_;
+};
+
+struct RefMM {
+  BackendRegistry reg;
+  std::unique_ptr<MemoryManager> mm;
+};
+MemoryManager* MM(void* h) { return static_cast<RefMM*>(h)->mm.get(); }
 
 }  // namespace
 
@@ -255,13 +291,40 @@ void* sfref_mm_create(long long tau, double tau_pressure, int chain_len, const c
   cfg.tau = tau;
   cfg.tau_pressure = tau_pressure;
   cfg.policy_chain.assign(chain, chain + chain_len);
-  return new MemoryManager(cfg);
+  auto* r = new RefMM;
+  r->mm = std::make_unique<MemoryManager>(cfg);
+  return r;
 }
-void sfref_mm_destroy(void* h) { delete static_cast<MemoryManager*>(h); }
+// The same with a BackendRegistry of test backends whose flush fails: mode 0 never, 1 on the
+// first attempt of every flush action (the retry succeeds), 2 always (apply_action gives up after
+// the retry, memory.cpp:189-203, and the tracker entry is only unpreserved, memory.cpp:322-324).
+void* sfref_mm_create_flaky(long long tau, double tau_pressure, int chain_len, const char* const* chain,
+                            int n_backends, const char* const* refs, const int* modes) {
+  MemoryConfig cfg;
+  cfg.tau = tau;
+  cfg.tau_pressure = tau_pressure;
+  cfg.policy_chain.assign(chain, chain + chain_len);
+  auto* r = new RefMM;
+  for (int i = 0; i < n_backends; ++i) r->reg.add(std::make_shared<FlakyBackend>(refs[i], modes[i]));
+  r->mm = std::make_unique<MemoryManager>(cfg, &r->reg);
+  return r;
+}
+void sfref_mm_destroy(void* h) { delete static_cast<RefMM*>(h); }
+
+// Tracker entry of (wf, backend): 0 absent, 1 present and preserved, 2 present unpreserved.
+int sfref_mm_entry(void* h, const char* wf, const char* backend) {
+  const CacheEntry* e = MM(h)->tracker().entry(wf, backend);
+  return e ? (e->preserved ? 1 : 2) : 0;
+}
+// Flush calls a flaky backend received (attempts, including failed ones).
+long long sfref_mm_flush_attempts(void* h, const char* backend) {
+  auto& r = static_cast<RefMM*>(h)->reg;
+  return static_cast<FlakyBackend&>(r.at(backend)).attempts;
+}
 
 void sfref_mm_set_chain(void* h, const char* wf, int len, const char* const* names) {
   std::vector<std::string> v(names, names + len);
-  static_cast<MemoryManager*>(h)->set_workflow_chain(wf, v);
+  MM(h)->set_workflow_chain(wf, v);
 }
 
 // kind 0/1/2 = StageStart/StageComplete/WorkflowComplete; override 0/1/2 = None/Preserve/Flush.
@@ -280,10 +343,11 @@ int sfref_mm_on_signal(void* h, int kind, const char* wf, const char* stage, con
   sig.ts = ts;
   sig.cache_override = static_cast<CachePolicyOverride>(override_);
   try {
-    static_cast<MemoryManager*>(h)->on_signal(sig);
+    MM(h)->on_signal(sig);
   } catch (const OutOfOrderSignalError&) {
     return 1;
-  } catch (const std::logic_error&) {
+  } catch (const std::logic_error& e) {
+    if (std::getenv("SFREF_DEBUG")) std::fprintf(stderr, "sfref_mm_on_signal: %s\n", e.what());
     return 3;
   }
   return 0;
@@ -305,27 +369,27 @@ long long sfref_mm_on_signal_batch(void* h, long long n, const int* kind, const 
 int sfref_mm_pressure_tick(void* h, int n, const char* const* refs, const double* util, double now) {
   std::map<std::string, double> u;
   for (int i = 0; i < n; ++i) u[refs[i]] = util[i];
-  return static_cast<int>(static_cast<MemoryManager*>(h)->pressure_tick(u, now).size());
+  return static_cast<int>(MM(h)->pressure_tick(u, now).size());
 }
 
 // MemoryManager::export_action_log (memory.cpp:389-401) into buf (cap bytes); returns its length.
 long long sfref_mm_export(void* h, char* buf, long long cap) {
   std::ostringstream os;
-  static_cast<MemoryManager*>(h)->export_action_log(os);
+  MM(h)->export_action_log(os);
   const std::string s = os.str();
   if (static_cast<long long>(s.size()) <= cap) std::memcpy(buf, s.data(), s.size());
   return static_cast<long long>(s.size());
 }
 
 long long sfref_mm_log_size(void* h) {
-  return static_cast<long long>(static_cast<MemoryManager*>(h)->action_log().size());
+  return static_cast<long long>(MM(h)->action_log().size());
 }
 
 // Record i of the action log: kind 0/1/2 = Preserve/Flush/NoOp; strings copied (NUL-terminated,
 // truncated to cap bytes).
 void sfref_mm_log_get(void* h, long long i, int* kind, char* wf, char* backend, char* reason,
                       char* trigger, int cap, double* ts) {
-  const auto& r = static_cast<MemoryManager*>(h)->action_log().at(static_cast<std::size_t>(i));
+  const auto& r = MM(h)->action_log().at(static_cast<std::size_t>(i));
   *kind = static_cast<int>(r.action.kind);
   *ts = r.ts;
   auto put = [cap](char* dst, const std::string& s) {

@@ -60,10 +60,27 @@ struct Recorder {
   }
 };
 
+// --flaky REF:MODE: the backend's flush throws (test double for apply_action's retry path,
+// memory.cpp:189-203): mode 1 on the first attempt of every flush action (the retry succeeds),
+// mode 2 always. A throwing attempt never reaches the pin cache.
+std::map<std::string, int> parse_flaky(const std::string& spec) {
+  std::map<std::string, int> m;
+  std::size_t i = 0;
+  while (i < spec.size()) {
+    std::size_t j = spec.find(',', i);
+    if (j == std::string::npos) j = spec.size();
+    const std::string item = spec.substr(i, j - i);
+    const std::size_t c = item.find(':');
+    if (c != std::string::npos) m[item.substr(0, c)] = std::stoi(item.substr(c + 1));
+    i = j + 1;
+  }
+  return m;
+}
+
 class RecordingBackend : public Backend {
  public:
-  RecordingBackend(std::shared_ptr<SimulatedBackend> inner, Recorder& rec)
-      : inner_(std::move(inner)), rec_(rec) {}
+  RecordingBackend(std::shared_ptr<SimulatedBackend> inner, Recorder& rec, int flaky = 0)
+      : inner_(std::move(inner)), rec_(rec), flaky_(flaky) {}
 
   const BackendDescriptor& descriptor() const override { return inner_->descriptor(); }
   bool has_capacity() const override { return inner_->has_capacity(); }
@@ -89,6 +106,11 @@ class RecordingBackend : public Backend {
   }
 
   long long flush(const FlushScope& scope) override {
+    ++flush_attempts_;
+    if (flaky_ == 2 || (flaky_ == 1 && flush_attempts_ % 2 == 1)) {
+      rec_.push({{"type", "op"}, {"op", "flush_failed"}, {"b", descriptor().ref}, {"wf", scope.workflow_id}});
+      throw BackendError("flush failed (flaky test backend)");
+    }
     long long freed = inner_->flush(scope);
     rec_.push({{"type", "op"}, {"op", "flush"}, {"b", descriptor().ref},
                {"all", scope.all}, {"wf", scope.workflow_id}, {"freed", freed},
@@ -162,6 +184,8 @@ class RecordingBackend : public Backend {
   std::deque<std::size_t> pending_;
   int busy_ = 0;
   std::uint64_t last_rejections_ = 0;
+  int flaky_ = 0;
+  long long flush_attempts_ = 0;
 };
 
 const char* override_name(CachePolicyOverride o) {
@@ -175,7 +199,7 @@ const char* override_name(CachePolicyOverride o) {
 }  // namespace
 
 int main(int argc, char** argv) {
-  std::string config_path, trace_path, out_path, tok_path;
+  std::string config_path, trace_path, out_path, tok_path, flaky_spec;
   bool no_tok = false;
   for (int i = 1; i < argc; ++i) {
     std::string a = argv[i];
@@ -185,11 +209,12 @@ int main(int argc, char** argv) {
     else if (a == "--trace") trace_path = argv[++i];
     else if (a == "--out") out_path = argv[++i];
     else if (a == "--tok-out") tok_path = argv[++i];
+    else if (a == "--flaky") flaky_spec = argv[++i];
   }
   if (config_path.empty() || trace_path.empty() || out_path.empty()) {
     std::fprintf(stderr,
                  "usage: sf_ref_replay --config C.json --trace T.jsonl --out O.jsonl "
-                 "[--tok-out T.u32 | --no-tok]\n");
+                 "[--tok-out T.u32 | --no-tok] [--flaky REF:MODE,...]\n");
     return 2;
   }
   auto config = load_config(config_path);
@@ -208,12 +233,13 @@ int main(int argc, char** argv) {
 
   // build_registry (config.cpp:170-184), with each simulated backend wrapped.
   BackendRegistry registry;
+  auto flaky = parse_flaky(flaky_spec);
   std::map<std::string, RecordingBackend*> recs;
   json meta_backends = json::array();
   for (const auto& b : config.backends) {
     if (b.descriptor.kind != BackendKind::Simulated) throw std::runtime_error("simulated only");
     auto sim = std::make_shared<SimulatedBackend>(loop, b.descriptor, b.sim, log);
-    auto wrapped = std::make_shared<RecordingBackend>(sim, rec);
+    auto wrapped = std::make_shared<RecordingBackend>(sim, rec, flaky[b.descriptor.ref]);
     recs[b.descriptor.ref] = wrapped.get();
     registry.add(wrapped);
     meta_backends.push_back({{"ref", b.descriptor.ref}, {"model", b.descriptor.model},
@@ -226,7 +252,7 @@ int main(int argc, char** argv) {
   rec.push({{"type", "meta"}, {"label", config.label}, {"backends", meta_backends},
             {"tau", config.memory.tau}, {"tau_pressure", config.memory.tau_pressure},
             {"monitor_interval_ms", config.memory.monitor_interval_ms},
-            {"chain", config.memory.policy_chain}});
+            {"chain", config.memory.policy_chain}, {"flaky", flaky}});
 
   ToolRegistry tools;
   SignalBus bus;

@@ -737,76 +737,207 @@ enum { O_NONE = 0, O_PRESERVE = 1, O_FLUSH = 2 };
 enum { P_PSI = 1, P_FAB = 2 };
 enum { A_PRESERVE = 0, A_FLUSH = 1, A_NOOP = 2 };
 enum { R_OVERRIDE = 0, R_PSI = 1, R_FAB = 2, R_PRESSURE = 3, R_EXHAUSTED = 4 };
-#define MAXCH 8
-
 struct sfo_tracker {
   sfo_mm_config cfg;
-  int32_t W, NB;
+  int32_t W, NB, SW;
+  uint32_t epoch;     /* operation counter: batches and ticks (flush-failure feedback) */
+  uint8_t* def_chain; /* the default chain (copied) */
   uint8_t* completed;
-  uint64_t* started; /* started_ever_ (memory.hpp:165) */
-  uint64_t* open_;   /* open_stages_ */
+  uint64_t* started;  /* started_ever_ (memory.hpp:165): [W][SW] */
+  uint64_t* open_;    /* open_stages_: [W][SW] */
+  int32_t* open_cnt;
   uint8_t* last_valid;
   int32_t* last_b;
   int32_t* last_model;
   int64_t* last_tokens;
   int32_t* chain_len; /* -1: default chain (workflow_chains_ has no entry) */
-  uint8_t* chain;
-  uint8_t* present; /* entries_ [(wf, backend)] */
+  uint8_t** chain;    /* per workflow, malloc'd */
+  uint8_t* present;   /* entries_ [(wf, backend)] */
   uint8_t* preserved;
   int64_t* tokens;
   double* ts;
-  int32_t* inflight; /* in_flight_ [backend][wf] */
+  int32_t* inflight;  /* in_flight_ [backend][wf] */
+  uint64_t* mod;      /* tag of the last modification (see tracker.cu) */
   uint32_t* rank;
-  uint8_t* failed; /* per batch */
+  int32_t* border;    /* backends in std::string order */
+  uint8_t* failed;    /* per batch */
 };
 
+static uint64_t mod_tag(uint32_t epoch, int64_t sig, int kind) {
+  return ((uint64_t)epoch << 32) | ((uint64_t)(sig & 0x7fffffff) << 1) | (uint64_t)kind;
+}
+
+/* (Re)allocates the shaped arrays for (W, NB, SW), copying the old contents. */
+static int tracker_shape(sfo_tracker* t, int32_t W1, int32_t NB1, int32_t SW1) {
+  const int32_t W0 = t->W, NB0 = t->NB, SW0 = t->SW;
+  size_t W = (size_t)W1, E = W * (size_t)NB1, WS = W * (size_t)SW1;
+  uint8_t* completed = calloc(W, 1);
+  uint64_t* started = calloc(WS, 8);
+  uint64_t* open_ = calloc(WS, 8);
+  int32_t* open_cnt = calloc(W, 4);
+  uint8_t* last_valid = calloc(W, 1);
+  int32_t* last_b = calloc(W, 4);
+  int32_t* last_model = calloc(W, 4);
+  int64_t* last_tokens = calloc(W, 8);
+  int32_t* chain_len = malloc(W * 4);
+  uint8_t** chain = calloc(W, sizeof(uint8_t*));
+  uint8_t* present = calloc(E, 1);
+  uint8_t* preserved = calloc(E, 1);
+  int64_t* tokens = calloc(E, 8);
+  double* ts = calloc(E, 8);
+  int32_t* inflight = calloc(E, 4);
+  uint64_t* mod = calloc(E, 8);
+  uint32_t* rank = calloc(W, 4);
+  int32_t* border = malloc((size_t)NB1 * 4);
+  uint8_t* failed = calloc(W, 1);
+  for (int32_t w = 0; w < W1; ++w) {
+    const int old = w < W0;
+    completed[w] = old ? t->completed[w] : 0;
+    for (int32_t q = 0; q < SW1; ++q) {
+      started[(size_t)w * SW1 + q] = old && q < SW0 ? t->started[(size_t)w * SW0 + q] : 0;
+      open_[(size_t)w * SW1 + q] = old && q < SW0 ? t->open_[(size_t)w * SW0 + q] : 0;
+    }
+    open_cnt[w] = old ? t->open_cnt[w] : 0;
+    last_valid[w] = old ? t->last_valid[w] : 0;
+    last_b[w] = old ? t->last_b[w] : -1;
+    last_model[w] = old ? t->last_model[w] : -1;
+    last_tokens[w] = old ? t->last_tokens[w] : 0;
+    chain_len[w] = old ? t->chain_len[w] : -1;
+    chain[w] = old ? t->chain[w] : NULL;
+    rank[w] = old ? t->rank[w] : (uint32_t)w;
+    for (int32_t b = 0; b < NB1; ++b) {
+      const int ob = old && b < NB0;
+      size_t e = (size_t)w * NB1 + b, f = (size_t)w * NB0 + b;
+      present[e] = ob ? t->present[f] : 0;
+      preserved[e] = ob ? t->preserved[f] : 0;
+      tokens[e] = ob ? t->tokens[f] : 0;
+      ts[e] = ob ? t->ts[f] : 0;
+      inflight[e] = ob ? t->inflight[f] : 0;
+      mod[e] = ob ? t->mod[f] : 0;
+    }
+  }
+  for (int32_t b = 0; b < NB1; ++b) border[b] = b < NB0 ? t->border[b] : b;
+  free(t->completed); free(t->started); free(t->open_); free(t->open_cnt); free(t->last_valid);
+  free(t->last_b); free(t->last_model); free(t->last_tokens); free(t->chain_len); free(t->chain);
+  free(t->present); free(t->preserved); free(t->tokens); free(t->ts); free(t->inflight);
+  free(t->mod); free(t->rank); free(t->border); free(t->failed);
+  t->completed = completed; t->started = started; t->open_ = open_; t->open_cnt = open_cnt;
+  t->last_valid = last_valid; t->last_b = last_b; t->last_model = last_model;
+  t->last_tokens = last_tokens; t->chain_len = chain_len; t->chain = chain; t->present = present;
+  t->preserved = preserved; t->tokens = tokens; t->ts = ts; t->inflight = inflight; t->mod = mod;
+  t->rank = rank; t->border = border; t->failed = failed;
+  t->W = W1; t->NB = NB1; t->SW = SW1;
+  return 0;
+}
+
 int sfo_tracker_create(const sfo_mm_config* cfg, sfo_tracker** out) {
-  if (!cfg || !out || cfg->max_workflows <= 0 || cfg->n_backends <= 0 || cfg->chain_len < 0 ||
-      cfg->chain_len > MAXCH || cfg->tau <= 0 || !(cfg->tau_pressure > 0) || cfg->tau_pressure > 1)
+  if (!cfg || !out || cfg->max_workflows <= 0 || cfg->n_backends <= 0 || cfg->max_stages < 0 ||
+      cfg->chain_len < 0 || (cfg->chain_len && !cfg->chain) || cfg->tau <= 0 ||
+      !(cfg->tau_pressure > 0) || cfg->tau_pressure > 1)
     return -1; /* memory.cpp:240-243 */
+  for (int32_t i = 0; i < cfg->chain_len; ++i)
+    if (cfg->chain[i] != P_PSI && cfg->chain[i] != P_FAB) return -1; /* memory.cpp:182 */
   sfo_tracker* t = (sfo_tracker*)calloc(1, sizeof(*t));
   t->cfg = *cfg;
-  t->W = cfg->max_workflows;
-  t->NB = cfg->n_backends;
-  size_t W = (size_t)t->W, E = W * (size_t)t->NB;
-  t->completed = calloc(W, 1);
-  t->started = calloc(W, 8);
-  t->open_ = calloc(W, 8);
-  t->last_valid = calloc(W, 1);
-  t->last_b = calloc(W, 4);
-  t->last_model = calloc(W, 4);
-  t->last_tokens = calloc(W, 8);
-  t->chain_len = malloc(W * 4);
-  for (size_t w = 0; w < W; ++w) t->chain_len[w] = -1;
-  t->chain = calloc(W * MAXCH, 1);
-  t->present = calloc(E, 1);
-  t->preserved = calloc(E, 1);
-  t->tokens = calloc(E, 8);
-  t->ts = calloc(E, 8);
-  t->inflight = calloc(E, 4);
-  t->rank = calloc(W, 4);
-  for (size_t w = 0; w < W; ++w) t->rank[w] = (uint32_t)w;
-  t->failed = calloc(W, 1);
+  t->def_chain = malloc((size_t)(cfg->chain_len > 0 ? cfg->chain_len : 1));
+  if (cfg->chain_len) memcpy(t->def_chain, cfg->chain, (size_t)cfg->chain_len);
+  t->cfg.chain = t->def_chain;
+  tracker_shape(t, cfg->max_workflows, cfg->n_backends, cfg->max_stages > 0 ? (cfg->max_stages + 63) / 64 : 1);
   *out = t;
   return 0;
 }
 
 int sfo_tracker_destroy(sfo_tracker* t) {
   if (!t) return -1;
-  free(t->completed); free(t->started); free(t->open_); free(t->last_valid); free(t->last_b);
-  free(t->last_model); free(t->last_tokens); free(t->chain_len); free(t->chain); free(t->present);
-  free(t->preserved); free(t->tokens); free(t->ts); free(t->inflight); free(t->rank); free(t->failed);
+  for (int32_t w = 0; w < t->W; ++w) free(t->chain[w]);
+  free(t->completed); free(t->started); free(t->open_); free(t->open_cnt); free(t->last_valid);
+  free(t->last_b); free(t->last_model); free(t->last_tokens); free(t->chain_len); free(t->chain);
+  free(t->present); free(t->preserved); free(t->tokens); free(t->ts); free(t->inflight);
+  free(t->mod); free(t->rank); free(t->border); free(t->failed); free(t->def_chain);
   free(t);
   return 0;
 }
 
-int sfo_set_workflow_chain(sfo_tracker* t, int32_t wf, int32_t len, const uint8_t* policies) {
-  if (!t || wf < 0 || wf >= t->W || len < 0 || len > MAXCH || (len && !policies)) return -1;
-  if (len == 0) return 0; /* memory.cpp:248 */
-  for (int32_t i = 0; i < len; ++i) {
-    if (policies[i] != P_PSI && policies[i] != P_FAB) return -1; /* unknown policy */
-    t->chain[(size_t)wf * MAXCH + i] = policies[i];
+int sfo_tracker_reserve(sfo_tracker* t, int32_t max_workflows, int32_t n_backends, int32_t max_stages) {
+  if (!t) return -1;
+  int32_t W1 = max_workflows > t->W ? max_workflows : t->W;
+  int32_t NB1 = n_backends > t->NB ? n_backends : t->NB;
+  int32_t SW1 = max_stages > 0 ? (max_stages + 63) / 64 : 1;
+  if (SW1 < t->SW) SW1 = t->SW;
+  if (W1 == t->W && NB1 == t->NB && SW1 == t->SW) return 0;
+  return tracker_shape(t, W1, NB1, SW1);
+}
+
+int sfo_tracker_shape(sfo_tracker* t, int32_t* max_workflows, int32_t* n_backends, int32_t* max_stages) {
+  if (!t) return -1;
+  if (max_workflows) *max_workflows = t->W;
+  if (n_backends) *n_backends = t->NB;
+  if (max_stages) *max_stages = t->SW * 64;
+  return 0;
+}
+
+static void forget_workflow(sfo_tracker* t, int32_t w) {
+  t->completed[w] = 0;
+  for (int32_t q = 0; q < t->SW; ++q) t->started[(size_t)w * t->SW + q] = t->open_[(size_t)w * t->SW + q] = 0;
+  t->open_cnt[w] = 0;
+  t->last_valid[w] = 0;
+  t->last_b[w] = -1;
+  t->last_model[w] = -1;
+  t->last_tokens[w] = 0;
+  t->chain_len[w] = -1;
+  free(t->chain[w]);
+  t->chain[w] = NULL;
+  for (int32_t b = 0; b < t->NB; ++b) {
+    size_t e = (size_t)w * t->NB + b;
+    t->present[e] = t->preserved[e] = 0;
+    t->tokens[e] = 0;
+    t->ts[e] = 0;
+    t->inflight[e] = 0;
+    t->mod[e] = 0;
   }
+}
+
+int sfo_reset_workflows(sfo_tracker* t, int64_t n, const int32_t* wf) {
+  if (!t || n < 0 || (n && !wf)) return -1;
+  for (int64_t i = 0; i < n; ++i)
+    if (wf[i] < 0 || wf[i] >= t->W) return -1;
+  for (int64_t i = 0; i < n; ++i) forget_workflow(t, wf[i]);
+  return 0;
+}
+
+int sfo_set_backend_order(sfo_tracker* t, int32_t n, const int32_t* order) {
+  if (!t || n != t->NB || !order) return -1;
+  for (int32_t k = 0; k < n; ++k) {
+    if (order[k] < 0 || order[k] >= n) return -1;
+    for (int32_t j = 0; j < k; ++j)
+      if (order[j] == order[k]) return -1;
+  }
+  memcpy(t->border, order, (size_t)n * 4);
+  return 0;
+}
+
+int sfo_flush_failed(sfo_tracker* t, int64_t n, const int32_t* wf, const int32_t* backend, const int64_t* sig) {
+  if (!t || n < 0 || (n && (!wf || !backend || !sig))) return -1;
+  for (int64_t i = 0; i < n; ++i)
+    if (wf[i] < 0 || wf[i] >= t->W || backend[i] < 0 || backend[i] >= t->NB) return -1;
+  for (int64_t i = 0; i < n; ++i) {
+    size_t e = (size_t)wf[i] * t->NB + backend[i];
+    if (t->mod[e] == mod_tag(t->epoch, sig[i] < 0 ? 0 : sig[i], 0)) { /* mark_unpreserved */
+      t->present[e] = 1;
+      t->preserved[e] = 0;
+    }
+  }
+  return 0;
+}
+
+int sfo_set_workflow_chain(sfo_tracker* t, int32_t wf, int32_t len, const uint8_t* policies) {
+  if (!t || wf < 0 || wf >= t->W || len < 0 || (len && !policies)) return -1;
+  if (len == 0) return 0; /* memory.cpp:248 */
+  for (int32_t i = 0; i < len; ++i)
+    if (policies[i] != P_PSI && policies[i] != P_FAB) return -1; /* unknown policy */
+  free(t->chain[wf]);
+  t->chain[wf] = malloc((size_t)len);
+  memcpy(t->chain[wf], policies, (size_t)len);
   t->chain_len[wf] = len;
   return 0;
 }
@@ -834,14 +965,16 @@ static int pol_psi(const sfo_tracker* t, int w, uint8_t kind, int32_t b, int32_t
 static int pol_fab(const sfo_tracker* t, int w, uint8_t kind, int32_t b, int32_t m, act_t* a) {
   int n = 0;
   size_t e0 = (size_t)w * t->NB;
-  if (kind == K_WF_COMPLETE) {
-    for (int32_t bb = 0; bb < t->NB; ++bb)
+  if (kind == K_WF_COMPLETE) { /* preserved_entries(wf): map order = backend-ref order */
+    for (int32_t k = 0; k < t->NB; ++k) {
+      const int32_t bb = t->border[k];
       if (t->present[e0 + bb] && t->preserved[e0 + bb]) {
         a[n].kind = A_FLUSH;
         a[n].b = bb;
         a[n].reason = R_FAB;
         ++n;
       }
+    }
     return n;
   }
   if (kind == K_START && t->last_valid[w] && (t->last_b[w] != b || t->last_model[w] != m)) {
@@ -856,11 +989,14 @@ static int pol_fab(const sfo_tracker* t, int w, uint8_t kind, int32_t b, int32_t
   return n;
 }
 
+static int stage_bit(const uint64_t* words, int32_t s) { return (int)((words[s >> 6] >> (s & 63)) & 1u); }
+
 int sfo_on_signal_batch(sfo_tracker* t, int64_t n, const sfo_signals* sg, const sfo_records* out) {
   if (!t || !sg || !out || n < 0) return -1;
-  const int32_t NB = t->NB;
+  const int32_t NB = t->NB, SW = t->SW;
   act_t* acts = (act_t*)malloc(sizeof(act_t) * (size_t)(NB > 1 ? NB : 1));
   memset(t->failed, 0, (size_t)t->W);
+  ++t->epoch;
   for (int64_t i = 0; i < n; ++i) {
     const int32_t w = sg->wf[i];
     const uint8_t kind = sg->kind[i];
@@ -871,7 +1007,8 @@ int sfo_on_signal_batch(sfo_tracker* t, int64_t n, const sfo_signals* sg, const 
     const double ts = sg->ts[i];
     const uint8_t ov = sg->override_ ? sg->override_[i] : O_NONE;
     out->count[i] = 0;
-    if (w < 0 || w >= t->W || kind > 2 || (kind != K_WF_COMPLETE && (b < 0 || b >= NB || s < 0 || s >= 64))) {
+    if (w < 0 || w >= t->W || kind > 2 ||
+        (kind != K_WF_COMPLETE && (b < 0 || b >= NB || s < 0 || s >= SW * 64))) {
       free(acts);
       return -1;
     }
@@ -879,11 +1016,12 @@ int sfo_on_signal_batch(sfo_tracker* t, int64_t n, const sfo_signals* sg, const 
       out->status[i] = 2;
       continue;
     }
+    uint64_t* started = t->started + (size_t)w * SW;
+    uint64_t* open_ = t->open_ + (size_t)w * SW;
     /* check_order (memory.cpp:256-285) */
-    const uint64_t bit = 1ull << s;
-    int bad = t->completed[w] || (kind == K_START && (t->started[w] & bit)) ||
-              (kind == K_COMPLETE && !(t->open_[w] & bit)) ||
-              (kind == K_WF_COMPLETE && t->open_[w] != 0);
+    int bad = t->completed[w] || (kind == K_START && stage_bit(started, s)) ||
+              (kind == K_COMPLETE && !stage_bit(open_, s)) ||
+              (kind == K_WF_COMPLETE && t->open_cnt[w] != 0);
     if (!bad && kind == K_COMPLETE && t->inflight[(size_t)w * NB + b] <= 0) {
       /* adjust_in_flight(-1) would go negative: logic_error (memory.cpp:92) after logging */
       bad = 3;
@@ -906,7 +1044,7 @@ int sfo_on_signal_batch(sfo_tracker* t, int64_t n, const sfo_signals* sg, const 
       na = 1;
     } else {
       const int32_t len = t->chain_len[w] >= 0 ? t->chain_len[w] : t->cfg.chain_len;
-      const uint8_t* ch = t->chain_len[w] >= 0 ? t->chain + (size_t)w * MAXCH : t->cfg.chain;
+      const uint8_t* ch = t->chain_len[w] >= 0 ? t->chain[w] : t->def_chain;
       for (int32_t p = 0; p < len && na == 0; ++p)
         na = ch[p] == P_PSI ? pol_psi(t, w, kind, b, m, T, acts) : pol_fab(t, w, kind, b, m, acts);
       if (na == 0) {
@@ -914,12 +1052,16 @@ int sfo_on_signal_batch(sfo_tracker* t, int64_t n, const sfo_signals* sg, const 
         na = 1;
       }
     }
-    /* apply_and_record (memory.cpp:312-328): flushes succeed -> mark_flushed */
+    /* apply_and_record (memory.cpp:312-328): flushes are recorded as applied -> mark_flushed
+     * (a failure reported later by sfo_flush_failed turns it into mark_unpreserved) */
     for (int a = 0; a < na; ++a) {
       out->kind[(size_t)i * NB + a] = acts[a].kind;
       out->backend[(size_t)i * NB + a] = acts[a].b;
       out->reason[(size_t)i * NB + a] = acts[a].reason;
-      if (acts[a].kind == A_FLUSH) t->present[(size_t)w * NB + acts[a].b] = 0;
+      if (acts[a].kind == A_FLUSH) {
+        t->present[(size_t)w * NB + acts[a].b] = 0;
+        t->mod[(size_t)w * NB + acts[a].b] = mod_tag(t->epoch, i, 0);
+      }
     }
     out->count[i] = na;
     if (bad == 3) { /* the records were logged, then update_tracker threw */
@@ -927,7 +1069,8 @@ int sfo_on_signal_batch(sfo_tracker* t, int64_t n, const sfo_signals* sg, const 
       t->failed[w] = 1;
       /* update_tracker erased the open stage, then adjust_in_flight stored -1 and threw
        * (memory.cpp:338-339, 90-92) */
-      t->open_[w] &= ~bit;
+      open_[s >> 6] &= ~(1ull << (s & 63));
+      t->open_cnt[w] -= 1;
       t->inflight[(size_t)w * NB + b] -= 1;
       continue;
     }
@@ -935,16 +1078,24 @@ int sfo_on_signal_batch(sfo_tracker* t, int64_t n, const sfo_signals* sg, const 
     /* update_tracker (memory.cpp:330-360) */
     const size_t e = (size_t)w * NB + (b < 0 ? 0 : b);
     if (kind == K_START) {
-      t->started[w] |= bit;
-      t->open_[w] |= bit;
+      started[s >> 6] |= 1ull << (s & 63);
+      open_[s >> 6] |= 1ull << (s & 63);
+      t->open_cnt[w] += 1;
       t->inflight[e] += 1;
+      if (t->inflight[e] < 0) { /* a count left negative by an earlier throw stays negative:
+                                  * adjust_in_flight(+1) stores it and throws (memory.cpp:90-92) */
+        out->status[i] = 3;
+        t->failed[w] = 1;
+      }
     } else if (kind == K_COMPLETE) {
-      t->open_[w] &= ~bit;
+      open_[s >> 6] &= ~(1ull << (s & 63));
+      t->open_cnt[w] -= 1;
       t->inflight[e] -= 1;
       t->present[e] = 1;
       t->preserved[e] = T > 0;
       t->tokens[e] = T;
       t->ts[e] = ts;
+      t->mod[e] = mod_tag(t->epoch, i, 1);
       t->last_valid[w] = 1;
       t->last_b[w] = b;
       t->last_model[w] = m;
@@ -954,11 +1105,14 @@ int sfo_on_signal_batch(sfo_tracker* t, int64_t n, const sfo_signals* sg, const 
       for (int32_t bb = 0; bb < NB; ++bb) {
         t->present[(size_t)w * NB + bb] = 0;
         t->inflight[(size_t)w * NB + bb] = 0;
+        t->mod[(size_t)w * NB + bb] = mod_tag(t->epoch, i, 1);
       }
       t->last_valid[w] = 0;
-      t->started[w] = 0;
-      t->open_[w] = 0;
+      for (int32_t q = 0; q < SW; ++q) started[q] = open_[q] = 0;
+      t->open_cnt[w] = 0;
       t->chain_len[w] = -1;
+      free(t->chain[w]);
+      t->chain[w] = NULL;
     }
   }
   free(acts);
@@ -968,6 +1122,7 @@ int sfo_on_signal_batch(sfo_tracker* t, int64_t n, const sfo_signals* sg, const 
 /* pressure_tick -> pressure_actions (memory.cpp:150-169, 382-387) */
 int sfo_pressure_tick(sfo_tracker* t, const double* util, int32_t* out_victim) {
   if (!t || !util || !out_victim) return -1;
+  ++t->epoch;
   for (int32_t b = 0; b < t->NB; ++b) {
     out_victim[b] = -1;
     if (!(util[b] > t->cfg.tau_pressure)) continue;
@@ -982,7 +1137,11 @@ int sfo_pressure_tick(sfo_tracker* t, const double* util, int32_t* out_victim) {
     out_victim[b] = best;
   }
   for (int32_t b = 0; b < t->NB; ++b)
-    if (out_victim[b] >= 0) t->present[(size_t)out_victim[b] * t->NB + b] = 0; /* mark_flushed */
+    if (out_victim[b] >= 0) { /* mark_flushed */
+      size_t e = (size_t)out_victim[b] * t->NB + b;
+      t->present[e] = 0;
+      t->mod[e] = mod_tag(t->epoch, 0, 0);
+    }
   return 0;
 }
 

@@ -87,8 +87,9 @@ typedef struct sfo_mm_config { /* same layout as sfmm_config */
   int32_t device;
   int32_t max_workflows;
   int32_t n_backends;
+  int32_t max_stages;
   int32_t chain_len;
-  uint8_t chain[8];
+  const uint8_t* chain;
   int64_t tau;
   double tau_pressure;
 } sfo_mm_config;
@@ -117,6 +118,12 @@ int sfo_on_signal_batch(sfo_tracker* t, int64_t n, const sfo_signals* sig, const
 int sfo_pressure_tick(sfo_tracker* t, const double* util, int32_t* out_victim);
 int sfo_tracker_entries(sfo_tracker* t, uint8_t* present, uint8_t* preserved, int64_t* tokens,
                         double* ts, int32_t* in_flight);
+int sfo_tracker_reserve(sfo_tracker* t, int32_t max_workflows, int32_t n_backends, int32_t max_stages);
+int sfo_tracker_shape(sfo_tracker* t, int32_t* max_workflows, int32_t* n_backends, int32_t* max_stages);
+int sfo_reset_workflows(sfo_tracker* t, int64_t n, const int32_t* wf);
+int sfo_set_backend_order(sfo_tracker* t, int32_t n, const int32_t* order);
+int sfo_flush_failed(sfo_tracker* t, int64_t n, const int32_t* wf, const int32_t* backend,
+                     const int64_t* sig);
 
 
 /* ---- tokenizer + interner (restates tokenize_whitespace / context_token_sequence) -------- */

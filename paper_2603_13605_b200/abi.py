@@ -97,6 +97,8 @@ GPU_ONLY = {
     "abi_version": [],
     "last_error": [],
     "pool_set_stream": [P, P],
+    "pool_reserve": [P, i32, i32, i64],
+    "pool_config_get": [P, C.POINTER(PoolConfig)],
     "pool_sync": [P],
     "match_batch_dev": [P, i64, P, P, P, i64, P, P],
     "lookup_batch_dev": [P, i64, P, P, i64, P, P],
@@ -134,12 +136,18 @@ MM_FNS = {
     "on_signal_batch": [P, i64, P, P],
     "pressure_tick": [P, P, P],
     "tracker_entries": [P, P, P, P, P, P],
+    "tracker_reserve": [P, i32, i32, i32],
+    "tracker_shape": [P, P, P, P],
+    "reset_workflows": [P, i64, P],
+    "set_backend_order": [P, i32, P],
+    "flush_failed": [P, i64, P, P, P],
 }
 MM_GPU_ONLY = {
     "tracker_set_stream": [P, P],
     "tracker_sync": [P],
     "tracker_reset": [P],
     "on_signal_batch_dev": [P, i64, P, P],
+    "pressure_tick_dev": [P, P, P],
 }
 _RESTYPES = {
     "block_digest": u64,
@@ -415,8 +423,9 @@ class MmConfig(C.Structure):  # sfmm_config / sfo_mm_config
         ("device", C.c_int32),
         ("max_workflows", C.c_int32),
         ("n_backends", C.c_int32),
+        ("max_stages", C.c_int32),
         ("chain_len", C.c_int32),
-        ("chain", C.c_uint8 * 8),
+        ("chain", C.c_void_p),
         ("tau", C.c_int64),
         ("tau_pressure", C.c_double),
     ]
@@ -435,16 +444,37 @@ class Tracker:
     """GPU-resident (or oracle) MemoryManager tracker over dense ids (host-pointer entry points)."""
 
     def __init__(self, api: Api, max_workflows: int, n_backends: int, chain=("preserve_small_increment",
-                 "flush_at_boundary"), tau=512, tau_pressure=0.85, device=0):
+                 "flush_at_boundary"), tau=512, tau_pressure=0.85, device=0, max_stages=0):
         cfg = MmConfig()
         cfg.device, cfg.max_workflows, cfg.n_backends = device, max_workflows, n_backends
-        cfg.chain_len = len(chain)
-        for i, c in enumerate(chain):
-            cfg.chain[i] = MM_POLICY[c]
+        cfg.max_stages = max_stages
+        codes = np.array([MM_POLICY[c] for c in chain] or [0], dtype=np.uint8)
+        cfg.chain_len, cfg.chain = len(chain), codes.ctypes.data
         cfg.tau, cfg.tau_pressure = tau, tau_pressure
         self.api, self.W, self.NB = api, max_workflows, n_backends
         self.h = C.c_void_p()
         api.check("tracker_create", api.mm_tracker_create(C.byref(cfg), C.byref(self.h)))
+
+    def reserve(self, max_workflows=0, n_backends=0, max_stages=0):
+        self.api.check("tracker_reserve", self.api.mm_tracker_reserve(self.h, max_workflows, n_backends, max_stages))
+        w, b, s = C.c_int32(), C.c_int32(), C.c_int32()
+        self.api.check("tracker_shape", self.api.mm_tracker_shape(self.h, C.byref(w), C.byref(b), C.byref(s)))
+        self.W, self.NB = w.value, b.value
+        return w.value, b.value, s.value
+
+    def reset_workflows(self, wf):
+        wf = np.ascontiguousarray(wf, np.int32)
+        self.api.check("reset_workflows", self.api.mm_reset_workflows(self.h, len(wf), _ptr(wf)))
+
+    def set_backend_order(self, order):
+        order = np.ascontiguousarray(order, np.int32)
+        self.api.check("set_backend_order", self.api.mm_set_backend_order(self.h, len(order), _ptr(order)))
+
+    def flush_failed(self, wf, backend, sig):
+        """Flush records that failed twice (sig = index in the last batch, -1 = the last tick)."""
+        wf, backend = np.ascontiguousarray(wf, np.int32), np.ascontiguousarray(backend, np.int32)
+        sig = np.ascontiguousarray(sig, np.int64)
+        self.api.check("flush_failed", self.api.mm_flush_failed(self.h, len(wf), _ptr(wf), _ptr(backend), _ptr(sig)))
 
     def close(self):
         if self.h:

@@ -108,6 +108,60 @@ static void pool_free(sfkv_pool* p) {
   delete p;
 }
 
+// sfkv_pool_reserve: pins copied into the grown [W2][MB2] block tables and [W2][32 G2][stride]
+// token copies; new slots start without a pin.
+__global__ void pin_regrow_kernel(const int64_t* len0, const int32_t* nblk0, const int32_t* blk0,
+                                  const uint32_t* tok0, int64_t W0, int64_t MB0, int64_t G0,
+                                  int64_t* len1, int32_t* nblk1, int32_t* blk1, uint32_t* tok1,
+                                  int64_t W1, int64_t MB1, int64_t G1) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t w = t0; w < W1; w += stride) {
+    len1[w] = w < W0 ? len0[w] : -1;
+    nblk1[w] = w < W0 ? nblk0[w] : 0;
+  }
+  // one thread per (workflow, block) of the old layout: table entry + its 16 token words
+  for (int64_t i = t0; i < W0 * MB0; i += stride) {
+    const int64_t w = i / MB0, k = i - w * MB0;
+    if (len0[w] < 0 || k >= nblk0[w]) continue;
+    blk1[w * MB1 + k] = blk0[i];
+    const uint4* s = reinterpret_cast<const uint4*>(tok0 + pin_tok_index(w, k, 0, G0));
+    uint4* d = reinterpret_cast<uint4*>(tok1 + pin_tok_index(w, k, 0, G1));
+#pragma unroll
+    for (int q = 0; q < BT / 4; ++q) d[q] = s[q];
+  }
+}
+
+// New block ids [B0, B1): unreferenced, free, outside the table.
+__global__ void blocks_grow_kernel(sfkv_pool P, int64_t B0) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = B0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < P.cfg.n_blocks; b += stride) {
+    P.blk_ref[b] = 0;
+    P.blk_in_table[b] = 0;
+    P.blk_n[b] = 0;
+    P.blk_slot[b] = -1;
+    P.blk_key[b] = 0;
+    atomicOr(&P.free_bits[b >> 5], 1u << (b & 31));
+  }
+}
+
+template <class T>
+static int dgrow(T** p, size_t old_n, size_t new_n, cudaStream_t st) {
+  T* q = nullptr;
+  if (int rc = dalloc(&q, new_n)) return rc;
+  if (old_n) {
+    cudaError_t e = cudaMemcpyAsync(q, *p, old_n * sizeof(T), cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) {
+      cudaFree(q);
+      return cuda_fail(e, "pool_reserve copy");
+    }
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(*p);
+  *p = q;
+  return 0;
+}
+
 static int read_counters(sfkv_pool* p) {
   SFKV_CUDA(cudaMemcpyAsync(p->ctr_host, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, p->stream));
   SFKV_CUDA(cudaStreamSynchronize(p->stream));
@@ -196,6 +250,91 @@ int sfkv_pool_create(const sfkv_pool_config* cfg, sfkv_pool** out) {
     return cuda_fail(e, "pool_create init");
   }
   *out = p;
+  return 0;
+}
+
+int sfkv_pool_reserve(sfkv_pool* p, int32_t max_workflows, int32_t max_pin_blocks, int64_t n_blocks) {
+  if (!p) return fail(SFKV_EINVAL, "null pool");
+  if (max_pin_blocks > (1 << 26) || n_blocks >= INT32_MAX)
+    return fail(SFKV_EINVAL, "pool_reserve: size out of range");
+  DeviceGuard g(p->cfg.device);
+  cudaStream_t st = p->stream;
+  SFKV_CUDA(cudaStreamSynchronize(st));
+  if (p->aux) SFKV_CUDA(cudaStreamSynchronize(p->aux));
+  const int64_t W0 = p->cfg.max_workflows, MB0 = p->cfg.max_pin_blocks, B0 = p->cfg.n_blocks;
+  const int64_t W1 = std::max<int64_t>(W0, max_workflows), MB1 = std::max<int64_t>(MB0, max_pin_blocks),
+                B1 = std::max<int64_t>(B0, n_blocks);
+  if (W1 > W0 || MB1 > MB0) {
+    sfkv_pool_config c1 = p->cfg;
+    c1.max_workflows = (int32_t)W1;
+    c1.max_pin_blocks = (int32_t)MB1;
+    const int64_t G0 = pin_groups(p->cfg), G1 = pin_groups(c1);
+    int64_t* len1 = nullptr;
+    int32_t *nblk1 = nullptr, *blk1 = nullptr;
+    uint32_t* tok1 = nullptr;
+    int rc = 0;
+    if ((rc = dalloc(&len1, W1)) || (rc = dalloc(&nblk1, W1)) || (rc = dalloc(&blk1, W1 * MB1)) ||
+        (rc = dalloc(&tok1, W1 * G1 * 32 * PIN_STRIDE))) {
+      cudaFree(len1); cudaFree(nblk1); cudaFree(blk1); cudaFree(tok1);
+      return rc;
+    }
+    pin_regrow_kernel<<<1184, 256, 0, st>>>(p->pin_len, p->pin_nblk, p->pin_blk, p->pin_tok, W0, MB0, G0,
+                                            len1, nblk1, blk1, tok1, W1, MB1, G1);
+    SFKV_LAUNCH_CHECK("pin_regrow_kernel");
+    SFKV_CUDA(cudaStreamSynchronize(st));
+    cudaFree(p->pin_len); cudaFree(p->pin_nblk); cudaFree(p->pin_blk); cudaFree(p->pin_tok);
+    p->pin_len = len1; p->pin_nblk = nblk1; p->pin_blk = blk1; p->pin_tok = tok1;
+    p->cfg.max_workflows = (int32_t)W1;
+    p->cfg.max_pin_blocks = (int32_t)MB1;
+  }
+  if (B1 > B0) {
+    if (p->kv && p->exported)
+      return fail(SFKV_EINVAL, "pool_reserve: the KV region was exported (CUDA IPC); it cannot move");
+    const int64_t nw1 = (B1 + 31) / 32;
+    int rc = 0;
+    if ((rc = dgrow(&p->blk_key, B0, B1, st)) || (rc = dgrow(&p->blk_tok, B0 * BT, B1 * BT, st)) ||
+        (rc = dgrow(&p->blk_n, B0, B1, st)) || (rc = dgrow(&p->blk_in_table, B0, B1, st)) ||
+        (rc = dgrow(&p->blk_ref, B0, B1, st)) || (rc = dgrow(&p->blk_slot, B0, B1, st)) ||
+        (rc = dgrow(&p->free_bits, p->n_words, nw1, st)))
+      return rc;
+    SFKV_CUDA(cudaMemsetAsync(p->blk_tok + B0 * BT, 0, (B1 - B0) * BT * sizeof(uint32_t), st));
+    if (nw1 > p->n_words)
+      SFKV_CUDA(cudaMemsetAsync(p->free_bits + p->n_words, 0, (nw1 - p->n_words) * sizeof(uint32_t), st));
+    if (p->kv) {
+      if ((rc = dgrow(&p->kv, B0 * p->block_bytes, B1 * p->block_bytes, st))) return rc;
+      SFKV_CUDA(cudaMemsetAsync(p->kv + B0 * p->block_bytes, 0, (B1 - B0) * p->block_bytes, st));
+    }
+    p->cfg.n_blocks = B1;
+    p->n_words = nw1;
+    blocks_grow_kernel<<<1184, 256, 0, st>>>(*p, B0);
+    SFKV_LAUNCH_CHECK("blocks_grow_kernel");
+    int log2 = p->cfg.table_log2;
+    while ((int64_t(1) << log2) < 2 * B1) ++log2;
+    if (log2 != p->cfg.table_log2) {  // keep the load factor <= 1/2: a larger table, re-indexed
+      Slot* slots1 = nullptr;
+      int64_t* towner1 = nullptr;
+      if ((rc = dalloc(&slots1, size_t(1) << log2)) || (rc = dalloc(&towner1, size_t(1) << log2))) {
+        cudaFree(slots1);
+        return rc;
+      }
+      SFKV_CUDA(cudaStreamSynchronize(st));
+      cudaFree(p->slots);
+      cudaFree(p->towner);
+      p->slots = slots1;
+      p->towner = towner1;
+      p->table_slots = int64_t(1) << log2;
+      p->cfg.table_log2 = log2;
+      if ((rc = rebuild_table_now(p))) return rc;
+    }
+  }
+  SFKV_CUDA(cudaStreamSynchronize(st));
+  SFKV_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int sfkv_pool_config_get(sfkv_pool* p, sfkv_pool_config* out) {
+  if (!p || !out) return fail(SFKV_EINVAL, "null argument");
+  *out = p->cfg;
   return 0;
 }
 
@@ -642,6 +781,7 @@ int sfkv_pool_export(sfkv_pool* p, sfkv_ipc_handle* out) {
   static_assert(sizeof(cudaIpcMemHandle_t) <= sizeof(out->handle), "ipc handle size");
   cudaIpcMemHandle_t h;
   SFKV_CUDA(cudaIpcGetMemHandle(&h, p->kv));
+  p->exported = true;
   memset(out, 0, sizeof(*out));
   memcpy(out->handle, &h, sizeof(h));
   out->kv_bytes = p->cfg.n_blocks * p->block_bytes;

@@ -543,6 +543,21 @@ int maybe_rebuild_table(sfkv_pool* p) {
   return 0;
 }
 
+__global__ void one_flag_kernel(int* flag) { *flag = 1; }
+
+int rebuild_table_now(sfkv_pool* p) {
+  cudaStream_t st = p->stream;
+  CommitArgs a = base_args(p);
+  int* flag = &p->ctr->pad;
+  one_flag_kernel<<<1, 1, 0, st>>>(flag);
+  const int sms = sm_count_c();
+  table_clear_kernel<<<sms * 4, 256, 0, st>>>(p->slots, p->towner, p->table_slots, flag);
+  table_reinsert_kernel<<<sms * 4, 256, 0, st>>>(a, flag);
+  rebuild_done_kernel<<<1, 1, 0, st>>>(p->ctr, flag);
+  SFKV_LAUNCH_CHECK("table rebuild (resize)");
+  return 0;
+}
+
 static int launch_commit_payload(sfkv_pool* p, const CommitArgs& a, const void* kv_src,
                                  const int64_t* kv_src_off, const PayloadSource* src,
                                  cudaStream_t st) {

@@ -4,9 +4,9 @@
 // tau_pressure (strict), flush the idle (in_flight == 0) preserved entry with the least
 // last_update_ts, ties to the lexicographically smallest workflow id (the reference scans entries
 // in workflow-id order and replaces only on strict <, memory.cpp:160-161). The tracker is a
-// struct-of-arrays in HBM; the lexicographic (ts, wf_rank) minimum per backend is reduced with three
-// order-independent atomic passes (min ts, min rank among ts ties, index), so the victim is
-// deterministic. 16 B per entry per pass.
+// struct-of-arrays in HBM; the lexicographic (ts, wf_rank, index) minimum per backend is one
+// launch: a segmented warp-shuffle argmin per CTA and a last-CTA reduction (argmin.cuh), order-
+// independent, so the victim is deterministic. 21 B per entry.
 //
 // K7 replaces map_threshold (mapper.cpp:19-31: light iff score <= threshold) and generalises it
 // to an R x C cost argmin with reroute_on_overload (orchestrator.cpp:78-87) applied in request
@@ -14,17 +14,12 @@
 #include <mutex>
 #include <vector>
 
+#include "argmin.cuh"
 #include "pool.cuh"
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
 namespace sfkv {
-
-__device__ __forceinline__ unsigned long long ts_order_key(double t) {
-  if (t == 0.0) t = 0.0;  // -0.0 == 0.0 in the reference's comparison
-  unsigned long long b = (unsigned long long)__double_as_longlong(t);
-  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-}
 
 struct PressArgs {
   int64_t n;
@@ -36,63 +31,56 @@ struct PressArgs {
   int32_t nb;
   const double* util;
   double tau;
-  unsigned long long* best_ts;
-  unsigned int* best_rank;
+  Cand* part;          // [gridDim.x][nb] CTA candidates
+  unsigned int* done;  // CTAs finished (the last one reduces; it leaves the counter at 0)
   long long* victim;
 };
 
-__device__ __forceinline__ bool eligible(const PressArgs& a, int64_t i, int32_t& b) {
-  b = a.backend[i];
-  return b >= 0 && b < a.nb && a.preserved[i] && a.in_flight[i] <= 0 && a.util[b] > a.tau;
-}
-
-__global__ void press_init(PressArgs a) {
-  int b = threadIdx.x + blockIdx.x * blockDim.x;
-  if (b < a.nb) {
-    a.best_ts[b] = ~0ull;
-    a.best_rank[b] = ~0u;
-    a.victim[b] = -1;
+// One launch: per backend above tau', every CTA reduces its grid-stride share of the entries to
+// one (ts, rank, index) candidate with warp shuffles; the last CTA to finish reduces the CTA
+// candidates into the victims. The entries of a CTA stay in L1 across the per-backend passes.
+__global__ void __launch_bounds__(256) press_kernel(PressArgs a) {
+  __shared__ Cand red[32];
+  __shared__ bool last;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int32_t b = 0; b < a.nb; ++b) {
+    Cand c = cand_none();
+    if (a.util[b] > a.tau) {
+      for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+        if (a.backend[i] == b && a.preserved[i] && a.in_flight[i] <= 0) {
+          const Cand d{ts_order_key(a.ts[i]), a.rank[i], i};
+          if (cand_less(d, c)) c = d;
+        }
+      }
+    }
+    c = block_argmin(c, red);
+    if (threadIdx.x == 0) a.part[(int64_t)blockIdx.x * a.nb + b] = c;
   }
-}
-__global__ void press_pass1(PressArgs a) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t b;
-    if (eligible(a, i, b)) atomicMin(&a.best_ts[b], ts_order_key(a.ts[i]));
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int32_t b = 0; b < a.nb; ++b) {
+    Cand c = cand_none();
+    for (int64_t p = threadIdx.x; p < gridDim.x; p += blockDim.x) {
+      const Cand d = cand_load(&a.part[p * a.nb + b]);
+      if (cand_less(d, c)) c = d;
+    }
+    c = block_argmin(c, red);
+    if (threadIdx.x == 0) a.victim[b] = c.idx;
   }
-}
-__global__ void press_pass2(PressArgs a) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t b;
-    if (eligible(a, i, b) && ts_order_key(a.ts[i]) == a.best_ts[b]) atomicMin(&a.best_rank[b], a.rank[i]);
-  }
-}
-__global__ void press_pass3(PressArgs a) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t b;
-    if (eligible(a, i, b) && ts_order_key(a.ts[i]) == a.best_ts[b] && a.rank[i] == a.best_rank[b])
-      atomicMin(reinterpret_cast<unsigned long long*>(&a.victim[b]), (unsigned long long)i);
-  }
-}
-__global__ void press_fix(PressArgs a) {  // victim starts at -1 (all ones) for atomicMin
-  int b = threadIdx.x + blockIdx.x * blockDim.x;
-  if (b < a.nb && a.best_ts[b] == ~0ull) a.victim[b] = -1;
+  if (threadIdx.x == 0) *a.done = 0;
 }
 
 int pressure_dev(cudaStream_t st, int64_t n, const int32_t* backend, const double* ts,
                  const uint32_t* rank, const int32_t* in_flight, const uint8_t* preserved,
-                 int32_t nb, const double* util, double tau, unsigned long long* best_ts,
-                 unsigned int* best_rank, long long* victim, int sms) {
-  PressArgs a{n, backend, ts, rank, in_flight, preserved, nb, util, tau, best_ts, best_rank, victim};
-  const int bg = (nb + 255) / 256;
-  press_init<<<bg, 256, 0, st>>>(a);
-  if (n > 0) {
-    const int g = grid_for(n, 256, sms * 8);
-    press_pass1<<<g, 256, 0, st>>>(a);
-    press_pass2<<<g, 256, 0, st>>>(a);
-    press_pass3<<<g, 256, 0, st>>>(a);
-  }
-  press_fix<<<bg, 256, 0, st>>>(a);
-  SFKV_LAUNCH_CHECK("pressure kernels");
+                 int32_t nb, const double* util, double tau, Cand* part, int grid,
+                 unsigned int* done, long long* victim) {
+  PressArgs a{n, backend, ts, rank, in_flight, preserved, nb, util, tau, part, done, victim};
+  press_kernel<<<grid, 256, 0, st>>>(a);
+  SFKV_LAUNCH_CHECK("press_kernel");
   return 0;
 }
 
@@ -384,6 +372,7 @@ struct DevCtx {
   std::mutex mu;
   cudaStream_t stream = nullptr;
   Scratch buf;
+  unsigned int* done = nullptr;  // K6 last-CTA counter (zero between launches)
   int sms = 148;
 };
 static DevCtx* ctx_for(int dev) {
@@ -395,6 +384,7 @@ static DevCtx* ctx_for(int dev) {
     auto* c = new DevCtx;
     cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaMalloc(&c->done, sizeof(unsigned int)) == cudaSuccess) cudaMemset(c->done, 0, sizeof(unsigned int));
     ctxs[dev] = c;
   }
   return ctxs[dev];
@@ -415,11 +405,12 @@ extern "C" int sfmm_pressure_argmin(int32_t device, int64_t n, const int32_t* ba
   DeviceGuard g(device);
   DevCtx* c = ctx_for(device);
   std::lock_guard<std::mutex> lk(c->mu);
+  if (!c->done) return fail(SFKV_ENOMEM, "pressure_argmin: device context");
+  const int grid = grid_for(n, 256, c->sms * 2);
   Carver cv;
   const size_t o_b = cv.take<int32_t>(n), o_ts = cv.take<double>(n), o_rk = cv.take<uint32_t>(n),
                o_if = cv.take<int32_t>(n), o_pr = cv.take<uint8_t>(n), o_u = cv.take<double>(n_backends),
-               o_bt = cv.take<unsigned long long>(n_backends), o_br = cv.take<unsigned int>(n_backends),
-               o_v = cv.take<long long>(n_backends);
+               o_p = cv.take<Cand>((size_t)grid * n_backends), o_v = cv.take<long long>(n_backends);
   if (int rc = c->buf.ensure(cv.off)) return rc;
   char* b = c->buf.as<char>();
   cudaStream_t st = c->stream;
@@ -434,14 +425,33 @@ extern "C" int sfmm_pressure_argmin(int32_t device, int64_t n, const int32_t* ba
   if (int rc = pressure_dev(st, n, reinterpret_cast<int32_t*>(b + o_b), reinterpret_cast<double*>(b + o_ts),
                            reinterpret_cast<uint32_t*>(b + o_rk), reinterpret_cast<int32_t*>(b + o_if),
                            reinterpret_cast<uint8_t*>(b + o_pr), n_backends,
-                           reinterpret_cast<double*>(b + o_u), tau,
-                           reinterpret_cast<unsigned long long*>(b + o_bt),
-                           reinterpret_cast<unsigned int*>(b + o_br), reinterpret_cast<long long*>(b + o_v),
-                           c->sms))
+                           reinterpret_cast<double*>(b + o_u), tau, reinterpret_cast<Cand*>(b + o_p), grid,
+                           c->done, reinterpret_cast<long long*>(b + o_v)))
     return rc;
   SFKV_CUDA(cudaMemcpyAsync(out_victim, b + o_v, n_backends * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   SFKV_CUDA(cudaStreamSynchronize(st));
   return 0;
+}
+
+/* Device pointers, asynchronous on cuda_stream (NULL = legacy default stream). */
+extern "C" int sfmm_pressure_argmin_dev(int32_t device, int64_t n, const int32_t* backend, const double* ts,
+                                        const uint32_t* wf_rank, const int32_t* in_flight,
+                                        const uint8_t* preserved, int32_t n_backends, const double* util,
+                                        double tau, int64_t* out_victim, void* cuda_stream) {
+  if (n < 0 || n_backends < 0 || (n > 0 && (!backend || !ts || !wf_rank || !in_flight || !preserved)) ||
+      (n_backends > 0 && (!util || !out_victim)))
+    return fail(SFKV_EINVAL, "pressure_argmin_dev: bad argument");
+  if (n_backends == 0) return 0;
+  if (int rc = check_device(device)) return rc;
+  DeviceGuard g(device);
+  DevCtx* c = ctx_for(device);
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (!c->done) return fail(SFKV_ENOMEM, "pressure_argmin_dev: device context");
+  const int grid = grid_for(n, 256, c->sms * 2);
+  if (int rc = c->buf.ensure((size_t)grid * n_backends * sizeof(Cand))) return rc;
+  return pressure_dev(static_cast<cudaStream_t>(cuda_stream), n, backend, ts, wf_rank, in_flight, preserved,
+                      n_backends, util, tau, c->buf.as<Cand>(), grid, c->done,
+                      reinterpret_cast<long long*>(out_victim));
 }
 
 extern "C" int sfmap_threshold_batch(int32_t device, int64_t n, const double* score, double threshold,

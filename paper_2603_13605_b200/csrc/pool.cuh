@@ -90,6 +90,7 @@ struct sfkv_pool {
   uint32_t prep_epoch = 0;
   void* host_stage = nullptr;  // pinned host staging
   size_t host_stage_bytes = 0;
+  bool exported = false;       // the KV region was handed out as a CUDA IPC handle (fixed)
 };
 
 namespace sfkv {
@@ -155,5 +156,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
 int flush_dev(sfkv_pool* p, int64_t n, const int32_t* wf, int64_t* out_freed, bool all);
 int gather_dev(sfkv_pool* p, int64_t n, const int32_t* wf, void* dst, const int64_t* dst_off);
 int maybe_rebuild_table(sfkv_pool* p);
+// Re-inserts every indexed block into the (already resized) empty table; resets tombstones.
+int rebuild_table_now(sfkv_pool* p);
 
 }  // namespace sfkv

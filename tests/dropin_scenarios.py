@@ -64,4 +64,8 @@ SCENARIOS = {
     "chain_flush": lambda: math_chain("flush"),
     "alt_pressure": lambda: synthetic("alt_pressure"),
     "chain_scale": lambda: synthetic("chain_scale"),
+    "alt_pressure_flaky": lambda: synthetic("alt_pressure"),
+    "chain_scale_flaky": lambda: synthetic("chain_scale"),
 }
+# Driver flags of the failure-path scenarios (make_golden.FLAKY: backends whose flush throws).
+FLAGS = {"alt_pressure_flaky": ["--flaky", "A:1,B:2"], "chain_scale_flaky": ["--flaky", "heavy:2"]}

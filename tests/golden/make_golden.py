@@ -19,6 +19,7 @@ Scenarios:
                     chain [preserve_small_increment]; pressure flushes, orphans, rejections
   chain_scale       synthetic, SURVEY §9 C2 probe at reduced scale: 300 math_chain_k workflows,
                     log-uniform bases, tight capacity (rejections) and pressure ticks
+  *_flaky           alt_pressure / chain_scale with backends whose flush throws (FLAKY below)
 Synthetic inputs are written to tests/golden/inputs/ and committed with the streams.
 
 Full-scale compact goldens (`python tests/golden/make_golden.py c2_probe c4_probe`, written to
@@ -193,10 +194,18 @@ def run_full(name):
     print(f"{name}: {n} records (compact)")
 
 
-def run(name, config_path, trace_path):
+# Failure-path scenarios: the same inputs with test backends whose flush throws (the drivers'
+# --flaky REF:MODE; mode 1 = the first attempt of every flush fails and the retry succeeds, mode
+# 2 = every attempt fails, so apply_action gives up and the entry is only unpreserved,
+# memory.cpp:189-203, 319-325).
+FLAKY = {"alt_pressure_flaky": ("alt_pressure", "A:1,B:2"),
+         "chain_scale_flaky": ("chain_scale", "heavy:2")}
+
+
+def run(name, config_path, trace_path, flaky=None):
     out = os.path.join("/tmp", f"golden_{name}.jsonl")
-    subprocess.run([DRIVER, "--config", config_path, "--trace", trace_path, "--out", out],
-                   check=True)
+    subprocess.run([DRIVER, "--config", config_path, "--trace", trace_path, "--out", out] +
+                   (["--flaky", flaky] if flaky else []), check=True)
     with open(out, "rb") as f, gzip.open(os.path.join(HERE, f"{name}.jsonl.gz"), "wb", 9) as g:
         g.write(f.read())
     n = sum(1 for _ in open(out))
@@ -222,6 +231,9 @@ def main():
             for rec in trace:
                 f.write(json.dumps(rec) + "\n")
         run(name, cp, tp)
+    for name, (base, flaky) in FLAKY.items():
+        run(name, os.path.join(INPUTS, f"{base}.config.json"), os.path.join(INPUTS, f"{base}.trace.jsonl"),
+            flaky)
 
 
 if __name__ == "__main__":

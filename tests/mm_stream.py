@@ -112,15 +112,35 @@ def tick_log(intern, victims, ts):
     return log
 
 
-def run_stream(tracker, intern, events, batch_between_ticks=True):
-    """events: ("sig", dict) / ("tick", {"util": {ref: u}, "ts": t}). Returns (log, statuses)."""
+def failed_flushes(out, flaky, backends):
+    """(wf slot, backend, signal index) of every flush record a backend refused twice: apply_action
+    retries once (memory.cpp:189-203), so only mode 2 (every attempt fails) gives up; mode 1 (the
+    first attempt of each flush fails) succeeds on the retry."""
+    cnt, st, k, b, r = out
+    res = []
+    for i in range(len(cnt)):
+        for j in range(int(cnt[i])):
+            if int(k[i, j]) == 1 and flaky.get(backends[int(b[i, j])], 0) == 2:
+                res.append((i, int(b[i, j])))
+    return res
+
+
+def run_stream(tracker, intern, events, batch_between_ticks=True, flaky=None):
+    """events: ("sig", dict) / ("tick", {"util": {ref: u}, "ts": t}). Returns (log, statuses).
+    flaky: {backend ref: mode} of backends whose flush throws (see failed_flushes); the host
+    reports the flushes that failed twice back to the tracker (sfmm_flush_failed)."""
     log, statuses, batch = [], [], []
+    flaky = flaky or {}
 
     def flush_batch():
         if not batch:
             return
         tracker.set_ranks(intern.ranks(tracker.W))
-        out = tracker.on_signals(*encode(intern, batch))
+        enc = encode(intern, batch)
+        out = tracker.on_signals(*enc)
+        bad = failed_flushes(out, flaky, intern.backends)
+        if bad:
+            tracker.flush_failed([enc[1][i] for i, _ in bad], [bb for _, bb in bad], [i for i, _ in bad])
         l, st = records_to_log(intern, batch, out)
         log.extend(l)
         statuses.extend(st)
@@ -140,7 +160,12 @@ def run_stream(tracker, intern, events, batch_between_ticks=True):
             flush_batch()
             tracker.set_ranks(intern.ranks(tracker.W))
             util = np.array([ev["util"].get(b, 0.0) for b in intern.backends], np.float64)
-            log.extend(tick_log(intern, tracker.pressure_tick(util), ev["ts"]))
+            victims = tracker.pressure_tick(util)
+            bad = [(int(w), bi) for bi, w in enumerate(victims)
+                   if w >= 0 and flaky.get(intern.backends[bi], 0) == 2]
+            if bad:
+                tracker.flush_failed([w for w, _ in bad], [bi for _, bi in bad], [-1] * len(bad))
+            log.extend(tick_log(intern, victims, ev["ts"]))
     flush_batch()
     return log, statuses
 
@@ -158,7 +183,7 @@ def golden_events(lines):
 
 # ---------------------------------------------------------------- random streams -----------
 def random_stream(seed, n_wf=40, backends=("A", "B", "C"), models=("m1", "m2"), n_stages=(1, 6),
-                  p_override=0.1, p_chain=0.2, p_bad=0.03, p_tick=0.05, tau=512):
+                  p_override=0.1, p_chain=0.2, p_bad=0.03, p_tick=0.05, tau=512, chain_len=(1, 4)):
     """Seeded lifecycle-signal stream with concurrency and deliberate order violations."""
     rng = np.random.default_rng(seed)
     plans = {}
@@ -175,7 +200,7 @@ def random_stream(seed, n_wf=40, backends=("A", "B", "C"), models=("m1", "m2"), 
         chain = None
         if rng.random() < p_chain:
             chain = [str(x) for x in rng.choice(["preserve_small_increment", "flush_at_boundary"],
-                                                size=int(rng.integers(1, 4)))]
+                                                size=int(rng.integers(*chain_len)))]
         plans[wid] = {"stages": stages, "next": 0, "open": [], "done": False, "chain": chain,
                       "first": True}
     events, ts = [], 0.0
@@ -222,12 +247,18 @@ def random_stream(seed, n_wf=40, backends=("A", "B", "C"), models=("m1", "m2"), 
 class RefManager:
     """The reference's MemoryManager through oracle/_ref/libsfref.so."""
 
-    def __init__(self, tau, tau_pressure, chain):
+    def __init__(self, tau, tau_pressure, chain, flaky=None, backends=()):
+        """flaky: {ref: mode} -> a BackendRegistry of test backends over `backends` whose flush
+        throws (sfref_mm_create_flaky); None -> no registry (every action applies)."""
         path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
                             "libsfref.so")
         L = C.CDLL(path)
         L.sfref_mm_create.restype = C.c_void_p
         L.sfref_mm_create.argtypes = [C.c_longlong, C.c_double, C.c_int, C.POINTER(C.c_char_p)]
+        L.sfref_mm_create_flaky.restype = C.c_void_p
+        L.sfref_mm_create_flaky.argtypes = [C.c_longlong, C.c_double, C.c_int, C.POINTER(C.c_char_p), C.c_int,
+                                            C.POINTER(C.c_char_p), C.POINTER(C.c_int)]
+        L.sfref_mm_entry.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p]
         L.sfref_mm_destroy.argtypes = [C.c_void_p]
         L.sfref_mm_set_chain.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.POINTER(C.c_char_p)]
         L.sfref_mm_on_signal.argtypes = [C.c_void_p, C.c_int, C.c_char_p, C.c_char_p, C.c_char_p,
@@ -241,7 +272,17 @@ class RefManager:
                                        C.POINTER(C.c_double)]
         self.L = L
         arr = (C.c_char_p * len(chain))(*[c.encode() for c in chain])
-        self.h = L.sfref_mm_create(tau, tau_pressure, len(chain), arr)
+        if flaky is None:
+            self.h = L.sfref_mm_create(tau, tau_pressure, len(chain), arr)
+        else:
+            refs = sorted(backends)
+            ra = (C.c_char_p * len(refs))(*[r.encode() for r in refs])
+            ma = (C.c_int * len(refs))(*[int(flaky.get(r, 0)) for r in refs])
+            self.h = L.sfref_mm_create_flaky(tau, tau_pressure, len(chain), arr, len(refs), ra, ma)
+
+    def entry(self, wf, backend):
+        """0 absent, 1 present + preserved, 2 present unpreserved (WorkflowTracker::entry)."""
+        return self.L.sfref_mm_entry(self.h, wf.encode(), backend.encode())
 
     def close(self):
         if self.h:

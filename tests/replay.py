@@ -43,7 +43,7 @@ def pool_config_for(lines, ref, n_slabs=0, slab_row_bytes=0, device=0):
     meta = lines[0]
     be = next(b for b in meta["backends"] if b["ref"] == ref)
     wfs = {l["wf"] for l in lines if l.get("b") == ref and "wf" in l}
-    max_p = max([l["P"] for l in lines if l.get("op") == "match" and l["b"] == ref] + [1])
+    max_p = max([l["P"] for l in lines if l.get("op") == "match" and l.get("b") == ref] + [1])
     mpb = (max_p + BLOCK_TOKENS - 1) // BLOCK_TOKENS + 1
     cap = int(be["capacity_tokens"])
     n_blocks = cap // BLOCK_TOKENS + len(wfs) + 2 * mpb + 64
@@ -55,8 +55,10 @@ def pool_config_for(lines, ref, n_slabs=0, slab_row_bytes=0, device=0):
                   slab_row_bytes=slab_row_bytes, device=device)
 
 
-def replay(lines, api, pressure=None, batched=False, device=0):
-    """pressure: callable(entries..) -> victims, defaults to api.pressure_argmin."""
+def replay(lines, api, pressure=None, batched=False, device=0, tokens=None):
+    """pressure: callable(entries..) -> victims, defaults to api.pressure_argmin.
+    tokens: the u32 token file of a stream recorded with --tok-out (match records carry "toff"
+    instead of inline "tok")."""
     meta = lines[0]
     assert meta["type"] == "meta"
     refs = [b["ref"] for b in meta["backends"]]
@@ -99,6 +101,8 @@ def replay(lines, api, pressure=None, batched=False, device=0):
             ref, op = l["b"], l["op"]
             pool = pools[ref]
             if op == "match":
+                if "tok" not in l:
+                    l["tok"] = tokens[l["toff"]:l["toff"] + l["P"]]
                 toks[ref][l["rid"]] = l["tok"]
             if batched and op in ("match", "pin"):
                 q = pending[ref]

@@ -18,7 +18,7 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def declared_symbols():
     src = open(os.path.join(REPO, "include", "sfkv.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b((?:sfkv|sfmm|sfmap)_[a-z0-9_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b((?:sfkv|sfmm|sfmap|sfmet)_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 25
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
-    assert lib.sfkv_abi_version() == 1
+    assert lib.sfkv_abi_version() == 2
 
 
 def test_pool_create_without_gpu_fails_loudly():

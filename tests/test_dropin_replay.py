@@ -13,7 +13,7 @@ import subprocess
 import pytest
 
 import replay
-from dropin_scenarios import SCENARIOS
+from dropin_scenarios import FLAGS, SCENARIOS
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 DRIVER = os.path.join(REPO, "oracle", "_ref", "sf_gpu_replay")
@@ -33,7 +33,7 @@ def test_reference_harness_on_gpu_pool_matches_golden(tmp_path, name, gpu_memory
     cp.write_text(json.dumps(cfg))
     tp.write_text("".join(json.dumps(r) + "\n" for r in trace))
     subprocess.run([DRIVER, "--config", str(cp), "--trace", str(tp), "--out", str(op)] +
-                   (["--gpu-memory"] if gpu_memory else []), check=True, timeout=600)
+                   (["--gpu-memory"] if gpu_memory else []) + FLAGS.get(name, []), check=True, timeout=600)
     got = [json.loads(l) for l in op.read_text().splitlines()]
     gold = replay.load_stream(name)
 

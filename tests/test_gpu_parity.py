@@ -324,3 +324,40 @@ def test_full_c2_size_match(gpu_api, oracle_api):
                                 table_log2=12))
     _, ho = o.match(wf, wl["req_off"], wl["req_tok"], want_hash=True)
     np.testing.assert_array_equal(hg, ho)
+
+
+def test_pool_reserve_grows_in_place(gpu_api, oracle_api):
+    """sfkv_pool_reserve: a pool created small grows its workflow slots, block-table length and
+    physical blocks (the dedup table re-indexed) mid-stream; every later state equals an oracle
+    pool created at the final size (allocation is lowest-free-id, so growth is invisible)."""
+    n_wf = 40
+    small = Config(max_workflows=8, n_blocks=300, capacity_tokens=60_000, max_pin_blocks=4, table_log2=9)
+    big = Config(max_workflows=n_wf, n_blocks=3000, capacity_tokens=60_000, max_pin_blocks=64, table_log2=13)
+    g, o = Pool(gpu_api, small), Pool(oracle_api, big)
+    wl = Workload(4, n_wf, n_sys=3, sys_len=(16, 60), ctx_len=(0, 40), append=(0, 40))
+    rng = np.random.default_rng(4)
+    for step in range(10):
+        if step == 2:
+            gpu_api.check("pool_reserve", gpu_api.pool_reserve(g.h, 16, 16, 900))
+        if step == 5:
+            gpu_api.check("pool_reserve", gpu_api.pool_reserve(g.h, n_wf, 64, 3000))
+            g.cfg = big
+        lim = 8 if step < 2 else (16 if step < 5 else n_wf)
+        wfs = rng.choice(lim, size=int(rng.integers(1, lim)), replace=False).astype(np.int32)
+        seqs, off, tok = wl.batch(wfs)
+        if step < 5:  # the small block tables bound the prompt length until the second reserve
+            cap = (4 if step < 2 else 16) * 16
+            seqs = [s[:cap] for s in seqs]
+            off, tok = csr(seqs)
+        np.testing.assert_array_equal(g.match(wfs, off, tok), o.match(wfs, off, tok))
+        np.testing.assert_array_equal(g.commit(wfs, off, tok), o.commit(wfs, off, tok))
+        bg, hg = g.lookup(off, tok)
+        bo, ho = o.lookup(off, tok)
+        np.testing.assert_array_equal(bg, bo)
+        np.testing.assert_array_equal(hg, ho)
+    sg, so = g.stats(), o.stats()
+    for k in ("occupancy_tokens", "blocks_in_use", "table_live"):
+        assert sg[k] == so[k], k
+    np.testing.assert_array_equal(g.refcounts(), o.refcounts())
+    for w in range(n_wf):
+        np.testing.assert_array_equal(g.pin_blocks(w)[0], o.pin_blocks(w)[0])
