@@ -1,6 +1,8 @@
 // sf_gpu_replay — the reference's own orchestrator, memory manager and harness loop driving the
 // B200 pool through GpuPinnedBackend (the drop-in). With --gpu-memory the reference's
-// MemoryManager is replaced by GpuMemoryManager (policy resolution and the tracker on the B200). Same wiring as run_benchmark
+// MemoryManager is replaced by GpuMemoryManager (policy resolution and the tracker on the B200);
+// with --gpu-router the stage routers are the GPU ones (gpu_router.hpp: threshold / one-bit /
+// plan decisions and reroute_on_overload through sfmap_*). Same wiring as run_benchmark
 // (proj/src/harness.cpp:8-116) with GpuPinnedBackend in place of SimulatedBackend. Emits:
 //   {"type":"req", b, wf, stage, P, M}   per dispatch, in dispatch order (M from the GPU)
 //   {"type":"act", ...}                   the memory manager's action log (memory.cpp:389-401)
@@ -11,6 +13,7 @@
 
 #include "gpu_memory_manager.hpp"
 #include "gpu_pinned_backend.hpp"
+#include "gpu_router.hpp"
 #include "stageflow/config.hpp"
 #include "stageflow/harness.hpp"
 
@@ -61,10 +64,11 @@ std::map<std::string, int> parse_flaky(const std::string& spec) {
 int main(int argc, char** argv) {
   std::string config_path, trace_path, out_path, flaky_spec;
   int device = 0;
-  bool gpu_memory = false;
+  bool gpu_memory = false, gpu_router = false;
   for (int i = 1; i < argc; ++i) {
     std::string a = argv[i];
     if (a == "--gpu-memory") { gpu_memory = true; continue; }
+    if (a == "--gpu-router") { gpu_router = true; continue; }
     if (i + 1 >= argc) break;
     if (a == "--config") config_path = argv[++i];
     else if (a == "--trace") trace_path = argv[++i];
@@ -141,7 +145,8 @@ int main(int argc, char** argv) {
     const auto& wf = *validated.workflow;
     if (!wf.spec().workflow_memory_policy.empty())
       set_chain(workflow_id, wf.spec().workflow_memory_policy);
-    orch.submit_at(static_cast<double>(r.arrival_ms), wf, make_router(config, registry, wf),
+    auto router = gpu_router ? make_gpu_router(config, registry, wf, orch, device) : make_router(config, registry, wf);
+    orch.submit_at(static_cast<double>(r.arrival_ms), wf, std::move(router),
                    [&remaining](ExecutionReport) { --remaining; }, r.annotations());
   }
   auto tick = std::make_shared<std::function<void()>>();

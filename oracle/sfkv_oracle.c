@@ -148,6 +148,7 @@ struct sfo_pool {
   uint64_t* pin_hash;
   /* blocks (Class B) */
   uint64_t* blk_key;
+  int32_t* blk_parent; /* the block at index k-1 of the pin that allocated it (-1 at k = 0) */
   uint32_t* blk_tok; /* [block][16] */
   uint8_t* blk_n;
   uint8_t* blk_in_table;
@@ -175,6 +176,8 @@ int sfo_pool_create(const sfo_pool_config* cfg, sfo_pool** out) {
   p->pin_blk = (int32_t*)calloc((size_t)(W * MB), sizeof(int32_t));
   p->pin_hash = (uint64_t*)calloc((size_t)(W * MB), sizeof(uint64_t));
   p->blk_key = (uint64_t*)calloc((size_t)B, sizeof(uint64_t));
+  p->blk_parent = (int32_t*)malloc((size_t)B * sizeof(int32_t));
+  for (int64_t i = 0; i < B; ++i) p->blk_parent[i] = -1;
   p->blk_tok = (uint32_t*)calloc((size_t)(B * BT), sizeof(uint32_t));
   p->blk_n = (uint8_t*)calloc((size_t)B, 1);
   p->blk_in_table = (uint8_t*)calloc((size_t)B, 1);
@@ -192,7 +195,7 @@ int sfo_pool_destroy(sfo_pool* p) {
   if (!p) return 0;
   for (int64_t i = 0; i < p->cfg.max_workflows; ++i) free(p->pin_tok[i]);
   free(p->pin_len); free(p->pin_tok); free(p->pin_nblk); free(p->pin_blk); free(p->pin_hash);
-  free(p->blk_key); free(p->blk_tok); free(p->blk_n); free(p->blk_in_table); free(p->blk_ref);
+  free(p->blk_key); free(p->blk_parent); free(p->blk_tok); free(p->blk_n); free(p->blk_in_table); free(p->blk_ref);
   free(p->blk_free); kmap_free(&p->table); free(p->kv); free(p);
   return 0;
 }
@@ -233,7 +236,9 @@ static int blk_tokens_eq(const sfo_pool* p, int32_t id, const uint32_t* t) {
   return p->blk_n[id] == BT && memcmp(p->blk_tok + (int64_t)id * BT, t, BT * sizeof(uint32_t)) == 0;
 }
 
-/* Global lookup: each FULL block's chained hash against the table, token-verified. */
+/* Global lookup: each FULL block's chained hash against the table, token-verified, and linked to
+ * its predecessor: block k hits only if the resident block's parent is the block the table holds
+ * for chained key k-1 (so a leading run of hits is an exact prefix, independent of the hash). */
 int sfo_lookup_batch(sfo_pool* p, int64_t n, const int64_t* tok_off, const uint32_t* tok,
                      int32_t* out_block, int64_t* out_hit_tokens) {
   int64_t ob = 0;
@@ -244,11 +249,16 @@ int sfo_lookup_batch(sfo_pool* p, int64_t n, const int64_t* tok_off, const uint3
     uint64_t* h = (uint64_t*)malloc((size_t)(nb > 0 ? nb : 1) * sizeof(uint64_t));
     sfo_chain_hashes(t, len, h);
     int64_t lead = 0, run = 1;
+    int32_t raw_prev = -1;
     for (int64_t k = 0; k < nb; ++k) {
       int32_t id = -1;
       if (k < nfull) {
-        id = kmap_get(&p->table, h[k]);
-        if (id >= 0 && !blk_tokens_eq(p, id, t + k * BT)) id = -1;
+        /* exact by induction: the resident block must hold these tokens AND descend from the
+         * block the table holds for the previous chained key (its parent link) */
+        const int32_t raw = kmap_get(&p->table, h[k]);
+        id = raw;
+        if (id >= 0 && (!blk_tokens_eq(p, id, t + k * BT) || (k > 0 && p->blk_parent[id] != raw_prev))) id = -1;
+        raw_prev = raw;
       }
       out_block[ob++] = id;
       if (id < 0) run = 0;
@@ -411,26 +421,54 @@ static int commit_impl(sfo_pool* p, int64_t n, const int32_t* wf, const int64_t*
   for (int64_t r = 0; r < n; ++r)
     for (int64_t it = item_off[r]; it < item_off[r + 1]; ++it) item_req[it] = r;
   int64_t scan_free = 0;
+  /* Exact sharing by parent links (a block is shared only when its whole prefix is): per request,
+   *   f_hit = first k that is not a linked hit: hit0[k] && (k == 0 || (hit0[k-1] &&
+   *           parent(bid[k]) == bid[k-1]))
+   *   f     = first k >= f_hit that is not a linked dup: a claim whose owner o is earlier, with
+   *           equal tokens, and k == 0, or the previous item is a dup of the owner's previous
+   *           item (owner[it-1] == o-1), or (k == f_hit) the previous item and the owner's
+   *           previous item are the same linked hit (o-1 < f_hit of the owner's request, same bid).
+   * Every test reads only probe results and f_hit, so the GPU resolves it in two parallel passes. */
+  int64_t* f_hit = (int64_t*)malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
+  for (int64_t r = 0; r < n; ++r) {
+    int64_t nb = item_off[r + 1] - item_off[r];
+    f_hit[r] = nb;
+    if (!out_status[r]) continue;
+    for (int64_t k = 0; k < nb; ++k) {
+      int64_t it = item_off[r] + k;
+      int ok = hit0[it] && (k == 0 || (hit0[it - 1] && p->blk_parent[bid[it]] == bid[it - 1]));
+      if (!ok) {
+        f_hit[r] = k;
+        break;
+      }
+    }
+  }
   for (int64_t r = 0; r < n; ++r) {
     if (!out_status[r]) continue;
     int64_t nb = item_off[r + 1] - item_off[r];
     int64_t f = nb;
-    for (int64_t k = 0; k < nb; ++k) {
+    for (int64_t k = f_hit[r]; k < nb; ++k) {
       int64_t it = item_off[r] + k;
       int dup = 0;
       if (claim[it] && owner[it] < it) {
         int64_t o = owner[it], orq = item_req[o], ok = o - item_off[orq];
         dup = memcmp(tok + tok_off[orq] + ok * BT, tok + tok_off[r] + k * BT,
                      BT * sizeof(uint32_t)) == 0;
+        if (dup && k > 0) {
+          const int dup_link = k > f_hit[r] && claim[it - 1] && owner[it - 1] == o - 1;
+          const int hit_link = k == f_hit[r] && ok - 1 < f_hit[orq] && bid[it - 1] == bid[o - 1];
+          dup = dup_link || hit_link;
+        }
       }
-      if (!(hit0[it] || dup)) {
+      if (!dup) {
         f = k;
         break;
       }
     }
     for (int64_t k = 0; k < nb; ++k) {
       int64_t it = item_off[r] + k;
-      if (k < f) cat[it] = hit0[it] ? C_HIT : C_DUP;
+      if (k < f_hit[r]) cat[it] = C_HIT;
+      else if (k < f) cat[it] = C_DUP;
       else cat[it] = (claim[it] && owner[it] == it) ? C_OWN : C_PRIV;
     }
   }
@@ -443,6 +481,7 @@ static int commit_impl(sfo_pool* p, int64_t n, const int32_t* wf, const int64_t*
        * been touched yet; the admission counters roll back), as sfkv_commit_batch */
       p->occupancy = occ_saved;
       p->rejections = rej_saved;
+      free(f_hit);
       free(M); free(item_off); free(key); free(cat); free(bid); free(owner); free(hit0);
       free(claim); free(item_req);
       return -5;
@@ -476,6 +515,14 @@ static int commit_impl(sfo_pool* p, int64_t n, const int32_t* wf, const int64_t*
     }
   }
   for (int64_t it = 0; it < n_items; ++it) p->blk_ref[bid[it]]++;
+  /* parent links of the new blocks: the block chosen for the previous item of the request */
+  for (int64_t r = 0; r < n; ++r) {
+    if (!out_status[r]) continue;
+    for (int64_t k = 0; k < item_off[r + 1] - item_off[r]; ++k) {
+      int64_t it = item_off[r] + k;
+      if (cat[it] == C_OWN || cat[it] == C_PRIV) p->blk_parent[bid[it]] = k > 0 ? bid[it - 1] : -1;
+    }
+  }
   /* 3. payload */
   for (int64_t r = 0; r < n; ++r) {
     if (!out_status[r] || !p->kv) continue;
@@ -534,7 +581,7 @@ static int commit_impl(sfo_pool* p, int64_t n, const int32_t* wf, const int64_t*
     }
   }
   free(M); free(item_off); free(key); free(cat); free(bid); free(owner); free(hit0); free(claim);
-  free(item_req);
+  free(item_req); free(f_hit);
   return 0;
 }
 

@@ -65,6 +65,7 @@ __global__ void pool_init_kernel(sfkv_pool P) {
     P.blk_in_table[b] = 0;
     P.blk_n[b] = 0;
     P.blk_slot[b] = -1;
+    P.blk_parent[b] = -1;
   }
 }
 
@@ -85,6 +86,7 @@ static void pool_free(sfkv_pool* p) {
   cudaFree(p->pin_blk);
   cudaFree(p->pin_tok);
   cudaFree(p->blk_key);
+  cudaFree(p->blk_parent);
   cudaFree(p->blk_tok);
   cudaFree(p->blk_n);
   cudaFree(p->blk_in_table);
@@ -141,6 +143,7 @@ __global__ void blocks_grow_kernel(sfkv_pool P, int64_t B0) {
     P.blk_n[b] = 0;
     P.blk_slot[b] = -1;
     P.blk_key[b] = 0;
+    P.blk_parent[b] = -1;
     atomicOr(&P.free_bits[b >> 5], 1u << (b & 31));
   }
 }
@@ -219,7 +222,7 @@ int sfkv_pool_create(const sfkv_pool_config* cfg, sfkv_pool** out) {
   int rc = 0;
   if ((rc = dalloc(&p->pin_len, W)) || (rc = dalloc(&p->pin_nblk, W)) ||
       (rc = dalloc(&p->pin_blk, W * MB)) || (rc = dalloc(&p->pin_tok, W * (size_t)pin_groups(*cfg) * 32 * PIN_STRIDE)) ||
-      (rc = dalloc(&p->blk_key, B)) || (rc = dalloc(&p->blk_tok, B * BT)) ||
+      (rc = dalloc(&p->blk_key, B)) || (rc = dalloc(&p->blk_parent, B)) || (rc = dalloc(&p->blk_tok, B * BT)) ||
       (rc = dalloc(&p->blk_n, B)) || (rc = dalloc(&p->blk_in_table, B)) ||
       (rc = dalloc(&p->blk_ref, B)) || (rc = dalloc(&p->blk_slot, B)) ||
       (rc = dalloc(&p->free_bits, (size_t)p->n_words)) ||
@@ -292,7 +295,8 @@ int sfkv_pool_reserve(sfkv_pool* p, int32_t max_workflows, int32_t max_pin_block
       return fail(SFKV_EINVAL, "pool_reserve: the KV region was exported (CUDA IPC); it cannot move");
     const int64_t nw1 = (B1 + 31) / 32;
     int rc = 0;
-    if ((rc = dgrow(&p->blk_key, B0, B1, st)) || (rc = dgrow(&p->blk_tok, B0 * BT, B1 * BT, st)) ||
+    if ((rc = dgrow(&p->blk_key, B0, B1, st)) || (rc = dgrow(&p->blk_parent, B0, B1, st)) ||
+        (rc = dgrow(&p->blk_tok, B0 * BT, B1 * BT, st)) ||
         (rc = dgrow(&p->blk_n, B0, B1, st)) || (rc = dgrow(&p->blk_in_table, B0, B1, st)) ||
         (rc = dgrow(&p->blk_ref, B0, B1, st)) || (rc = dgrow(&p->blk_slot, B0, B1, st)) ||
         (rc = dgrow(&p->free_bits, p->n_words, nw1, st)))

@@ -9,9 +9,14 @@
 //              path when the whole 32-request chunk fits, exact sequential fallback otherwise
 //   probe      per full block: table probe; verified pre-existing key -> hit0; new key ->
 //              claim (atomicCAS into an empty slot) + atomicMin(owner) = lowest claiming item
-//   resolve    claim items with a lower owner compare tokens with the owner's (dup);
-//              atomicMin(first_nonhit[r]) over blocks that are neither hit0 nor dup
-//   categorize HIT / DUP below first_nonhit, OWN (key owner) / PRIV above
+//   resolve1   linked hits: hit0 and (k = 0 or the previous item is a hit0 of the block's parent);
+//              atomicMin(f_hit[r]) over the rest
+//   resolve2   linked dups at k >= f_hit: a claim with a lower owner o, equal tokens, and the
+//              previous item resolving to the same block as o's previous item (a dup of o-1, or
+//              at k = f_hit the same linked hit); atomicMin(first_nonhit[r]) over the rest.
+//              Sharing is exact by induction over parent links: a shared block's whole prefix is
+//              the request's, whatever the chained hash does (keys only locate candidates)
+//   categorize HIT below f_hit, DUP below first_nonhit, OWN (key owner) / PRIV above
 //   scan x2    exclusive scan of new-block flags (rank) and of free-bitmap popcounts
 //   alloc      rank -> the rank-th free block id (lowest ids first, batch order: deterministic,
 //              independent of atomic order); OWN publishes its id into the table slot
@@ -19,7 +24,7 @@
 //   payload    copy-on-share + staging scatter of new blocks                        (copy.cu)
 //   release    old pins drop their references; blocks reaching 0 return to the free bitmap and
 //              leave the table (tombstone)
-//   install    new block tables / hashes / lengths
+//   install    new block tables / hashes / lengths, parent links of the new blocks
 // The batch is phase-ordered, so a block shared by an old and a new pin never transiently hits
 // a refcount of zero. Scratch is sized by an item-count bound from the caller (token-buffer
 // size / 16 + requests); every kernel reads the exact count blk_off[n] on the device.
@@ -41,6 +46,7 @@ struct CommitScratch {
   uint8_t* claim;         // [items]
   uint8_t* cat;           // [items]
   int64_t* first_nonhit;  // [n]
+  int64_t* f_hit;         // [n] first item that is not a linked hit
   int64_t* rank;          // [items+1]
   int64_t* wprefix;       // [words+1]
   int64_t* alloc_list;    // [items]
@@ -63,6 +69,7 @@ struct CommitArgs {
   int32_t* pin_blk;
   uint32_t* pin_tok;
   uint64_t* blk_key;
+  int32_t* blk_parent;
   uint32_t* blk_tok;
   uint8_t* blk_n;
   uint8_t* blk_in_table;
@@ -150,6 +157,7 @@ __global__ void admit_kernel(CommitArgs a) {
       const int64_t len = a.tok_off[r + 1] - a.tok_off[r];
       delta = len - (pl < 0 ? 0 : pl);
       a.s.first_nonhit[r] = (len + BT - 1) / BT;
+      a.s.f_hit[r] = (len + BT - 1) / BT;
     }
     // fast path: every prefix of the chunk fits
     long long incl = delta;
@@ -223,7 +231,8 @@ __global__ void probe_kernel(CommitArgs a) {
   }
 }
 
-__global__ void resolve_kernel(CommitArgs a) {
+// Linked hits: the pre-existing block of item k must descend from the block of item k-1.
+__global__ void resolve_hits_kernel(CommitArgs a) {
   pdl_enter();
   if (a.ctr->error) return;
   FOR_ITEMS(a, item) {
@@ -231,6 +240,24 @@ __global__ void resolve_kernel(CommitArgs a) {
     int nval;
     item_coords(a, item, r, k, nval);
     if (a.s.status[r] != SFKV_PIN_ACCEPTED) continue;
+    const bool ok = a.s.hit0[item] &&
+                    (k == 0 || (a.s.hit0[item - 1] && a.blk_parent[a.s.bid[item]] == a.s.bid[item - 1]));
+    if (!ok) atomicMin(reinterpret_cast<unsigned long long*>(&a.s.f_hit[r]), (unsigned long long)k);
+  }
+}
+
+// Linked dups past the hit run (see the header): the owner o's block is shared only if the
+// previous items of both requests resolve to the same block.
+__global__ void resolve_dups_kernel(CommitArgs a) {
+  pdl_enter();
+  if (a.ctr->error) return;
+  FOR_ITEMS(a, item) {
+    int64_t r, k;
+    int nval;
+    item_coords(a, item, r, k, nval);
+    if (a.s.status[r] != SFKV_PIN_ACCEPTED) continue;
+    const int64_t fh = a.s.f_hit[r];
+    if (k < fh) continue;
     bool dup = false;
     if (a.s.claim[item]) {
       const int64_t o = a.towner[a.s.slot_of[item]];
@@ -244,10 +271,14 @@ __global__ void resolve_kernel(CommitArgs a) {
         dup = true;
 #pragma unroll
         for (int j = 0; j < BT; ++j) dup &= t[j] == u[j];
+        if (dup && k > 0) {
+          const bool dup_link = k > fh && a.s.claim[item - 1] && a.towner[a.s.slot_of[item - 1]] == o - 1;
+          const bool hit_link = k == fh && ko - 1 < a.s.f_hit[ro] && a.s.bid[item - 1] == a.s.bid[o - 1];
+          dup = dup_link || hit_link;
+        }
       }
     }
-    if (!(a.s.hit0[item] || dup))
-      atomicMin(reinterpret_cast<unsigned long long*>(&a.s.first_nonhit[r]), (unsigned long long)k);
+    if (!dup) atomicMin(reinterpret_cast<unsigned long long*>(&a.s.first_nonhit[r]), (unsigned long long)k);
   }
 }
 
@@ -263,8 +294,10 @@ __global__ void categorize_kernel(CommitArgs a) {
       const int64_t r = upper_index(a.s.blk_off, a.n, item);
       const int64_t k = item - a.s.blk_off[r];
       if (a.s.status[r] == SFKV_PIN_ACCEPTED) {
-        if (k < a.s.first_nonhit[r]) {
-          cat = a.s.hit0[item] ? CAT_HIT : CAT_DUP;
+        if (k < a.s.f_hit[r]) {
+          cat = CAT_HIT;
+        } else if (k < a.s.first_nonhit[r]) {
+          cat = CAT_DUP;
         } else {
           const bool own = a.s.claim[item] && a.towner[a.s.slot_of[item]] == item;
           cat = own ? CAT_OWN : CAT_PRIV;
@@ -444,7 +477,10 @@ __global__ void install_kernel(CommitArgs a) {
     const int64_t r = upper_index(a.s.blk_off, a.n, item);
     const int64_t k = item - a.s.blk_off[r];
     const int64_t pb = (int64_t)a.wf[r] * a.max_pin_blocks;
-    a.pin_blk[pb + k] = a.s.bid[item];
+    const int32_t id = a.s.bid[item];
+    a.pin_blk[pb + k] = id;
+    const uint8_t cat = a.s.cat[item];
+    if (cat == CAT_OWN || cat == CAT_PRIV) a.blk_parent[id] = k > 0 ? a.s.bid[item - 1] : -1;
     // pin-major token copy (zero padded), read by the match kernel without indirection
     const int64_t rem = a.tok_off[r + 1] - a.tok_off[r] - k * BT;
     uint32_t t[BT];
@@ -502,6 +538,7 @@ static CommitArgs base_args(sfkv_pool* p) {
   a.pin_tok = p->pin_tok;
   a.pin_groups = pin_groups(p->cfg);
   a.blk_key = p->blk_key;
+  a.blk_parent = p->blk_parent;
   a.blk_tok = p->blk_tok;
   a.blk_n = p->blk_n;
   a.blk_in_table = p->blk_in_table;
@@ -589,7 +626,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
                o_st = cv.take<int32_t>(n), o_slot = cv.take<int64_t>(ni),
                o_bid = cv.take<int32_t>(ni), o_hit = cv.take<uint8_t>(ni),
                o_claim = cv.take<uint8_t>(ni), o_cat = cv.take<uint8_t>(ni),
-               o_fnh = cv.take<int64_t>(n), o_rank = cv.take<int64_t>(ni + 1),
+               o_fnh = cv.take<int64_t>(n), o_fh = cv.take<int64_t>(n), o_rank = cv.take<int64_t>(ni + 1),
                o_wp = cv.take<int64_t>(p->n_words + 1), o_al = cv.take<int64_t>(ni), o_cow = cv.take<int32_t>(ni),
                o_tmp = cv.take<int64_t>(scan_scratch_elems(ni > p->n_words ? ni : p->n_words) +
                                         scan_scratch_elems(n));
@@ -614,6 +651,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   a.s.claim = reinterpret_cast<uint8_t*>(base + o_claim);
   a.s.cat = reinterpret_cast<uint8_t*>(base + o_cat);
   a.s.first_nonhit = reinterpret_cast<int64_t*>(base + o_fnh);
+  a.s.f_hit = reinterpret_cast<int64_t*>(base + o_fh);
   a.s.rank = reinterpret_cast<int64_t*>(base + o_rank);
   a.s.wprefix = reinterpret_cast<int64_t*>(base + o_wp);
   a.s.alloc_list = reinterpret_cast<int64_t*>(base + o_al);
@@ -638,7 +676,8 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   const int sms = sm_count_c();
   const int g = grid_for(ni, 256, sms * 8);
   SFKV_CUDA(launch_pdl(probe_kernel, dim3(g), dim3(256), st, a));
-  SFKV_CUDA(launch_pdl(resolve_kernel, dim3(g), dim3(256), st, a));
+  SFKV_CUDA(launch_pdl(resolve_hits_kernel, dim3(g), dim3(256), st, a));
+  SFKV_CUDA(launch_pdl(resolve_dups_kernel, dim3(g), dim3(256), st, a));
   SFKV_CUDA(launch_pdl(categorize_kernel, dim3(g), dim3(256), st, a));
   SFKV_LAUNCH_CHECK("probe/resolve/categorize");
   if (int rc = exclusive_scan(NeedAlloc{a.s.cat}, ni, a.s.rank, a.s.scan_tmp, st)) return rc;

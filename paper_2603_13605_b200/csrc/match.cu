@@ -10,7 +10,9 @@
 //             first truly differing block — is exact with no dependence on hashing.
 //   digest  = block_digest(k, n, tokens), per block (include/sfkv.h)
 //   c_k     = chain_finalize(sum_{i<=k} digest_i mod 2^62)   (chained block hash, segmented scan)
-//   lookup  : probe the global table for c_k (full blocks), verify tokens, report the block id.
+//   lookup  : probe the global table for c_k (full blocks), verify tokens and the parent link (the
+//             resident block must descend from the table's block for c_{k-1}), report the block
+//             id: a leading run of hits is an exact prefix by induction, whatever the hash does.
 //
 // Launches (no kernel ever waits on another CTA or warp; consecutive launches overlap their
 // prologues with the predecessor's tail through programmatic dependent launch):
@@ -241,6 +243,7 @@ struct MatchKernelArgs {
   const ReqRec* rec;
   const uint32_t* pin_tok;
   const uint32_t* blk_tok;
+  const int32_t* blk_parent;
   const uint8_t* blk_n;
   const Slot* slots;
   uint64_t slot_mask;
@@ -655,6 +658,7 @@ __global__ void __launch_bounds__(MATCH_THREADS) match_chain_kernel(MatchKernelA
       if (incl) break;
     }
   }
+  [[maybe_unused]] const uint64_t carry0 = carry;  // sum through the item before the warp's first
   uint64_t c[CH_TPW];
 #pragma unroll
   for (int i = 0; i < CH_TPW; ++i) {
@@ -665,8 +669,9 @@ __global__ void __launch_bounds__(MATCH_THREADS) match_chain_kernel(MatchKernelA
     const int64_t item = (t0 + i) * WT + lane;
     if (item < n_items && A.out_hash) A.out_hash[item] = c[i];
   }
-  if constexpr (LOOKUP) {  // global table probe, token-verified; all probes of the warp in flight
+  if constexpr (LOOKUP) {  // global table probe, token-verified and parent-linked; probes in flight together
     const int64_t tok_total = K.rec[A.n].tok_off;
+    const int64_t item0 = t0 * WT;
     uint4 raw[CH_TPW];
 #pragma unroll
     for (int i = 0; i < CH_TPW; ++i) {
@@ -675,19 +680,41 @@ __global__ void __launch_bounds__(MATCH_THREADS) match_chain_kernel(MatchKernelA
       if (item < n_items && (rk[i] & RK_FULL))
         raw[i] = __ldg(reinterpret_cast<const uint4*>(K.slots + (c[i] & K.slot_mask)));
     }
+    // the block the table holds for the previous chained key, for the warp's first item: its
+    // request (rk of the previous item) and, inside a request, a probe of fin(carry)
+    uint32_t prev_rk = 0xffffffffu;
+    int32_t prev_raw = -1;
+    if (lane == 0 && item0 > 0) {
+      prev_rk = __ldg(&K.rk[item0 - 1]);
+      if ((prev_rk & ~RK_FULL) == (rk[0] & ~RK_FULL) && (prev_rk & RK_FULL)) {
+        const uint64_t cp = chain_finalize(carry0);
+        uint64_t sl = cp & K.slot_mask;
+        for (;;) {
+          const uint4 w = __ldg(reinterpret_cast<const uint4*>(K.slots + sl));
+          const uint64_t key = (uint64_t)w.x | ((uint64_t)w.y << 32);
+          if (key == cp) {
+            prev_raw = (int32_t)w.z;
+            break;
+          }
+          if (key == KEY_EMPTY) break;
+          sl = (sl + 1) & K.slot_mask;
+        }
+      }
+    }
 #pragma unroll
     for (int i = 0; i < CH_TPW; ++i) {
       const int64_t item = (t0 + i) * WT + lane;
       const bool valid = item < n_items;
       const int64_t r = (int64_t)(rk[i] & ~RK_FULL);
-      int32_t id = -1;
+      int32_t cand = -1;  // the table's block for this key (no token check)
+      bool eq = false;
       if (valid && (rk[i] & RK_FULL)) {
         uint64_t sl = c[i] & K.slot_mask;
         uint4 w = raw[i];
         for (;;) {
           const uint64_t key = (uint64_t)w.x | ((uint64_t)w.y << 32);
           if (key == c[i]) {
-            const int32_t cand = (int32_t)w.z;
+            cand = (int32_t)w.z;
             if (cand >= 0) {  // only full blocks are ever published; a pending claim reads -1
               int64_t bo, to;
               int32_t len, pl, wf;
@@ -695,10 +722,9 @@ __global__ void __launch_bounds__(MATCH_THREADS) match_chain_kernel(MatchKernelA
               uint32_t t[BT], q[BT];
               load_block(A.tok, to + (item - bo) * BT, BT, tok_total, t);
               load16_aligned(K.blk_tok + (int64_t)cand * BT, q);
-              bool eq = true;
+              eq = true;
 #pragma unroll
               for (int j = 0; j < BT; ++j) eq &= q[j] == t[j];
-              if (eq) id = cand;
             }
             break;
           }
@@ -707,6 +733,16 @@ __global__ void __launch_bounds__(MATCH_THREADS) match_chain_kernel(MatchKernelA
           w = __ldg(reinterpret_cast<const uint4*>(K.slots + sl));
         }
       }
+      // predecessor item: the lane below, the previous tile's last lane, or the warp's carry-in
+      const uint32_t up_rk = __shfl_up_sync(0xffffffffu, rk[i], 1);
+      const int32_t up_raw = __shfl_up_sync(0xffffffffu, cand, 1);
+      const uint32_t p_rk = lane > 0 ? up_rk : prev_rk;
+      const int32_t p_raw = lane > 0 ? up_raw : prev_raw;
+      const bool head = (p_rk & ~RK_FULL) != (uint32_t)r || item == 0;
+      int32_t id = -1;
+      if (eq && (head || __ldg(&K.blk_parent[cand]) == p_raw)) id = cand;
+      prev_rk = __shfl_sync(0xffffffffu, rk[i], 31);
+      prev_raw = __shfl_sync(0xffffffffu, cand, 31);
       if (valid) A.out_block[item] = id;
       // leading hit length: the first miss of each request segment in the tile lowers out_hit
       const uint32_t prev = __shfl_up_sync(0xffffffffu, rk[i] & ~RK_FULL, 1);
@@ -781,6 +817,7 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   K.rec = rec;
   K.pin_tok = p->pin_tok;
   K.blk_tok = p->blk_tok;
+  K.blk_parent = p->blk_parent;
   K.blk_n = p->blk_n;
   K.slots = p->slots;
   K.slot_mask = (uint64_t)p->table_slots - 1;

@@ -6,7 +6,8 @@
 //          pin's tokens block by block (pin-major), so the blocks of one request segment of a
 //          match tile are one contiguous extent that a single bulk copy (TMA) stages, with no
 //          block-id indirection; the block's chained hash is blk_key[pin_blk]
-//   blocks blk_key[B] u64, blk_tok[B][16] u32 (tokens: verify-on-hit for shared blocks),
+//   blocks blk_key[B] u64, blk_parent[B] i32 (exact sharing: a hit must descend from the block
+//          chosen for its predecessor), blk_tok[B][16] u32 (tokens: verify-on-hit),
 //          blk_n[B] u8 (valid tokens), blk_in_table[B] u8, blk_ref[B] u32, blk_slot[B] i64,
 //          free_bits[ceil(B/32)] u32 (1 = free)
 //   table  slots[S] of 16 B {u64 key, i32 block, i32 pad} (open addressing, linear probing,
@@ -68,6 +69,7 @@ struct sfkv_pool {
   int32_t* pin_blk = nullptr;
   uint32_t* pin_tok = nullptr;  // [W][MB][16] a pin's tokens, block by block (pin-major copy)
   uint64_t* blk_key = nullptr;
+  int32_t* blk_parent = nullptr;  // the block at index k-1 of the pin that allocated it (-1 at k = 0)
   uint32_t* blk_tok = nullptr;
   uint8_t* blk_n = nullptr;
   uint8_t* blk_in_table = nullptr;

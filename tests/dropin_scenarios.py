@@ -1,8 +1,9 @@
 """Drop-in scenarios (SURVEY §8d C1 and the synthetic ones): reference-format configs and traces
 for the reference's harness, shared by tests/test_dropin_replay.py and bench.py's C1 leg. The
-reference demo parameters (proj/configs/support_demo.json, proj/traces/support_demo.jsonl) are
-restated as Python data because the reference tree is absent on the GPU box; the synthetic
-scenarios come from tests/golden/make_golden.py's generators."""
+reference demo parameters (proj/configs/support_demo.json, proj/traces/support_demo.jsonl;
+mapped_one_bit.json x mixed_workload.jsonl in make_golden.py) are restated as Python data because
+the reference tree is absent on the GPU box; the synthetic scenarios come from
+tests/golden/make_golden.py's generators."""
 import os
 import sys
 
@@ -66,6 +67,9 @@ SCENARIOS = {
     "chain_scale": lambda: synthetic("chain_scale"),
     "alt_pressure_flaky": lambda: synthetic("alt_pressure"),
     "chain_scale_flaky": lambda: synthetic("chain_scale"),
+    "mapped_one_bit": lambda: synthetic("mapped_one_bit"),
+    "mapped_one_bit_reroute": lambda: synthetic("mapped_one_bit_reroute"),
+    "mapped_threshold_reroute": lambda: synthetic("mapped_threshold_reroute"),
 }
 # Driver flags of the failure-path scenarios (make_golden.FLAKY: backends whose flush throws).
 FLAGS = {"alt_pressure_flaky": ["--flaky", "A:1,B:2"], "chain_scale_flaky": ["--flaky", "heavy:2"]}

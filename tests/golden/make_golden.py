@@ -20,6 +20,7 @@ Scenarios:
   chain_scale       synthetic, SURVEY §9 C2 probe at reduced scale: 300 math_chain_k workflows,
                     log-uniform bases, tight capacity (rejections) and pressure ticks
   *_flaky           alt_pressure / chain_scale with backends whose flush throws (FLAKY below)
+  mapped_*_reroute  one-bit / threshold stage mapping under overload (reroute_on_overload)
 Synthetic inputs are written to tests/golden/inputs/ and committed with the streams.
 
 Full-scale compact goldens (`python tests/golden/make_golden.py c2_probe c4_probe`, written to
@@ -160,6 +161,70 @@ def c4_probe():
     return cfg, trace
 
 
+def mixed_workload_trace(n=24, words=20, lengths=None):
+    """proj/traces/mixed_workload.jsonl restated: n single_shot_patch requests at t = 0,
+    "repair request i: ctx{i}w0 .. ctx{i}w{words-1}", complexity labels simple for i in [0, 5) and
+    [12, 17), complex otherwise, 40 expected output tokens (lengths: per-request word counts)."""
+    trace = []
+    for i in range(n):
+        k = words if lengths is None else lengths[i]
+        prompt = f"repair request {i}: " + " ".join(f"ctx{i}w{j}" for j in range(k))
+        cx = "simple" if (i < 5 or 12 <= i < 17) else "complex"
+        trace.append({"template": "single_shot_patch", "arrival_ms": 0,
+                      "payload": {"prompt": prompt, "complexity": cx, "expected_output_tokens": 40}})
+    return trace
+
+
+def one_bit_config(reroute=None, maxc=8):
+    """proj/configs/mapped_one_bit.json restated (one-bit routing, the light backend's echo script
+    as the classifier)."""
+    cfg = {
+        "label": "mapped-one-bit",
+        "backends": [
+            {"ref": "light", "kind": "simulated", "model": "sim-light-4b", "tier": "light",
+             "price": {"input_per_1m": 0.1, "output_per_1m": 0.4},
+             "sim": {"prefill_ms_per_token": 1.0, "decode_ms_per_token": 10.0, "max_concurrency": maxc,
+                     "cache_capacity_tokens": 1000000, "output": {"rule": "script", "name": "one_bit_light"}}},
+            {"ref": "heavy", "kind": "simulated", "model": "sim-heavy-8b", "tier": "heavy",
+             "price": {"input_per_1m": 0.5, "output_per_1m": 1.5},
+             "sim": {"prefill_ms_per_token": 2.0, "decode_ms_per_token": 20.0, "max_concurrency": maxc,
+                     "cache_capacity_tokens": 1000000,
+                     "output": {"rule": "from_trace", "key": "expected_output_tokens", "fallback_tokens": 40}}}],
+        "mapper": {"type": "one_bit", "classifier": "light", "light": "light", "heavy": "heavy"},
+        "templates": {"single_shot_patch": {"backend": "heavy", "max_tokens": 4096}},
+    }
+    if reroute:
+        cfg["reroute"] = reroute
+    return cfg
+
+
+REROUTE = {"limit": 3, "alternates": {"heavy": ["light"], "light": ["heavy"]}}
+
+
+def mapped_one_bit():
+    return one_bit_config(), mixed_workload_trace()
+
+
+def mapped_one_bit_reroute():
+    """One-bit routing under overload: max_concurrency 2 and queue limit 3, so the burst of 24
+    requests spills onto the alternate backend (reroute_on_overload, orchestrator.cpp:78-87)."""
+    return one_bit_config(REROUTE, maxc=2), mixed_workload_trace()
+
+
+def mapped_threshold_reroute():
+    """Threshold routing (score = count_context_tokens, config.cpp:193; light iff score <= 40,
+    ties light) over prompts of 4..66 words, with overload rerouting."""
+    cfg = one_bit_config(REROUTE, maxc=2)
+    cfg["label"] = "mapped-threshold"
+    cfg["mapper"] = {"type": "threshold", "threshold": 40, "light": "light", "heavy": "heavy"}
+    lengths = [4 + (i * 37) % 63 for i in range(24)]
+    lengths[3] = 37  # 40 tokens exactly: the tie goes light (mapper.cpp:30)
+    return cfg, mixed_workload_trace(lengths=lengths)
+
+
+ROUTER_SCENARIOS = {"mapped_one_bit_reroute": mapped_one_bit_reroute,
+                    "mapped_threshold_reroute": mapped_threshold_reroute}
+
 FULL = os.path.join(HERE, "full")  # compact full-scale goldens (no token ids)
 FULL_SCENARIOS = {"c2_probe": c2_probe, "c4_probe": c4_probe}
 
@@ -222,6 +287,16 @@ def main():
     run("mapped_one_bit", f"{REF}/configs/mapped_one_bit.json", f"{REF}/traces/mixed_workload.jsonl")
     run("single_heavy", f"{REF}/configs/single_heavy.json", f"{REF}/traces/mixed_workload.jsonl")
     for name, fn in (("alt_pressure", alt_pressure), ("chain_scale", chain_scale)):
+        cfg, trace = fn()
+        cp = os.path.join(INPUTS, f"{name}.config.json")
+        tp = os.path.join(INPUTS, f"{name}.trace.jsonl")
+        with open(cp, "w") as f:
+            json.dump(cfg, f, indent=1)
+        with open(tp, "w") as f:
+            for rec in trace:
+                f.write(json.dumps(rec) + "\n")
+        run(name, cp, tp)
+    for name, fn in ROUTER_SCENARIOS.items():
         cfg, trace = fn()
         cp = os.path.join(INPUTS, f"{name}.config.json")
         tp = os.path.join(INPUTS, f"{name}.trace.jsonl")

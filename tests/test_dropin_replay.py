@@ -21,11 +21,16 @@ DRIVER = os.path.join(REPO, "oracle", "_ref", "sf_gpu_replay")
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("gpu_memory", [False, True], ids=["ref-memory", "gpu-memory"])
+MODES = {"ref-memory": [], "gpu-memory": ["--gpu-memory"], "gpu-all": ["--gpu-memory", "--gpu-router"]}
+
+
+@pytest.mark.parametrize("mode", sorted(MODES))
 @pytest.mark.parametrize("name", sorted(SCENARIOS))
-def test_reference_harness_on_gpu_pool_matches_golden(tmp_path, name, gpu_memory):
+def test_reference_harness_on_gpu_pool_matches_golden(tmp_path, name, mode):
     """gpu-memory: the reference's MemoryManager is replaced by GpuMemoryManager (integration/),
-    so pin cache, policy resolution, tracker and pressure ticks all run on the B200."""
+    so pin cache, policy resolution, tracker and pressure ticks all run on the B200; gpu-all also
+    replaces the stage routers (integration/gpu_router.hpp: plan / threshold / one-bit decisions
+    and reroute_on_overload through sfmap_*)."""
     if not os.path.exists(DRIVER):
         pytest.fail("oracle/_ref/sf_gpu_replay missing: build it where /root/reference exists")
     cfg, trace = SCENARIOS[name]()
@@ -33,7 +38,7 @@ def test_reference_harness_on_gpu_pool_matches_golden(tmp_path, name, gpu_memory
     cp.write_text(json.dumps(cfg))
     tp.write_text("".join(json.dumps(r) + "\n" for r in trace))
     subprocess.run([DRIVER, "--config", str(cp), "--trace", str(tp), "--out", str(op)] +
-                   (["--gpu-memory"] if gpu_memory else []) + FLAGS.get(name, []), check=True, timeout=600)
+                   MODES[mode] + FLAGS.get(name, []), check=True, timeout=600)
     got = [json.loads(l) for l in op.read_text().splitlines()]
     gold = replay.load_stream(name)
 
