@@ -26,5 +26,5 @@ def load_library():
 def api() -> Api:
     global _api
     if _api is None:
-        _api = Api(load_library(), "gpu")
+        _api = Api(load_library())
     return _api

@@ -1,8 +1,8 @@
 """ctypes binding of the sfkv C ABI (include/sfkv.h) and a numpy-level pool wrapper.
 
-The binding is prefix-parameterised because the CPU oracle (oracle/sfkv_oracle.h) restates the
-same entry points under the ``sfo_`` prefix: tests bind both libraries through this one table
-and drive them with identical arguments. The product path binds only ``libsfkv.so``.
+The product binds only ``libsfkv.so``. The signature tables are module-level so that the tests'
+checker binding (tests/oracle_lib.py, the CPU oracle's ``sfo_`` restatement of the same entry
+points) can reuse them; nothing in this package loads or branches on the oracle.
 """
 from __future__ import annotations
 
@@ -92,7 +92,7 @@ SIGNATURES = {
     "tokenize_batch": [P, i64, P, P, P, P, P, i64, C.POINTER(i64)],
     "chain_finalize": [u64],
 }
-# entry points whose name differs between the GPU ABI and the oracle
+# entry points without a counterpart in SIGNATURES' shared list
 GPU_ONLY = {
     "abi_version": [],
     "last_error": [],
@@ -114,20 +114,16 @@ GPU_ONLY = {
     "handoff_recv_batch": [P, P, i64, P, P, P, P, P],
     "handoff_recv_batch_dev": [P, P, i64, P, P, P, i64, P, P],
 }
-ORACLE_ONLY = {
-    "gather": [P, i64, P, P, P],
-    "chain_hashes": [P, i64, P],
-}
-MET_FNS = {  # sfmet_* on the GPU (first argument: device), sfo_* in the oracle
+MET_FNS = {  # sfmet_* (first argument: device ordinal)
     "latency_batch": [P, i64, P, P, P, P, P, i32, P, P, P, P, P, P],
     "nearest_rank": [P, i64, P, i32, P, P],
 }
-GLOBAL_FNS = {  # prefix differs: sfmm_/sfmap_ on the GPU, sfo_ in the oracle
+GLOBAL_FNS = {  # sfmm_pressure_argmin / sfmap_* (first argument: device ordinal)
     "pressure_argmin": [P, i64, P, P, P, P, P, i32, P, f64, P],
     "threshold_batch": [P, i64, P, f64, P],
     "cost_batch": [P, i64, i32, P, P, P, P, P, P, P, P, P, u64, P, P],
 }
-# memory-manager tracker: sfmm_* on the GPU, sfo_* in the oracle (same argument lists)
+# memory-manager tracker: sfmm_*
 MM_FNS = {
     "tracker_create": [P, C.POINTER(P)],
     "tracker_destroy": [P],
@@ -164,34 +160,33 @@ class SfkvError(RuntimeError):
 
 
 class Api:
-    """Bound entry points of one library: ``api.match_batch(...)`` etc. (raw ints returned)."""
+    """Bound entry points of libsfkv.so: ``api.match_batch(...)`` etc. (raw ints returned).
 
-    def __init__(self, lib: C.CDLL, kind: str):
-        assert kind in ("gpu", "oracle")
-        self.lib, self.kind = lib, kind
-        pre = "sfkv_" if kind == "gpu" else "sfo_"
+    The product binds nothing else. Calls whose argument lists carry a device ordinal go through
+    ``dev_call``; the few pool operations that move payload bytes between a pool and torch
+    (``gather_payload`` / ``kv_staging``) are methods here so that code above the binding stays
+    free of per-library branches."""
+
+    kind = "gpu"
+
+    def __init__(self, lib: C.CDLL):
+        self.lib = lib
+        self._bind_tables()
+
+    def _bind_tables(self):
         table = dict(SIGNATURES)
-        table.update(GPU_ONLY if kind == "gpu" else ORACLE_ONLY)
+        table.update(GPU_ONLY)
         for name, argt in table.items():
-            self._bind(pre + name, name, argt)
-        for name, argt in MM_FNS.items():
-            self._bind(("sfmm_" if kind == "gpu" else "sfo_") + name, "mm_" + name, argt)
-        if kind == "gpu":
-            for name, argt in MM_GPU_ONLY.items():
-                self._bind("sfmm_" + name, "mm_" + name, argt)
+            self._bind("sfkv_" + name, name, argt)
+        for name, argt in {**MM_FNS, **MM_GPU_ONLY}.items():
+            self._bind("sfmm_" + name, "mm_" + name, argt)
         for name, argt in MET_FNS.items():
-            if kind == "gpu":
-                self._bind("sfmet_" + name, name, [i32] + argt[1:])
-            else:
-                self._bind("sfo_" + name, name, argt[1:])
+            self._bind("sfmet_" + name, name, [i32] + argt[1:])
         for name, argt in GLOBAL_FNS.items():
-            if kind == "gpu":
-                sym = ("sfmm_" if name == "pressure_argmin" else "sfmap_") + name
-                self._bind(sym, name, [i32] + argt[1:])  # first arg: device ordinal
-            else:
-                self._bind("sfo_" + name, name, argt[1:])
-        if kind == "gpu":  # device-pointer mapper batch (+ stream)
-            self._bind("sfmap_cost_batch_dev", "cost_batch_dev", [i32] + GLOBAL_FNS["cost_batch"][1:] + [P])
+            sym = ("sfmm_" if name == "pressure_argmin" else "sfmap_") + name
+            self._bind(sym, name, [i32] + argt[1:])  # first arg: device ordinal
+        # device-pointer mapper batch (+ stream)
+        self._bind("sfmap_cost_batch_dev", "cost_batch_dev", [i32] + GLOBAL_FNS["cost_batch"][1:] + [P])
 
     def _bind(self, sym, name, argt):
         fn = getattr(self.lib, sym)
@@ -199,13 +194,36 @@ class Api:
         fn.restype = _RESTYPES.get(name, C.c_int)
         setattr(self, name, fn)
 
+    def dev_call(self, name: str, device: int, *args):
+        """Entry points of MET_FNS / GLOBAL_FNS: the device ordinal leads the argument list."""
+        return getattr(self, name)(int(device), *args)
+
+    def error_detail(self) -> str:
+        msg = self.lib.sfkv_last_error()
+        return msg.decode() if msg else ""
+
     def check(self, fn: str, rc: int):
         if rc != 0:
-            detail = ""
-            if self.kind == "gpu":
-                msg = self.lib.sfkv_last_error()
-                detail = msg.decode() if msg else ""
-            raise SfkvError(fn, rc, detail)
+            raise SfkvError(fn, rc, self.error_detail())
+
+    # -- payload movement between a pool and torch (device memory) ------------------------------
+    def gather_payload(self, pool: "Pool", wf: int, nbytes: int, device=None):
+        """The pin's KV rows [slab][L][row] as a flat uint8 device tensor (sfkv_gather_dev)."""
+        import torch
+        buf = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=device)
+        w = torch.tensor([wf], dtype=torch.int32, device=device)
+        off = torch.zeros(1, dtype=torch.int64, device=device)
+        self.check("gather_dev", self.gather_dev(pool.h, 1, C.c_void_p(w.data_ptr()),
+                                                 C.c_void_p(buf.data_ptr()), C.c_void_p(off.data_ptr())))
+        self.check("pool_sync", self.pool_sync(pool.h))
+        return buf[:nbytes]
+
+    def kv_staging(self, staging, device=None):
+        """A commit's kv_src argument from a torch byte tensor: device memory, never empty."""
+        import torch
+        if staging.numel() == 0:
+            return torch.zeros(16, dtype=torch.uint8, device=device)
+        return staging
 
 
 def _ptr(a):
@@ -441,7 +459,7 @@ class MmRecords(C.Structure):
 
 
 class Tracker:
-    """GPU-resident (or oracle) MemoryManager tracker over dense ids (host-pointer entry points)."""
+    """GPU-resident MemoryManager tracker over dense ids (host-pointer entry points)."""
 
     def __init__(self, api: Api, max_workflows: int, n_backends: int, chain=("preserve_small_increment",
                  "flush_at_boundary"), tau=512, tau_pressure=0.85, device=0, max_stages=0):
@@ -599,9 +617,7 @@ def latency_batch(api: Api, backend, queue_ms, P, M, O, overhead, prefill, decod
     par = [np.ascontiguousarray(x, np.float64) for x in (overhead, prefill, decode)]
     ttft, total, svc = np.zeros(n), np.zeros(n), np.zeros(n)
     args = [n] + [_ptr(a) for a in arrs] + [len(par[0])] + [_ptr(x) for x in par] + [_ptr(ttft), _ptr(total), _ptr(svc)]
-    if api.kind == "gpu":
-        args = [device] + args
-    api.check("latency_batch", api.latency_batch(*args))
+    api.check("latency_batch", api.dev_call("latency_batch", device, *args))
     return ttft, total, svc
 
 
@@ -610,7 +626,5 @@ def nearest_rank(api: Api, samples, pct, device=0):
     pct = np.ascontiguousarray(pct, np.int32)
     out = np.zeros(len(pct))
     args = [len(samples), _ptr(samples), len(pct), _ptr(pct), _ptr(out)]
-    if api.kind == "gpu":
-        args = [device] + args
-    api.check("nearest_rank", api.nearest_rank(*args))
+    api.check("nearest_rank", api.dev_call("nearest_rank", device, *args))
     return out

@@ -7,7 +7,7 @@ mapped to another backend ships the workflow's retained context to that backend'
     header (pin length L)  ->  token ids [L] (u32)  ->  KV rows [slab][L][row] (payload pools)
 
 sent point to point with torch.distributed (the portable message path: `send_pin` / `recv_pin`,
-also what the CPU oracle pools run under gloo). The receiver commits it as its own pin: M =
+which also runs under gloo in the CPU tests). The receiver commits it as its own pin: M =
 LCP(its old pin, tokens) rows come from its old pin by copy-on-share inside sfkv_commit_batch, only
 rows [M, L) are read from the message.
 
@@ -39,26 +39,10 @@ def _dist():
 
 
 def gather_pin(pool: Pool, wf: int, device=None):
-    """The pin's KV rows as a flat uint8 tensor [slab][L][row] (torch; on `device` for GPU pools)."""
-    import torch
+    """The pin's KV rows as a flat uint8 tensor [slab][L][row] (on `device`)."""
     L = pool.pinned_token_count(wf)
     nbytes = pool.cfg.n_slabs * L * pool.cfg.slab_row_bytes
-    if pool.api.kind == "oracle":
-        buf = np.zeros(max(nbytes, 1), dtype=np.uint8)
-        w = np.array([wf], dtype=np.int32)
-        off = np.zeros(1, dtype=np.int64)
-        pool.api.check("gather", pool.api.gather(pool.h, 1, w.ctypes.data, buf.ctypes.data,
-                                                 off.ctypes.data))
-        return torch.from_numpy(buf[:nbytes].copy())
-    import ctypes as C
-    buf = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=device)
-    w = torch.tensor([wf], dtype=torch.int32, device=device)
-    off = torch.zeros(1, dtype=torch.int64, device=device)
-    pool.api.check("gather_dev", pool.api.gather_dev(pool.h, 1, C.c_void_p(w.data_ptr()),
-                                                     C.c_void_p(buf.data_ptr()),
-                                                     C.c_void_p(off.data_ptr())))
-    pool.api.check("pool_sync", pool.api.pool_sync(pool.h))
-    return buf[:nbytes]
+    return pool.api.gather_payload(pool, wf, nbytes, device)
 
 
 def send_pin(pool: Pool, wf: int, dst: int, device=None, group=None):
@@ -99,12 +83,7 @@ def recv_pin(pool: Pool, wf: int, src: int, device=None, group=None):
     M = int(pool.match(wfa, off, t)[0])
     # staging rows [M, L) per slab; rows below M are copied on share from the old pin
     staging = payload.view(S, L, row)[:, M:, :].contiguous().view(-1)
-    if pool.api.kind == "oracle":
-        staging = staging.cpu().numpy()
-        if staging.size == 0:
-            staging = np.zeros(16, dtype=np.uint8)
-    elif staging.numel() == 0:
-        staging = torch.zeros(16, dtype=torch.uint8, device=dev)
+    staging = pool.api.kv_staging(staging, dev)
     st = pool.commit(wfa, off, t, kv_src=staging, kv_src_off=np.zeros(1, dtype=np.int64),
                      m_expected=np.array([M], dtype=np.int64))
     return int(st[0])
@@ -203,18 +182,29 @@ class PeerLink:
         return st
 
 
+def gather_columns(m_col, group=None):
+    """SURVEY §8e exchange 2's collective: every rank contributes its pool's M column (int64[R]);
+    returns the R x C request-major matrix on m_col's device. NCCL groups gather in place on the
+    GPU (all_gather_into_tensor); gloo groups through the host."""
+    dist = _dist()
+    import torch
+    world = dist.get_world_size(group)
+    R = m_col.numel()
+    mdev = _meta_device(group)
+    m_all = torch.empty(world * R, dtype=torch.int64, device=mdev)
+    dist.all_gather_into_tensor(m_all, m_col.to(mdev), group=group)
+    return m_all.to(m_col.device).view(world, R).t().contiguous()
+
+
 def route_step(api, pool: Pool, wf, tok_off, tok, P, O, overhead, prefill, decode, qpen, alternates, depth,
                limit: int, device: int = 0, group=None):
     """SURVEY §8e exchange 2: this rank's backend is candidate `rank`; returns (choice[R], cost[R],
-    depth[C]) — identical on every rank. GPU pools: the M column, the gathered matrix and the mapper
-    stay on the device (sfkv_match_batch_dev, all_gather_into_tensor — in place under NCCL, through
-    the host under gloo — and sfmap_cost_batch_dev); oracle pools run the host entry points with the
-    same exchange."""
+    depth[C]) — identical on every rank. The M column, the gathered matrix and the mapper stay on
+    the device: sfkv_match_batch_dev, gather_columns, sfmap_cost_batch_dev."""
     import ctypes as C
 
     import torch
-    dist = _dist()
-    world = dist.get_world_size(group)
+    world = _dist().get_world_size(group)
     R = len(wf)
     wf = np.ascontiguousarray(wf, dtype=np.int32)
     tok_off = np.ascontiguousarray(tok_off, dtype=np.int64)
@@ -223,42 +213,27 @@ def route_step(api, pool: Pool, wf, tok_off, tok, P, O, overhead, prefill, decod
     P = np.ascontiguousarray(P, dtype=np.int64)
     O = np.ascontiguousarray(O, dtype=np.int64)
     depth = np.ascontiguousarray(depth, dtype=np.uint64).copy()
-    if api.kind == "gpu":
-        dev = torch.device("cuda", device)
-        t = lambda x: torch.from_numpy(x).to(dev)  # noqa: E731
-        ptr = lambda x: C.c_void_p(x.data_ptr()) if x is not None else None  # noqa: E731
-        d_wf, d_off, d_tok = t(wf), t(tok_off), t(np.ascontiguousarray(tok, dtype=np.uint32).view(np.int32))
-        m_col = torch.empty(R, dtype=torch.int64, device=dev)
-        api.check("match_dev", api.match_batch_dev(pool.h, R, ptr(d_wf), ptr(d_off), ptr(d_tok), int(tok_off[-1]),
-                                                   ptr(m_col), None))
-        api.check("sync", api.pool_sync(pool.h))
-        mdev = _meta_device(group)  # NCCL: gathered in place on the GPU; gloo: through the host
-        m_all = torch.empty(world * R, dtype=torch.int64, device=mdev)
-        dist.all_gather_into_tensor(m_all, m_col.to(mdev), group=group)
-        M = m_all.to(dev).view(world, R).t().contiguous()  # R x C, request-major
-        d = {k: t(v) for k, v in dict(P=P, O=O, oh=par[0], pf=par[1], dc=par[2], qp=par[3],
-                                      dp=depth.view(np.int64)).items()}
-        d_alt = t(alt) if alt is not None else None
-        choice = torch.empty(R, dtype=torch.int32, device=dev)
-        cost = torch.empty(R, dtype=torch.float64, device=dev)
-        stream = torch.cuda.current_stream(dev)
-        api.check("cost_batch_dev", api.cost_batch_dev(
-            device, R, world, ptr(d["P"]), ptr(M), ptr(d["O"]), ptr(d["oh"]), ptr(d["pf"]), ptr(d["dc"]),
-            ptr(d["qp"]), ptr(d_alt), ptr(d["dp"]), int(limit), ptr(choice), ptr(cost),
-            C.c_void_p(stream.cuda_stream)))
-        stream.synchronize()
-        return choice.cpu().numpy(), cost.cpu().numpy(), d["dp"].cpu().numpy().view(np.uint64)
-    # oracle pools (CPU, gloo): the same exchange through the host entry points
-    m_col = torch.from_numpy(pool.match(wf, tok_off, np.ascontiguousarray(tok, dtype=np.uint32)).astype(np.int64))
-    parts = [torch.empty(R, dtype=torch.int64) for _ in range(world)]
-    dist.all_gather(parts, m_col, group=group)
-    M = np.ascontiguousarray(torch.stack(parts, 1).numpy())  # R x C
-    choice = np.zeros(R, np.int32)
-    cost = np.zeros(R, np.float64)
-    api.check("cost_batch", api.cost_batch(R, world, P.ctypes.data, M.ctypes.data, O.ctypes.data,
-                                           *[x.ctypes.data for x in par], alt.ctypes.data if alt is not None else None,
-                                           depth.ctypes.data, int(limit), choice.ctypes.data, cost.ctypes.data))
-    return choice, cost, depth
+    dev = torch.device("cuda", device)
+    t = lambda x: torch.from_numpy(x).to(dev)  # noqa: E731
+    ptr = lambda x: C.c_void_p(x.data_ptr()) if x is not None else None  # noqa: E731
+    d_wf, d_off, d_tok = t(wf), t(tok_off), t(np.ascontiguousarray(tok, dtype=np.uint32).view(np.int32))
+    m_col = torch.empty(R, dtype=torch.int64, device=dev)
+    api.check("match_dev", api.match_batch_dev(pool.h, R, ptr(d_wf), ptr(d_off), ptr(d_tok), int(tok_off[-1]),
+                                               ptr(m_col), None))
+    api.check("sync", api.pool_sync(pool.h))
+    M = gather_columns(m_col, group)  # R x C, request-major
+    d = {k: t(v) for k, v in dict(P=P, O=O, oh=par[0], pf=par[1], dc=par[2], qp=par[3],
+                                  dp=depth.view(np.int64)).items()}
+    d_alt = t(alt) if alt is not None else None
+    choice = torch.empty(R, dtype=torch.int32, device=dev)
+    cost = torch.empty(R, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    api.check("cost_batch_dev", api.cost_batch_dev(
+        device, R, world, ptr(d["P"]), ptr(M), ptr(d["O"]), ptr(d["oh"]), ptr(d["pf"]), ptr(d["dc"]),
+        ptr(d["qp"]), ptr(d_alt), ptr(d["dp"]), int(limit), ptr(choice), ptr(cost),
+        C.c_void_p(stream.cuda_stream)))
+    stream.synchronize()
+    return choice.cpu().numpy(), cost.cpu().numpy(), d["dp"].cpu().numpy().view(np.uint64)
 
 
 def max_over_ranks(x: float, device=None) -> float:

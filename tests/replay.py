@@ -174,8 +174,6 @@ def default_pressure(api, device=0):
         args = [len(backend), backend.ctypes.data, ts.ctypes.data, wr.ctypes.data,
                 inf.ctypes.data, pres.ctypes.data, len(util), util.ctypes.data, tau,
                 out.ctypes.data]
-        if api.kind == "gpu":
-            args = [device] + args
-        api.check("pressure_argmin", api.pressure_argmin(*args))
+        api.check("pressure_argmin", api.dev_call("pressure_argmin", device, *args))
         return out
     return run

@@ -202,9 +202,7 @@ def _cost(api, dev, n, c, P, M, O, par, alt, depth, limit):
     args = [n, c, P.ctypes.data, M.ctypes.data, O.ctypes.data] + [x.ctypes.data for x in par] + \
            [alt.ctypes.data if alt is not None else None, depth.ctypes.data, limit,
             choice.ctypes.data, cost.ctypes.data]
-    if api.kind == "gpu":
-        args = [dev] + args
-    api.check("cost_batch", api.cost_batch(*args))
+    api.check("cost_batch", api.dev_call("cost_batch", dev, *args))
     return choice, cost
 
 

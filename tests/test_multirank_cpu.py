@@ -146,7 +146,8 @@ def _route_worker(rank, world, port, q, kind="oracle"):
         wf = np.arange(R, dtype=np.int32)
         assert pool.commit(wf, *csr(pins[rank])).all()
         off, tok = csr(reqs)
-        res = sfdist.route_step(api, pool, wf, off, tok, P, O, *par, alt, np.zeros(world, np.uint64), limit=20)
+        route = sfdist.route_step if kind == "gpu" else oracle_lib.route_step_host
+        res = route(api, pool, wf, off, tok, P, O, *par, alt, np.zeros(world, np.uint64), limit=20)
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, res, None))
