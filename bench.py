@@ -173,55 +173,84 @@ def ref_lib():
     if not os.path.exists(so):
         return None
     L = C.CDLL(so)
-    L.sfref_pool_create.restype = C.c_void_p
-    L.sfref_pool_create.argtypes = [C.c_longlong]
-    L.sfref_complete.restype = C.c_longlong
-    L.sfref_complete.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p, C.c_longlong, C.c_void_p]
-    L.sfref_batch_create.restype = C.c_void_p
-    L.sfref_batch_create.argtypes = [C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p]
-    L.sfref_prefix_match_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     L.sfref_pool_destroy.argtypes = [C.c_void_p]
     L.sfref_batch_destroy.argtypes = [C.c_void_p]
+    L.sfref_workers_create.restype = C.c_void_p
+    L.sfref_workers_create.argtypes = [C.c_int, C.c_void_p]
+    L.sfref_workers_destroy.argtypes = [C.c_void_p]
+    L.sfref_prefix_match_parallel.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.sfref_build_shards_parallel.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     return L
 
 
-def ref_shard(L, wl, idx):
-    """A reference SimulatedBackend holding the pins of workflows idx, plus their request batch."""
-    h = L.sfref_pool_create(1 << 40)
-    acc = C.c_int()
-    for w in idx:
-        t = wl["pin_tok"][wl["pin_off"][w]:wl["pin_off"][w + 1]]
-        L.sfref_complete(h, f"wf{w}".encode(), t.ctypes.data, len(t), C.byref(acc))
-    seqs = [wl["req_tok"][wl["req_off"][w]:wl["req_off"][w + 1]] for w in idx]
-    off = np.zeros(len(idx) + 1, np.int64)
-    off[1:] = np.cumsum([len(s) for s in seqs])
-    tok = np.concatenate(seqs).astype(np.uint32) if seqs else np.zeros(1, np.uint32)
-    names = (C.c_char_p * len(idx))(*[f"wf{w}".encode() for w in idx])
-    b = L.sfref_batch_create(len(idx), names, off.ctypes.data, tok.ctypes.data)
-    blocks = int(blocks_of(np.diff(off)).sum())
-    return h, b, blocks, len(idx)
+class _ShardSpec(C.Structure):  # ref_capi.cpp ShardSpec
+    _fields_ = [("n", C.c_longlong), ("wf", C.c_void_p), ("pin_off", C.c_void_p), ("pin_tok", C.c_void_p),
+                ("req_off", C.c_void_p), ("req_tok", C.c_void_p)]
 
 
-def time_ref(L, shards, steps, warmup):
-    """Concurrent prefix_match over all shards (one thread each; ctypes drops the GIL)."""
-    outs = [np.zeros(n, np.int64) for (_, _, _, n) in shards]
+def host_info():
+    """CPU model, online cores and this process's affinity (the cores a CPU baseline may use)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    aff = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else list(range(os.cpu_count() or 1))
+    return {"cpu_model": model, "nproc": os.cpu_count(), "affinity": len(aff)}, aff
 
-    def one(i):
-        h, b, _, _ = shards[i]
-        L.sfref_prefix_match_batch(h, b, outs[i].ctypes.data)
 
-    times = []
-    for it in range(warmup + steps):
-        ths = [threading.Thread(target=one, args=(i,)) for i in range(len(shards))]
-        t0 = time.perf_counter()
-        for t in ths:
-            t.start()
-        for t in ths:
-            t.join()
-        dt = time.perf_counter() - t0
-        if it >= warmup:
-            times.append(dt)
-    return times, outs
+class RefShards:
+    """The reference's SimulatedBackend::prefix_match over `cores` shards (one backend per core, each
+    holding its workflows' pins), run by a persistent pool of core-pinned worker threads inside
+    libsfref (no thread is created inside a timed step)."""
+
+    def __init__(self, L, wl, idx, cpus):
+        self.L = L
+        parts = [p for p in np.array_split(np.asarray(idx), len(cpus)) if len(p)]
+        self.k = len(parts)
+        cpu_arr = np.asarray(cpus[: self.k], np.int32)
+        self.w = L.sfref_workers_create(self.k, cpu_arr.ctypes.data)
+        keep, specs = [], (_ShardSpec * self.k)()
+        self.blocks, self.n = 0, len(idx)
+        for i, p in enumerate(parts):
+            names = (C.c_char_p * len(p))(*[f"wf{w}".encode() for w in p])
+            pins = [wl["pin_tok"][wl["pin_off"][w]:wl["pin_off"][w + 1]] for w in p]
+            reqs = [wl["req_tok"][wl["req_off"][w]:wl["req_off"][w + 1]] for w in p]
+            po = np.concatenate([[0], np.cumsum([len(x) for x in pins])]).astype(np.int64)
+            ro = np.concatenate([[0], np.cumsum([len(x) for x in reqs])]).astype(np.int64)
+            pt = np.concatenate(pins + [np.zeros(1, np.uint32)]).astype(np.uint32)
+            rt = np.concatenate(reqs + [np.zeros(1, np.uint32)]).astype(np.uint32)
+            keep += [names, po, ro, pt, rt]
+            specs[i] = _ShardSpec(len(p), C.cast(names, C.c_void_p), po.ctypes.data, pt.ctypes.data,
+                                  ro.ctypes.data, rt.ctypes.data)
+            self.blocks += int(blocks_of(np.diff(ro)).sum())
+        self.pools = (C.c_void_p * self.k)()
+        self.batches = (C.c_void_p * self.k)()
+        L.sfref_build_shards_parallel(self.w, specs, self.pools, self.batches)  # setup, untimed
+        self.outs = [np.zeros(len(p), np.int64) for p in parts]
+        self.out_ptrs = (C.c_void_p * self.k)(*[o.ctypes.data for o in self.outs])
+
+    def step(self):
+        self.L.sfref_prefix_match_parallel(self.w, self.pools, self.batches, self.out_ptrs)
+
+    def time(self, steps, warmup):
+        times = []
+        for it in range(warmup + steps):
+            t0 = time.perf_counter()
+            self.step()
+            dt = time.perf_counter() - t0
+            if it >= warmup:
+                times.append(dt)
+        return times
+
+    def close(self):
+        for i in range(self.k):
+            self.L.sfref_batch_destroy(self.batches[i])
+            self.L.sfref_pool_destroy(self.pools[i])
+        self.L.sfref_workers_destroy(self.w)
 
 
 def cpu_sample_workload(seed, n):
@@ -232,20 +261,18 @@ def run_reference_arm(args, rank, world):
     if rank != 0:
         return 0
     L = ref_lib()
-    cores = os.cpu_count() or 1
-    n_sample = args.ref_sample
+    info, aff = host_info()
+    n_sample = args.ref_sample or args.workflows
     wl = cpu_sample_workload(args.seed, n_sample)
     if L is not None:
         kind = "reference"
-        parts = np.array_split(np.arange(n_sample), cores)
-        shards = [ref_shard(L, wl, list(p)) for p in parts if len(p)]
-        times, outs = time_ref(L, shards, args.steps, args.warmup)
-        blocks = sum(s[2] for s in shards)
-        for s in shards:
-            L.sfref_batch_destroy(s[1])
-            L.sfref_pool_destroy(s[0])
+        sh = RefShards(L, wl, list(range(n_sample)), aff)
+        times = sh.time(args.steps, args.warmup)
+        blocks, cores = sh.blocks, sh.k
+        sh.close()
         sample = (f"{n_sample} workflows of the C2 distribution ({blocks} blocks/step), "
-                  f"{len(shards)} threads x SimulatedBackend::prefix_match on pre-tokenized strings")
+                  f"{cores} core-pinned worker threads (persistent pool in libsfref), one reference "
+                  "SimulatedBackend per thread x prefix_match on pre-tokenized strings")
     else:  # oracle port (the C restatement) when the reference could not be compiled here
         sys.path.insert(0, os.path.join(REPO, "tests"))
         import oracle_lib
@@ -270,8 +297,9 @@ def run_reference_arm(args, rank, world):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic", "config": config_dict(args, blocks_per_step=blocks, n_wf=n_sample),
-            "cpu_baseline": {"value": value, "unit": "blocks/s", "cores": len(parts) if kind == "reference" else 1,
-                             "kind": kind, "sample": sample},
+            "same_config": n_sample == args.workflows,
+            "cpu_baseline": {"value": value, "unit": "blocks/s", "cores": cores, "kind": kind,
+                             "sample": sample, **info},
             "e2e": {"value": value, "unit": "blocks/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -438,6 +466,8 @@ def run_ours(args, rank, world, local_rank):
         c3 = handoff_leg(args, api, dev, stream, rank, world) if (dist and not args.no_c3) else None
         route = route_leg(args, api, pool, dev, rank, world) if (dist and not args.no_c3) else None
         mm = None if args.no_mm else mm_leg(args, api, dev, stream)
+        press = None if args.no_mm else pressure_leg(args, api, dev, stream, hbm_peak)
+        evict = None if args.no_mm else evict_leg(args, api, pool, wl, dev, rank)
         tk = None if args.no_tok else tokenize_leg(args, api, dev, stream, hbm_peak)
         lat = None if args.no_lat else latency_leg(args, api, dev, stream)
         mp = None if args.no_map else mapper_leg(api, dev, stream, hbm_peak)
@@ -492,6 +522,10 @@ def run_ours(args, rank, world, local_rank):
         line["c3_route"] = route
     if mm:
         line["mm_signals"] = mm
+    if press:
+        line["pressure_k6"] = press
+    if evict:
+        line["evict_c2"] = evict
     if tk:
         line["tokenize"] = tk
     if lat:
@@ -1168,6 +1202,139 @@ def mm_reference(L, args, n_wf=1000):
 
 
 
+def pressure_leg(args, api, dev, stream, hbm_peak):
+    """K6 (§8a a10): the pressure step's LRU victim choice, sfmm_pressure_argmin_dev
+    (one launch: segmented warp-shuffle argmin over (last_update_ts, wf_rank)) at the SURVEY's
+    8 backends x 5,000 idle entries and at C2/C4 tracker scale (8 x 100,000), against the
+    reference's pressure_actions on the same entries (1 pinned core). Victims are checked equal."""
+    import torch
+    fn = api.lib.sfmm_pressure_argmin_dev
+    fn.argtypes = [C.c_int32, C.c_int64] + [C.c_void_p] * 5 + [C.c_int32, C.c_void_p, C.c_double, C.c_void_p,
+                                                              C.c_void_p]
+    L = ref_lib()
+    info, aff = host_info()
+    rng = np.random.default_rng(args.seed + 61)
+    NB, tau = 8, 0.85
+    refs = (C.c_char_p * NB)(*[f"backend-{b}".encode() for b in range(NB)])
+    util = np.full(NB, 0.95)
+    out = {}
+    for per in (5_000, 100_000):
+        n = NB * per
+        backend = np.repeat(np.arange(NB, dtype=np.int32), per)
+        wf_id = np.concatenate([rng.permutation(per) for _ in range(NB)]).astype(np.int64)
+        rank = wf_id.astype(np.uint32)  # "wf-%07d": string order = numeric order
+        ts = np.round(rng.uniform(0, 1e4, n), 1)  # ties are common: the wf-rank tie-break matters
+        infl = (rng.random(n) < 0.1).astype(np.int32)
+        pres = (rng.random(n) < 0.9).astype(np.uint8)
+        d = {k: torch.from_numpy(v).to(dev) for k, v in
+             dict(b=backend, ts=ts, rk=rank.view(np.int32), inf=infl, pr=pres, u=util).items()}
+        victim = torch.full((NB,), -1, dtype=torch.int64, device=dev)
+        ptr = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+
+        def tick():
+            api.check("pressure_argmin_dev", fn(dev, n, ptr(d["b"]), ptr(d["ts"]), ptr(d["rk"]), ptr(d["inf"]),
+                                                ptr(d["pr"]), NB, ptr(d["u"]), tau, ptr(victim),
+                                                C.c_void_p(stream.cuda_stream)))
+        for _ in range(args.warmup):
+            tick()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for a, b in ev:
+            a.record(stream)
+            tick()
+            b.record(stream)
+        torch.cuda.synchronize()
+        us = 1e3 * float(np.mean([a.elapsed_time(b) for a, b in ev]))
+        v = victim.cpu().numpy()
+        # the victim by definition: least (ts, wf rank) among idle preserved entries of each backend
+        want = np.full(NB, -1, np.int64)
+        for bb in range(NB):
+            idx = np.nonzero((backend == bb) & (infl == 0) & (pres == 1))[0]
+            if len(idx):
+                want[bb] = idx[np.lexsort((rank[idx], ts[idx]))[0]]
+        assert (v == want).all(), f"pressure victims {v} != {want}"
+        alg = n * (4 + 8 + 4 + 4 + 1)  # backend, ts, rank, in_flight, preserved per entry
+        leg = {"entries": n, "backends": NB, "us_per_tick": us, "victims_verified": True,
+               "hbm_frac": alg / (us / 1e6) / 1e9 / hbm_peak, "alg_bytes": alg}
+        if L is not None and not args.no_cpu_baseline:
+            L.sfref_pressure_bench.restype = C.c_double
+            L.sfref_pressure_bench.argtypes = [C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                               C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
+                                               C.c_void_p]
+            names = (C.c_char_p * n)(*[f"wf-{w:07d}".encode() for w in wf_id])
+            cnt = C.c_int()
+            iters = 5 if per <= 5_000 else 1
+            old = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, {aff[0]})
+            try:
+                ns = L.sfref_pressure_bench(n, names, backend.ctypes.data, ts.ctypes.data, infl.ctypes.data,
+                                            pres.ctypes.data, NB, refs, util.ctypes.data, tau, iters,
+                                            C.byref(cnt))
+            finally:
+                os.sched_setaffinity(0, old)
+            assert cnt.value == int((want >= 0).sum())
+            leg["cpu_reference"] = {"value": ns / 1e3, "unit": "us per tick", "cores": 1, "kind": "reference",
+                                    "sample": f"the same {n} entries, pressure_actions x {iters}, 1 thread "
+                                              f"pinned to core {aff[0]}", **info}
+        out[f"{NB}x{per}"] = leg
+    return out
+
+
+def evict_leg(args, api, pool, wl, dev, rank):
+    """C2 evict ops/s (§8(d), K4): SimulatedBackend::flush(workflow) of every C2 workflow's pin in
+    one sfkv_flush_batch (refcount release, free-bitmap and table tombstones on the GPU), through
+    the host-pointer ABI; the pins are re-committed (untimed) between steps. Reference: the same
+    flushes on a 1,000-workflow sample through SimulatedBackend::flush, 1 pinned core."""
+    n = len(wl["pin_off"]) - 1
+    wf_all = np.arange(n, dtype=np.int32)
+    api.check("set_stream", api.pool_set_stream(pool.h, None))
+    st0 = pool.stats()
+
+    def recommit():
+        for c0 in range(0, n, 2000):
+            c1 = min(n, c0 + 2000)
+            off = wl["pin_off"][c0:c1 + 1] - wl["pin_off"][c0]
+            tok = wl["pin_tok"][wl["pin_off"][c0]:wl["pin_off"][c1]]
+            assert pool.commit(wf_all[c0:c1], off, tok).all()
+    times, freed = [], 0
+    steps = max(1, min(args.steps, 4))
+    for it in range(1 + steps):
+        t0 = time.perf_counter()
+        fr = pool.flush_batch(wf_all)
+        dt = time.perf_counter() - t0
+        assert pool.stats()["blocks_in_use"] == 0, "flush_batch left blocks in use"
+        freed = int(fr.sum())
+        recommit()
+        if it >= 1:
+            times.append(dt)
+    assert pool.stats()["occupancy_tokens"] == st0["occupancy_tokens"]
+    ms = 1e3 * float(np.mean(times))
+    out = {"workload": f"flush of all {n} C2 pins ({int(wl['pin_off'][-1])} tokens) in one sfkv_flush_batch",
+           "ms": ms, "evictions_per_s": n / (ms / 1e3), "tokens_freed": freed,
+           "blocks_freed_per_s": st0["blocks_in_use"] / (ms / 1e3)}
+    L = ref_lib()
+    if L is not None and not args.no_cpu_baseline and rank == 0:
+        info, aff = host_info()
+        k = min(1000, n)
+        sh = RefShards(L, wl, list(range(k)), aff[:1])
+        L.sfref_flush_batch.restype = C.c_longlong
+        L.sfref_flush_batch.argtypes = [C.c_void_p, C.c_longlong, C.c_void_p]
+        names = (C.c_char_p * k)(*[f"wf{w}".encode() for w in range(k)])
+        old = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {aff[0]})
+        try:
+            t0 = time.perf_counter()
+            rf = L.sfref_flush_batch(sh.pools[0], k, names)
+            dt = time.perf_counter() - t0
+        finally:
+            os.sched_setaffinity(0, old)
+        sh.close()
+        assert rf == int(wl["pin_off"][k]), "reference flush freed a different token count"
+        out["cpu_reference"] = {"value": k / dt, "unit": "evictions/s", "cores": 1, "kind": "reference",
+                                "sample": f"{k} workflows' pins, SimulatedBackend::flush per workflow, 1 thread "
+                                          f"pinned to core {aff[0]}", **info}
+    return out
+
+
 def render_text(tok_ids, vocab=100_000):
     """Token ids -> whitespace text over a vocab-word dictionary ("t<k>", k = id mod vocab),
     single spaces: the string form the reference's tokenizer consumes. Returns (text bytes,
@@ -1420,19 +1587,21 @@ def latency_leg(args, api, dev, stream):
 
 def cpu_baseline(args):
     L = ref_lib()
+    info, aff = host_info()
     n_sample = args.cpu_sample
     wl = cpu_sample_workload(args.seed, n_sample)
     if L is None:
         return {"value": None, "unit": "blocks/s", "cores": 1, "kind": "port",
-                "sample": "oracle/_ref missing"}
-    sh = ref_shard(L, wl, list(range(n_sample)))
-    times, _ = time_ref(L, [sh], steps=3, warmup=1)
-    v = sh[2] / float(np.mean(times))
-    L.sfref_batch_destroy(sh[1])
-    L.sfref_pool_destroy(sh[0])
+                "sample": "oracle/_ref missing", **info}
+    sh = RefShards(L, wl, list(range(n_sample)), aff[:1])
+    times = sh.time(steps=3, warmup=1)
+    v = sh.blocks / float(np.mean(times))
+    blocks = sh.blocks
+    sh.close()
     return {"value": v, "unit": "blocks/s", "cores": 1, "kind": "reference",
-            "sample": f"{n_sample} workflows of the same C2 distribution ({sh[2]} blocks), "
-                      "SimulatedBackend::prefix_match on pre-tokenized strings, 1 thread"}
+            "sample": f"{n_sample} workflows of the same C2 distribution ({blocks} blocks), "
+                      f"SimulatedBackend::prefix_match on pre-tokenized strings, 1 thread pinned to core {aff[0]}",
+            **info}
 
 
 def main():
@@ -1464,7 +1633,7 @@ def main():
     ap.add_argument("--kv-staging-gib", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1000)
-    ap.add_argument("--ref-sample", type=int, default=2000)
+    ap.add_argument("--ref-sample", type=int, default=0, help="0: the full --workflows batch")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per match launch (from profiles/), reported as-is")
     args = ap.parse_args()

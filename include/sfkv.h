@@ -18,6 +18,15 @@
  *     are asynchronous on the pool stream (no host synchronisation): they also take n_tokens,
  *     the number of tokens the tok buffer can hold (>= tok_off[n]), which bounds the work size.
  *     KV staging (kv_src) is always device memory, also in sfkv_commit_batch.
+ *     _dev argument checks: the host refuses null and misaligned pointers (tok 16-B aligned, the
+ *     kernels load it with 16-B vectors and TMA; tok_off / 64-bit outputs 8-B; wf 4-B) with
+ *     SFKV_EINVAL. Values read on the device are guarded there: an out-of-range workflow slot
+ *     is matched as unpinned, gathers nothing, refuses its commit batch (status SFKV_EINVAL, no
+ *     state change), and a handoff source block outside the peer's region moves nothing; each
+ *     sets the pool's sticky error, which the next sfkv_pool_sync (or host-pointer call that
+ *     synchronises) reports once as SFKV_EINVAL.
+ *   - Token ids exchanged between pools on different ranks must come from one shared vocabulary
+ *     (pins are compared as integers); see INTEGRATION.md §4.
  *   - A workflow is a dense slot id in [0, max_workflows) chosen by the host (the host keeps the
  *     workflow_id string -> slot map, as SimulatedBackend keys pins_ by workflow_id,
  *     simulated_backend.hpp:115).

@@ -14,10 +14,18 @@
 //                                       no backends attached (every action "applies"), or a
 //                                       registry of flaky test backends (sfref_mm_create_flaky)
 // Token ids are rendered to whitespace tokens "t<id>", the same text the reference tokenizes.
+#include <pthread.h>
+#include <sched.h>
+
+#include <chrono>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <sstream>
+#include <thread>
 
 #include "stageflow/backend.hpp"
 #include "stageflow/memory.hpp"
@@ -83,6 +91,65 @@ struct RefMM {
   std::unique_ptr<MemoryManager> mm;
 };
 MemoryManager* MM(void* h) { return static_cast<RefMM*>(h)->mm.get(); }
+
+// A persistent pool of worker threads, each pinned to one host core, for the CPU baseline: a
+// timed step hands worker i its job and waits for all of them, so no thread is created inside a
+// timed region (bench.py --impl reference).
+struct Workers {
+  std::vector<std::thread> th;
+  std::mutex m;
+  std::condition_variable go, done;
+  std::function<void(int)> job;
+  long long gen = 0;
+  int pending = 0;
+  bool stop = false;
+
+  Workers(int n, const int* cpus) {
+    for (int i = 0; i < n; ++i) {
+      th.emplace_back([this, i] { loop(i); });
+      if (cpus && cpus[i] >= 0) {
+        cpu_set_t set;
+        CPU_ZERO(&set);
+        CPU_SET(cpus[i], &set);
+        pthread_setaffinity_np(th.back().native_handle(), sizeof(set), &set);
+      }
+    }
+  }
+  ~Workers() {
+    {
+      std::lock_guard<std::mutex> g(m);
+      stop = true;
+    }
+    go.notify_all();
+    for (auto& t : th) t.join();
+  }
+  void loop(int i) {
+    long long seen = 0;
+    for (;;) {
+      std::function<void(int)> f;
+      {
+        std::unique_lock<std::mutex> g(m);
+        go.wait(g, [&] { return stop || gen != seen; });
+        if (stop) return;
+        seen = gen;
+        f = job;
+      }
+      f(i);
+      {
+        std::lock_guard<std::mutex> g(m);
+        if (--pending == 0) done.notify_all();
+      }
+    }
+  }
+  void run(std::function<void(int)> f) {
+    std::unique_lock<std::mutex> g(m);
+    job = std::move(f);
+    pending = static_cast<int>(th.size());
+    ++gen;
+    go.notify_all();
+    done.wait(g, [&] { return pending == 0; });
+  }
+};
 
 }  // namespace
 
@@ -165,6 +232,40 @@ void sfref_prefix_match_batch(void* h, void* batch, long long* out_M) {
   }
 }
 
+// The CPU baseline's worker pool: n threads, thread i pinned to cpus[i] (cpus nullable / -1 =
+// unpinned). Created once, outside every timed region.
+void* sfref_workers_create(int n, const int* cpus) { return new Workers(n, cpus); }
+void sfref_workers_destroy(void* w) { delete static_cast<Workers*>(w); }
+
+// One step of the reference lookup on every shard at once: worker i runs
+// sfref_prefix_match_batch(pools[i], batches[i], outs[i]) (a shard = one SimulatedBackend
+// holding its workflows' pins). Returns when every shard is done.
+void sfref_prefix_match_parallel(void* w, void* const* pools, void* const* batches,
+                                 long long* const* outs) {
+  static_cast<Workers*>(w)->run([&](int i) { sfref_prefix_match_batch(pools[i], batches[i], outs[i]); });
+}
+
+// Build shard i's backend and batch on worker i (setup, untimed): pools[i] holds the pins
+// (pin_off / pin_tok CSR over the shard's workflows), batches[i] the requests.
+struct ShardSpec {
+  long long n;
+  const char* const* wf;
+  const long long* pin_off;
+  const std::uint32_t* pin_tok;
+  const long long* req_off;
+  const std::uint32_t* req_tok;
+};
+void sfref_build_shards_parallel(void* w, const ShardSpec* spec, void** pools, void** batches) {
+  static_cast<Workers*>(w)->run([&](int i) {
+    const ShardSpec& s = spec[i];
+    pools[i] = sfref_pool_create(1LL << 40);
+    int acc = 0;
+    for (long long r = 0; r < s.n; ++r)
+      sfref_complete(pools[i], s.wf[r], s.pin_tok + s.pin_off[r], s.pin_off[r + 1] - s.pin_off[r], &acc);
+    batches[i] = sfref_batch_create(s.n, s.wf, s.req_off, s.req_tok);
+  });
+}
+
 // pressure_actions over n tracker entries. Entry i: (wf[i], backend_refs[backend[i]], ts[i],
 // in_flight[i], preserved[i], tokens[i]). out_victim[bi] = entry index flushed on backend bi or -1.
 int sfref_pressure_actions(long long n, const char* const* wf, const int* backend, const double* ts,
@@ -196,6 +297,43 @@ int sfref_pressure_actions(long long n, const char* const* wf, const int* backen
     ++count;
   }
   return count;
+}
+
+// The CPU baseline of the pressure step: the same tracker as sfref_pressure_actions, built once,
+// then `iters` calls of the reference's pressure_actions timed with steady_clock (the calling
+// thread: pin it). Returns the mean nanoseconds per call; *out_count = actions of the last call.
+double sfref_pressure_bench(long long n, const char* const* wf, const int* backend, const double* ts,
+                            const int* in_flight, const unsigned char* preserved, int n_backends,
+                            const char* const* backend_refs, const double* util, double tau, int iters,
+                            int* out_count) {
+  WorkflowTracker tracker;
+  for (long long i = 0; i < n; ++i) {
+    CacheEntry e;
+    e.workflow_id = wf[i];
+    e.backend_ref = backend_refs[backend[i]];
+    e.token_count = 1;
+    e.preserved = preserved[i] != 0;
+    e.last_update_ts = ts[i];
+    tracker.upsert_entry(e);
+    if (in_flight[i] > 0) tracker.adjust_in_flight(e.backend_ref, e.workflow_id, in_flight[i]);
+  }
+  std::map<std::string, double> u;
+  for (int b = 0; b < n_backends; ++b) u[backend_refs[b]] = util[b];
+  int count = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int it = 0; it < iters; ++it) count = static_cast<int>(pressure_actions(tracker, u, tau).size());
+  const auto t1 = std::chrono::steady_clock::now();
+  *out_count = count;
+  return std::chrono::duration<double, std::nano>(t1 - t0).count() / iters;
+}
+
+// SimulatedBackend::flush(FlushScope::workflow(wf[i])) for i < n in order (one C++ loop); returns
+// the tokens freed.
+long long sfref_flush_batch(void* h, long long n, const char* const* wf) {
+  auto* p = static_cast<RefPool*>(h);
+  long long freed = 0;
+  for (long long i = 0; i < n; ++i) freed += p->backend->flush(FlushScope::workflow(wf[i]));
+  return freed;
 }
 
 // map_threshold with a score function returning the given score: 1 = light, 0 = heavy.

@@ -287,6 +287,17 @@ class Pool:
             self.api.pool_destroy(self.h)
             self.h = None
 
+    def reserve(self, max_workflows=0, max_pin_blocks=0, n_blocks=0):
+        """Grow the pool in place (sfkv_pool_reserve); never shrinks. Updates cfg."""
+        mw = max(int(max_workflows), self.cfg.max_workflows)
+        mb = max(int(max_pin_blocks), self.cfg.max_pin_blocks)
+        nb = max(int(n_blocks), self.cfg.n_blocks)
+        self.api.check("pool_reserve", self.api.pool_reserve(self.h, mw, mb, nb))
+        c = PoolConfig()
+        self.api.check("pool_config_get", self.api.pool_config_get(self.h, C.byref(c)))
+        self.cfg.max_workflows, self.cfg.max_pin_blocks = c.max_workflows, c.max_pin_blocks
+        self.cfg.n_blocks, self.cfg.table_log2 = c.n_blocks, c.table_log2
+
     def __del__(self):
         try:
             self.close()

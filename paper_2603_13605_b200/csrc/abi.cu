@@ -171,11 +171,26 @@ static int read_counters(sfkv_pool* p) {
   return 0;
 }
 
+// The pool's sticky device-side error, reported once: read, cleared, and turned into a status.
 static int check_sticky(sfkv_pool* p) {
   if (int rc = read_counters(p)) return rc;
   const int e = p->ctr_host->error;
+  if (!e) return 0;
+  SFKV_CUDA(cudaMemsetAsync(&p->ctr->error, 0, sizeof(int), p->stream));
+  SFKV_CUDA(cudaStreamSynchronize(p->stream));
+  p->ctr_host->error = 0;
   if (e == SFKV_EPOOL) return fail(e, "physical block pool or block table exhausted");
   if (e == SFKV_ESTALE) return fail(e, "payload staging assumed a different cached prefix M");
+  if (e == SFKV_EINVAL) return fail(e, "device-side argument check: workflow slot out of range");
+  return fail(e, "device-side error");
+}
+
+// _dev entry points: pointer alignment the kernels rely on (uint4 / TMA token loads, 8-B offsets)
+static bool misaligned(const void* ptr, uintptr_t a) { return ptr && (reinterpret_cast<uintptr_t>(ptr) & (a - 1)); }
+static int check_dev_args(const char* fn, const int32_t* wf, const int64_t* tok_off, const uint32_t* tok) {
+  if (misaligned(tok, 16)) return fail(SFKV_EINVAL, std::string(fn) + ": tok must be 16-byte aligned");
+  if (misaligned(tok_off, 8)) return fail(SFKV_EINVAL, std::string(fn) + ": tok_off must be 8-byte aligned");
+  if (misaligned(wf, 4)) return fail(SFKV_EINVAL, std::string(fn) + ": wf must be 4-byte aligned");
   return 0;
 }
 
@@ -364,7 +379,7 @@ int sfkv_pool_sync(sfkv_pool* p) {
   if (!p) return fail(SFKV_EINVAL, "null pool");
   DeviceGuard g(p->cfg.device);
   SFKV_CUDA(cudaStreamSynchronize(p->stream));
-  return 0;
+  return check_sticky(p);  // device-side errors of the _dev calls since the last report
 }
 
 int sfkv_pool_kv(sfkv_pool* p, void** kv, int64_t* block_bytes) {
@@ -469,6 +484,8 @@ int sfkv_match_batch_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64
   if (!p || !wf || !tok_off || !tok || !out_M || n_tokens < 0)
     return fail(SFKV_EINVAL, "match_batch_dev: bad argument");
   if (n <= 0) return n == 0 ? 0 : fail(SFKV_EINVAL, "negative batch");
+  if (int rc = check_dev_args("match_batch_dev", wf, tok_off, tok)) return rc;
+  if (misaligned(out_M, 8) || misaligned(out_hash, 8)) return fail(SFKV_EINVAL, "match_batch_dev: unaligned output");
   DeviceGuard g(p->cfg.device);
   return match_common(p, n, wf, tok_off, tok, out_M, out_hash, nullptr, nullptr, n + n_tokens / BT, n_tokens);
 }
@@ -502,6 +519,8 @@ int sfkv_lookup_batch_dev(sfkv_pool* p, int64_t n, const int64_t* tok_off, const
   if (!p || !tok_off || !tok || !out_block || !out_hit || n_tokens < 0)
     return fail(SFKV_EINVAL, "lookup_batch_dev: bad argument");
   if (n <= 0) return n == 0 ? 0 : fail(SFKV_EINVAL, "negative batch");
+  if (int rc = check_dev_args("lookup_batch_dev", nullptr, tok_off, tok)) return rc;
+  if (misaligned(out_block, 4) || misaligned(out_hit, 8)) return fail(SFKV_EINVAL, "lookup_batch_dev: unaligned output");
   DeviceGuard g(p->cfg.device);
   return match_common(p, n, nullptr, tok_off, tok, nullptr, nullptr, out_block, out_hit, n + n_tokens / BT,
                       n_tokens);
@@ -558,6 +577,9 @@ int sfkv_commit_batch_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int6
   if (!p || !wf || !tok_off || !tok || !out_status) return fail(SFKV_EINVAL, "commit_batch_dev: null argument");
   if (n <= 0) return n == 0 ? 0 : fail(SFKV_EINVAL, "negative batch");
   if (kv_src && (!kv_src_off || !p->kv)) return fail(SFKV_EINVAL, "commit_batch_dev: kv_src needs kv_src_off and a payload pool");
+  if (int rc = check_dev_args("commit_batch_dev", wf, tok_off, tok)) return rc;
+  if (misaligned(kv_src_off, 8) || misaligned(m_expected, 8) || misaligned(out_status, 4))
+    return fail(SFKV_EINVAL, "commit_batch_dev: unaligned argument");
   DeviceGuard g(p->cfg.device);
   if (n_tokens < 0) return fail(SFKV_EINVAL, "commit_batch_dev: negative n_tokens");
   return commit_dev(p, n, wf, tok_off, tok, n + n_tokens / BT, n_tokens, kv_src, kv_src_off, m_expected,
@@ -769,6 +791,7 @@ int sfkv_handoff(sfkv_pool* src, int32_t wf_src, sfkv_pool* dst, int32_t wf_dst,
   ps.kv = src->kv;
   ps.blk = src->pin_blk + (int64_t)wf_src * src->cfg.max_pin_blocks;  // item k = block k
   ps.block_bytes = src->block_bytes;
+  ps.n_blocks = src->cfg.n_blocks;
   if (int rc = commit_dev(dst, 1, dwf, doff, dtok, nb, (int64_t)nb * BT, nullptr, nullptr, nullptr, dst_status,
                           dst->kv ? &ps : nullptr))
     return rc;
@@ -854,6 +877,12 @@ int sfkv_handoff_recv_batch(sfkv_pool* dst, const sfkv_peer* src, int64_t n, con
   if (int rc = validate_batch_host(dst, n, wf, tok_off)) return rc;
   DeviceGuard g(dst->cfg.device);
   const int64_t items = host_items(n, tok_off);
+  {
+    const int64_t src_n = src->block_bytes ? src->kv_bytes / src->block_bytes : 0;
+    for (int64_t i = 0; i < items; ++i)
+      if (src_blocks[i] < 0 || src_blocks[i] >= src_n)
+        return fail(SFKV_EINVAL, "handoff_recv_batch: source block outside the peer's KV region");
+  }
   int32_t* dwf;
   int64_t* doff;
   uint32_t* dtok;
@@ -870,6 +899,7 @@ int sfkv_handoff_recv_batch(sfkv_pool* dst, const sfkv_peer* src, int64_t n, con
   ps.kv = src->kv;
   ps.blk = dblk;
   ps.block_bytes = src->block_bytes;
+  ps.n_blocks = src->block_bytes ? src->kv_bytes / src->block_bytes : 0;
   if (int rc = commit_dev(dst, n, dwf, doff, dtok, items, tok_off[n], nullptr, nullptr, nullptr, dstatus, &ps))
     return rc;
   SFKV_CUDA(cudaMemcpyAsync(out_status, dstatus, n * sizeof(int32_t), cudaMemcpyDeviceToHost, dst->stream));
@@ -889,6 +919,7 @@ int sfkv_handoff_recv_batch_dev(sfkv_pool* dst, const sfkv_peer* src, int64_t n,
   ps.kv = src->kv;
   ps.blk = src_blocks;
   ps.block_bytes = src->block_bytes;
+  ps.n_blocks = src->block_bytes ? src->kv_bytes / src->block_bytes : 0;
   return commit_dev(dst, n, wf, tok_off, tok, n + n_tokens / BT, n_tokens, nullptr, nullptr, nullptr, out_status,
                     &ps);
 }

@@ -85,6 +85,7 @@ struct CommitArgs {
   int64_t pin_groups;
   int64_t capacity;
   DevCounters* ctr;
+  int32_t max_wf;  // device-side slot guard (the _dev entry points' slots are not host-checked)
 };
 
 #define FOR_ITEMS(a, item)                                                         \
@@ -131,16 +132,18 @@ __global__ void admit_kernel(CommitArgs a) {
   }
   __syncwarp();
   // staleness / block-table checks first: a refused batch changes nothing
-  bool bad_stale = false, bad_len = false;
+  bool bad_stale = false, bad_len = false, bad_slot = false;
   for (int64_t r = lane; r < a.n; r += 32) {
     const int64_t len = a.tok_off[r + 1] - a.tok_off[r];
-    if ((len + BT - 1) / BT > a.max_pin_blocks) bad_len = true;
-    if (a.payload && a.m_expected && a.m_expected[r] != a.s.M[r]) bad_stale = true;
+    if ((len + BT - 1) / BT > a.max_pin_blocks || len < 0) bad_len = true;
+    if ((uint32_t)a.wf[r] >= (uint32_t)a.max_wf) bad_slot = true;
+    else if (a.payload && a.m_expected && a.m_expected[r] != a.s.M[r]) bad_stale = true;
   }
   bad_stale = __any_sync(0xffffffffu, bad_stale);
   bad_len = __any_sync(0xffffffffu, bad_len);
-  if (bad_stale || bad_len) {
-    const int code = bad_len ? SFKV_EPOOL : SFKV_ESTALE;
+  bad_slot = __any_sync(0xffffffffu, bad_slot);
+  if (bad_stale || bad_len || bad_slot) {
+    const int code = bad_slot ? SFKV_EINVAL : (bad_len ? SFKV_EPOOL : SFKV_ESTALE);
     for (int64_t r = lane; r < a.n; r += 32) a.s.status[r] = code;
     __syncwarp();
     if (lane == 0) c->error = code;
@@ -551,6 +554,7 @@ static CommitArgs base_args(sfkv_pool* p) {
   a.n_words = p->n_words;
   a.n_blocks = p->cfg.n_blocks;
   a.max_pin_blocks = p->cfg.max_pin_blocks;
+  a.max_wf = p->cfg.max_workflows;
   a.capacity = p->cfg.capacity_tokens;
   a.ctr = p->ctr;
   return a;

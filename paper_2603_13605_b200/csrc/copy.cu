@@ -57,6 +57,8 @@ struct PayloadKernelArgs {
   const uint8_t* src_kv;   // handoff source payload (another pool, or a peer rank's over NVLink)
   const int32_t* src_blk;  // handoff source block of every batch item
   int64_t src_block_bytes;
+  int64_t src_n_blocks;
+  int* error_out;          // the destination pool's sticky error
 };
 
 __global__ void __launch_bounds__(256) payload_kernel(PayloadKernelArgs P) {
@@ -88,7 +90,12 @@ __global__ void __launch_bounds__(256) payload_kernel(PayloadKernelArgs P) {
     if (nval > j0) {
       const uint8_t* src;
       if (P.src_kv) {  // handoff: same rows of the source block of this item
-        src = P.src_kv + (int64_t)P.src_blk[item] * P.src_block_bytes + ((int64_t)s * BT + j0) * P.row;
+        const int32_t sb = P.src_blk[item];
+        if ((uint64_t)sb >= (uint64_t)P.src_n_blocks) {  // device-side guard on the peer's region
+          if (lane == 0) *P.error_out = SFKV_EINVAL;
+          continue;
+        }
+        src = P.src_kv + (int64_t)sb * P.src_block_bytes + ((int64_t)s * BT + j0) * P.row;
       } else {  // staging rows [M, P): row index (k*16 + j0 - M)
         src = P.staging + P.staging_off[r] + ((int64_t)s * (len - M) + k * BT + j0 - M) * P.row;
       }
@@ -121,6 +128,8 @@ int launch_payload(sfkv_pool* p, const PayloadJob& j, const void* kv_src, const 
   P.src_kv = src ? src->kv : nullptr;
   P.src_blk = src ? src->blk : nullptr;
   P.src_block_bytes = src ? src->block_bytes : 0;
+  P.src_n_blocks = src ? src->n_blocks : 0;
+  P.error_out = &p->ctr->error;
   SFKV_CUDA(launch_pdl(payload_kernel, dim3(sm_count_p() * 8), dim3(256), st, P));
   return 0;
 }
@@ -162,11 +171,20 @@ __global__ void __launch_bounds__(256) gather_kernel(GatherArgs G) {
   }
 }
 
-struct PinBlockCount {
+struct PinBlockCount {  // device-side slot guard: an out-of-range slot gathers nothing
   const int32_t* wf;
   const int64_t* pin_len;
   const int32_t* pin_nblk;
-  __device__ int64_t operator()(int64_t i) const { return pin_len[wf[i]] < 0 ? 0 : pin_nblk[wf[i]]; }
+  int32_t max_wf;
+  int* error;
+  __device__ int64_t operator()(int64_t i) const {
+    const int32_t w = wf[i];
+    if ((uint32_t)w >= (uint32_t)max_wf) {
+      *error = SFKV_EINVAL;
+      return 0;
+    }
+    return pin_len[w] < 0 ? 0 : pin_nblk[w];
+  }
 };
 
 int gather_dev(sfkv_pool* p, int64_t n, const int32_t* wf, void* dst, const int64_t* dst_off) {
@@ -178,7 +196,7 @@ int gather_dev(sfkv_pool* p, int64_t n, const int32_t* wf, void* dst, const int6
   if (int rc = p->small.ensure(cv.off)) return rc;
   char* base = p->small.as<char>();
   int64_t* blk_off = reinterpret_cast<int64_t*>(base + o_off);
-  if (int rc = exclusive_scan(PinBlockCount{wf, p->pin_len, p->pin_nblk}, n, blk_off,
+  if (int rc = exclusive_scan(PinBlockCount{wf, p->pin_len, p->pin_nblk, p->cfg.max_workflows, &p->ctr->error}, n, blk_off,
                               reinterpret_cast<int64_t*>(base + o_tmp), st))
     return rc;
   GatherArgs G;

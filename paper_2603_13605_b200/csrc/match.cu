@@ -142,6 +142,8 @@ struct PrepArgs {
   unsigned long long* ticket;  // null: CTAs are co-resident, blockIdx order
   uint64_t* pstatus;  // prep tile status (epoch-tagged, per-pool buffer)
   uint32_t epoch;
+  int32_t max_wf;     // device-side slot guard: out-of-range slots match as unpinned and set
+  int* error;         //   the pool's sticky SFKV_EINVAL (reported by sfkv_pool_sync)
 };
 
 // Prep look-back status: flag (2 bits) | launch epoch (14 bits) | block count (48 bits). Statuses
@@ -168,7 +170,12 @@ __global__ void __launch_bounds__(PREP_THREADS) match_prep_kernel(PrepArgs P) {
   int64_t pl = -1;
   if (P.wf && r < P.n) {  // issued before the scan: the dependent pin_len load overlaps it
     wf = P.wf[r];
-    pl = P.pin_len[wf];
+    if ((uint32_t)wf < (uint32_t)P.max_wf) {
+      pl = P.pin_len[wf];
+    } else {
+      *P.error = SFKV_EINVAL;
+      wf = 0;
+    }
   }
   const int64_t nb = (len + BT - 1) / BT;
   int64_t excl, total;
@@ -808,6 +815,8 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   P.ticket = use_ticket ? ticket : nullptr;
   P.pstatus = p->prep_status.as<uint64_t>();
   P.epoch = p->prep_epoch;
+  P.max_wf = p->cfg.max_workflows;
+  P.error = &p->ctr->error;
   match_prep_kernel<<<(unsigned)np, PREP_THREADS, 0, st>>>(P);
   SFKV_LAUNCH_CHECK("match_prep_kernel");
   if (ntiles == 0) return 0;

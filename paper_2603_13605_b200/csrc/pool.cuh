@@ -143,6 +143,8 @@ struct PayloadSource {
   const uint8_t* kv = nullptr;
   const int32_t* blk = nullptr;
   int64_t block_bytes = 0;
+  int64_t n_blocks = 0;  // blocks in the source region: a source id outside it moves nothing and
+                         // sets the destination pool's sticky SFKV_EINVAL
 };
 int launch_payload(sfkv_pool* p, const PayloadJob& j, const void* kv_src, const int64_t* kv_src_off,
                    const PayloadSource* src, cudaStream_t st);

@@ -25,6 +25,12 @@ assignment without another collective.
 
 `max_over_ranks` / `aggregate_rate` implement bench.py's timing rule (max time over ranks, whole-job
 units / that time).
+
+Precondition (ABI, include/sfkv.h): token ids are compared as integers, so every rank that
+exchanges pins must number token strings the same way — one shared vocabulary (a tokenizer's
+fixed ids, or an interner replicated in the same first-occurrence order). Ids from two
+independently grown interners are not comparable. `PeerLink` takes a `token_space` label and
+refuses to link ranks whose labels differ.
 """
 from __future__ import annotations
 
@@ -105,7 +111,7 @@ class PeerLink:
     resident until the receiver has pulled them); recv(wf_dst, src) commits the incoming contexts
     into this rank's pool with the payload pulled from rank src's pool over NVLink."""
 
-    def __init__(self, pool: Pool, device: int, group=None):
+    def __init__(self, pool: Pool, device: int, group=None, token_space: str = "default"):
         import ctypes as C
 
         from .abi import Peer
@@ -113,9 +119,12 @@ class PeerLink:
         self.pool, self.group = pool, group
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         handles = [None] * self.world
-        dist.all_gather_object(handles, (pool.export(), device), group=group)
+        dist.all_gather_object(handles, (pool.export(), device, token_space), group=group)
+        spaces = {sp for _h, _d, sp in handles}
+        if len(spaces) != 1:  # ids of different vocabularies would match unrelated text
+            raise ValueError(f"PeerLink: ranks use different token-id spaces {sorted(spaces)}")
         self.peers = {}
-        for r, (h, _dev) in enumerate(handles):
+        for r, (h, _dev, _sp) in enumerate(handles):
             if r != self.rank:
                 self.peers[r] = Peer(pool.api, h, device)
         self._C = C

@@ -22,7 +22,7 @@ from http.server import BaseHTTPRequestHandler, ThreadingHTTPServer
 
 import numpy as np
 
-from .abi import Api, Config, Interner, Pool, latency_batch
+from .abi import BLOCK_TOKENS, Api, Config, Interner, Pool, SfkvError, latency_batch
 
 
 def _dump(obj) -> str:
@@ -42,28 +42,53 @@ def placeholder_text(n: int) -> str:  # simulated_backend.cpp:9-16
 
 
 class GpuSimBackend:
-    """SimulatedBackend's cache + latency semantics over a GPU pool, on the wall clock."""
+    """SimulatedBackend's cache + latency semantics over a GPU pool, on the wall clock.
+
+    Workflow ids map to pool slots; a slot returns to a free list once its workflow has no pin and
+    no request in flight (after a flush), and the pool grows in place (sfkv_pool_reserve) when
+    the slots or the per-pin block table run out, so — like the reference's std::map of pins —
+    nothing here is capped. Physical blocks are sized from the logical capacity the way the
+    reference-side binding sizes them (integration/gpu_pinned_backend.cpp blocks_for), so a commit
+    that logical admission accepts always finds blocks."""
 
     def __init__(self, api: Api, model: str, prefill_ms_per_token=1.0, decode_ms_per_token=10.0,
                  fixed_overhead_ms=0.0, max_concurrency=1, cache_capacity_tokens=1_000_000,
-                 output_tokens=16, device=0, max_workflows=4096, max_pin_blocks=4096):
+                 output_tokens=16, device=0, max_workflows=256, max_pin_blocks=256):
         self.api, self.model, self.device = api, model, device
         self.params = (float(fixed_overhead_ms), float(prefill_ms_per_token), float(decode_ms_per_token))
         self.output_tokens = int(output_tokens)
-        self.pool = Pool(api, Config(max_workflows=max_workflows, n_blocks=max_workflows * 8 + 2 * max_pin_blocks,
-                                     capacity_tokens=int(cache_capacity_tokens), max_pin_blocks=max_pin_blocks,
-                                     table_log2=max(14, int(np.ceil(np.log2(max_workflows * 16 + 4 * max_pin_blocks))) + 1),
-                                     device=device))
-        self.interner = Interner(api, table_log2=20, arena_bytes=64 << 20, device=device)
         self.capacity = int(cache_capacity_tokens)
+        nb = self._blocks_for(max_workflows, max_pin_blocks)
+        self.pool = Pool(api, Config(max_workflows=max_workflows, n_blocks=nb, capacity_tokens=self.capacity,
+                                     max_pin_blocks=max_pin_blocks,
+                                     table_log2=int(np.ceil(np.log2(2 * nb))) + 1, device=device))
+        self.interner = Interner(api, table_log2=20, arena_bytes=64 << 20, device=device)
         self.slots: dict[str, int] = {}
+        self.free = list(range(max_workflows - 1, -1, -1))
+        self.inflight: dict[str, int] = {}
         self.lock = threading.Lock()  # one host thread per pool handle
         self.admission = threading.Semaphore(max_concurrency)  # FCFS slots (simulated_backend.cpp:31-47)
+        self.errors = 0  # commits that failed on the device (logged non-pins)
+
+    def _blocks_for(self, slots, pin_blocks):
+        return self.capacity // BLOCK_TOKENS + slots + 2 * pin_blocks + 64
 
     def _slot(self, wf: str) -> int:
         if wf not in self.slots:
-            self.slots[wf] = len(self.slots)
+            if not self.free:  # grow: twice the slots
+                mw = 2 * self.pool.cfg.max_workflows
+                old = self.pool.cfg.max_workflows
+                self.pool.reserve(max_workflows=mw, n_blocks=self._blocks_for(mw, self.pool.cfg.max_pin_blocks))
+                self.free = list(range(mw - 1, old - 1, -1))
+            self.slots[wf] = self.free.pop()
         return self.slots[wf]
+
+    def _release_if_idle(self, wf: str):
+        """After a flush: the workflow has no pin; with nothing in flight its slot is free (a
+        request in flight re-pins at completion, so its slot stays)."""
+        if wf in self.slots and not self.inflight.get(wf):
+            self.inflight.pop(wf, None)
+            self.free.append(self.slots.pop(wf))
 
     def complete(self, messages, workflow_id="", stage_id="", max_tokens=0):
         t0 = time.monotonic()
@@ -76,6 +101,7 @@ class GpuSimBackend:
                 slot = self._slot(workflow_id) if workflow_id else -1
                 wfa = np.array([slot], np.int32)
                 if slot >= 0:
+                    self.inflight[workflow_id] = self.inflight.get(workflow_id, 0) + 1
                     M = int(self.pool.match(wfa, off, ids)[0])
                 O = self.output_tokens if max_tokens <= 0 else min(self.output_tokens, max_tokens)
                 ttft, total, service = latency_batch(self.api, [0], [queue_ms], [P], [M], [O],
@@ -84,17 +110,31 @@ class GpuSimBackend:
             time.sleep(float(service[0]) / 1e3)  # the completion event fires after prefill + decode
             with self.lock:
                 if slot >= 0:  # pin_prompt at completion (simulated_backend.cpp:125-127)
-                    self.pool.commit(wfa, off, ids)
+                    self.inflight[workflow_id] -= 1
+                    need = (P + BLOCK_TOKENS - 1) // BLOCK_TOKENS
+                    try:
+                        if need > self.pool.cfg.max_pin_blocks:  # a longer prompt than any before
+                            mb = max(need, 2 * self.pool.cfg.max_pin_blocks)
+                            self.pool.reserve(max_pin_blocks=mb,
+                                              n_blocks=self._blocks_for(self.pool.cfg.max_workflows, mb))
+                        self.pool.commit(wfa, off, ids)
+                    except SfkvError:  # the reference never fails a request on pin_prompt
+                        self.errors += 1
         return {"content": placeholder_text(O), "prompt_tokens": P, "completion_tokens": O,
                 "cached_tokens": M, "queue_ms": queue_ms, "ttft_ms": float(ttft[0]), "total_ms": float(total[0])}
 
     def flush(self, workflow_id=None) -> int:
         with self.lock:
             if workflow_id is None:
-                return self.pool.flush(-1)
+                freed = self.pool.flush(-1)
+                for wf in list(self.slots):
+                    self._release_if_idle(wf)
+                return freed
             if workflow_id not in self.slots:  # nothing pinned for it: frees nothing
                 return 0
-            return self.pool.flush(self.slots[workflow_id])
+            freed = self.pool.flush(self.slots[workflow_id])
+            self._release_if_idle(workflow_id)
+            return freed
 
     def utilization(self):
         with self.lock:

@@ -88,6 +88,17 @@ def _worker(rank, port, q, shape):
             res["pins"] = [pool.pin_tokens(w).tolist() for w in DST_WF]
             res["payload"] = [_payload(pool, w) for w in DST_WF]
             res["stats"] = pool.stats()
+            # a source block outside the peer's KV region is refused before anything moves
+            from paper_2603_13605_b200.abi import SfkvError, csr
+            off, tok = csr([np.arange(1, 33, dtype=np.uint32)])
+            n_src = pool.cfg.n_blocks
+            try:
+                pool.handoff_recv(link.peers[0], np.array([4], np.int32), off, tok,
+                                  np.array([n_src, 0], np.int32))
+                res["oob"] = "accepted"
+            except SfkvError as e:
+                res["oob"] = e.code
+            res["stats_after_oob"] = pool.stats()
         dist.barrier()
         link.close()
         dist.destroy_process_group()
@@ -123,6 +134,8 @@ def test_peerlink_pull_handoff_matches_oracle(oracle_api, shape):
     so = dst.stats()
     for k in ("occupancy_tokens", "blocks_in_use", "table_live"):
         assert out[1]["stats"][k] == so[k], k
+    assert out[1]["oob"] == -1  # SFKV_EINVAL
+    assert out[1]["stats_after_oob"] == out[1]["stats"]
 
 
 def _payload_oracle(pool, wf):

@@ -82,3 +82,28 @@ def test_sim_server_round_trip_host_logic(oracle_api):
 @pytest.mark.gpu
 def test_sim_server_round_trip_gpu(gpu_api):
     _round_trip(gpu_api)
+
+
+@pytest.mark.gpu
+def test_sim_backend_grows_and_recycles_slots_gpu(gpu_api):
+    """Nothing is capped (the reference's pins are a std::map): more workflows than slots and longer
+    prompts than the block table grow the pool in place; a flushed workflow's slot is reused."""
+    be = GpuSimBackend(gpu_api, "shim", prefill_ms_per_token=0.001, decode_ms_per_token=0.001,
+                       cache_capacity_tokens=100_000, output_tokens=1, max_workflows=2, max_pin_blocks=2)
+    try:
+        msg = lambda n, s="": [synthetic_prompt(n, s)]  # noqa: E731
+        for w in ("a", "b", "c"):
+            assert be.complete(msg(100, w), workflow_id=w)["cached_tokens"] == 0
+        assert be.pool.cfg.max_workflows >= 3 and be.pool.cfg.max_pin_blocks >= 7
+        assert be.complete(msg(130, "a"), workflow_id="a")["cached_tokens"] == 100
+        assert be.complete(msg(130, "c"), workflow_id="c")["cached_tokens"] == 100
+        slot_a = be.slots["a"]
+        assert be.flush("a") == 130
+        assert "a" not in be.slots
+        assert be.complete(msg(50, "d"), workflow_id="d")["cached_tokens"] == 0
+        assert be.slots["d"] == slot_a  # recycled, and cold: the flushed pin is gone
+        assert be.complete(msg(60, "d"), workflow_id="d")["cached_tokens"] == 50
+        assert be.utilization()["occupancy_tokens"] == 100 + 130 + 60
+        assert be.errors == 0
+    finally:
+        be.close()
