@@ -11,7 +11,8 @@ from .abi import Api, Config, Pool, csr  # noqa: F401
 
 PKG_DIR = _os.path.dirname(_os.path.abspath(__file__))
 LIB_DIR = _os.path.join(PKG_DIR, "_lib")
-LIB_PATH = _os.path.join(LIB_DIR, "libsfkv.so")
+# SFKV_LIBRARY: an alternative build of the same ABI (compile-time variants under measurement)
+LIB_PATH = _os.environ.get("SFKV_LIBRARY") or _os.path.join(LIB_DIR, "libsfkv.so")
 _api = None
 
 

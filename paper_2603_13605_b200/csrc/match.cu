@@ -412,6 +412,17 @@ __device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAITP_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAITP_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
@@ -426,12 +437,25 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
 // Pin block of a lane staged at lane * PIN_STRIDE words. With the padded 80-B stride the 8 lanes of
 // a quarter-warp read 8 distinct bank groups: plain 16-B loads. (The unpadded 64-B stride needs a
 // per-lane chunk rotation and two select stages to undo it.)
+#ifndef SFKV_PIN_ROT
+#define SFKV_PIN_ROT 0
+#endif
 __device__ __forceinline__ void load_pin_staged(const uint32_t* s, uint32_t* q) {
   const int lane = threadIdx.x & 31;
 #if SFKV_PIN_PAD
 #pragma unroll
   for (int x = 0; x < 4; ++x) {
     const uint4 w = *reinterpret_cast<const uint4*>(s + lane * PIN_STRIDE + 4 * x);
+    q[4 * x] = w.x;
+    q[4 * x + 1] = w.y;
+    q[4 * x + 2] = w.z;
+    q[4 * x + 3] = w.w;
+  }
+#elif !SFKV_PIN_ROT
+  // unpadded 64-B stride, plain reads: lanes 2 apart share a bank group (4-way conflicts)
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const uint4 w = *reinterpret_cast<const uint4*>(s + lane * BT + 4 * x);
     q[4 * x] = w.x;
     q[4 * x + 1] = w.y;
     q[4 * x + 2] = w.z;
@@ -767,6 +791,134 @@ __global__ void __launch_bounds__(MATCH_THREADS) match_chain_kernel(MatchKernelA
   }
 }
 
+// ---------------------------------------------------------------- per-request lookup --------
+// Lookup batches of many requests of moderate length (C5: 100k prefixes of 65-127 blocks) take a
+// one-pass path: one warp per request walks its blocks 32 at a time with the running chain sum in
+// a register. Each tile's tokens are staged once (2D tensor-map TMA, double-buffered: the next
+// tile's load is in flight while this one is processed), and the probe, the token verify against
+// the resident block and the parent check run while the block's tokens are still in registers —
+// no chain pass, no per-block local sums / request ids in HBM, no second read of the request's
+// tokens (the two-pass lookup re-read them for the verify: ~1.64x the algorithmic traffic).
+// Output identical to the two-pass path (and sfo_lookup_batch): out_block per block, out_hit.
+constexpr int LR_THREADS = 128;
+#ifndef SFKV_LR_MINB
+#define SFKV_LR_MINB 1
+#endif
+constexpr int LR_MIN_REQUESTS = 2048;  // below: too few warps to fill the GPU one request each
+constexpr int64_t LR_MAX_AVG_BLOCKS = 1024;  // above: one warp per request serialises too much
+
+__global__ void __launch_bounds__(LR_THREADS, SFKV_LR_MINB) lookup_req_kernel(MatchKernelArgs K,
+                                                               const __grid_constant__ CUtensorMap tmap) {
+  __shared__ __align__(1024) uint32_t s_tok[LR_THREADS / 32][2][768];  // 18 rows each, 1 KB aligned
+  __shared__ __align__(8) uint64_t s_bar[LR_THREADS / 32][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (lane == 0) {
+    mbar_init(&s_bar[warp][0]);
+    mbar_init(&s_bar[warp][1]);
+  }
+  __syncwarp();
+  pdl_trigger();
+  pdl_wait();
+  const MatchArgs& A = K.a;
+  if (r >= A.n) return;
+  int64_t bo, to;
+  int32_t len, pl, wf;
+  unpack_rec(K.rec + r, bo, to, len, pl, wf);
+  const int64_t nb = (len + BT - 1) / BT, nfull = len / BT;
+  const int64_t tok_total = K.rec[A.n].tok_off;
+  const int64_t ntile = (nb + WT - 1) / WT;
+  const int64_t tok_limit = K.tok_rows * 32;
+  // staging of tile i into buffer i & 1 (uniform across the warp); false: read from global
+  auto issue = [&](int64_t i) -> bool {
+    const int64_t k0 = i * WT, kl = min(nb - 1, k0 + WT - 1);
+    const int64_t s0 = to + k0 * BT, sl = to + kl * BT;
+    const bool staged = ((sl & ~int64_t(3)) + 20) <= tok_limit;
+    if (staged && lane == 0) {
+      uint64_t* bar = &s_bar[warp][i & 1];
+      fence_proxy_async_smem();  // the warp's generic reads of this buffer precede the refill
+      mbar_expect_tx(bar, TMAP_ROWS * 128);
+      bulk_tensor_2d(s_tok[warp][i & 1], &tmap, 0, (int)(s0 >> 5), bar);
+    }
+    return staged;
+  };
+  bool staged = ntile > 0 ? issue(0) : false;
+  uint64_t carry = 0;
+  int32_t prev_raw = -1;
+  bool run = true;
+  int64_t lead = 0;
+  for (int64_t i = 0; i < ntile; ++i) {
+    const bool staged_next = i + 1 < ntile ? issue(i + 1) : false;
+    const int64_t k = i * WT + lane;
+    const bool valid = k < nb;
+    const int64_t start = to + k * BT;
+    const int nval = valid ? (int)min((int64_t)BT, (int64_t)len - k * BT) : 0;
+    uint32_t t[BT];
+    if (staged) {
+      mbar_wait(&s_bar[warp][i & 1], (uint32_t)((i >> 1) & 1));
+      if (valid) load_block_swz(s_tok[warp][i & 1], (int)(start - (((to + i * WT * BT) >> 5) << 5)), nval, t);
+    } else if (valid) {
+      load_block(A.tok, start, nval, tok_total, t);
+    }
+    if (!valid) {
+#pragma unroll
+      for (int j = 0; j < BT; ++j) t[j] = 0u;
+    }
+    __syncwarp();
+    // chained key: warp inclusive scan of the digests on top of the request's running sum
+    uint64_t v = valid ? block_digest_words((uint64_t)k, (uint32_t)nval, t) : 0ull;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t u = __shfl_up_sync(0xffffffffu, v, d);
+      if (lane >= d) v += u;
+    }
+    v += carry;
+    carry = __shfl_sync(0xffffffffu, v, 31);
+    const uint64_t c = chain_finalize(v);
+    // probe (full blocks only; a pending claim reads -1), then verify + parent together
+    int32_t raw = -1;
+    if (valid && k < nfull) {
+      uint64_t sl = c & K.slot_mask;
+      for (;;) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(K.slots + sl));
+        const uint64_t key = (uint64_t)w.x | ((uint64_t)w.y << 32);
+        if (key == c) {
+          raw = (int32_t)w.z;
+          break;
+        }
+        if (key == KEY_EMPTY) break;
+        sl = (sl + 1) & K.slot_mask;
+      }
+    }
+    bool eq = false;
+    int32_t par = -1;
+    if (raw >= 0) {
+      uint32_t q[BT];
+      load16_aligned(K.blk_tok + (int64_t)raw * BT, q);
+      par = __ldg(&K.blk_parent[raw]);
+      eq = true;
+#pragma unroll
+      for (int j = 0; j < BT; ++j) eq &= q[j] == t[j];
+    }
+    const int32_t up_raw = __shfl_up_sync(0xffffffffu, raw, 1);
+    const int32_t p_raw = lane > 0 ? up_raw : prev_raw;
+    const int32_t id = (eq && (k == 0 || par == p_raw)) ? raw : -1;
+    prev_raw = __shfl_sync(0xffffffffu, raw, 31);
+    if (valid) A.out_block[bo + k] = id;
+    const unsigned miss = __ballot_sync(0xffffffffu, valid && id < 0);
+    if (run) {
+      if (miss) {
+        lead += __ffs(miss) - 1;
+        run = false;
+      } else {
+        lead += min((int64_t)WT, nb - i * WT);
+      }
+    }
+    staged = staged_next;
+  }
+  if (lane == 0) A.out_hit[r] = lead * BT;
+}
+
 int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStream_t st) {
   if (a.n <= 0) return 0;
   const int64_t ntiles = (a.n_items + WT - 1) / WT;
@@ -842,7 +994,9 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   CUtensorMap tm;
   memset(&tm, 0, sizeof(tm));
   K.tok_rows = a.n_tok_bound / 32;
-  if (a.out_M && K.tok_rows > 0) {
+  const bool per_request = a.out_block && !a.out_M && a.n >= LR_MIN_REQUESTS &&
+                           a.n_items <= LR_MAX_AVG_BLOCKS * a.n;
+  if ((a.out_M || per_request) && K.tok_rows > 0) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
       cudaDriverEntryPointQueryResult q;
@@ -861,6 +1015,11 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
     if (r != CUDA_SUCCESS) return fail(SFKV_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   } else {
     K.tok_rows = 0;
+  }
+  if (per_request) {
+    const unsigned lgrid = (unsigned)((a.n + LR_THREADS / 32 - 1) / (LR_THREADS / 32));
+    SFKV_CUDA(launch_pdl(lookup_req_kernel, dim3(lgrid), dim3(LR_THREADS), st, K, tm));
+    return 0;
   }
   if (a.out_M) SFKV_CUDA(launch_pdl(match_block_kernel<true>, dim3((unsigned)grid), dim3(BLOCK_THREADS), st, K, tm));
   else SFKV_CUDA(launch_pdl(match_block_kernel<false>, dim3((unsigned)grid), dim3(BLOCK_THREADS), st, K, tm));

@@ -74,11 +74,83 @@ __global__ void __launch_bounds__(256) press_kernel(PressArgs a) {
   if (threadIdx.x == 0) *a.done = 0;
 }
 
+// Single-pass variant for up to PRESS_NB_MAX backends (the common case): every entry is read
+// once. A warp reduces its 32 entries segmented by backend — one warp_argmin per distinct backend
+// among them (__ballot groups; a warp of one backend, as in a backend-major layout, is a single
+// 5-step shuffle reduction) — into its own shared-memory row of per-backend candidates; one
+// __syncthreads, then the CTA's candidates go out per backend and the last CTA reduces them with
+// one warp per backend. No per-backend passes over the entries, no block-wide barrier per backend.
+constexpr int PRESS_NB_MAX = 64;
+constexpr int PRESS_THREADS = 256;
+__global__ void __launch_bounds__(PRESS_THREADS) press1_kernel(PressArgs a) {
+  __shared__ Cand s_c[PRESS_THREADS / 32][PRESS_NB_MAX];
+  __shared__ unsigned char s_on[PRESS_NB_MAX];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = PRESS_THREADS / 32;
+  for (int i = threadIdx.x; i < NW * PRESS_NB_MAX; i += PRESS_THREADS) s_c[i / PRESS_NB_MAX][i % PRESS_NB_MAX] = cand_none();
+  for (int b = threadIdx.x; b < a.nb; b += PRESS_THREADS) s_on[b] = a.util[b] > a.tau;
+  __syncthreads();
+  const int64_t gw = ((int64_t)blockIdx.x * PRESS_THREADS + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * PRESS_THREADS) >> 5;
+  for (int64_t base = gw * 32; base < a.n; base += nwarps * 32) {
+    const int64_t i = base + lane;
+    int32_t b = -1;
+    Cand c = cand_none();
+    if (i < a.n) {
+      b = a.backend[i];
+      if (b >= 0 && b < a.nb && s_on[b] && a.preserved[i] && a.in_flight[i] <= 0) {
+        c = Cand{ts_order_key(a.ts[i]), a.rank[i], i};
+      } else {
+        b = -1;
+      }
+    }
+    unsigned rem = __ballot_sync(0xffffffffu, b >= 0);
+    while (rem) {
+      const int32_t bb = __shfl_sync(0xffffffffu, b, __ffs(rem) - 1);
+      const unsigned grp = __ballot_sync(0xffffffffu, b == bb);
+      const Cand m = warp_argmin(b == bb ? c : cand_none());
+      if (lane == 0 && cand_less(m, s_c[warp][bb])) s_c[warp][bb] = m;
+      rem &= ~grp;
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < a.nb; b += PRESS_THREADS) {
+    Cand c = s_c[0][b];
+#pragma unroll
+    for (int w = 1; w < NW; ++w)
+      if (cand_less(s_c[w][b], c)) c = s_c[w][b];
+    a.part[(int64_t)blockIdx.x * a.nb + b] = c;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int b = warp; b < a.nb; b += NW) {
+    Cand c = cand_none();
+    for (int64_t p = lane; p < gridDim.x; p += 32) {
+      const Cand d = cand_load(&a.part[p * a.nb + b]);
+      if (cand_less(d, c)) c = d;
+    }
+    c = warp_argmin(c);
+    if (lane == 0) a.victim[b] = c.idx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *a.done = 0;
+}
+
 int pressure_dev(cudaStream_t st, int64_t n, const int32_t* backend, const double* ts,
                  const uint32_t* rank, const int32_t* in_flight, const uint8_t* preserved,
                  int32_t nb, const double* util, double tau, Cand* part, int grid,
                  unsigned int* done, long long* victim) {
   PressArgs a{n, backend, ts, rank, in_flight, preserved, nb, util, tau, part, done, victim};
+  if (nb <= PRESS_NB_MAX) {
+    press1_kernel<<<grid, PRESS_THREADS, 0, st>>>(a);
+    SFKV_LAUNCH_CHECK("press1_kernel");
+    return 0;
+  }
   press_kernel<<<grid, 256, 0, st>>>(a);
   SFKV_LAUNCH_CHECK("press_kernel");
   return 0;
@@ -406,7 +478,7 @@ extern "C" int sfmm_pressure_argmin(int32_t device, int64_t n, const int32_t* ba
   DevCtx* c = ctx_for(device);
   std::lock_guard<std::mutex> lk(c->mu);
   if (!c->done) return fail(SFKV_ENOMEM, "pressure_argmin: device context");
-  const int grid = grid_for(n, 256, c->sms * 2);
+  const int grid = grid_for(n, 256, c->sms * 4);
   Carver cv;
   const size_t o_b = cv.take<int32_t>(n), o_ts = cv.take<double>(n), o_rk = cv.take<uint32_t>(n),
                o_if = cv.take<int32_t>(n), o_pr = cv.take<uint8_t>(n), o_u = cv.take<double>(n_backends),
@@ -447,7 +519,7 @@ extern "C" int sfmm_pressure_argmin_dev(int32_t device, int64_t n, const int32_t
   DevCtx* c = ctx_for(device);
   std::lock_guard<std::mutex> lk(c->mu);
   if (!c->done) return fail(SFKV_ENOMEM, "pressure_argmin_dev: device context");
-  const int grid = grid_for(n, 256, c->sms * 2);
+  const int grid = grid_for(n, 256, c->sms * 4);
   if (int rc = c->buf.ensure((size_t)grid * n_backends * sizeof(Cand))) return rc;
   return pressure_dev(static_cast<cudaStream_t>(cuda_stream), n, backend, ts, wf_rank, in_flight, preserved,
                       n_backends, util, tau, c->buf.as<Cand>(), grid, c->done,

@@ -196,6 +196,31 @@ def test_pressure_argmin_random(gpu_api, oracle_api):
                                       po(backend, ts, wr, inf, pres, util, 0.85))
 
 
+@pytest.mark.parametrize("nb,n,layout", [(8, 40_000, "backend_major"), (8, 40_000, "interleaved"),
+                                         (40, 200_000, "random"), (100, 50_000, "random")])
+def test_pressure_argmin_large(gpu_api, oracle_api, nb, n, layout):
+    """The single-pass segmented kernel (<= 64 backends: warps of one backend reduce in one
+    shuffle tree, mixed warps once per distinct backend) and the per-backend-pass fallback
+    (> 64 backends) at tracker scale, against the oracle."""
+    rng = np.random.default_rng(nb * 7 + n)
+    if layout == "backend_major":
+        backend = np.repeat(np.arange(nb, dtype=np.int32), n // nb)
+    elif layout == "interleaved":  # the tracker's dense (workflow, backend) order
+        backend = np.tile(np.arange(nb, dtype=np.int32), n // nb)
+    else:
+        backend = rng.integers(0, nb, size=n).astype(np.int32)
+    n = len(backend)
+    ts = np.round(rng.uniform(0, 50, n), 0)  # heavy ties: the rank tie-break decides
+    wr = rng.permutation(n).astype(np.uint32)
+    inf = (rng.random(n) < 0.2).astype(np.int32)
+    pres = (rng.random(n) < 0.7).astype(np.uint8)
+    util = rng.choice([0.5, 0.86, 1.0], size=nb).astype(np.float64)
+    got = replay.default_pressure(gpu_api)(backend, ts, wr, inf, pres, util, 0.85)
+    want = replay.default_pressure(oracle_api)(backend, ts, wr, inf, pres, util, 0.85)
+    np.testing.assert_array_equal(got, want)
+    assert (got >= 0).sum() == (util > 0.85).sum()
+
+
 def _cost(api, dev, n, c, P, M, O, par, alt, depth, limit):
     choice = np.zeros(n, dtype=np.int32)
     cost = np.zeros(n, dtype=np.float64)
@@ -359,3 +384,52 @@ def test_pool_reserve_grows_in_place(gpu_api, oracle_api):
     np.testing.assert_array_equal(g.refcounts(), o.refcounts())
     for w in range(n_wf):
         np.testing.assert_array_equal(g.pin_blocks(w)[0], o.pin_blocks(w)[0])
+
+
+def test_lookup_one_pass_and_two_pass_agree_with_oracle(gpu_api, oracle_api):
+    """Lookup batches of >= 2048 requests take the one-warp-per-request path (lookup_req_kernel:
+    running chain sum, TMA double buffer, probe + verify + parent check in one pass); smaller
+    batches take the block/chain two-pass path. Both equal sfo_lookup_batch on the same requests:
+    shared and private prefixes, partial hits, empty and sub-block requests, requests of up to
+    ~300 blocks (many tiles per warp) and the tail tiles that read past the last full 128-B token row."""
+    n_wf = 600
+    cfg = Config(max_workflows=n_wf, n_blocks=150_000, capacity_tokens=1 << 40, max_pin_blocks=320,
+                 table_log2=19)
+    g, o = _pair(gpu_api, oracle_api, cfg)
+    wl = Workload(21, n_wf, n_sys=6, sys_len=(16, 700), ctx_len=(0, 4000), append=(0, 60))
+    wfs = np.arange(n_wf, dtype=np.int32)
+    seqs, off, tok = wl.batch(wfs)
+    np.testing.assert_array_equal(g.commit(wfs, off, tok), o.commit(wfs, off, tok))
+    rng = np.random.default_rng(22)
+    reqs = []
+    for i in range(3000):
+        base = seqs[int(rng.integers(0, n_wf))]
+        u = rng.random()
+        if u < 0.05:
+            q = np.zeros(0, np.uint32)
+        elif u < 0.1:
+            q = base[: int(rng.integers(1, 16))]
+        elif u < 0.3:  # a rewritten token: a miss mid-prefix, hits may resume after it
+            q = base.copy()
+            if len(q):
+                q[int(rng.integers(0, len(q)))] ^= np.uint32(0x77)
+        else:
+            q = np.concatenate([base[: int(rng.integers(0, len(base) + 1))],
+                                rng.integers(1, 1 << 30, size=int(rng.integers(0, 40))).astype(np.uint32)])
+        reqs.append(q.astype(np.uint32))
+    off2, tok2 = csr(reqs)
+    bo, ho = o.lookup(off2, tok2)
+    bg, hg = g.lookup(off2, tok2)  # one pass (3000 requests)
+    np.testing.assert_array_equal(hg, ho)
+    np.testing.assert_array_equal(bg, bo)
+    assert (ho > 0).mean() > 0.5
+    # the same requests in batches below the one-pass threshold: the two-pass path
+    pos = 0
+    for c0 in range(0, 3000, 1000):
+        sub = reqs[c0:c0 + 1000]
+        so, st = csr(sub)
+        b2, h2 = g.lookup(so, st)
+        nblk = len(b2)
+        np.testing.assert_array_equal(h2, ho[c0:c0 + 1000])
+        np.testing.assert_array_equal(b2, bo[pos:pos + nblk])
+        pos += nblk
