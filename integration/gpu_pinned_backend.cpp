@@ -54,13 +54,23 @@ GpuPinnedBackend::GpuPinnedBackend(EventLoop& loop, BackendDescriptor descriptor
   pc.n_slabs = 0;  // the reference holds no KV bytes; this binding is metadata-only
   pc.slab_row_bytes = 0;
   check(sfkv_pool_create(&pc, &pool_), "sfkv_pool_create");
+  if (options_.gpu_tokenizer) {
+    const int rc = sfkv_interner_create(options_.device, options_.interner_log2, options_.interner_arena, &interner_);
+    if (rc != SFKV_OK) {
+      sfkv_pool_destroy(pool_);
+      check(rc, "sfkv_interner_create");
+    }
+  }
   slot_requests_.assign(slot_cap_, 0);
   slot_pinned_.assign(slot_cap_, 0);
   slot_names_.assign(slot_cap_, std::string());
   for (int32_t s = slot_cap_ - 1; s >= 0; --s) free_slots_.push_back(s);
 }
 
-GpuPinnedBackend::~GpuPinnedBackend() { sfkv_pool_destroy(pool_); }
+GpuPinnedBackend::~GpuPinnedBackend() {
+  if (interner_) sfkv_interner_destroy(interner_);
+  sfkv_pool_destroy(pool_);
+}
 
 std::uint32_t GpuPinnedBackend::intern(const std::string& token) {
   auto [it, inserted] = intern_.emplace(token, static_cast<std::uint32_t>(intern_.size()));
@@ -127,10 +137,67 @@ void GpuPinnedBackend::complete(CompletionRequest req, CompletionCallback cb) {
 }
 
 void GpuPinnedBackend::pump() {
+  if (interner_) {
+    std::vector<Pending> batch;
+    while (busy_ + static_cast<int>(batch.size()) < config_.max_concurrency && !pending_.empty()) {
+      batch.push_back(std::move(pending_.front()));
+      pending_.pop_front();
+    }
+    if (!batch.empty()) start_batch(std::move(batch));
+    return;
+  }
   while (busy_ < config_.max_concurrency && !pending_.empty()) {
     Pending p = std::move(pending_.front());
     pending_.pop_front();
     start(std::move(p));
+  }
+}
+
+void GpuPinnedBackend::start_batch(std::vector<Pending> items) {
+  const int64_t n = static_cast<int64_t>(items.size());
+  // the requests' message contents as one text buffer (context_token_sequence reads content only)
+  std::vector<int64_t> req_msg_off(n + 1, 0), msg_off(1, 0);
+  std::vector<uint8_t> text;
+  for (int64_t r = 0; r < n; ++r) {
+    for (const auto& m : items[r].req.messages) {
+      text.insert(text.end(), m.content.begin(), m.content.end());
+      msg_off.push_back(static_cast<int64_t>(text.size()));
+    }
+    req_msg_off[r + 1] = static_cast<int64_t>(msg_off.size()) - 1;
+  }
+  const int64_t n_msg = static_cast<int64_t>(msg_off.size()) - 1;
+  const int64_t cap = std::max<int64_t>((static_cast<int64_t>(text.size()) + n_msg + 1) / 2, 1);
+  std::vector<int64_t> tok_off(n + 1, 0);
+  std::vector<uint32_t> tok(static_cast<std::size_t>(cap));
+  int64_t nt = 0;
+  if (text.empty()) text.push_back(0);
+  check(sfkv_tokenize_batch(interner_, n, req_msg_off.data(), msg_off.data(), text.data(), tok_off.data(),
+                            tok.data(), cap, &nt),
+        "sfkv_tokenize_batch");
+  // one match for the requests that carry a workflow id (held slots since complete())
+  std::vector<int32_t> slots(n, -1), wsl;
+  std::vector<int64_t> woff(1, 0);
+  std::vector<uint32_t> wtok;
+  for (int64_t r = 0; r < n; ++r) {
+    const std::string& wf = items[r].req.metadata.workflow_id;
+    if (wf.empty()) continue;  // the empty workflow id never holds a pin (simulated_backend.cpp:125)
+    slots[r] = find_slot(wf);
+    wsl.push_back(slots[r]);
+    wtok.insert(wtok.end(), tok.begin() + tok_off[r], tok.begin() + tok_off[r + 1]);
+    woff.push_back(static_cast<int64_t>(wtok.size()));
+  }
+  std::vector<int64_t> M(wsl.size(), 0);
+  if (!wsl.empty()) {
+    if (wtok.empty()) wtok.push_back(0);
+    check(sfkv_match_batch(pool_, static_cast<int64_t>(wsl.size()), wsl.data(), woff.data(), wtok.data(), M.data(),
+                           nullptr),
+          "sfkv_match_batch");
+  }
+  std::size_t k = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    std::vector<uint32_t> ids(tok.begin() + tok_off[r], tok.begin() + tok_off[r + 1]);
+    const long long m = slots[r] >= 0 ? M[k++] : 0;
+    dispatch(std::move(items[r]), std::move(ids), m, slots[r]);
   }
 }
 
@@ -150,15 +217,11 @@ ScriptedReply GpuPinnedBackend::reply_for(const CompletionRequest& req, int turn
   return {numbered_words(n), {}};
 }
 
-void GpuPinnedBackend::start(Pending item) {
-  const double now = loop_.now_ms();
-  const double queue_ms = now - item.arrival_ms;
-  const std::string wf = item.req.metadata.workflow_id;
-
+void GpuPinnedBackend::start(Pending item) {  // host tokenizer path (gpu_tokenizer = false)
+  const std::string& wf = item.req.metadata.workflow_id;
   std::vector<std::uint32_t> ids;
   for (const auto& t : context_token_sequence(item.req.messages)) ids.push_back(intern(t));
-  const long long P = static_cast<long long>(ids.size());
-  const int64_t off[2] = {0, P};
+  const int64_t off[2] = {0, static_cast<int64_t>(ids.size())};
   long long M = 0;
   int32_t slot = -1;
   if (!wf.empty()) {  // the empty workflow id never holds a pin (simulated_backend.cpp:125)
@@ -167,6 +230,16 @@ void GpuPinnedBackend::start(Pending item) {
     check(sfkv_match_batch(pool_, 1, &slot, off, ids.data(), &m, nullptr), "sfkv_match_batch");
     M = m;
   }
+  dispatch(std::move(item), std::move(ids), M, slot);
+}
+
+// SimulatedBackend::start after the cache lookup (simulated_backend.cpp:81-133): reply, latency,
+// completion event (which pins the prompt).
+void GpuPinnedBackend::dispatch(Pending item, std::vector<std::uint32_t> ids, long long M, int32_t slot) {
+  const double now = loop_.now_ms();
+  const double queue_ms = now - item.arrival_ms;
+  const std::string wf = item.req.metadata.workflow_id;
+  const long long P = static_cast<long long>(ids.size());
   if (observer_) observer_(wf, item.req.metadata.stage_id, P, M);
 
   const int turn = turns_[{wf, item.req.metadata.stage_id}]++;

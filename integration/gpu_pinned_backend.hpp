@@ -34,6 +34,12 @@ struct GpuPoolOptions {
   int device = 0;
   int max_workflows = 256;
   int max_pin_blocks = 256;  // 4,096-token pins before the first reserve
+  // Tokenize + intern on the GPU (sfkv_tokenize_batch over this backend's interner), one call for
+  // every request a pump() starts, instead of context_token_sequence + a host string map. Token
+  // ids are only ever compared within this backend's pool, so each backend has its own interner.
+  bool gpu_tokenizer = true;
+  int interner_log2 = 22;               // 4 M distinct token strings
+  long long interner_arena = 256 << 20;  // bytes of token text
 };
 
 class GpuPinnedBackend : public Backend {
@@ -85,8 +91,13 @@ class GpuPinnedBackend : public Backend {
   std::unordered_map<std::string, std::uint32_t> intern_;  // this backend's token ids
   DispatchObserver observer_;
 
+  sfkv_interner* interner_ = nullptr;  // gpu_tokenizer: this backend's token ids
   void pump();
   void start(Pending item);
+  // GPU tokenizer path: every item pump() starts at this instant, tokenized and matched in one
+  // batch (M is read at start, pins change only at completion, so batching is exact).
+  void start_batch(std::vector<Pending> items);
+  void dispatch(Pending item, std::vector<std::uint32_t> ids, long long M, int32_t slot);
   ScriptedReply reply_for(const CompletionRequest& req, int turn) const;
   int32_t slot_for(const std::string& workflow_id);  // creates (grows the pool if needed)
   int32_t find_slot(const std::string& workflow_id) const;  // -1 when none is held

@@ -2,7 +2,8 @@
 // B200 pool through GpuPinnedBackend (the drop-in). With --gpu-memory the reference's
 // MemoryManager is replaced by GpuMemoryManager (policy resolution and the tracker on the B200);
 // with --gpu-router the stage routers are the GPU ones (gpu_router.hpp: threshold / one-bit /
-// plan decisions and reroute_on_overload through sfmap_*). Same wiring as run_benchmark
+// plan decisions and reroute_on_overload through sfmap_*); with --host-tokenizer the backends
+// tokenize on the host (context_token_sequence) instead of sfkv_tokenize_batch. Same wiring as run_benchmark
 // (proj/src/harness.cpp:8-116) with GpuPinnedBackend in place of SimulatedBackend. Emits:
 //   {"type":"req", b, wf, stage, P, M}   per dispatch, in dispatch order (M from the GPU)
 //   {"type":"act", ...}                   the memory manager's action log (memory.cpp:389-401)
@@ -64,11 +65,12 @@ std::map<std::string, int> parse_flaky(const std::string& spec) {
 int main(int argc, char** argv) {
   std::string config_path, trace_path, out_path, flaky_spec;
   int device = 0;
-  bool gpu_memory = false, gpu_router = false;
+  bool gpu_memory = false, gpu_router = false, host_tokenizer = false;
   for (int i = 1; i < argc; ++i) {
     std::string a = argv[i];
     if (a == "--gpu-memory") { gpu_memory = true; continue; }
     if (a == "--gpu-router") { gpu_router = true; continue; }
+    if (a == "--host-tokenizer") { host_tokenizer = true; continue; }
     if (i + 1 >= argc) break;
     if (a == "--config") config_path = argv[++i];
     else if (a == "--trace") trace_path = argv[++i];
@@ -93,6 +95,7 @@ int main(int argc, char** argv) {
   for (const auto& b : config.backends) {
     GpuPoolOptions opt;  // default sizes: the pool grows on demand (sfkv_pool_reserve)
     opt.device = device;
+    opt.gpu_tokenizer = !host_tokenizer;
     auto be = std::make_shared<GpuPinnedBackend>(loop, b.descriptor, b.sim, opt, log);
     const std::string ref = b.descriptor.ref;
     be->set_dispatch_observer([&out, ref](const std::string& wf, const std::string& st,

@@ -21,13 +21,16 @@ DRIVER = os.path.join(REPO, "oracle", "_ref", "sf_gpu_replay")
 pytestmark = pytest.mark.gpu
 
 
-MODES = {"ref-memory": [], "gpu-memory": ["--gpu-memory"], "gpu-all": ["--gpu-memory", "--gpu-router"]}
+MODES = {"ref-memory": [], "gpu-memory": ["--gpu-memory"], "gpu-all": ["--gpu-memory", "--gpu-router"],
+         "host-tokenizer": ["--host-tokenizer"]}
 
 
 @pytest.mark.parametrize("mode", sorted(MODES))
 @pytest.mark.parametrize("name", sorted(SCENARIOS))
 def test_reference_harness_on_gpu_pool_matches_golden(tmp_path, name, mode):
-    """gpu-memory: the reference's MemoryManager is replaced by GpuMemoryManager (integration/),
+    """Every mode tokenizes and interns on the GPU (sfkv_tokenize_batch, one batch per dispatch
+    instant) except host-tokenizer (context_token_sequence + a host string map).
+    gpu-memory: the reference's MemoryManager is replaced by GpuMemoryManager (integration/),
     so pin cache, policy resolution, tracker and pressure ticks all run on the B200; gpu-all also
     replaces the stage routers (integration/gpu_router.hpp: plan / threshold / one-bit decisions
     and reroute_on_overload through sfmap_*)."""
