@@ -1410,10 +1410,82 @@ def tokenize_leg(args, api, dev, stream, hbm_peak):
     out["roofline"] = {"bound": "hbm", "alg_bytes_per_step": alg, "achieved": alg / (ms / 1e3) / 1e9,
                        "peak": hbm_peak, "unit": "GB/s", "frac": alg / (ms / 1e3) / 1e9 / hbm_peak}
     it.close()
+    out["cold"] = tokenize_cold(args, api, dev, stream, hbm_peak)
     L = ref_lib()
     if L is not None and not args.no_cpu_baseline:
         out["cpu_reference"] = tokenize_reference(L, text, msg_off, min(n, 300))
     return out
+
+
+def cold_corpus(seed, n_words, n_req=10_000):
+    """n_words distinct words of 8-24 bytes ("w" + 7 digits + random letters: every token is
+    longer than 7 bytes, so the interner takes its hash + arena-verify path), one space each,
+    split into n_req requests."""
+    rng = np.random.default_rng(seed)
+    W = 25
+    i = np.arange(n_words, dtype=np.int64)
+    L = rng.integers(8, 25, size=n_words)
+    mat = np.zeros((n_words, W), np.uint8)
+    mat[:, 0] = ord("w")
+    for j in range(7):
+        mat[:, 7 - j] = 48 + (i // 10 ** j) % 10
+    letters = rng.integers(97, 123, size=(n_words, W - 8), dtype=np.uint8)
+    col = np.arange(W - 8)[None, :]
+    mat[:, 8:] = np.where(col < (L - 8)[:, None], letters, 0)
+    mat[np.arange(n_words), L] = 32
+    text = mat.ravel()
+    text = text[text != 0]
+    woff = np.zeros(n_words + 1, np.int64)
+    np.cumsum(L + 1, out=woff[1:])
+    bounds = np.linspace(0, n_words, n_req + 1).astype(np.int64)
+    return text, woff[bounds], L
+
+
+def tokenize_cold(args, api, dev, stream, hbm_peak, n_words=2_000_000):
+    """§8f-2 cold batch: a fresh interner per step and every word new and longer than 7 bytes
+    (CAS claims, first-occurrence ranks, arena copy, hash + verify) — the interner's worst case
+    beside the steady state above. Ids must come out 0..n-1 in first-occurrence order."""
+    import torch
+
+    from paper_2603_13605_b200.abi import Interner
+    text, msg_off, L = cold_corpus(args.seed + 77, n_words)
+    n = len(msg_off) - 1
+    nbytes = int(msg_off[-1])
+    d_req = torch.arange(n + 1, dtype=torch.int64, device=dev)
+    d_moff = torch.from_numpy(msg_off).to(dev)
+    d_text = torch.from_numpy(np.concatenate([text, np.zeros(16, np.uint8)])).to(dev)
+    d_off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    d_tok = torch.zeros((nbytes + n + 1) // 2 + 1, dtype=torch.int32, device=dev)
+    d_nt = torch.zeros(1, dtype=torch.int64, device=dev)
+    times = []
+    for i in range(args.warmup + args.steps):
+        it = Interner(api, table_log2=22, arena_bytes=64 << 20, device=dev)  # untimed: a fresh interner
+        api.check("interner_set_stream", api.interner_set_stream(it.h, C.c_void_p(stream.cuda_stream)))
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        api.check("tokenize_batch_dev", api.tokenize_batch_dev(
+            it.h, n, C.c_void_p(d_req.data_ptr()), n, C.c_void_p(d_moff.data_ptr()),
+            C.c_void_p(d_text.data_ptr()), nbytes, C.c_void_p(d_off.data_ptr()),
+            C.c_void_p(d_tok.data_ptr()), C.c_void_p(d_nt.data_ptr())))
+        b.record(stream)
+        torch.cuda.synchronize()
+        api.check("interner_check", api.interner_check(it.h))
+        if i >= args.warmup:
+            times.append(a.elapsed_time(b))
+        size = it.size()
+        it.close()
+    nt = int(d_nt.item())
+    assert nt == n_words and size == n_words
+    assert (d_tok[:nt].cpu().numpy() == np.arange(n_words)).all(), "cold ids are not first-occurrence order"
+    ms = float(np.mean(times))
+    # text in + ids out + per new string: 8 B start, the string's bytes into the arena, a 16 B slot
+    alg = nbytes + 4 * nt + 8 * (n + 1) * 3 + n_words * (8 + 16) + int(L.sum())
+    return {"workload": f"{n_words} distinct words of 8-24 bytes (every token new, hash + verify path), "
+                        f"{nbytes / 1e6:.0f} MB in {n} requests, fresh interner per step",
+            "tokens_per_step": nt, "ms": ms, "tokens_per_s": nt / (ms / 1e3), "text_gbps": nbytes / (ms / 1e3) / 1e9,
+            "roofline": {"bound": "hbm", "alg_bytes_per_step": alg, "achieved": alg / (ms / 1e3) / 1e9,
+                         "peak": hbm_peak, "unit": "GB/s", "frac": alg / (ms / 1e3) / 1e9 / hbm_peak}}
 
 
 def tokenize_reference(L, text, msg_off, n_req):

@@ -236,6 +236,13 @@ int sfkv_handoff_recv_batch_dev(sfkv_pool* dst, const sfkv_peer* src, int64_t n,
 typedef struct sfkv_interner sfkv_interner;
 int sfkv_interner_create(int32_t device, int32_t table_log2, int64_t arena_bytes, sfkv_interner** out);
 int sfkv_interner_destroy(sfkv_interner* it);
+/* Grows the interner in place (never shrinks): a 2^table_log2-slot table (at most 2^(table_log2-1)
+ * ids) and arena_bytes of token text. Every existing string keeps its id. A batch that failed with
+ * SFKV_EPOOL (table, id space or arena full) changed nothing and can be retried after a reserve.
+ * (The reference's token strings live in unbounded std::strings, backend.cpp:60-91.) */
+int sfkv_interner_reserve(sfkv_interner* it, int32_t table_log2, int64_t arena_bytes);
+/* Arena bytes used / capacity and the current table size (log2). */
+int sfkv_interner_arena(sfkv_interner* it, int64_t* used, int64_t* cap, int32_t* table_log2);
 int sfkv_interner_set_stream(sfkv_interner* it, void* cuda_stream);  /* NULL = legacy default stream */
 int sfkv_interner_size(sfkv_interner* it, int64_t* n_ids);
 int sfkv_interner_token(sfkv_interner* it, uint32_t id, char* out, int32_t cap, int32_t* len);

@@ -170,10 +170,21 @@ void GpuPinnedBackend::start_batch(std::vector<Pending> items) {
   std::vector<int64_t> tok_off(n + 1, 0);
   std::vector<uint32_t> tok(static_cast<std::size_t>(cap));
   int64_t nt = 0;
+  const int64_t text_bytes = static_cast<int64_t>(text.size());
   if (text.empty()) text.push_back(0);
-  check(sfkv_tokenize_batch(interner_, n, req_msg_off.data(), msg_off.data(), text.data(), tok_off.data(),
-                            tok.data(), cap, &nt),
-        "sfkv_tokenize_batch");
+  // the interner grows like the reference's strings: a full table / arena is reserved and the
+  // batch (which changed nothing) retried; existing ids never change
+  for (int attempt = 0;; ++attempt) {
+    const int rc = sfkv_tokenize_batch(interner_, n, req_msg_off.data(), msg_off.data(), text.data(),
+                                       tok_off.data(), tok.data(), cap, &nt);
+    if (rc == SFKV_OK) break;
+    if (rc != SFKV_EPOOL || attempt >= 16) check(rc, "sfkv_tokenize_batch");
+    int64_t used = 0, acap = 0;
+    int32_t lg = 0;
+    check(sfkv_interner_arena(interner_, &used, &acap, &lg), "sfkv_interner_arena");
+    check(sfkv_interner_reserve(interner_, lg + 1, std::max<int64_t>(2 * acap, used + 2 * text_bytes + 4096)),
+          "sfkv_interner_reserve");
+  }
   // one match for the requests that carry a workflow id (held slots since complete())
   std::vector<int32_t> slots(n, -1), wsl;
   std::vector<int64_t> woff(1, 0);

@@ -106,6 +106,8 @@ GPU_ONLY = {
     "gather_dev": [P, i64, P, P, P],
     "interner_set_stream": [P, P],
     "interner_check": [P],
+    "interner_reserve": [P, i32, i64],
+    "interner_arena": [P, C.POINTER(i64), C.POINTER(i64), C.POINTER(i32)],
     "tokenize_batch_dev": [P, i64, P, i64, P, P, i64, P, P, P],
     "pool_export": [P, C.POINTER(IpcHandle)],
     "peer_open": [C.POINTER(IpcHandle), i32, C.POINTER(P)],
@@ -592,6 +594,29 @@ class Interner:
             self.close()
         except Exception:
             pass
+
+    def arena(self):
+        """(arena bytes used, arena capacity, table log2)."""
+        u, c, lg = C.c_int64(), C.c_int64(), C.c_int32()
+        self.api.check("interner_arena", self.api.interner_arena(self.h, C.byref(u), C.byref(c), C.byref(lg)))
+        return u.value, c.value, lg.value
+
+    def reserve(self, table_log2, arena_bytes):
+        """Grow in place (sfkv_interner_reserve); every existing string keeps its id."""
+        self.api.check("interner_reserve", self.api.interner_reserve(self.h, int(table_log2), int(arena_bytes)))
+
+    def tokenize_growing(self, requests, max_grow=16):
+        """tokenize(); on a full table / arena (SFKV_EPOOL: the batch changed nothing) reserve twice
+        the size and retry."""
+        for attempt in range(max_grow + 1):
+            try:
+                return self.tokenize(requests)
+            except SfkvError as e:
+                if e.code != -5 or attempt == max_grow:
+                    raise
+                used, cap, lg = self.arena()
+                nbytes = sum(len(m) for r in requests for m in r)
+                self.reserve(lg + 1, max(2 * cap, used + 2 * nbytes + 4096))
 
     def tokenize(self, requests):
         """-> (tok_off int64[n+1], tok uint32[T]) for a list of requests (lists of messages)."""

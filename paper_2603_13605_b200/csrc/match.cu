@@ -434,9 +434,13 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-// Pin block of a lane staged at lane * PIN_STRIDE words. With the padded 80-B stride the 8 lanes of
-// a quarter-warp read 8 distinct bank groups: plain 16-B loads. (The unpadded 64-B stride needs a
-// per-lane chunk rotation and two select stages to undo it.)
+// Pin block of a lane staged at lane * PIN_STRIDE words. Default (SFKV_PIN_PAD 0, SFKV_PIN_ROT 1):
+// the pin copy is unpadded (64 B per block, no HBM bytes beyond the tokens) and each lane reads its
+// four 16-B chunks in an order rotated by (lane >> 1) & 3, so the 8 lanes of a quarter-warp hit 8
+// distinct bank groups; two select stages undo the rotation. Measured on the C2 step (B200, 3
+// interleaved rounds): padded 80-B stride 74.5 us (M only 63.5), unpadded with 4-way conflicts
+// 74.2 (60.9), unpadded rotated 72.7 (60.1): the 16 B/block the padding cost in HBM outweigh the
+// selects.
 #ifndef SFKV_PIN_ROT
 #define SFKV_PIN_ROT 1
 #endif
@@ -517,35 +521,6 @@ __device__ __forceinline__ void load_block_swz(const uint32_t* s, int o, int nva
   }
 }
 
-
-// M of one tile: the first differing token of every in-pin block against the pin's block; the
-// first mismatching lane of each request segment issues the only atomicMin.
-__device__ __forceinline__ void tile_match(const MatchArgs& A, const Ctx& c, bool in_pin, const uint32_t* t,
-                                           const uint32_t* q) {
-  const int lane = threadIdx.x & 31;
-  const unsigned below = (1u << lane) - 1u;
-  const unsigned heads = __ballot_sync(0xffffffffu, c.valid && c.k == 0);
-  const unsigned segs = heads | 1u | __ballot_sync(0xffffffffu, !c.valid);
-  const int seg0 = 31 - __clz(segs & (below | (1u << lane)));
-  int lcp = BT, lim = 0;
-  if (in_pin) {
-    uint32_t d = 0;
-#pragma unroll
-    for (int j = 0; j < BT; ++j) d |= q[j] ^ t[j];
-    if (d) {
-      const int pn = min(c.pin_len - c.k * BT, BT);
-      lim = min(c.nval, pn);
-      unsigned ne = 1u << lim;
-#pragma unroll
-      for (int j = 0; j < BT; ++j) ne |= (q[j] != t[j]) ? (1u << j) : 0u;
-      lcp = __ffs(ne) - 1;
-    }
-  }
-  const bool mism = in_pin && lcp < lim;
-  const unsigned mm = __ballot_sync(0xffffffffu, mism);
-  if (mism && (mm & below & ~((1u << seg0) - 1u)) == 0)
-    atomicMin(reinterpret_cast<unsigned long long*>(A.out_M + c.r), (unsigned long long)((int64_t)c.k * BT + lcp));
-}
 
 // M and chained-hash work of one tile once every lane holds its block's tokens t (zero padded)
 // and, for blocks inside the pin, the pin's block q.
@@ -681,225 +656,6 @@ __global__ void __launch_bounds__(BLOCK_THREADS, 10) match_block_kernel(MatchKer
     for (int j = 0; j < BT; ++j) t[j] = 0u;
   }
   tile_finish(K, tile, c, in_pin, t, q);
-}
-
-// ---------------------------------------------------------------- range pass (match mode) ----
-// One warp per range of RANGE_TILES consecutive 32-block tiles, taken in ticket order (so every
-// predecessor range has started). The warp walks its tiles in order with the next tile's token and
-// pin staging in flight (two buffers, one mbarrier each), computes M exactly as the block pass,
-// and carries the chain sum from tile to tile in a register. Hashes of blocks after a request head
-// inside the range are final at once; blocks before the range's first head need the carry of the
-// preceding ranges of their request, found by a decoupled look-back over per-range statuses
-// (AGG: the range's sum, no head; INCL: the sum since its last head) that are published after the
-// range's memory work, so the wait is for predecessors that are finishing too. No chain pass, no
-// per-block local sums in HBM.
-#ifndef SFKV_RANGE_TILES
-#define SFKV_RANGE_TILES 4
-#endif
-constexpr int RANGE_TILES = SFKV_RANGE_TILES;
-constexpr int RNG_THREADS = 128;
-#ifndef SFKV_RNG_MINB
-#define SFKV_RNG_MINB 5
-#endif
-constexpr uint32_t RF_AGG = 1u, RF_INCL = 2u;  // range flag: epoch << 2 | kind
-
-struct RangeState {
-  unsigned long long* ticket;
-  uint32_t* flag;
-  uint64_t* agg;
-  uint64_t* incl;
-  unsigned long long base;
-  uint32_t epoch;
-};
-
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-struct Staged {
-  bool staged;   // tokens came by TMA (else read from global)
-  int64_t a0;    // first staged token
-};
-
-// Issue the staging of one tile (tokens + the pin blocks of its in-pin request segments) on `bar`
-// (always arms the barrier, with 0 bytes when nothing is staged, so phases stay in step).
-__device__ __forceinline__ Staged stage_tile(const MatchKernelArgs& K, const CUtensorMap* tmap, const Ctx& c,
-                                             bool in_pin, uint32_t* s_tok, uint32_t* s_pin, uint64_t* bar) {
-  const int lane = threadIdx.x & 31;
-  const int nv = __popc(__ballot_sync(0xffffffffu, c.valid));
-  const int64_t row0 = __shfl_sync(0xffffffffu, c.start, 0) >> 5;
-  Staged S;
-  S.a0 = row0 << 5;
-  const int64_t a1 = __shfl_sync(0xffffffffu, (c.start & ~int64_t(3)) + 20, nv - 1);
-  S.staged = a1 <= K.tok_rows * 32;
-  const unsigned pin_m = __ballot_sync(0xffffffffu, in_pin);
-  const int64_t prev_r = __shfl_up_sync(0xffffffffu, c.r, 1);
-  const bool head = in_pin && (lane == 0 || !((pin_m >> (lane - 1)) & 1u) || prev_r != c.r);
-  const unsigned heads = __ballot_sync(0xffffffffu, head);
-  uint32_t pin_bytes = 0;
-  if (head) {
-    const unsigned after = ~((2u << lane) - 1u);
-    const unsigned stop = (heads | ~pin_m) & after;
-    const int end = stop ? __ffs(stop) - 1 : 32;
-    pin_bytes = (uint32_t)(end - lane) * (PIN_STRIDE * 4);
-  }
-  const uint32_t tok_bytes = S.staged ? (uint32_t)(TMAP_ROWS * 128) : 0u;
-  const uint32_t total = __reduce_add_sync(0xffffffffu, pin_bytes) + tok_bytes;
-  if (lane == 0) {
-    fence_proxy_async_smem();  // this warp's earlier generic reads of the buffers precede the refill
-    mbar_expect_tx(bar, total);
-  }
-  __syncwarp();
-  if (S.staged && lane == 0) bulk_tensor_2d(s_tok, tmap, 0, (int)row0, bar);
-  if (head) bulk_copy(s_pin + lane * PIN_STRIDE, K.pin_tok + pin_tok_index(c.wf, c.k, 0, K.pin_groups), pin_bytes, bar);
-  return S;
-}
-
-template <bool HASH>
-__global__ void __launch_bounds__(RNG_THREADS, SFKV_RNG_MINB) match_range_kernel(MatchKernelArgs K, RangeState R,
-                                                                              const __grid_constant__ CUtensorMap tmap) {
-  constexpr int NW = RNG_THREADS / 32;
-  // per warp and buffer: the token box (18 rows, 1 KB aligned for the 128-B swizzle) and the pin
-  // blocks right behind it, in 5 KB: 40 KB per CTA, five CTAs per SM
-  constexpr int TOK_B = TMAP_ROWS * 128, BUF_B = ((TOK_B + WT * PIN_STRIDE * 4) + 1023) & ~1023;
-  __shared__ __align__(1024) uint8_t s_buf[NW][2][BUF_B];
-  __shared__ __align__(8) uint64_t s_bar[NW][2];
-  const MatchArgs& A = K.a;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  auto s_tok = [&](int b) { return reinterpret_cast<uint32_t*>(s_buf[warp][b]); };
-  auto s_pin = [&](int b) { return reinterpret_cast<uint32_t*>(s_buf[warp][b] + TOK_B); };
-  if (lane == 0) {
-    mbar_init(&s_bar[warp][0]);
-    mbar_init(&s_bar[warp][1]);
-  }
-  __syncwarp();
-  pdl_trigger();
-  pdl_wait();
-  const int64_t n_items = K.rec[A.n].blk_off;
-  const int64_t ntiles = (n_items + WT - 1) / WT;
-  const int64_t tok_total = K.rec[A.n].tok_off;
-  unsigned long long tk = 0;
-  if (lane == 0) tk = atomicAdd(R.ticket, 1ull);
-  const int64_t u = (int64_t)(__shfl_sync(0xffffffffu, tk, 0) - R.base);
-  const int64_t t0 = u * RANGE_TILES;
-  if (t0 >= ntiles) return;
-  const int64_t t1 = min(ntiles, t0 + RANGE_TILES);
-
-  Ctx c = resolve(K, t0, n_items);
-  bool in_pin = c.valid && c.pin_len >= 0 && c.k < (c.pin_len + BT - 1) / BT;
-  Staged S = stage_tile(K, &tmap, c, in_pin, s_tok(0), s_pin(0), &s_bar[warp][0]);
-  [[maybe_unused]] uint64_t run = 0;        // chain sum at the end of the previous tile
-  [[maybe_unused]] bool seen_head = false;  // a request head occurred earlier in the range
-  [[maybe_unused]] bool first_head = false; // the range starts with a request head
-  [[maybe_unused]] uint64_t pre_v[RANGE_TILES];
-  [[maybe_unused]] unsigned pre_m[RANGE_TILES];  // lanes whose hash waits for the carry (per tile)
-#pragma unroll
-  for (int j = 0; j < RANGE_TILES; ++j) {
-    const int64_t tile = t0 + j;
-    if (tile >= t1) break;
-    const int b = j & 1;
-    Ctx cn;
-    bool in_pin_n = false;
-    Staged Sn{false, 0};
-    if (tile + 1 < t1) {  // the next tile's staging flies while this one is processed
-      cn = resolve(K, tile + 1, n_items);
-      in_pin_n = cn.valid && cn.pin_len >= 0 && cn.k < (cn.pin_len + BT - 1) / BT;
-      Sn = stage_tile(K, &tmap, cn, in_pin_n, s_tok(b ^ 1), s_pin(b ^ 1), &s_bar[warp][b ^ 1]);
-    }
-    mbar_wait(&s_bar[warp][b], (uint32_t)((j >> 1) & 1));
-    uint32_t t[BT], q[BT];
-    if (c.valid) {
-      if (S.staged) load_block_swz(s_tok(b), (int)(c.start - S.a0), c.nval, t);
-      else load_block(A.tok, c.start, c.nval, tok_total, t);
-    } else {
-#pragma unroll
-      for (int i = 0; i < BT; ++i) t[i] = 0u;
-    }
-    if (in_pin) load_pin_staged(s_pin(b), q);
-    __syncwarp();
-    tile_match(A, c, in_pin, t, q);
-    if constexpr (HASH) {
-      const unsigned below = (1u << lane) - 1u;
-      const unsigned heads = __ballot_sync(0xffffffffu, c.valid && c.k == 0);
-      uint64_t v = c.valid ? block_digest_words((uint64_t)c.k, (uint32_t)c.nval, t) : 0ull;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint64_t w = __shfl_up_sync(0xffffffffu, v, d);
-        if (lane >= d) v += w;
-      }
-      const unsigned hl = heads & (below | (1u << lane));
-      const int hs = 31 - __clz(hl | 1u);  // last head at or before this lane (if any)
-      const uint64_t base = __shfl_sync(0xffffffffu, v, hs > 0 ? hs - 1 : 0);  // every lane shuffles
-      if (hl) {  // sum since that head
-        if (hs > 0) v -= base;
-      } else {
-        v += run;
-      }
-      if (j == 0) first_head = heads & 1u;
-      const bool fin = hl || seen_head;
-      const int64_t item = tile * WT + lane;
-      if (c.valid && fin && A.out_hash) A.out_hash[item] = chain_finalize(v);
-      pre_v[j] = v;
-      pre_m[j] = __ballot_sync(0xffffffffu, c.valid && !fin);
-      run = __shfl_sync(0xffffffffu, v, 31);
-      seen_head |= heads != 0;
-    }
-    c = cn;
-    in_pin = in_pin_n;
-    S = Sn;
-  }
-  if constexpr (HASH) {
-    const int nt = (int)(t1 - t0);
-    const bool any_pre = !first_head;
-    if (lane == 0) {
-      if (seen_head) {  // the carry into the next range does not depend on the predecessors
-        R.incl[u] = run;
-        st_release_u32(R.flag + u, (R.epoch << 2) | RF_INCL);
-      } else {
-        R.agg[u] = run;
-        st_release_u32(R.flag + u, (R.epoch << 2) | RF_AGG);
-      }
-    }
-    if (any_pre) {  // look back: the request's sum before this range
-      uint64_t carry = 0;
-      for (int64_t base = u - 1;; base -= 32) {
-        const int64_t pr = base - lane;
-        uint32_t f = 0;
-        unsigned incl;
-        int first;
-        for (;;) {
-          f = pr >= 0 ? ld_acquire_u32(R.flag + pr) : ((R.epoch << 2) | RF_INCL);
-          const bool cur = (f >> 2) == R.epoch && (f & 3u);
-          incl = __ballot_sync(0xffffffffu, cur && (f & 3u) == RF_INCL);
-          first = incl ? __ffs(incl) - 1 : 31;
-          const unsigned need = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
-          if ((__ballot_sync(0xffffffffu, cur) & need) == need) break;
-        }
-        uint64_t val = 0;
-        if (lane <= first && pr >= 0) val = (f & 3u) == RF_INCL ? ld_relaxed_u64(R.incl + pr) : ld_relaxed_u64(R.agg + pr);
-        carry += warp_sum(val);
-        if (incl) break;
-      }
-#pragma unroll
-      for (int j = 0; j < RANGE_TILES; ++j) {
-        if (j < nt && ((pre_m[j] >> lane) & 1u)) A.out_hash[(t0 + j) * WT + lane] = chain_finalize(carry + pre_v[j]);
-      }
-      if (!seen_head && lane == 0) {
-        R.incl[u] = carry + run;
-        st_release_u32(R.flag + u, (R.epoch << 2) | RF_INCL);
-      }
-    }
-  }
 }
 
 // ---------------------------------------------------------------- chain pass ---------------
@@ -1048,9 +804,6 @@ __global__ void __launch_bounds__(MATCH_THREADS) match_chain_kernel(MatchKernelA
 // no chain pass, no per-block local sums / request ids in HBM, no second read of the request's
 // tokens (the two-pass lookup re-read them for the verify: ~1.64x the algorithmic traffic).
 // Output identical to the two-pass path (and sfo_lookup_batch): out_block per block, out_hit.
-#ifndef SFKV_USE_RANGE
-#define SFKV_USE_RANGE 1
-#endif
 constexpr int LR_THREADS = 128;
 #ifndef SFKV_LR_MINB
 #define SFKV_LR_MINB 1
@@ -1270,38 +1023,6 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   if (per_request) {
     const unsigned lgrid = (unsigned)((a.n + LR_THREADS / 32 - 1) / (LR_THREADS / 32));
     SFKV_CUDA(launch_pdl(lookup_req_kernel, dim3(lgrid), dim3(LR_THREADS), st, K, tm));
-    return 0;
-  }
-  if (a.out_M && SFKV_USE_RANGE) {
-    const int64_t units = (ntiles + RANGE_TILES - 1) / RANGE_TILES;
-    // per-range statuses: epoch-tagged flags (no memset per launch), a ticket that only grows
-    const size_t need = 256 + (size_t)units * (4 + 8 + 8) + 64;
-    if (p->range_cap < units) {
-      if (int rc = p->range_state.ensure(need)) return rc;
-      SFKV_CUDA(cudaMemsetAsync(p->range_state.ptr, 0, p->range_state.bytes, st));
-      p->range_cap = (int64_t)((p->range_state.bytes - 256 - 64) / 20);
-      p->range_base = 0;
-      p->range_epoch = 0;
-    }
-    p->range_epoch = (p->range_epoch + 1) & 0x3FFFFFFF;
-    if (p->range_epoch == 0) {
-      SFKV_CUDA(cudaMemsetAsync(p->range_state.ptr, 0, p->range_state.bytes, st));
-      p->range_base = 0;
-      p->range_epoch = 1;
-    }
-    char* rs = p->range_state.as<char>();
-    RangeState R;
-    R.ticket = reinterpret_cast<unsigned long long*>(rs);
-    R.flag = reinterpret_cast<uint32_t*>(rs + 256);
-    R.agg = reinterpret_cast<uint64_t*>(rs + 256 + (((size_t)p->range_cap * 4 + 63) & ~size_t(63)));
-    R.incl = R.agg + p->range_cap;
-    R.base = p->range_base;
-    R.epoch = p->range_epoch;
-    p->range_base += (uint64_t)units;  // every warp of the launch takes exactly one ticket
-    const int64_t rgrid = (units + RNG_THREADS / 32 - 1) / (RNG_THREADS / 32);
-    p->range_base += (uint64_t)(rgrid * (RNG_THREADS / 32) - units);
-    if (a.out_hash) SFKV_CUDA(launch_pdl(match_range_kernel<true>, dim3((unsigned)rgrid), dim3(RNG_THREADS), st, K, R, tm));
-    else SFKV_CUDA(launch_pdl(match_range_kernel<false>, dim3((unsigned)rgrid), dim3(RNG_THREADS), st, K, R, tm));
     return 0;
   }
   if (a.out_M) SFKV_CUDA(launch_pdl(match_block_kernel<true>, dim3((unsigned)grid), dim3(BLOCK_THREADS), st, K, tm));

@@ -90,10 +90,6 @@ struct sfkv_pool {
   sfkv::Scratch io;            // device copies of host-pointer inputs/outputs
   sfkv::Scratch prep_status;   // match prep look-back statuses (epoch-tagged)
   uint32_t prep_epoch = 0;
-  sfkv::Scratch range_state;   // match range pass: [ticket u64][flags u32 x cap][agg u64 x cap][incl u64 x cap]
-  int64_t range_cap = 0;       // ranges the state holds
-  uint64_t range_base = 0;     // ticket value at the start of the next launch (host mirror)
-  uint32_t range_epoch = 0;
   void* host_stage = nullptr;  // pinned host staging
   size_t host_stage_bytes = 0;
   bool exported = false;       // the KV region was handed out as a CUDA IPC handle (fixed)

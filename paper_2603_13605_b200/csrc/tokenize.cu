@@ -603,6 +603,22 @@ static int sm_count_k() {
   return sms;
 }
 
+// Re-insert every published id into a larger table (sfkv_interner_reserve): same keys, same ids.
+__global__ void interner_rehash_kernel(TSlot* slots, uint64_t mask, int shift, const uint8_t* arena,
+                                       const int64_t* id_off, const int32_t* id_len, int64_t n_ids) {
+  for (int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; id < n_ids; id += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long key = tok_key(arena + id_off[id], id_len[id]);
+    uint64_t sl = (key * 0x9E3779B97F4A7C15ull) >> shift;
+    for (;;) {
+      if (atomicCAS(&slots[sl].key, 0ull, key) == 0ull) {
+        slots[sl].id = (uint32_t)id;
+        break;
+      }
+      sl = (sl + 1) & mask;
+    }
+  }
+}
+
 __global__ void interner_init_kernel(TSlot* slots, int64_t* owner, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     slots[i].key = 0;
@@ -765,6 +781,73 @@ int sfkv_interner_create(int32_t device, int32_t table_log2, int64_t arena_bytes
     return cuda_fail(e, "interner init");
   }
   *out = it;
+  return 0;
+}
+
+int sfkv_interner_reserve(sfkv_interner* it, int32_t table_log2, int64_t arena_bytes) {
+  if (!it || table_log2 > 34) return fail(SFKV_EINVAL, "interner_reserve: bad argument");
+  DeviceGuard g(it->device);
+  SFKV_CUDA(cudaStreamSynchronize(it->stream));
+  SFKV_CUDA(cudaMemcpy(it->ctr_host, it->ctr, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  const int64_t n_ids = (int64_t)it->ctr_host[0], used = (int64_t)it->ctr_host[1];
+  if (arena_bytes > it->arena_cap) {  // the text moves; offsets stay
+    uint8_t* a1 = nullptr;
+    SFKV_CUDA(cudaMalloc(&a1, arena_bytes));
+    if (used) SFKV_CUDA(cudaMemcpy(a1, it->arena, used, cudaMemcpyDeviceToDevice));
+    cudaFree(it->arena);
+    it->arena = a1;
+    it->arena_cap = arena_bytes;
+  }
+  const int64_t slots1 = int64_t(1) << table_log2;
+  if (slots1 > it->slots_n) {  // a larger table re-indexed by the same keys; ids unchanged
+    TSlot* s1 = nullptr;
+    int64_t *o1 = nullptr, *off1 = nullptr;
+    int32_t* len1 = nullptr;
+    const int64_t max1 = slots1 / 2;
+    cudaError_t e;
+    if ((e = cudaMalloc(&s1, slots1 * sizeof(TSlot))) != cudaSuccess ||
+        (e = cudaMalloc(&o1, slots1 * sizeof(int64_t))) != cudaSuccess ||
+        (e = cudaMalloc(&off1, max1 * sizeof(int64_t))) != cudaSuccess ||
+        (e = cudaMalloc(&len1, max1 * sizeof(int32_t))) != cudaSuccess) {
+      cudaFree(s1);
+      cudaFree(o1);
+      cudaFree(off1);
+      return cuda_fail(e, "interner_reserve");
+    }
+    if (n_ids) {
+      SFKV_CUDA(cudaMemcpy(off1, it->id_off, n_ids * sizeof(int64_t), cudaMemcpyDeviceToDevice));
+      SFKV_CUDA(cudaMemcpy(len1, it->id_len, n_ids * sizeof(int32_t), cudaMemcpyDeviceToDevice));
+    }
+    interner_init_kernel<<<grid_for(slots1, 256, 4096), 256, 0, it->stream>>>(s1, o1, slots1);
+    SFKV_LAUNCH_CHECK("interner_init_kernel");
+    if (n_ids) {
+      interner_rehash_kernel<<<grid_for(n_ids, 256, 4096), 256, 0, it->stream>>>(
+          s1, (uint64_t)slots1 - 1, 64 - table_log2, it->arena, off1, len1, n_ids);
+      SFKV_LAUNCH_CHECK("interner_rehash_kernel");
+    }
+    SFKV_CUDA(cudaStreamSynchronize(it->stream));
+    cudaFree(it->slots);
+    cudaFree(it->owner);
+    cudaFree(it->id_off);
+    cudaFree(it->id_len);
+    it->slots = s1;
+    it->owner = o1;
+    it->id_off = off1;
+    it->id_len = len1;
+    it->slots_n = slots1;
+    it->max_ids = max1;
+  }
+  return 0;
+}
+
+int sfkv_interner_arena(sfkv_interner* it, int64_t* used, int64_t* cap, int32_t* table_log2) {
+  if (!it || !used || !cap || !table_log2) return fail(SFKV_EINVAL, "interner_arena: null argument");
+  DeviceGuard g(it->device);
+  SFKV_CUDA(cudaMemcpyAsync(it->ctr_host, it->ctr, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, it->stream));
+  SFKV_CUDA(cudaStreamSynchronize(it->stream));
+  *used = (int64_t)it->ctr_host[1];
+  *cap = it->arena_cap;
+  *table_log2 = __builtin_ctzll((unsigned long long)it->slots_n);
   return 0;
 }
 

@@ -62,7 +62,7 @@ class GpuSimBackend:
         self.pool = Pool(api, Config(max_workflows=max_workflows, n_blocks=nb, capacity_tokens=self.capacity,
                                      max_pin_blocks=max_pin_blocks,
                                      table_log2=int(np.ceil(np.log2(2 * nb))) + 1, device=device))
-        self.interner = Interner(api, table_log2=20, arena_bytes=64 << 20, device=device)
+        self.interner = Interner(api, table_log2=16, arena_bytes=1 << 20, device=device)  # grows on demand
         self.slots: dict[str, int] = {}
         self.free = list(range(max_workflows - 1, -1, -1))
         self.inflight: dict[str, int] = {}
@@ -95,7 +95,7 @@ class GpuSimBackend:
         with self.admission:
             queue_ms = (time.monotonic() - t0) * 1e3
             with self.lock:
-                off, ids = self.interner.tokenize([[m.encode() for m in messages]])
+                off, ids = self.interner.tokenize_growing([[m.encode() for m in messages]])
                 P = int(off[-1])
                 M = 0
                 slot = self._slot(workflow_id) if workflow_id else -1

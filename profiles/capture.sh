@@ -14,11 +14,12 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/la
 F="ncu --set full --clock-control none --import-source on"
 Q="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-kv --no-c4 --no-c1"
 # C2 step kernels: the 7th match_block / match_chain launch of this command is a timed C2 step;
-# the C5 lookup chain pass is the 20th match_chain launch (19 hash-mode ones precede it)
+# the C5 lookup is the 3rd lookup_req launch (one-pass lookup: gate, warm-up, timed)
 $F -k regex:match_prep --launch-skip 6 --launch-count 1 -o $O/match_prep $Q > /dev/null 2>&1
 $F -k regex:match_block --launch-skip 6 --launch-count 1 -o $O/match_block $Q > /dev/null 2>&1
 $F -k regex:match_chain --launch-skip 6 --launch-count 1 -o $O/match_chain $Q > /dev/null 2>&1
-$F -k regex:match_chain --launch-skip 19 --launch-count 1 -o $O/c5_chain $Q > /dev/null 2>&1
+$F -k regex:lookup_req --launch-skip 2 --launch-count 1 -o $O/c5_lookup_req $Q > /dev/null 2>&1
+$F -k regex:press1 --launch-skip 2 --launch-count 1 -o $O/press1 $Q > /dev/null 2>&1
 $F -k regex:chunk_emit --launch-skip 1 --launch-count 1 -o $O/chunk_emit $Q > /dev/null 2>&1
 $F -k regex:sig_resolve --launch-skip 1 --launch-count 1 -o $O/sig_resolve $Q > /dev/null 2>&1
 $F -k regex:latency_kernel --launch-skip 1 --launch-count 1 -o $O/latency $Q > /dev/null 2>&1

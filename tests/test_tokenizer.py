@@ -108,6 +108,28 @@ def test_gpu_interner_overflow_fails_without_change(gpu_api):
     assert tok.tolist() == [2, 0, 1, 3]
 
 
+@pytest.mark.gpu
+def test_gpu_interner_reserve_keeps_ids(gpu_api, oracle_api):
+    """A tiny interner that grows in place whenever a batch does not fit (sfkv_interner_reserve:
+    larger table re-indexed by the same keys, arena copied) hands out exactly the ids a large one
+    does, batch after batch — short (exact-key) and long (hash + verify) tokens alike."""
+    g = Interner(gpu_api, table_log2=5, arena_bytes=32)
+    o = Interner(oracle_api, table_log2=20, arena_bytes=16 << 20)
+    grown = 0
+    for seed in range(6):
+        reqs = random_requests(300 + seed, n=int(20 + 30 * seed))
+        lg0 = g.arena()[2]
+        go, gt = g.tokenize_growing(reqs)
+        grown += g.arena()[2] > lg0
+        oo, ot = o.tokenize(reqs)
+        np.testing.assert_array_equal(go, oo)
+        np.testing.assert_array_equal(gt, ot)
+        assert g.size() == o.size()
+    assert grown >= 3
+    for i in range(0, o.size(), 3):
+        assert g.token(i) == o.token(i)
+
+
 def _edge_batches():
     rng = np.random.default_rng(5)
     one_byte = [[bytes([97 + i % 26]) for i in range(5000)], [b"x"] * 3 + [b" "], []]  # 4096 tokens in a chunk
