@@ -490,7 +490,8 @@ __global__ void install_kernel(CommitArgs a) {
     load_req_block(a, r, k, (int)(rem < BT ? rem : BT), t);
     uint4* dst = reinterpret_cast<uint4*>(a.pin_tok + pin_tok_index(a.wf[r], k, 0, a.pin_groups));
 #pragma unroll
-    for (int i = 0; i < 4; ++i) dst[i] = make_uint4(t[4 * i], t[4 * i + 1], t[4 * i + 2], t[4 * i + 3]);
+    for (int i = 0; i < 4; ++i)
+      dst[(i + pin_rot(k)) & 3] = make_uint4(t[4 * i], t[4 * i + 1], t[4 * i + 2], t[4 * i + 3]);
   }
 }
 

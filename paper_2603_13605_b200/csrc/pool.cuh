@@ -90,6 +90,11 @@ struct sfkv_pool {
   sfkv::Scratch io;            // device copies of host-pointer inputs/outputs
   sfkv::Scratch prep_status;   // match prep look-back statuses (epoch-tagged)
   uint32_t prep_epoch = 0;
+  sfkv::Scratch span_state;    // match span pass: ticket + per-span statuses, two parities
+  int64_t span_cap = 0;        // slots per status array
+  uint64_t span_base = 0;      // tickets taken by earlier launches
+  int span_parity = 0;
+  int64_t span_dirty_lo[2] = {0, 0}, span_dirty_hi[2] = {0, 0};  // written, not yet cleared
   void* host_stage = nullptr;  // pinned host staging
   size_t host_stage_bytes = 0;
   bool exported = false;       // the KV region was handed out as a CUDA IPC handle (fixed)
@@ -106,6 +111,11 @@ __host__ __device__ __forceinline__ int64_t pin_tok_index(int64_t wf, int64_t k,
   return (wf * (groups << 5) + k) * PIN_STRIDE + j;
 }
 inline int64_t pin_groups(const sfkv_pool_config& c) { return (c.max_pin_blocks + 31) / 32; }
+// A pin block's four 16-B chunks are stored rotated: chunk x of block k sits in chunk slot
+// (x + pin_rot(k)) & 3. Lane L of a match tile reads block k0 + L staged at L * 64 B; reading its
+// chunks in slot order (x + pin_rot(k)) & 3 puts the 8 lanes of a quarter-warp on 8 distinct bank
+// groups for any k0, and every chunk still lands in its own register (no selects).
+__host__ __device__ __forceinline__ int pin_rot(int64_t k) { return (int)((k >> 1) & 3); }
 
 // Outputs of the hashing/matching pass shared by match, lookup and commit.
 struct MatchArgs {
