@@ -103,7 +103,6 @@ static void pool_free(sfkv_pool* p) {
   p->small.release();
   p->io.release();
   p->prep_status.release();
-  p->span_state.release();
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   if (p->aux) cudaStreamDestroy(p->aux);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);

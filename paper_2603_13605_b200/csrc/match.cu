@@ -70,6 +70,7 @@ constexpr int CH_TPW_LOOKUP = SFKV_CH_TPW_LOOKUP;  // 54 registers: more warps i
 #define SFKV_PREP_THREADS 256
 #endif
 constexpr int PREP_THREADS = SFKV_PREP_THREADS;
+
 constexpr int PREP_TILE = PREP_THREADS;
 
 constexpr uint64_t ST_AGG = 1ull << 62;
@@ -145,6 +146,7 @@ struct PrepArgs {
   int32_t max_wf;     // device-side slot guard: out-of-range slots match as unpinned and set
   int* error;         //   the pool's sticky SFKV_EINVAL (reported by sfkv_pool_sync)
 };
+
 
 // Prep look-back status: flag (2 bits) | launch epoch (14 bits) | block count (48 bits). Statuses
 // live in a per-pool buffer that nothing else writes, so a status is current iff its epoch is
@@ -434,56 +436,6 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-// Pin block of a lane staged at lane * PIN_STRIDE words. Default (SFKV_PIN_PAD 0, SFKV_PIN_ROT 1):
-// the pin copy is unpadded (64 B per block, no HBM bytes beyond the tokens) and each lane reads its
-// four 16-B chunks in an order rotated by (lane >> 1) & 3, so the 8 lanes of a quarter-warp hit 8
-// distinct bank groups; two select stages undo the rotation. Measured on the C2 step (B200, 3
-// interleaved rounds): padded 80-B stride 74.5 us (M only 63.5), unpadded with 4-way conflicts
-// 74.2 (60.9), unpadded rotated 72.7 (60.1): the 16 B/block the padding cost in HBM outweigh the
-// selects.
-#ifndef SFKV_PIN_ROT
-#define SFKV_PIN_ROT 1
-#endif
-__device__ __forceinline__ void load_pin_staged(const uint32_t* s, uint32_t* q) {
-  const int lane = threadIdx.x & 31;
-#if SFKV_PIN_PAD
-#pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    const uint4 w = *reinterpret_cast<const uint4*>(s + lane * PIN_STRIDE + 4 * x);
-    q[4 * x] = w.x;
-    q[4 * x + 1] = w.y;
-    q[4 * x + 2] = w.z;
-    q[4 * x + 3] = w.w;
-  }
-#elif !SFKV_PIN_ROT
-  // unpadded 64-B stride, plain reads: lanes 2 apart share a bank group (4-way conflicts)
-#pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    const uint4 w = *reinterpret_cast<const uint4*>(s + lane * BT + 4 * x);
-    q[4 * x] = w.x;
-    q[4 * x + 1] = w.y;
-    q[4 * x + 2] = w.z;
-    q[4 * x + 3] = w.w;
-  }
-#else
-  const int rr = (lane >> 1) & 3;
-  uint4 v[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) v[i] = *reinterpret_cast<const uint4*>(s + lane * BT + 4 * ((i + rr) & 3));
-  uint4 u[4];
-#pragma unroll
-  for (int x = 0; x < 4; ++x) u[x] = (rr & 1) ? v[(x + 3) & 3] : v[x];
-#pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    const uint4 w = (rr & 2) ? u[(x + 2) & 3] : u[x];
-    q[4 * x] = w.x;
-    q[4 * x + 1] = w.y;
-    q[4 * x + 2] = w.z;
-    q[4 * x + 3] = w.w;
-  }
-#endif
-}
-
 // Tensor-map staging of the token range: the token buffer viewed as rows of 32 ids (128 B); a
 // tile's range is TMAP_ROWS rows from the row holding its first token, loaded with the 128-B
 // swizzle (16-B chunk c of row r lands at chunk c ^ (r & 7)), so the lanes of a quarter-warp —
@@ -521,6 +473,39 @@ __device__ __forceinline__ void load_block_swz(const uint32_t* s, int o, int nva
   }
 }
 
+
+// Block tokens of a lane whose block starts at word o (o & 3 == SH) of a swizzled staged range.
+template <int SH>
+__device__ __forceinline__ void load_swz_sh(const uint32_t* s, int o, uint32_t* t) {
+  const int c0 = o >> 2;
+  constexpr int NC = SH ? 5 : 4;
+  uint32_t w[20];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int g = c0 + i;
+    const uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(s) + ((g ^ ((g >> 3) & 7)) << 4));
+    w[4 * i] = v.x;
+    w[4 * i + 1] = v.y;
+    w[4 * i + 2] = v.z;
+    w[4 * i + 3] = v.w;
+  }
+#pragma unroll
+  for (int j = 0; j < BT; ++j) t[j] = w[j + SH];
+}
+
+// Pin block k of a lane, staged at lane * 64 B in the rotated layout: in-order, conflict-free.
+__device__ __forceinline__ void load_pin_rot(const uint32_t* s, int lane, int64_t k, uint32_t* q) {
+  const int rot = pin_rot(k);
+  const uint32_t* b = s + lane * BT;
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const uint4 w = *reinterpret_cast<const uint4*>(b + 4 * ((x + rot) & 3));
+    q[4 * x] = w.x;
+    q[4 * x + 1] = w.y;
+    q[4 * x + 2] = w.z;
+    q[4 * x + 3] = w.w;
+  }
+}
 
 // M and chained-hash work of one tile once every lane holds its block's tokens t (zero padded)
 // and, for blocks inside the pin, the pin's block q.
@@ -590,7 +575,10 @@ __device__ __forceinline__ void tile_finish(const MatchKernelArgs& K, int64_t ti
 // cover the window -> tokens/pin-tokens round trips.
 // 5 CTAs (40 warps) per SM: the register cap (48) trades a few spilled bytes for occupancy.
 template <bool STAGED>
-__global__ void __launch_bounds__(BLOCK_THREADS, 10) match_block_kernel(MatchKernelArgs K,
+#ifndef SFKV_MB_MINB
+#define SFKV_MB_MINB 8
+#endif
+__global__ void __launch_bounds__(BLOCK_THREADS, SFKV_MB_MINB) match_block_kernel(MatchKernelArgs K,
                                                                        const __grid_constant__ CUtensorMap tmap) {
   __shared__ __align__(1024) uint32_t s_tok[STAGED ? BLOCK_THREADS / 32 : 1][STAGED ? 768 : 4];  // 18 rows, 1 KB-aligned
   __shared__ __align__(128) uint32_t s_pin[STAGED ? BLOCK_THREADS / 32 : 1][STAGED ? WT * PIN_STRIDE : 4];
@@ -643,11 +631,30 @@ __global__ void __launch_bounds__(BLOCK_THREADS, 10) match_block_kernel(MatchKer
                           pin_bytes, &s_bar[warp]);
       mbar_wait0(&s_bar[warp]);
     }
-    if (c.valid) {
-      if (staged) load_block_swz(s_tok[warp], (int)(c.start - a0), c.nval, t);
-      else load_block(A.tok, c.start, c.nval, tok_total, t);
+    if (staged) {
+      // every lane of a tile inside one request shares the token alignment: a warp-uniform
+      // specialisation reads the swizzled range with no per-lane funnel selects
+      const int o = c.valid ? (int)(c.start - a0) : 0;
+      const int sh0 = __shfl_sync(0xffffffffu, o & 3, 0);
+      if (__all_sync(0xffffffffu, !c.valid || (o & 3) == sh0)) {
+        switch (sh0) {
+          case 0: load_swz_sh<0>(s_tok[warp], o, t); break;
+          case 1: load_swz_sh<1>(s_tok[warp], o, t); break;
+          case 2: load_swz_sh<2>(s_tok[warp], o, t); break;
+          default: load_swz_sh<3>(s_tok[warp], o, t); break;
+        }
+        if (c.nval < BT) {
+#pragma unroll
+          for (int j = 0; j < BT; ++j)
+            if (j >= c.nval) t[j] = 0u;
+        }
+      } else if (c.valid) {
+        load_block_swz(s_tok[warp], o, c.nval, t);
+      }
+    } else if (c.valid) {
+      load_block(A.tok, c.start, c.nval, tok_total, t);
     }
-    if (in_pin) load_pin_staged(s_pin[warp], q);
+    if (in_pin) load_pin_rot(s_pin[warp], lane, c.k, q);
   } else if (c.valid) {
     load_block(A.tok, c.start, c.nval, tok_total, t);
   }
@@ -923,639 +930,6 @@ __global__ void __launch_bounds__(LR_THREADS, SFKV_LR_MINB) lookup_req_kernel(Ma
   if (lane == 0) A.out_hit[r] = lead * BT;
 }
 
-// ---------------------------------------------------------------- span pass (match mode) ----
-// One launch per match batch: no prep scan, no chain pass, no per-block sums in HBM.
-// CTA c (ticket order: every lower-numbered span has started) owns the blocks whose FIRST token
-// lies in the token span [c*SPAN, (c+1)*SPAN) of the CSR batch: the tail of the request that crosses
-// c*SPAN (the carry-in request) and every request whose first token lies in the span (found by a
-// 32-ary search of tok_off). Only two facts about earlier spans are needed, both by decoupled
-// look-back over per-span statuses:
-//   * the flat index of the span's first block (blk_off): every span publishes its block count as
-//     soon as its request table is built, so this look-back resolves while the first tiles load;
-//   * the carry-in request's chain sum and first mismatch before the span: published when a
-//     predecessor has hashed its blocks; only the carry-in blocks wait for it, at the very end.
-// Inside the span, warps take 32-block tiles (one block per lane; a tile may cross requests): the
-// tile's token range is staged by one 2D tensor-map TMA load (128-B swizzle) and the pin blocks of
-// each in-pin request segment by bulk copies, double-buffered per warp. A tile whose lanes share one
-// token alignment (every tile inside one request) reads its blocks with a warp-uniform
-// specialisation (no per-lane funnel selects); pins are stored pre-rotated (pin_rot) so their reads
-// are conflict-free with no selects either. Block digests go to shared memory and one segmented
-// CTA scan turns them into chained sums; M mismatches are shared-memory atomic minima per request.
-// Statuses are self-validating 64-bit words (kind | value; 0 = unpublished) in one of two buffers
-// that alternate between launches: CTA c clears slot c of the other buffer, so a launch needs no
-// memset and no memory fence.
-#ifndef SFKV_SPAN_TOKENS
-#define SFKV_SPAN_TOKENS 16384
-#endif
-#ifndef SFKV_SP_WARPS
-#define SFKV_SP_WARPS 8
-#endif
-#ifndef SFKV_SP_MINB
-#define SFKV_SP_MINB 2
-#endif
-constexpr int SPAN = SFKV_SPAN_TOKENS;
-constexpr int SP_WARPS = SFKV_SP_WARPS;
-constexpr int SP_THREADS = SP_WARPS * 32;
-constexpr int SP_RREQ = SP_THREADS;                 // table entries per round (one thread each)
-constexpr int SP_RBLK = SPAN / BT + SP_RREQ;        // blocks of one round: <= SPAN/16 + entries
-constexpr int SP_IPT = (SP_RBLK + SP_THREADS - 1) / SP_THREADS;
-constexpr int SP_CARRY = SPAN / BT;                 // carry-in blocks of one span
-constexpr int SP_TOKB = TMAP_ROWS * 128;            // staged token box (1 KB aligned)
-constexpr int SP_BUF = ((SP_TOKB + WT * 64) + 1023) & ~1023;
-constexpr size_t SP_DYN = (size_t)SP_WARPS * 2 * SP_BUF + 1024;  // + base alignment slack
-constexpr uint64_t SP_KIND = 3ull << 62;
-constexpr uint64_t SP_AGG = 1ull << 62;    // chain: the span's own sum (no request head in it)
-constexpr uint64_t SP_INCL = 2ull << 62;   // chain: sum since the trailing request's head (in span)
-constexpr uint64_t SP_INCLD = 3ull << 62;  // chain: no head in span, prefix resolved by look-back
-constexpr uint64_t SP_MVALID = 1ull << 63; // mismatch word: valid | u32 first mismatch of the
-                                           // span's trailing request inside the span
-
-struct SpanState {
-  unsigned long long* ticket;  // grows by the grid size every launch (never reset)
-  unsigned long long base;
-  uint64_t *blk, *chain, *mism;        // this launch: kind | count, kind | sum, valid | position
-  uint64_t *blk_o, *chain_o, *mism_o;  // the other launch parity: slot c cleared by CTA c
-  const int64_t* pin_len;
-  int max_wf;
-  int* error;
-};
-
-__device__ __forceinline__ uint64_t ld_status_spin(const uint64_t* p) {
-  uint64_t v;
-  do {
-    v = ld_status(p);
-  } while (!v);
-  return v;
-}
-
-// Block tokens of a lane whose block starts at word o (o & 3 == SH) of a swizzled staged range.
-template <int SH>
-__device__ __forceinline__ void load_swz_sh(const uint32_t* s, int o, uint32_t* t) {
-  const int c0 = o >> 2;
-  constexpr int NC = SH ? 5 : 4;
-  uint32_t w[20];
-#pragma unroll
-  for (int i = 0; i < NC; ++i) {
-    const int g = c0 + i;
-    const uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(s) + ((g ^ ((g >> 3) & 7)) << 4));
-    w[4 * i] = v.x;
-    w[4 * i + 1] = v.y;
-    w[4 * i + 2] = v.z;
-    w[4 * i + 3] = v.w;
-  }
-#pragma unroll
-  for (int j = 0; j < BT; ++j) t[j] = w[j + SH];
-}
-
-// Pin block k of a lane, staged at lane * 64 B in the rotated layout: in-order, conflict-free.
-__device__ __forceinline__ void load_pin_rot(const uint32_t* s, int lane, int64_t k, uint32_t* q) {
-  const int rot = pin_rot(k);
-  const uint32_t* b = s + lane * BT;
-#pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    const uint4 w = *reinterpret_cast<const uint4*>(b + 4 * ((x + rot) & 3));
-    q[4 * x] = w.x;
-    q[4 * x + 1] = w.y;
-    q[4 * x + 2] = w.z;
-    q[4 * x + 3] = w.w;
-  }
-}
-
-struct SpTable {  // one round's entries (shared memory)
-  int64_t to[SP_RREQ];
-  int32_t r[SP_RREQ], len[SP_RREQ], k0[SP_RREQ], sb[SP_RREQ + 1], wf[SP_RREQ], pl[SP_RREQ], mn[SP_RREQ];
-};
-
-// Span-local block b -> table entry: the last entry in [lo, hi) whose first block is <= b (never
-// an empty entry: an entry followed by a larger first block contains b).
-__device__ __forceinline__ int sp_find(const int32_t* sb, int lo, int hi, int b) {
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (sb[mid] <= b) lo = mid;
-    else hi = mid;
-  }
-  return lo;
-}
-
-struct SpLane {
-  int e, k, nval;
-  int64_t start;
-  bool valid, in_pin;
-};
-
-__device__ __forceinline__ SpLane sp_resolve(const SpTable& T, int ne, int nblk, int tile) {
-  const int lane = threadIdx.x & 31;
-  SpLane L;
-  const int b = tile * WT + lane;
-  L.valid = b < nblk;
-  int ex = 0;
-  if (lane == 0) ex = sp_find(T.sb, 0, ne, tile * WT);
-  if (lane == 1) ex = sp_find(T.sb, 0, ne, min(nblk - 1, tile * WT + WT - 1));
-  const int e0 = __shfl_sync(0xffffffffu, ex, 0), e1 = __shfl_sync(0xffffffffu, ex, 1);
-  L.e = (e0 == e1 || !L.valid) ? e0 : sp_find(T.sb, e0, e1 + 1, b);
-  L.k = T.k0[L.e] + (b - T.sb[L.e]);
-  L.start = T.to[L.e] + (int64_t)L.k * BT;
-  const int nv = T.len[L.e] - L.k * BT;
-  L.nval = L.valid ? (nv > BT ? BT : nv) : 0;
-  const int pl = T.pl[L.e];
-  L.in_pin = L.valid && pl >= 0 && L.k < (pl + BT - 1) / BT;
-  return L;
-}
-
-// Issue the staging of one tile on `bar` (always arms the barrier, so phases stay in step).
-// Returns the token at staged word 0, or -1 when the tile is read from global memory.
-__device__ __forceinline__ int64_t sp_stage(const MatchKernelArgs& K, const CUtensorMap* tm, const SpTable& T,
-                                            const SpLane& L, uint8_t* buf, uint64_t* bar) {
-  const int lane = threadIdx.x & 31;
-  const unsigned vm = __ballot_sync(0xffffffffu, L.valid);
-  const int lastv = vm ? 31 - __clz(vm) : 0;
-  const int64_t row0 = __shfl_sync(0xffffffffu, L.start, 0) >> 5;
-  const int64_t a1 = __shfl_sync(0xffffffffu, (L.start & ~int64_t(3)) + 20, lastv);
-  const bool staged = K.tok_rows > 0 && a1 <= K.tok_rows * 32;
-  const unsigned pin_m = __ballot_sync(0xffffffffu, L.in_pin);
-  const int prev_e = __shfl_up_sync(0xffffffffu, L.e, 1);
-  const bool head = L.in_pin && (lane == 0 || !((pin_m >> (lane - 1)) & 1u) || prev_e != L.e);
-  const unsigned heads = __ballot_sync(0xffffffffu, head);
-  uint32_t pin_bytes = 0;
-  if (head) {
-    const unsigned after = ~((2u << lane) - 1u);
-    const unsigned stop = (heads | ~pin_m) & after;
-    const int end = stop ? __ffs(stop) - 1 : 32;
-    pin_bytes = (uint32_t)(end - lane) * 64u;
-  }
-  const uint32_t total = __reduce_add_sync(0xffffffffu, pin_bytes) + (staged ? (uint32_t)SP_TOKB : 0u);
-  if (lane == 0) {
-    fence_proxy_async_smem();  // this warp's earlier generic reads of the buffer precede the refill
-    mbar_expect_tx(bar, total);
-  }
-  __syncwarp();
-  if (staged && lane == 0) bulk_tensor_2d(buf, tm, 0, (int)row0, bar);
-  if (head)
-    bulk_copy(buf + SP_TOKB + lane * 64, K.pin_tok + pin_tok_index(T.wf[L.e], L.k, 0, K.pin_groups), pin_bytes, bar);
-  return staged ? (row0 << 5) : -1;
-}
-
-// first r in [0, n] with tok_off[r] >= x, n + 1 if none (one warp, 32-ary: ~3 dependent loads)
-__device__ __forceinline__ int64_t sp_lower(const int64_t* __restrict__ off, int64_t n, int64_t x) {
-  const int lane = threadIdx.x & 31;
-  int64_t lo = 0, hi = n + 1;  // answer in [lo, hi]; off[hi] >= x (or hi == n + 1)
-  while (lo < hi) {
-    const int64_t step = (hi - lo + 31) / 32;
-    const int64_t idx = lo + (int64_t)lane * step;
-    const unsigned m = __ballot_sync(0xffffffffu, idx < hi && __ldg(off + idx) >= x);
-    const int cnt = (int)min((int64_t)32, (hi - lo + step - 1) / step);
-    const int f = m ? __ffs(m) - 1 : cnt;
-    if (f == 0) return lo;
-    if (m) hi = lo + (int64_t)f * step;
-    lo = lo + (int64_t)(f - 1) * step + 1;
-  }
-  return lo;
-}
-
-template <bool HASH>
-__global__ void __launch_bounds__(SP_THREADS, SFKV_SP_MINB) match_span_kernel(MatchKernelArgs K, SpanState S,
-                                                                           const __grid_constant__ CUtensorMap tmap) {
-  extern __shared__ uint8_t s_dyn[];
-  __shared__ __align__(8) uint64_t s_bar[SP_WARPS][2];
-  __shared__ SpTable T;
-  __shared__ uint64_t s_dig[SP_RBLK];
-  __shared__ uint32_t s_head[(SP_RBLK + 31) / 32];
-  __shared__ uint64_t s_car[SP_CARRY];
-  __shared__ uint64_t s_wagg[SP_WARPS];
-  __shared__ uint32_t s_wflag[SP_WARPS];
-  __shared__ int64_t s_c, s_ra, s_rb, s_base, s_total;
-  __shared__ uint64_t s_trail;
-  __shared__ int32_t s_trail_mn, s_any_head;
-  const MatchArgs& A = K.a;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint8_t* bufs = s_dyn + ((1024 - (smem_u32(s_dyn) & 1023)) & 1023);  // 1 KB aligned (swizzle)
-  auto buf = [&](int b) { return bufs + (size_t)(warp * 2 + b) * SP_BUF; };
-  if (lane == 0) {
-    mbar_init(&s_bar[warp][0]);
-    mbar_init(&s_bar[warp][1]);
-  }
-  pdl_trigger();
-  pdl_wait();
-  if (tid == 0) {
-    s_c = (int64_t)(atomicAdd(S.ticket, 1ull) - S.base);
-    s_any_head = 0;
-    s_trail = 0;
-    s_trail_mn = INT32_MAX;
-  }
-  __syncthreads();
-  const int64_t c = s_c;
-  if (tid == 0) {  // the other parity's statuses for this span start out unpublished
-    S.blk_o[c] = 0;
-    S.chain_o[c] = 0;
-    S.mism_o[c] = 0;
-  }
-  const int64_t n = A.n;
-  int64_t total = __ldg(&A.tok_off[n]);
-  if (total > A.n_tok_bound) {  // a device batch larger than its declared buffer: fail loudly
-    if (tid == 0) *S.error = SFKV_EINVAL;
-    total = A.n_tok_bound;
-  }
-  const int64_t cS = c * SPAN, cE = cS + SPAN;
-  if (cS > total) return;
-  if (warp == 0) {  // owned requests [ra, rb): first token in [cS, cE)
-    const int64_t ra = sp_lower(A.tok_off, n, cS);
-    const int64_t rb = sp_lower(A.tok_off, n, cE);
-    if (lane == 0) {
-      s_ra = ra > n ? n : ra;
-      s_rb = rb > n ? n : rb;
-    }
-  }
-  __syncthreads();
-  const int64_t ra = s_ra, rb = s_rb;
-  int64_t rc = -1;  // the carry-in request: ra - 1 when it has a block starting at or after cS
-  int32_t kc = 0;
-  if (ra > 0) {
-    const int64_t to = __ldg(&A.tok_off[ra - 1]), len = __ldg(&A.tok_off[ra]) - to;
-    const int64_t k = (cS - to + BT - 1) / BT;
-    if (k * BT < len) {
-      rc = ra - 1;
-      kc = (int32_t)k;
-    }
-  }
-  const int has_cin = rc >= 0 ? 1 : 0;
-  const int64_t ne_all = has_cin + (rb - ra);
-  // at least one round: a span with no entry (it starts at the batch end) still publishes its
-  // block count and writes the closing offset
-  const int rounds = ne_all > 0 ? (int)((ne_all + SP_RREQ - 1) / SP_RREQ) : 1;
-  auto entry = [&](int64_t i, int64_t& r, int64_t& to, int64_t& len, int32_t& k0, int32_t& nin) {
-    r = (has_cin && i == 0) ? rc : ra + i - has_cin;
-    to = __ldg(&A.tok_off[r]);
-    len = __ldg(&A.tok_off[r + 1]) - to;
-    k0 = (r == rc) ? kc : 0;
-    const int64_t nb = (len + BT - 1) / BT;
-    const int64_t kl = cE > to ? (cE - to + BT - 1) / BT : 0;
-    const int64_t hi = nb < kl ? nb : kl;
-    nin = (int32_t)(hi > k0 ? hi - k0 : 0);
-  };
-  if (rounds > 1) {  // the span's block count first (one extra pass over dense spans only)
-    int64_t s = 0;
-    for (int64_t i = tid; i < ne_all; i += SP_THREADS) {
-      int64_t r, to, len;
-      int32_t k0, nin;
-      entry(i, r, to, len, k0, nin);
-      s += nin;
-    }
-    s = (int64_t)warp_sum((uint64_t)s);
-    if (lane == 0) s_wagg[warp] = (uint64_t)s;
-    __syncthreads();
-    if (tid == 0) {
-      int64_t t = 0;
-      for (int w = 0; w < SP_WARPS; ++w) t += (int64_t)s_wagg[w];
-      s_total = t;
-    }
-    __syncthreads();
-  }
-  // carry-in facts kept across rounds (round 0's table is rebuilt by later rounds)
-  int64_t cin_len = 0;
-  int32_t cin_pl = -1, cin_nin = 0, cin_mn = INT32_MAX;
-  bool cin_ends = false;
-  uint32_t ph = 0u;  // mbarrier phase parity per buffer (bit b)
-  int64_t roff = 0;           // span-local index of this round's first block
-  for (int rd = 0; rd < rounds; ++rd) {
-    // ---- round table: one entry per thread, block counts scanned over the CTA ----
-    const int64_t i0 = (int64_t)rd * SP_RREQ;
-    const int ne = (int)min((int64_t)SP_RREQ, ne_all - i0);
-    int32_t nin = 0;
-    if (tid < (SP_RBLK + 31) / 32) s_head[tid] = 0;
-    if (tid < ne) {
-      int64_t r, to, len;
-      int32_t k0;
-      entry(i0 + tid, r, to, len, k0, nin);
-      int32_t wf = __ldg(&A.wf[r]), pl = -1;
-      if ((uint32_t)wf < (uint32_t)S.max_wf) {
-        pl = (int32_t)__ldg(&S.pin_len[wf]);
-      } else {  // device-side slot guard: matches as unpinned, sticky SFKV_EINVAL
-        *S.error = SFKV_EINVAL;
-        wf = 0;
-      }
-      T.to[tid] = to;
-      T.r[tid] = (int32_t)r;
-      T.len[tid] = (int32_t)len;
-      T.k0[tid] = k0;
-      T.wf[tid] = wf;
-      T.pl[tid] = pl;
-      T.mn[tid] = INT32_MAX;
-    }
-    int32_t x = nin;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int32_t u = __shfl_up_sync(0xffffffffu, x, d);
-      if (lane >= d) x += u;
-    }
-    if (lane == 31) s_wagg[warp] = (uint64_t)x;
-    __syncthreads();
-    int32_t wpre = 0, nblk = 0;
-#pragma unroll
-    for (int w = 0; w < SP_WARPS; ++w) {
-      const int32_t v = (int32_t)s_wagg[w];
-      if (w < warp) wpre += v;
-      nblk += v;
-    }
-    if (tid < ne) {
-      const int32_t sb = wpre + x - nin;
-      T.sb[tid] = sb;
-      if (T.k0[tid] == 0 && nin > 0) atomicOr(&s_head[sb >> 5], 1u << (sb & 31));
-    }
-    if (tid == 0) {
-      T.sb[ne] = nblk;
-      if (rd == 0) {
-        if (rounds == 1) s_total = nblk;
-        st_status(S.blk + c, SP_AGG | (uint64_t)(rounds == 1 ? nblk : s_total));
-      }
-    }
-    __syncthreads();
-    if (rd == 0 && has_cin) {
-      cin_len = T.len[0];
-      cin_pl = T.pl[0];
-      cin_nin = T.sb[1];
-    }
-    // ---- stage this warp's first two tiles, then (round 0, warp 0) the span's first block ----
-    const int ntiles = (nblk + WT - 1) / WT;
-    int64_t a0_0 = -1, a0_1 = -1;  // first staged token per buffer (-1: read from global)
-    if (warp < ntiles) a0_0 = sp_stage(K, &tmap, T, sp_resolve(T, ne, nblk, warp), buf(0), &s_bar[warp][0]);
-    if (warp + SP_WARPS < ntiles)
-      a0_1 = sp_stage(K, &tmap, T, sp_resolve(T, ne, nblk, warp + SP_WARPS), buf(1), &s_bar[warp][1]);
-    if (rd == 0 && warp == 0) {
-      uint64_t prefix = 0;
-      for (int64_t bs = c - 1; bs >= 0; bs -= 32) {
-        const int64_t p = bs - lane;
-        const uint64_t v = p >= 0 ? ld_status_spin(S.blk + p) : SP_INCL;
-        const unsigned incl = __ballot_sync(0xffffffffu, (v & SP_KIND) == SP_INCL);
-        const int first = incl ? __ffs(incl) - 1 : 31;
-        prefix += warp_sum(lane <= first ? (v & ~SP_KIND) : 0ull);
-        if (incl) break;
-      }
-      if (lane == 0) {
-        st_status(S.blk + c, SP_INCL | (prefix + (uint64_t)s_total));
-        s_base = (int64_t)prefix;
-      }
-    }
-    // ---- tiles ----
-    int jn = 0;
-    for (int tile = warp; tile < ntiles; tile += SP_WARPS, ++jn) {
-      const int bi = jn & 1;
-      const SpLane L = sp_resolve(T, ne, nblk, tile);
-      mbar_wait(&s_bar[warp][bi], (ph >> bi) & 1u);
-      ph ^= 1u << bi;
-      const int64_t a0 = bi ? a0_1 : a0_0;
-      uint32_t t[BT], q[BT];
-      const uint32_t* st = reinterpret_cast<const uint32_t*>(buf(bi));
-      if (a0 >= 0) {
-        const int o = L.valid ? (int)(L.start - a0) : 0;
-        const int sh0 = __shfl_sync(0xffffffffu, o & 3, 0);
-        if (__all_sync(0xffffffffu, !L.valid || (o & 3) == sh0)) {
-          switch (sh0) {
-            case 0: load_swz_sh<0>(st, o, t); break;
-            case 1: load_swz_sh<1>(st, o, t); break;
-            case 2: load_swz_sh<2>(st, o, t); break;
-            default: load_swz_sh<3>(st, o, t); break;
-          }
-          if (L.nval < BT) {
-#pragma unroll
-            for (int j = 0; j < BT; ++j)
-              if (j >= L.nval) t[j] = 0u;
-          }
-        } else {
-          load_block_swz(st, o, L.nval, t);
-        }
-      } else if (L.valid) {
-        load_block(A.tok, L.start, L.nval, A.n_tok_bound, t);
-      }
-      if (!L.valid) {
-#pragma unroll
-        for (int j = 0; j < BT; ++j) t[j] = 0u;
-      }
-      if (L.in_pin) load_pin_rot(reinterpret_cast<const uint32_t*>(buf(bi) + SP_TOKB), lane, L.k, q);
-      __syncwarp();
-      if (tile + 2 * SP_WARPS < ntiles) {  // the buffer is free: stage this warp's tile after next
-        const int64_t an = sp_stage(K, &tmap, T, sp_resolve(T, ne, nblk, tile + 2 * SP_WARPS), buf(bi), &s_bar[warp][bi]);
-        if (bi) a0_1 = an;
-        else a0_0 = an;
-      }
-      // M: a block whose 16 words agree with the pin's has no mismatch (both sides zero padded);
-      // a differing one finds its exact first mismatch below min(valid tokens, pin tokens)
-      if (L.in_pin) {
-        uint32_t d = 0;
-#pragma unroll
-        for (int j = 0; j < BT; ++j) d |= q[j] ^ t[j];
-        if (d) {
-          const int lim = min(L.nval, min(T.pl[L.e] - L.k * BT, BT));
-          unsigned nem = 1u << lim;
-#pragma unroll
-          for (int j = 0; j < BT; ++j) nem |= (q[j] != t[j]) ? (1u << j) : 0u;
-          const int lcp = __ffs(nem) - 1;
-          if (lcp < lim) atomicMin(&T.mn[L.e], L.k * BT + lcp);
-        }
-      }
-      if constexpr (HASH) {
-        if (L.valid) s_dig[tile * WT + lane] = block_digest_words((uint64_t)L.k, (uint32_t)L.nval, t);
-      }
-    }
-    __syncthreads();
-    const int64_t base = s_base;
-    // ---- segmented scan of the digests: chain sums since the last request head (or the span
-    //      start, for the carry-in blocks) ----
-    if constexpr (HASH) {
-      uint64_t v[SP_IPT];
-      uint32_t hm = 0;
-      uint64_t run = 0;
-#pragma unroll
-      for (int i = 0; i < SP_IPT; ++i) {
-        const int b = tid * SP_IPT + i;
-        if (b < nblk && ((s_head[b >> 5] >> (b & 31)) & 1u)) {
-          run = 0;
-          hm |= 1u << i;
-        }
-        run += b < nblk ? s_dig[b] : 0ull;
-        v[i] = run;
-      }
-      // (flag, sum) pairs combine as (f1, a1) + (f2, a2) = (f1 | f2, f2 ? a2 : a1 + a2)
-      uint64_t a = run;
-      uint32_t f = hm ? 1u : 0u;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint64_t ua = __shfl_up_sync(0xffffffffu, a, d);
-        const uint32_t uf = __shfl_up_sync(0xffffffffu, f, d);
-        if (lane >= d) {
-          if (!f) a += ua;
-          f |= uf;
-        }
-      }
-      if (lane == 31) {
-        s_wagg[warp] = a;
-        s_wflag[warp] = f;
-      }
-      uint64_t ea = __shfl_up_sync(0xffffffffu, a, 1);
-      uint32_t ef = __shfl_up_sync(0xffffffffu, f, 1);
-      if (lane == 0) {
-        ea = 0;
-        ef = 0;
-      }
-      __syncthreads();
-      uint64_t wa = 0;
-      uint32_t wfl = 0;
-      for (int w = 0; w < warp; ++w) {
-        if (s_wflag[w]) {
-          wa = s_wagg[w];
-          wfl = 1;
-        } else {
-          wa += s_wagg[w];
-        }
-      }
-      if (!ef) ea += wa;
-      ef |= wfl;
-#pragma unroll
-      for (int i = 0; i < SP_IPT; ++i) {
-        const int b = tid * SP_IPT + i;
-        if (b < nblk) {
-          uint64_t sum = v[i];
-          bool fin = true;
-          if ((hm & ((2u << i) - 1u)) == 0) {  // no head in this thread up to item i
-            sum += ea;
-            fin = ef != 0;
-          }
-          sum &= CHAIN_MASK;
-          if (fin) {
-            if (A.out_hash) A.out_hash[base + roff + b] = chain_finalize(sum);
-          } else {
-            s_car[b] = sum;  // a carry-in block: waits for the predecessors' sum
-          }
-          s_dig[b] = sum;
-        }
-      }
-      __syncthreads();
-    }
-    // ---- per-request outputs of this round ----
-    if (tid < ne) {
-      const int32_t sbv = T.sb[tid], ninv = T.sb[tid + 1] - sbv;
-      const int64_t len = T.len[tid];
-      const int64_t nb = (len + BT - 1) / BT;
-      const bool ends = T.k0[tid] + ninv == nb;
-      const int32_t pl = T.pl[tid], mn = T.mn[tid];
-      if (rd == 0 && has_cin && tid == 0) {
-        cin_mn = mn;
-        cin_ends = ends;
-      } else {
-        const int32_t r = T.r[tid];
-        A.blk_off[r] = base + roff + sbv;
-        if (ends) A.out_M[r] = pl < 0 ? 0 : min(min((int64_t)pl, len), (int64_t)mn);
-      }
-    }
-    if (tid == 0 && nblk > 0) {  // the trailing request so far: the entry holding the last block
-      const int e = sp_find(T.sb, 0, ne, nblk - 1);
-      s_trail = HASH ? s_dig[nblk - 1] : 0ull;
-      s_trail_mn = T.mn[e];
-      bool any = false;
-      for (int w = 0; w < (nblk + 31) / 32; ++w) any |= s_head[w] != 0;
-      if (any) s_any_head = 1;
-    }
-    roff += nblk;
-    __syncthreads();
-  }
-  // ---- closing offset, the span's chain statuses, the carry-in request ----
-  const int64_t base = s_base;
-  if (tid == 0 && total < cE) A.blk_off[n] = base + s_total;
-  // INCL: the trailing request's head lies in the span (or the span holds no block at all, so no
-  // later span continues through it); AGG: the whole span is one request's middle
-  const bool incl = s_any_head != 0 || s_total == 0;
-  if (tid == 0) {
-    st_status(S.mism + c, SP_MVALID | (uint32_t)(incl ? s_trail_mn : cin_mn));
-    st_status(S.chain + c, (incl ? SP_INCL : SP_AGG) | (s_trail & CHAIN_MASK));
-  }
-  if (!has_cin || warp != 0) return;
-  // carry: predecessors' sums up to the first inclusive status; first mismatch: their words up to
-  // the span holding the request's head (SP_INCL), through derived-inclusive spans (SP_INCLD)
-  uint64_t carry = 0;
-  bool carry_done = false;
-  int32_t mn = cin_mn;
-  for (int64_t bs = c - 1;; bs -= 32) {
-    const int64_t p = bs - lane;
-    const uint64_t v = p >= 0 ? ld_status_spin(S.chain + p) : SP_INCL;
-    if (!carry_done) {
-      const unsigned im = __ballot_sync(0xffffffffu, (v & SP_KIND) >= SP_INCL);
-      const int first = im ? __ffs(im) - 1 : 31;
-      carry += warp_sum(lane <= first ? (v & CHAIN_MASK) : 0ull);
-      carry_done = im != 0;
-    }
-    const unsigned hm = __ballot_sync(0xffffffffu, (v & SP_KIND) == SP_INCL);
-    const int firsth = hm ? __ffs(hm) - 1 : 31;
-    const int32_t pm = (lane <= firsth && p >= 0) ? (int32_t)(uint32_t)ld_status_spin(S.mism + p) : INT32_MAX;
-    mn = min(mn, __reduce_min_sync(0xffffffffu, pm));
-    if (hm) break;
-  }
-  carry &= CHAIN_MASK;
-  if (!incl && lane == 0) st_status(S.chain + c, SP_INCLD | ((carry + s_trail) & CHAIN_MASK));
-  if (HASH && A.out_hash)
-    for (int b = lane; b < cin_nin; b += 32) A.out_hash[base + b] = chain_finalize((carry + s_car[b]) & CHAIN_MASK);
-  if (lane == 0 && cin_ends) A.out_M[rc] = cin_pl < 0 ? 0 : min(min((int64_t)cin_pl, cin_len), (int64_t)mn);
-}
-
-static int launch_span(sfkv_pool* p, const MatchArgs& a, MatchKernelArgs K, const CUtensorMap& tm, cudaStream_t st) {
-  const int64_t nspans = a.n_tok_bound / SPAN + 1;
-  if (p->span_cap < nspans) {  // [ticket][blk, chain, mism] x 2 parities, all clear
-    int64_t cap = p->span_cap ? p->span_cap : 4096;
-    while (cap < nspans) cap *= 2;
-    if (int rc = p->span_state.ensure(256 + 6 * sizeof(uint64_t) * (size_t)cap)) return rc;
-    SFKV_CUDA(cudaMemsetAsync(p->span_state.ptr, 0, p->span_state.bytes, st));
-    p->span_cap = cap;
-    p->span_base = 0;
-    for (int b = 0; b < 2; ++b) p->span_dirty_lo[b] = p->span_dirty_hi[b] = 0;
-  }
-  const int b = p->span_parity, o = b ^ 1;
-  uint64_t* arr = reinterpret_cast<uint64_t*>(p->span_state.as<char>() + 256);
-  auto par = [&](int q) { return arr + (size_t)q * 3 * p->span_cap; };
-  // statuses of this parity left by an earlier, larger launch that nothing has cleared yet
-  if (p->span_dirty_hi[b] > p->span_dirty_lo[b] && p->span_dirty_lo[b] < nspans) {
-    for (int k = 0; k < 3; ++k)
-      SFKV_CUDA(cudaMemsetAsync(par(b) + k * p->span_cap + p->span_dirty_lo[b], 0,
-                                sizeof(uint64_t) * (size_t)(p->span_dirty_hi[b] - p->span_dirty_lo[b]), st));
-    p->span_dirty_lo[b] = p->span_dirty_hi[b] = 0;
-  }
-  SpanState S;
-  S.ticket = p->span_state.as<unsigned long long>();
-  S.base = p->span_base;
-  S.blk = par(b);
-  S.chain = S.blk + p->span_cap;
-  S.mism = S.chain + p->span_cap;
-  S.blk_o = par(o);
-  S.chain_o = S.blk_o + p->span_cap;
-  S.mism_o = S.chain_o + p->span_cap;
-  S.pin_len = p->pin_len;
-  S.max_wf = p->cfg.max_workflows;
-  S.error = &p->ctr->error;
-  static bool attr = false;
-  if (!attr) {
-    SFKV_CUDA(cudaFuncSetAttribute(match_span_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SP_DYN));
-    SFKV_CUDA(cudaFuncSetAttribute(match_span_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SP_DYN));
-    attr = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)nspans);
-  cfg.blockDim = dim3(SP_THREADS);
-  cfg.dynamicSmemBytes = SP_DYN;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  if (a.out_hash) SFKV_CUDA(cudaLaunchKernelEx(&cfg, match_span_kernel<true>, K, S, tm));
-  else SFKV_CUDA(cudaLaunchKernelEx(&cfg, match_span_kernel<false>, K, S, tm));
-  // bookkeeping: this parity now holds [0, nspans); the other parity's [0, nspans) was cleared
-  p->span_base += (uint64_t)nspans;
-  p->span_dirty_lo[b] = 0;
-  p->span_dirty_hi[b] = std::max(p->span_dirty_hi[b], nspans);
-  if (p->span_dirty_hi[o] <= nspans) p->span_dirty_lo[o] = p->span_dirty_hi[o] = 0;
-  else p->span_dirty_lo[o] = std::max(p->span_dirty_lo[o], nspans);
-  p->span_parity = o;
-  return 0;
-}
-
 static int encode_token_map(const MatchArgs& a, CUtensorMap& tm, int64_t rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
@@ -1578,19 +952,6 @@ static int encode_token_map(const MatchArgs& a, CUtensorMap& tm, int64_t rows) {
 
 int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStream_t st) {
   if (a.n <= 0) return 0;
-  if (a.out_M && !a.out_block) {  // match mode (M, optional chained hashes): one span-pass launch
-    MatchKernelArgs K{};
-    K.a = a;
-    K.pin_tok = p->pin_tok;
-    K.pin_groups = pin_groups(p->cfg);
-    K.tok_rows = a.n_tok_bound / 32;
-    CUtensorMap tm;
-    memset(&tm, 0, sizeof(tm));
-    if (K.tok_rows > 0) {
-      if (int rc = encode_token_map(a, tm, K.tok_rows)) return rc;
-    }
-    return launch_span(p, a, K, tm, st);
-  }
   const int64_t ntiles = (a.n_items + WT - 1) / WT;
   const int64_t np = prep_tiles(a.n);
   unsigned long long* ticket = reinterpret_cast<unsigned long long*>(tile_state);

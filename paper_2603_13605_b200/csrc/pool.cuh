@@ -90,11 +90,6 @@ struct sfkv_pool {
   sfkv::Scratch io;            // device copies of host-pointer inputs/outputs
   sfkv::Scratch prep_status;   // match prep look-back statuses (epoch-tagged)
   uint32_t prep_epoch = 0;
-  sfkv::Scratch span_state;    // match span pass: ticket + per-span statuses, two parities
-  int64_t span_cap = 0;        // slots per status array
-  uint64_t span_base = 0;      // tickets taken by earlier launches
-  int span_parity = 0;
-  int64_t span_dirty_lo[2] = {0, 0}, span_dirty_hi[2] = {0, 0};  // written, not yet cleared
   void* host_stage = nullptr;  // pinned host staging
   size_t host_stage_bytes = 0;
   bool exported = false;       // the KV region was handed out as a CUDA IPC handle (fixed)
@@ -102,10 +97,7 @@ struct sfkv_pool {
 
 namespace sfkv {
 
-#ifndef SFKV_PIN_PAD
-#define SFKV_PIN_PAD 0
-#endif
-constexpr int PIN_STRIDE = SFKV_PIN_PAD ? 20 : 16;  // words per pin block (16 tokens + padding)
+constexpr int PIN_STRIDE = 16;  // words per pin block (16 tokens, stored chunk-rotated: pin_rot)
 // Word index of token j of pin block k of workflow wf in pin_tok (see the layout above).
 __host__ __device__ __forceinline__ int64_t pin_tok_index(int64_t wf, int64_t k, int j, int64_t groups) {
   return (wf * (groups << 5) + k) * PIN_STRIDE + j;
