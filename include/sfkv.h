@@ -243,6 +243,10 @@ int sfkv_interner_destroy(sfkv_interner* it);
 int sfkv_interner_reserve(sfkv_interner* it, int32_t table_log2, int64_t arena_bytes);
 /* Arena bytes used / capacity and the current table size (log2). */
 int sfkv_interner_arena(sfkv_interner* it, int64_t* used, int64_t* cap, int32_t* table_log2);
+/* Forgets every string (empty table, id 0 next, arena cursor 0) and keeps the allocations and the
+ * per-batch scratch: a new vocabulary without re-creating the interner. Asynchronous on the
+ * interner's stream. */
+int sfkv_interner_reset(sfkv_interner* it);
 int sfkv_interner_set_stream(sfkv_interner* it, void* cuda_stream);  /* NULL = legacy default stream */
 int sfkv_interner_size(sfkv_interner* it, int64_t* n_ids);
 int sfkv_interner_token(sfkv_interner* it, uint32_t id, char* out, int32_t cap, int32_t* len);

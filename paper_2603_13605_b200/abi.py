@@ -108,6 +108,7 @@ GPU_ONLY = {
     "interner_check": [P],
     "interner_reserve": [P, i32, i64],
     "interner_arena": [P, C.POINTER(i64), C.POINTER(i64), C.POINTER(i32)],
+    "interner_reset": [P],
     "tokenize_batch_dev": [P, i64, P, i64, P, P, i64, P, P, P],
     "pool_export": [P, C.POINTER(IpcHandle)],
     "peer_open": [C.POINTER(IpcHandle), i32, C.POINTER(P)],
@@ -600,6 +601,10 @@ class Interner:
         u, c, lg = C.c_int64(), C.c_int64(), C.c_int32()
         self.api.check("interner_arena", self.api.interner_arena(self.h, C.byref(u), C.byref(c), C.byref(lg)))
         return u.value, c.value, lg.value
+
+    def reset(self):
+        """Forget every string (sfkv_interner_reset); allocations and batch scratch are kept."""
+        self.api.check("interner_reset", self.api.interner_reset(self.h))
 
     def reserve(self, table_log2, arena_bytes):
         """Grow in place (sfkv_interner_reserve); every existing string keeps its id."""

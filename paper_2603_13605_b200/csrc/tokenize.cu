@@ -29,7 +29,12 @@
 //                       the batch brings no new string (steady state).
 //   tok_final* kernels  duplicates read the published ids; per-request token offsets
 // Byte-stream work, HBM/latency-bound; no tensor cores.
+#include <cooperative_groups.h>
+#include <cooperative_groups/reduce.h>
+
 #include "pool.cuh"
+
+namespace cg = cooperative_groups;
 
 struct sfkv_interner {
   int32_t device = 0;
@@ -68,7 +73,7 @@ constexpr uint32_t TOK_PENDING = 0xffffffffu;
 // 4 KiB 0.380, 8 KiB 0.465 per C2 batch)
 constexpr int CHUNK_THREADS = SFKV_TOK_CHUNK_THREADS;
 constexpr int CHUNK = CHUNK_THREADS * 16;
-constexpr int RANK_TILE = 8192;     // tokens per CTA of the rank pass (256 threads x 32)
+constexpr int RANK_TILE = 1024;     // tokens per CTA tile of the rank pass (256 threads x 4)
 enum : int { TERR_COLLISION = 1, TERR_ARENA = 2, TERR_IDS = 4, TERR_TABLE = 8 };
 // ctr: [0] ids, [1] arena cursor, [2] error, [3] new bytes, [4] pending, [5] new ids (batch)
 
@@ -128,6 +133,8 @@ struct TokArgs {
   int32_t* pend_len;
   uint8_t* tnew;         // [token bound] owner flags (kept zero between batches)
   int64_t* tile_cnt;     // [rank tiles + 1]
+  int64_t* tile_bytes;   // [rank tiles + 1] bytes of the tile's new strings (arena offsets)
+  int32_t* tlen;         // [token bound] byte length of pending tokens
   int64_t* tok_off;      // out [n_req + 1]
   uint32_t* tok;         // out
   int64_t* n_tokens;     // out (device scalar)
@@ -367,8 +374,14 @@ __device__ void probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned l
     return;
   }
   a.tstart[t] = start;
+  a.tlen[t] = len;
   atomicMin(reinterpret_cast<unsigned long long*>(a.owner + found), (unsigned long long)t);
-  const unsigned long long j = atomicAdd(a.ctr + 4, 1ull);
+  // one list append per group of converged threads (a cold batch appends every token: per-thread
+  // atomics on one counter serialise in one L2 slice)
+  cg::coalesced_group g = cg::coalesced_threads();
+  unsigned long long j0 = 0;
+  if (g.thread_rank() == 0) j0 = atomicAdd(a.ctr + 4, (unsigned long long)g.size());
+  const unsigned long long j = g.shfl(j0, 0) + g.thread_rank();
   a.pend_t[j] = t;
   a.pend_slot[j] = found;
   a.pend_len[j] = len;
@@ -385,8 +398,12 @@ __global__ void tok_resolve_kernel(TokArgs a) {
     const int64_t o = a.owner[sl];
     if (o == t) {
       a.tnew[t] = 1;
-      atomicAdd(a.ctr + 5, 1ull);
-      atomicAdd(a.ctr + 3, (unsigned long long)len);
+      cg::coalesced_group g = cg::coalesced_threads();
+      const unsigned long long bytes = cg::reduce(g, (unsigned long long)len, cg::plus<unsigned long long>());
+      if (g.thread_rank() == 0) {
+        atomicAdd(a.ctr + 5, (unsigned long long)g.size());
+        atomicAdd(a.ctr + 3, bytes);
+      }
     } else if (!(a.slots[sl].key >> 63) && !bytes_equal(a.text + a.tstart[t], a.text + a.tstart[o], len)) {
       atomicOr(a.ctr + 2, (unsigned long long)TERR_COLLISION);
     }
@@ -405,81 +422,97 @@ __global__ void tok_check_kernel(TokArgs a) {
 // over tiles, an in-tile block scan). Every pass exits at once when the batch has no new string.
 __global__ void __launch_bounds__(256) rank_count_kernel(TokArgs a) {
   pdl_enter();
-  using BR = cub::BlockReduce<int, 256>;
+  using BR = cub::BlockReduce<int2, 256>;
   __shared__ typename BR::TempStorage tmp;
   const int64_t nt = *a.n_tokens;
   if (a.ctr[5] == 0 || a.ctr[2]) return;  // steady state: no new string
   for (int64_t tile = blockIdx.x; tile * RANK_TILE < nt; tile += gridDim.x) {
     const int64_t t0 = tile * RANK_TILE;
-    int c = 0;
+    int2 c = make_int2(0, 0);  // new strings, their bytes
     for (int k = 0; k < RANK_TILE / 256; ++k) {
       const int64_t t = t0 + (int64_t)k * 256 + threadIdx.x;
-      if (t < nt) c += a.tnew[t];
+      if (t < nt && a.tnew[t]) {
+        c.x += 1;
+        c.y += a.tlen[t];
+      }
     }
-    c = BR(tmp).Sum(c);
-    if (threadIdx.x == 0) a.tile_cnt[tile] = c;
+    c = BR(tmp).Reduce(c, [](int2 x, int2 y) { return make_int2(x.x + y.x, x.y + y.y); });
+    if (threadIdx.x == 0) {
+      a.tile_cnt[tile] = c.x;
+      a.tile_bytes[tile] = c.y;
+    }
     __syncthreads();  // tmp reused
   }
 }
 
 __global__ void __launch_bounds__(1024) rank_scan_kernel(TokArgs a) {
   pdl_enter();
-  using BS = cub::BlockScan<int64_t, 1024>;
+  using BS = cub::BlockScan<longlong2, 1024>;
   __shared__ typename BS::TempStorage tmp;
-  __shared__ int64_t carry;
+  __shared__ longlong2 carry;
   const int64_t nt = *a.n_tokens;
   if (a.ctr[5] == 0 || a.ctr[2]) return;
   const int64_t ntiles = (nt + RANK_TILE - 1) / RANK_TILE;
-  if (threadIdx.x == 0) carry = 0;
+  if (threadIdx.x == 0) carry = make_longlong2(0, 0);
   __syncthreads();
+  auto add = [](longlong2 x, longlong2 y) { return make_longlong2(x.x + y.x, x.y + y.y); };
   for (int64_t b = 0; b < ntiles; b += 1024) {
     const int64_t i = b + threadIdx.x;
-    int64_t v = i < ntiles ? a.tile_cnt[i] : 0, ex, tot;
-    BS(tmp).ExclusiveSum(v, ex, tot);
-    if (i < ntiles) a.tile_cnt[i] = carry + ex;
+    longlong2 v = i < ntiles ? make_longlong2(a.tile_cnt[i], a.tile_bytes[i]) : make_longlong2(0, 0), ex, tot;
+    BS(tmp).ExclusiveScan(v, ex, make_longlong2(0, 0), add, tot);
+    if (i < ntiles) {
+      a.tile_cnt[i] = carry.x + ex.x;
+      a.tile_bytes[i] = carry.y + ex.y;
+    }
     __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
+    if (threadIdx.x == 0) carry = add(carry, tot);
     __syncthreads();
   }
 }
 
 __device__ void rank_publish_tile(const TokArgs& a, int64_t tile, int64_t nt,
-                                  typename cub::BlockScan<int, 256>::TempStorage& tmp) {
-  using BS = cub::BlockScan<int, 256>;
+                                  typename cub::BlockScan<int2, 256>::TempStorage& tmp) {
+  using BS = cub::BlockScan<int2, 256>;
   const int64_t t0 = tile * RANK_TILE;
   constexpr int PT = RANK_TILE / 256;
   const int64_t tb = t0 + (int64_t)threadIdx.x * PT;  // blocked
-  int c = 0;
+  int2 c = make_int2(0, 0);
   uint32_t f = 0;
-  for (int k = 0; k < PT; ++k)
+  int lens[PT];
+#pragma unroll
+  for (int k = 0; k < PT; ++k) {
+    lens[k] = 0;
     if (tb + k < nt && a.tnew[tb + k]) {
       f |= 1u << k;
-      ++c;
+      lens[k] = a.tlen[tb + k];
+      c.x += 1;
+      c.y += lens[k];
     }
-  int ex;
-  BS(tmp).ExclusiveSum(c, ex);
-  int64_t id = (int64_t)a.ctr[0] + a.tile_cnt[tile] + ex;
-  while (f) {
-    const int k = __ffs(f) - 1;
-    f &= f - 1;
+  }
+  int2 ex;
+  BS(tmp).ExclusiveScan(c, ex, make_int2(0, 0), [](int2 x, int2 y) { return make_int2(x.x + y.x, x.y + y.y); });
+  // ids in first-occurrence order; arena bytes in the same order (offsets from the byte scan)
+  int64_t id = (int64_t)a.ctr[0] + a.tile_cnt[tile] + ex.x;
+  int64_t off = (int64_t)a.ctr[1] + a.tile_bytes[tile] + ex.y;
+#pragma unroll
+  for (int k = 0; k < PT; ++k) {
+    if (!((f >> k) & 1u)) continue;
     const int64_t t = tb + k;
     a.tnew[t] = 0;
-    const int64_t s = a.tstart[t];
-    int64_t e = s + 1;
-    while (e < a.n_bytes && !is_space(a.text[e]) && !is_mstart(a, e)) ++e;
-    const int len = (int)(e - s);
-    const unsigned long long off = atomicAdd(a.ctr + 1, (unsigned long long)len);
-    for (int i = 0; i < len; ++i) a.arena[off + i] = a.text[s + i];
-    a.id_off[id] = (int64_t)off;
+    const uint8_t* src = a.text + a.tstart[t];
+    const int len = lens[k];
+    for (int i = 0; i < len; ++i) a.arena[off + i] = src[i];
+    a.id_off[id] = off;
     a.id_len[id] = len;
     a.tok[t] = (uint32_t)id;
     ++id;
+    off += len;
   }
 }
 
 __global__ void __launch_bounds__(256) rank_publish_kernel(TokArgs a) {
   pdl_enter();
-  __shared__ typename cub::BlockScan<int, 256>::TempStorage tmp;
+  __shared__ typename cub::BlockScan<int2, 256>::TempStorage tmp;
   const int64_t nt = *a.n_tokens;
   if (a.ctr[5] == 0 || a.ctr[2]) return;  // steady state: no new string
   for (int64_t tile = blockIdx.x; tile * RANK_TILE < nt; tile += gridDim.x) {
@@ -582,7 +615,10 @@ __global__ void tok_owner_reset_kernel(TokArgs a) {  // and the message-start bi
 __global__ void tok_commit_kernel(TokArgs a) {  // advance the id counter once per batch
   pdl_enter();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
-    if (!a.ctr[2]) a.ctr[0] += a.ctr[5];
+    if (!a.ctr[2]) {
+      a.ctr[0] += a.ctr[5];  // ids
+      a.ctr[1] += a.ctr[3];  // arena cursor (the batch's strings were placed by the byte scan)
+    }
     a.ctr[3] = a.ctr[4] = a.ctr[5] = 0;  // batch counters zero for the next batch
   }
 }
@@ -643,6 +679,7 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   const size_t o_cnt = cv.take<int64_t>(nchunks + 1),
                o_co = cv.take<int64_t>(nchunks + 1), o_ts = cv.take<int64_t>(tb), o_pt = cv.take<int64_t>(tb),
                o_ps = cv.take<int64_t>(tb), o_pl = cv.take<int32_t>(tb), o_tc = cv.take<int64_t>(nrt + 1),
+               o_tby = cv.take<int64_t>(nrt + 1), o_tl = cv.take<int32_t>(tb),
                o_tmp = cv.take<int64_t>(scan_scratch_elems(nchunks));
   if (int rc = it->scratch.ensure(cv.off)) return rc;
   if (it->mbits.bytes < nwords * sizeof(uint32_t)) {  // grown: zero once, then kept zero
@@ -673,6 +710,8 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   a.pend_len = reinterpret_cast<int32_t*>(base + o_pl);
   a.tnew = it->tnew;
   a.tile_cnt = reinterpret_cast<int64_t*>(base + o_tc);
+  a.tile_bytes = reinterpret_cast<int64_t*>(base + o_tby);
+  a.tlen = reinterpret_cast<int32_t*>(base + o_tl);
   a.tok_off = tok_off;
   a.tok = tok;
   a.n_tokens = n_tokens;
@@ -781,6 +820,15 @@ int sfkv_interner_create(int32_t device, int32_t table_log2, int64_t arena_bytes
     return cuda_fail(e, "interner init");
   }
   *out = it;
+  return 0;
+}
+
+int sfkv_interner_reset(sfkv_interner* it) {
+  if (!it) return fail(SFKV_EINVAL, "interner_reset: null interner");
+  DeviceGuard g(it->device);
+  interner_init_kernel<<<grid_for(it->slots_n, 256, 4096), 256, 0, it->stream>>>(it->slots, it->owner, it->slots_n);
+  SFKV_LAUNCH_CHECK("interner_init_kernel");
+  SFKV_CUDA(cudaMemsetAsync(it->ctr, 0, 8 * sizeof(unsigned long long), it->stream));
   return 0;
 }
 
