@@ -578,10 +578,10 @@ __device__ __forceinline__ void tile_finish(const MatchKernelArgs& K, int64_t ti
 // cover the window -> tokens/pin-tokens round trips.
 // 16 CTAs (32 warps) per SM at <= 64 registers: no spills (48 registers spilled and 10 CTAs of 4 warps
 // measured 2 us slower).
-template <bool STAGED>
 #ifndef SFKV_MB_MINB
 #define SFKV_MB_MINB 16
 #endif
+template <bool STAGED>
 __global__ void __launch_bounds__(BLOCK_THREADS, SFKV_MB_MINB) match_block_kernel(MatchKernelArgs K,
                                                                        const __grid_constant__ CUtensorMap tmap) {
   __shared__ __align__(1024) uint32_t s_tok[STAGED ? BLOCK_THREADS / 32 : 1][STAGED ? 768 : 4];  // 18 rows, 1 KB-aligned
@@ -857,107 +857,79 @@ __global__ void __launch_bounds__(LR_THREADS, SFKV_LR_MINB) lookup_req_kernel(Ma
     }
     return staged;
   };
-  // Two-stage software pipeline over the request's tiles: iteration i computes tile i's chained
-  // keys and issues its first table probe, then finishes tile i-1 (probe chain, token verify
-  // against the resident block, parent link, outputs) — so the probe round trip of a tile overlaps
-  // the next tile's token wait and hashing instead of stalling the warp.
   bool staged = ntile > 0 ? issue(0) : false;
   uint64_t carry = 0;
   int32_t prev_raw = -1;
   bool run = true;
   int64_t lead = 0;
-  uint32_t tp[BT];  // tile i-1: tokens, key, first probed slot, coordinates
-  uint64_t cp = 0;
-  uint4 wp = make_uint4(0, 0, 0xffffffffu, 0);
-  bool vp = false, fp = false;
-  int64_t kp = 0;
-#pragma unroll
-  for (int j = 0; j < BT; ++j) tp[j] = 0u;
-  for (int64_t i = 0; i <= ntile; ++i) {
+  for (int64_t i = 0; i < ntile; ++i) {
+    const bool staged_next = i + 1 < ntile ? issue(i + 1) : false;
+    const int64_t k = i * WT + lane;
+    const bool valid = k < nb;
+    const int64_t start = to + k * BT;
+    const int nval = valid ? (int)min((int64_t)BT, (int64_t)len - k * BT) : 0;
     uint32_t t[BT];
-    uint64_t c = 0;
-    uint4 w = make_uint4(0, 0, 0xffffffffu, 0);
-    bool valid = false, full = false;
-    int64_t k = 0;
-    if (i < ntile) {
-      const bool staged_next = i + 1 < ntile ? issue(i + 1) : false;
-      k = i * WT + lane;
-      valid = k < nb;
-      full = valid && k < nfull;
-      const int64_t start = to + k * BT;
-      const int nval = valid ? (int)min((int64_t)BT, (int64_t)len - k * BT) : 0;
-      if (staged) {
-        mbar_wait(&s_bar[warp][i & 1], (uint32_t)((i >> 1) & 1));
-        if (valid) load_block_swz(s_tok[warp][i & 1], (int)(start - (((to + i * WT * BT) >> 5) << 5)), nval, t);
-      } else if (valid) {
-        load_block(A.tok, start, nval, tok_total, t);
-      }
-      if (!valid) {
-#pragma unroll
-        for (int j = 0; j < BT; ++j) t[j] = 0u;
-      }
-      __syncwarp();
-      // chained key: warp inclusive scan of the digests on top of the request's running sum
-      uint64_t v = valid ? block_digest_words((uint64_t)k, (uint32_t)nval, t) : 0ull;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint64_t u = __shfl_up_sync(0xffffffffu, v, d);
-        if (lane >= d) v += u;
-      }
-      v += carry;
-      carry = __shfl_sync(0xffffffffu, v, 31);
-      c = chain_finalize(v);
-      if (full) w = __ldg(reinterpret_cast<const uint4*>(K.slots + (c & K.slot_mask)));  // first probe
-      staged = staged_next;
+    if (staged) {
+      mbar_wait(&s_bar[warp][i & 1], (uint32_t)((i >> 1) & 1));
+      if (valid) load_block_swz(s_tok[warp][i & 1], (int)(start - (((to + i * WT * BT) >> 5) << 5)), nval, t);
+    } else if (valid) {
+      load_block(A.tok, start, nval, tok_total, t);
     }
-    if (i > 0) {  // finish tile i-1 (full blocks only; a pending claim reads -1)
-      int32_t raw = -1;
-      if (fp) {
-        uint64_t sl = cp & K.slot_mask;
-        uint4 x = wp;
-        for (;;) {
-          const uint64_t key = (uint64_t)x.x | ((uint64_t)x.y << 32);
-          if (key == cp) {
-            raw = (int32_t)x.z;
-            break;
-          }
-          if (key == KEY_EMPTY) break;
-          sl = (sl + 1) & K.slot_mask;
-          x = __ldg(reinterpret_cast<const uint4*>(K.slots + sl));
-        }
-      }
-      bool eq = false;
-      int32_t par = -1;
-      if (raw >= 0) {
-        uint32_t q[BT];
-        load16_aligned(K.blk_tok + (int64_t)raw * BT, q);
-        par = __ldg(&K.blk_parent[raw]);
-        eq = true;
+    if (!valid) {
 #pragma unroll
-        for (int j = 0; j < BT; ++j) eq &= q[j] == tp[j];
-      }
-      const int32_t up_raw = __shfl_up_sync(0xffffffffu, raw, 1);
-      const int32_t p_raw = lane > 0 ? up_raw : prev_raw;
-      const int32_t id = (eq && (kp == 0 || par == p_raw)) ? raw : -1;
-      prev_raw = __shfl_sync(0xffffffffu, raw, 31);
-      if (vp) A.out_block[bo + kp] = id;
-      const unsigned miss = __ballot_sync(0xffffffffu, vp && id < 0);
-      if (run) {
-        if (miss) {
-          lead += __ffs(miss) - 1;
-          run = false;
-        } else {
-          lead += min((int64_t)WT, nb - (i - 1) * WT);
+      for (int j = 0; j < BT; ++j) t[j] = 0u;
+    }
+    __syncwarp();
+    // chained key: warp inclusive scan of the digests on top of the request's running sum
+    uint64_t v = valid ? block_digest_words((uint64_t)k, (uint32_t)nval, t) : 0ull;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t u = __shfl_up_sync(0xffffffffu, v, d);
+      if (lane >= d) v += u;
+    }
+    v += carry;
+    carry = __shfl_sync(0xffffffffu, v, 31);
+    const uint64_t c = chain_finalize(v);
+    // probe (full blocks only; a pending claim reads -1), then verify + parent together
+    int32_t raw = -1;
+    if (valid && k < nfull) {
+      uint64_t sl = c & K.slot_mask;
+      for (;;) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(K.slots + sl));
+        const uint64_t key = (uint64_t)w.x | ((uint64_t)w.y << 32);
+        if (key == c) {
+          raw = (int32_t)w.z;
+          break;
         }
+        if (key == KEY_EMPTY) break;
+        sl = (sl + 1) & K.slot_mask;
       }
     }
+    bool eq = false;
+    int32_t par = -1;
+    if (raw >= 0) {
+      uint32_t q[BT];
+      load16_aligned(K.blk_tok + (int64_t)raw * BT, q);
+      par = __ldg(&K.blk_parent[raw]);
+      eq = true;
 #pragma unroll
-    for (int j = 0; j < BT; ++j) tp[j] = t[j];
-    cp = c;
-    wp = w;
-    vp = valid;
-    fp = full;
-    kp = k;
+      for (int j = 0; j < BT; ++j) eq &= q[j] == t[j];
+    }
+    const int32_t up_raw = __shfl_up_sync(0xffffffffu, raw, 1);
+    const int32_t p_raw = lane > 0 ? up_raw : prev_raw;
+    const int32_t id = (eq && (k == 0 || par == p_raw)) ? raw : -1;
+    prev_raw = __shfl_sync(0xffffffffu, raw, 31);
+    if (valid) A.out_block[bo + k] = id;
+    const unsigned miss = __ballot_sync(0xffffffffu, valid && id < 0);
+    if (run) {
+      if (miss) {
+        lead += __ffs(miss) - 1;
+        run = false;
+      } else {
+        lead += min((int64_t)WT, nb - i * WT);
+      }
+    }
+    staged = staged_next;
   }
   if (lane == 0) A.out_hit[r] = lead * BT;
 }

@@ -118,6 +118,25 @@ __device__ __forceinline__ unsigned long long tok_key(const uint8_t* p, int len)
   return h ? h : 1;
 }
 
+// tok_key of a token staged in shared memory at byte s0 (the buffer is 8-B aligned and readable
+// 16 bytes past the token): the same key, read as 8-byte words (two aligned loads + a funnel
+// shift each) instead of byte by byte.
+__device__ __forceinline__ unsigned long long ld8_smem(const uint8_t* sb, int pos) {
+  const int a8 = pos & ~7, b8 = (pos & 7) * 8;
+  const unsigned long long lo = *reinterpret_cast<const unsigned long long*>(sb + a8);
+  const unsigned long long hi = *reinterpret_cast<const unsigned long long*>(sb + a8 + 8);
+  return b8 ? (lo >> b8) | (hi << (64 - b8)) : lo;
+}
+__device__ __forceinline__ unsigned long long tok_key_smem(const uint8_t* sb, int s0, int len) {
+  if (len <= 7) return (1ull << 63) | ((unsigned long long)len << 56) | (ld8_smem(sb, s0) & ((1ull << (8 * len)) - 1));
+  unsigned long long h = 0x9E3779B97F4A7C15ull ^ (unsigned long long)len;
+  int i = 0;
+  for (; i + 8 <= len; i += 8) h = mix64(h + ld8_smem(sb, s0 + i) * 0xD6E8FEB86659FD93ull);
+  if (i < len) h = mix64(h + (ld8_smem(sb, s0 + i) & ((1ull << (8 * (len - i))) - 1)) * 0xD6E8FEB86659FD93ull);
+  h = mix64(h) & ~(1ull << 63);
+  return h ? h : 1;
+}
+
 struct TokArgs {
   int64_t n_req;
   const int64_t* req_msg_off;
@@ -129,8 +148,7 @@ struct TokArgs {
   int64_t* chunk_off;    // [nchunks + 1]
   int64_t* tstart;       // [token bound] byte start of pending tokens (claims / duplicates)
   int64_t* pend_t;       // pending tokens (claims / duplicates of new strings)
-  int64_t* pend_slot;
-  int32_t* pend_len;
+  int64_t* pend_slot;    // [token bound] slot of a pending token (by token index)
   uint8_t* tnew;         // [token bound] owner flags (kept zero between batches)
   int64_t* tile_cnt;     // [rank tiles + 1]
   int64_t* tile_bytes;   // [rank tiles + 1] bytes of the tile's new strings (arena offsets)
@@ -237,8 +255,8 @@ __device__ __forceinline__ bool bytes_equal(const uint8_t* x, const uint8_t* y, 
 __device__ __forceinline__ bool is_mstart(const TokArgs& a, int64_t i) {
   return (a.mbits[i >> 5] >> (i & 31)) & 1u;
 }
-__device__ void probe_token(const TokArgs& a, int64_t t, int64_t start, const uint8_t* p, int len);
-__device__ void probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned long long key, const uint8_t* p,
+__device__ bool probe_token(const TokArgs& a, int64_t t, int64_t start, const uint8_t* p, int len);
+__device__ bool probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned long long key, const uint8_t* p,
                           int len);
 
 // Token starts of the chunk in order (CTA scan) into a shared list, and every token probed right
@@ -254,7 +272,7 @@ __global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
   pdl_enter();
   using BS = cub::BlockScan<int, CHUNK_THREADS>;
   __shared__ typename BS::TempStorage tmp;
-  __shared__ __align__(16) uint8_t sb[CHUNK + OVER];
+  __shared__ __align__(16) uint8_t sb[CHUNK + OVER + 16];  // + 16: word reads past a token's end
   __shared__ uint32_t sbits[(CHUNK + OVER) / 32];
   const int64_t c0 = (int64_t)blockIdx.x * CHUNK;
   const int64_t base = c0 + (int64_t)threadIdx.x * 16;
@@ -279,6 +297,12 @@ __global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
   }
   __shared__ uint16_t slist[CHUNK];
   __shared__ uint32_t sbnd[(CHUNK + OVER) / 32 + 1];
+  constexpr int PW = CHUNK / 32;  // pending bitmap words (<= CHUNK tokens: every byte may start a message)
+  __shared__ uint32_t s_pend[PW];
+  __shared__ int s_any_pend;
+  __shared__ unsigned long long s_pbase;
+  if (threadIdx.x < PW) s_pend[threadIdx.x] = 0u;
+  if (threadIdx.x == 0) s_any_pend = 0;
   __syncthreads();
   // from the staged bytes: 16 boundary bits (space | message start) per thread into the bitmap, and
   // the thread's token starts (non-space after a space or at a message start)
@@ -305,6 +329,7 @@ __global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
   const int64_t tb0 = a.chunk_off[blockIdx.x];
   for (int i = threadIdx.x; i < total; i += CHUNK_THREADS) {
     const int s0 = slist[i];
+    bool pend;
     int w = (s0 + 1) >> 5;
     uint32_t bits = sbnd[w] & (~0u << ((s0 + 1) & 31));
     while (!bits && (w + 1) * 32 < stage_end) bits = sbnd[++w];
@@ -317,27 +342,46 @@ __global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
         const unsigned long long hi = *reinterpret_cast<const unsigned long long*>(sb + a8 + 8);
         unsigned long long raw = b8 ? (lo >> b8) | (hi << (64 - b8)) : lo;
         raw &= (1ull << (8 * len)) - 1;
-        probe_key(a, tb0 + i, c0 + s0, (1ull << 63) | ((unsigned long long)len << 56) | raw, sb + s0, len);
+        pend = probe_key(a, tb0 + i, c0 + s0, (1ull << 63) | ((unsigned long long)len << 56) | raw, sb + s0, len);
       } else {
-        probe_token(a, tb0 + i, c0 + s0, sb + s0, len);
+        pend = probe_key(a, tb0 + i, c0 + s0, tok_key_smem(sb, s0, len), sb + s0, len);
       }
     } else {
       int64_t g = c0 + s0 + 1;
       while (g < a.n_bytes && !is_space(a.text[g]) && !is_mstart(a, g)) ++g;
-      probe_token(a, tb0 + i, c0 + s0, a.text + c0 + s0, (int)(g - (c0 + s0)));
+      pend = probe_token(a, tb0 + i, c0 + s0, a.text + c0 + s0, (int)(g - (c0 + s0)));
     }
+    if (pend) {
+      atomicOr(&s_pend[i >> 5], 1u << (i & 31));
+      s_any_pend = 1;
+    }
+  }
+  // pending tokens join the batch list with one global atomic per chunk (a cold batch makes every
+  // token pending: per-token atomics on one counter serialise in one L2 slice)
+  __syncthreads();
+  if (!s_any_pend) return;
+  const int nw = (total + 31) / 32;
+  int c = threadIdx.x < nw ? __popc(s_pend[threadIdx.x]) : 0, ex;
+  BS(tmp).ExclusiveSum(c, ex);
+  if (threadIdx.x == nw - 1) s_pbase = atomicAdd(a.ctr + 4, (unsigned long long)(ex + c));
+  __syncthreads();
+  if (threadIdx.x < nw) {
+    unsigned long long j = s_pbase + ex;
+    for (uint32_t m = s_pend[threadIdx.x]; m; m &= m - 1) a.pend_t[j++] = tb0 + threadIdx.x * 32 + __ffs(m) - 1;
   }
 }
 
 // Probe one token (bytes p[0..len), position t): published strings resolve here (short keys
 // exactly, long keys verified against the arena); claims and duplicates of this batch's new
 // strings go to the pending list.
-__device__ void probe_token(const TokArgs& a, int64_t t, int64_t start, const uint8_t* p, int len) {
-  probe_key(a, t, start, tok_key(p, len), p, len);
+__device__ bool probe_token(const TokArgs& a, int64_t t, int64_t start, const uint8_t* p, int len) {
+  return probe_key(a, t, start, tok_key(p, len), p, len);
 }
 
-// (start: the token's byte position, recorded only for pending tokens)
-__device__ void probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned long long key, const uint8_t* p,
+// (start: the token's byte position, recorded only for pending tokens). Returns true when the
+// token is pending (a claim or a duplicate of this batch's new string): its start, length and
+// slot are recorded by token index and the caller appends it to the pending list.
+__device__ bool probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned long long key, const uint8_t* p,
                           int len) {
   // home slot by Fibonacci hashing: the top bits of key x 2^64/phi spread the raw bytes of short
   // keys (one multiply; mix64 here cost 7.5 % of the batch, the probe loop is issue-bound)
@@ -365,48 +409,46 @@ __device__ void probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned l
   }
   if (found < 0) {
     atomicOr(a.ctr + 2, (unsigned long long)TERR_TABLE);
-    return;
+    return false;
   }
   if (id != TOK_PENDING) {  // published before this batch
     if (!(key >> 63) && (a.id_len[id] != len || !bytes_equal(p, a.arena + a.id_off[id], len)))
       atomicOr(a.ctr + 2, (unsigned long long)TERR_COLLISION);
     a.tok[t] = id;
-    return;
+    return false;
   }
   a.tstart[t] = start;
   a.tlen[t] = len;
+  a.pend_slot[t] = found;
   atomicMin(reinterpret_cast<unsigned long long*>(a.owner + found), (unsigned long long)t);
-  // one list append per group of converged threads (a cold batch appends every token: per-thread
-  // atomics on one counter serialise in one L2 slice)
-  cg::coalesced_group g = cg::coalesced_threads();
-  unsigned long long j0 = 0;
-  if (g.thread_rank() == 0) j0 = atomicAdd(a.ctr + 4, (unsigned long long)g.size());
-  const unsigned long long j = g.shfl(j0, 0) + g.thread_rank();
-  a.pend_t[j] = t;
-  a.pend_slot[j] = found;
-  a.pend_len[j] = len;
+  return true;
 }
 
 // Pending tokens: the lowest position owns a new string; the others are duplicates (long keys
 // compare bytes with the owner's: a 64-bit hash collision fails the batch loudly).
-__global__ void tok_resolve_kernel(TokArgs a) {
+__global__ void __launch_bounds__(256) tok_resolve_kernel(TokArgs a) {
   pdl_enter();
+  using BR = cub::BlockReduce<longlong2, 256>;
+  __shared__ typename BR::TempStorage tmp;
   const int64_t np = (int64_t)a.ctr[4];
+  longlong2 own = make_longlong2(0, 0);  // this thread's new strings and their bytes
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = a.pend_t[j], sl = a.pend_slot[j];
-    const int len = a.pend_len[j];
+    const int64_t t = a.pend_t[j], sl = a.pend_slot[t];
+    const int len = a.tlen[t];
     const int64_t o = a.owner[sl];
     if (o == t) {
       a.tnew[t] = 1;
-      cg::coalesced_group g = cg::coalesced_threads();
-      const unsigned long long bytes = cg::reduce(g, (unsigned long long)len, cg::plus<unsigned long long>());
-      if (g.thread_rank() == 0) {
-        atomicAdd(a.ctr + 5, (unsigned long long)g.size());
-        atomicAdd(a.ctr + 3, bytes);
-      }
+      own.x += 1;
+      own.y += len;
     } else if (!(a.slots[sl].key >> 63) && !bytes_equal(a.text + a.tstart[t], a.text + a.tstart[o], len)) {
       atomicOr(a.ctr + 2, (unsigned long long)TERR_COLLISION);
     }
+  }
+  // one pair of counter atomics per CTA
+  own = BR(tmp).Reduce(own, [](longlong2 x, longlong2 y) { return make_longlong2(x.x + y.x, x.y + y.y); });
+  if (threadIdx.x == 0 && own.x) {
+    atomicAdd(a.ctr + 5, (unsigned long long)own.x);
+    atomicAdd(a.ctr + 3, (unsigned long long)own.y);
   }
 }
 
@@ -470,8 +512,22 @@ __global__ void __launch_bounds__(1024) rank_scan_kernel(TokArgs a) {
   }
 }
 
-__device__ void rank_publish_tile(const TokArgs& a, int64_t tile, int64_t nt,
-                                  typename cub::BlockScan<int2, 256>::TempStorage& tmp) {
+// Owners ranked by position get consecutive ids and consecutive arena bytes, so a tile's new
+// strings form one contiguous arena range, and their source bytes one contiguous text range (from
+// the first owner's start to the last owner's end). Both are staged in shared memory: the text
+// range is read with coalesced loads, each owner's bytes are moved inside shared memory, and the
+// arena range is written with coalesced stores (a tile whose ranges exceed the staging buffers
+// copies byte by byte from global memory instead).
+constexpr int PUB_TXT = 20 * 1024, PUB_OUT = 20 * 1024;
+struct PubSmem {
+  typename cub::BlockScan<int2, 256>::TempStorage scan;
+  uint8_t txt[PUB_TXT];
+  uint8_t out[PUB_OUT];
+  int64_t lo, hi;
+  int2 agg;
+};
+
+__device__ void rank_publish_tile(const TokArgs& a, int64_t tile, int64_t nt, PubSmem& S) {
   using BS = cub::BlockScan<int2, 256>;
   const int64_t t0 = tile * RANK_TILE;
   constexpr int PT = RANK_TILE / 256;
@@ -479,45 +535,77 @@ __device__ void rank_publish_tile(const TokArgs& a, int64_t tile, int64_t nt,
   int2 c = make_int2(0, 0);
   uint32_t f = 0;
   int lens[PT];
+  int64_t ts[PT];
 #pragma unroll
   for (int k = 0; k < PT; ++k) {
     lens[k] = 0;
+    ts[k] = 0;
     if (tb + k < nt && a.tnew[tb + k]) {
       f |= 1u << k;
       lens[k] = a.tlen[tb + k];
+      ts[k] = a.tstart[tb + k];
       c.x += 1;
       c.y += lens[k];
     }
   }
-  int2 ex;
-  BS(tmp).ExclusiveScan(c, ex, make_int2(0, 0), [](int2 x, int2 y) { return make_int2(x.x + y.x, x.y + y.y); });
-  // ids in first-occurrence order; arena bytes in the same order (offsets from the byte scan)
+  int2 ex, agg;
+  BS(S.scan).ExclusiveScan(c, ex, make_int2(0, 0), [](int2 x, int2 y) { return make_int2(x.x + y.x, x.y + y.y); },
+                           agg);
+  if (agg.x == 0) return;  // uniform: no new string in this tile
+  // the tile's first owner (global rank 0 in the tile) and last owner fix the text range
+  int64_t first = -1, last_end = -1;
+#pragma unroll
+  for (int k = 0; k < PT; ++k)
+    if ((f >> k) & 1u) {
+      if (first < 0) first = ts[k];
+      last_end = ts[k] + lens[k];
+    }
+  if (f && ex.x == 0) S.lo = first;
+  if (f && ex.x + c.x == agg.x) S.hi = last_end;
+  __syncthreads();
+  const int64_t lo = S.lo, hi = S.hi;
+  const int64_t base = (int64_t)a.ctr[1] + a.tile_bytes[tile];  // arena offset of the tile's first byte
   int64_t id = (int64_t)a.ctr[0] + a.tile_cnt[tile] + ex.x;
-  int64_t off = (int64_t)a.ctr[1] + a.tile_bytes[tile] + ex.y;
+  const bool staged = hi - lo <= PUB_TXT && agg.y <= PUB_OUT;
+  if (staged) {
+    for (int64_t i = threadIdx.x; i < hi - lo; i += 256) S.txt[i] = a.text[lo + i];
+    __syncthreads();
+  }
+  int off = ex.y;  // tile-relative arena offset of this thread's first string
 #pragma unroll
   for (int k = 0; k < PT; ++k) {
     if (!((f >> k) & 1u)) continue;
     const int64_t t = tb + k;
-    a.tnew[t] = 0;
-    const uint8_t* src = a.text + a.tstart[t];
     const int len = lens[k];
-    for (int i = 0; i < len; ++i) a.arena[off + i] = src[i];
-    a.id_off[id] = off;
+    a.tnew[t] = 0;
+    if (staged) {
+      const uint8_t* src = S.txt + (ts[k] - lo);
+      for (int i = 0; i < len; ++i) S.out[off + i] = src[i];
+    } else {
+      const uint8_t* src = a.text + ts[k];
+      uint8_t* dst = a.arena + base + off;
+      for (int i = 0; i < len; ++i) dst[i] = src[i];
+    }
+    a.id_off[id] = base + off;
     a.id_len[id] = len;
     a.tok[t] = (uint32_t)id;
     ++id;
     off += len;
   }
+  if (staged) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < agg.y; i += 256) a.arena[base + i] = S.out[i];
+  }
 }
 
 __global__ void __launch_bounds__(256) rank_publish_kernel(TokArgs a) {
   pdl_enter();
-  __shared__ typename cub::BlockScan<int2, 256>::TempStorage tmp;
+  __shared__ PubSmem S;
   const int64_t nt = *a.n_tokens;
   if (a.ctr[5] == 0 || a.ctr[2]) return;  // steady state: no new string
   for (int64_t tile = blockIdx.x; tile * RANK_TILE < nt; tile += gridDim.x) {
-    rank_publish_tile(a, tile, nt, tmp);
-    __syncthreads();  // tmp reused
+    rank_publish_tile(a, tile, nt, S);
+    __syncthreads();  // shared memory reused
   }
 }
 
@@ -529,7 +617,7 @@ __global__ void tok_final_kernel(TokArgs a) {
   const int64_t np = (int64_t)a.ctr[4];
   const bool failed = a.ctr[2] != 0;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = a.pend_t[j], sl = a.pend_slot[j];
+    const int64_t t = a.pend_t[j], sl = a.pend_slot[t];
     if (a.owner[sl] != t) continue;
     if (failed) {
       a.slots[sl].key = 0;
@@ -544,7 +632,7 @@ __global__ void tok_final2_kernel(TokArgs a) {  // duplicates of new strings
   pdl_enter();
   const int64_t np = (int64_t)a.ctr[4];
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = a.pend_t[j], sl = a.pend_slot[j];
+    const int64_t t = a.pend_t[j], sl = a.pend_slot[t];
     if (a.owner[sl] != t) a.tok[t] = a.slots[sl].id;
   }
 }
@@ -605,7 +693,7 @@ __global__ void tok_owner_reset_kernel(TokArgs a) {  // and the message-start bi
   pdl_enter();
   const int64_t np = (int64_t)a.ctr[4];
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x)
-    a.owner[a.pend_slot[j]] = INT64_MAX;
+    a.owner[a.pend_slot[a.pend_t[j]]] = INT64_MAX;
   for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < a.n_msg; m += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = a.msg_off[m];
     if (i < a.n_bytes) a.mbits[i >> 5] = 0u;
@@ -678,7 +766,7 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   Carver cv;
   const size_t o_cnt = cv.take<int64_t>(nchunks + 1),
                o_co = cv.take<int64_t>(nchunks + 1), o_ts = cv.take<int64_t>(tb), o_pt = cv.take<int64_t>(tb),
-               o_ps = cv.take<int64_t>(tb), o_pl = cv.take<int32_t>(tb), o_tc = cv.take<int64_t>(nrt + 1),
+               o_ps = cv.take<int64_t>(tb), o_tc = cv.take<int64_t>(nrt + 1),
                o_tby = cv.take<int64_t>(nrt + 1), o_tl = cv.take<int32_t>(tb),
                o_tmp = cv.take<int64_t>(scan_scratch_elems(nchunks));
   if (int rc = it->scratch.ensure(cv.off)) return rc;
@@ -707,7 +795,6 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   a.tstart = reinterpret_cast<int64_t*>(base + o_ts);
   a.pend_t = reinterpret_cast<int64_t*>(base + o_pt);
   a.pend_slot = reinterpret_cast<int64_t*>(base + o_ps);
-  a.pend_len = reinterpret_cast<int32_t*>(base + o_pl);
   a.tnew = it->tnew;
   a.tile_cnt = reinterpret_cast<int64_t*>(base + o_tc);
   a.tile_bytes = reinterpret_cast<int64_t*>(base + o_tby);
