@@ -451,6 +451,41 @@ __device__ __forceinline__ void bulk_tensor_2d(void* dst, const CUtensorMap* tm,
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+
+// L2 residency hints (SFKV_L2HINT): the streamed request tokens and pin blocks are read once
+// (evict_first), while the per-block chain sums the block pass writes for the chain pass should
+// still be in L2 when it reads them (evict_last).
+#ifndef SFKV_L2HINT
+#define SFKV_L2HINT 1
+#endif
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_copy_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_tensor_2d_hint(void* dst, const CUtensorMap* tm, int x, int y, uint64_t* bar,
+                                                    uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void st_u64_hint(uint64_t* p, uint64_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
 // Block tokens of a lane whose block starts at word o of a swizzled staged range.
 __device__ __forceinline__ void load_block_swz(const uint32_t* s, int o, int nval, uint32_t* t) {
   const int c0 = o >> 2, sh = o & 3;
@@ -566,7 +601,11 @@ __device__ __forceinline__ void tile_finish(const MatchKernelArgs& K, int64_t ti
     if (hl && hs > 0) v -= base;
     const int64_t item = tile * WT + lane;
     if (c.valid) {
+#if SFKV_L2HINT
+      st_u64_hint(K.local + item, (h << 63) | (v & CHAIN_MASK), l2_policy_last());
+#else
       K.local[item] = (h << 63) | (v & CHAIN_MASK);
+#endif
       if (K.rk) K.rk[item] = (uint32_t)c.r | (c.nval == BT ? RK_FULL : 0u);
     }
     if (lane == 31) K.status[tile] = (h ? ST_INCL : ST_AGG) | (v & CHAIN_MASK);
@@ -581,92 +620,141 @@ __device__ __forceinline__ void tile_finish(const MatchKernelArgs& K, int64_t ti
 #ifndef SFKV_MB_MINB
 #define SFKV_MB_MINB 16
 #endif
+#ifndef SFKV_MB_TPW
+#define SFKV_MB_TPW 1
+#endif
+// Staging of one tile into a warp's buffers: the token range (one 2D tensor-map box) and, per
+// request segment of in-pin blocks, that segment's pin blocks (pin-major: one extent at lane*64 B),
+// all on one mbarrier phase. Returns whether the barrier was armed (something to wait for).
+__device__ __forceinline__ bool stage_tile(const MatchKernelArgs& K, const CUtensorMap* tmap, const Ctx& c,
+                                           bool in_pin, uint32_t* s_tok, uint32_t* s_pin, uint64_t* bar,
+                                           int64_t& a0, bool& staged) {
+  const int lane = threadIdx.x & 31;
+  const int nv = __popc(__ballot_sync(0xffffffffu, c.valid));
+  const int64_t row0 = __shfl_sync(0xffffffffu, c.start, 0) >> 5;
+  a0 = row0 << 5;
+  const int64_t a1 = __shfl_sync(0xffffffffu, (c.start & ~int64_t(3)) + 20, nv - 1);
+  staged = a1 <= K.tok_rows * 32;  // all but the tiles touching the last partial row
+  const unsigned pin_m = __ballot_sync(0xffffffffu, in_pin);
+  const int64_t prev_r = __shfl_up_sync(0xffffffffu, c.r, 1);
+  const bool head = in_pin && (lane == 0 || !((pin_m >> (lane - 1)) & 1u) || prev_r != c.r);
+  const unsigned heads = __ballot_sync(0xffffffffu, head);
+  uint32_t pin_bytes = 0;
+  if (head) {
+    const unsigned after = ~((2u << lane) - 1u);
+    const unsigned stop = (heads | ~pin_m) & after;
+    const int end = stop ? __ffs(stop) - 1 : 32;
+    pin_bytes = (uint32_t)(end - lane) * (PIN_STRIDE * 4);
+  }
+  const uint32_t tok_bytes = staged ? (uint32_t)(TMAP_ROWS * 128) : 0u;
+  const uint32_t total = __reduce_add_sync(0xffffffffu, pin_bytes) + tok_bytes;
+  if (!total) return false;
+  if (lane == 0) mbar_expect_tx(bar, total);
+  __syncwarp();
+#if SFKV_L2HINT
+  const uint64_t pol = l2_policy_first();
+  if (staged && lane == 0) bulk_tensor_2d_hint(s_tok, tmap, 0, (int)row0, bar, pol);
+  if (head)
+    bulk_copy_hint(s_pin + lane * PIN_STRIDE, K.pin_tok + pin_tok_index(c.wf, c.k, 0, K.pin_groups), pin_bytes, bar, pol);
+#else
+  if (staged && lane == 0) bulk_tensor_2d(s_tok, tmap, 0, (int)row0, bar);
+  if (head) bulk_copy(s_pin + lane * PIN_STRIDE, K.pin_tok + pin_tok_index(c.wf, c.k, 0, K.pin_groups), pin_bytes, bar);
+#endif
+  return true;
+}
+
+// Block tokens t (zero padded) and, for in-pin blocks, the pin's block q of a staged tile.
+__device__ __forceinline__ void load_staged_tile(const MatchKernelArgs& K, const Ctx& c, bool in_pin, bool staged,
+                                                 int64_t a0, int64_t tok_total, const uint32_t* s_tok,
+                                                 const uint32_t* s_pin, uint32_t* t, uint32_t* q) {
+  const int lane = threadIdx.x & 31;
+  if (staged) {
+    // every lane of a tile inside one request shares the token alignment: a warp-uniform
+    // specialisation reads the swizzled range with no per-lane funnel selects
+    const int o = c.valid ? (int)(c.start - a0) : 0;
+    const int sh0 = __shfl_sync(0xffffffffu, o & 3, 0);
+    if (__all_sync(0xffffffffu, !c.valid || (o & 3) == sh0)) {
+      switch (sh0) {
+        case 0: load_swz_sh<0>(s_tok, o, t); break;
+        case 1: load_swz_sh<1>(s_tok, o, t); break;
+        case 2: load_swz_sh<2>(s_tok, o, t); break;
+        default: load_swz_sh<3>(s_tok, o, t); break;
+      }
+      if (c.nval < BT) {
+#pragma unroll
+        for (int j = 0; j < BT; ++j)
+          if (j >= c.nval) t[j] = 0u;
+      }
+    } else if (c.valid) {
+      load_block_swz(s_tok, o, c.nval, t);
+    }
+  } else if (c.valid) {
+    load_block(K.a.tok, c.start, c.nval, tok_total, t);
+  }
+  if (in_pin) load_pin_rot(s_pin, lane, c.k, q);
+}
+
+// Match mode (STAGED): a warp takes TPW consecutive tiles and stages all of them before
+// processing the first, so the later tiles' loads overlap the earlier tiles' compute.
 template <bool STAGED>
 __global__ void __launch_bounds__(BLOCK_THREADS, SFKV_MB_MINB) match_block_kernel(MatchKernelArgs K,
                                                                        const __grid_constant__ CUtensorMap tmap) {
-  __shared__ __align__(1024) uint32_t s_tok[STAGED ? BLOCK_THREADS / 32 : 1][STAGED ? 768 : 4];  // 18 rows, 1 KB-aligned
-  __shared__ __align__(128) uint32_t s_pin[STAGED ? BLOCK_THREADS / 32 : 1][STAGED ? WT * PIN_STRIDE : 4];
-  __shared__ __align__(8) uint64_t s_bar[BLOCK_THREADS / 32];
+  constexpr int TPW = STAGED ? SFKV_MB_TPW : 1;
+  constexpr int NW = BLOCK_THREADS / 32;
+  __shared__ __align__(1024) uint32_t s_tok[STAGED ? NW * TPW : 1][STAGED ? 768 : 4];  // 18 rows, 1 KB-aligned
+  __shared__ __align__(128) uint32_t s_pin[STAGED ? NW * TPW : 1][STAGED ? WT * PIN_STRIDE : 4];
+  __shared__ __align__(8) uint64_t s_bar[NW * TPW];
   const MatchArgs& A = K.a;
   const int lane = threadIdx.x & 31;
   [[maybe_unused]] const int warp = threadIdx.x >> 5;
-  const int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t tile0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * TPW;
   if constexpr (STAGED) {
-    if (lane == 0) mbar_init(&s_bar[warp]);
+    if (lane < TPW) mbar_init(&s_bar[warp * TPW + lane]);
     __syncwarp();
   }
   pdl_trigger();
   pdl_wait();
   const int64_t n_items = K.rec[A.n].blk_off;
-  if (tile * WT >= n_items) return;
+  if (tile0 * WT >= n_items) return;
   const int64_t tok_total = K.rec[A.n].tok_off;
-  const bool match_mode = A.out_M != nullptr;
-  const Ctx c = resolve(K, tile, n_items);
-
-  const bool in_pin = match_mode && c.valid && c.pin_len >= 0 && c.k < (c.pin_len + BT - 1) / BT;
-  uint32_t q[BT];
-  uint32_t t[BT];
   if constexpr (STAGED) {
-    // one mbarrier phase for the tile: its token range (one bulk copy) and, per request segment
-    // of in-pin blocks, that segment's pin blocks (pin-major: one extent, placed at lane * 64 B)
-    const int nv = __popc(__ballot_sync(0xffffffffu, c.valid));
-    const int64_t row0 = __shfl_sync(0xffffffffu, c.start, 0) >> 5;
-    const int64_t a0 = row0 << 5;
-    const int64_t a1 = __shfl_sync(0xffffffffu, (c.start & ~int64_t(3)) + 20, nv - 1);
-    const bool staged = a1 <= K.tok_rows * 32;  // all but the tiles touching the last partial row
-    const unsigned pin_m = __ballot_sync(0xffffffffu, in_pin);
-    const int64_t prev_r = __shfl_up_sync(0xffffffffu, c.r, 1);
-    const bool head = in_pin && (lane == 0 || !((pin_m >> (lane - 1)) & 1u) || prev_r != c.r);
-    const unsigned heads = __ballot_sync(0xffffffffu, head);
-    uint32_t pin_bytes = 0;
-    if (head) {
-      const unsigned after = ~((2u << lane) - 1u);
-      const unsigned stop = (heads | ~pin_m) & after;
-      const int end = stop ? __ffs(stop) - 1 : 32;
-      pin_bytes = (uint32_t)(end - lane) * (PIN_STRIDE * 4);
-    }
-    const uint32_t tok_bytes = staged ? (uint32_t)(TMAP_ROWS * 128) : 0u;
-    const uint32_t total = __reduce_add_sync(0xffffffffu, pin_bytes) + tok_bytes;
-    if (total) {
-      if (lane == 0) mbar_expect_tx(&s_bar[warp], total);
-      __syncwarp();
-      if (staged && lane == 0) bulk_tensor_2d(s_tok[warp], &tmap, 0, (int)row0, &s_bar[warp]);
-      if (head) bulk_copy(s_pin[warp] + lane * PIN_STRIDE, K.pin_tok + pin_tok_index(c.wf, c.k, 0, K.pin_groups),
-                          pin_bytes, &s_bar[warp]);
-      mbar_wait0(&s_bar[warp]);
-    }
-    if (staged) {
-      // every lane of a tile inside one request shares the token alignment: a warp-uniform
-      // specialisation reads the swizzled range with no per-lane funnel selects
-      const int o = c.valid ? (int)(c.start - a0) : 0;
-      const int sh0 = __shfl_sync(0xffffffffu, o & 3, 0);
-      if (__all_sync(0xffffffffu, !c.valid || (o & 3) == sh0)) {
-        switch (sh0) {
-          case 0: load_swz_sh<0>(s_tok[warp], o, t); break;
-          case 1: load_swz_sh<1>(s_tok[warp], o, t); break;
-          case 2: load_swz_sh<2>(s_tok[warp], o, t); break;
-          default: load_swz_sh<3>(s_tok[warp], o, t); break;
-        }
-        if (c.nval < BT) {
+    Ctx cs[TPW];
+    bool inp[TPW], armed[TPW], stg[TPW];
+    int64_t a0[TPW];
 #pragma unroll
-          for (int j = 0; j < BT; ++j)
-            if (j >= c.nval) t[j] = 0u;
-        }
-      } else if (c.valid) {
-        load_block_swz(s_tok[warp], o, c.nval, t);
+    for (int j = 0; j < TPW; ++j) {
+      armed[j] = false;
+      if ((tile0 + j) * WT < n_items) {
+        cs[j] = resolve(K, tile0 + j, n_items);
+        inp[j] = cs[j].valid && cs[j].pin_len >= 0 && cs[j].k < (cs[j].pin_len + BT - 1) / BT;
+        armed[j] = stage_tile(K, &tmap, cs[j], inp[j], s_tok[warp * TPW + j], s_pin[warp * TPW + j],
+                              &s_bar[warp * TPW + j], a0[j], stg[j]);
       }
-    } else if (c.valid) {
-      load_block(A.tok, c.start, c.nval, tok_total, t);
     }
-    if (in_pin) load_pin_rot(s_pin[warp], lane, c.k, q);
-  } else if (c.valid) {
-    load_block(A.tok, c.start, c.nval, tok_total, t);
-  }
-  if (!c.valid) {
 #pragma unroll
-    for (int j = 0; j < BT; ++j) t[j] = 0u;
+    for (int j = 0; j < TPW; ++j) {
+      if ((tile0 + j) * WT >= n_items) break;
+      if (armed[j]) mbar_wait0(&s_bar[warp * TPW + j]);
+      uint32_t q[BT], t[BT];
+      load_staged_tile(K, cs[j], inp[j], stg[j], a0[j], tok_total, s_tok[warp * TPW + j], s_pin[warp * TPW + j], t,
+                       q);
+      if (!cs[j].valid) {
+#pragma unroll
+        for (int i = 0; i < BT; ++i) t[i] = 0u;
+      }
+      tile_finish(K, tile0 + j, cs[j], inp[j], t, q);
+    }
+  } else {
+    const int64_t tile = tile0;
+    const Ctx c = resolve(K, tile, n_items);
+    uint32_t q[BT], t[BT];
+    if (c.valid) load_block(A.tok, c.start, c.nval, tok_total, t);
+    else {
+#pragma unroll
+      for (int j = 0; j < BT; ++j) t[j] = 0u;
+    }
+    tile_finish(K, tile, c, false, t, q);
   }
-  tile_finish(K, tile, c, in_pin, t, q);
 }
 
 // ---------------------------------------------------------------- chain pass ---------------
@@ -1041,7 +1129,8 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
     SFKV_CUDA(launch_pdl(lookup_req_kernel, dim3(lgrid), dim3(LR_THREADS), st, K, tm));
     return 0;
   }
-  if (a.out_M) SFKV_CUDA(launch_pdl(match_block_kernel<true>, dim3((unsigned)grid), dim3(BLOCK_THREADS), st, K, tm));
+  const int64_t sgrid = (ntiles + (BLOCK_THREADS / 32) * SFKV_MB_TPW - 1) / ((BLOCK_THREADS / 32) * SFKV_MB_TPW);
+  if (a.out_M) SFKV_CUDA(launch_pdl(match_block_kernel<true>, dim3((unsigned)sgrid), dim3(BLOCK_THREADS), st, K, tm));
   else SFKV_CUDA(launch_pdl(match_block_kernel<false>, dim3((unsigned)grid), dim3(BLOCK_THREADS), st, K, tm));
   if (K.hashes) {
     const int tpw = a.out_block ? CH_TPW_LOOKUP : CH_TPW_HASH;
