@@ -53,6 +53,34 @@ __host__ __device__ __forceinline__ uint64_t block_digest_words(uint64_t k, uint
   return mix64(a0 ^ ((a1 << 32) | (a1 >> 32)) ^ (k * 0xD6E8FEB86659FD93ull + n));
 }
 
+// ---- L2 residency hints --------------------------------------------------------------------
+// Streamed data (read or written once per batch) is marked evict_first so it does not push out
+// what a later pass of the same batch re-reads (evict_last): chain sums, tables, records.
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_u64_hint(uint64_t* p, uint64_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_u32_hint(uint32_t* p, uint32_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+// 16-B read-only load, no L1 allocation, with an L2 policy
+__device__ __forceinline__ uint4 ld_nc16_hint(const void* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
 // The chain sum is taken mod 2^62 so a look-back status word can carry it next to a 2-bit flag.
 constexpr uint64_t CHAIN_MASK = (1ull << 62) - 1;
 

@@ -458,16 +458,6 @@ __device__ __forceinline__ void bulk_tensor_2d(void* dst, const CUtensorMap* tm,
 #ifndef SFKV_L2HINT
 #define SFKV_L2HINT 1
 #endif
-__device__ __forceinline__ uint64_t l2_policy_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t l2_policy_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
 __device__ __forceinline__ void bulk_copy_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
@@ -482,9 +472,6 @@ __device__ __forceinline__ void bulk_tensor_2d_hint(void* dst, const CUtensorMap
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
-}
-__device__ __forceinline__ void st_u64_hint(uint64_t* p, uint64_t v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
 }
 // Block tokens of a lane whose block starts at word o of a swizzled staged range.
 __device__ __forceinline__ void load_block_swz(const uint32_t* s, int o, int nval, uint32_t* t) {
@@ -801,7 +788,11 @@ __global__ void __launch_bounds__(MATCH_THREADS) match_chain_kernel(MatchKernelA
     carry = __shfl_sync(0xffffffffu, sum, 31);
     c[i] = chain_finalize(sum);
     const int64_t item = (t0 + i) * WT + lane;
+#if SFKV_L2HINT
+    if (item < n_items && A.out_hash) st_u64_hint(A.out_hash + item, c[i], l2_policy_first());  // not re-read here
+#else
     if (item < n_items && A.out_hash) A.out_hash[item] = c[i];
+#endif
   }
   if constexpr (LOOKUP) {  // global table probe, token-verified and parent-linked; probes in flight together
     const int64_t tok_total = K.rec[A.n].tok_off;
@@ -925,6 +916,7 @@ __global__ void __launch_bounds__(LR_THREADS, SFKV_LR_MINB) lookup_req_kernel(Ma
   pdl_wait();
   const MatchArgs& A = K.a;
   if (r >= A.n) return;
+  const uint64_t pol_stream = l2_policy_first();
   int64_t bo, to;
   int32_t len, pl, wf;
   unpack_rec(K.rec + r, bo, to, len, pl, wf);
@@ -941,7 +933,11 @@ __global__ void __launch_bounds__(LR_THREADS, SFKV_LR_MINB) lookup_req_kernel(Ma
       uint64_t* bar = &s_bar[warp][i & 1];
       fence_proxy_async_smem();  // the warp's generic reads of this buffer precede the refill
       mbar_expect_tx(bar, TMAP_ROWS * 128);
+#if SFKV_L2HINT
+      bulk_tensor_2d_hint(s_tok[warp][i & 1], &tmap, 0, (int)(s0 >> 5), bar, l2_policy_first());  // streamed once
+#else
       bulk_tensor_2d(s_tok[warp][i & 1], &tmap, 0, (int)(s0 >> 5), bar);
+#endif
     }
     return staged;
   };
@@ -1007,7 +1003,7 @@ __global__ void __launch_bounds__(LR_THREADS, SFKV_LR_MINB) lookup_req_kernel(Ma
     const int32_t p_raw = lane > 0 ? up_raw : prev_raw;
     const int32_t id = (eq && (k == 0 || par == p_raw)) ? raw : -1;
     prev_raw = __shfl_sync(0xffffffffu, raw, 31);
-    if (valid) A.out_block[bo + k] = id;
+    if (valid) st_u32_hint(reinterpret_cast<uint32_t*>(A.out_block + bo + k), (uint32_t)id, pol_stream);
     const unsigned miss = __ballot_sync(0xffffffffu, valid && id < 0);
     if (run) {
       if (miss) {

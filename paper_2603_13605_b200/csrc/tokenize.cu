@@ -118,6 +118,12 @@ __device__ __forceinline__ unsigned long long tok_key(const uint8_t* p, int len)
   return h ? h : 1;
 }
 
+// Home slot: the top log2(slots) bits of a Fibonacci hash (key x 2^64/phi). A 32-bit fold
+// (lo ^ hi) was measured 2x slower: structured words (digit runs) collide in the fold.
+__device__ __forceinline__ uint64_t home_slot(unsigned long long key, int shift) {
+  return (key * 0x9E3779B97F4A7C15ull) >> shift;
+}
+
 // tok_key of a token staged in shared memory at byte s0 (the buffer is 8-B aligned and readable
 // 16 bytes past the token): the same key, read as 8-byte words (two aligned loads + a funnel
 // shift each) instead of byte by byte.
@@ -207,13 +213,14 @@ __global__ void __launch_bounds__(COUNT_WARPS * 32) chunk_count_kernel(TokArgs a
   const int64_t chunk = (int64_t)blockIdx.x * COUNT_WARPS + (threadIdx.x >> 5);
   if (chunk >= nchunks) return;
   const int64_t c0 = chunk * CHUNK;
+  const uint64_t pol = l2_policy_first();
   uint4 v[KW];
   uint32_t mw[KW];
 #pragma unroll
   for (int k = 0; k < KW; ++k) {
     const int64_t w = c0 + 512 * k + 16 * lane;
     v[k] = make_uint4(0x20202020u, 0x20202020u, 0x20202020u, 0x20202020u);
-    if (w + 16 <= a.n_bytes) v[k] = __ldg(reinterpret_cast<const uint4*>(a.text + w));
+    if (w + 16 <= a.n_bytes) v[k] = ld_nc16_hint(a.text + w, pol);  // streamed: evict_first
     mw[k] = w < a.n_bytes ? __ldg(a.mbits + (w >> 5)) : 0u;
   }
   uint32_t prev_last = c0 == 0 ? 1u : (uint32_t)is_space(a.text[c0 - 1]);  // before lane 0, round 0
@@ -279,14 +286,14 @@ __global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
   const int64_t lim = a.n_bytes - c0;  // valid staged bytes: [0, min(lim, CHUNK + OVER))
   // stage bytes (16 B per thread, OVER / 16 threads take the overflow) and bits
   if (base + 16 <= a.n_bytes) {
-    *reinterpret_cast<uint4*>(sb + threadIdx.x * 16) = __ldg(reinterpret_cast<const uint4*>(a.text + base));
+    *reinterpret_cast<uint4*>(sb + threadIdx.x * 16) = ld_nc16_hint(a.text + base, l2_policy_first());
   } else {
     for (int j = 0; j < 16; ++j) sb[threadIdx.x * 16 + j] = base + j < a.n_bytes ? a.text[base + j] : ' ';
   }
   if (threadIdx.x < OVER / 16) {
     const int64_t ob = c0 + CHUNK + threadIdx.x * 16;
     if (ob + 16 <= a.n_bytes) {
-      *reinterpret_cast<uint4*>(sb + CHUNK + threadIdx.x * 16) = __ldg(reinterpret_cast<const uint4*>(a.text + ob));
+      *reinterpret_cast<uint4*>(sb + CHUNK + threadIdx.x * 16) = ld_nc16_hint(a.text + ob, l2_policy_first());
     } else {
       for (int j = 0; j < 16; ++j) sb[CHUNK + threadIdx.x * 16 + j] = ob + j < a.n_bytes ? a.text[ob + j] : ' ';
     }
@@ -302,7 +309,10 @@ __global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
   __shared__ int s_any_pend;
   __shared__ unsigned long long s_pbase;
   if (threadIdx.x < PW) s_pend[threadIdx.x] = 0u;
-  if (threadIdx.x == 0) s_any_pend = 0;
+  if (threadIdx.x == 0) {
+    s_any_pend = 0;
+    sbnd[(CHUNK + OVER) / 32] = 0xffffffffu;  // past the staged bytes: all boundaries (end windows)
+  }
   __syncthreads();
   // from the staged bytes: 16 boundary bits (space | message start) per thread into the bitmap, and
   // the thread's token starts (non-space after a space or at a message start)
@@ -330,10 +340,20 @@ __global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
   for (int i = threadIdx.x; i < total; i += CHUNK_THREADS) {
     const int s0 = slist[i];
     bool pend;
+    // the token's end: the first boundary bit after s0, from a 64-bit window of the bitmap (one
+    // step for tokens of up to 32 bytes; longer ones walk on)
     int w = (s0 + 1) >> 5;
-    uint32_t bits = sbnd[w] & (~0u << ((s0 + 1) & 31));
-    while (!bits && (w + 1) * 32 < stage_end) bits = sbnd[++w];
-    const int e = bits ? w * 32 + __ffs(bits) - 1 : CHUNK + OVER;
+    const uint64_t win = (((uint64_t)sbnd[w + 1] << 32) | sbnd[w]) >> ((s0 + 1) & 31);
+    uint32_t bits = 1u;
+    int e;
+    if (win) {
+      e = s0 + __ffsll((long long)win);
+    } else {
+      ++w;
+      bits = 0u;
+      while (!bits && (w + 1) * 32 < stage_end) bits = sbnd[++w];
+      e = bits ? w * 32 + __ffs(bits) - 1 : CHUNK + OVER;
+    }
     if (e < stage_end || (bits && stage_end == lim)) {
       const int len = e - s0;
       if (len <= 7) {
@@ -385,7 +405,7 @@ __device__ bool probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned l
                           int len) {
   // home slot by Fibonacci hashing: the top bits of key x 2^64/phi spread the raw bytes of short
   // keys (one multiply; mix64 here cost 7.5 % of the batch, the probe loop is issue-bound)
-  uint64_t sl = (key * 0x9E3779B97F4A7C15ull) >> a.slot_shift;
+  uint64_t sl = home_slot(key, a.slot_shift);
   int64_t found = -1;
   uint32_t id = TOK_PENDING;
   for (uint64_t probes = 0; probes <= a.mask; ++probes) {
@@ -414,7 +434,7 @@ __device__ bool probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned l
   if (id != TOK_PENDING) {  // published before this batch
     if (!(key >> 63) && (a.id_len[id] != len || !bytes_equal(p, a.arena + a.id_off[id], len)))
       atomicOr(a.ctr + 2, (unsigned long long)TERR_COLLISION);
-    a.tok[t] = id;
+    st_u32_hint(a.tok + t, id, l2_policy_first());  // output ids: written once
     return false;
   }
   a.tstart[t] = start;
@@ -732,7 +752,7 @@ __global__ void interner_rehash_kernel(TSlot* slots, uint64_t mask, int shift, c
                                        const int64_t* id_off, const int32_t* id_len, int64_t n_ids) {
   for (int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; id < n_ids; id += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long key = tok_key(arena + id_off[id], id_len[id]);
-    uint64_t sl = (key * 0x9E3779B97F4A7C15ull) >> shift;
+    uint64_t sl = home_slot(key, shift);
     for (;;) {
       if (atomicCAS(&slots[sl].key, 0ull, key) == 0ull) {
         slots[sl].id = (uint32_t)id;
