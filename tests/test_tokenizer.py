@@ -163,3 +163,28 @@ def test_gpu_tokenizer_edge_batches_match_oracle(gpu_api, oracle_api):
         np.testing.assert_array_equal(go, oo)
         np.testing.assert_array_equal(gt, ot)
     assert g.size() == o.size()
+
+
+@pytest.mark.gpu
+def test_gpu_cold_batch_and_reset(gpu_api, oracle_api):
+    """A batch of only new strings (the cold path: every token pending, owners ranked by a
+    (count, bytes) tile scan, arena written through shared memory or, for tiles of long strings,
+    byte by byte) gives the oracle's ids and arena bytes; sfkv_interner_reset empties the
+    interner, after which the same batch gets the same ids again."""
+    rng = np.random.default_rng(77)
+    words = [b"w%07d" % i + bytes(int(x) for x in rng.integers(97, 123, size=int(rng.integers(0, 17))))
+             for i in range(20_000)]
+    words += [bytes(int(x) for x in rng.integers(33, 127, size=int(rng.integers(50, 300)))) for _ in range(300)]
+    reqs = [[b" ".join(words[i:i + 500])] for i in range(0, len(words), 500)]
+    g = Interner(gpu_api, table_log2=16, arena_bytes=4 << 20)
+    for rep in range(2):
+        o = Interner(oracle_api, table_log2=16, arena_bytes=4 << 20)
+        go, gt = g.tokenize(reqs)
+        oo, ot = o.tokenize(reqs)
+        np.testing.assert_array_equal(go, oo)
+        np.testing.assert_array_equal(gt, ot)
+        assert g.size() == o.size() == len(set(words))
+        for i in list(range(0, 50)) + list(range(o.size() - 350, o.size(), 7)):
+            assert g.token(i) == o.token(i)
+        g.reset()
+        assert g.size() == 0
