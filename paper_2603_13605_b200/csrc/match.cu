@@ -73,6 +73,9 @@ constexpr int CH_TPW_LOOKUP = SFKV_CH_TPW_LOOKUP;  // 54 registers: more warps i
 #define SFKV_PREP_THREADS 256
 #endif
 constexpr int PREP_THREADS = SFKV_PREP_THREADS;
+#ifndef SFKV_PREP_PDL
+#define SFKV_PREP_PDL 1
+#endif
 
 constexpr int PREP_TILE = PREP_THREADS;
 
@@ -163,6 +166,7 @@ __global__ void __launch_bounds__(PREP_THREADS) match_prep_kernel(PrepArgs P) {
   __shared__ typename BS::TempStorage tmp;
   __shared__ int64_t s_tile, s_prefix;
   pdl_trigger();
+  pdl_wait();  // a no-op unless launched as a programmatic dependent
   const int tid = threadIdx.x;
   // With every prep CTA co-resident (the usual case) the launch order is the tile order; a
   // ticket (zeroed by the host) orders CTAs otherwise, so a predecessor is always running.
@@ -295,12 +299,10 @@ __device__ __forceinline__ void unpack_rec(const ReqRec* q, int64_t& blk_off, in
 //   rem_j = len_j - 16 kb_j       (tokens from there to the request's end)
 // and lane L belongs to the largest j with kb_j >= -L. Tiles covering > 32 requests (empty
 // requests) fall back to a binary search over blk_off for the lanes past the window.
-__device__ __forceinline__ Ctx resolve(const MatchKernelArgs& K, int64_t tile, int64_t n_items) {
+__device__ __forceinline__ Ctx resolve(const MatchKernelArgs& K, int64_t tile, int64_t n_items, int4 ta, int4 tb) {
   const int lane = threadIdx.x & 31;
   const int64_t n = K.a.n;
   const int64_t T0 = tile * WT;
-  const int4* tp = reinterpret_cast<const int4*>(K.trec + tile);
-  const int4 ta = __ldg(tp), tb = __ldg(tp + 1);
   const int64_t s0 = (int64_t)(((uint64_t)(uint32_t)ta.y << 32) | (uint32_t)ta.x);
   const int64_t r0 = ta.z;
   Ctx c;
@@ -353,6 +355,11 @@ __device__ __forceinline__ Ctx resolve(const MatchKernelArgs& K, int64_t tile, i
   }
   c.nval = c.valid ? (nv < 0 ? 0 : (nv > BT ? BT : nv)) : 0;
   return c;
+}
+
+__device__ __forceinline__ Ctx resolve(const MatchKernelArgs& K, int64_t tile, int64_t n_items) {
+  const int4* tp = reinterpret_cast<const int4*>(K.trec + tile);
+  return resolve(K, tile, n_items, __ldg(tp), __ldg(tp + 1));
 }
 
 __device__ __forceinline__ void load16_aligned(const uint32_t* __restrict__ p, uint32_t* t) {
@@ -701,6 +708,10 @@ __global__ void __launch_bounds__(BLOCK_THREADS, SFKV_MB_MINB) match_block_kerne
   }
   pdl_trigger();
   pdl_wait();
+  // the first tile record is loaded together with the batch totals (speculatively: the record
+  // array is carved for the launch's tile bound), saving one round trip before the staging
+  const int4* tp0 = reinterpret_cast<const int4*>(K.trec + tile0);
+  const int4 ta0 = __ldg(tp0), tb0 = __ldg(tp0 + 1);
   const int64_t n_items = K.rec[A.n].blk_off;
   if (tile0 * WT >= n_items) return;
   const int64_t tok_total = K.rec[A.n].tok_off;
@@ -712,7 +723,7 @@ __global__ void __launch_bounds__(BLOCK_THREADS, SFKV_MB_MINB) match_block_kerne
     for (int j = 0; j < TPW; ++j) {
       armed[j] = false;
       if ((tile0 + j) * WT < n_items) {
-        cs[j] = resolve(K, tile0 + j, n_items);
+        cs[j] = j == 0 ? resolve(K, tile0, n_items, ta0, tb0) : resolve(K, tile0 + j, n_items);
         inp[j] = cs[j].valid && cs[j].pin_len >= 0 && cs[j].k < (cs[j].pin_len + BT - 1) / BT;
         armed[j] = stage_tile(K, &tmap, cs[j], inp[j], s_tok[warp * TPW + j], s_pin[warp * TPW + j],
                               &s_bar[warp * TPW + j], a0[j], stg[j]);
@@ -1088,7 +1099,11 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   P.epoch = p->prep_epoch;
   P.max_wf = p->cfg.max_workflows;
   P.error = &p->ctr->error;
+#if SFKV_PREP_PDL
+  SFKV_CUDA(launch_pdl(match_prep_kernel, dim3((unsigned)np), dim3(PREP_THREADS), st, P));
+#else
   match_prep_kernel<<<(unsigned)np, PREP_THREADS, 0, st>>>(P);
+#endif
   SFKV_LAUNCH_CHECK("match_prep_kernel");
   if (ntiles == 0) return 0;
 
