@@ -507,15 +507,22 @@ __device__ __forceinline__ void load_block_swz(const uint32_t* s, int o, int nva
 
 
 // Block tokens of a lane whose block starts at word o (o & 3 == SH) of a swizzled staged range.
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {  // 16-B shared load by 32-bit address
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
 template <int SH>
 __device__ __forceinline__ void load_swz_sh(const uint32_t* s, int o, uint32_t* t) {
+  const uint32_t base = smem_u32(s);
   const int c0 = o >> 2;
   constexpr int NC = SH ? 5 : 4;
   uint32_t w[20];
 #pragma unroll
   for (int i = 0; i < NC; ++i) {
-    const int g = c0 + i;
-    const uint4 v = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(s) + ((g ^ ((g >> 3) & 7)) << 4));
+    const uint32_t g = (uint32_t)(c0 + i);
+    const uint4 v = lds128(base + ((g ^ ((g >> 3) & 7u)) << 4));
     w[4 * i] = v.x;
     w[4 * i + 1] = v.y;
     w[4 * i + 2] = v.z;
@@ -524,14 +531,11 @@ __device__ __forceinline__ void load_swz_sh(const uint32_t* s, int o, uint32_t* 
 #pragma unroll
   for (int j = 0; j < BT; ++j) t[j] = w[j + SH];
 }
-
-// Pin block k of a lane, staged at lane * 64 B in the rotated layout: in-order, conflict-free.
 __device__ __forceinline__ void load_pin_rot(const uint32_t* s, int lane, int64_t k, uint32_t* q) {
-  const int rot = pin_rot(k);
-  const uint32_t* b = s + lane * BT;
+  const uint32_t base = smem_u32(s) + (uint32_t)lane * 64u, r = (uint32_t)pin_rot(k);
 #pragma unroll
   for (int x = 0; x < 4; ++x) {
-    const uint4 w = *reinterpret_cast<const uint4*>(b + 4 * ((x + rot) & 3));
+    const uint4 w = lds128(base + (((r + (uint32_t)x) & 3u) << 4));
     q[4 * x] = w.x;
     q[4 * x + 1] = w.y;
     q[4 * x + 2] = w.z;

@@ -27,12 +27,17 @@ def step(hash_=True):
     api.check("m", api.match_batch_dev(pool.h, n, C.c_void_p(d_wf.data_ptr()), C.c_void_p(d_off.data_ptr()),
               C.c_void_p(d_tok.data_ptr()), int(wl["req_off"][-1]), C.c_void_p(d_M.data_ptr()),
               C.c_void_p(d_h.data_ptr()) if hash_ else None))
+FLUSH = os.environ.get("FLUSH", "write")  # write | writeread (dirty lines written back before the step)
+def flush():
+    l2.zero_()
+    if FLUSH == "writeread":
+        l2.view(torch.int64).max()  # reads the buffer: the flush's dirty lines leave L2 now
 for _ in range(3):
-    l2.zero_(); step()
+    flush(); step()
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(3):
-        l2.zero_(); step()
+        flush(); torch.cuda.synchronize(); step()
     torch.cuda.synchronize()
 evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
 preps = [i for i, e in enumerate(evs) if "match_prep" in e.name]
