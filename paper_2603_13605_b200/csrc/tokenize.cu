@@ -275,7 +275,10 @@ __device__ bool probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned l
 #define SFKV_TOK_OVER 256
 #endif
 constexpr int OVER = SFKV_TOK_OVER;
-__global__ void __launch_bounds__(CHUNK_THREADS) chunk_emit_kernel(TokArgs a) {
+#ifndef SFKV_EMIT_MINB
+#define SFKV_EMIT_MINB 16
+#endif
+__global__ void __launch_bounds__(CHUNK_THREADS, SFKV_EMIT_MINB) chunk_emit_kernel(TokArgs a) {
   pdl_enter();
   using BS = cub::BlockScan<int, CHUNK_THREADS>;
   __shared__ typename BS::TempStorage tmp;
@@ -434,7 +437,7 @@ __device__ bool probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned l
   if (id != TOK_PENDING) {  // published before this batch
     if (!(key >> 63) && (a.id_len[id] != len || !bytes_equal(p, a.arena + a.id_off[id], len)))
       atomicOr(a.ctr + 2, (unsigned long long)TERR_COLLISION);
-    st_u32_hint(a.tok + t, id, l2_policy_first());  // output ids: written once
+    a.tok[t] = id;
     return false;
   }
   a.tstart[t] = start;
