@@ -296,9 +296,20 @@ struct PackAdd {
     return z;
   }
 };
+// Register-only access by a runtime candidate index (a dynamically indexed register array
+// would live in local memory): select / predicated add over the W words.
 template <int W>
 __device__ __forceinline__ unsigned lane16(const PackN<W>& p, int j) {
-  return (unsigned)((p.w[j >> 2] >> (16 * (j & 3))) & 0xffffu);
+  unsigned long long x = 0;
+#pragma unroll
+  for (int i = 0; i < W; ++i) x = (j >> 2) == i ? p.w[i] : x;
+  return (unsigned)((x >> (16 * (j & 3))) & 0xffffu);
+}
+template <int W>
+__device__ __forceinline__ void bump16(PackN<W>& p, int j) {
+  const unsigned long long inc = 1ull << (16 * (j & 3));
+#pragma unroll
+  for (int i = 0; i < W; ++i) p.w[i] += (j >> 2) == i ? inc : 0ull;
 }
 constexpr int RWT = 512;         // threads of the window kernel
 constexpr int RK = 8;            // consecutive requests per thread
@@ -307,7 +318,7 @@ template <int W>  // W u64 words = 4 W candidates
 __global__ void __launch_bounds__(RWT) reroute_window_kernel(CostArgs a) {
   pdl_enter();
   using P = PackN<W>;
-  using BS = cub::BlockScan<P, RWT>;
+  using BS = cub::BlockScan<P, RWT, cub::BLOCK_SCAN_WARP_SCANS>;
   using BR = cub::BlockReduce<int, RWT>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ typename BR::TempStorage rtmp;
@@ -362,7 +373,7 @@ __global__ void __launch_bounds__(RWT) reroute_window_kernel(CostArgs a) {
     for (int k = 0; k < RK; ++k) {
       c0[k] = cn[k];
       pick[k] = spick[c0[k]];
-      if (r0 + k < a.n) loc.w[pick[k] >> 2] += 1ull << (16 * (pick[k] & 3));
+      if (r0 + k < a.n) bump16<W>(loc, pick[k]);
       // the following window's choice, assuming no saturation event here (else reloaded below)
       cn[k] = r0 + RWIN + k < a.n ? a.choice[r0 + RWIN + k] : 0;
     }
@@ -379,7 +390,7 @@ __global__ void __launch_bounds__(RWT) reroute_window_kernel(CostArgs a) {
         if (ev == RWIN && r0 + k < a.n && !((sat >> pick[k]) & 1u) &&
             sdepth[pick[k]] + lane16<W>(run, pick[k]) + 1 >= a.limit)
           ev = tid * RK + k;
-        if (r0 + k < a.n) run.w[pick[k] >> 2] += 1ull << (16 * (pick[k] & 3));
+        if (r0 + k < a.n) bump16<W>(run, pick[k]);
       }
     }
     const int p = BR(rtmp).Reduce(ev, cub::Min());
@@ -393,7 +404,7 @@ __global__ void __launch_bounds__(RWT) reroute_window_kernel(CostArgs a) {
       P incl = pre;
 #pragma unroll
       for (int k = 0; k < RK; ++k)
-        if (tid * RK + k <= pp) incl.w[pick[k] >> 2] += 1ull << (16 * (pick[k] & 3));
+        if (tid * RK + k <= pp) bump16<W>(incl, pick[k]);
       s_incl = incl;
       ssat |= 1u << pick[pp % RK];
     }
