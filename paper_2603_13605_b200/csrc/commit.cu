@@ -46,6 +46,7 @@ struct CommitScratch {
   uint8_t* claim;         // [items]
   uint8_t* cat;           // [items]
   int64_t* first_nonhit;  // [n]
+  int64_t* delta;         // [n] occupancy change of each request if admitted
   int64_t* f_hit;         // [n] first item that is not a linked hit
   int64_t* rank;          // [items+1]
   int64_t* wprefix;       // [words+1]
@@ -120,49 +121,58 @@ __device__ __forceinline__ bool blk_tokens_equal(const uint32_t* __restrict__ bl
   return eq;
 }
 
-// ---- admission: one warp, exact reference order ----------------------------------------
-__global__ void admit_kernel(CommitArgs a) {
+// ---- admission: exact reference order ------------------------------------------------------
+// Every request's checks and occupancy delta are computed by the whole CTA with all loads in
+// flight (the dependent wf -> pin_len load once per request, not once per step of the sequential
+// rule); then one warp applies the rule in request order, 32 requests per step: a warp scan
+// accepts the whole step when every prefix fits, else the exact sequential rule
+// (simulated_backend.cpp:141-150) runs over the step's deltas.
+constexpr int ADMIT_THREADS = 1024;
+constexpr int ADMIT_SMEM = 4096;  // deltas kept in shared memory for batches up to this size
+__global__ void __launch_bounds__(ADMIT_THREADS) admit_kernel(CommitArgs a) {
   pdl_enter();
-  const int lane = threadIdx.x;
+  __shared__ int64_t s_delta[ADMIT_SMEM];
+  const int tid = threadIdx.x, lane = tid & 31;
   DevCounters* c = a.ctr;
-  if (lane == 0) {
+  if (tid == 0) {
     c->error = 0;
     c->occ_saved = c->occupancy;
     c->rej_saved = c->rejections;
   }
-  __syncwarp();
   // staleness / block-table checks first: a refused batch changes nothing
-  bool bad_stale = false, bad_len = false, bad_slot = false;
-  for (int64_t r = lane; r < a.n; r += 32) {
+  int stale = 0, blen = 0, bslot = 0;
+  for (int64_t r = tid; r < a.n; r += ADMIT_THREADS) {
     const int64_t len = a.tok_off[r + 1] - a.tok_off[r];
-    if ((len + BT - 1) / BT > a.max_pin_blocks || len < 0) bad_len = true;
-    if ((uint32_t)a.wf[r] >= (uint32_t)a.max_wf) bad_slot = true;
-    else if (a.payload && a.m_expected && a.m_expected[r] != a.s.M[r]) bad_stale = true;
+    const int32_t w = a.wf[r];
+    if ((len + BT - 1) / BT > a.max_pin_blocks || len < 0) blen = 1;
+    int64_t d = 0;
+    if ((uint32_t)w >= (uint32_t)a.max_wf) {
+      bslot = 1;
+    } else {
+      if (a.payload && a.m_expected && a.m_expected[r] != a.s.M[r]) stale = 1;
+      const int64_t pl = a.pin_len[w];
+      d = len - (pl < 0 ? 0 : pl);
+    }
+    if (r < ADMIT_SMEM) s_delta[r] = d;
+    else a.s.delta[r] = d;
+    a.s.first_nonhit[r] = (len + BT - 1) / BT;
+    a.s.f_hit[r] = (len + BT - 1) / BT;
   }
-  bad_stale = __any_sync(0xffffffffu, bad_stale);
-  bad_len = __any_sync(0xffffffffu, bad_len);
-  bad_slot = __any_sync(0xffffffffu, bad_slot);
-  if (bad_stale || bad_len || bad_slot) {
-    const int code = bad_slot ? SFKV_EINVAL : (bad_len ? SFKV_EPOOL : SFKV_ESTALE);
-    for (int64_t r = lane; r < a.n; r += 32) a.s.status[r] = code;
-    __syncwarp();
-    if (lane == 0) c->error = code;
+  const int any_stale = __syncthreads_or(stale), any_len = __syncthreads_or(blen), any_slot = __syncthreads_or(bslot);
+  if (any_stale || any_len || any_slot) {
+    const int code = any_slot ? SFKV_EINVAL : (any_len ? SFKV_EPOOL : SFKV_ESTALE);
+    for (int64_t r = tid; r < a.n; r += ADMIT_THREADS) a.s.status[r] = code;
+    if (tid == 0) c->error = code;
     return;
   }
+  if (tid >= 32) return;
   long long occ = c->occupancy;
   unsigned long long rej = 0;
   for (int64_t base = 0; base < a.n; base += 32) {
     const int64_t r = base + lane;
     const bool act = r < a.n;
-    long long delta = 0;
-    if (act) {
-      const int64_t pl = a.pin_len[a.wf[r]];
-      const int64_t len = a.tok_off[r + 1] - a.tok_off[r];
-      delta = len - (pl < 0 ? 0 : pl);
-      a.s.first_nonhit[r] = (len + BT - 1) / BT;
-      a.s.f_hit[r] = (len + BT - 1) / BT;
-    }
-    // fast path: every prefix of the chunk fits
+    const long long delta = act ? (r < ADMIT_SMEM ? s_delta[r] : a.s.delta[r]) : 0;
+    // fast path: every prefix of the step fits
     long long incl = delta;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -572,8 +582,7 @@ static int sm_count_c() {
   return sms;
 }
 
-int maybe_rebuild_table(sfkv_pool* p) {
-  cudaStream_t st = p->stream;
+int maybe_rebuild_table(sfkv_pool* p, cudaStream_t st) {
   CommitArgs a = base_args(p);
   int* flag = &p->ctr->pad;
   SFKV_CUDA(launch_pdl(rebuild_check_kernel, dim3(1), dim3(1), st, p->ctr, p->table_slots, flag));
@@ -631,7 +640,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
                o_st = cv.take<int32_t>(n), o_slot = cv.take<int64_t>(ni),
                o_bid = cv.take<int32_t>(ni), o_hit = cv.take<uint8_t>(ni),
                o_claim = cv.take<uint8_t>(ni), o_cat = cv.take<uint8_t>(ni),
-               o_fnh = cv.take<int64_t>(n), o_fh = cv.take<int64_t>(n), o_rank = cv.take<int64_t>(ni + 1),
+               o_fnh = cv.take<int64_t>(n), o_fh = cv.take<int64_t>(n), o_dl = cv.take<int64_t>(n), o_rank = cv.take<int64_t>(ni + 1),
                o_wp = cv.take<int64_t>(p->n_words + 1), o_al = cv.take<int64_t>(ni), o_cow = cv.take<int32_t>(ni),
                o_tmp = cv.take<int64_t>(scan_scratch_elems(ni > p->n_words ? ni : p->n_words) +
                                         scan_scratch_elems(n));
@@ -657,6 +666,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   a.s.cat = reinterpret_cast<uint8_t*>(base + o_cat);
   a.s.first_nonhit = reinterpret_cast<int64_t*>(base + o_fnh);
   a.s.f_hit = reinterpret_cast<int64_t*>(base + o_fh);
+  a.s.delta = reinterpret_cast<int64_t*>(base + o_dl);
   a.s.rank = reinterpret_cast<int64_t*>(base + o_rank);
   a.s.wprefix = reinterpret_cast<int64_t*>(base + o_wp);
   a.s.alloc_list = reinterpret_cast<int64_t*>(base + o_al);
@@ -676,7 +686,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   m.out_hash = a.s.hash;
   if (int rc = launch_match(p, m, a.s.tile_state, st)) return rc;
   // 2. admission, classification, allocation, references
-  SFKV_CUDA(launch_pdl(admit_kernel, dim3(1), dim3(32), st, a));
+  SFKV_CUDA(launch_pdl(admit_kernel, dim3(1), dim3(ADMIT_THREADS), st, a));
   SFKV_LAUNCH_CHECK("admit_kernel");
   const int sms = sm_count_c();
   const int g = grid_for(ni, 256, sms * 8);
@@ -712,11 +722,14 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   SFKV_CUDA(launch_pdl(install_kernel, dim3(g), dim3(256), meta, a));
   SFKV_CUDA(launch_pdl(commit_finish_kernel, dim3(grid_for(n, 256, sms)), dim3(256), meta, a));
   SFKV_LAUNCH_CHECK("release/install");
+  // the tombstone check / rebuild touches only the table: it follows the release on the aux stream,
+  // beside the payload copy, and the join orders it before anything later on the pool stream
+  if (int rc = maybe_rebuild_table(p, meta)) return rc;
   if (meta != st) {
     SFKV_CUDA(cudaEventRecord(p->ev_join, meta));
     SFKV_CUDA(cudaStreamWaitEvent(st, p->ev_join, 0));
   }
-  return maybe_rebuild_table(p);
+  return 0;
 }
 
 int flush_dev(sfkv_pool* p, int64_t n, const int32_t* wf, int64_t* out_freed, bool all) {
@@ -728,7 +741,7 @@ int flush_dev(sfkv_pool* p, int64_t n, const int32_t* wf, int64_t* out_freed, bo
   const int sms = sm_count_c();
   release_kernel<<<grid_for(a.n * 32, 256, sms * 8), 256, 0, st>>>(a, all ? 2 : 1, out_freed);
   SFKV_LAUNCH_CHECK("flush release_kernel");
-  return maybe_rebuild_table(p);
+  return maybe_rebuild_table(p, p->stream);
 }
 
 }  // namespace sfkv

@@ -161,7 +161,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
                const PayloadSource* src);
 int flush_dev(sfkv_pool* p, int64_t n, const int32_t* wf, int64_t* out_freed, bool all);
 int gather_dev(sfkv_pool* p, int64_t n, const int32_t* wf, void* dst, const int64_t* dst_off);
-int maybe_rebuild_table(sfkv_pool* p);
+int maybe_rebuild_table(sfkv_pool* p, cudaStream_t st);
 // Re-inserts every indexed block into the (already resized) empty table; resets tombstones.
 int rebuild_table_now(sfkv_pool* p);
 
