@@ -642,7 +642,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
                o_claim = cv.take<uint8_t>(ni), o_cat = cv.take<uint8_t>(ni),
                o_fnh = cv.take<int64_t>(n), o_fh = cv.take<int64_t>(n), o_dl = cv.take<int64_t>(n), o_rank = cv.take<int64_t>(ni + 1),
                o_wp = cv.take<int64_t>(p->n_words + 1), o_al = cv.take<int64_t>(ni), o_cow = cv.take<int32_t>(ni),
-               o_tmp = cv.take<int64_t>(scan_scratch_elems(ni > p->n_words ? ni : p->n_words) +
+               o_tmp = cv.take<int64_t>(scan_scratch_elems(ni) + scan_scratch_elems(p->n_words) +
                                         scan_scratch_elems(n));
   if (int rc = p->scratch.ensure(cv.off)) return rc;
   char* base = p->scratch.as<char>();
@@ -673,6 +673,18 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   a.s.cow_src = reinterpret_cast<int32_t*>(base + o_cow);
   a.s.scan_tmp = reinterpret_cast<int64_t*>(base + o_tmp);
 
+  if (!p->aux) {
+    SFKV_CUDA(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
+    SFKV_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+    SFKV_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+  }
+  // 0. the free-bitmap prefix (allocation order) depends only on the pool before this batch: it
+  //    runs on the aux stream beside the match / admission / classification and joins before alloc
+  int64_t* tmp_free = a.s.scan_tmp + scan_scratch_elems(ni);
+  SFKV_CUDA(cudaEventRecord(p->ev_fork, st));
+  SFKV_CUDA(cudaStreamWaitEvent(p->aux, p->ev_fork, 0));
+  if (int rc = exclusive_scan(FreeCount{p->free_bits}, p->n_words, a.s.wprefix, tmp_free, p->aux)) return rc;
+  SFKV_CUDA(cudaEventRecord(p->ev_join, p->aux));
   // 1. blocks per request, chained hashes, M = LCP(old pin, tokens)
   MatchArgs m{};  // the match launch also writes blk_off (its prep kernel scans the requests)
   m.n = n;
@@ -696,8 +708,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   SFKV_CUDA(launch_pdl(categorize_kernel, dim3(g), dim3(256), st, a));
   SFKV_LAUNCH_CHECK("probe/resolve/categorize");
   if (int rc = exclusive_scan(NeedAlloc{a.s.cat}, ni, a.s.rank, a.s.scan_tmp, st)) return rc;
-  if (int rc = exclusive_scan(FreeCount{p->free_bits}, p->n_words, a.s.wprefix, a.s.scan_tmp, st))
-    return rc;
+  SFKV_CUDA(cudaStreamWaitEvent(st, p->ev_join, 0));  // the free-bitmap prefix
   SFKV_CUDA(launch_pdl(alloc_kernel, dim3(g), dim3(256), st, a));
   SFKV_CUDA(launch_pdl(refs_kernel, dim3(g), dim3(256), st, a));
   SFKV_CUDA(launch_pdl(clear_owner_kernel, dim3(g), dim3(256), st, a));
@@ -708,11 +719,6 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   //    freed blocks cannot be reallocated before the join
   cudaStream_t meta = st;
   if (a.payload) {
-    if (!p->aux) {
-      SFKV_CUDA(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
-      SFKV_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
-      SFKV_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
-    }
     SFKV_CUDA(cudaEventRecord(p->ev_fork, st));
     SFKV_CUDA(cudaStreamWaitEvent(p->aux, p->ev_fork, 0));
     meta = p->aux;
