@@ -433,3 +433,33 @@ def test_lookup_one_pass_and_two_pass_agree_with_oracle(gpu_api, oracle_api):
         np.testing.assert_array_equal(h2, ho[c0:c0 + 1000])
         np.testing.assert_array_equal(b2, bo[pos:pos + nblk])
         pos += nblk
+
+
+@pytest.mark.parametrize("n_wf,lo,hi", [(300, 1200, 1800), (900, 1500, 2400)])
+def test_commit_mid_size_batches(gpu_api, oracle_api, n_wf, lo, hi):
+    """Commit batches of 28k-150k blocks (the device-wide new-block rank scan takes its
+    three-phase path): block tables, refcounts, statuses and the free-block accounting equal the
+    oracle's, across a second overlapping batch."""
+    rng = np.random.default_rng(n_wf)
+    base = rng.integers(1, 1 << 20, size=hi).astype(np.uint32)
+    seqs = []
+    for i in range(n_wf):
+        L = int(rng.integers(lo, hi))
+        s = base[:L].copy() if i % 3 else rng.integers(1, 1 << 20, size=L).astype(np.uint32)
+        seqs.append(s)
+    wfs = np.arange(n_wf, dtype=np.int32)
+    nb = sum((len(s) + 15) // 16 for s in seqs) * 2 + 1024
+    cfg = Config(max_workflows=n_wf, n_blocks=nb, capacity_tokens=1 << 40, max_pin_blocks=hi // 16 + 8,
+                 table_log2=int(np.ceil(np.log2(2 * nb))) + 1)
+    g, o = _pair(gpu_api, oracle_api, cfg)
+    off, tok = csr(seqs)
+    np.testing.assert_array_equal(g.commit(wfs, off, tok), o.commit(wfs, off, tok))
+    _assert_same_state(g, o, range(0, n_wf, 7))
+    seqs2 = [np.concatenate([s, rng.integers(1, 99, size=int(rng.integers(0, 40))).astype(np.uint32)]) for s in seqs]
+    off2, tok2 = csr(seqs2)
+    Mg, hg = g.match(wfs, off2, tok2, want_hash=True)
+    Mo, ho = o.match(wfs, off2, tok2, want_hash=True)
+    np.testing.assert_array_equal(Mg, Mo)
+    np.testing.assert_array_equal(hg, ho)
+    np.testing.assert_array_equal(g.commit(wfs, off2, tok2), o.commit(wfs, off2, tok2))
+    _assert_same_state(g, o, range(0, n_wf, 5))
