@@ -22,12 +22,15 @@
 //                       published by an earlier batch resolves here; claims (CAS into an empty
 //                       slot + atomicMin(position): the lowest position owns the new string) and
 //                       duplicates of this batch's new strings go to a pending list
-//   tok_resolve_kernel  pending tokens: owners flagged; long duplicates compare bytes with the owner
-//                       (a 64-bit hash collision fails the batch loudly)
-//   rank_* kernels      owners ranked by position (tile counts, scan, in-tile scan) -> new ids in
-//                       first-occurrence order; bytes copied to the arena. They exit at once when
-//                       the batch brings no new string (steady state).
-//   tok_final* kernels  duplicates read the published ids; per-request token offsets
+//   req_tokoff_kernel   per-request token offsets (chunk offset + starts before the request)
+//   tok_pending_kernel  one cooperative launch with grid barriers between its steps: owners
+//                       flagged and long duplicates compared with their owner (a 64-bit hash
+//                       collision fails the batch loudly), capacity check, owners ranked by
+//                       position (tile counts of strings and bytes, scan, in-tile scan) -> new ids
+//                       in first-occurrence order and arena offsets in the same order, arena
+//                       written through shared memory, ids published, duplicates resolved, owners
+//                       reset, the batch's message-start bits cleared. A steady-state batch (no
+//                       pending token) only clears the bits.
 // Byte-stream work, HBM/latency-bound; no tensor cores.
 #include <cooperative_groups.h>
 #include <cooperative_groups/reduce.h>
@@ -447,93 +450,9 @@ __device__ bool probe_key(const TokArgs& a, int64_t t, int64_t start, unsigned l
   return true;
 }
 
-// Pending tokens: the lowest position owns a new string; the others are duplicates (long keys
-// compare bytes with the owner's: a 64-bit hash collision fails the batch loudly).
-__global__ void __launch_bounds__(256) tok_resolve_kernel(TokArgs a) {
-  pdl_enter();
-  using BR = cub::BlockReduce<longlong2, 256>;
-  __shared__ typename BR::TempStorage tmp;
-  const int64_t np = (int64_t)a.ctr[4];
-  longlong2 own = make_longlong2(0, 0);  // this thread's new strings and their bytes
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = a.pend_t[j], sl = a.pend_slot[t];
-    const int len = a.tlen[t];
-    const int64_t o = a.owner[sl];
-    if (o == t) {
-      a.tnew[t] = 1;
-      own.x += 1;
-      own.y += len;
-    } else if (!(a.slots[sl].key >> 63) && !bytes_equal(a.text + a.tstart[t], a.text + a.tstart[o], len)) {
-      atomicOr(a.ctr + 2, (unsigned long long)TERR_COLLISION);
-    }
-  }
-  // one pair of counter atomics per CTA
-  own = BR(tmp).Reduce(own, [](longlong2 x, longlong2 y) { return make_longlong2(x.x + y.x, x.y + y.y); });
-  if (threadIdx.x == 0 && own.x) {
-    atomicAdd(a.ctr + 5, (unsigned long long)own.x);
-    atomicAdd(a.ctr + 3, (unsigned long long)own.y);
-  }
-}
 
-// Capacity check before anything is published: a failing batch leaves the interner unchanged.
-__global__ void tok_check_kernel(TokArgs a) {
-  pdl_enter();
-  if (threadIdx.x || blockIdx.x || a.ctr[2]) return;
-  if ((int64_t)(a.ctr[0] + a.ctr[5]) > a.max_ids) a.ctr[2] |= TERR_IDS;
-  if ((int64_t)(a.ctr[1] + a.ctr[3]) > a.arena_cap) a.ctr[2] |= TERR_ARENA;
-}
 
-// New ids in first-occurrence order: owners are ranked by token position (tile counts, a scan
-// over tiles, an in-tile block scan). Every pass exits at once when the batch has no new string.
-__global__ void __launch_bounds__(256) rank_count_kernel(TokArgs a) {
-  pdl_enter();
-  using BR = cub::BlockReduce<int2, 256>;
-  __shared__ typename BR::TempStorage tmp;
-  const int64_t nt = *a.n_tokens;
-  if (a.ctr[5] == 0 || a.ctr[2]) return;  // steady state: no new string
-  for (int64_t tile = blockIdx.x; tile * RANK_TILE < nt; tile += gridDim.x) {
-    const int64_t t0 = tile * RANK_TILE;
-    int2 c = make_int2(0, 0);  // new strings, their bytes
-    for (int k = 0; k < RANK_TILE / 256; ++k) {
-      const int64_t t = t0 + (int64_t)k * 256 + threadIdx.x;
-      if (t < nt && a.tnew[t]) {
-        c.x += 1;
-        c.y += a.tlen[t];
-      }
-    }
-    c = BR(tmp).Reduce(c, [](int2 x, int2 y) { return make_int2(x.x + y.x, x.y + y.y); });
-    if (threadIdx.x == 0) {
-      a.tile_cnt[tile] = c.x;
-      a.tile_bytes[tile] = c.y;
-    }
-    __syncthreads();  // tmp reused
-  }
-}
 
-__global__ void __launch_bounds__(1024) rank_scan_kernel(TokArgs a) {
-  pdl_enter();
-  using BS = cub::BlockScan<longlong2, 1024>;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ longlong2 carry;
-  const int64_t nt = *a.n_tokens;
-  if (a.ctr[5] == 0 || a.ctr[2]) return;
-  const int64_t ntiles = (nt + RANK_TILE - 1) / RANK_TILE;
-  if (threadIdx.x == 0) carry = make_longlong2(0, 0);
-  __syncthreads();
-  auto add = [](longlong2 x, longlong2 y) { return make_longlong2(x.x + y.x, x.y + y.y); };
-  for (int64_t b = 0; b < ntiles; b += 1024) {
-    const int64_t i = b + threadIdx.x;
-    longlong2 v = i < ntiles ? make_longlong2(a.tile_cnt[i], a.tile_bytes[i]) : make_longlong2(0, 0), ex, tot;
-    BS(tmp).ExclusiveScan(v, ex, make_longlong2(0, 0), add, tot);
-    if (i < ntiles) {
-      a.tile_cnt[i] = carry.x + ex.x;
-      a.tile_bytes[i] = carry.y + ex.y;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) carry = add(carry, tot);
-    __syncthreads();
-  }
-}
 
 // Owners ranked by position get consecutive ids and consecutive arena bytes, so a tile's new
 // strings form one contiguous arena range, and their source bytes one contiguous text range (from
@@ -621,44 +540,8 @@ __device__ void rank_publish_tile(const TokArgs& a, int64_t tile, int64_t nt, Pu
   }
 }
 
-__global__ void __launch_bounds__(256) rank_publish_kernel(TokArgs a) {
-  pdl_enter();
-  __shared__ PubSmem S;
-  const int64_t nt = *a.n_tokens;
-  if (a.ctr[5] == 0 || a.ctr[2]) return;  // steady state: no new string
-  for (int64_t tile = blockIdx.x; tile * RANK_TILE < nt; tile += gridDim.x) {
-    rank_publish_tile(a, tile, nt, S);
-    __syncthreads();  // shared memory reused
-  }
-}
 
-// Pending tokens take their ids from the published slots (or, when the batch failed, the claims
-// are rolled back: the table returns to its pre-batch state — claims sit at the first empty slot
-// of their probe path, so clearing them restores every chain).
-__global__ void tok_final_kernel(TokArgs a) {
-  pdl_enter();
-  const int64_t np = (int64_t)a.ctr[4];
-  const bool failed = a.ctr[2] != 0;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = a.pend_t[j], sl = a.pend_slot[t];
-    if (a.owner[sl] != t) continue;
-    if (failed) {
-      a.slots[sl].key = 0;
-      a.tnew[t] = 0;
-    } else {
-      a.slots[sl].id = a.tok[t];
-    }
-  }
-}
 
-__global__ void tok_final2_kernel(TokArgs a) {  // duplicates of new strings
-  pdl_enter();
-  const int64_t np = (int64_t)a.ctr[4];
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = a.pend_t[j], sl = a.pend_slot[t];
-    if (a.owner[sl] != t) a.tok[t] = a.slots[sl].id;
-  }
-}
 
 // tok_off[r]: tokens before request r's first byte b = its chunk's offset + the token starts in
 // [chunk start, b) (one warp per request, every load of the <= 2 KiB prefix in flight at once).
@@ -712,25 +595,145 @@ __global__ void req_tokoff_kernel(TokArgs a) {
   }
 }
 
-__global__ void tok_owner_reset_kernel(TokArgs a) {  // and the message-start bits of this batch
-  pdl_enter();
-  const int64_t np = (int64_t)a.ctr[4];
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < np; j += (int64_t)gridDim.x * blockDim.x)
-    a.owner[a.pend_slot[a.pend_t[j]]] = INT64_MAX;
-  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < a.n_msg; m += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = a.msg_off[m];
-    if (i < a.n_bytes) a.mbits[i >> 5] = 0u;
-  }
-}
 
-__global__ void tok_commit_kernel(TokArgs a) {  // advance the id counter once per batch
+
+// The pending phase of a batch (resolve → capacity check → rank count / scan / publish → final →
+// duplicates → owner reset + message-start bits → counters) as ONE cooperative launch with grid
+// barriers between the steps. A steady-state batch has no pending token: the kernel clears the
+// batch's message-start bits and returns — one launch where eight early-exiting kernels used to
+// run back to back.
+__global__ void __launch_bounds__(256) tok_pending_kernel(TokArgs a) {
+  namespace cgn = cooperative_groups;
+  using BRL = cub::BlockReduce<longlong2, 256>;
+  using BRI = cub::BlockReduce<int2, 256>;
+  using BSL = cub::BlockScan<longlong2, 256>;
+  union PendTmp {
+    typename BRL::TempStorage rl;
+    typename BRI::TempStorage ri;
+    typename BSL::TempStorage sl;
+  };
+  __shared__ PubSmem S;
+  __shared__ PendTmp T;
+  __shared__ longlong2 s_carry;
   pdl_enter();
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    if (!a.ctr[2]) {
-      a.ctr[0] += a.ctr[5];  // ids
-      a.ctr[1] += a.ctr[3];  // arena cursor (the batch's strings were placed by the byte scan)
+  cgn::grid_group grid = cgn::this_grid();
+  const int64_t np = (int64_t)a.ctr[4];
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  auto clear_mbits = [&]() {
+    for (int64_t m = gtid; m < a.n_msg; m += gstride) {
+      const int64_t i = a.msg_off[m];
+      if (i < a.n_bytes) a.mbits[i >> 5] = 0u;
     }
-    a.ctr[3] = a.ctr[4] = a.ctr[5] = 0;  // batch counters zero for the next batch
+  };
+  if (np == 0) {  // uniform: no new string and no duplicate of one (the counters are already zero)
+    clear_mbits();
+    return;
+  }
+  // 1. owners flagged, duplicates of long keys compared with their owner; CTA-reduced counters
+  {
+    longlong2 own = make_longlong2(0, 0);
+    for (int64_t j = gtid; j < np; j += gstride) {
+      const int64_t t = a.pend_t[j], sl = a.pend_slot[t];
+      const int len = a.tlen[t];
+      const int64_t o = a.owner[sl];
+      if (o == t) {
+        a.tnew[t] = 1;
+        own.x += 1;
+        own.y += len;
+      } else if (!(a.slots[sl].key >> 63) && !bytes_equal(a.text + a.tstart[t], a.text + a.tstart[o], len)) {
+        atomicOr(a.ctr + 2, (unsigned long long)TERR_COLLISION);
+      }
+    }
+    own = BRL(T.rl).Reduce(own, [](longlong2 x, longlong2 y) { return make_longlong2(x.x + y.x, x.y + y.y); });
+    if (threadIdx.x == 0 && own.x) {
+      atomicAdd(a.ctr + 5, (unsigned long long)own.x);
+      atomicAdd(a.ctr + 3, (unsigned long long)own.y);
+    }
+  }
+  grid.sync();
+  // 2. capacity check before anything is published
+  if (gtid == 0 && !a.ctr[2]) {
+    if ((int64_t)(a.ctr[0] + a.ctr[5]) > a.max_ids) a.ctr[2] |= TERR_IDS;
+    if ((int64_t)(a.ctr[1] + a.ctr[3]) > a.arena_cap) a.ctr[2] |= TERR_ARENA;
+  }
+  grid.sync();
+  const bool failed = a.ctr[2] != 0;
+  const int64_t nt = *a.n_tokens;
+  const int64_t ntiles = (nt + RANK_TILE - 1) / RANK_TILE;
+  if (!failed) {
+    // 3. new strings and their bytes per rank tile
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t t0 = tile * RANK_TILE;
+      int2 c = make_int2(0, 0);
+      for (int k = 0; k < RANK_TILE / 256; ++k) {
+        const int64_t t = t0 + (int64_t)k * 256 + threadIdx.x;
+        if (t < nt && a.tnew[t]) {
+          c.x += 1;
+          c.y += a.tlen[t];
+        }
+      }
+      c = BRI(T.ri).Reduce(c, [](int2 x, int2 y) { return make_int2(x.x + y.x, x.y + y.y); });
+      if (threadIdx.x == 0) {
+        a.tile_cnt[tile] = c.x;
+        a.tile_bytes[tile] = c.y;
+      }
+      __syncthreads();
+    }
+    grid.sync();
+    // 4. exclusive scan of (count, bytes) over the tiles (one CTA)
+    if (blockIdx.x == 0) {
+      auto add = [](longlong2 x, longlong2 y) { return make_longlong2(x.x + y.x, x.y + y.y); };
+      if (threadIdx.x == 0) s_carry = make_longlong2(0, 0);
+      __syncthreads();
+      for (int64_t b = 0; b < ntiles; b += 256) {
+        const int64_t i = b + threadIdx.x;
+        longlong2 v = i < ntiles ? make_longlong2(a.tile_cnt[i], a.tile_bytes[i]) : make_longlong2(0, 0), ex, tot;
+        BSL(T.sl).ExclusiveScan(v, ex, make_longlong2(0, 0), add, tot);
+        if (i < ntiles) {
+          a.tile_cnt[i] = s_carry.x + ex.x;
+          a.tile_bytes[i] = s_carry.y + ex.y;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry = add(s_carry, tot);
+        __syncthreads();
+      }
+    }
+    grid.sync();
+    // 5. ids and arena bytes
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      rank_publish_tile(a, tile, nt, S);
+      __syncthreads();
+    }
+  }
+  grid.sync();
+  // 6. owners publish their ids (or, when the batch failed, their claims are rolled back)
+  for (int64_t j = gtid; j < np; j += gstride) {
+    const int64_t t = a.pend_t[j], sl = a.pend_slot[t];
+    if (a.owner[sl] != t) continue;
+    if (failed) {
+      a.slots[sl].key = 0;
+      a.tnew[t] = 0;
+    } else {
+      a.slots[sl].id = a.tok[t];
+    }
+  }
+  grid.sync();
+  // 7. duplicates of new strings read the published ids
+  for (int64_t j = gtid; j < np; j += gstride) {
+    const int64_t t = a.pend_t[j], sl = a.pend_slot[t];
+    if (a.owner[sl] != t) a.tok[t] = a.slots[sl].id;
+  }
+  grid.sync();
+  // 8. owners reset, the batch's message-start bits cleared, counters advanced
+  for (int64_t j = gtid; j < np; j += gstride) a.owner[a.pend_slot[a.pend_t[j]]] = INT64_MAX;
+  clear_mbits();
+  if (gtid == 0) {
+    if (!failed) {
+      a.ctr[0] += a.ctr[5];
+      a.ctr[1] += a.ctr[3];
+    }
+    a.ctr[3] = a.ctr[4] = a.ctr[5] = 0;
   }
 }
 
@@ -848,18 +851,32 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   if (nchunks > 0) SFKV_CUDA(launch_pdl(chunk_emit_kernel, dim3((unsigned)nchunks), dim3(CHUNK_THREADS), st, a));
   SFKV_CUDA(launch_pdl(copy_count_kernel, dim3(1), dim3(1), st, a.chunk_off, nchunks, n_tokens));
   const int g = grid_for(tb, 256, sms * 8);
-  SFKV_CUDA(launch_pdl(tok_resolve_kernel, dim3(g), dim3(256), st, a));
-  SFKV_CUDA(launch_pdl(tok_check_kernel, dim3(1), dim3(32), st, a));
-  SFKV_LAUNCH_CHECK("chunk_emit/probe/resolve");
-  const unsigned rg = (unsigned)(nrt < sms * 4 ? (nrt > 0 ? nrt : 1) : sms * 4);  // grid-stride over tiles
-  SFKV_CUDA(launch_pdl(rank_count_kernel, dim3(rg), dim3(256), st, a));
-  SFKV_CUDA(launch_pdl(rank_scan_kernel, dim3(1), dim3(1024), st, a));
-  SFKV_CUDA(launch_pdl(rank_publish_kernel, dim3(rg), dim3(256), st, a));
-  SFKV_CUDA(launch_pdl(tok_final_kernel, dim3(g), dim3(256), st, a));
-  SFKV_CUDA(launch_pdl(tok_final2_kernel, dim3(g), dim3(256), st, a));
   SFKV_CUDA(launch_pdl(req_tokoff_kernel, dim3(grid_for((n_req + 1) * 32, 256, sms * 8)), dim3(256), st, a));
-  SFKV_CUDA(launch_pdl(tok_owner_reset_kernel, dim3(g), dim3(256), st, a));
-  SFKV_CUDA(launch_pdl(tok_commit_kernel, dim3(1), dim3(32), st, a));
+  {  // the pending phase: one cooperative launch (grid barriers between its steps)
+    static int coop_grid = 0;
+    if (!coop_grid) {
+      int per_sm = 0;
+      SFKV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tok_pending_kernel, 256, 0));
+      coop_grid = std::max(1, std::min(per_sm, 4)) * sms;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)coop_grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tok_pending_kernel, a);
+    if (e != cudaSuccess) {  // a cooperative launch may not take programmatic serialization
+      cudaGetLastError();
+      cfg.numAttrs = 1;
+      SFKV_CUDA(cudaLaunchKernelEx(&cfg, tok_pending_kernel, a));
+    }
+  }
   SFKV_LAUNCH_CHECK("rank/publish/final");
   return 0;
 }
