@@ -342,14 +342,17 @@ __device__ __forceinline__ int select_bit(uint32_t w, int r) {  // position of t
   return -1;
 }
 
-__global__ void alloc_kernel(CommitArgs a) {
+__global__ void __launch_bounds__(256) alloc_kernel(CommitArgs a) {
   pdl_enter();
-  if (a.ctr->error) return;
+  __shared__ int s_skip;  // one CTA-uniform decision (the block reduce below needs every thread)
   const int64_t total_free = a.s.wprefix[a.n_words];
-  if (a.s.rank[a.n_items] > total_free) {  // exhausted: abort before any block is touched
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.ctr->error = SFKV_EPOOL;
-    return;
+  if (threadIdx.x == 0) s_skip = a.ctr->error ? 1 : (a.s.rank[a.n_items] > total_free ? 2 : 0);
+  __syncthreads();
+  if (s_skip) {
+    if (s_skip == 2 && blockIdx.x == 0 && threadIdx.x == 0) a.ctr->error = SFKV_EPOOL;  // exhausted: abort
+    return;                                                                            // before any block is touched
   }
+  int n_new = 0, n_live = 0;
   FOR_ITEMS(a, item) {
     const uint8_t cat = a.s.cat[item];
     if (cat != CAT_OWN && cat != CAT_PRIV) continue;
@@ -384,12 +387,20 @@ __global__ void alloc_kernel(CommitArgs a) {
       a.slots[s].val = id;
       a.blk_slot[id] = s;
       a.blk_in_table[id] = 1;
-      atomic_add_i64(&a.ctr->table_live, 1ll);
+      ++n_live;
     } else {
       a.blk_slot[id] = -1;
       a.blk_in_table[id] = 0;
     }
-    atomic_add_i64(&a.ctr->blocks_in_use, 1ll);
+    ++n_new;
+  }
+  // one pair of counter atomics per CTA (per-block atomics on one address serialise in L2)
+  using BR = cub::BlockReduce<int2, 256>;
+  __shared__ typename BR::TempStorage tmp;
+  const int2 tot = BR(tmp).Reduce(make_int2(n_new, n_live), [](int2 x, int2 y) { return make_int2(x.x + y.x, x.y + y.y); });
+  if (threadIdx.x == 0 && tot.x) {
+    atomic_add_i64(&a.ctr->blocks_in_use, (long long)tot.x);
+    if (tot.y) atomic_add_i64(&a.ctr->table_live, (long long)tot.y);
   }
 }
 
