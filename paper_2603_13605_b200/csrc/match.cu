@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(PREP_THREADS) match_prep_kernel(PrepArgs P) {
   q.pad = 0;
   P.rec[r] = q;
   P.blk_off[r] = b;
-  for (int64_t t = (b + WT - 1) / WT; t * WT < b + nb; ++t) {
+  for (int64_t t = (b + WT - 1) / WT; P.trec && t * WT < b + nb; ++t) {  // (the per-request lookup has no tiles)
     TileRec tr;
     tr.kb = (int32_t)(t * WT - b);
     tr.s = q.tok_off + (int64_t)tr.kb * BT;
@@ -1095,7 +1095,9 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   P.pin_len = p->pin_len;
   P.blk_off = a.blk_off;
   P.rec = rec;
-  P.trec = trec;
+  // the one-pass lookup (one warp per request) reads request records only: no tile records
+  const bool per_request = a.out_block && !a.out_M && a.n >= LR_MIN_REQUESTS && a.n_items <= LR_MAX_AVG_BLOCKS * a.n;
+  P.trec = per_request ? nullptr : trec;
   P.out_M = a.out_M;
   P.out_hit = a.out_hit;
   P.ticket = use_ticket ? ticket : nullptr;
@@ -1132,8 +1134,7 @@ int launch_match(sfkv_pool* p, const MatchArgs& a, int64_t* tile_state, cudaStre
   CUtensorMap tm;
   memset(&tm, 0, sizeof(tm));
   K.tok_rows = a.n_tok_bound / 32;
-  const bool per_request = a.out_block && !a.out_M && a.n >= LR_MIN_REQUESTS &&
-                           a.n_items <= LR_MAX_AVG_BLOCKS * a.n;
+
   if ((a.out_M || per_request) && K.tok_rows > 0) {
     if (int rc = encode_token_map(a, tm, K.tok_rows)) return rc;
   } else {
