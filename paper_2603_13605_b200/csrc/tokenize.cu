@@ -341,33 +341,43 @@ __global__ void __launch_bounds__(CHUNK_THREADS, SFKV_EMIT_MINB) chunk_emit_kern
     for (uint32_t mm = m; mm; mm &= mm - 1) slist[k++] = (uint16_t)(threadIdx.x * 16 + __ffs(mm) - 1);
   }
   __syncthreads();
+  // loop invariants in 32-bit form (the loop runs at the 32-register cap: 64-bit invariants get
+  // rematerialised every iteration)
   const int stage_end = (int)(lim < CHUNK + OVER ? lim : CHUNK + OVER);
+  const bool text_ends_here = lim <= CHUNK + OVER;  // bytes past the text are staged as spaces
   const int64_t tb0 = a.chunk_off[blockIdx.x];
+  const uint32_t* sb32 = reinterpret_cast<const uint32_t*>(sb);
   for (int i = threadIdx.x; i < total; i += CHUNK_THREADS) {
     const int s0 = slist[i];
     bool pend;
-    // the token's end: the first boundary bit after s0, from a 64-bit window of the bitmap (one
-    // step for tokens of up to 32 bytes; longer ones walk on)
+    // the token's end: the first boundary bit after s0, from a 32-bit funnel window of the
+    // bitmap (one step for tokens of up to 32 bytes; longer ones walk on)
     int w = (s0 + 1) >> 5;
-    const uint64_t win = (((uint64_t)sbnd[w + 1] << 32) | sbnd[w]) >> ((s0 + 1) & 31);
-    uint32_t bits = 1u;
+    uint32_t bits = __funnelshift_r(sbnd[w], sbnd[w + 1], (s0 + 1) & 31);
     int e;
-    if (win) {
-      e = s0 + __ffsll((long long)win);
+    if (bits) {
+      e = s0 + __ffs(bits);
     } else {
-      ++w;
-      bits = 0u;
-      while (!bits && (w + 1) * 32 < stage_end) bits = sbnd[++w];
-      e = bits ? w * 32 + __ffs(bits) - 1 : CHUNK + OVER;
+      e = CHUNK + OVER;
+      for (int p = s0 + 33; p < stage_end; p = (p & ~31) + 32) {
+        const uint32_t wb = sbnd[p >> 5] & (~0u << (p & 31));
+        if (wb) {
+          e = (p & ~31) + __ffs(wb) - 1;
+          bits = 1u;
+          break;
+        }
+      }
     }
-    if (e < stage_end || (bits && stage_end == lim)) {
+    if (e < stage_end || (bits && text_ends_here)) {
       const int len = e - s0;
       if (len <= 7) {
-        const int a8 = s0 & ~7, b8 = (s0 & 7) * 8;
-        const unsigned long long lo = *reinterpret_cast<const unsigned long long*>(sb + a8);
-        const unsigned long long hi = *reinterpret_cast<const unsigned long long*>(sb + a8 + 8);
-        unsigned long long raw = b8 ? (lo >> b8) | (hi << (64 - b8)) : lo;
-        raw &= (1ull << (8 * len)) - 1;
+        // the token's bytes from three aligned 32-bit words and two funnel shifts
+        const int a4 = s0 >> 2, sh = (s0 & 3) * 8;
+        const uint32_t w0 = sb32[a4], w1 = sb32[a4 + 1], w2 = sb32[a4 + 2];
+        uint32_t lo = __funnelshift_r(w0, w1, sh), hi = __funnelshift_r(w1, w2, sh);
+        lo = len >= 4 ? lo : lo & ((1u << (8 * len)) - 1u);
+        hi = len > 4 ? hi & ((1u << (8 * (len - 4))) - 1u) : 0u;
+        const unsigned long long raw = ((unsigned long long)hi << 32) | lo;
         pend = probe_key(a, tb0 + i, c0 + s0, (1ull << 63) | ((unsigned long long)len << 56) | raw, sb + s0, len);
       } else {
         pend = probe_key(a, tb0 + i, c0 + s0, tok_key_smem(sb, s0, len), sb + s0, len);
