@@ -32,6 +32,13 @@
 
 namespace sfkv {
 
+#ifndef SFKV_FREE_FORK
+#define SFKV_FREE_FORK 1
+#endif
+#ifndef SFKV_REBUILD_AUX
+#define SFKV_REBUILD_AUX 1
+#endif
+
 enum : uint8_t { CAT_NONE = 0, CAT_HIT = 1, CAT_DUP = 2, CAT_OWN = 3, CAT_PRIV = 4 };
 
 struct CommitScratch {
@@ -692,10 +699,14 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   // 0. the free-bitmap prefix (allocation order) depends only on the pool before this batch: it
   //    runs on the aux stream beside the match / admission / classification and joins before alloc
   int64_t* tmp_free = a.s.scan_tmp + scan_scratch_elems(ni);
+#if SFKV_FREE_FORK
   SFKV_CUDA(cudaEventRecord(p->ev_fork, st));
   SFKV_CUDA(cudaStreamWaitEvent(p->aux, p->ev_fork, 0));
   if (int rc = exclusive_scan(FreeCount{p->free_bits}, p->n_words, a.s.wprefix, tmp_free, p->aux)) return rc;
   SFKV_CUDA(cudaEventRecord(p->ev_join, p->aux));
+#else
+  if (int rc = exclusive_scan(FreeCount{p->free_bits}, p->n_words, a.s.wprefix, tmp_free, st)) return rc;
+#endif
   // 1. blocks per request, chained hashes, M = LCP(old pin, tokens)
   MatchArgs m{};  // the match launch also writes blk_off (its prep kernel scans the requests)
   m.n = n;
@@ -719,7 +730,9 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   SFKV_CUDA(launch_pdl(categorize_kernel, dim3(g), dim3(256), st, a));
   SFKV_LAUNCH_CHECK("probe/resolve/categorize");
   if (int rc = exclusive_scan(NeedAlloc{a.s.cat}, ni, a.s.rank, a.s.scan_tmp, st)) return rc;
+#if SFKV_FREE_FORK
   SFKV_CUDA(cudaStreamWaitEvent(st, p->ev_join, 0));  // the free-bitmap prefix
+#endif
   SFKV_CUDA(launch_pdl(alloc_kernel, dim3(g), dim3(256), st, a));
   SFKV_CUDA(launch_pdl(refs_kernel, dim3(g), dim3(256), st, a));
   SFKV_CUDA(launch_pdl(clear_owner_kernel, dim3(g), dim3(256), st, a));
@@ -741,11 +754,16 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
   SFKV_LAUNCH_CHECK("release/install");
   // the tombstone check / rebuild touches only the table: it follows the release on the aux stream,
   // beside the payload copy, and the join orders it before anything later on the pool stream
+#if SFKV_REBUILD_AUX
   if (int rc = maybe_rebuild_table(p, meta)) return rc;
+#endif
   if (meta != st) {
     SFKV_CUDA(cudaEventRecord(p->ev_join, meta));
     SFKV_CUDA(cudaStreamWaitEvent(st, p->ev_join, 0));
   }
+#if !SFKV_REBUILD_AUX
+  if (int rc = maybe_rebuild_table(p, st)) return rc;
+#endif
   return 0;
 }
 

@@ -936,6 +936,7 @@ __global__ void __launch_bounds__(LR_THREADS, SFKV_LR_MINB) lookup_req_kernel(Ma
   int32_t len, pl, wf;
   unpack_rec(K.rec + r, bo, to, len, pl, wf);
   const int64_t nb = (len + BT - 1) / BT, nfull = len / BT;
+  const int sh_req = (int)(to & 3);
   const int64_t tok_total = K.rec[A.n].tok_off;
   const int64_t ntile = (nb + WT - 1) / WT;
   const int64_t tok_limit = K.tok_rows * 32;
@@ -970,7 +971,20 @@ __global__ void __launch_bounds__(LR_THREADS, SFKV_LR_MINB) lookup_req_kernel(Ma
     uint32_t t[BT];
     if (staged) {
       mbar_wait(&s_bar[warp][i & 1], (uint32_t)((i >> 1) & 1));
-      if (valid) load_block_swz(s_tok[warp][i & 1], (int)(start - (((to + i * WT * BT) >> 5) << 5)), nval, t);
+      if (valid) {  // every block of the request shares the token alignment: no per-lane funnel
+        const int o = (int)(start - (((to + i * WT * BT) >> 5) << 5));
+        switch (sh_req) {
+          case 0: load_swz_sh<0>(s_tok[warp][i & 1], o, t); break;
+          case 1: load_swz_sh<1>(s_tok[warp][i & 1], o, t); break;
+          case 2: load_swz_sh<2>(s_tok[warp][i & 1], o, t); break;
+          default: load_swz_sh<3>(s_tok[warp][i & 1], o, t); break;
+        }
+        if (nval < BT) {
+#pragma unroll
+          for (int j = 0; j < BT; ++j)
+            if (j >= nval) t[j] = 0u;
+        }
+      }
     } else if (valid) {
       load_block(A.tok, start, nval, tok_total, t);
     }
