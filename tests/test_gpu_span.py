@@ -1,11 +1,12 @@
-"""Match span pass (csrc/match.cu, match_span_kernel) against the CPU oracle on batch shapes that
-stress its decomposition: a CTA owns the blocks whose first token lies in one 2048-token span of
-the CSR batch, so requests that cross many spans (the carry-in chain sum and first mismatch travel
-by look-back), spans dense with tiny or empty requests (several table rounds per span), batches
-whose length is an exact multiple of the span, mismatches in any span of a long request, and
-successive launches of very different sizes (the per-span statuses alternate between two
-buffers that each launch clears for the next) must all give the oracle's M and chained hashes
-bit for bit. Reference semantics: prefix_match (simulated_backend.cpp:153-162)."""
+"""Match-path stress shapes against the CPU oracle (M and chained hashes bit for bit). Written for
+the one-launch span pass this round measured and dropped (commit 050696d), they
+now exercise the prep / block / chain path on the batch shapes that stress any decomposition:
+requests crossing many tiles with the first mismatch in any of them (or at a tile / span
+boundary), thousands of tiny and empty requests (tiles crossing dozens of requests, the
+request-window fallback of the block pass), batch lengths at exact multiples of 2048 tokens,
+successive launches of very different sizes on one pool (the prep look-back statuses are
+epoch-tagged in a per-pool buffer, never cleared between launches), repeated and unpinned
+workflows. Reference semantics: prefix_match (simulated_backend.cpp:153-162)."""
 import numpy as np
 import pytest
 
