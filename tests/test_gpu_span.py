@@ -72,8 +72,8 @@ def test_span_long_requests_mismatch_in_every_span(gpu_api, oracle_api):
 
 
 def test_span_dense_tiny_and_empty_requests(gpu_api, oracle_api):
-    """Thousands of 0-20-token requests: ~200 requests per span, so a span needs several table
-    rounds; empty requests sit at span boundaries and at the batch end."""
+    """Thousands of 0-20-token requests: tiles that cross dozens of requests (the block pass's
+    request-window fallback); empty requests among them and at the batch end."""
     rng = np.random.default_rng(12)
     n = 3000
     g, o = _pools(gpu_api, oracle_api, n, 4)
@@ -113,9 +113,8 @@ def test_span_exact_multiples_and_boundaries(gpu_api, oracle_api, tail):
 
 
 def test_span_launches_of_alternating_size(gpu_api, oracle_api):
-    """Large, small, large, tiny, larger launches in a row on one pool: each launch's statuses
-    live in one of two buffers that the other parity's launches clear (slots left by a larger
-    earlier launch are cleared by the host first)."""
+    """Large, small, large, tiny, larger launches in a row on one pool: stale look-back statuses
+    left by a larger earlier launch must never be read as current (epoch-tagged prep statuses)."""
     rng = np.random.default_rng(14)
     n = 64
     g, o = _pools(gpu_api, oracle_api, n, 1100)
