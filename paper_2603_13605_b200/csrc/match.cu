@@ -909,7 +909,10 @@ __global__ void __launch_bounds__(MATCH_THREADS) match_chain_kernel(MatchKernelA
 // no chain pass, no per-block local sums / request ids in HBM, no second read of the request's
 // tokens (the two-pass lookup re-read them for the verify: ~1.64x the algorithmic traffic).
 // Output identical to the two-pass path (and sfo_lookup_batch): out_block per block, out_hit.
-constexpr int LR_THREADS = 128;
+#ifndef SFKV_LR_THREADS
+#define SFKV_LR_THREADS 32
+#endif
+constexpr int LR_THREADS = SFKV_LR_THREADS;
 #ifndef SFKV_LR_MINB
 #define SFKV_LR_MINB 1
 #endif
