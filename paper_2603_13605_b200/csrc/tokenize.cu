@@ -88,12 +88,15 @@ __device__ __forceinline__ bool is_space(uint8_t c) { return c == ' ' || (c >= '
 //   eq20:       ((b & 0x7F) ^ 0x20) + 0x7F leaves bit 7 clear iff the byte is 0x20
 // bytes >= 0x80 are never spaces. (The __vcmp*4 intrinsics are emulated on sm_100: ~3x the
 // instructions; the count pass was issue-bound on them.)
-__device__ __forceinline__ uint32_t space_mask4(uint32_t w) {
+// bit 7 of every byte of w that is a C-locale space (the SWAR test below, uncompacted)
+__device__ __forceinline__ uint32_t space_hi4(uint32_t w) {
   const uint32_t lo7 = w & 0x7F7F7F7Fu;
   const uint32_t ge9 = lo7 + 0x77777777u, ge14 = lo7 + 0x72727272u;
   const uint32_t ne20 = (lo7 ^ 0x20202020u) + 0x7F7F7F7Fu;
-  const uint32_t sp = ((ge9 & ~ge14) | ~ne20) & ~w & 0x80808080u;
-  return (((sp >> 7) * 0x01020408u) >> 24) & 0xFu;
+  return ((ge9 & ~ge14) | ~ne20) & ~w & 0x80808080u;
+}
+__device__ __forceinline__ uint32_t space_mask4(uint32_t w) {
+  return (((space_hi4(w) >> 7) * 0x01020408u) >> 24) & 0xFu;
 }
 
 // Table keys: tokens of <= 7 bytes are their own key (tag bit 63 | length | bytes): exact, no
@@ -237,15 +240,25 @@ __global__ void __launch_bounds__(COUNT_WARPS * 32) chunk_count_kernel(TokArgs a
         q[j >> 2] = (q[j >> 2] & ~(0xffu << (8 * (j & 3)))) | ((uint32_t)a.text[w + j] << (8 * (j & 3)));
       v[k] = make_uint4(q[0], q[1], q[2], q[3]);
     }
-    const uint32_t sp = space_mask4(v[k].x) | (space_mask4(v[k].y) << 4) | (space_mask4(v[k].z) << 8) |
-                        (space_mask4(v[k].w) << 12);
-    const uint32_t last = (sp >> 15) & 1u;
+    // starts counted in the uncompacted domain (bit 7 of each byte; the previous byte's space bit
+    // moves in by a byte shift): no multiply, the count pass was issue-bound on the IMAD pipe
+    const uint32_t s0 = space_hi4(v[k].x), s1 = space_hi4(v[k].y), s2 = space_hi4(v[k].z), s3 = space_hi4(v[k].w);
+    const uint32_t last = s3 >> 31;
     uint32_t prev = __shfl_up_sync(0xffffffffu, last, 1);
     if (lane == 0) prev = prev_last;
     prev_last = __shfl_sync(0xffffffffu, last, 31);
     const uint32_t ms = (mw[k] >> (w & 31)) & 0xffffu;
-    const uint32_t m = w < a.n_bytes ? (~sp & (((sp << 1) | prev) | ms) & 0xffffu) : 0u;
-    c += __popc(m);
+    if (w < a.n_bytes) {
+      if (!ms) {
+        constexpr uint32_t H = 0x80808080u;
+        c += __popc(~s0 & ((s0 << 8) | (prev << 7)) & H) + __popc(~s1 & ((s1 << 8) | (s0 >> 24)) & H) +
+             __popc(~s2 & ((s2 << 8) | (s1 >> 24)) & H) + __popc(~s3 & ((s3 << 8) | (s2 >> 24)) & H);
+      } else {  // a message starts in this window (rare): the compact 16-bit form
+        const uint32_t sp = space_mask4(v[k].x) | (space_mask4(v[k].y) << 4) | (space_mask4(v[k].z) << 8) |
+                            (space_mask4(v[k].w) << 12);
+        c += __popc(~sp & (((sp << 1) | prev) | ms) & 0xffffu);
+      }
+    }
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
