@@ -54,7 +54,10 @@
 namespace sfkv {
 
 constexpr int WT = 32;                        // items per warp tile
-constexpr int MATCH_THREADS = 256;
+#ifndef SFKV_MATCH_THREADS
+#define SFKV_MATCH_THREADS 256
+#endif
+constexpr int MATCH_THREADS = SFKV_MATCH_THREADS;  // chain pass CTA
 #ifndef SFKV_BLOCK_THREADS
 #define SFKV_BLOCK_THREADS 64
 #endif
