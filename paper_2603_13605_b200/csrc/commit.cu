@@ -436,18 +436,17 @@ __global__ void clear_owner_kernel(CommitArgs a) {
 }
 
 // Drops one reference; frees the block at zero.
-__device__ __forceinline__ void release_block(const CommitArgs& a, int32_t id) {
+// Drops one reference; returns 1 when the block was freed (2 when it also left the table). The
+// caller sums the pool counters per warp: a flush of all pins frees ~1.7 M blocks, and three
+// global atomics per block on the same counters serialise in one L2 slice.
+__device__ __forceinline__ int release_block(const CommitArgs& a, int32_t id) {
   const uint32_t old = atomicSub(&a.blk_ref[id], 1u);
-  if (old == 1u) {
-    atomicOr(&a.free_bits[id >> 5], 1u << (id & 31));
-    atomic_add_i64(&a.ctr->blocks_in_use, -1ll);
-    if (a.blk_in_table[id]) {
-      a.slots[a.blk_slot[id]].key = KEY_TOMB;
-      a.blk_in_table[id] = 0;
-      atomic_add_i64(&a.ctr->table_live, -1ll);
-      atomic_add_i64(&a.ctr->table_tomb, 1ll);
-    }
-  }
+  if (old != 1u) return 0;
+  atomicOr(&a.free_bits[id >> 5], 1u << (id & 31));
+  if (!a.blk_in_table[id]) return 1;
+  a.slots[a.blk_slot[id]].key = KEY_TOMB;
+  a.blk_in_table[id] = 0;
+  return 2;
 }
 
 // One warp per request: release the old pin; install the new length (commit) or none (flush).
@@ -457,6 +456,7 @@ __global__ void release_kernel(CommitArgs a, int mode /*0 commit, 1 flush list, 
   if (mode == 0 && a.ctr->error) return;
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  int freed_blocks = 0, left_table = 0;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < a.n; r += warps) {
     if (mode == 0 && a.s.status[r] != SFKV_PIN_ACCEPTED) continue;
     const int32_t w = mode == 2 ? (int32_t)r : a.wf[r];
@@ -464,7 +464,11 @@ __global__ void release_kernel(CommitArgs a, int mode /*0 commit, 1 flush list, 
     if (pl >= 0) {
       const int32_t nb = a.pin_nblk[w];
       const int64_t pb = (int64_t)w * a.max_pin_blocks;
-      for (int32_t k = lane; k < nb; k += 32) release_block(a, a.pin_blk[pb + k]);
+      for (int32_t k = lane; k < nb; k += 32) {
+        const int f = release_block(a, a.pin_blk[pb + k]);
+        freed_blocks += f != 0;
+        left_table += f == 2;
+      }
     }
     __syncwarp();
     if (lane == 0) {
@@ -479,6 +483,15 @@ __global__ void release_kernel(CommitArgs a, int mode /*0 commit, 1 flush list, 
         a.pin_len[w] = -1;
         a.pin_nblk[w] = 0;
       }
+    }
+  }
+  freed_blocks = __reduce_add_sync(0xffffffffu, freed_blocks);
+  left_table = __reduce_add_sync(0xffffffffu, left_table);
+  if (lane == 0 && freed_blocks) {
+    atomic_add_i64(&a.ctr->blocks_in_use, -(long long)freed_blocks);
+    if (left_table) {
+      atomic_add_i64(&a.ctr->table_live, -(long long)left_table);
+      atomic_add_i64(&a.ctr->table_tomb, (long long)left_table);
     }
   }
 }
