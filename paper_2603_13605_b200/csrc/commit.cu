@@ -38,6 +38,10 @@ namespace sfkv {
 #ifndef SFKV_REBUILD_AUX
 #define SFKV_REBUILD_AUX 1
 #endif
+#ifndef SFKV_REL_THREADS
+#define SFKV_REL_THREADS 256
+#endif
+constexpr int REL_THREADS = SFKV_REL_THREADS;  // release: one warp per workflow
 
 enum : uint8_t { CAT_NONE = 0, CAT_HIT = 1, CAT_DUP = 2, CAT_OWN = 3, CAT_PRIV = 4 };
 
@@ -457,6 +461,7 @@ __global__ void release_kernel(CommitArgs a, int mode /*0 commit, 1 flush list, 
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   int freed_blocks = 0, left_table = 0;
+  long long occ_freed = 0;  // lane 0: tokens freed by this warp's workflows (flush modes)
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < a.n; r += warps) {
     if (mode == 0 && a.s.status[r] != SFKV_PIN_ACCEPTED) continue;
     const int32_t w = mode == 2 ? (int32_t)r : a.wf[r];
@@ -479,12 +484,13 @@ __global__ void release_kernel(CommitArgs a, int mode /*0 commit, 1 flush list, 
       } else {
         const int64_t freed = pl < 0 ? 0 : pl;
         if (out_freed) out_freed[r] = freed;
-        if (freed) atomic_add_i64(&a.ctr->occupancy, -(long long)freed);
+        occ_freed += freed;
         a.pin_len[w] = -1;
         a.pin_nblk[w] = 0;
       }
     }
   }
+  if (lane == 0 && occ_freed) atomic_add_i64(&a.ctr->occupancy, -occ_freed);
   freed_blocks = __reduce_add_sync(0xffffffffu, freed_blocks);
   left_table = __reduce_add_sync(0xffffffffu, left_table);
   if (lane == 0 && freed_blocks) {
@@ -761,7 +767,7 @@ int commit_dev(sfkv_pool* p, int64_t n, const int32_t* wf, const int64_t* tok_of
     meta = p->aux;
     if (int rc = launch_commit_payload(p, a, kv_src, kv_src_off, src, st)) return rc;
   }
-  SFKV_CUDA(launch_pdl(release_kernel, dim3(grid_for(n * 32, 256, sms * 8)), dim3(256), meta, a, 0, (int64_t*)nullptr));
+  SFKV_CUDA(launch_pdl(release_kernel, dim3(grid_for(n * 32, REL_THREADS, sms * 8 * (256 / REL_THREADS))), dim3(REL_THREADS), meta, a, 0, (int64_t*)nullptr));
   SFKV_CUDA(launch_pdl(install_kernel, dim3(g), dim3(256), meta, a));
   SFKV_CUDA(launch_pdl(commit_finish_kernel, dim3(grid_for(n, 256, sms)), dim3(256), meta, a));
   SFKV_LAUNCH_CHECK("release/install");
@@ -787,7 +793,7 @@ int flush_dev(sfkv_pool* p, int64_t n, const int32_t* wf, int64_t* out_freed, bo
   a.wf = wf;
   if (a.n <= 0) return 0;
   const int sms = sm_count_c();
-  release_kernel<<<grid_for(a.n * 32, 256, sms * 8), 256, 0, st>>>(a, all ? 2 : 1, out_freed);
+  release_kernel<<<grid_for(a.n * 32, REL_THREADS, sms * 8 * (256 / REL_THREADS)), REL_THREADS, 0, st>>>(a, all ? 2 : 1, out_freed);
   SFKV_LAUNCH_CHECK("flush release_kernel");
   return maybe_rebuild_table(p, p->stream);
 }
