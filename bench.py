@@ -1730,7 +1730,8 @@ def main():
         import torch
         import torch.distributed as tdist
         torch.cuda.set_device(local_rank)
-        backend = args.dist_backend or ("nccl" if args.impl == "ours" else "gloo")
+        # NCCL refuses two ranks on one device: the same-device test mode runs over gloo
+        backend = args.dist_backend or ("nccl" if args.impl == "ours" and not args.same_device else "gloo")
         tdist.init_process_group(backend)
     if args.impl == "reference":
         rc = run_reference_arm(args, rank, world)
