@@ -100,6 +100,14 @@ __device__ __forceinline__ uint32_t space_hi4(uint32_t w) {
 __device__ __forceinline__ uint32_t space_mask4(uint32_t w) {
   return (((space_hi4(w) >> 7) * 0x01020408u) >> 24) & 0xFu;
 }
+// 16 bytes -> 16-bit space mask with one multiply per two words: the hi bits of word x at 8j and
+// of word y at 8j + 4 gather into bits 24-27 / 28-31 of the product (no colliding partial products,
+// so no carries).
+__device__ __forceinline__ uint32_t space_bits16(uint4 v) {
+  const uint32_t lo = (((space_hi4(v.x) >> 7) | (space_hi4(v.y) >> 3)) * 0x01020408u) >> 24;
+  const uint32_t hi = (((space_hi4(v.z) >> 7) | (space_hi4(v.w) >> 3)) * 0x01020408u) >> 24;
+  return lo | (hi << 8);
+}
 
 // Table keys: tokens of <= 7 bytes are their own key (tag bit 63 | length | bytes): exact, no
 // verification. Longer tokens key on a 63-bit hash and are verified against the arena / owner.
@@ -159,6 +167,7 @@ struct TokArgs {
   const uint8_t* text;
   int64_t n_bytes;
   uint32_t* mbits;       // message-start bitmap
+  uint16_t* spbits;      // [nchunks * CHUNK / 16] space masks per 16-byte window (count pass)
   int64_t* chunk_off;    // [nchunks + 1]
   int64_t* tstart;       // [token bound] byte start of pending tokens (claims / duplicates)
   int64_t* pend_t;       // pending tokens (claims / duplicates of new strings)
@@ -214,6 +223,9 @@ __device__ __forceinline__ uint32_t start_mask16(const TokArgs& a, int64_t base)
 // loads, no branch between them), the previous byte of a window comes from the neighbouring lane
 // (or the previous round's last lane) instead of another load, then a warp reduction.
 constexpr int COUNT_WARPS = 8;
+#ifndef SFKV_TOK_SPBITS
+#define SFKV_TOK_SPBITS 1
+#endif
 #ifndef SFKV_TOKOFF_FORK
 #define SFKV_TOKOFF_FORK 1
 #endif
@@ -272,6 +284,16 @@ __global__ void __launch_bounds__(COUNT_WARPS * 32) chunk_count_kernel(TokArgs a
         q[j >> 2] = (q[j >> 2] & ~(0xffu << (8 * (j & 3)))) | ((uint32_t)a.text[w + j] << (8 * (j & 3)));
       v[k] = make_uint4(q[0], q[1], q[2], q[3]);
     }
+#if SFKV_TOK_SPBITS
+    // the window's compact 16-bit space mask is stored for the emit pass (which then builds its
+    // boundary bitmap and start masks from it instead of re-testing every staged byte)
+    const uint32_t sp = space_bits16(v[k]);
+    a.spbits[w >> 4] = (uint16_t)sp;  // every window of the chunk (past the text: all spaces)
+    uint32_t prev = __shfl_up_sync(0xffffffffu, sp >> 15, 1);
+    if (lane == 0) prev = prev_last;
+    prev_last = __shfl_sync(0xffffffffu, sp >> 15, 31);
+    if (w < a.n_bytes) c += __popc(~sp & (((sp << 1) | prev) | ((mw[k] >> (w & 31)) & 0xffffu)) & 0xffffu);
+#else
     // starts counted in the uncompacted domain (bit 7 of each byte; the previous byte's space bit
     // moves in by a byte shift): no multiply, the count pass was issue-bound on the IMAD pipe
     const uint32_t s0 = space_hi4(v[k].x), s1 = space_hi4(v[k].y), s2 = space_hi4(v[k].z), s3 = space_hi4(v[k].w);
@@ -291,6 +313,7 @@ __global__ void __launch_bounds__(COUNT_WARPS * 32) chunk_count_kernel(TokArgs a
         c += __popc(~sp & (((sp << 1) | prev) | ms) & 0xffffu);
       }
     }
+#endif
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
@@ -350,12 +373,30 @@ __global__ void __launch_bounds__(CHUNK_THREADS, SFKV_EMIT_MINB) chunk_emit_kern
       for (int j = 0; j < 16; ++j) sb[CHUNK + threadIdx.x * 16 + j] = ob + j < a.n_bytes ? a.text[ob + j] : ' ';
     }
   }
+  __shared__ uint16_t slist[CHUNK];
+  __shared__ uint32_t sbnd[(CHUNK + OVER) / 32 + 1];
+#if SFKV_TOK_SPBITS
+  // boundary bitmap = the count pass's space masks | message starts (words past the text: all set)
+  __shared__ uint32_t s_sp[CHUNK / 32 + 1];  // [0]: the word before the chunk
+  {
+    const uint32_t* sp32 = reinterpret_cast<const uint32_t*>(a.spbits);
+    if (threadIdx.x < (CHUNK + OVER) / 32) {
+      const int64_t w = (c0 >> 5) + threadIdx.x;
+      const bool in = c0 + threadIdx.x * 32 < a.n_bytes;
+      const uint32_t ms = in ? a.mbits[w] : 0xffffffffu, sp = in ? sp32[w] : 0xffffffffu;
+      sbits[threadIdx.x] = ms;
+      sbnd[threadIdx.x] = sp | ms;
+      if (threadIdx.x < CHUNK / 32) s_sp[threadIdx.x + 1] = sp;
+    } else if (threadIdx.x == (CHUNK + OVER) / 32) {
+      s_sp[0] = c0 == 0 ? 0x80000000u : sp32[(c0 >> 5) - 1];
+    }
+  }
+#else
   if (threadIdx.x < (CHUNK + OVER) / 32) {
     const int64_t w = (c0 >> 5) + threadIdx.x;
     sbits[threadIdx.x] = (c0 + threadIdx.x * 32 < a.n_bytes) ? a.mbits[w] : 0xffffffffu;
   }
-  __shared__ uint16_t slist[CHUNK];
-  __shared__ uint32_t sbnd[(CHUNK + OVER) / 32 + 1];
+#endif
   constexpr int PW = CHUNK / 32;  // pending bitmap words (<= CHUNK tokens: every byte may start a message)
   __shared__ uint32_t s_pend[PW];
   __shared__ int s_any_pend;
@@ -369,6 +410,15 @@ __global__ void __launch_bounds__(CHUNK_THREADS, SFKV_EMIT_MINB) chunk_emit_kern
   // from the staged bytes: 16 boundary bits (space | message start) per thread into the bitmap, and
   // the thread's token starts (non-space after a space or at a message start)
   uint32_t m = 0;
+#if SFKV_TOK_SPBITS
+  if (base < a.n_bytes) {  // the thread's 16 bytes: starts from the staged space / message words
+    const int t = threadIdx.x, sh = (t & 1) * 16;
+    const uint32_t spw = s_sp[(t >> 1) + 1];
+    const uint32_t sp = (spw >> sh) & 0xffffu, ms = (sbits[t >> 1] >> sh) & 0xffffu;
+    const uint32_t prev = (t & 1) ? (spw >> 15) & 1u : s_sp[t >> 1] >> 31;
+    m = ~sp & ((sp << 1) | prev | ms) & 0xffffu;
+  }
+#else
   for (int o = threadIdx.x * 16; o < CHUNK + OVER; o += CHUNK_THREADS * 16) {
     const uint4 v = *reinterpret_cast<const uint4*>(sb + o);
     const uint32_t sp = space_mask4(v.x) | (space_mask4(v.y) << 4) | (space_mask4(v.z) << 8) | (space_mask4(v.w) << 12);
@@ -380,6 +430,7 @@ __global__ void __launch_bounds__(CHUNK_THREADS, SFKV_EMIT_MINB) chunk_emit_kern
       m = ~sp & (((sp << 1) | prev_sp) | ms) & 0xffffu;
     }
   }
+#endif
   int excl, total;
   BS(tmp).ExclusiveSum(__popc(m), excl, total);
   {
@@ -850,7 +901,8 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
                o_co = cv.take<int64_t>(nchunks + 1), o_ts = cv.take<int64_t>(tb), o_pt = cv.take<int64_t>(tb),
                o_ps = cv.take<int64_t>(tb), o_tc = cv.take<int64_t>(nrt + 1),
                o_tby = cv.take<int64_t>(nrt + 1), o_tl = cv.take<int32_t>(tb),
-               o_tmp = cv.take<int64_t>(scan_scratch_elems(nchunks));
+               o_tmp = cv.take<int64_t>(scan_scratch_elems(nchunks)),
+               o_sp = cv.take<uint32_t>(nchunks * (CHUNK / 32) + 1);
   if (int rc = it->scratch.ensure(cv.off)) return rc;
   if (it->mbits.bytes < nwords * sizeof(uint32_t)) {  // grown: zero once, then kept zero
     if (int rc = it->mbits.ensure(nwords * sizeof(uint32_t))) return rc;
@@ -873,6 +925,7 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   a.text = text;
   a.n_bytes = n_bytes;
   a.mbits = it->mbits.as<uint32_t>();
+  a.spbits = reinterpret_cast<uint16_t*>(base + o_sp);
   a.chunk_off = reinterpret_cast<int64_t*>(base + o_co);
   a.tstart = reinterpret_cast<int64_t*>(base + o_ts);
   a.pend_t = reinterpret_cast<int64_t*>(base + o_pt);
