@@ -471,11 +471,12 @@ __global__ void __launch_bounds__(CHUNK_THREADS, SFKV_EMIT_MINB) chunk_emit_kern
         // the token's bytes from three aligned 32-bit words and two funnel shifts
         const int a4 = s0 >> 2, sh = (s0 & 3) * 8;
         const uint32_t w0 = sb32[a4], w1 = sb32[a4 + 1], w2 = sb32[a4 + 2];
-        uint32_t lo = __funnelshift_r(w0, w1, sh), hi = __funnelshift_r(w1, w2, sh);
-        lo = len >= 4 ? lo : lo & ((1u << (8 * len)) - 1u);
-        hi = len > 4 ? hi & ((1u << (8 * (len - 4))) - 1u) : 0u;
-        const unsigned long long raw = ((unsigned long long)hi << 32) | lo;
-        pend = probe_key(a, tb0 + i, c0 + s0, (1ull << 63) | ((unsigned long long)len << 56) | raw, sb + s0, len);
+        // one 64-bit byte mask (len <= 7: at most 56 bits) and the tag / length OR-ed into the
+        // high word: no per-length selects
+        const unsigned long long msk = ~(~0ull << (8 * len));
+        const uint32_t lo = __funnelshift_r(w0, w1, sh) & (uint32_t)msk;
+        const uint32_t hi = (__funnelshift_r(w1, w2, sh) & (uint32_t)(msk >> 32)) | 0x80000000u | ((uint32_t)len << 24);
+        pend = probe_key(a, tb0 + i, c0 + s0, ((unsigned long long)hi << 32) | lo, sb + s0, len);
       } else {
         pend = probe_key(a, tb0 + i, c0 + s0, tok_key_smem(sb, s0, len), sb + s0, len);
       }
