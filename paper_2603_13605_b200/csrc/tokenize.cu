@@ -229,96 +229,72 @@ constexpr int COUNT_WARPS = 8;
 #ifndef SFKV_TOKOFF_FORK
 #define SFKV_TOKOFF_FORK 1
 #endif
-#ifndef SFKV_COUNT_PERSIST
-#define SFKV_COUNT_PERSIST 0
-#endif
-// The warp's loads for one chunk (issued together, predicated) and the byte before it.
-struct CountLoads {
-  uint4 v[CHUNK / 512];
-  uint32_t mw[CHUNK / 512];
-  uint8_t before;
-};
-__device__ __forceinline__ void count_load(const TokArgs& a, int64_t chunk, int lane, uint64_t pol, CountLoads& L) {
-  const int64_t c0 = chunk * CHUNK;
+// One warp per chunk. A full chunk (every chunk but the text's last) takes a fast path with
+// chunk-relative 32-bit offsets and no bounds checks (the count pass is issue-bound: 64-bit window
+// arithmetic and per-window bounds tests were half its instructions); the last chunk takes the
+// generic path (bytes past the text are spaces). Every window's compact 16-bit space mask is
+// stored for the emit pass, which builds its boundary bitmap and start masks from those words.
+__device__ __forceinline__ int count_windows(const uint4* v, const uint32_t* mw, int lane, uint32_t prev_last,
+                                             uint16_t* spo) {
+  constexpr int KW = CHUNK / 512;
+  int c = 0;
 #pragma unroll
-  for (int k = 0; k < CHUNK / 512; ++k) {
-    const int64_t w = c0 + 512 * k + 16 * lane;
-    L.v[k] = make_uint4(0x20202020u, 0x20202020u, 0x20202020u, 0x20202020u);
-    if (w + 16 <= a.n_bytes) L.v[k] = ld_nc16_hint(a.text + w, pol);  // streamed: evict_first
-    L.mw[k] = w < a.n_bytes ? __ldg(a.mbits + (w >> 5)) : 0u;
+  for (int k = 0; k < KW; ++k) {
+    const uint32_t sp = space_bits16(v[k]);
+    spo[32 * k] = (uint16_t)sp;
+    uint32_t prev = __shfl_up_sync(0xffffffffu, sp >> 15, 1);
+    if (lane == 0) prev = prev_last;
+    prev_last = __shfl_sync(0xffffffffu, sp >> 15, 31);
+    c += __popc(~sp & (((sp << 1) | prev) | mw[k]) & 0xffffu);
   }
-  L.before = c0 == 0 ? (uint8_t)' ' : a.text[c0 - 1];
+  return c;
 }
-// Persistent warps (SFKV_COUNT_PERSIST=1): a warp walks chunks grid-stride with the next chunk's
-// loads in flight while it counts the current one. Measured slower (steady batch 0.325 vs 0.319 ms:
-// 72 registers, 3 CTAs per SM); one chunk per short-lived warp is kept.
 __global__ void __launch_bounds__(COUNT_WARPS * 32) chunk_count_kernel(TokArgs a, int64_t* counts, int64_t nchunks) {
   pdl_enter();
   constexpr int KW = CHUNK / 512;
   const int lane = threadIdx.x & 31;
-  const int64_t nwarps = SFKV_COUNT_PERSIST ? (int64_t)gridDim.x * COUNT_WARPS : nchunks;
-  int64_t chunk = (int64_t)blockIdx.x * COUNT_WARPS + (threadIdx.x >> 5);
+  const int64_t chunk = (int64_t)blockIdx.x * COUNT_WARPS + (threadIdx.x >> 5);
   if (chunk >= nchunks) return;
-  const uint64_t pol = l2_policy_first();
-  CountLoads nx;
-  count_load(a, chunk, lane, pol, nx);
-  for (; chunk < nchunks; chunk += nwarps) {
-  const CountLoads L = nx;
-  if (chunk + nwarps < nchunks) count_load(a, chunk + nwarps, lane, pol, nx);
   const int64_t c0 = chunk * CHUNK;
+  const uint64_t pol = l2_policy_first();
   uint4 v[KW];
-  uint32_t mw[KW];
+  uint32_t mw[KW];  // the window's 16 message-start bits
+  uint16_t* spo = a.spbits + (c0 >> 4) + lane;
+  const uint32_t prev0 = c0 == 0 ? 1u : (uint32_t)is_space(a.text[c0 - 1]);  // before lane 0, round 0
+  int c;
+  if (c0 + CHUNK <= a.n_bytes) {
+    const uint8_t* tx = a.text + c0 + 16 * lane;
+    const uint32_t* mb = a.mbits + (c0 >> 5) + (lane >> 1);
+    const int sh = (lane & 1) * 16;
 #pragma unroll
-  for (int k = 0; k < KW; ++k) {
-    v[k] = L.v[k];
-    mw[k] = L.mw[k];
-  }
-  uint32_t prev_last = (uint32_t)is_space(L.before);  // before lane 0, round 0
-  int c = 0;
-#pragma unroll
-  for (int k = 0; k < KW; ++k) {
-    const int64_t w = c0 + 512 * k + 16 * lane;
-    if (w < a.n_bytes && w + 16 > a.n_bytes) {  // the text's last, partial window: bytes past the end are spaces
-      uint32_t q[4] = {0x20202020u, 0x20202020u, 0x20202020u, 0x20202020u};
-      for (int j = 0; w + j < a.n_bytes; ++j)
-        q[j >> 2] = (q[j >> 2] & ~(0xffu << (8 * (j & 3)))) | ((uint32_t)a.text[w + j] << (8 * (j & 3)));
-      v[k] = make_uint4(q[0], q[1], q[2], q[3]);
+    for (int k = 0; k < KW; ++k) {
+      v[k] = ld_nc16_hint(tx + 512 * k, pol);  // streamed: evict_first
+      mw[k] = __ldg(mb + 16 * k);
     }
-#if SFKV_TOK_SPBITS
-    // the window's compact 16-bit space mask is stored for the emit pass (which then builds its
-    // boundary bitmap and start masks from it instead of re-testing every staged byte)
-    const uint32_t sp = space_bits16(v[k]);
-    a.spbits[w >> 4] = (uint16_t)sp;  // every window of the chunk (past the text: all spaces)
-    uint32_t prev = __shfl_up_sync(0xffffffffu, sp >> 15, 1);
-    if (lane == 0) prev = prev_last;
-    prev_last = __shfl_sync(0xffffffffu, sp >> 15, 31);
-    if (w < a.n_bytes) c += __popc(~sp & (((sp << 1) | prev) | ((mw[k] >> (w & 31)) & 0xffffu)) & 0xffffu);
-#else
-    // starts counted in the uncompacted domain (bit 7 of each byte; the previous byte's space bit
-    // moves in by a byte shift): no multiply, the count pass was issue-bound on the IMAD pipe
-    const uint32_t s0 = space_hi4(v[k].x), s1 = space_hi4(v[k].y), s2 = space_hi4(v[k].z), s3 = space_hi4(v[k].w);
-    const uint32_t last = s3 >> 31;
-    uint32_t prev = __shfl_up_sync(0xffffffffu, last, 1);
-    if (lane == 0) prev = prev_last;
-    prev_last = __shfl_sync(0xffffffffu, last, 31);
-    const uint32_t ms = (mw[k] >> (w & 31)) & 0xffffu;
-    if (w < a.n_bytes) {
-      if (!ms) {
-        constexpr uint32_t H = 0x80808080u;
-        c += __popc(~s0 & ((s0 << 8) | (prev << 7)) & H) + __popc(~s1 & ((s1 << 8) | (s0 >> 24)) & H) +
-             __popc(~s2 & ((s2 << 8) | (s1 >> 24)) & H) + __popc(~s3 & ((s3 << 8) | (s2 >> 24)) & H);
-      } else {  // a message starts in this window (rare): the compact 16-bit form
-        const uint32_t sp = space_mask4(v[k].x) | (space_mask4(v[k].y) << 4) | (space_mask4(v[k].z) << 8) |
-                            (space_mask4(v[k].w) << 12);
-        c += __popc(~sp & (((sp << 1) | prev) | ms) & 0xffffu);
+#pragma unroll
+    for (int k = 0; k < KW; ++k) mw[k] = (mw[k] >> sh) & 0xffffu;
+    c = count_windows(v, mw, lane, prev0, spo);
+  } else {
+#pragma unroll
+    for (int k = 0; k < KW; ++k) {
+      const int64_t w = c0 + 512 * k + 16 * lane;
+      v[k] = make_uint4(0x20202020u, 0x20202020u, 0x20202020u, 0x20202020u);
+      if (w + 16 <= a.n_bytes) {
+        v[k] = ld_nc16_hint(a.text + w, pol);
+      } else if (w < a.n_bytes) {  // the text's last, partial window: bytes past the end are spaces
+        uint32_t q[4] = {0x20202020u, 0x20202020u, 0x20202020u, 0x20202020u};
+        for (int j = 0; w + j < a.n_bytes; ++j)
+          q[j >> 2] = (q[j >> 2] & ~(0xffu << (8 * (j & 3)))) | ((uint32_t)a.text[w + j] << (8 * (j & 3)));
+        v[k] = make_uint4(q[0], q[1], q[2], q[3]);
       }
+      // past the text: no starts (all spaces, no message bits)
+      mw[k] = w < a.n_bytes ? (__ldg(a.mbits + (w >> 5)) >> (w & 31)) & 0xffffu : 0u;
     }
-#endif
+    c = count_windows(v, mw, lane, prev0, spo);
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
   if (lane == 0) counts[chunk] = c;
-  }
 }
 
 struct ChunkCount {
@@ -954,16 +930,9 @@ static int tokenize_dev(sfkv_interner* it, int64_t n_req, const int64_t* req_msg
   const int sms = sm_count_k();
   // (the bitmap and the batch counters ctr[3..5] were left zero by the previous batch's last kernels)
   if (n_msg > 0) SFKV_CUDA(launch_pdl(msg_mark_kernel, dim3(grid_for(n_msg, 256, sms * 4)), dim3(256), st, a));
-  if (nchunks > 0) {
-    int64_t cg = (nchunks + COUNT_WARPS - 1) / COUNT_WARPS;
-    if (SFKV_COUNT_PERSIST) {
-      static int count_per_sm = 0;
-      if (!count_per_sm)
-        SFKV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&count_per_sm, chunk_count_kernel, COUNT_WARPS * 32, 0));
-      cg = std::min<int64_t>(cg, (int64_t)std::max(1, count_per_sm) * sms);
-    }
-    SFKV_CUDA(launch_pdl(chunk_count_kernel, dim3((unsigned)cg), dim3(COUNT_WARPS * 32), st, a, counts, nchunks));
-  }
+  if (nchunks > 0)
+    SFKV_CUDA(launch_pdl(chunk_count_kernel, dim3((unsigned)((nchunks + COUNT_WARPS - 1) / COUNT_WARPS)),
+                         dim3(COUNT_WARPS * 32), st, a, counts, nchunks));
   SFKV_LAUNCH_CHECK("msg_mark/chunk_count");
   if (int rc = exclusive_scan(ChunkCount{counts}, nchunks, a.chunk_off, tmp, st)) return rc;
   // request offsets need only the chunk offsets: forked onto the (high-priority) aux stream, they
