@@ -223,9 +223,6 @@ __device__ __forceinline__ uint32_t start_mask16(const TokArgs& a, int64_t base)
 // loads, no branch between them), the previous byte of a window comes from the neighbouring lane
 // (or the previous round's last lane) instead of another load, then a warp reduction.
 constexpr int COUNT_WARPS = 8;
-#ifndef SFKV_TOK_SPBITS
-#define SFKV_TOK_SPBITS 1
-#endif
 #ifndef SFKV_TOKOFF_FORK
 #define SFKV_TOKOFF_FORK 1
 #endif
@@ -333,80 +330,73 @@ __global__ void __launch_bounds__(CHUNK_THREADS, SFKV_EMIT_MINB) chunk_emit_kern
   __shared__ __align__(16) uint8_t sb[CHUNK + OVER + 16];  // + 16: word reads past a token's end
   __shared__ uint32_t sbits[(CHUNK + OVER) / 32];
   const int64_t c0 = (int64_t)blockIdx.x * CHUNK;
-  const int64_t base = c0 + (int64_t)threadIdx.x * 16;
   const int64_t lim = a.n_bytes - c0;  // valid staged bytes: [0, min(lim, CHUNK + OVER))
-  // stage bytes (16 B per thread, OVER / 16 threads take the overflow) and bits
-  if (base + 16 <= a.n_bytes) {
-    *reinterpret_cast<uint4*>(sb + threadIdx.x * 16) = ld_nc16_hint(a.text + base, l2_policy_first());
-  } else {
-    for (int j = 0; j < 16; ++j) sb[threadIdx.x * 16 + j] = base + j < a.n_bytes ? a.text[base + j] : ' ';
-  }
-  if (threadIdx.x < OVER / 16) {
-    const int64_t ob = c0 + CHUNK + threadIdx.x * 16;
-    if (ob + 16 <= a.n_bytes) {
-      *reinterpret_cast<uint4*>(sb + CHUNK + threadIdx.x * 16) = ld_nc16_hint(a.text + ob, l2_policy_first());
-    } else {
-      for (int j = 0; j < 16; ++j) sb[CHUNK + threadIdx.x * 16 + j] = ob + j < a.n_bytes ? a.text[ob + j] : ' ';
-    }
-  }
   __shared__ uint16_t slist[CHUNK];
   __shared__ uint32_t sbnd[(CHUNK + OVER) / 32 + 1];
-#if SFKV_TOK_SPBITS
-  // boundary bitmap = the count pass's space masks | message starts (words past the text: all set)
   __shared__ uint32_t s_sp[CHUNK / 32 + 1];  // [0]: the word before the chunk
-  {
-    const uint32_t* sp32 = reinterpret_cast<const uint32_t*>(a.spbits);
-    if (threadIdx.x < (CHUNK + OVER) / 32) {
-      const int64_t w = (c0 >> 5) + threadIdx.x;
-      const bool in = c0 + threadIdx.x * 32 < a.n_bytes;
-      const uint32_t ms = in ? a.mbits[w] : 0xffffffffu, sp = in ? sp32[w] : 0xffffffffu;
-      sbits[threadIdx.x] = ms;
-      sbnd[threadIdx.x] = sp | ms;
-      if (threadIdx.x < CHUNK / 32) s_sp[threadIdx.x + 1] = sp;
-    } else if (threadIdx.x == (CHUNK + OVER) / 32) {
-      s_sp[0] = c0 == 0 ? 0x80000000u : sp32[(c0 >> 5) - 1];
+  constexpr int WORDS = (CHUNK + OVER) / 32;
+  const int tid = threadIdx.x;
+  const uint64_t pol = l2_policy_first();
+  // stage the chunk (16 B per thread) and OVER bytes of the next one (OVER / 16 threads), the
+  // count pass's space words and the message-start words; boundary bitmap = space | message start
+  const uint32_t* sp32 = reinterpret_cast<const uint32_t*>(a.spbits) + (c0 >> 5);
+  const uint32_t* mb32 = a.mbits + (c0 >> 5);
+  if (lim >= CHUNK + OVER) {  // every staged byte inside the text (all chunks but the last one or two)
+    const uint8_t* tx = a.text + c0;
+    *reinterpret_cast<uint4*>(sb + tid * 16) = ld_nc16_hint(tx + tid * 16, pol);
+    if (tid < OVER / 16) *reinterpret_cast<uint4*>(sb + CHUNK + tid * 16) = ld_nc16_hint(tx + CHUNK + tid * 16, pol);
+    if (tid < WORDS) {
+      const uint32_t ms = mb32[tid], sp = sp32[tid];
+      sbits[tid] = ms;
+      sbnd[tid] = sp | ms;
+      if (tid < CHUNK / 32) s_sp[tid + 1] = sp;
+    } else if (tid == WORDS) {
+      s_sp[0] = c0 == 0 ? 0x80000000u : sp32[-1];
+    }
+  } else {  // bytes past the text are staged as spaces, words past it as all boundaries
+    const int64_t base = c0 + (int64_t)tid * 16;
+    if (base + 16 <= a.n_bytes) {
+      *reinterpret_cast<uint4*>(sb + tid * 16) = ld_nc16_hint(a.text + base, pol);
+    } else {
+      for (int j = 0; j < 16; ++j) sb[tid * 16 + j] = base + j < a.n_bytes ? a.text[base + j] : ' ';
+    }
+    if (tid < OVER / 16) {
+      const int64_t ob = c0 + CHUNK + tid * 16;
+      if (ob + 16 <= a.n_bytes) {
+        *reinterpret_cast<uint4*>(sb + CHUNK + tid * 16) = ld_nc16_hint(a.text + ob, pol);
+      } else {
+        for (int j = 0; j < 16; ++j) sb[CHUNK + tid * 16 + j] = ob + j < a.n_bytes ? a.text[ob + j] : ' ';
+      }
+    }
+    if (tid < WORDS) {
+      const bool in = c0 + tid * 32 < a.n_bytes;
+      const uint32_t ms = in ? mb32[tid] : 0xffffffffu, sp = in ? sp32[tid] : 0xffffffffu;
+      sbits[tid] = ms;
+      sbnd[tid] = sp | ms;
+      if (tid < CHUNK / 32) s_sp[tid + 1] = sp;
+    } else if (tid == WORDS) {
+      s_sp[0] = c0 == 0 ? 0x80000000u : sp32[-1];
     }
   }
-#else
-  if (threadIdx.x < (CHUNK + OVER) / 32) {
-    const int64_t w = (c0 >> 5) + threadIdx.x;
-    sbits[threadIdx.x] = (c0 + threadIdx.x * 32 < a.n_bytes) ? a.mbits[w] : 0xffffffffu;
-  }
-#endif
   constexpr int PW = CHUNK / 32;  // pending bitmap words (<= CHUNK tokens: every byte may start a message)
   __shared__ uint32_t s_pend[PW];
   __shared__ int s_any_pend;
   __shared__ unsigned long long s_pbase;
-  if (threadIdx.x < PW) s_pend[threadIdx.x] = 0u;
-  if (threadIdx.x == 0) {
+  if (tid < PW) s_pend[tid] = 0u;
+  if (tid == 0) {
     s_any_pend = 0;
-    sbnd[(CHUNK + OVER) / 32] = 0xffffffffu;  // past the staged bytes: all boundaries (end windows)
+    sbnd[WORDS] = 0xffffffffu;  // past the staged bytes: all boundaries (end windows)
   }
   __syncthreads();
-  // from the staged bytes: 16 boundary bits (space | message start) per thread into the bitmap, and
-  // the thread's token starts (non-space after a space or at a message start)
+  // the thread's token starts (non-space after a space or at a message start) from the staged words
   uint32_t m = 0;
-#if SFKV_TOK_SPBITS
-  if (base < a.n_bytes) {  // the thread's 16 bytes: starts from the staged space / message words
-    const int t = threadIdx.x, sh = (t & 1) * 16;
-    const uint32_t spw = s_sp[(t >> 1) + 1];
-    const uint32_t sp = (spw >> sh) & 0xffffu, ms = (sbits[t >> 1] >> sh) & 0xffffu;
-    const uint32_t prev = (t & 1) ? (spw >> 15) & 1u : s_sp[t >> 1] >> 31;
+  if (tid * 16 < lim) {
+    const int sh = (tid & 1) * 16;
+    const uint32_t spw = s_sp[(tid >> 1) + 1];
+    const uint32_t sp = (spw >> sh) & 0xffffu, ms = (sbits[tid >> 1] >> sh) & 0xffffu;
+    const uint32_t prev = (tid & 1) ? (spw >> 15) & 1u : s_sp[tid >> 1] >> 31;
     m = ~sp & ((sp << 1) | prev | ms) & 0xffffu;
   }
-#else
-  for (int o = threadIdx.x * 16; o < CHUNK + OVER; o += CHUNK_THREADS * 16) {
-    const uint4 v = *reinterpret_cast<const uint4*>(sb + o);
-    const uint32_t sp = space_mask4(v.x) | (space_mask4(v.y) << 4) | (space_mask4(v.z) << 8) | (space_mask4(v.w) << 12);
-    const uint32_t ms = (sbits[o >> 5] >> (o & 31)) & 0xffffu;
-    reinterpret_cast<uint16_t*>(sbnd)[o >> 4] = (uint16_t)(sp | ms);
-    if (o < CHUNK && base < a.n_bytes) {
-      const uint32_t prev_sp = o > 0 ? (uint32_t)is_space(sb[o - 1])
-                                     : (c0 == 0 ? 1u : (uint32_t)is_space(a.text[c0 - 1]));
-      m = ~sp & (((sp << 1) | prev_sp) | ms) & 0xffffu;
-    }
-  }
-#endif
   int excl, total;
   BS(tmp).ExclusiveSum(__popc(m), excl, total);
   {
