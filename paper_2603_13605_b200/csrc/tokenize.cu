@@ -12,17 +12,20 @@
 //   msg_mark_kernel     message-start bitmap (a message start is a forced token boundary)
 //   chunk_count_kernel  token starts per 2 KiB chunk (a warp each): 16-B loads, C-locale space
 //                       test on 4 bytes at a time (per-byte SWAR), start = non-space &
-//                       (prev space | message start)
+//                       (prev space | message start); each 16-byte window's compact space mask
+//                       is stored for the emit pass
 //   exclusive scan      over chunks
 //   chunk_emit_kernel   CTA scan inside each chunk: token start positions, in order, in a shared
-//                       list; the chunk (+256 B) and a boundary bitmap are staged in shared memory
-//                       and the list is probed one token per thread: length, key, probe. Tokens
+//                       list; the chunk (+256 B) is staged in shared memory with a boundary bitmap
+//                       built from the count pass's space masks and the message-start words, and
+//                       the list is probed one token per thread: length, key, probe. Tokens
 //                       of <= 7 bytes key on their own bytes (exact); longer ones on a 63-bit
 //                       hash verified against the arena. A string
 //                       published by an earlier batch resolves here; claims (CAS into an empty
 //                       slot + atomicMin(position): the lowest position owns the new string) and
 //                       duplicates of this batch's new strings go to a pending list
-//   req_tokoff_kernel   per-request token offsets (chunk offset + starts before the request)
+//   req_tokoff_kernel   per-request token offsets (chunk offset + starts before the request), on
+//                       an aux stream beside the emit pass
 //   tok_pending_kernel  one cooperative launch with grid barriers between its steps: owners
 //                       flagged and long duplicates compared with their owner (a 64-bit hash
 //                       collision fails the batch loudly), capacity check, owners ranked by
