@@ -1700,7 +1700,68 @@ def cpu_baseline(args):
     return {"value": v, "unit": "blocks/s", "cores": 1, "kind": "reference",
             "sample": f"{n_sample} workflows of the same C2 distribution ({blocks} blocks), "
                       f"SimulatedBackend::prefix_match on pre-tokenized strings, 1 thread pinned to core {aff[0]}",
-            **info}
+            **info, "restatement": restatement_baselines(args, info, aff)}
+
+
+def restatement_baselines(args, info, aff):
+    """the reference holds no KV bytes and has no cross-workflow lookup, so those two
+    legs get CPU restatement baselines, labelled as such (never the reference baseline):
+      kv_gather — an N-thread memcpy of the same per-block row lists over a host-memory pool
+                  (slab-major like the GPU pool: 64 slabs x 2 KiB rows per 2 MiB block);
+      c5_lookup — the CPU restatement's hash-table lookup (oracle sfo_lookup_batch, test
+                  infrastructure: only this leg of bench.py runs it) on a sample of the C5 batch
+                  against the full 1,048,576-block resident set."""
+    from concurrent.futures import ThreadPoolExecutor
+    out = {}
+    label = "CPU restatement, not reference"
+    # ---- KV gather: N-thread memcpy over a host pool -------------------------------------
+    nthr = max(1, len(aff))
+    n_pool, n_get = 1024, 256
+    pool = np.empty((KV_SLABS, n_pool, KV_ROW), np.uint8)
+    pool[...] = 7  # touch every page before timing
+    dst = np.empty((KV_SLABS, n_get, KV_ROW), np.uint8)
+    dst[...] = 0
+    blocks = np.random.default_rng(args.seed + 77).permutation(n_pool)[:n_get]
+    parts = np.array_split(np.arange(n_get), nthr)
+
+    def work(js):
+        for j in js:
+            np.copyto(dst[:, j, :], pool[:, blocks[j], :])
+    with ThreadPoolExecutor(nthr) as ex:
+        ts = []
+        for _ in range(4):
+            t0 = time.perf_counter()
+            list(ex.map(work, parts))
+            ts.append(time.perf_counter() - t0)
+    assert (dst[:, 0, :] == 7).all()
+    moved = 2 * n_get * KV_SLABS * KV_ROW  # read + write, as the GPU gather counts
+    out["kv_gather"] = {"value": moved / float(np.mean(ts[1:])) / 1e9, "unit": "GB/s", "cores": nthr,
+                        "kind": "port", "label": label,
+                        "sample": f"{n_get} of {n_pool} 2 MiB blocks (64 x 2 KiB rows each) gathered from a "
+                                  f"host pool by {nthr} threads (numpy copyto per block)", **info}
+    del pool, dst
+    # ---- C5: the restatement's hash table ---------------------------------------------------
+    sys.path.insert(0, os.path.join(REPO, "tests"))
+    import oracle_lib  # test infrastructure: the CPU restatement
+    from paper_2603_13605_b200.abi import Pool
+    n_pref = 20_000
+    cfg, resident, (off, tok, expect_hit) = c5_workload(args.seed + 7, n_pref)
+    o = Pool(oracle_lib.load(), cfg)
+    for wf, woff, wtok in resident:
+        o.commit(wf, woff, wtok)
+    nblk = int((np.diff(off) // BT).sum())
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        _, hit = o.lookup(off, tok)
+        ts.append(time.perf_counter() - t0)
+    assert (hit == expect_hit).all()
+    out["c5_lookup"] = {"value": nblk / float(np.mean(ts)), "unit": "blocks/s", "cores": 1, "kind": "port",
+                        "label": label,
+                        "sample": f"{n_pref} C5 stage prefixes ({nblk} blocks) against the full 1,048,576-block "
+                                  f"resident set, sfo_lookup_batch, 1 thread", **info}
+    o.close()
+    return out
 
 
 def main():
