@@ -188,3 +188,39 @@ def test_gpu_cold_batch_and_reset(gpu_api, oracle_api):
             assert g.token(i) == o.token(i)
         g.reset()
         assert g.size() == 0
+
+
+def _boundary_batch(total, seed):
+    """Two requests whose text is exactly `total` bytes in all (one message per piece): random
+    words over all six C-locale spaces, message starts in the middle of words."""
+    rng = np.random.default_rng(seed)
+    spaces = b" \t\n\v\f\r"
+    raw = bytearray(rng.integers(33, 127, size=total).astype(np.uint8).tobytes())
+    for i in rng.choice(total, size=total // 5, replace=False):
+        raw[i] = spaces[int(rng.integers(0, 6))]
+    cuts = sorted(set(int(c) for c in rng.integers(1, max(2, total), size=6)))
+    pieces, prev = [], 0
+    for c in cuts + [total]:
+        if c > prev:
+            pieces.append(bytes(raw[prev:c]))
+            prev = c
+    h = max(1, len(pieces) // 2)  # two requests; the batch's text is exactly `total` bytes
+    return [pieces[:h], pieces[h:]]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("total", [2047, 2048, 2049, 2048 + 255, 2048 + 256, 2048 + 257, 4095, 4096, 4097,
+                                   4096 + 256, 6144 + 1])
+def test_gpu_tokenizer_chunk_boundaries_match_oracle(gpu_api, oracle_api, total):
+    """Texts ending at and around the 2 KiB chunk and the chunk + 256-byte staged window: the count
+    pass's full-chunk fast path and the emit pass's full-window fast path against their generic
+    paths (the text's last chunks), message starts inside words, every C-locale space."""
+    g = Interner(gpu_api, table_log2=16, arena_bytes=1 << 20)
+    o = Interner(oracle_api, table_log2=16, arena_bytes=1 << 20)
+    for seed in range(3):
+        reqs = _boundary_batch(total, seed)
+        go, gt = g.tokenize(reqs)
+        oo, ot = o.tokenize(reqs)
+        np.testing.assert_array_equal(go, oo)
+        np.testing.assert_array_equal(gt, ot)
+    assert g.size() == o.size()
